@@ -1,0 +1,231 @@
+/*
+ * respec_b200.h -- C-ABI of the B200-native ReSpec rollout hot path.
+ *
+ * The reference (/root/reference/proj/core) exposes this path as C++ value-type functions
+ * in the static library respec_core; it has no FFI. These entry points
+ * are what a reference-side binding would call instead; each one names the reference
+ * interface it replaces. Conventions:
+ *   - every function returns RS_OK (0) or an error code; rs_last_error() returns the
+ *     thread-local message, verbatim from the reference where the reference throws
+ *     (e.g. "BatchEngine: empty batch", server.cpp:274).
+ *   - plain pointers + sizes only; all buffers passed in are HOST memory unless the
+ *     parameter name ends in _dev.
+ *   - handles are not thread-safe; use one rs_ctx per host thread / GPU.
+ */
+#ifndef RESPEC_B200_H
+#define RESPEC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_OK 0
+#define RS_EINVAL 1 /* std::invalid_argument in the reference */
+#define RS_ESTATE 2 /* std::runtime_error */
+#define RS_ELOGIC 3 /* std::logic_error */
+#define RS_ECUDA 4  /* CUDA launch / runtime failure */
+#define RS_ENOMEM 5
+
+#define RS_VERIFY_SAMPLE 0 /* lossless rejection sampling, specdec.cpp:197-267 */
+#define RS_VERIFY_GREEDY 1 /* greedy verification (not in the reference) */
+
+typedef struct rs_ctx rs_ctx;       /* one GPU + stream + scratch */
+typedef struct rs_model rs_model;   /* immutable device-resident model (tabular or transformer) */
+typedef struct rs_table rs_table;   /* ProfileTable, server.hpp:21-49 */
+typedef struct rs_engine rs_engine; /* BatchEngine, server.hpp:98-132 */
+
+/* SDConfig (specdec.hpp:17-37). enabled=0 is the non-spec configuration. */
+typedef struct {
+    int32_t rounds;    /* s */
+    int32_t branching; /* t */
+    int32_t draft_len; /* n */
+    int32_t enabled;
+} rs_sdconfig;
+
+/* RoleTiming / TimingModel (costsim.hpp:34-53): the simulated ledger is kept for parity. */
+typedef struct {
+    double unit_cost;
+    int32_t saturation_tokens;
+    double latency_floor;
+} rs_role_timing;
+typedef struct {
+    rs_role_timing target;
+    rs_role_timing drafter;
+} rs_timing_model;
+
+/* RequestState (server.hpp:69-83); rng = DecodeRng::from_seed(seed, stream_id) (rng.hpp:37-43). */
+typedef struct {
+    int32_t id;
+    const int32_t *prompt;
+    int32_t prompt_len;
+    double eos_bias;
+    int32_t max_len;
+    uint64_t seed;
+    uint64_t stream_id;
+} rs_request;
+
+/* SwitchEvent (server.hpp:85-90). */
+typedef struct {
+    int32_t cycle;
+    int32_t active_batch;
+    rs_sdconfig from;
+    rs_sdconfig to;
+} rs_switch_event;
+
+/* ForwardEvent (costsim.hpp:14-20); role 1 = target, 0 = drafter. */
+typedef struct {
+    int32_t role;
+    int32_t positions;
+    int32_t batch_tokens;
+} rs_forward_event;
+
+/* Per-step summary returned by rs_engine_step (not in the reference: measured, not simulated). */
+typedef struct {
+    int32_t active_batch;
+    rs_sdconfig mode;
+    int32_t drafter_version;
+    int32_t emitted_tokens;   /* tokens appended across the batch this step */
+    int32_t drafted_cycles;   /* sequences whose cycle drafted (accept_len recorded) */
+    int32_t accepted_drafted; /* sum of accept_len over those sequences */
+    int32_t redraft_passes;   /* extra drafting passes for EOS-truncated chains (sampling) */
+    float step_ms;            /* device time of the step, CUDA events on the engine stream */
+} rs_step_info;
+
+/* Transformer shape (Qwen2-style target; EAGLE-3-style drafter uses the same d/heads). */
+typedef struct {
+    int32_t vocab;
+    int32_t d_model;
+    int32_t n_layers;
+    int32_t n_heads;
+    int32_t n_kv_heads;
+    int32_t head_dim;
+    int32_t d_ff;
+    int32_t max_ctx;   /* KV capacity per sequence (prompt + max_len + tree slots) */
+    float rope_theta;
+    float rms_eps;
+    float init_std;    /* synthetic weights ~ N(0, init_std) */
+    float logit_scale; /* LM-head output scale (synthetic weights) */
+    double temperature;
+} rs_transformer_shape;
+
+/* KDPolicy (learner.hpp:17-23); mode 0 = Reward, 1 = Uniform, 2 = Frozen. */
+typedef struct {
+    int32_t interval;
+    int32_t mode;
+    double clip_lo;
+    double clip_hi;
+    double lr;
+} rs_kd_policy;
+
+/* One RolloutSample (rollout.hpp:12-20) for the KD learner; target_logprobs is
+   response_len x vocab (the StepRecord::target_logprobs rows, specdec.hpp:42). */
+typedef struct {
+    const int32_t *prompt;
+    int32_t prompt_len;
+    const int32_t *response;
+    int32_t response_len;
+    const double *target_logprobs;
+    double eos_bias;
+    double reward;
+} rs_kd_sample;
+
+/* KDUpdateResult (learner.hpp:53-62). */
+typedef struct {
+    int32_t updated;
+    int32_t samples_used;
+    double loss;
+    double weight_mean;
+    double weight_min;
+    double weight_max;
+    double sim_time;
+} rs_kd_result;
+
+/* ---- errors / version ---------------------------------------------------------------- */
+const char *rs_last_error(void);
+int rs_version(void);
+/* Number of CUDA kernel launches issued by this thread since the last reset. */
+int64_t rs_launch_count(void);
+void rs_launch_count_reset(void);
+
+/* ---- context ------------------------------------------------------------------------- */
+int rs_ctx_create(int device, rs_ctx **out);
+int rs_ctx_destroy(rs_ctx *ctx);
+int rs_ctx_sync(rs_ctx *ctx);
+/* Run subsequent work on an externally owned cudaStream_t (e.g. torch's current stream). */
+int rs_ctx_set_stream(rs_ctx *ctx, void *cuda_stream);
+
+/* ---- models -------------------------------------------------------------------------- */
+/* TabularARModel(vocab, order, logits, temperature, version) -- model.hpp:105-108. The
+   rows x vocab table is copied to HBM in fp64 ("parity mode"). */
+int rs_tabular_create(rs_ctx *ctx, int32_t vocab, int32_t order, double temperature, const double *logits,
+                      int32_t version, rs_model **out);
+/* TabularARModel::logits() -- model.hpp:118 */
+int rs_tabular_logits(const rs_model *m, double *out, int64_t n);
+/* Qwen2-shaped target with synthetic N(0, init_std) weights generated on device from seed. */
+int rs_transformer_create(rs_ctx *ctx, const rs_transformer_shape *shape, uint64_t seed, rs_model **out);
+/* EAGLE-3-style drafter bound to a target (consumes the target's low/mid/high hidden states). */
+int rs_drafter_create(rs_ctx *ctx, const rs_model *target, uint64_t seed, int32_t version, rs_model **out);
+int rs_model_version(const rs_model *m, int32_t *out);
+int rs_model_vocab(const rs_model *m, int32_t *out);
+int rs_model_destroy(rs_model *m);
+
+/* ---- ProfileTable (server.hpp:21-49, server.cpp:21-145) -------------------------------- */
+int rs_table_create(const int32_t *buckets, int32_t n, rs_table **out);
+int rs_table_set_entry(rs_table *t, int32_t bucket, rs_sdconfig cfg, double time_per_token);
+int rs_table_finalize(rs_table *t);
+int rs_table_bucket_for(const rs_table *t, int32_t active_batch, int32_t *out);
+int rs_table_solve(const rs_table *t, int32_t active_batch, rs_sdconfig *out);
+int rs_table_best_for_bucket(const rs_table *t, int32_t bucket, rs_sdconfig *out);
+int rs_table_entry(const rs_table *t, int32_t bucket, rs_sdconfig cfg, double *out);
+/* ProfileTable::to_csv (server.cpp:136-145); writes at most cap bytes incl. NUL, *len = full length. */
+int rs_table_to_csv(const rs_table *t, char *buf, int64_t cap, int64_t *len);
+int rs_table_destroy(rs_table *t);
+
+/* ---- BatchEngine / run_generation (server.hpp:98-148, server.cpp:266-376) ------------- */
+/* table == NULL selects fixed mode with `forced`; drafter may be NULL when forced is off.
+   The target is borrowed and must outlive the engine (server.hpp:119). */
+int rs_engine_create(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const rs_table *table,
+                     const rs_timing_model *tm, const rs_request *reqs, int32_t n, rs_sdconfig forced,
+                     int32_t verify_mode, int32_t record_full_logprobs, rs_engine **out);
+/* DrafterSnapshotFn (server.hpp:92): the snapshot is read once, at the next step boundary. */
+int rs_engine_set_drafter(rs_engine *e, const rs_model *drafter);
+/* BatchEngine::step (server.cpp:266-349); throws "BatchEngine: empty batch" when done. */
+int rs_engine_step(rs_engine *e, rs_step_info *info);
+int rs_engine_all_done(const rs_engine *e, int32_t *out);
+int rs_engine_active_batch(const rs_engine *e, int32_t *out);
+int rs_engine_cycles(const rs_engine *e, int32_t *out);
+int rs_engine_prefill_events(const rs_engine *e, int32_t *out);
+int rs_engine_ledger_time(const rs_engine *e, double *out);
+int rs_engine_ledger(const rs_engine *e, rs_forward_event *out, int32_t cap, int32_t *n);
+int rs_engine_switches(const rs_engine *e, rs_switch_event *out, int32_t cap, int32_t *n);
+int rs_engine_active_trace(const rs_engine *e, int32_t *out, int32_t cap, int32_t *n);
+int rs_engine_drafter_versions(const rs_engine *e, int32_t *out, int32_t cap, int32_t *n);
+/* RolloutSample fields of request `req` (request order, server.cpp:365-374). */
+int rs_engine_response(rs_engine *e, int32_t req, int32_t *tokens, int32_t cap, int32_t *len);
+int rs_engine_steps(rs_engine *e, int32_t req, double *logp, uint8_t *drafted, double *logq, int32_t cap, int32_t *n);
+int rs_engine_step_logprobs(rs_engine *e, int32_t req, double *out, int64_t cap, int32_t *rows);
+int rs_engine_accept_lens(rs_engine *e, int32_t req, int32_t *out, int32_t cap, int32_t *n);
+int rs_engine_destroy(rs_engine *e);
+/* Debug: capture the logit rows of the next steps (for replay against the CPU oracle). */
+int rs_engine_set_capture(rs_engine *e, int32_t enable);
+int rs_engine_capture_count(const rs_engine *e, int64_t *rows, int32_t *vocab);
+int rs_engine_capture_read(rs_engine *e, int64_t first, int64_t count, int32_t *role, int32_t *req,
+                           int32_t *ctx_len, int32_t *ext, double *logits);
+
+/* ---- KD learner (learner.hpp:27-69, learner.cpp:10-160) -------------------------------- */
+double rs_kd_weight(double r, const double *batch_rewards, int32_t n, rs_kd_policy policy, int *status);
+/* kd_update on a tabular drafter: host selects ceil(N/I) samples with `selection_rng`
+   (an mt19937_64 seeded state advanced in place, 312 words + index), device computes
+   loss + analytic gradient and applies one SGD step into a NEW model (version + 1). */
+int rs_kd_update_tabular(rs_ctx *ctx, const rs_model *drafter, const rs_kd_sample *buf, int32_t n,
+                         rs_kd_policy policy, uint64_t *selection_rng_state, double sim_cost_per_token,
+                         rs_model **new_drafter, rs_kd_result *out);
+/* mt19937_64 state helper for rs_kd_update_tabular: 313 uint64 (312 words + index). */
+int rs_mt19937_64_seed(uint64_t seed, uint64_t *state313);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RESPEC_B200_H */

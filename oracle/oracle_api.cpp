@@ -1,0 +1,224 @@
+// oracle/oracle_api.cpp -- TEST INFRASTRUCTURE ONLY.
+// JSON-in / JSON-out C entry point over the CPU restatement (restate.cpp), so the Python
+// tests can drive it with ctypes. oracle/ref_shim.cpp exposes the SAME schema over the
+// compiled reference, which is how the restatement is pinned (tests/test_oracle.py).
+#include <cstdlib>
+#include <cstring>
+#include <json.hpp>
+#include <memory>
+
+#include "restate.hpp"
+
+using nlohmann::json;
+using namespace orc;
+
+namespace {
+
+SDConfig cfg_of(const json & j) {
+    SDConfig c;
+    c.rounds = j.value("s", 1);
+    c.branching = j.value("t", 1);
+    c.draft_len = j.value("n", 1);
+    c.enabled = j.value("enabled", false);
+    return c;
+}
+json cfg_json(const SDConfig & c) { return {{"s", c.rounds}, {"t", c.branching}, {"n", c.draft_len}, {"enabled", c.enabled}}; }
+
+std::shared_ptr<Model> model_of(const json & j) {
+    const std::string kind = j.value("kind", "tabular");
+    if (kind == "tabular") {
+        auto m = std::make_shared<TabularModel>();
+        m->vocab = j.at("vocab");
+        m->order = j.at("order");
+        m->temperature = j.value("temperature", 1.0);
+        m->version = j.value("version", 0);
+        m->table = j.at("logits").get<std::vector<double>>();
+        size_t rows = 1;
+        for (int i = 0; i < m->order; ++i) rows *= static_cast<size_t>(m->vocab);
+        if (m->table.size() != rows * static_cast<size_t>(m->vocab)) throw std::invalid_argument("tabular: wrong table size");
+        return m;
+    }
+    if (kind == "lookup") {
+        auto m = std::make_shared<LookupModel>();
+        m->vocab = j.at("vocab");
+        m->temperature = j.value("temperature", 1.0);
+        m->version = j.value("version", 0);
+        for (const auto & r : j.at("rows")) m->rows.emplace(r.at("ctx").get<std::vector<int>>(), r.at("logits").get<std::vector<double>>());
+        return m;
+    }
+    throw std::invalid_argument("unknown model kind " + kind);
+}
+
+TimingModel timing_of(const json & j) {
+    TimingModel tm;
+    if (j.is_object()) {
+        auto rt = [](const json & a) { return RoleTiming{a.at(0).get<double>(), a.at(1).get<int>(), a.at(2).get<double>()}; };
+        if (j.contains("target")) tm.target = rt(j.at("target"));
+        if (j.contains("drafter")) tm.drafter = rt(j.at("drafter"));
+    }
+    return tm;
+}
+
+ProfileTable table_of(const json & j) {
+    ProfileTable t(j.at("buckets").get<std::vector<int>>());
+    for (const auto & e : j.at("entries")) t.set_entry(e.at("bucket"), cfg_of(e), e.at("time_per_token"));
+    t.finalize();
+    return t;
+}
+
+json step_json(const StepRecord & s) {
+    json j = {{"token", s.token}, {"logp", s.logp}, {"drafted", s.drafted}, {"logq", s.logq}};
+    if (!s.target_logprobs.empty()) j["target_logprobs"] = s.target_logprobs;
+    return j;
+}
+
+VerifyMode mode_of(const json & req) { return req.value("verify_mode", "sample") == "greedy" ? VerifyMode::Greedy : VerifyMode::Sample; }
+
+json op_run_generation(const json & req) {
+    auto target = model_of(req.at("target"));
+    std::shared_ptr<const Model> drafter;
+    if (req.contains("drafter") && !req.at("drafter").is_null()) drafter = model_of(req.at("drafter"));
+    std::unique_ptr<ProfileTable> table;
+    if (req.contains("table") && !req.at("table").is_null()) table = std::make_unique<ProfileTable>(table_of(req.at("table")));
+    const TimingModel tm = timing_of(req.value("timing", json()));
+    const bool full = req.value("record_logprobs", true);
+    std::vector<RequestState> reqs;
+    for (const auto & r : req.at("requests")) {
+        RequestState s;
+        s.id = r.value("id", 0);
+        s.prompt = r.at("prompt").get<std::vector<int>>();
+        s.eos_bias = r.value("eos_bias", 0.0);
+        s.max_len = r.at("max_len");
+        s.rng = DecodeRng::from_seed(r.at("seed").get<uint64_t>(), r.at("stream").get<uint64_t>());
+        reqs.push_back(std::move(s));
+    }
+    std::function<std::shared_ptr<const Model>()> snap;
+    if (drafter) snap = [drafter]() { return drafter; };
+    BatchEngine eng(*target, snap, table.get(), std::move(reqs), cfg_of(req.value("forced", json::object())),
+                    mode_of(req), full);
+    const int max_cycles = req.value("max_cycles", -1);
+    while (!eng.all_done() && (max_cycles < 0 || eng.cycles() < max_cycles)) eng.step();
+    json out;
+    out["cycles"] = eng.cycles();
+    out["total_time"] = ledger_time(tm, eng.ledger());
+    out["active_trace"] = eng.active_trace();
+    out["prefill_events"] = eng.prefill_events();
+    out["drafter_versions"] = eng.drafter_versions();
+    json sw = json::array();
+    for (const auto & s : eng.switches()) sw.push_back({{"cycle", s.cycle}, {"active_batch", s.active_batch}, {"from", cfg_json(s.from)}, {"to", cfg_json(s.to)}});
+    out["switches"] = sw;
+    json ledger = json::array();
+    for (const auto & e : eng.ledger()) ledger.push_back({e.target ? 1 : 0, e.positions, e.batch_tokens});
+    out["ledger"] = ledger;
+    json samples = json::array();
+    std::vector<int> all_al;
+    for (const auto & r : eng.requests()) {
+        json steps = json::array();
+        for (const auto & s : r.steps) steps.push_back(step_json(s));
+        samples.push_back({{"prompt", r.prompt}, {"response", r.generated}, {"steps", steps}, {"eos_bias", r.eos_bias},
+                           {"accept_lens", r.accept_lens}, {"done", r.done}, {"draws", {r.rng.n_draft, r.rng.n_accept}}});
+        all_al.insert(all_al.end(), r.accept_lens.begin(), r.accept_lens.end());
+    }
+    out["samples"] = samples;
+    out["accept_lens"] = all_al;
+    return out;
+}
+
+json op_spec_step_tree(const json & req) {
+    auto target = model_of(req.at("target"));
+    auto drafter = model_of(req.at("drafter"));
+    std::vector<int> ctx = req.at("ctx").get<std::vector<int>>();
+    DecodeRng rng = DecodeRng::from_seed(req.at("seed").get<uint64_t>(), req.value("stream", uint64_t{0}));
+    const int cycles = req.value("cycles", 1);
+    json outs = json::array();
+    for (int c = 0; c < cycles; ++c) {
+        VerifyOutcome o = spec_step_tree(*target, *drafter, ctx, cfg_of(req.at("cfg")), rng, req.value("eos_bias", 0.0),
+                                         req.value("stop_at_eos", true), req.value("max_emit", 1 << 30), mode_of(req),
+                                         req.value("record_logprobs", false));
+        json rounds = json::array();
+        for (const auto & r : o.rounds) rounds.push_back({r.drafter_forwards, r.drafter_tokens_each, r.target_tokens});
+        json steps = json::array();
+        for (const auto & s : o.steps) steps.push_back(step_json(s));
+        outs.push_back({{"accepted_tokens", o.accepted_tokens}, {"accept_len", o.accept_len}, {"bonus_token", o.bonus_token},
+                        {"ended", o.ended}, {"rounds", rounds}, {"steps", steps}, {"draft_records", o.draft_records}});
+        if (req.value("advance_ctx", false)) ctx.insert(ctx.end(), o.accepted_tokens.begin(), o.accepted_tokens.end());
+    }
+    return {{"outcomes", outs}, {"draws", {rng.n_draft, rng.n_accept}}};
+}
+
+json op_kd_update(const json & req) {
+    auto dm = model_of(req.at("drafter"));
+    auto * drafter = dynamic_cast<TabularModel *>(dm.get());
+    if (!drafter) throw std::invalid_argument("kd_update: tabular drafter required");
+    std::vector<Rollout> buf;
+    for (const auto & s : req.at("buffer")) {
+        Rollout r;
+        r.prompt = s.at("prompt").get<std::vector<int>>();
+        r.response = s.at("response").get<std::vector<int>>();
+        for (const auto & st : s.at("steps")) r.target_logprobs.push_back(st.at("target_logprobs").get<std::vector<double>>());
+        r.eos_bias = s.value("eos_bias", 0.0);
+        r.reward = s.value("reward", 0.0);
+        buf.push_back(std::move(r));
+    }
+    const json & pj = req.at("policy");
+    KDPolicy p;
+    p.interval = pj.value("interval", 1);
+    const std::string mode = pj.value("mode", "reward");
+    p.mode = mode == "uniform" ? WeightMode::Uniform : mode == "frozen" ? WeightMode::Frozen : WeightMode::Reward;
+    p.clip_lo = pj.value("clip_lo", 0.0);
+    p.clip_hi = pj.value("clip_hi", 4.0);
+    p.lr = pj.value("lr", 0.1);
+    std::mt19937_64 sel(req.at("selection_seed").get<uint64_t>());
+    KDUpdateResult r = kd_update(*drafter, buf, p, sel, req.value("cost_per_token", 0.0));
+    json losses = json::array();
+    for (size_t i = 0; i < buf.size(); ++i) losses.push_back(kd_loss(*drafter, buf[i], 1.0));
+    return {{"updated", r.updated}, {"loss", r.loss}, {"samples_used", r.samples_used}, {"weight_mean", r.weight_mean},
+            {"weight_min", r.weight_min}, {"weight_max", r.weight_max}, {"sim_time", r.sim_time}, {"logits", r.logits},
+            {"selected", r.selected}, {"per_sample_loss_w1", losses}};
+}
+
+json op_profile_table(const json & req) {
+    ProfileTable t(req.at("buckets").get<std::vector<int>>());
+    for (const auto & e : req.at("entries")) t.set_entry(e.at("bucket"), cfg_of(e), e.at("time_per_token"));
+    t.finalize();
+    json best = json::array();
+    for (int b : t.buckets()) best.push_back({{"bucket", b}, {"cfg", cfg_json(t.best_for_bucket(b))}});
+    json solved = json::array();
+    for (int b : req.value("solve", std::vector<int>{})) solved.push_back({{"batch", b}, {"bucket", t.bucket_for(b)}, {"cfg", cfg_json(t.solve(b))}});
+    return {{"best", best}, {"solve", solved}, {"csv", t.to_csv()}};
+}
+
+json dispatch(const json & req) {
+    const std::string op = req.at("op");
+    if (op == "run_generation") return op_run_generation(req);
+    if (op == "spec_step_tree") return op_spec_step_tree(req);
+    if (op == "kd_update") return op_kd_update(req);
+    if (op == "profile_table") return op_profile_table(req);
+    throw std::invalid_argument("oracle: unknown op " + op);
+}
+
+char * dup(const std::string & s) {
+    char * p = static_cast<char *>(std::malloc(s.size() + 1));
+    std::memcpy(p, s.c_str(), s.size() + 1);
+    return p;
+}
+
+}  // namespace
+
+extern "C" {
+// Returns a malloc'd JSON string; {"error": {"type": ..., "what": ...}} on exception.
+char * oracle_call(const char * req) {
+    try {
+        return dup(dispatch(json::parse(req)).dump());
+    } catch (const std::invalid_argument & e) {
+        return dup(json{{"error", {{"type", "invalid_argument"}, {"what", e.what()}}}}.dump());
+    } catch (const std::logic_error & e) {
+        return dup(json{{"error", {{"type", "logic_error"}, {"what", e.what()}}}}.dump());
+    } catch (const std::runtime_error & e) {
+        return dup(json{{"error", {{"type", "runtime_error"}, {"what", e.what()}}}}.dump());
+    } catch (const std::exception & e) {
+        return dup(json{{"error", {{"type", "exception"}, {"what", e.what()}}}}.dump());
+    }
+}
+void oracle_free(char * p) { std::free(p); }
+}

@@ -1,0 +1,775 @@
+"""paper_2510_26475_b200 -- B200-native ReSpec rollout hot path.
+
+Python mirror of the reference's C++ API for the batched speculative-decode step
+(/root/reference/proj/core: specdec.hpp, server.hpp, learner.hpp), bound with ctypes to
+the C-ABI library librespec_b200.so (include/respec_b200.h). Every compute call runs in
+the CUDA library; there is no CPU fallback -- if the library is missing the import of
+`lib()` raises.
+
+Names, argument meaning and error behaviour follow the reference:
+  SDConfig, TabularARModel, ProfileTable, RequestState, DecodeRng, BatchEngine,
+  run_generation, GenerationRun, RolloutSample, StepRecord, KDPolicy, WeightMode,
+  kd_weight, kd_update.
+Exceptions: std::invalid_argument -> InvalidArgument (ValueError), std::runtime_error ->
+EngineError (RuntimeError), std::logic_error -> LogicError.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librespec_b200.so")
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class EngineError(RuntimeError):
+    """std::runtime_error in the reference."""
+
+
+class LogicError(RuntimeError):
+    """std::logic_error in the reference."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+RS_OK, RS_EINVAL, RS_ESTATE, RS_ELOGIC, RS_ECUDA, RS_ENOMEM = range(6)
+RS_VERIFY_SAMPLE, RS_VERIFY_GREEDY = 0, 1
+
+
+# ---- C structs ------------------------------------------------------------------------------
+class _SDConfig(ctypes.Structure):
+    _fields_ = [("rounds", ctypes.c_int32), ("branching", ctypes.c_int32), ("draft_len", ctypes.c_int32),
+                ("enabled", ctypes.c_int32)]
+
+
+class _RoleTiming(ctypes.Structure):
+    _fields_ = [("unit_cost", ctypes.c_double), ("saturation_tokens", ctypes.c_int32),
+                ("latency_floor", ctypes.c_double)]
+
+
+class _TimingModel(ctypes.Structure):
+    _fields_ = [("target", _RoleTiming), ("drafter", _RoleTiming)]
+
+
+class _Request(ctypes.Structure):
+    _fields_ = [("id", ctypes.c_int32), ("prompt", ctypes.POINTER(ctypes.c_int32)), ("prompt_len", ctypes.c_int32),
+                ("eos_bias", ctypes.c_double), ("max_len", ctypes.c_int32), ("seed", ctypes.c_uint64),
+                ("stream_id", ctypes.c_uint64)]
+
+
+class _SwitchEvent(ctypes.Structure):
+    _fields_ = [("cycle", ctypes.c_int32), ("active_batch", ctypes.c_int32), ("from_", _SDConfig), ("to", _SDConfig)]
+
+
+class _ForwardEvent(ctypes.Structure):
+    _fields_ = [("role", ctypes.c_int32), ("positions", ctypes.c_int32), ("batch_tokens", ctypes.c_int32)]
+
+
+class _StepInfo(ctypes.Structure):
+    _fields_ = [("active_batch", ctypes.c_int32), ("mode", _SDConfig), ("drafter_version", ctypes.c_int32),
+                ("emitted_tokens", ctypes.c_int32), ("drafted_cycles", ctypes.c_int32),
+                ("accepted_drafted", ctypes.c_int32), ("redraft_passes", ctypes.c_int32), ("step_ms", ctypes.c_float)]
+
+
+class _TransformerShape(ctypes.Structure):
+    _fields_ = [("vocab", ctypes.c_int32), ("d_model", ctypes.c_int32), ("n_layers", ctypes.c_int32),
+                ("n_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("d_ff", ctypes.c_int32), ("max_ctx", ctypes.c_int32), ("rope_theta", ctypes.c_float),
+                ("rms_eps", ctypes.c_float), ("init_std", ctypes.c_float), ("logit_scale", ctypes.c_float),
+                ("temperature", ctypes.c_double)]
+
+
+class _KDPolicy(ctypes.Structure):
+    _fields_ = [("interval", ctypes.c_int32), ("mode", ctypes.c_int32), ("clip_lo", ctypes.c_double),
+                ("clip_hi", ctypes.c_double), ("lr", ctypes.c_double)]
+
+
+class _KDSample(ctypes.Structure):
+    _fields_ = [("prompt", ctypes.POINTER(ctypes.c_int32)), ("prompt_len", ctypes.c_int32),
+                ("response", ctypes.POINTER(ctypes.c_int32)), ("response_len", ctypes.c_int32),
+                ("target_logprobs", ctypes.POINTER(ctypes.c_double)), ("eos_bias", ctypes.c_double),
+                ("reward", ctypes.c_double)]
+
+
+class _KDResult(ctypes.Structure):
+    _fields_ = [("updated", ctypes.c_int32), ("samples_used", ctypes.c_int32), ("loss", ctypes.c_double),
+                ("weight_mean", ctypes.c_double), ("weight_min", ctypes.c_double), ("weight_max", ctypes.c_double),
+                ("sim_time", ctypes.c_double)]
+
+
+# Every symbol include/respec_b200.h declares (checked by tests/test_abi.py).
+EXPORTED_SYMBOLS = [
+    "rs_last_error", "rs_version", "rs_launch_count", "rs_launch_count_reset",
+    "rs_ctx_create", "rs_ctx_destroy", "rs_ctx_sync", "rs_ctx_set_stream",
+    "rs_tabular_create", "rs_tabular_logits", "rs_transformer_create", "rs_drafter_create",
+    "rs_model_version", "rs_model_vocab", "rs_model_destroy",
+    "rs_table_create", "rs_table_set_entry", "rs_table_finalize", "rs_table_bucket_for", "rs_table_solve",
+    "rs_table_best_for_bucket", "rs_table_entry", "rs_table_to_csv", "rs_table_destroy",
+    "rs_engine_create", "rs_engine_set_drafter", "rs_engine_step", "rs_engine_all_done", "rs_engine_active_batch",
+    "rs_engine_cycles", "rs_engine_prefill_events", "rs_engine_ledger_time", "rs_engine_ledger",
+    "rs_engine_switches", "rs_engine_active_trace", "rs_engine_drafter_versions", "rs_engine_response",
+    "rs_engine_steps", "rs_engine_step_logprobs", "rs_engine_accept_lens", "rs_engine_destroy",
+    "rs_engine_set_capture", "rs_engine_capture_count", "rs_engine_capture_read",
+    "rs_kd_weight", "rs_kd_update_tabular", "rs_mt19937_64_seed",
+]
+
+_lib = None
+
+
+def lib():
+    """Load librespec_b200.so (built in-tree by __graft_entry__.build()). Fails loudly."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.POINTER
+        i32, i64, u64, dbl, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
+        sig = {
+            "rs_last_error": ([], ctypes.c_char_p),
+            "rs_version": ([], ctypes.c_int),
+            "rs_launch_count": ([], i64),
+            "rs_launch_count_reset": ([], None),
+            "rs_ctx_create": ([ctypes.c_int, P(vp)], ctypes.c_int),
+            "rs_ctx_destroy": ([vp], ctypes.c_int),
+            "rs_ctx_sync": ([vp], ctypes.c_int),
+            "rs_ctx_set_stream": ([vp, vp], ctypes.c_int),
+            "rs_tabular_create": ([vp, i32, i32, dbl, P(dbl), i32, P(vp)], ctypes.c_int),
+            "rs_tabular_logits": ([vp, P(dbl), i64], ctypes.c_int),
+            "rs_transformer_create": ([vp, P(_TransformerShape), u64, P(vp)], ctypes.c_int),
+            "rs_drafter_create": ([vp, vp, u64, i32, P(vp)], ctypes.c_int),
+            "rs_model_version": ([vp, P(i32)], ctypes.c_int),
+            "rs_model_vocab": ([vp, P(i32)], ctypes.c_int),
+            "rs_model_destroy": ([vp], ctypes.c_int),
+            "rs_table_create": ([P(i32), i32, P(vp)], ctypes.c_int),
+            "rs_table_set_entry": ([vp, i32, _SDConfig, dbl], ctypes.c_int),
+            "rs_table_finalize": ([vp], ctypes.c_int),
+            "rs_table_bucket_for": ([vp, i32, P(i32)], ctypes.c_int),
+            "rs_table_solve": ([vp, i32, P(_SDConfig)], ctypes.c_int),
+            "rs_table_best_for_bucket": ([vp, i32, P(_SDConfig)], ctypes.c_int),
+            "rs_table_entry": ([vp, i32, _SDConfig, P(dbl)], ctypes.c_int),
+            "rs_table_to_csv": ([vp, ctypes.c_char_p, i64, P(i64)], ctypes.c_int),
+            "rs_table_destroy": ([vp], ctypes.c_int),
+            "rs_engine_create": ([vp, vp, vp, vp, P(_TimingModel), P(_Request), i32, _SDConfig, i32, i32, P(vp)],
+                                 ctypes.c_int),
+            "rs_engine_set_drafter": ([vp, vp], ctypes.c_int),
+            "rs_engine_step": ([vp, P(_StepInfo)], ctypes.c_int),
+            "rs_engine_all_done": ([vp, P(i32)], ctypes.c_int),
+            "rs_engine_active_batch": ([vp, P(i32)], ctypes.c_int),
+            "rs_engine_cycles": ([vp, P(i32)], ctypes.c_int),
+            "rs_engine_prefill_events": ([vp, P(i32)], ctypes.c_int),
+            "rs_engine_ledger_time": ([vp, P(dbl)], ctypes.c_int),
+            "rs_engine_ledger": ([vp, P(_ForwardEvent), i32, P(i32)], ctypes.c_int),
+            "rs_engine_switches": ([vp, P(_SwitchEvent), i32, P(i32)], ctypes.c_int),
+            "rs_engine_active_trace": ([vp, P(i32), i32, P(i32)], ctypes.c_int),
+            "rs_engine_drafter_versions": ([vp, P(i32), i32, P(i32)], ctypes.c_int),
+            "rs_engine_response": ([vp, i32, P(i32), i32, P(i32)], ctypes.c_int),
+            "rs_engine_steps": ([vp, i32, P(dbl), P(ctypes.c_uint8), P(dbl), i32, P(i32)], ctypes.c_int),
+            "rs_engine_step_logprobs": ([vp, i32, P(dbl), i64, P(i32)], ctypes.c_int),
+            "rs_engine_accept_lens": ([vp, i32, P(i32), i32, P(i32)], ctypes.c_int),
+            "rs_engine_destroy": ([vp], ctypes.c_int),
+            "rs_engine_set_capture": ([vp, i32], ctypes.c_int),
+            "rs_engine_capture_count": ([vp, P(i64), P(i32)], ctypes.c_int),
+            "rs_engine_capture_read": ([vp, i64, i64, P(i32), P(i32), P(i32), P(i32), P(dbl)], ctypes.c_int),
+            "rs_kd_weight": ([dbl, P(dbl), i32, _KDPolicy, P(ctypes.c_int)], dbl),
+            "rs_kd_update_tabular": ([vp, vp, P(_KDSample), i32, _KDPolicy, P(u64), dbl, P(vp), P(_KDResult)],
+                                     ctypes.c_int),
+            "rs_mt19937_64_seed": ([u64, P(u64)], ctypes.c_int),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(status):
+    if status == RS_OK:
+        return
+    msg = lib().rs_last_error().decode()
+    raise {RS_EINVAL: InvalidArgument, RS_ESTATE: EngineError, RS_ELOGIC: LogicError,
+           RS_ECUDA: CudaError, RS_ENOMEM: MemoryError}.get(status, RuntimeError)(msg)
+
+
+def _i32arr(xs):
+    xs = list(xs)
+    return (ctypes.c_int32 * max(1, len(xs)))(*xs)
+
+
+def _f64arr(xs):
+    xs = list(xs)
+    return (ctypes.c_double * max(1, len(xs)))(*xs)
+
+
+# ---- device context ---------------------------------------------------------------------------
+class Device:
+    """One GPU + stream (rs_ctx). One per host thread."""
+
+    def __init__(self, index: int = 0):
+        h = ctypes.c_void_p()
+        _check(lib().rs_ctx_create(index, ctypes.byref(h)))
+        self.handle = h
+        self.index = index
+
+    def sync(self):
+        _check(lib().rs_ctx_sync(self.handle))
+
+    def set_stream(self, cuda_stream_ptr: int):
+        _check(lib().rs_ctx_set_stream(self.handle, ctypes.c_void_p(cuda_stream_ptr)))
+
+    def close(self):
+        if self.handle:
+            lib().rs_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_device: Optional[Device] = None
+
+
+def default_device() -> Device:
+    global _default_device
+    if _default_device is None:
+        _default_device = Device(0)
+    return _default_device
+
+
+def launch_count() -> int:
+    return int(lib().rs_launch_count())
+
+
+def reset_launch_count():
+    lib().rs_launch_count_reset()
+
+
+# ---- SDConfig (specdec.hpp:17-37) ---------------------------------------------------------------
+@dataclass(frozen=True)
+class SDConfig:
+    rounds: int = 1
+    branching: int = 1
+    draft_len: int = 1
+    enabled: bool = False
+
+    @staticmethod
+    def off() -> "SDConfig":
+        return SDConfig()
+
+    @staticmethod
+    def chain(k: int) -> "SDConfig":
+        return SDConfig(1, 1, k, True)
+
+    @staticmethod
+    def tree(s: int, t: int, n: int) -> "SDConfig":
+        return SDConfig(s, t, n, True)
+
+    def drafted_per_cycle(self) -> int:
+        return self.rounds * self.branching * self.draft_len
+
+    def key(self) -> str:
+        return "off" if not self.enabled else f"s{self.rounds}_t{self.branching}_n{self.draft_len}"
+
+    def __eq__(self, o):
+        if not isinstance(o, SDConfig):
+            return NotImplemented
+        if not self.enabled and not o.enabled:
+            return True
+        return (self.enabled == o.enabled and self.rounds == o.rounds and self.branching == o.branching
+                and self.draft_len == o.draft_len)
+
+    def __hash__(self):
+        return hash(self.key())
+
+    def _c(self) -> _SDConfig:
+        return _SDConfig(self.rounds, self.branching, self.draft_len, 1 if self.enabled else 0)
+
+    @staticmethod
+    def _from_c(c: _SDConfig) -> "SDConfig":
+        return SDConfig(c.rounds, c.branching, c.draft_len, bool(c.enabled))
+
+
+# ---- TimingModel (costsim.hpp:34-53) ---------------------------------------------------------------
+@dataclass
+class RoleTiming:
+    unit_cost: float = 1.0
+    saturation_tokens: int = 32
+    latency_floor: float = 0.0
+
+
+@dataclass
+class TimingModel:
+    target: RoleTiming = field(default_factory=lambda: RoleTiming(1.0, 32, 2.0))
+    drafter: RoleTiming = field(default_factory=lambda: RoleTiming(0.1, 32, 0.4))
+
+    def _c(self):
+        return _TimingModel(_RoleTiming(self.target.unit_cost, self.target.saturation_tokens, self.target.latency_floor),
+                            _RoleTiming(self.drafter.unit_cost, self.drafter.saturation_tokens,
+                                        self.drafter.latency_floor))
+
+
+# ---- models ------------------------------------------------------------------------------------------
+class Model:
+    handle = None
+
+    @property
+    def version(self) -> int:
+        v = ctypes.c_int32()
+        _check(lib().rs_model_version(self.handle, ctypes.byref(v)))
+        return v.value
+
+    @property
+    def vocab_size(self) -> int:
+        v = ctypes.c_int32()
+        _check(lib().rs_model_vocab(self.handle, ctypes.byref(v)))
+        return v.value
+
+    def eos(self) -> int:  # Vocabulary::eos, model.hpp:20
+        return self.vocab_size - 1
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().rs_model_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+class TabularARModel(Model):
+    """TabularARModel (model.hpp:105-147) held in HBM in fp64 (parity mode)."""
+
+    def __init__(self, vocab: int, order: int, logits: Sequence[float], temperature: float = 1.0, version: int = 0,
+                 device: Optional[Device] = None):
+        self.device = device or default_device()
+        rows = vocab ** order if order >= 0 and vocab >= 2 else 0
+        logits = list(logits)
+        if vocab >= 2 and order >= 0 and temperature > 0 and len(logits) != rows * vocab:
+            raise InvalidArgument("TabularARModel: logits table has wrong shape")
+        self.order = order
+        self.temperature = temperature
+        h = ctypes.c_void_p()
+        _check(lib().rs_tabular_create(self.device.handle, vocab, order, temperature, _f64arr(logits), version,
+                                       ctypes.byref(h)))
+        self.handle = h
+
+    @staticmethod
+    def from_json(j: dict, device: Optional[Device] = None) -> "TabularARModel":  # model.cpp:183-191
+        return TabularARModel(j["vocab_size"] if "vocab_size" in j else j["vocab"], j["order"], j["logits"],
+                              j.get("temperature", 1.0), j.get("version", 0), device)
+
+    @staticmethod
+    def _wrap(handle, order, temperature, device):
+        m = TabularARModel.__new__(TabularARModel)
+        m.handle, m.order, m.temperature, m.device = handle, order, temperature, device
+        return m
+
+    def logits(self) -> List[float]:
+        n = self.vocab_size ** (self.order + 1)
+        buf = (ctypes.c_double * n)()
+        _check(lib().rs_tabular_logits(self.handle, buf, n))
+        return list(buf)
+
+    def to_json(self) -> dict:
+        return {"vocab_size": self.vocab_size, "order": self.order, "temperature": self.temperature,
+                "logits": self.logits()}
+
+
+# ---- ProfileTable (server.hpp:21-49) ------------------------------------------------------------------
+class ProfileTable:
+    def __init__(self, buckets: Sequence[int]):
+        h = ctypes.c_void_p()
+        _check(lib().rs_table_create(_i32arr(buckets), len(buckets), ctypes.byref(h)))
+        self.handle = h
+        self._buckets = sorted(buckets)
+        self._entries = {}
+
+    def set_entry(self, bucket: int, cfg: SDConfig, time_per_token: float):
+        _check(lib().rs_table_set_entry(self.handle, bucket, cfg._c(), time_per_token))
+        self._entries.setdefault(bucket, []).append((cfg, time_per_token))
+
+    def finalize(self):
+        _check(lib().rs_table_finalize(self.handle))
+
+    def bucket_for(self, active_batch: int) -> int:
+        v = ctypes.c_int32()
+        _check(lib().rs_table_bucket_for(self.handle, active_batch, ctypes.byref(v)))
+        return v.value
+
+    def solve(self, active_batch: int) -> SDConfig:
+        c = _SDConfig()
+        _check(lib().rs_table_solve(self.handle, active_batch, ctypes.byref(c)))
+        return SDConfig._from_c(c)
+
+    def best_for_bucket(self, bucket: int) -> SDConfig:
+        c = _SDConfig()
+        _check(lib().rs_table_best_for_bucket(self.handle, bucket, ctypes.byref(c)))
+        return SDConfig._from_c(c)
+
+    def entry(self, bucket: int, cfg: SDConfig) -> float:
+        v = ctypes.c_double()
+        _check(lib().rs_table_entry(self.handle, bucket, cfg._c(), ctypes.byref(v)))
+        return v.value
+
+    def baseline(self, bucket: int) -> float:
+        return self.entry(bucket, SDConfig.off())
+
+    def buckets(self) -> List[int]:
+        return list(self._buckets)
+
+    def entries_for(self, bucket: int):
+        if bucket not in self._entries:
+            raise InvalidArgument("ProfileTable: unknown bucket")
+        return list(self._entries[bucket])
+
+    def to_csv(self) -> str:
+        n = ctypes.c_int64()
+        _check(lib().rs_table_to_csv(self.handle, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        _check(lib().rs_table_to_csv(self.handle, buf, n.value + 1, ctypes.byref(n)))
+        return buf.value.decode()
+
+    def to_json(self) -> dict:  # server.cpp:98-118 schema
+        entries = [{"bucket": b, "s": c.rounds, "t": c.branching, "n": c.draft_len, "enabled": c.enabled,
+                    "time_per_token": t} for b in self._buckets for (c, t) in self._entries.get(b, [])]
+        best = [{"bucket": b, "s": c.rounds, "t": c.branching, "n": c.draft_len, "enabled": c.enabled}
+                for b in self._buckets for c in [self.best_for_bucket(b)]]
+        return {"buckets": self._buckets, "entries": entries, "best": best}
+
+    @staticmethod
+    def from_json(j: dict) -> "ProfileTable":  # server.cpp:120-130
+        t = ProfileTable(j["buckets"])
+        for e in j["entries"]:
+            t.set_entry(e["bucket"], SDConfig(e["s"], e["t"], e["n"], e["enabled"]), e["time_per_token"])
+        t.finalize()
+        return t
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().rs_table_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+# ---- requests / records ------------------------------------------------------------------------------------
+@dataclass(frozen=True)
+class DecodeRng:
+    """DecodeRng::from_seed(seed, stream_id) (rng.hpp:37-43); the streams live on the device."""
+    seed: int = 0
+    stream_id: int = 0
+
+    @staticmethod
+    def from_seed(seed: int, stream_id: int = 0) -> "DecodeRng":
+        return DecodeRng(seed, stream_id)
+
+
+@dataclass
+class StepRecord:
+    token: int
+    logp: float
+    drafted: bool
+    logq: float
+    target_logprobs: Optional[List[float]] = None
+
+
+@dataclass
+class RequestState:
+    """RequestState (server.hpp:69-83)."""
+    id: int = 0
+    prompt: List[int] = field(default_factory=list)
+    eos_bias: float = 0.0
+    max_len: int = 1
+    rng: DecodeRng = field(default_factory=DecodeRng)
+    generated: List[int] = field(default_factory=list)
+    steps: List[StepRecord] = field(default_factory=list)
+    accept_lens: List[int] = field(default_factory=list)
+    done: bool = False
+
+    def full_ctx(self) -> List[int]:
+        return list(self.prompt) + list(self.generated)
+
+    def remaining(self) -> int:
+        return self.max_len - len(self.generated)
+
+
+@dataclass
+class RolloutSample:
+    """RolloutSample (rollout.hpp:12-20)."""
+    prompt: List[int]
+    response: List[int]
+    steps: List[StepRecord]
+    eos_bias: float = 0.0
+    reward: float = 0.0
+    actor_version: int = 0
+    drafter_version: int = 0
+
+
+@dataclass
+class SwitchEvent:
+    cycle: int
+    active_batch: int
+    from_: SDConfig
+    to: SDConfig
+
+
+@dataclass
+class GenerationRun:
+    """GenerationRun (server.hpp:134-142)."""
+    samples: List[RolloutSample]
+    total_time: float
+    accept_lens: List[int]
+    switches: List[SwitchEvent]
+    active_trace: List[int]
+    ledger: List[tuple]
+    cycles: int
+    prefill_events: int = 0
+    wall_ms: float = 0.0  # measured device time over all steps
+
+
+DrafterSnapshotFn = Callable[[], Optional[Model]]
+
+
+class BatchEngine:
+    """BatchEngine (server.hpp:98-132) on the GPU: cycle-synchronous spec/non-spec state machine.
+
+    table=None selects fixed mode with `forced`. `drafter` is a DrafterSnapshotFn read once per
+    cycle, or None. verify_mode is "sample" (the reference's lossless rejection sampling) or
+    "greedy" (not in the reference)."""
+
+    def __init__(self, target: Model, drafter: Optional[DrafterSnapshotFn], table: Optional[ProfileTable],
+                 tm: Optional[TimingModel], requests: Sequence[RequestState], forced: SDConfig = SDConfig.off(),
+                 verify_mode: str = "sample", record_full_logprobs: bool = True, device: Optional[Device] = None):
+        self.device = device or getattr(target, "device", None) or default_device()
+        self._target = target
+        self._drafter_fn = drafter
+        self._table = table
+        self._reqs = [r for r in requests]
+        self._record_full = record_full_logprobs
+        self._vmode = {"sample": RS_VERIFY_SAMPLE, "greedy": RS_VERIFY_GREEDY}[verify_mode]
+        self._keep = []
+        arr = (_Request * max(1, len(self._reqs)))()
+        for i, r in enumerate(self._reqs):
+            p = _i32arr(r.prompt)
+            self._keep.append(p)
+            arr[i] = _Request(r.id, ctypes.cast(p, ctypes.POINTER(ctypes.c_int32)), len(r.prompt), r.eos_bias,
+                              r.max_len, r.rng.seed & (2 ** 64 - 1), r.rng.stream_id & (2 ** 64 - 1))
+        snap = drafter() if drafter is not None else None
+        self._snap = snap
+        tmc = (tm or TimingModel())._c()
+        h = ctypes.c_void_p()
+        _check(lib().rs_engine_create(self.device.handle, target.handle, snap.handle if snap else None,
+                                      table.handle if table else None, ctypes.byref(tmc), arr, len(self._reqs),
+                                      forced._c(), self._vmode, 1 if record_full_logprobs else 0, ctypes.byref(h)))
+        self.handle = h
+        self.last_info = None
+
+    def step(self):
+        """One engine cycle (server.cpp:266-349); raises EngineError on an empty batch."""
+        snap = self._drafter_fn() if self._drafter_fn is not None else None
+        self._snap = snap
+        _check(lib().rs_engine_set_drafter(self.handle, snap.handle if snap else None))
+        info = _StepInfo()
+        _check(lib().rs_engine_step(self.handle, ctypes.byref(info)))
+        self.last_info = info
+        return info
+
+    def _i(self, fn):
+        v = ctypes.c_int32()
+        _check(fn(self.handle, ctypes.byref(v)))
+        return v.value
+
+    def all_done(self) -> bool:
+        return bool(self._i(lib().rs_engine_all_done))
+
+    def active_batch(self) -> int:
+        return self._i(lib().rs_engine_active_batch)
+
+    def cycles(self) -> int:
+        return self._i(lib().rs_engine_cycles)
+
+    def prefill_events(self) -> int:
+        return self._i(lib().rs_engine_prefill_events)
+
+    def ledger_time(self) -> float:
+        v = ctypes.c_double()
+        _check(lib().rs_engine_ledger_time(self.handle, ctypes.byref(v)))
+        return v.value
+
+    def _arr(self, fn, ctype):
+        n = ctypes.c_int32()
+        _check(fn(self.handle, None, 0, ctypes.byref(n)))
+        buf = (ctype * max(1, n.value))()
+        _check(fn(self.handle, buf, n.value, ctypes.byref(n)))
+        return list(buf)[: n.value]
+
+    def ledger(self):
+        return [(e.role, e.positions, e.batch_tokens) for e in self._arr(lib().rs_engine_ledger, _ForwardEvent)]
+
+    def switches(self) -> List[SwitchEvent]:
+        return [SwitchEvent(s.cycle, s.active_batch, SDConfig._from_c(s.from_), SDConfig._from_c(s.to))
+                for s in self._arr(lib().rs_engine_switches, _SwitchEvent)]
+
+    def active_trace(self) -> List[int]:
+        return self._arr(lib().rs_engine_active_trace, ctypes.c_int32)
+
+    def drafter_version_at_cycle(self, cycle: int) -> int:
+        v = self._arr(lib().rs_engine_drafter_versions, ctypes.c_int32)
+        if cycle < 0 or cycle >= len(v):
+            raise IndexError("drafter_version_at_cycle: out of range")
+        return v[cycle]
+
+    def _response(self, i):
+        n = ctypes.c_int32()
+        _check(lib().rs_engine_response(self.handle, i, None, 0, ctypes.byref(n)))
+        buf = (ctypes.c_int32 * max(1, n.value))()
+        _check(lib().rs_engine_response(self.handle, i, buf, n.value, ctypes.byref(n)))
+        return list(buf)[: n.value]
+
+    def _steps(self, i, V):
+        n = len(self._response(i))
+        lp = (ctypes.c_double * max(1, n))()
+        lq = (ctypes.c_double * max(1, n))()
+        dr = (ctypes.c_uint8 * max(1, n))()
+        m = ctypes.c_int32()
+        _check(lib().rs_engine_steps(self.handle, i, lp, dr, lq, n, ctypes.byref(m)))
+        full = None
+        if self._record_full and n:
+            fb = (ctypes.c_double * (n * V))()
+            _check(lib().rs_engine_step_logprobs(self.handle, i, fb, n * V, ctypes.byref(m)))
+            full = [list(fb[k * V:(k + 1) * V]) for k in range(n)]
+        toks = self._response(i)
+        return [StepRecord(toks[k], lp[k], bool(dr[k]), lq[k], full[k] if full else None) for k in range(n)]
+
+    def requests(self) -> List[RequestState]:
+        V = self._target.vocab_size
+        out = []
+        for i, r in enumerate(self._reqs):
+            al = self._arr(lambda h, b, c, n, i=i: lib().rs_engine_accept_lens(h, i, b, c, n), ctypes.c_int32)
+            gen = self._response(i)
+            out.append(RequestState(r.id, list(r.prompt), r.eos_bias, r.max_len, r.rng, gen, self._steps(i, V), al,
+                                    len(gen) >= r.max_len or (len(gen) > 0 and gen[-1] == V - 1)))
+        return out
+
+    # debug: logits capture for replay against the CPU oracle
+    def set_capture(self, on: bool):
+        _check(lib().rs_engine_set_capture(self.handle, 1 if on else 0))
+
+    def captured_rows(self):
+        n, V = ctypes.c_int64(), ctypes.c_int32()
+        _check(lib().rs_engine_capture_count(self.handle, ctypes.byref(n), ctypes.byref(V)))
+        k, V = n.value, V.value
+        if k == 0:
+            return []
+        nmax = 64
+        role, req, cl = (ctypes.c_int32 * k)(), (ctypes.c_int32 * k)(), (ctypes.c_int32 * k)()
+        ext = (ctypes.c_int32 * (k * nmax))()
+        lg = (ctypes.c_double * (k * V))()
+        _check(lib().rs_engine_capture_read(self.handle, 0, k, role, req, cl, ext, lg))
+        return role, req, cl, ext, lg, V
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().rs_engine_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def run_generation(requests: Sequence[RequestState], target: Model, drafter: Optional[DrafterSnapshotFn],
+                   table: Optional[ProfileTable], tm: TimingModel, forced: SDConfig = SDConfig.off(),
+                   actor_version: int = 0, verify_mode: str = "sample", record_full_logprobs: bool = True,
+                   device: Optional[Device] = None) -> GenerationRun:
+    """run_generation (server.cpp:351-376): step until every request completes."""
+    eng = BatchEngine(target, drafter, table, tm, requests, forced, verify_mode, record_full_logprobs, device)
+    wall = 0.0
+    while not eng.all_done():
+        wall += eng.step().step_ms
+    reqs = eng.requests()
+    samples = [RolloutSample(r.prompt, r.generated, r.steps, r.eos_bias, 0.0, actor_version) for r in reqs]
+    al = [a for r in reqs for a in r.accept_lens]
+    return GenerationRun(samples, eng.ledger_time(), al, eng.switches(), eng.active_trace(), eng.ledger(),
+                         eng.cycles(), eng.prefill_events(), wall)
+
+
+# ---- KD learner (learner.hpp:15-69) --------------------------------------------------------------------------
+class WeightMode:
+    Reward, Uniform, Frozen = 0, 1, 2
+
+
+@dataclass
+class KDPolicy:
+    interval: int = 1
+    mode: int = WeightMode.Reward
+    clip_lo: float = 0.0
+    clip_hi: float = 4.0
+    lr: float = 0.1
+
+    def _c(self):
+        return _KDPolicy(self.interval, self.mode, self.clip_lo, self.clip_hi, self.lr)
+
+
+def kd_weight(r: float, batch_rewards: Sequence[float], policy: KDPolicy) -> float:
+    st = ctypes.c_int()
+    w = lib().rs_kd_weight(r, _f64arr(batch_rewards), len(batch_rewards), policy._c(), ctypes.byref(st))
+    _check(st.value)
+    return w
+
+
+class SelectionRng:
+    """std::mt19937_64 selection stream for kd_update, state kept host-side (learner.cpp:116-121)."""
+
+    def __init__(self, seed: int):
+        self.state = (ctypes.c_uint64 * 313)()
+        _check(lib().rs_mt19937_64_seed(seed & (2 ** 64 - 1), self.state))
+
+
+@dataclass
+class KDUpdateResult:
+    drafter: TabularARModel
+    updated: bool
+    loss: float
+    samples_used: int
+    weight_mean: float
+    weight_min: float
+    weight_max: float
+    sim_time: float
+
+
+def kd_update(drafter: TabularARModel, buffer: Sequence[RolloutSample], policy: KDPolicy, selection_rng: SelectionRng,
+              sim_cost_per_token: float) -> KDUpdateResult:
+    """kd_update (learner.cpp:98-160): loss + analytic gradient + SGD step on the device."""
+    V = drafter.vocab_size
+    keep = []
+    arr = (_KDSample * max(1, len(buffer)))()
+    for i, s in enumerate(buffer):
+        p, r = _i32arr(s.prompt), _i32arr(s.response)
+        if len(s.steps) != len(s.response):
+            raise InvalidArgument("kd_loss: steps/response length mismatch")
+        flat = [x for st in s.steps for x in st.target_logprobs]
+        lp = _f64arr(flat)
+        keep += [p, r, lp]
+        arr[i] = _KDSample(ctypes.cast(p, ctypes.POINTER(ctypes.c_int32)), len(s.prompt),
+                           ctypes.cast(r, ctypes.POINTER(ctypes.c_int32)), len(s.response),
+                           ctypes.cast(lp, ctypes.POINTER(ctypes.c_double)), s.eos_bias, s.reward)
+    h = ctypes.c_void_p()
+    res = _KDResult()
+    _check(lib().rs_kd_update_tabular(drafter.device.handle, drafter.handle, arr, len(buffer), policy._c(),
+                                      selection_rng.state, sim_cost_per_token, ctypes.byref(h), ctypes.byref(res)))
+    new = TabularARModel._wrap(h, drafter.order, drafter.temperature, drafter.device)
+    return KDUpdateResult(new, bool(res.updated), res.loss, res.samples_used, res.weight_mean, res.weight_min,
+                          res.weight_max, res.sim_time)

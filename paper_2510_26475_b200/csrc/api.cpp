@@ -1,0 +1,511 @@
+// api.cpp -- extern "C" entry points (include/respec_b200.h). Every entry point converts the
+// internal C++ exception into the status code of the reference's exception class and
+// keeps the message in a thread-local buffer for rs_last_error().
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "common.cuh"
+#include "engine.h"
+#include "kd.h"
+
+namespace {
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+template <class F>
+int guard(F &&f) {
+    try {
+        f();
+        return RS_OK;
+    } catch (const rs::CudaError &e) {
+        g_err = e.what();
+        return RS_ECUDA;
+    } catch (const std::bad_alloc &e) {
+        g_err = "out of memory";
+        return RS_ENOMEM;
+    } catch (const std::invalid_argument &e) {
+        g_err = e.what();
+        return RS_EINVAL;
+    } catch (const std::out_of_range &e) {
+        g_err = e.what();
+        return RS_EINVAL;
+    } catch (const std::logic_error &e) {
+        g_err = e.what();
+        return RS_ELOGIC;
+    } catch (const std::runtime_error &e) {
+        g_err = e.what();
+        return RS_ESTATE;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return RS_ESTATE;
+    }
+}
+
+void need(const void *p, const char *what) {
+    if (!p) throw std::invalid_argument(std::string(what) + ": null pointer");
+}
+
+void check_cfg(const rs_sdconfig &c) {
+    if (!c.enabled) return;
+    if (c.rounds < 1 || c.branching < 1 || c.draft_len < 1)
+        throw std::invalid_argument("SDConfig: rounds, branching and draft_len must be >= 1");
+    if (c.rounds > rs::kMaxRounds || c.branching > rs::kMaxBranch || c.draft_len > rs::kMaxDraft)
+        throw std::invalid_argument("SDConfig: exceeds engine limits (s<=8, t<=16, n<=32)");
+    // per-cycle RNG consumption must fit one mt19937_64 block (SURVEY App. A maxima)
+    if (c.rounds * c.branching * c.draft_len > rs::kMtN || c.rounds * (c.branching + c.draft_len - 1) + 1 > rs::kMtN)
+        throw std::invalid_argument("SDConfig: per-cycle draws exceed 312");
+}
+}  // namespace
+
+namespace {
+template <class T>
+void copy_out(const std::vector<T> &v, T *out, int32_t cap, int32_t *n) {
+    if (n) *n = (int32_t)v.size();
+    if (out) std::copy(v.begin(), v.begin() + std::min<size_t>(v.size(), (size_t)std::max(cap, 0)), out);
+}
+
+}  // namespace
+
+namespace rs {
+void note_launch() { ++g_launches; }
+}  // namespace rs
+
+using namespace rs;
+
+extern "C" {
+
+const char *rs_last_error(void) { return g_err.c_str(); }
+int rs_version(void) { return 10000; }
+int64_t rs_launch_count(void) { return g_launches; }
+void rs_launch_count_reset(void) { g_launches = 0; }
+
+int rs_ctx_create(int device, rs_ctx **out) {
+    return guard([&] {
+        need(out, "rs_ctx_create");
+        auto c = std::make_unique<rs_ctx>();
+        c->device = device;
+        RS_CUDA(cudaSetDevice(device));
+        RS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+        RS_CUDA(cudaEventCreate(&c->ev0));
+        RS_CUDA(cudaEventCreate(&c->ev1));
+        *out = c.release();
+    });
+}
+
+int rs_ctx_destroy(rs_ctx *ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+        if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+        if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+        if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+        delete ctx;
+    });
+}
+
+int rs_ctx_sync(rs_ctx *ctx) {
+    return guard([&] {
+        need(ctx, "rs_ctx_sync");
+        RS_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int rs_ctx_set_stream(rs_ctx *ctx, void *s) {
+    return guard([&] {
+        need(ctx, "rs_ctx_set_stream");
+        RS_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+        ctx->stream = static_cast<cudaStream_t>(s);
+        ctx->own_stream = false;
+    });
+}
+
+// ---- models --------------------------------------------------------------------------------
+int rs_tabular_create(rs_ctx *ctx, int32_t vocab, int32_t order, double temperature, const double *logits,
+                      int32_t version, rs_model **out) {
+    return guard([&] {
+        need(ctx, "rs_tabular_create");
+        need(out, "rs_tabular_create");
+        // TabularARModel constructor checks (model.cpp:80-94)
+        if (vocab < 2) throw std::invalid_argument("TabularARModel: vocab size must be >= 2");
+        if (order < 0) throw std::invalid_argument("TabularARModel: negative order");
+        if (!(temperature > 0.0)) throw std::invalid_argument("TabularARModel: temperature must be positive");
+        auto m = std::make_unique<TabularModel>();
+        m->ctx = ctx;
+        m->vocab = vocab;
+        m->order = order;
+        m->temperature = temperature;
+        m->version = version;
+        size_t rows = 1;
+        for (int i = 0; i < order; ++i) rows *= static_cast<size_t>(vocab);
+        m->rows = rows;
+        const size_t cnt = rows * static_cast<size_t>(vocab);
+        if (!logits) throw std::invalid_argument("TabularARModel: logits table has wrong shape");
+        m->host.assign(logits, logits + cnt);
+        m->table.alloc(cnt);
+        RS_CUDA(cudaMemcpy(m->table.p, logits, cnt * sizeof(double), cudaMemcpyHostToDevice));
+        *out = m.release();
+    });
+}
+
+int rs_tabular_logits(const rs_model *m, double *out, int64_t n) {
+    return guard([&] {
+        need(m, "rs_tabular_logits");
+        if (m->kind != rs_model::Tabular) throw std::invalid_argument("rs_tabular_logits: not a tabular model");
+        auto *t = static_cast<const TabularModel *>(m);
+        if (n < (int64_t)t->host.size()) throw std::invalid_argument("rs_tabular_logits: buffer too small");
+        std::memcpy(out, t->host.data(), t->host.size() * sizeof(double));
+    });
+}
+
+int rs_model_version(const rs_model *m, int32_t *out) {
+    return guard([&] { need(m, "rs_model_version"); *out = m->version; });
+}
+int rs_model_vocab(const rs_model *m, int32_t *out) {
+    return guard([&] { need(m, "rs_model_vocab"); *out = m->vocab; });
+}
+int rs_model_destroy(rs_model *m) {
+    return guard([&] { delete m; });
+}
+
+// ---- ProfileTable ----------------------------------------------------------------------------
+int rs_table_create(const int32_t *buckets, int32_t n, rs_table **out) {
+    return guard([&] {
+        need(out, "rs_table_create");
+        std::vector<int> b(buckets, buckets + std::max(0, n));
+        *out = new rs_table{ProfileTable(std::move(b))};
+    });
+}
+int rs_table_set_entry(rs_table *t, int32_t bucket, rs_sdconfig cfg, double tpt) {
+    return guard([&] { need(t, "rs_table_set_entry"); t->t.set_entry(bucket, cfg, tpt); });
+}
+int rs_table_finalize(rs_table *t) {
+    return guard([&] { need(t, "rs_table_finalize"); t->t.finalize(); });
+}
+int rs_table_bucket_for(const rs_table *t, int32_t b, int32_t *out) {
+    return guard([&] { need(t, "rs_table_bucket_for"); *out = t->t.bucket_for(b); });
+}
+int rs_table_solve(const rs_table *t, int32_t b, rs_sdconfig *out) {
+    return guard([&] { need(t, "rs_table_solve"); *out = t->t.solve(b); });
+}
+int rs_table_best_for_bucket(const rs_table *t, int32_t b, rs_sdconfig *out) {
+    return guard([&] { need(t, "rs_table_best_for_bucket"); *out = t->t.best_for_bucket(b); });
+}
+int rs_table_entry(const rs_table *t, int32_t b, rs_sdconfig cfg, double *out) {
+    return guard([&] { need(t, "rs_table_entry"); *out = t->t.entry(b, cfg); });
+}
+int rs_table_to_csv(const rs_table *t, char *buf, int64_t cap, int64_t *len) {
+    return guard([&] {
+        need(t, "rs_table_to_csv");
+        const std::string s = t->t.to_csv();
+        if (len) *len = (int64_t)s.size();
+        if (buf && cap > 0) {
+            const size_t k = std::min<size_t>(s.size(), (size_t)cap - 1);
+            std::memcpy(buf, s.data(), k);
+            buf[k] = 0;
+        }
+    });
+}
+int rs_table_destroy(rs_table *t) {
+    return guard([&] { delete t; });
+}
+
+// ---- engine -----------------------------------------------------------------------------------
+int rs_engine_create(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const rs_table *table,
+                     const rs_timing_model *tm, const rs_request *reqs, int32_t n, rs_sdconfig forced,
+                     int32_t verify_mode, int32_t record_full, rs_engine **out) {
+    return guard([&] {
+        need(ctx, "rs_engine_create");
+        need(target, "rs_engine_create: target");
+        need(out, "rs_engine_create");
+        if (n < 0 || (n > 0 && !reqs)) throw std::invalid_argument("rs_engine_create: bad request array");
+        if (verify_mode != RS_VERIFY_SAMPLE && verify_mode != RS_VERIFY_GREEDY)
+            throw std::invalid_argument("rs_engine_create: unknown verify mode");
+        if (target->kind == rs_model::Drafter) throw std::invalid_argument("rs_engine_create: target must not be a drafter");
+        check_cfg(forced);
+        auto e = std::make_unique<rs_engine>();
+        e->ctx = ctx;
+        e->target = target;
+        e->pending_drafter = drafter;
+        e->table = table ? &table->t : nullptr;
+        if (tm) e->tm = *tm;
+        else e->tm = rs_timing_model{{1.0, 32, 2.0}, {0.1, 32, 0.4}};
+        e->mode = forced;
+        e->verify_mode = verify_mode;
+        e->record_full = record_full != 0;
+        e->n = n;
+        e->V = target->vocab;
+        // sizes for every config this engine may run
+        std::vector<rs_sdconfig> cfgs{forced};
+        if (e->table) {
+            auto more = e->table->all_configs();
+            cfgs.insert(cfgs.end(), more.begin(), more.end());
+        }
+        for (const auto &c : cfgs) {
+            check_cfg(c);
+            if (!c.enabled) continue;
+            e->t_max = std::max(e->t_max, (int)c.branching);
+            e->n_max = std::max(e->n_max, (int)c.draft_len);
+            e->s_max = std::max(e->s_max, (int)c.rounds);
+            e->slots_max = std::max(e->slots_max, 1 + c.branching * c.draft_len);
+        }
+        int tok_cap = 1, steps_cap = 1;
+        std::vector<int32_t> h_tok;
+        std::vector<std::vector<int>> prompts;
+        for (int i = 0; i < n; ++i) {
+            const rs_request &r = reqs[i];
+            if (r.prompt_len < 0 || (r.prompt_len > 0 && !r.prompt)) throw std::invalid_argument("rs_request: bad prompt");
+            for (int k = 0; k < r.prompt_len; ++k)
+                if (r.prompt[k] < 0 || r.prompt[k] >= e->V) throw std::invalid_argument("row_index: token out of vocabulary");
+            tok_cap = std::max(tok_cap, r.prompt_len + std::max(r.max_len, 0) + 1);
+            steps_cap = std::max(steps_cap, std::max(r.max_len, 1));
+        }
+        e->tok_cap = tok_cap;
+        e->steps_cap = steps_cap;
+        h_tok.assign((size_t)std::max(n, 1) * tok_cap, 0);
+        std::vector<uint64_t> seeds(n), sids(n);
+        for (int i = 0; i < n; ++i) {
+            const rs_request &r = reqs[i];
+            e->ids.push_back(r.id);
+            e->prompt_len.push_back(r.prompt_len);
+            e->max_len.push_back(r.max_len);
+            e->len.push_back(r.prompt_len);
+            // a request with max_len <= 0 can never step (BatchEngine keeps it active; we
+            // mark it done so the engine cannot spin on it)
+            e->done.push_back(r.max_len <= 0 ? 1 : 0);
+            e->eos_bias.push_back(r.eos_bias);
+            std::copy(r.prompt, r.prompt + r.prompt_len, h_tok.begin() + (size_t)i * tok_cap);
+            seeds[i] = r.seed;
+            sids[i] = r.stream_id;
+            prompts.emplace_back(r.prompt, r.prompt + r.prompt_len);
+        }
+        e->accept_lens.resize(n);
+        const int N = std::max(n, 1);
+        e->d_tok.alloc((size_t)N * tok_cap);
+        RS_CUDA(cudaMemcpy(e->d_tok.p, h_tok.data(), h_tok.size() * 4, cudaMemcpyHostToDevice));
+        auto up_i = [&](DBuf<int32_t> &b, const std::vector<int> &v) {
+            b.alloc(N);
+            if (!v.empty()) RS_CUDA(cudaMemcpy(b.p, v.data(), v.size() * 4, cudaMemcpyHostToDevice));
+        };
+        up_i(e->d_len, e->len);
+        up_i(e->d_plen, e->prompt_len);
+        up_i(e->d_maxlen, e->max_len);
+        up_i(e->d_done, e->done);
+        e->d_active.alloc(N);
+        e->d_bias.alloc(N);
+        if (n) RS_CUDA(cudaMemcpy(e->d_bias.p, e->eos_bias.data(), n * 8, cudaMemcpyHostToDevice));
+        e->d_rng.alloc(2 * (size_t)N);
+        DBuf<uint64_t> dseed(N), dsid(N);
+        if (n) {
+            RS_CUDA(cudaMemcpy(dseed.p, seeds.data(), n * 8, cudaMemcpyHostToDevice));
+            RS_CUDA(cudaMemcpy(dsid.p, sids.data(), n * 8, cudaMemcpyHostToDevice));
+            rng_init(e->d_rng.p, dseed.p, dsid.p, n, ctx->stream);
+        }
+        e->d_st_tok.alloc((size_t)N * steps_cap);
+        e->d_st_logp.alloc((size_t)N * steps_cap);
+        e->d_st_logq.alloc((size_t)N * steps_cap);
+        e->d_st_drafted.alloc((size_t)N * steps_cap);
+        if (e->record_full) e->d_st_full.alloc((size_t)N * steps_cap * e->V);
+        e->d_cyc.alloc((size_t)N * 9);
+        e->d_round_cost.alloc((size_t)N * kMaxRounds * 3);
+        e->d_chain.alloc((size_t)N * e->t_max * (e->n_max + 3));
+        RS_CUDA(cudaMemset(e->d_chain.p, 0, e->d_chain.bytes()));
+        e->d_err.alloc(1);
+        e->d_flag.alloc(1);
+        RS_CUDA(cudaMemset(e->d_err.p, 0, 4));
+        RS_CUDA(cudaMemset(e->d_flag.p, 0, 4));
+        e->d_summary.alloc((size_t)N * (kSummaryFixed + 3 * kMaxRounds));
+        RS_CUDA(cudaMallocHost(&e->h_summary, (size_t)N * (kSummaryFixed + 3 * kMaxRounds) * 4));
+        RS_CUDA(cudaMallocHost(&e->h_active, (size_t)N * 4));
+        RS_CUDA(cudaMallocHost(&e->h_misc, 16));
+        std::memset(e->h_misc, 0, 16);
+
+        if (target->kind == rs_model::Tabular) {
+            if (drafter && drafter->kind != rs_model::Tabular) throw std::invalid_argument("tabular target needs a tabular drafter");
+            const size_t rows = (size_t)N * e->slots_max * e->V * sizeof(double);
+            e->d_P.alloc(rows);
+            e->d_Q.alloc(rows);
+            e->pair = make_tabular_pair(static_cast<const TabularModel *>(target), static_cast<const TabularModel *>(drafter));
+        } else {
+            const size_t rows = (size_t)N * e->slots_max * e->V * sizeof(float);
+            e->d_P.alloc(rows);
+            e->d_Q.alloc(rows);
+            e->pair = make_transformer_pair(ctx, target, drafter, n, e->slots_max, e->prompt_len, prompts, tok_cap);
+        }
+        if (drafter && drafter->vocab != e->V) throw std::invalid_argument("BatchEngine: drafter vocabulary differs from target");
+        RS_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = e.release();
+    });
+}
+
+int rs_engine_set_drafter(rs_engine *e, const rs_model *drafter) {
+    return guard([&] { need(e, "rs_engine_set_drafter"); e->pending_drafter = drafter; });
+}
+int rs_engine_step(rs_engine *e, rs_step_info *info) {
+    return guard([&] { need(e, "rs_engine_step"); e->step(info); });
+}
+int rs_engine_all_done(const rs_engine *e, int32_t *out) {
+    return guard([&] {
+        need(e, "rs_engine_all_done");
+        *out = std::all_of(e->done.begin(), e->done.end(), [](int d) { return d != 0; });
+    });
+}
+int rs_engine_active_batch(const rs_engine *e, int32_t *out) {
+    return guard([&] {
+        need(e, "rs_engine_active_batch");
+        *out = (int32_t)std::count(e->done.begin(), e->done.end(), 0);
+    });
+}
+int rs_engine_cycles(const rs_engine *e, int32_t *out) {
+    return guard([&] { need(e, "rs_engine_cycles"); *out = e->cycle; });
+}
+int rs_engine_prefill_events(const rs_engine *e, int32_t *out) {
+    return guard([&] { need(e, "rs_engine_prefill_events"); *out = e->prefill_events; });
+}
+int rs_engine_ledger_time(const rs_engine *e, double *out) {
+    return guard([&] {
+        need(e, "rs_engine_ledger_time");
+        // ledger_time / forward_time (costsim.cpp:13-27)
+        double total = 0.0;
+        for (const auto &ev : e->ledger) {
+            const rs_role_timing &t = ev.role ? e->tm.target : e->tm.drafter;
+            if (ev.batch_tokens < 1) throw std::invalid_argument("forward_time: total_tokens must be >= 1");
+            total += t.latency_floor + t.unit_cost * (double)std::max(ev.batch_tokens, t.saturation_tokens);
+        }
+        *out = total;
+    });
+}
+
+int rs_engine_ledger(const rs_engine *e, rs_forward_event *out, int32_t cap, int32_t *n) {
+    return guard([&] { need(e, "rs_engine_ledger"); copy_out(e->ledger, out, cap, n); });
+}
+int rs_engine_switches(const rs_engine *e, rs_switch_event *out, int32_t cap, int32_t *n) {
+    return guard([&] { need(e, "rs_engine_switches"); copy_out(e->switches, out, cap, n); });
+}
+int rs_engine_active_trace(const rs_engine *e, int32_t *out, int32_t cap, int32_t *n) {
+    return guard([&] { need(e, "rs_engine_active_trace"); copy_out(e->active_trace, (int *)out, cap, n); });
+}
+int rs_engine_drafter_versions(const rs_engine *e, int32_t *out, int32_t cap, int32_t *n) {
+    return guard([&] { need(e, "rs_engine_drafter_versions"); copy_out(e->drafter_versions, (int *)out, cap, n); });
+}
+
+static void check_req(const rs_engine *e, int32_t req) {
+    if (req < 0 || req >= e->n) throw std::invalid_argument("request index out of range");
+}
+
+int rs_engine_response(rs_engine *e, int32_t req, int32_t *tokens, int32_t cap, int32_t *len) {
+    return guard([&] {
+        need(e, "rs_engine_response");
+        check_req(e, req);
+        const int gen = e->len[req] - e->prompt_len[req];
+        if (len) *len = gen;
+        const int k = std::min(gen, std::max(cap, 0));
+        if (tokens && k > 0)
+            RS_CUDA(cudaMemcpy(tokens, e->d_tok.p + (size_t)req * e->tok_cap + e->prompt_len[req], k * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+int rs_engine_steps(rs_engine *e, int32_t req, double *logp, uint8_t *drafted, double *logq, int32_t cap, int32_t *n) {
+    return guard([&] {
+        need(e, "rs_engine_steps");
+        check_req(e, req);
+        const int gen = e->len[req] - e->prompt_len[req];
+        if (n) *n = gen;
+        const int k = std::min(gen, std::max(cap, 0));
+        if (k <= 0) return;
+        const size_t off = (size_t)req * e->steps_cap;
+        if (logp) RS_CUDA(cudaMemcpy(logp, e->d_st_logp.p + off, k * 8, cudaMemcpyDeviceToHost));
+        if (drafted) RS_CUDA(cudaMemcpy(drafted, e->d_st_drafted.p + off, k, cudaMemcpyDeviceToHost));
+        if (logq) RS_CUDA(cudaMemcpy(logq, e->d_st_logq.p + off, k * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int rs_engine_step_logprobs(rs_engine *e, int32_t req, double *out, int64_t cap, int32_t *rows) {
+    return guard([&] {
+        need(e, "rs_engine_step_logprobs");
+        check_req(e, req);
+        if (!e->record_full) throw std::invalid_argument("engine was created without record_full_logprobs");
+        const int gen = e->len[req] - e->prompt_len[req];
+        if (rows) *rows = gen;
+        const int64_t k = std::min<int64_t>((int64_t)gen * e->V, cap);
+        if (out && k > 0)
+            RS_CUDA(cudaMemcpy(out, e->d_st_full.p + (size_t)req * e->steps_cap * e->V, k * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int rs_engine_accept_lens(rs_engine *e, int32_t req, int32_t *out, int32_t cap, int32_t *n) {
+    return guard([&] {
+        need(e, "rs_engine_accept_lens");
+        check_req(e, req);
+        copy_out(e->accept_lens[req], (int *)out, cap, n);
+    });
+}
+
+int rs_engine_destroy(rs_engine *e) {
+    return guard([&] {
+        if (e && e->ctx) cudaStreamSynchronize(e->ctx->stream);
+        delete e;
+    });
+}
+
+int rs_engine_set_capture(rs_engine *e, int32_t enable) {
+    return guard([&] { need(e, "rs_engine_set_capture"); e->capture = enable != 0; });
+}
+int rs_engine_capture_count(const rs_engine *e, int64_t *rows, int32_t *vocab) {
+    return guard([&] {
+        need(e, "rs_engine_capture_count");
+        *rows = (int64_t)e->cap_role.size();
+        *vocab = e->V;
+    });
+}
+int rs_engine_capture_read(rs_engine *e, int64_t first, int64_t count, int32_t *role, int32_t *req, int32_t *ctx_len,
+                           int32_t *ext, double *logits) {
+    return guard([&] {
+        need(e, "rs_engine_capture_read");
+        const int64_t total = (int64_t)e->cap_role.size();
+        if (first < 0 || count < 0 || first + count > total) throw std::invalid_argument("capture range");
+        for (int64_t i = 0; i < count; ++i) {
+            const int64_t k = first + i;
+            if (role) role[i] = e->cap_role[k];
+            if (req) req[i] = e->cap_req[k];
+            if (ctx_len) ctx_len[i] = e->cap_ctx_len[k];
+            if (ext) std::copy_n(&e->cap_ext[k * e->n_max], e->n_max, ext + i * e->n_max);
+            if (logits) std::copy_n(&e->cap_logits[k * e->V], e->V, logits + i * e->V);
+        }
+    });
+}
+
+// ---- KD ---------------------------------------------------------------------------------------
+double rs_kd_weight(double r, const double *br, int32_t n, rs_kd_policy p, int *status) {
+    double w = 0.0;
+    const int s = guard([&] { w = kd_weight(r, std::vector<double>(br, br + std::max(n, 0)), p); });
+    if (status) *status = s;
+    return w;
+}
+
+int rs_kd_update_tabular(rs_ctx *ctx, const rs_model *drafter, const rs_kd_sample *buf, int32_t n, rs_kd_policy policy,
+                         uint64_t *sel_state, double cost, rs_model **new_drafter, rs_kd_result *out) {
+    return guard([&] {
+        need(ctx, "rs_kd_update_tabular");
+        need(drafter, "rs_kd_update_tabular: drafter");
+        need(sel_state, "rs_kd_update_tabular: selection rng");
+        need(new_drafter, "rs_kd_update_tabular: out");
+        if (drafter->kind != rs_model::Tabular) throw std::invalid_argument("rs_kd_update_tabular: tabular drafter required");
+        kd_update_tabular(ctx, static_cast<const TabularModel *>(drafter), buf, n, policy, sel_state, cost, new_drafter, out);
+    });
+}
+
+int rs_mt19937_64_seed(uint64_t seed, uint64_t *state) {
+    return guard([&] {
+        need(state, "rs_mt19937_64_seed");
+        HostMt m;
+        m.seed(seed);
+        std::copy(m.mt, m.mt + kMtN, state);
+        state[kMtN] = (uint64_t)m.idx;
+    });
+}
+
+}  // extern "C"

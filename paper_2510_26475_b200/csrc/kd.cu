@@ -1,0 +1,276 @@
+// kd.cu -- K5: reward-weighted KL distillation loss + analytic gradient (learner.cpp:33-82).
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <numeric>
+#include <stdexcept>
+
+#include "common.cuh"
+#include "kd.h"
+
+namespace rs {
+
+double kd_weight(double r, const std::vector<double> &br, const rs_kd_policy &p) {
+    switch (p.mode) {
+        case 1: return 1.0;  // Uniform
+        case 2: throw std::logic_error("kd_weight: frozen drafter takes no updates");
+        case 0: break;
+        default: throw std::invalid_argument("kd_weight: unknown weight mode");
+    }
+    if (br.empty()) throw std::invalid_argument("kd_weight: empty batch");
+    const double mean = std::accumulate(br.begin(), br.end(), 0.0) / static_cast<double>(br.size());
+    const double w = r / std::max(1e-6, mean);
+    return std::clamp(w, p.clip_lo, p.clip_hi);
+}
+
+namespace {
+
+struct Job {
+    int seq_off;   // offset of the sample's token sequence (prompt + response)
+    int ctx_len;   // context length for this position
+    int lp_off;    // row offset (in units of V) into the target logprob rows
+    int sample;    // selected-sample index
+    double bias;
+};
+
+// Per position: drafter row stats (max, sum) and sum_x p(x) (lp(x) - log q(x)) (learner.cpp:33-54).
+__global__ void __launch_bounds__(1024, 1) kd_job_kernel(const double *table, int order, int V, double tau, const int *tokens, const Job *jobs,
+                              const double *lp, double *job_m, double *job_s, double *job_kl, long long *job_row) {
+    __shared__ double red[32];
+    const Job jb = jobs[blockIdx.x];
+    long long row = 0;
+    for (int i = 0; i < order; ++i) {  // row_index, model.cpp:113-130
+        const int p = jb.ctx_len - (order - i);
+        const int tok = p >= 0 ? tokens[jb.seq_off + p] : 0;
+        row = row * V + tok;
+    }
+    const double *z = table + row * V;
+    auto zv = [&](int x) { double y = z[x]; if (x == V - 1) y += jb.bias; return y / tau; };
+    double m = -INFINITY;
+    for (int x = threadIdx.x; x < V; x += blockDim.x) m = fmax(m, zv(x));
+    m = block_max(m, red);
+    double s = 0.0;
+    for (int x = threadIdx.x; x < V; x += blockDim.x) s += exp(zv(x) - m);
+    s = block_sum(s, red);
+    const double *l = lp + (size_t)jb.lp_off * V;
+    double kl = 0.0;
+    for (int x = threadIdx.x; x < V; x += blockDim.x) {
+        if (isinf(l[x])) continue;  // p = 0 contributes nothing
+        const double logq = log(exp(zv(x) - m) / s);
+        kl += exp(l[x]) * (l[x] - logq);
+    }
+    kl = block_sum(kl, red);
+    if (threadIdx.x == 0) {
+        job_m[blockIdx.x] = m;
+        job_s[blockIdx.x] = s;
+        job_kl[blockIdx.x] = kl;
+        job_row[blockIdx.x] = row;
+    }
+}
+
+// One block per touched table row: grad(x) = sum over that row's jobs, in the reference's
+// order (sample, then position), of w * (q(x) - p(x)) / tau; new = old + grad * (-lr)
+// (learner.cpp:62-82, :146-151, model.cpp:161-170).
+__global__ void __launch_bounds__(1024, 1) kd_row_kernel(const double *table, double *out, int V, double tau, const Job *jobs,
+                              const int *row_jobs, const int *row_ptr, const long long *rows, const double *lp,
+                              const double *job_m, const double *job_s, const double *w, double neg_lr) {
+    const long long row = rows[blockIdx.x];
+    const double inv_tau = 1.0 / tau;
+    for (int x = threadIdx.x; x < V; x += blockDim.x) {
+        double g = 0.0;
+        for (int k = row_ptr[blockIdx.x]; k < row_ptr[blockIdx.x + 1]; ++k) {
+            const int j = row_jobs[k];
+            const Job jb = jobs[j];
+            double y = table[row * V + x];
+            if (x == V - 1) y += jb.bias;
+            const double q = exp(y / tau - job_m[j]) / job_s[j];
+            const double l = lp[(size_t)jb.lp_off * V + x];
+            const double p = isinf(l) ? 0.0 : exp(l);
+            g += w[jb.sample] * (q - p) * inv_tau;
+        }
+        out[row * V + x] = table[row * V + x] + g * neg_lr;
+    }
+}
+
+// K5 for transformer-sized rows.
+__global__ void __launch_bounds__(1024, 1) kd_rows_kernel(const float *trow, const float *drow, const double *w, const double *bias, int V,
+                               double tau_p, double tau_q, double *loss, float *dz) {
+    __shared__ double red[32];
+    const int i = blockIdx.x;
+    const float *zt = trow + (size_t)i * V;
+    const float *zd = drow + (size_t)i * V;
+    const double b = bias ? bias[i] : 0.0;
+    auto vt = [&](int x) { double y = zt[x]; if (x == V - 1) y += b; return y / tau_p; };
+    auto vd = [&](int x) { double y = zd[x]; if (x == V - 1) y += b; return y / tau_q; };
+    double mt = -INFINITY, md = -INFINITY;
+    for (int x = threadIdx.x; x < V; x += blockDim.x) {
+        mt = fmax(mt, vt(x));
+        md = fmax(md, vd(x));
+    }
+    mt = block_max(mt, red);
+    md = block_max(md, red);
+    double st = 0.0, sd = 0.0;
+    for (int x = threadIdx.x; x < V; x += blockDim.x) {
+        st += exp(vt(x) - mt);
+        sd += exp(vd(x) - md);
+    }
+    st = block_sum(st, red);
+    sd = block_sum(sd, red);
+    const double lst = log(st), lsd = log(sd);
+    const double wi = w[i];
+    double kl = 0.0;
+    for (int x = threadIdx.x; x < V; x += blockDim.x) {
+        const double lp = vt(x) - mt - lst, lq = vd(x) - md - lsd;
+        const double p = exp(lp), q = exp(lq);
+        if (p > 0.0) kl += p * (lp - lq);
+        dz[(size_t)i * V + x] = static_cast<float>(wi * (q - p) / tau_q);
+    }
+    kl = block_sum(kl, red);
+    if (threadIdx.x == 0) loss[i] = wi * kl;
+}
+
+}  // namespace
+
+void kd_rows_loss_grad(const float *target_rows, const float *drafter_rows, const double *weights,
+                       const double *eos_bias, int rows, int V, double tau_p, double tau_q, double *loss_out,
+                       float *dz_out, cudaStream_t st) {
+    if (rows <= 0) return;
+    kd_rows_kernel<<<rows, V <= 4096 ? 256 : 1024, 0, st>>>(target_rows, drafter_rows, weights, eos_bias, V, tau_p,
+                                                             tau_q, loss_out, dz_out);
+    RS_LAUNCHED();
+}
+
+void kd_update_tabular(rs_ctx *ctx, const TabularModel *drafter, const rs_kd_sample *buf, int n,
+                       const rs_kd_policy &policy, uint64_t *sel_state, double cost, rs_model **out_model,
+                       rs_kd_result *out) {
+    if (policy.mode == 2) throw std::logic_error("kd_update: frozen drafter takes no updates");
+    if (policy.interval < 1) throw std::invalid_argument("kd_update: interval must be >= 1");
+    const int V = drafter->vocab;
+    auto copy_model = [&](bool bump) {
+        auto m = std::make_unique<TabularModel>();
+        m->ctx = ctx;
+        m->vocab = V;
+        m->order = drafter->order;
+        m->rows = drafter->rows;
+        m->temperature = drafter->temperature;
+        m->version = drafter->version + (bump ? 1 : 0);
+        m->host = drafter->host;
+        m->table.alloc(m->host.size());
+        return m;
+    };
+    rs_kd_result res{};
+    if (n <= 0) {  // empty buffer: no-op (learner.cpp:103-105)
+        auto m = copy_model(false);
+        RS_CUDA(cudaMemcpy(m->table.p, drafter->table.p, m->host.size() * 8, cudaMemcpyDeviceToDevice));
+        *out_model = m.release();
+        if (out) *out = res;
+        return;
+    }
+    // selection (learner.cpp:107-121): partial Fisher-Yates with selection_rng() % (n - i)
+    HostMt rng;
+    std::copy(sel_state, sel_state + kMtN, rng.mt);
+    rng.idx = static_cast<int>(sel_state[kMtN]);
+    const size_t N = static_cast<size_t>(n);
+    const size_t take = (N + static_cast<size_t>(policy.interval) - 1) / static_cast<size_t>(policy.interval);
+    std::vector<size_t> idx(N);
+    std::iota(idx.begin(), idx.end(), size_t{0});
+    for (size_t i = 0; i < take; ++i) {
+        const size_t j = i + static_cast<size_t>(rng.next() % (N - i));
+        std::swap(idx[i], idx[j]);
+    }
+    std::copy(rng.mt, rng.mt + kMtN, sel_state);
+    sel_state[kMtN] = static_cast<uint64_t>(rng.idx);
+
+    std::vector<double> br(take), w(take);
+    for (size_t i = 0; i < take; ++i) br[i] = buf[idx[i]].reward;
+    double wsum = 0, wmin = 0, wmax = 0;
+    size_t distilled = 0;
+    std::vector<int32_t> tokens;
+    std::vector<double> lp;
+    std::vector<Job> jobs;
+    std::vector<std::vector<int>> per_sample_jobs(take);
+    for (size_t i = 0; i < take; ++i) {
+        const rs_kd_sample &s = buf[idx[i]];
+        w[i] = kd_weight(s.reward, br, policy);
+        wsum += w[i];
+        wmin = i == 0 ? w[i] : std::min(wmin, w[i]);
+        wmax = i == 0 ? w[i] : std::max(wmax, w[i]);
+        distilled += static_cast<size_t>(s.response_len);
+        const int seq_off = static_cast<int>(tokens.size());
+        tokens.insert(tokens.end(), s.prompt, s.prompt + s.prompt_len);
+        tokens.insert(tokens.end(), s.response, s.response + s.response_len);
+        for (int t = 0; t < s.response_len; ++t) {
+            const int lp_off = static_cast<int>(lp.size() / V);
+            lp.insert(lp.end(), s.target_logprobs + (size_t)t * V, s.target_logprobs + (size_t)(t + 1) * V);
+            per_sample_jobs[i].push_back(static_cast<int>(jobs.size()));
+            jobs.push_back(Job{seq_off, s.prompt_len + t, lp_off, static_cast<int>(i), s.eos_bias});
+        }
+    }
+    for (int v : tokens)
+        if (v < 0 || v >= V) throw std::invalid_argument("row_index: token out of vocabulary");
+
+    auto m = copy_model(true);
+    cudaStream_t st = ctx->stream;
+    const int J = static_cast<int>(jobs.size());
+    std::vector<double> kl(J);
+    std::vector<long long> rows(J);
+    if (J > 0) {
+        DBuf<int32_t> d_tok(tokens.size());
+        DBuf<double> d_lp(lp.size()), d_m(J), d_s(J), d_kl(J), d_w(take);
+        DBuf<Job> d_jobs(J);
+        DBuf<long long> d_row(J);
+        RS_CUDA(cudaMemcpyAsync(d_tok.p, tokens.data(), tokens.size() * 4, cudaMemcpyHostToDevice, st));
+        RS_CUDA(cudaMemcpyAsync(d_lp.p, lp.data(), lp.size() * 8, cudaMemcpyHostToDevice, st));
+        RS_CUDA(cudaMemcpyAsync(d_jobs.p, jobs.data(), J * sizeof(Job), cudaMemcpyHostToDevice, st));
+        RS_CUDA(cudaMemcpyAsync(d_w.p, w.data(), take * 8, cudaMemcpyHostToDevice, st));
+        const int th = V <= 256 ? 32 : V <= 4096 ? 256 : 1024;
+        kd_job_kernel<<<J, th, 0, st>>>(drafter->table.p, drafter->order, V, drafter->temperature, d_tok.p, d_jobs.p,
+                                        d_lp.p, d_m.p, d_s.p, d_kl.p, d_row.p);
+        RS_LAUNCHED();
+        RS_CUDA(cudaMemcpyAsync(kl.data(), d_kl.p, J * 8, cudaMemcpyDeviceToHost, st));
+        RS_CUDA(cudaMemcpyAsync(rows.data(), d_row.p, J * 8, cudaMemcpyDeviceToHost, st));
+        RS_CUDA(cudaStreamSynchronize(st));
+        // group jobs by row, keeping job order (= sample order, then position)
+        std::map<long long, std::vector<int>> by_row;
+        for (int j = 0; j < J; ++j) by_row[rows[j]].push_back(j);
+        std::vector<int> row_jobs, row_ptr{0};
+        std::vector<long long> urows;
+        for (auto &[r, js] : by_row) {
+            urows.push_back(r);
+            row_jobs.insert(row_jobs.end(), js.begin(), js.end());
+            row_ptr.push_back(static_cast<int>(row_jobs.size()));
+        }
+        DBuf<int32_t> d_rj(row_jobs.size()), d_rp(row_ptr.size());
+        DBuf<long long> d_ur(urows.size());
+        RS_CUDA(cudaMemcpyAsync(d_rj.p, row_jobs.data(), row_jobs.size() * 4, cudaMemcpyHostToDevice, st));
+        RS_CUDA(cudaMemcpyAsync(d_rp.p, row_ptr.data(), row_ptr.size() * 4, cudaMemcpyHostToDevice, st));
+        RS_CUDA(cudaMemcpyAsync(d_ur.p, urows.data(), urows.size() * 8, cudaMemcpyHostToDevice, st));
+        RS_CUDA(cudaMemcpyAsync(m->table.p, drafter->table.p, m->host.size() * 8, cudaMemcpyDeviceToDevice, st));
+        kd_row_kernel<<<(int)urows.size(), th, 0, st>>>(drafter->table.p, m->table.p, V, drafter->temperature,
+                                                        d_jobs.p, d_rj.p, d_rp.p, d_ur.p, d_lp.p, d_m.p, d_s.p, d_w.p,
+                                                        -policy.lr);
+        RS_LAUNCHED();
+        RS_CUDA(cudaMemcpyAsync(m->host.data(), m->table.p, m->host.size() * 8, cudaMemcpyDeviceToHost, st));
+        RS_CUDA(cudaStreamSynchronize(st));
+    } else {
+        RS_CUDA(cudaMemcpy(m->table.p, drafter->table.p, m->host.size() * 8, cudaMemcpyDeviceToDevice));
+    }
+    // loss on the pre-update drafter: sum_i w_i * sum_t KL_t (learner.cpp:142-145)
+    double loss = 0.0;
+    for (size_t i = 0; i < take; ++i) {
+        double total = 0.0;
+        for (int j : per_sample_jobs[i]) total += kl[j];
+        loss += w[i] * total;
+    }
+    res.updated = 1;
+    res.samples_used = static_cast<int>(take);
+    res.loss = loss;
+    res.weight_mean = wsum / static_cast<double>(take);
+    res.weight_min = wmin;
+    res.weight_max = wmax;
+    res.sim_time = cost * static_cast<double>(distilled);
+    *out_model = m.release();
+    if (out) *out = res;
+}
+
+}  // namespace rs

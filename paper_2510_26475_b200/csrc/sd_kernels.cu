@@ -1,0 +1,650 @@
+// sd_kernels.cu -- model-agnostic speculative-decoding kernels (sm_100a).
+//
+// K3 "fused softmax + acceptance": one CTA per active sequence walks the reference's
+// acceptance algorithm (specdec.cpp:197-267) over the logit rows the model forwards
+// produced, with block-wide max/sum reductions for the softmax normaliser, warp-segmented
+// prefix scans for the inverse CDF (model.cpp:23-40) and argmax reductions for greedy
+// verification. All probability arithmetic is fp64, exactly the reference's formula
+// p = exp(z/tau - max) / sum (model.cpp:53-68); only the summation ORDER differs (parallel
+// tree instead of sequential), i.e. ulp-level differences that can flip a token only when a
+// uniform lands within ~1e-16 of a CDF boundary.
+//
+// The drafting sampler draws each chain's tokens from the drafter rows with the request's
+// own draft stream at the offsets the reference's sequential loop would use
+// (specdec.cpp:177-192); chains are drafted level-synchronously (all chains of all requests
+// at depth j in one launch) and an EOS-shortened chain triggers a redraft pass with
+// corrected offsets (sd_redraft_check), so the stream order is preserved exactly.
+#include <cfloat>
+#include <climits>
+
+#include "common.cuh"
+#include "sd.h"
+
+namespace rs {
+
+namespace {
+
+template <class T>
+struct RowRef {
+    const T *z;
+    int V;
+    double bias;
+    double tau;
+    // z'/tau with the EOS bias added to the last logit before the temperature division
+    // (model.cpp:137-138, model.cpp:58-61)
+    __device__ __forceinline__ double v(int x) const {
+        double y = static_cast<double>(z[x]);
+        if (x == V - 1) y += bias;
+        return y / tau;
+    }
+};
+
+struct Stats {
+    double m, S;
+};
+
+template <class T>
+__device__ Stats row_stats(const RowRef<T> &r, double *red) {
+    double m = -INFINITY;
+    for (int x = threadIdx.x; x < r.V; x += blockDim.x) m = fmax(m, r.v(x));
+    m = block_max(m, red);
+    double s = 0.0;
+    for (int x = threadIdx.x; x < r.V; x += blockDim.x) s += exp(r.v(x) - m);
+    s = block_sum(s, red);
+    return {m, s};
+}
+
+template <class T>
+__device__ __forceinline__ double prob(const RowRef<T> &r, const Stats &s, int x) {
+    return exp(r.v(x) - s.m) / s.S;
+}
+
+template <class T>
+struct ProbFn {
+    RowRef<T> r;
+    Stats s;
+    __device__ __forceinline__ double operator()(int x) const { return prob(r, s, x); }
+};
+
+// p_cur after k sibling rejections: r_j = max(0, r_{j-1} - q1) / Z_j (specdec.cpp:209 -> :35-52)
+template <class T>
+struct PCurFn {
+    RowRef<T> p;
+    Stats sp;
+    RowRef<T> q;
+    Stats sq;
+    const double *Z;
+    int k;
+    __device__ __forceinline__ double operator()(int x) const {
+        double r = prob(p, sp, x);
+        if (k > 0) {
+            const double qq = prob(q, sq, x);
+            for (int j = 0; j < k; ++j) r = fmax(0.0, r - qq) / Z[j];
+        }
+        return r;
+    }
+};
+
+// Chain-position residual max(0, pd - qd) / Z (specdec.cpp:238)
+template <class T>
+struct ResidFn {
+    RowRef<T> p;
+    Stats sp;
+    RowRef<T> q;
+    Stats sq;
+    double Z;
+    __device__ __forceinline__ double operator()(int x) const {
+        return fmax(0.0, prob(p, sp, x) - prob(q, sq, x)) / Z;
+    }
+};
+
+template <class F>
+__device__ double block_total(const F &f, int V, double *red) {
+    double s = 0.0;
+    for (int x = threadIdx.x; x < V; x += blockDim.x) s += f(x);
+    return block_sum(s, red);
+}
+
+// Inverse-CDF draw (model.cpp:23-40): first x with u < cum(x); on rounding slack the last
+// x with nonzero mass. Warp w owns the contiguous segment [w*Sw, (w+1)*Sw); pass A sums the
+// segments, pass B rescans only the segment(s) whose range brackets u.
+template <class F>
+__device__ int inv_cdf(const F &f, int V, double u, double *red, long long *redl, int *err) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int Sw = (V + nw - 1) / nw;
+    const int lo = min(V, w * Sw), hi = min(V, lo + Sw);
+    double s = 0.0;
+    for (int x = lo + lane; x < hi; x += 32) s += f(x);
+    s = warp_sum(s);
+    __syncthreads();
+    if (lane == 0) red[w] = s;
+    __syncthreads();
+    double prefix = 0.0;
+    for (int k = 0; k < w; ++k) prefix += red[k];
+    long long cand = LLONG_MAX;
+    if (hi > lo && u >= prefix - 1e-9 && u < prefix + s + 1e-9) {
+        double cum = prefix;
+        for (int base = lo; base < hi; base += 32) {
+            const int x = base + lane;
+            const double vx = x < hi ? f(x) : 0.0;
+            double sc = vx;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, sc, o);
+                if (lane >= o) sc += y;
+            }
+            const bool hit = x < hi && u < cum + sc;
+            const unsigned b = __ballot_sync(0xffffffffu, hit);
+            if (b) {
+                cand = base + (__ffs(b) - 1);
+                break;
+            }
+            cum += __shfl_sync(0xffffffffu, sc, 31);
+        }
+    }
+    cand = block_min_ll(cand, redl);
+    if (cand != LLONG_MAX) return static_cast<int>(cand);
+    long long last = -1;
+    for (int x = threadIdx.x; x < V; x += blockDim.x)
+        if (f(x) > 0.0) last = x;
+    last = block_max_ll(last, redl);
+    if (last < 0) {
+        if (threadIdx.x == 0) atomicCAS(err, 0, kErrAllZero);
+        return 0;
+    }
+    return static_cast<int>(last);
+}
+
+// argmax of p with lowest-index tie break, skipping `excl` (greedy verification / top-k).
+template <class T>
+__device__ int row_argmax(const RowRef<T> &r, const Stats &st, double *red, long long *redl, const int *excl,
+                          int n_excl) {
+    double best = -1.0;
+    int bi = INT_MAX;
+    for (int x = threadIdx.x; x < r.V; x += blockDim.x) {
+        bool skip = false;
+        for (int e = 0; e < n_excl; ++e) skip |= excl[e] == x;
+        if (skip) continue;
+        const double p = prob(r, st, x);
+        if (p > best) {
+            best = p;
+            bi = x;
+        }
+    }
+    const double m = block_max(best, red);
+    long long key = (best == m) ? bi : LLONG_MAX;
+    key = block_min_ll(key, redl);
+    return static_cast<int>(key);
+}
+
+struct Seq {
+    int r;        // request id
+    int a;        // active slot
+    int len;      // current token count (prompt + generated)
+    int plen;
+    int maxlen;
+    double bias;
+};
+
+__device__ __forceinline__ double u_of(const MtStream &ms, int k) { return to_unit_double(ms.out[ms.pos + k]); }
+
+// Append one emitted token with its StepRecord (specdec.cpp:62-74, :276-283).
+template <class T>
+__device__ void emit(const SdDev &d, Seq &q, int tok, const RowRef<T> &row, const Stats &st, bool drafted,
+                     double logq, bool &ended) {
+    const int gen = q.len - q.plen;
+    if (threadIdx.x == 0) {
+        if (q.len < d.tok_cap && gen < d.steps_cap) {
+            d.tok[(size_t)q.r * d.tok_cap + q.len] = tok;
+            const size_t si = (size_t)q.r * d.steps_cap + gen;
+            d.st_tok[si] = tok;
+            d.st_logp[si] = log(prob(row, st, tok));
+            d.st_drafted[si] = drafted ? 1 : 0;
+            d.st_logq[si] = drafted ? logq : 0.0;
+        } else {
+            atomicCAS(d.err, 0, kErrCapacity);
+        }
+    }
+    if (d.st_full && gen < d.steps_cap) {
+        double *dst = d.st_full + ((size_t)q.r * d.steps_cap + gen) * d.V;
+        for (int x = threadIdx.x; x < d.V; x += blockDim.x) dst[x] = log(prob(row, st, x));
+    }
+    q.len += 1;
+    if (tok == d.eos) ended = true;
+}
+
+template <class T>
+__device__ __forceinline__ RowRef<T> prow(const SdDev &d, const Seq &q, int slot) {
+    return RowRef<T>{static_cast<const T *>(d.P) + ((size_t)q.a * d.slots + slot) * d.V, d.V, q.bias, d.tau_p};
+}
+template <class T>
+__device__ __forceinline__ RowRef<T> qrow(const SdDev &d, const Seq &q, int slot) {
+    return RowRef<T>{static_cast<const T *>(d.Q) + ((size_t)q.a * d.slots + slot) * d.V, d.V, q.bias, d.tau_q};
+}
+
+__global__ void cycle_begin_kernel(SdDev d) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= d.nact) return;
+    const int r = d.active[a];
+    d.d_used[r] = 0;
+    d.a_used[r] = 0;
+    d.cont[r] = 1;
+    d.ended[r] = 0;
+    d.accept_len[r] = 0;
+    d.drafted[r] = 0;
+    d.emitted[r] = 0;
+    d.n_rounds[r] = 0;
+}
+
+// specdec.cpp:165-171: remaining = max_emit - |accepted|; < 2 -> no drafting this round.
+__global__ void round_setup_kernel(SdDev d, int round) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= d.nact) return;
+    const int r = d.active[a];
+    int ne = -1;
+    if (d.cont[r]) {
+        const int gen = d.len[r] - d.prompt_len[r];
+        const int rem = d.max_len[r] - gen;
+        ne = rem < 2 ? (round == 0 ? 0 : -1) : min(d.n, rem - 1);
+    }
+    d.n_eff[r] = ne;
+    for (int i = 0; i < d.t; ++i) {
+        const size_t ci = (size_t)r * d.t_max + i;
+        d.chain_len[ci] = 0;
+        d.chain_stop[ci] = 0;
+        d.chain_off[ci] = d.d_used[r] + i * max(ne, 0);  // provisional: no EOS truncation
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(1024, 1) draft_sample_kernel(SdDev d, int depth) {
+    __shared__ double red[32];
+    __shared__ long long redl[32];
+    __shared__ int picked[kMaxBranch];
+    const int a = blockIdx.x;
+    const int r = d.active[a];
+    const int ne = d.n_eff[r];
+    if (depth >= ne) return;  // also covers ne <= 0
+    Seq q{r, a, d.len[r], d.prompt_len[r], d.max_len[r], d.eos_bias[r]};
+    const MtStream &D = d.rng[2 * r];
+    const bool greedy = d.verify_mode == 1;
+    if (depth == 0) {
+        const RowRef<T> row = qrow<T>(d, q, 0);
+        const Stats st = row_stats(row, red);
+        for (int i = 0; i < d.t; ++i) {
+            int c;
+            if (greedy) {
+                c = row_argmax(row, st, red, redl, picked, i);
+            } else {
+                const double u = u_of(D, d.chain_off[(size_t)r * d.t_max + i]);
+                c = inv_cdf(ProbFn<T>{row, st}, d.V, u, red, redl, d.err);
+            }
+            if (threadIdx.x == 0) {
+                picked[i] = c;
+                const size_t ci = (size_t)r * d.t_max + i;
+                d.chain_tok[ci * d.n_max + 0] = c;
+                d.chain_len[ci] = 1;
+                d.chain_stop[ci] = c == d.eos;
+            }
+            __syncthreads();
+        }
+        return;
+    }
+    const int i = blockIdx.y;
+    const size_t ci = (size_t)r * d.t_max + i;
+    if (d.chain_stop[ci] || d.chain_len[ci] != depth) return;
+    const RowRef<T> row = qrow<T>(d, q, 1 + i * d.n + depth);
+    const Stats st = row_stats(row, red);
+    int c;
+    if (greedy) c = row_argmax(row, st, red, redl, picked, 0);
+    else c = inv_cdf(ProbFn<T>{row, st}, d.V, u_of(D, d.chain_off[ci] + depth), red, redl, d.err);
+    if (threadIdx.x == 0) {
+        d.chain_tok[ci * d.n_max + depth] = c;
+        d.chain_len[ci] = depth + 1;
+        d.chain_stop[ci] = c == d.eos;
+    }
+}
+
+// Offsets must equal the reference's sequential consumption: chain i starts after the
+// draws of chains 0..i-1 (specdec.cpp:177-192). Any mismatch -> fix + request a redraft.
+__global__ void redraft_check_kernel(SdDev d) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= d.nact) return;
+    const int r = d.active[a];
+    if (d.n_eff[r] <= 0 || d.verify_mode == 1) return;
+    int off = d.d_used[r];
+    bool bad = false;
+    for (int i = 0; i < d.t; ++i) {
+        const size_t ci = (size_t)r * d.t_max + i;
+        if (d.chain_off[ci] != off) bad = true;
+        off += d.chain_len[ci];
+    }
+    if (!bad) return;
+    off = d.d_used[r];
+    for (int i = 0; i < d.t; ++i) {
+        const size_t ci = (size_t)r * d.t_max + i;
+        const int li = d.chain_len[ci];
+        d.chain_off[ci] = off;
+        off += li;
+        d.chain_len[ci] = 0;
+        d.chain_stop[ci] = 0;
+    }
+    atomicExch(d.flag, 1);
+}
+
+template <class T>
+__global__ void __launch_bounds__(1024, 1) accept_kernel(SdDev d, int round, int naive) {
+    __shared__ double red[32];
+    __shared__ long long redl[32];
+    __shared__ double Z[kMaxBranch];
+    const int a = blockIdx.x;
+    const int r = d.active[a];
+    Seq q{r, a, d.len[r], d.prompt_len[r], d.max_len[r], d.eos_bias[r]};
+    const bool greedy = d.verify_mode == 1;
+    const MtStream &A = d.rng[2 * r + 1];
+    const MtStream &D = d.rng[2 * r];
+    bool ended = false;
+    int emitted = 0;
+
+    if (naive) {
+        // Non-spec step (server.cpp:328-347): one target sample on the DRAFT stream.
+        const RowRef<T> p = prow<T>(d, q, 0);
+        const Stats sp = row_stats(p, red);
+        int x;
+        if (greedy) x = row_argmax(p, sp, red, redl, nullptr, 0);
+        else x = inv_cdf(ProbFn<T>{p, sp}, d.V, u_of(D, d.d_used[r]), red, redl, d.err);
+        emit(d, q, x, p, sp, false, 0.0, ended);
+        if (threadIdx.x == 0) {
+            if (!greedy) d.d_used[r] += 1;
+            d.len[r] = q.len;
+            d.emitted[r] += 1;
+            d.ended[r] = ended;
+            d.cont[r] = 0;
+        }
+        return;
+    }
+
+    const int ne = d.n_eff[r];
+    if (ne < 0) return;
+    int acur = d.a_used[r];
+    int alen = d.accept_len[r];
+    int cont = 0;
+    const int t = d.t, n = d.n;
+    const int *ctok = d.chain_tok + (size_t)r * d.t_max * d.n_max;
+    const int *clen = d.chain_len + (size_t)r * d.t_max;
+
+    if (ne == 0) {
+        // max_emit == 1: no round runs, the single token is the bonus from the target on the
+        // ACCEPT stream (specdec.cpp:256-266; SURVEY App. A "Engine != generate()").
+        const RowRef<T> p = prow<T>(d, q, 0);
+        const Stats sp = row_stats(p, red);
+        const int x = greedy ? row_argmax(p, sp, red, redl, nullptr, 0)
+                             : inv_cdf(ProbFn<T>{p, sp}, d.V, u_of(A, acur++), red, redl, d.err);
+        emit(d, q, x, p, sp, false, 0.0, ended);
+        ++emitted;
+        if (threadIdx.x == 0) {
+            int *rc = d.round_cost + ((size_t)r * kMaxRounds + 0) * 3;
+            rc[0] = 0; rc[1] = 0; rc[2] = 1;
+            d.n_rounds[r] = 1;
+        }
+        goto done;
+    }
+
+    {
+        // RoundCost{longest, t, tree_tokens + 1} (specdec.cpp:195)
+        int longest = 0, tree = 0;
+        for (int i = 0; i < t; ++i) {
+            longest = max(longest, clen[i]);
+            tree += clen[i];
+        }
+        if (threadIdx.x == 0) {
+            int *rc = d.round_cost + ((size_t)r * kMaxRounds + round) * 3;
+            rc[0] = longest; rc[1] = t; rc[2] = tree + 1;
+            d.n_rounds[r] = round + 1;
+            d.drafted[r] = 1;
+            d.d_used[r] += tree;
+        }
+
+        const RowRef<T> p1 = prow<T>(d, q, 0);
+        const RowRef<T> q1 = qrow<T>(d, q, 0);
+        const Stats s1 = row_stats(p1, red);
+        const Stats t1 = row_stats(q1, red);
+        int sel = -1;
+        if (greedy) {
+            const int a1 = row_argmax(p1, s1, red, redl, nullptr, 0);
+            for (int i = 0; i < t && sel < 0; ++i)
+                if (ctok[(size_t)i * d.n_max] == a1) sel = i;
+            if (sel < 0) {
+                emit(d, q, a1, p1, s1, false, 0.0, ended);
+                ++emitted;
+                goto done;
+            }
+        } else {
+            // Branch point: recursive rejection over the t siblings (specdec.cpp:197-217).
+            int k = 0;
+            for (int i = 0; i < t; ++i) {
+                const int cand = ctok[(size_t)i * d.n_max];
+                PCurFn<T> pc{p1, s1, q1, t1, Z, k};
+                const double pv = pc(cand), qv = prob(q1, t1, cand);
+                const double acc = fmin(1.0, pv / qv);
+                if (u_of(A, acur++) < acc) {
+                    sel = i;
+                    break;
+                }
+                const double z = block_total(
+                    [&](int x) { return fmax(0.0, pc(x) - prob(q1, t1, x)); }, d.V, red);
+                if (z <= 1e-12 && threadIdx.x == 0) atomicCAS(d.err, 0, kErrResidual);
+                if (threadIdx.x == 0) Z[k] = z;
+                __syncthreads();
+                ++k;
+            }
+            if (sel < 0) {
+                const int x = inv_cdf(PCurFn<T>{p1, s1, q1, t1, Z, k}, d.V, u_of(A, acur++), red, redl, d.err);
+                emit(d, q, x, p1, s1, false, 0.0, ended);  // StepRecord keeps p1 (specdec.cpp:214)
+                ++emitted;
+                goto done;
+            }
+        }
+        const int *chain = ctok + (size_t)sel * d.n_max;
+        const int L = clen[sel];
+        emit(d, q, chain[0], p1, s1, true, log(prob(q1, t1, chain[0])), ended);
+        ++emitted;
+        ++alen;
+        if (ended) goto done;
+        // Chain-style verification of the selected chain (specdec.cpp:226-245).
+        for (int pos = 1; pos < L; ++pos) {
+            const RowRef<T> pd = prow<T>(d, q, 1 + sel * n + pos - 1);
+            const RowRef<T> qd = qrow<T>(d, q, 1 + sel * n + pos);
+            const Stats sp = row_stats(pd, red);
+            const Stats sq = row_stats(qd, red);
+            const int dt = chain[pos];
+            bool ok;
+            int repl = -1;
+            const double qv = prob(qd, sq, dt);
+            if (greedy) {
+                repl = row_argmax(pd, sp, red, redl, nullptr, 0);
+                ok = dt == repl;
+            } else {
+                const double pv = prob(pd, sp, dt);
+                if (!(qv > 0.0) && threadIdx.x == 0) atomicCAS(d.err, 0, kErrAcceptQ);
+                if ((pv < 0.0 || pv > 1.0 || qv > 1.0) && threadIdx.x == 0) atomicCAS(d.err, 0, kErrAcceptRange);
+                ok = u_of(A, acur++) < fmin(1.0, pv / qv);
+            }
+            if (ok) {
+                emit(d, q, dt, pd, sp, true, log(qv), ended);
+                ++emitted;
+                ++alen;
+                if (ended) goto done;
+            } else {
+                int x = repl;
+                if (!greedy) {
+                    const double z = block_total([&](int y) { return fmax(0.0, prob(pd, sp, y) - prob(qd, sq, y)); },
+                                                 d.V, red);
+                    if (z <= 1e-12 && threadIdx.x == 0) atomicCAS(d.err, 0, kErrResidual);
+                    x = inv_cdf(ResidFn<T>{pd, sp, qd, sq, z}, d.V, u_of(A, acur++), red, redl, d.err);
+                }
+                emit(d, q, x, pd, sp, false, 0.0, ended);
+                ++emitted;
+                goto done;
+            }
+        }
+        // Full acceptance: next round, or the bonus from the target (specdec.cpp:165-169, :256-267).
+        const int rem_after = q.maxlen - (q.len - q.plen);
+        if (round + 1 < d.s && rem_after >= 2) {
+            cont = 1;
+        } else {
+            const RowRef<T> pb = prow<T>(d, q, 1 + sel * n + L - 1);
+            const Stats sb = row_stats(pb, red);
+            const int x = greedy ? row_argmax(pb, sb, red, redl, nullptr, 0)
+                                 : inv_cdf(ProbFn<T>{pb, sb}, d.V, u_of(A, acur++), red, redl, d.err);
+            emit(d, q, x, pb, sb, false, 0.0, ended);
+            ++emitted;
+        }
+    }
+done:
+    if (threadIdx.x == 0) {
+        d.len[r] = q.len;
+        d.a_used[r] = acur;
+        d.accept_len[r] = alen;
+        d.emitted[r] += emitted;
+        d.ended[r] = ended;
+        d.cont[r] = cont && !ended;
+    }
+}
+
+__global__ void cycle_end_kernel(SdDev d, int naive) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= d.nact) return;
+    const int r = d.active[a];
+    const int gen = d.len[r] - d.prompt_len[r];
+    const int done = d.ended[r] || gen >= d.max_len[r];
+    d.done[r] = done;
+    d.rng[2 * r].pos += d.d_used[r];
+    d.rng[2 * r + 1].pos += d.a_used[r];
+    int *s = d.summary + (size_t)a * (kSummaryFixed + 3 * kMaxRounds);
+    s[0] = done;
+    s[1] = d.emitted[r];
+    s[2] = naive ? 0 : d.accept_len[r];
+    s[3] = naive ? 0 : d.drafted[r];
+    s[4] = naive ? 0 : d.n_rounds[r];
+    s[5] = d.len[r];
+    if (!naive)
+        for (int k = 0; k < 3 * d.n_rounds[r]; ++k) s[kSummaryFixed + k] = d.round_cost[(size_t)r * kMaxRounds * 3 + k];
+}
+
+// ---- tabular model rows ------------------------------------------------------------------
+// row index from the last `order` tokens of tok[r][0..len) ++ ext[0..e) (model.cpp:113-130)
+__device__ long long tab_row_index(const SdDev &d, const TabDev &m, int r, int len, const int *ext, int e) {
+    long long idx = 0;
+    for (int i = 0; i < m.order; ++i) {
+        const int p = len + e - (m.order - i);
+        int tok = 0;
+        if (p >= 0) tok = p < len ? d.tok[(size_t)r * d.tok_cap + p] : ext[p - len];
+        if (tok < 0 || tok >= m.V) return -1;
+        idx = idx * m.V + tok;
+    }
+    return idx;
+}
+
+__global__ void tab_rows_kernel(SdDev d, TabDev m, int depth, int verify, int naive) {
+    // blockIdx.x = active slot, blockIdx.y = tree slot
+    const int a = blockIdx.x, slot = blockIdx.y;
+    const int r = d.active[a];
+    const int ne = naive ? 0 : d.n_eff[r];
+    if (!naive && ne < 0) return;
+    const int len = d.len[r];
+    const int *ext = nullptr;
+    int e = 0;
+    double *dst;
+    if (verify) {
+        if (slot > 0) {
+            const int i = (slot - 1) / d.n, j = (slot - 1) % d.n;
+            if (i >= d.t || j >= d.chain_len[(size_t)r * d.t_max + i]) return;
+            ext = d.chain_tok + ((size_t)r * d.t_max + i) * d.n_max;
+            e = j + 1;
+        }
+        dst = const_cast<double *>(static_cast<const double *>(d.P)) + ((size_t)a * d.slots + slot) * d.V;
+    } else {
+        if (depth >= ne) return;
+        if (depth == 0) {
+            if (slot != 0) return;
+        } else {
+            const int i = slot;
+            if (i >= d.t) return;
+            const size_t ci = (size_t)r * d.t_max + i;
+            if (d.chain_stop[ci] || d.chain_len[ci] != depth) return;
+            ext = d.chain_tok + ci * d.n_max;
+            e = depth;
+        }
+        const int qslot = depth == 0 ? 0 : 1 + slot * d.n + depth;
+        dst = const_cast<double *>(static_cast<const double *>(d.Q)) + ((size_t)a * d.slots + qslot) * d.V;
+    }
+    const long long row = tab_row_index(d, m, r, len, ext, e);
+    if (row < 0) {
+        if (threadIdx.x == 0) atomicCAS(d.err, 0, kErrRowIndex);
+        return;
+    }
+    const double *src = m.table + row * m.V;
+    for (int x = threadIdx.x; x < m.V; x += blockDim.x) dst[x] = src[x];
+}
+
+inline int sd_threads(int V) { return V <= 256 ? 32 : V <= 4096 ? 256 : 1024; }
+
+}  // namespace
+
+void sd_cycle_begin(const SdDev &d, cudaStream_t st) {
+    if (d.nact <= 0) return;
+    cycle_begin_kernel<<<(d.nact + 127) / 128, 128, 0, st>>>(d);
+    RS_LAUNCHED();
+}
+
+void sd_round_setup(const SdDev &d, int round, cudaStream_t st) {
+    if (d.nact <= 0) return;
+    round_setup_kernel<<<(d.nact + 127) / 128, 128, 0, st>>>(d, round);
+    RS_LAUNCHED();
+}
+
+void sd_draft_sample(const SdDev &d, int depth, RowType rt, cudaStream_t st) {
+    if (d.nact <= 0) return;
+    dim3 grid(d.nact, depth == 0 ? 1 : d.t);
+    const int th = sd_threads(d.V);
+    if (rt == RowType::F64) draft_sample_kernel<double><<<grid, th, 0, st>>>(d, depth);
+    else draft_sample_kernel<float><<<grid, th, 0, st>>>(d, depth);
+    RS_LAUNCHED();
+}
+
+void sd_redraft_check(const SdDev &d, cudaStream_t st) {
+    if (d.nact <= 0) return;
+    redraft_check_kernel<<<(d.nact + 127) / 128, 128, 0, st>>>(d);
+    RS_LAUNCHED();
+}
+
+void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t st) {
+    if (d.nact <= 0) return;
+    const int th = sd_threads(d.V);
+    if (rt == RowType::F64) accept_kernel<double><<<d.nact, th, 0, st>>>(d, round, naive ? 1 : 0);
+    else accept_kernel<float><<<d.nact, th, 0, st>>>(d, round, naive ? 1 : 0);
+    RS_LAUNCHED();
+}
+
+void sd_cycle_end(const SdDev &d, bool naive, cudaStream_t st) {
+    if (d.nact <= 0) return;
+    cycle_end_kernel<<<(d.nact + 127) / 128, 128, 0, st>>>(d, naive ? 1 : 0);
+    RS_LAUNCHED();
+}
+
+void tab_draft_rows(const SdDev &d, const TabDev &m, int depth, cudaStream_t st) {
+    if (d.nact <= 0) return;
+    dim3 grid(d.nact, depth == 0 ? 1 : d.t);
+    tab_rows_kernel<<<grid, 32, 0, st>>>(d, m, depth, 0, 0);
+    RS_LAUNCHED();
+}
+
+void tab_verify_rows(const SdDev &d, const TabDev &m, bool naive, cudaStream_t st) {
+    if (d.nact <= 0) return;
+    dim3 grid(d.nact, naive ? 1 : d.slots);
+    tab_rows_kernel<<<grid, 32, 0, st>>>(d, m, 0, 1, naive ? 1 : 0);
+    RS_LAUNCHED();
+}
+
+}  // namespace rs

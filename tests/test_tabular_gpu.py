@@ -1,0 +1,135 @@
+"""GPU parity: the CUDA engine (fp64 parity mode, tabular models) against the compiled
+reference's own outputs (golden fixtures) and the CPU restatement (oracle/), bit-exact on
+tokens / accept lengths / cycles / ledger, logprobs within 1e-12 (the reference's own
+tolerance, test_specdec.cpp:99-116)."""
+import random
+
+import pytest
+
+import paper_2510_26475_b200 as rb
+from conftest import load_golden
+from helpers import model_of, requests_of, run_engine
+from oracle_client import fnv1a_responses
+
+pytestmark = pytest.mark.gpu
+
+
+def _assert_same(out, exp, logprob_tol=1e-12, full=True):
+    assert out["responses"] == exp["responses"]
+    assert out["accept_lens"] == exp["accept_lens"]
+    assert out["cycles"] == exp["cycles"]
+    assert out["active_trace"] == exp["active_trace"]
+    assert out["ledger"] == exp["ledger"]
+    assert out["total_time"] == pytest.approx(exp["total_time"], rel=1e-12)
+    for s, es in zip(out["steps"], exp["steps"]):
+        for (lp, dr, lq), (elp, edr, elq) in zip(s, es):
+            assert dr == edr
+            assert lp == pytest.approx(elp, abs=logprob_tol)
+            assert lq == pytest.approx(elq, abs=logprob_tol)
+    if full and "target_logprobs" in exp:
+        for s, es in zip(out["target_logprobs"], exp["target_logprobs"]):
+            for row, erow in zip(s, es):
+                for a, b in zip(row, erow):
+                    assert (a == b) or abs(a - b) < 1e-12
+
+
+def test_appendix_b_fingerprints_on_gpu():
+    g = load_golden("appendix_b.json")
+    for c in g["cases"]:
+        case = {"target": g["actor"], "drafter": g["drafter"], "requests": g["requests"], "forced": c["forced"]}
+        out, run = run_engine(case, record="target_logprobs" in c["out"])
+        _assert_same(out, c["out"])
+        assert fnv1a_responses(out["responses"]) == c["out"]["fnv"]
+
+
+def test_adaptive_engine_matches_reference():
+    g = load_golden("appendix_b.json")
+    case = {"target": g["actor"], "drafter": g["drafter"], "requests": g["requests"], "table": g["table"]}
+    out, run = run_engine(case, record=False)
+    _assert_same(out, g["adaptive"], full=False)
+    assert out["switches"] == g["adaptive"]["switches"]
+    assert out["prefill_events"] == g["adaptive"]["prefill_events"]
+
+
+@pytest.mark.parametrize("idx", range(24))
+def test_random_tabular_engines_match_reference(idx):
+    item = load_golden("tabular_engine.json")[idx]
+    out, _ = run_engine(item["case"], record="target_logprobs" in item["out"])
+    _assert_same(out, item["out"])
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_engine_vs_restatement_live(oracle, seed):
+    """Fresh random cases each seed, larger vocab (warp-segmented scans span many warps)."""
+    rng = random.Random(1000 + seed)
+    V = [64, 300, 1000, 5000][seed]
+    tgt = {"vocab": V, "order": 1, "temperature": 1.0, "logits": [rng.gauss(0, 2.0) for _ in range(V * V)]}
+    drf = {"vocab": V, "order": 0, "temperature": 1.0, "logits": [rng.gauss(0, 2.0) for _ in range(V)]}
+    reqs = [{"id": i, "prompt": [rng.randrange(V - 1)], "eos_bias": -2.0, "max_len": rng.choice([5, 17]),
+             "seed": 77, "stream": i} for i in range(6)]
+    for forced in [{"s": 1, "t": 4, "n": 3, "enabled": True}, {"s": 2, "t": 2, "n": 2, "enabled": True},
+                   {"enabled": False}]:
+        case = {"target": tgt, "drafter": drf, "requests": reqs, "forced": forced}
+        exp = oracle("run_generation", record_logprobs=False, **case)
+        out, _ = run_engine(case, record=False)
+        assert out["responses"] == [s["response"] for s in exp["samples"]]
+        assert out["accept_lens"] == exp["accept_lens"]
+        assert out["ledger"] == exp["ledger"]
+
+
+def test_greedy_engine_equals_greedy_decode(oracle):
+    rng = random.Random(9)
+    V = 50
+    tgt = {"vocab": V, "order": 2, "logits": [rng.gauss(0, 2) for _ in range(V ** 3)]}
+    drf = {"vocab": V, "order": 1, "logits": [rng.gauss(0, 2) for _ in range(V ** 2)]}
+    reqs = [{"id": i, "prompt": [i, i + 1], "eos_bias": -2.0, "max_len": 20, "seed": 3, "stream": i}
+            for i in range(5)]
+    base, _ = run_engine({"target": tgt, "drafter": drf, "requests": reqs, "forced": {"enabled": False}},
+                         verify_mode="greedy", record=False)
+    for c in [{"s": 1, "t": 1, "n": 3}, {"s": 2, "t": 3, "n": 2}, {"s": 1, "t": 4, "n": 5}]:
+        c["enabled"] = True
+        case = {"target": tgt, "drafter": drf, "requests": reqs, "forced": c}
+        out, _ = run_engine(case, verify_mode="greedy", record=False)
+        exp = oracle("run_generation", verify_mode="greedy", record_logprobs=False, **case)
+        assert out["responses"] == base["responses"] == [s["response"] for s in exp["samples"]]
+        assert out["accept_lens"] == exp["accept_lens"]
+
+
+def test_engine_errors_match_reference():
+    g = load_golden("appendix_b.json")
+    target = model_of(g["actor"])
+    reqs = requests_of(g["requests"][:2])
+    eng = rb.BatchEngine(target, None, None, rb.TimingModel(), reqs, rb.SDConfig.chain(2))
+    with pytest.raises(rb.EngineError, match="spec mode requires a drafter snapshot"):
+        eng.step()
+    eng2 = rb.BatchEngine(target, None, None, rb.TimingModel(), [], rb.SDConfig.off())
+    with pytest.raises(rb.EngineError, match="BatchEngine: empty batch"):
+        eng2.step()
+    drafter = model_of(g["actor"])  # drafter == target: residual is degenerate, never reached
+    eng3 = rb.BatchEngine(target, lambda: drafter, None, rb.TimingModel(), requests_of(g["requests"][:4]),
+                          rb.SDConfig.chain(3))
+    while not eng3.all_done():
+        eng3.step()
+    for r in eng3.requests():  # drafter == target accepts every drafted token (test_specdec.cpp:76-85)
+        assert all(a == min(3, a) for a in r.accept_lens)
+
+
+def test_kd_update_matches_reference():
+    g = load_golden("kd_update.json")
+    drafter = model_of(g["drafter"])
+    buf = [rb.RolloutSample(s["prompt"], s["response"],
+                            [rb.StepRecord(st["token"], st["logp"], st["drafted"], st["logq"], st["target_logprobs"])
+                             for st in s["steps"]], s["eos_bias"], s["reward"]) for s in g["buffer"]]
+    mode = {"reward": rb.WeightMode.Reward, "uniform": rb.WeightMode.Uniform}
+    for c in g["cases"]:
+        p = c["policy"]
+        pol = rb.KDPolicy(p["interval"], mode[p["mode"]], p["clip_lo"], p["clip_hi"], p["lr"])
+        res = rb.kd_update(drafter, buf, pol, rb.SelectionRng(c["selection_seed"]), 0.02)
+        e = c["out"]
+        assert res.updated and res.samples_used == e["samples_used"]
+        assert res.drafter.version == g["drafter"]["version"] + 1
+        assert res.loss == pytest.approx(e["loss"], rel=1e-10)
+        assert res.weight_mean == e["weight_mean"] and res.weight_min == e["weight_min"]
+        assert res.sim_time == pytest.approx(e["sim_time"], rel=1e-12)
+        new = res.drafter.logits()
+        assert max(abs(a - b) for a, b in zip(new, e["logits"])) < 1e-12
