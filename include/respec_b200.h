@@ -222,6 +222,13 @@ double rs_kd_weight(double r, const double *batch_rewards, int32_t n, rs_kd_poli
 int rs_kd_update_tabular(rs_ctx *ctx, const rs_model *drafter, const rs_kd_sample *buf, int32_t n,
                          rs_kd_policy policy, uint64_t *selection_rng_state, double sim_cost_per_token,
                          rs_model **new_drafter, rs_kd_result *out);
+/* ---- kernels exposed for tests / microbenchmarks (device pointers) ------------------------ */
+/* C = A . B^T on tcgen05 tensor cores; A [M,K] bf16, B [N,K] bf16 (K-major), epilogue:
+   0 = bf16 out (+ bias[N] bf16), 1 = fp32 out * scale, 2 = fp32 out += acc, 3 = SwiGLU bf16 out [M, N/2].
+   block_n: 0 (auto) | 128 | 256. Runs on the context stream. */
+int rs_gemm_bf16(rs_ctx *ctx, const void *A_dev, const void *B_dev, void *C_dev, const void *bias_dev, int32_t M,
+                 int32_t N, int32_t K, int32_t epilogue, float scale, int32_t block_n);
+
 /* mt19937_64 state helper for rs_kd_update_tabular: 313 uint64 (312 words + index). */
 int rs_mt19937_64_seed(uint64_t seed, uint64_t *state313);
 

@@ -118,7 +118,7 @@ EXPORTED_SYMBOLS = [
     "rs_engine_switches", "rs_engine_active_trace", "rs_engine_drafter_versions", "rs_engine_response",
     "rs_engine_steps", "rs_engine_step_logprobs", "rs_engine_accept_lens", "rs_engine_destroy",
     "rs_engine_set_capture", "rs_engine_capture_count", "rs_engine_capture_read",
-    "rs_kd_weight", "rs_kd_update_tabular", "rs_mt19937_64_seed",
+    "rs_kd_weight", "rs_kd_update_tabular", "rs_mt19937_64_seed", "rs_gemm_bf16",
 ]
 
 _lib = None
@@ -183,6 +183,7 @@ def lib():
             "rs_kd_update_tabular": ([vp, vp, P(_KDSample), i32, _KDPolicy, P(u64), dbl, P(vp), P(_KDResult)],
                                      ctypes.c_int),
             "rs_mt19937_64_seed": ([u64, P(u64)], ctypes.c_int),
+            "rs_gemm_bf16": ([vp, vp, vp, vp, vp, i32, i32, i32, i32, ctypes.c_float, i32], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

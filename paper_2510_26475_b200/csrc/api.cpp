@@ -8,6 +8,7 @@
 
 #include "common.cuh"
 #include "engine.h"
+#include "gemm.h"
 #include "kd.h"
 
 namespace {
@@ -495,6 +496,28 @@ int rs_kd_update_tabular(rs_ctx *ctx, const rs_model *drafter, const rs_kd_sampl
         need(new_drafter, "rs_kd_update_tabular: out");
         if (drafter->kind != rs_model::Tabular) throw std::invalid_argument("rs_kd_update_tabular: tabular drafter required");
         kd_update_tabular(ctx, static_cast<const TabularModel *>(drafter), buf, n, policy, sel_state, cost, new_drafter, out);
+    });
+}
+
+int rs_gemm_bf16(rs_ctx *ctx, const void *A, const void *B, void *Cp, const void *bias, int32_t M, int32_t N, int32_t K,
+                 int32_t epilogue, float scale, int32_t block_n) {
+    return guard([&] {
+        need(ctx, "rs_gemm_bf16");
+        GemmArgs g;
+        g.A = A;
+        g.B = B;
+        g.M = M;
+        g.N = N;
+        g.K = K;
+        g.lda = K;
+        g.ldb = K;
+        g.block_n = block_n;
+        g.epi.kind = epilogue;
+        g.epi.out = Cp;
+        g.epi.ldo = epilogue == kEpiSwiGLU ? N / 2 : N;
+        g.epi.bias = bias;
+        g.epi.scale = scale;
+        gemm_bf16(g, ctx->stream);
     });
 }
 

@@ -1,0 +1,29 @@
+// gemm.h -- tcgen05 bf16 GEMM launcher (gemm_sm100.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace rs {
+
+enum GemmEpiKind { kEpiBF16 = 0, kEpiF32 = 1, kEpiResidual = 2, kEpiSwiGLU = 3 };
+
+struct GemmEpi {
+    int kind = kEpiBF16;
+    void *out = nullptr;         // bf16 [M, ldo] (BF16/SwiGLU) or fp32 [M, ldo] (F32/Residual)
+    int ldo = 0;
+    const void *bias = nullptr;  // bf16 [N] (kEpiBF16 only)
+    float scale = 1.0f;          // kEpiF32 only
+};
+
+struct GemmArgs {
+    const void *A = nullptr;  // bf16 [M, lda], K-major
+    const void *B = nullptr;  // bf16 [N, ldb], K-major (weights)
+    int M = 0, N = 0, K = 0, lda = 0, ldb = 0;
+    int block_n = 0;          // 0 = auto (256)
+    GemmEpi epi;
+};
+
+// SwiGLU layout: B rows are interleaved per 256-row block as [128 gate rows, 128 up rows];
+// output column j = silu(gate_j) * up_j, N_out = N / 2.
+void gemm_bf16(const GemmArgs &g, cudaStream_t st);
+
+}  // namespace rs

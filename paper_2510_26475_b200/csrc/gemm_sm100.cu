@@ -1,0 +1,396 @@
+// gemm_sm100.cu -- persistent warp-specialised bf16 GEMM on 5th-gen tensor cores.
+//
+//   C[M, N] = A[M, K] . B[N, K]^T      (A activations, B weights; both K-major bf16)
+//
+// One CTA per SM loops over 128 x BN output tiles (M fastest, so co-resident CTAs share the
+// weight tile in L2). Warp 0 streams A/B k-blocks (64 wide, 128B-swizzled) into a STAGES-deep
+// shared-memory ring with TMA; one elected lane of warp 1 issues tcgen05.mma (kind::f16,
+// 128 x BN x 16, fp32 accumulation in TMEM) and commits to the ring's empty barriers; two
+// TMEM accumulators (2 x BN columns) let warps 4-7 drain tile i (tcgen05.ld 32x32b) while
+// tile i+1 accumulates. Epilogues are fused: bias + bf16 store, scaled fp32 store (LM head
+// logits), fp32 residual add, and SiLU(gate) * up for the interleaved gate/up projection.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "common.cuh"
+#include "gemm.h"
+
+namespace rs {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+
+// Shared-memory matrix descriptor: K-major, 128B swizzle, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_desc(const void *tile) {
+    const uint32_t a = smem_u32(tile);
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((a & 0x3FFFF) >> 4);
+    d |= static_cast<uint64_t>(1) << 16;           // LBO (unused for swizzled K-major)
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;   // SBO
+    d |= static_cast<uint64_t>(1) << 46;           // descriptor version (sm_100)
+    d |= static_cast<uint64_t>(2) << 61;           // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+          "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int BN>
+struct Cfg {
+    static constexpr int kStages = BN >= 256 ? 4 : 6;
+    static constexpr int kABytes = BM * BK * 2;
+    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256;
+    static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                                       (static_cast<uint32_t>(BM >> 4) << 24);
+};
+
+__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+
+// Epilogue for one thread = one output row, 32 consecutive accumulator columns.
+template <int EPI, int BN>
+__device__ __forceinline__ void epilogue_chunk(const GemmEpi &ep, uint32_t tbase, int row, int col0, int chunk, int M,
+                                               int N) {
+    uint32_t v[32];
+    if constexpr (EPI == kEpiSwiGLU) {
+        // accumulator columns [0, BN/2) are gate, [BN/2, BN) are up, for BN/2 outputs
+        uint32_t u[32];
+        tmem_ld32(tbase + chunk * 32, v);
+        tmem_ld32(tbase + BN / 2 + chunk * 32, u);
+        if (row >= M) return;
+        const int n0 = col0 / 2 + chunk * 32;  // output column
+        const int Nout = N / 2;
+        __nv_bfloat16 *out = static_cast<__nv_bfloat16 *>(ep.out) + static_cast<size_t>(row) * ep.ldo + n0;
+        if (n0 + 32 <= Nout) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+                __align__(16) __nv_bfloat162 h[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float a = silu(__uint_as_float(v[j + 2 * k])) * __uint_as_float(u[j + 2 * k]);
+                    const float b = silu(__uint_as_float(v[j + 2 * k + 1])) * __uint_as_float(u[j + 2 * k + 1]);
+                    h[k] = __floats2bfloat162_rn(a, b);
+                }
+                *reinterpret_cast<int4 *>(out + j) = *reinterpret_cast<int4 *>(h);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (n0 + j < Nout) out[j] = __float2bfloat16(silu(__uint_as_float(v[j])) * __uint_as_float(u[j]));
+        }
+        return;
+    } else {
+        tmem_ld32(tbase + chunk * 32, v);
+        if (row >= M) return;
+        const int n0 = col0 + chunk * 32;
+        if constexpr (EPI == kEpiBF16) {
+            __nv_bfloat16 *out = static_cast<__nv_bfloat16 *>(ep.out) + static_cast<size_t>(row) * ep.ldo + n0;
+            const __nv_bfloat16 *bias = static_cast<const __nv_bfloat16 *>(ep.bias);
+            if (n0 + 32 <= N) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 8) {
+                    __align__(16) __nv_bfloat162 h[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        float a = __uint_as_float(v[j + 2 * k]), b = __uint_as_float(v[j + 2 * k + 1]);
+                        if (bias) {
+                            a += __bfloat162float(bias[n0 + j + 2 * k]);
+                            b += __bfloat162float(bias[n0 + j + 2 * k + 1]);
+                        }
+                        h[k] = __floats2bfloat162_rn(a, b);
+                    }
+                    *reinterpret_cast<int4 *>(out + j) = *reinterpret_cast<int4 *>(h);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (n0 + j >= N) continue;
+                    float a = __uint_as_float(v[j]);
+                    if (bias) a += __bfloat162float(bias[n0 + j]);
+                    out[j] = __float2bfloat16(a);
+                }
+            }
+        } else if constexpr (EPI == kEpiF32) {
+            float *out = static_cast<float *>(ep.out) + static_cast<size_t>(row) * ep.ldo + n0;
+            if (n0 + 32 <= N) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {
+                    float4 f = make_float4(__uint_as_float(v[j]) * ep.scale, __uint_as_float(v[j + 1]) * ep.scale,
+                                           __uint_as_float(v[j + 2]) * ep.scale, __uint_as_float(v[j + 3]) * ep.scale);
+                    *reinterpret_cast<float4 *>(out + j) = f;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (n0 + j < N) out[j] = __uint_as_float(v[j]) * ep.scale;
+            }
+        } else {  // kEpiResidual: out (fp32) += acc
+            float *out = static_cast<float *>(ep.out) + static_cast<size_t>(row) * ep.ldo + n0;
+            if (n0 + 32 <= N) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {
+                    float4 f = *reinterpret_cast<float4 *>(out + j);
+                    f.x += __uint_as_float(v[j]);
+                    f.y += __uint_as_float(v[j + 1]);
+                    f.z += __uint_as_float(v[j + 2]);
+                    f.w += __uint_as_float(v[j + 3]);
+                    *reinterpret_cast<float4 *>(out + j) = f;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (n0 + j < N) out[j] += __uint_as_float(v[j]);
+            }
+        }
+    }
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmEpi ep, int M,
+                int N, int K) {
+    using C = Cfg<BN>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + C::kStages * C::kABytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::kStages * C::kStageBytes);
+    uint64_t *empty = full + C::kStages;
+    uint64_t *tfull = empty + C::kStages;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+    const int num_tiles = num_m * num_n;
+    const int num_k = (K + BK - 1) / BK;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(C::kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                    tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK, m0);
+                    tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, n0);
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+                const int acc = it & 1;
+                const uint32_t aphase = (it >> 1) & 1;
+                mbar_wait(&tempty[acc], aphase ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + acc * BN;
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint64_t ad = sw128_desc(sA + stage * C::kABytes);
+                    const uint64_t bd = sw128_desc(sB + stage * C::kBBytes);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)  // +32 bytes per 16-wide K step inside the swizzle atom
+                        tc_mma(tmem_d, ad + 2 * k, bd + 2 * k, C::kIdesc, (kb | k) != 0);
+                    tc_commit(&empty[stage]);
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit(&tfull[acc]);
+            }
+        }
+    } else if (warp >= 4) {
+        const int q = warp - 4;  // TMEM lane quadrant == warp % 4
+        int it = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+            const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
+            const int acc = it & 1;
+            mbar_wait(&tfull[acc], (it >> 1) & 1);
+            tc_fence_after();
+            const uint32_t tb = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+            const int row = m0 + q * 32 + lane;
+            constexpr int kChunks = (EPI == kEpiSwiGLU ? BN / 2 : BN) / 32;
+#pragma unroll 1
+            for (int c = 0; c < kChunks; ++c) epilogue_chunk<EPI, BN>(ep, tb, row, n0, c, M, N);
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::kTmemCols));
+    }
+}
+
+// ---- host: tensor maps ------------------------------------------------------------------------
+using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                              const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+CUtensorMap make_map(const void *base, int rows, int cols, int ld, int box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+    const cuuint32_t box[2] = {BK, static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides,
+                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return m;
+}
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        RS_CUDA(cudaGetDevice(&dev));
+        RS_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return n;
+}
+
+template <int BN, int EPI>
+void launch(const GemmArgs &g, cudaStream_t st) {
+    using C = Cfg<BN>;
+    static bool attr = false;
+    if (!attr) {
+        RS_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+        attr = true;
+    }
+    const CUtensorMap ta = make_map(g.A, g.M, g.K, g.lda, BM);
+    const CUtensorMap tb = make_map(g.B, g.N, g.K, g.ldb, BN);
+    const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+    const int grid = std::min(tiles, num_sms());
+    gemm_kernel<BN, EPI><<<grid, kThreads, C::kSmem, st>>>(ta, tb, g.epi, g.M, g.N, g.K);
+    RS_LAUNCHED();
+}
+
+}  // namespace
+
+void gemm_bf16(const GemmArgs &g, cudaStream_t st) {
+    if (g.M <= 0 || g.N <= 0) return;
+    if (g.K % 8 || g.lda % 8 || g.ldb % 8) throw std::invalid_argument("gemm_bf16: K and leading dims must be multiples of 8");
+    if (g.epi.kind == kEpiSwiGLU && (g.N % 256)) throw std::invalid_argument("gemm_bf16: SwiGLU needs N % 256 == 0");
+    const int bn = g.block_n ? g.block_n : 256;
+    switch (g.epi.kind) {
+        case kEpiBF16: bn == 128 ? launch<128, kEpiBF16>(g, st) : launch<256, kEpiBF16>(g, st); break;
+        case kEpiF32: bn == 128 ? launch<128, kEpiF32>(g, st) : launch<256, kEpiF32>(g, st); break;
+        case kEpiResidual: bn == 128 ? launch<128, kEpiResidual>(g, st) : launch<256, kEpiResidual>(g, st); break;
+        case kEpiSwiGLU: launch<256, kEpiSwiGLU>(g, st); break;
+        default: throw std::invalid_argument("gemm_bf16: unknown epilogue");
+    }
+}
+
+}  // namespace rs

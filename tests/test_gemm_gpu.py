@@ -1,0 +1,73 @@
+"""GPU: tcgen05 GEMM (gemm_sm100.cu) against a plain PyTorch fp32 reference of the same op.
+Tolerance: bf16 inputs, fp32 accumulation -> compare to fp32 matmul of the bf16 inputs with
+rel 2e-3 of the row scale (accumulation-order differences only); bf16 outputs add one bf16
+rounding (rel 8e-3)."""
+import ctypes
+
+import pytest
+import torch
+
+import paper_2510_26475_b200 as rb
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(A, B, out, bias=None, epi=0, scale=1.0, block_n=0):
+    dev = rb.default_device()
+    torch.cuda.synchronize()
+    rb._check(rb.lib().rs_gemm_bf16(dev.handle, ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
+                                    ctypes.c_void_p(out.data_ptr()),
+                                    ctypes.c_void_p(bias.data_ptr()) if bias is not None else None,
+                                    A.shape[0], B.shape[0], A.shape[1], epi, scale, block_n))
+    dev.sync()
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(128, 256, 64, 0), (1344, 2560, 2048, 0), (200, 1000, 256, 128),
+                                      (7, 96, 136, 128), (1, 151936 // 64, 2048, 0), (513, 2048, 11008, 256)])
+def test_gemm_bf16_bias(M, N, K, bn):
+    torch.manual_seed(M + N + K)
+    A = (torch.randn(M, K, device="cuda") * 0.5).bfloat16()
+    B = (torch.randn(N, K, device="cuda") * 0.05).bfloat16()
+    bias = (torch.randn(N, device="cuda") * 0.1).bfloat16()
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    _run(A, B, out, bias, 0, 1.0, bn)
+    ref = A.float() @ B.float().t() + bias.float()
+    err = (out.float() - ref).abs().max().item()
+    assert err <= 8e-3 * ref.abs().max().item() + 1e-3, err
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 1024, 256), (1344, 4096, 2048)])
+def test_gemm_f32_scaled(M, N, K):
+    torch.manual_seed(1)
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    B = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
+    out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    _run(A, B, out, None, 1, 3.0)
+    ref = (A.float() @ B.float().t()) * 3.0
+    assert (out - ref).abs().max().item() <= 2e-3 * ref.abs().max().item()
+
+
+def test_gemm_residual_add():
+    torch.manual_seed(2)
+    M, N, K = 777, 2048, 2048
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    B = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
+    R = torch.randn(M, N, device="cuda")
+    out = R.clone()
+    _run(A, B, out, None, 2)
+    ref = R + A.float() @ B.float().t()
+    assert (out - ref).abs().max().item() <= 2e-3 * ref.abs().max().item()
+
+
+def test_gemm_swiglu():
+    torch.manual_seed(3)
+    M, F, K = 333, 512, 256  # N = 2F interleaved per 256-row block: [128 gate, 128 up]
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    G = (torch.randn(F, K, device="cuda") * 0.05).bfloat16()
+    U = (torch.randn(F, K, device="cuda") * 0.05).bfloat16()
+    B = torch.cat([torch.cat([G[b * 128:(b + 1) * 128], U[b * 128:(b + 1) * 128]]) for b in range(F // 128)])
+    out = torch.empty(M, F, device="cuda", dtype=torch.bfloat16)
+    _run(A, B.contiguous(), out, None, 3)
+    g, u = A.float() @ G.float().t(), A.float() @ U.float().t()
+    ref = torch.nn.functional.silu(g) * u
+    assert (out.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item() + 1e-3
