@@ -210,7 +210,7 @@ int rs_engine_accept_lens(rs_engine *e, int32_t req, int32_t *out, int32_t cap, 
 int rs_engine_destroy(rs_engine *e);
 /* Debug: capture the logit rows of the next steps (for replay against the CPU oracle). */
 int rs_engine_set_capture(rs_engine *e, int32_t enable);
-int rs_engine_capture_count(const rs_engine *e, int64_t *rows, int32_t *vocab);
+int rs_engine_capture_count(const rs_engine *e, int64_t *rows, int32_t *vocab, int32_t *ext_width);
 int rs_engine_capture_read(rs_engine *e, int64_t first, int64_t count, int32_t *role, int32_t *req,
                            int32_t *ctx_len, int32_t *ext, double *logits);
 
@@ -228,6 +228,14 @@ int rs_kd_update_tabular(rs_ctx *ctx, const rs_model *drafter, const rs_kd_sampl
    block_n: 0 (auto) | 128 | 256. Runs on the context stream. */
 int rs_gemm_bf16(rs_ctx *ctx, const void *A_dev, const void *B_dev, void *C_dev, const void *bias_dev, int32_t M,
                  int32_t N, int32_t K, int32_t epilogue, float scale, int32_t block_n);
+/* Device pointer + byte size of a named weight tensor of a transformer target / drafter
+   ("emb", "final_norm", "rope", per layer "qkv_w", "qkv_b", "o_w", "gu_w", "down_w", "ln1",
+   "ln2"; drafter "fc_w", "norm_emb", "norm_hid", "lm_w"), for export / test references. */
+int rs_model_tensor(const rs_model *m, const char *name, int32_t layer, void **dev_ptr, int64_t *bytes);
+/* Device-to-device copy on the context stream (synchronous). */
+int rs_memcpy_d2d(rs_ctx *ctx, void *dst_dev, const void *src_dev, int64_t bytes);
+/* Parameter count of a model (tabular: table size). */
+int rs_model_params(const rs_model *m, int64_t *out);
 
 /* mt19937_64 state helper for rs_kd_update_tabular: 313 uint64 (312 words + index). */
 int rs_mt19937_64_seed(uint64_t seed, uint64_t *state313);

@@ -43,7 +43,10 @@ std::shared_ptr<Model> model_of(const json & j) {
         m->vocab = j.at("vocab");
         m->temperature = j.value("temperature", 1.0);
         m->version = j.value("version", 0);
-        for (const auto & r : j.at("rows")) m->rows.emplace(r.at("ctx").get<std::vector<int>>(), r.at("logits").get<std::vector<double>>());
+        m->depth_aware = j.value("depth_aware", false);
+        for (const auto & r : j.at("rows"))
+            m->rows.emplace(std::make_pair(r.at("ctx").get<std::vector<int>>(), m->depth_aware ? r.value("depth", 0) : 0),
+                            r.at("logits").get<std::vector<double>>());
         return m;
     }
     throw std::invalid_argument("unknown model kind " + kind);

@@ -30,8 +30,8 @@ std::vector<double> TabularModel::logits(const std::vector<int> & ctx) const {
                                table.begin() + static_cast<long>((r + 1) * V));
 }
 
-std::vector<double> LookupModel::logits(const std::vector<int> & ctx) const {
-    auto it = rows.find(ctx);
+std::vector<double> LookupModel::logits_at(const std::vector<int> & ctx, int depth) const {
+    auto it = rows.find({ctx, depth_aware ? depth : 0});
     if (it == rows.end()) {
         std::string s = "LookupModel: no row for context of length " + std::to_string(ctx.size()) + " [";
         for (size_t i = ctx.size() > 6 ? ctx.size() - 6 : 0; i < ctx.size(); ++i) s += std::to_string(ctx[i]) + " ";
@@ -55,8 +55,8 @@ std::vector<double> softmax(const std::vector<double> & z, double tau) {
 }
 
 // model.cpp:132-139: EOS bias added to z[V-1] before the temperature division.
-std::vector<double> dist(const Model & m, const std::vector<int> & ctx, double eos_bias) {
-    std::vector<double> z = m.logits(ctx);
+std::vector<double> dist(const Model & m, const std::vector<int> & ctx, double eos_bias, int depth) {
+    std::vector<double> z = m.logits_at(ctx, depth);
     if (static_cast<int>(z.size()) != m.vocab) throw std::invalid_argument("dist: row has wrong width");
     z[z.size() - 1] += eos_bias;
     return softmax(z, m.temperature);
@@ -169,11 +169,11 @@ VerifyOutcome spec_step_tree(const Model & target, const Model & drafter, const 
         size_t longest = 0;
         int tree_tokens = 0;
         std::vector<int> roots;
-        if (greedy) roots = top_k_first(dist(drafter, round_ctx, eos_bias), cfg.branching);
+        if (greedy) roots = top_k_first(dist(drafter, round_ctx, eos_bias, 0), cfg.branching);
         for (size_t ci = 0; ci < chains.size(); ++ci) {
             auto & chain = chains[ci];
             for (int pos = 0; pos < n_eff; ++pos) {
-                std::vector<double> qd = dist(drafter, extend(round_ctx, chain), eos_bias);
+                std::vector<double> qd = dist(drafter, extend(round_ctx, chain), eos_bias, static_cast<int>(chain.size()));
                 int d;
                 if (greedy) d = pos == 0 ? roots[std::min(ci, roots.size() - 1)] : argmax_first(qd);
                 else d = sample_from(qd, rng.du());
@@ -188,7 +188,7 @@ VerifyOutcome spec_step_tree(const Model & target, const Model & drafter, const 
 
         // branch point (specdec.cpp:197-217)
         const std::vector<double> p1 = dist(target, round_ctx, eos_bias);
-        const std::vector<double> q1 = dist(drafter, round_ctx, eos_bias);
+        const std::vector<double> q1 = dist(drafter, round_ctx, eos_bias, 0);
         int selected = -1;
         if (greedy) {
             const int a1 = argmax_first(p1);
@@ -224,7 +224,7 @@ VerifyOutcome spec_step_tree(const Model & target, const Model & drafter, const 
         for (size_t pos = 1; pos < chain.size() && !out.ended; ++pos) {
             const std::vector<int> c = extend(ctx, accepted);
             const std::vector<double> pd = dist(target, c, eos_bias);
-            const std::vector<double> qd = dist(drafter, c, eos_bias);
+            const std::vector<double> qd = dist(drafter, c, eos_bias, static_cast<int>(pos));
             const int d = chain[pos];
             bool ok;
             int repl = -1;

@@ -60,6 +60,10 @@ struct Model {
     int version = 0;
     virtual ~Model() = default;
     virtual std::vector<double> logits(const std::vector<int> & ctx) const = 0;
+    // `depth` = tokens beyond the current round's root (0 at the root). Tabular models ignore
+    // it; an EAGLE drafter's row depends on it (target features at the root, its own hidden
+    // state deeper in the tree), so captured drafter rows are keyed by (ctx, depth).
+    virtual std::vector<double> logits_at(const std::vector<int> & ctx, int /*depth*/) const { return logits(ctx); }
     int eos() const { return vocab - 1; }  // model.hpp:20
 };
 
@@ -73,12 +77,14 @@ struct TabularModel : Model {
 // Logit rows captured from another implementation (the CUDA engine), keyed by context.
 // Used to replay the acceptance logic bit-for-bit on exactly the rows the GPU computed.
 struct LookupModel : Model {
-    std::map<std::vector<int>, std::vector<double>> rows;
-    std::vector<double> logits(const std::vector<int> & ctx) const override;
+    bool depth_aware = false;
+    std::map<std::pair<std::vector<int>, int>, std::vector<double>> rows;  // (ctx, depth or 0)
+    std::vector<double> logits(const std::vector<int> & ctx) const override { return logits_at(ctx, 0); }
+    std::vector<double> logits_at(const std::vector<int> & ctx, int depth) const override;
 };
 
 std::vector<double> softmax(const std::vector<double> & z, double tau);             // model.cpp:53-68
-std::vector<double> dist(const Model & m, const std::vector<int> & ctx, double eos_bias);
+std::vector<double> dist(const Model & m, const std::vector<int> & ctx, double eos_bias, int depth = 0);
 int sample_from(const std::vector<double> & p, double u);                           // model.cpp:23-40
 int argmax_first(const std::vector<double> & p);                                     // greedy: lowest index wins ties
 double accept_prob(double p, double q);                                              // specdec.cpp:25-33

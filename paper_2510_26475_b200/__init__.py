@@ -119,6 +119,7 @@ EXPORTED_SYMBOLS = [
     "rs_engine_steps", "rs_engine_step_logprobs", "rs_engine_accept_lens", "rs_engine_destroy",
     "rs_engine_set_capture", "rs_engine_capture_count", "rs_engine_capture_read",
     "rs_kd_weight", "rs_kd_update_tabular", "rs_mt19937_64_seed", "rs_gemm_bf16",
+    "rs_model_tensor", "rs_memcpy_d2d", "rs_model_params",
 ]
 
 _lib = None
@@ -177,13 +178,16 @@ def lib():
             "rs_engine_accept_lens": ([vp, i32, P(i32), i32, P(i32)], ctypes.c_int),
             "rs_engine_destroy": ([vp], ctypes.c_int),
             "rs_engine_set_capture": ([vp, i32], ctypes.c_int),
-            "rs_engine_capture_count": ([vp, P(i64), P(i32)], ctypes.c_int),
+            "rs_engine_capture_count": ([vp, P(i64), P(i32), P(i32)], ctypes.c_int),
             "rs_engine_capture_read": ([vp, i64, i64, P(i32), P(i32), P(i32), P(i32), P(dbl)], ctypes.c_int),
             "rs_kd_weight": ([dbl, P(dbl), i32, _KDPolicy, P(ctypes.c_int)], dbl),
             "rs_kd_update_tabular": ([vp, vp, P(_KDSample), i32, _KDPolicy, P(u64), dbl, P(vp), P(_KDResult)],
                                      ctypes.c_int),
             "rs_mt19937_64_seed": ([u64, P(u64)], ctypes.c_int),
             "rs_gemm_bf16": ([vp, vp, vp, vp, vp, i32, i32, i32, i32, ctypes.c_float, i32], ctypes.c_int),
+            "rs_model_tensor": ([vp, ctypes.c_char_p, i32, P(vp), P(i64)], ctypes.c_int),
+            "rs_memcpy_d2d": ([vp, vp, vp, i64], ctypes.c_int),
+            "rs_model_params": ([vp, P(i64)], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -386,6 +390,106 @@ class TabularARModel(Model):
     def to_json(self) -> dict:
         return {"vocab_size": self.vocab_size, "order": self.order, "temperature": self.temperature,
                 "logits": self.logits()}
+
+
+@dataclass
+class TransformerShape:
+    """Qwen2-style decoder shape. Presets follow the public Qwen2.5 config.json values."""
+    vocab: int
+    d_model: int
+    n_layers: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int = 128
+    d_ff: int = 0
+    max_ctx: int = 4096
+    rope_theta: float = 1e6
+    rms_eps: float = 1e-6
+    init_std: float = 0.02
+    logit_scale: float = 1.0
+    temperature: float = 1.0
+
+    @staticmethod
+    def tiny(vocab=1024, max_ctx=512, **kw):
+        """BASELINE cfg1: 2-layer d=256 target (CPU-runnable size)."""
+        return TransformerShape(vocab, 256, 2, 4, 2, 128, 512, max_ctx, **kw)
+
+    @staticmethod
+    def qwen2_5_3b(max_ctx=4096, **kw):
+        return TransformerShape(151936, 2048, 36, 16, 2, 128, 11008, max_ctx, **kw)
+
+    @staticmethod
+    def qwen2_5_7b(max_ctx=4096, **kw):
+        return TransformerShape(152064, 3584, 28, 28, 4, 128, 18944, max_ctx, **kw)
+
+    @staticmethod
+    def qwen2_5_14b(max_ctx=4096, **kw):
+        return TransformerShape(152064, 5120, 48, 40, 8, 128, 13824, max_ctx, **kw)
+
+    def _c(self):
+        return _TransformerShape(self.vocab, self.d_model, self.n_layers, self.n_heads, self.n_kv_heads, self.head_dim,
+                                 self.d_ff, self.max_ctx, self.rope_theta, self.rms_eps, self.init_std,
+                                 self.logit_scale, self.temperature)
+
+    def macs_per_token(self) -> int:
+        """Dense MACs per token (QKV+O+MLP over all layers + LM head), SURVEY.md §8."""
+        q = (self.n_heads + 2 * self.n_kv_heads) * self.head_dim
+        per_layer = self.d_model * q + self.n_heads * self.head_dim * self.d_model + 3 * self.d_model * self.d_ff
+        return self.n_layers * per_layer + self.d_model * self.vocab
+
+    def kv_bytes_per_token(self) -> int:
+        return self.n_layers * 2 * self.n_kv_heads * self.head_dim * 2
+
+
+class _NeuralModel(Model):
+    def tensor(self, name: str, layer: int = -1):
+        """(device pointer, bytes) of a named weight tensor."""
+        p, b = ctypes.c_void_p(), ctypes.c_int64()
+        _check(lib().rs_model_tensor(self.handle, name.encode(), layer, ctypes.byref(p), ctypes.byref(b)))
+        return p.value, b.value
+
+    def to_torch(self, name: str, layer: int = -1, dtype=None, shape=None):
+        """Copy a weight tensor into a new torch CUDA tensor (tests / export only)."""
+        import torch
+        ptr, nbytes = self.tensor(name, layer)
+        dtype = dtype or (torch.float32 if name in ("ln1", "ln2", "final_norm", "norm_emb", "norm_hid", "rope")
+                          else torch.bfloat16)
+        t = torch.empty(nbytes // torch.tensor([], dtype=dtype).element_size(), dtype=dtype, device="cuda")
+        torch.cuda.synchronize()
+        _check(lib().rs_memcpy_d2d(self.device.handle, ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(ptr), nbytes))
+        return t.view(*shape) if shape else t
+
+    @property
+    def n_params(self) -> int:
+        v = ctypes.c_int64()
+        _check(lib().rs_model_params(self.handle, ctypes.byref(v)))
+        return v.value
+
+
+class TransformerModel(_NeuralModel):
+    """Qwen2-shaped target with synthetic N(0, init_std) bf16 weights generated on the device."""
+
+    def __init__(self, shape: TransformerShape, seed: int = 0, device: Optional[Device] = None):
+        self.device = device or default_device()
+        self.shape = shape
+        h = ctypes.c_void_p()
+        sc = shape._c()
+        _check(lib().rs_transformer_create(self.device.handle, ctypes.byref(sc), seed & (2 ** 64 - 1),
+                                           ctypes.byref(h)))
+        self.handle = h
+
+
+class EagleDrafter(_NeuralModel):
+    """EAGLE-3-style drafter bound to `target` (consumes its low/mid/high hidden states)."""
+
+    def __init__(self, target: TransformerModel, seed: int = 1, version: int = 0):
+        self.device = target.device
+        self.target = target
+        self.shape = target.shape
+        h = ctypes.c_void_p()
+        _check(lib().rs_drafter_create(self.device.handle, target.handle, seed & (2 ** 64 - 1), version,
+                                       ctypes.byref(h)))
+        self.handle = h
 
 
 # ---- ProfileTable (server.hpp:21-49) ------------------------------------------------------------------
@@ -670,17 +774,23 @@ class BatchEngine:
         _check(lib().rs_engine_set_capture(self.handle, 1 if on else 0))
 
     def captured_rows(self):
-        n, V = ctypes.c_int64(), ctypes.c_int32()
-        _check(lib().rs_engine_capture_count(self.handle, ctypes.byref(n), ctypes.byref(V)))
-        k, V = n.value, V.value
+        """[(role, request, ctx_len, ext_tokens, logits)] for every row produced since capture was
+        enabled; role 1 = target (p rows), 0 = drafter (q rows). The row's context is the
+        request's first ctx_len tokens followed by ext_tokens."""
+        n, V, W = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().rs_engine_capture_count(self.handle, ctypes.byref(n), ctypes.byref(V), ctypes.byref(W)))
+        k, V, W = n.value, V.value, W.value
         if k == 0:
             return []
-        nmax = 64
         role, req, cl = (ctypes.c_int32 * k)(), (ctypes.c_int32 * k)(), (ctypes.c_int32 * k)()
-        ext = (ctypes.c_int32 * (k * nmax))()
+        ext = (ctypes.c_int32 * (k * W))()
         lg = (ctypes.c_double * (k * V))()
         _check(lib().rs_engine_capture_read(self.handle, 0, k, role, req, cl, ext, lg))
-        return role, req, cl, ext, lg, V
+        out = []
+        for i in range(k):
+            e = [x for x in ext[i * W:(i + 1) * W] if x >= 0]
+            out.append((role[i], req[i], cl[i], e, lg[i * V:(i + 1) * V]))
+        return out
 
     def __del__(self):
         try:

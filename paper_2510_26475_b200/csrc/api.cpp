@@ -10,6 +10,7 @@
 #include "engine.h"
 #include "gemm.h"
 #include "kd.h"
+#include "model.h"
 
 namespace {
 thread_local std::string g_err;
@@ -310,7 +311,7 @@ int rs_engine_create(rs_ctx *ctx, const rs_model *target, const rs_model *drafte
         e->d_st_logq.alloc((size_t)N * steps_cap);
         e->d_st_drafted.alloc((size_t)N * steps_cap);
         if (e->record_full) e->d_st_full.alloc((size_t)N * steps_cap * e->V);
-        e->d_cyc.alloc((size_t)N * 9);
+        e->d_cyc.alloc((size_t)N * 11);
         e->d_round_cost.alloc((size_t)N * kMaxRounds * 3);
         e->d_chain.alloc((size_t)N * e->t_max * (e->n_max + 3));
         RS_CUDA(cudaMemset(e->d_chain.p, 0, e->d_chain.bytes()));
@@ -334,7 +335,7 @@ int rs_engine_create(rs_ctx *ctx, const rs_model *target, const rs_model *drafte
             const size_t rows = (size_t)N * e->slots_max * e->V * sizeof(float);
             e->d_P.alloc(rows);
             e->d_Q.alloc(rows);
-            e->pair = make_transformer_pair(ctx, target, drafter, n, e->slots_max, e->prompt_len, prompts, tok_cap);
+            e->pair = make_transformer_pair(ctx, e.get(), target, drafter, n, e->slots_max, e->prompt_len, prompts, tok_cap);
         }
         if (drafter && drafter->vocab != e->V) throw std::invalid_argument("BatchEngine: drafter vocabulary differs from target");
         RS_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -455,11 +456,12 @@ int rs_engine_destroy(rs_engine *e) {
 int rs_engine_set_capture(rs_engine *e, int32_t enable) {
     return guard([&] { need(e, "rs_engine_set_capture"); e->capture = enable != 0; });
 }
-int rs_engine_capture_count(const rs_engine *e, int64_t *rows, int32_t *vocab) {
+int rs_engine_capture_count(const rs_engine *e, int64_t *rows, int32_t *vocab, int32_t *ext_width) {
     return guard([&] {
         need(e, "rs_engine_capture_count");
         *rows = (int64_t)e->cap_role.size();
         *vocab = e->V;
+        if (ext_width) *ext_width = e->n_max;
     });
 }
 int rs_engine_capture_read(rs_engine *e, int64_t first, int64_t count, int32_t *role, int32_t *req, int32_t *ctx_len,
@@ -499,6 +501,68 @@ int rs_kd_update_tabular(rs_ctx *ctx, const rs_model *drafter, const rs_kd_sampl
     });
 }
 
+int rs_model_tensor(const rs_model *m, const char *name, int32_t layer, void **ptr, int64_t *bytes) {
+    return guard([&] {
+        need(m, "rs_model_tensor");
+        need(name, "rs_model_tensor: name");
+        const std::string nm(name);
+        void *p = nullptr;
+        size_t b = 0;
+        auto layer_tensor = [&](const LayerW &w, const TfShape &s, int d_in) {
+            const size_t q = s.qkv_dim();
+            if (nm == "qkv_w") { p = w.qkv_w; b = q * d_in * 2; }
+            else if (nm == "qkv_b") { p = w.qkv_b; b = q * 2; }
+            else if (nm == "o_w") { p = w.o_w; b = (size_t)s.d * s.H * s.hd * 2; }
+            else if (nm == "gu_w") { p = w.gu_w; b = 2 * (size_t)s.dff * s.d * 2; }
+            else if (nm == "down_w") { p = w.down_w; b = (size_t)s.d * s.dff * 2; }
+            else if (nm == "ln1") { p = w.ln1; b = (size_t)d_in * 4; }
+            else if (nm == "ln2") { p = w.ln2; b = (size_t)s.d * 4; }
+        };
+        if (m->kind == rs_model::Transformer) {
+            const auto *t = static_cast<const TransformerModel *>(m);
+            const TfShape &s = t->s;
+            if (nm == "emb") { p = t->emb; b = (size_t)s.V * s.d * 2; }
+            else if (nm == "final_norm") { p = t->final_norm; b = (size_t)s.d * 4; }
+            else if (nm == "rope") { p = t->rope; b = (size_t)s.max_ctx * s.hd * 4; }
+            else {
+                if (layer < 0 || layer >= s.L) throw std::invalid_argument("rs_model_tensor: layer out of range");
+                layer_tensor(t->layers[layer], s, s.d);
+            }
+        } else if (m->kind == rs_model::Drafter) {
+            const auto *dm = static_cast<const DrafterModel *>(m);
+            const TfShape &s = dm->s;
+            if (nm == "fc_w") { p = dm->fc_w; b = (size_t)s.d * 3 * s.d * 2; }
+            else if (nm == "norm_emb") { p = dm->norm_emb; b = (size_t)s.d * 4; }
+            else if (nm == "norm_hid") { p = dm->norm_hid; b = (size_t)s.d * 4; }
+            else if (nm == "final_norm") { p = dm->final_norm; b = (size_t)s.d * 4; }
+            else if (nm == "lm_w") { p = dm->lm_w; b = (size_t)s.V * s.d * 2; }
+            else layer_tensor(dm->layer, s, 2 * s.d);
+        } else {
+            throw std::invalid_argument("rs_model_tensor: tabular models have no named tensors");
+        }
+        if (!p) throw std::invalid_argument("rs_model_tensor: unknown tensor " + nm);
+        *ptr = p;
+        *bytes = (int64_t)b;
+    });
+}
+
+int rs_memcpy_d2d(rs_ctx *ctx, void *dst, const void *src, int64_t bytes) {
+    return guard([&] {
+        need(ctx, "rs_memcpy_d2d");
+        RS_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+        RS_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int rs_model_params(const rs_model *m, int64_t *out) {
+    return guard([&] {
+        need(m, "rs_model_params");
+        if (m->kind == rs_model::Transformer) *out = (int64_t) static_cast<const TransformerModel *>(m)->n_params;
+        else if (m->kind == rs_model::Drafter) *out = (int64_t) static_cast<const DrafterModel *>(m)->n_params;
+        else *out = (int64_t) static_cast<const TabularModel *>(m)->host.size();
+    });
+}
+
 int rs_gemm_bf16(rs_ctx *ctx, const void *A, const void *B, void *Cp, const void *bias, int32_t M, int32_t N, int32_t K,
                  int32_t epilogue, float scale, int32_t block_n) {
     return guard([&] {
@@ -518,6 +582,24 @@ int rs_gemm_bf16(rs_ctx *ctx, const void *A, const void *B, void *Cp, const void
         g.epi.bias = bias;
         g.epi.scale = scale;
         gemm_bf16(g, ctx->stream);
+    });
+}
+
+int rs_transformer_create(rs_ctx *ctx, const rs_transformer_shape *sh, uint64_t seed, rs_model **out) {
+    return guard([&] {
+        need(ctx, "rs_transformer_create");
+        need(sh, "rs_transformer_create: shape");
+        need(out, "rs_transformer_create");
+        *out = create_transformer(ctx, *sh, seed);
+    });
+}
+
+int rs_drafter_create(rs_ctx *ctx, const rs_model *target, uint64_t seed, int32_t version, rs_model **out) {
+    return guard([&] {
+        need(ctx, "rs_drafter_create");
+        need(target, "rs_drafter_create: target");
+        need(out, "rs_drafter_create");
+        *out = create_drafter(ctx, target, seed, version);
     });
 }
 

@@ -1,0 +1,240 @@
+// attention.cu -- tree-causal GQA attention over the paged-by-sequence KV cache.
+//
+// A work item is up to 64/G query tokens of one sequence that share one key mapping; the CTA
+// for (item, kv head) holds those tokens x G query heads as 64 rows (4 warps x 16). Keys are
+// visited in LOGICAL position order in 64-key chunks from position 0 up to the item's last
+// query position; a key at logical position p >= ltree of a tree row lives in the row's own
+// chain slots (tbase + chain*nstride + p - ltree), so a drafted token sees the context, the
+// root and exactly its own chain prefix -- the tree-causal mask of SURVEY.md §8 A3 -- and
+// nothing else. Because the chunking and the online-softmax merge order depend only on
+// logical positions, a row's result does not depend on which other rows share its CTA: the
+// same token gives the same output whether it is verified inside a tree or decoded alone.
+// Q.K^T and P.V run on the tensor cores with mma.sync m16n8k16 (bf16 in, fp32 accumulate),
+// K/V chunks are double-buffered with cp.async into XOR-swizzled shared memory.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "model.h"
+
+namespace rs {
+
+namespace {
+
+constexpr int kHD = 128;
+constexpr int kChunk = 64;
+constexpr int kRows = 64;
+constexpr int kRowBytes = kHD * 2;                 // 256
+constexpr int kTileBytes = kChunk * kRowBytes;     // 16 KB
+constexpr int kSmem = kTileBytes * 5 + kRows * 4;  // Q + 2x(K,V) + row positions
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ int swz(int row, int chunk) { return row * kRowBytes + ((chunk ^ (row & 7)) << 4); }
+
+__device__ __forceinline__ void cp16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+
+__global__ void __launch_bounds__(128) attn_kernel(const bf16 *q, const RowDesc *rows, const AttnItem *items,
+                                                   KvCache kv, int layer, int H, int KV, float scale_log2,
+                                                   bf16 *out) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint8_t *sQ = sm;
+    uint8_t *sK = sm + kTileBytes;
+    uint8_t *sV = sK + 2 * kTileBytes;
+    int *rowpos = reinterpret_cast<int *>(sV + 2 * kTileBytes);
+
+    const AttnItem it = items[blockIdx.x];
+    const int kvh = blockIdx.y;
+    const int G = H / KV;
+    const int nr = it.nrows * G;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    for (int idx = tid; idx < kRows * 16; idx += 128) {
+        const int r = idx >> 4, c = idx & 15;
+        uint8_t *dst = sQ + swz(r, c);
+        if (r < nr) {
+            const int tok = it.row0 + r / G, head = kvh * G + r % G;
+            cp16(dst, q + ((size_t)tok * H + head) * kHD + c * 8);
+        } else {
+            *reinterpret_cast<int4 *>(dst) = make_int4(0, 0, 0, 0);
+        }
+    }
+    if (tid < kRows) rowpos[tid] = tid < nr ? rows[it.row0 + tid / G].pos : -1;
+
+    auto load_kv = [&](int c, int buf) {
+        uint8_t *k = sK + buf * kTileBytes, *v = sV + buf * kTileBytes;
+        for (int idx = tid; idx < kChunk * 16; idx += 128) {
+            const int kk = idx >> 4, ch = idx & 15;
+            const int p = c * kChunk + kk;
+            if (p <= it.maxpos) {
+                const int phys = (it.chain < 0 || p < it.ltree) ? p : it.tbase + it.chain * it.nstride + (p - it.ltree);
+                const size_t o = kv.off(layer, it.seq, kvh, phys) + ch * 8;
+                cp16(k + swz(kk, ch), kv.k + o);
+                cp16(v + swz(kk, ch), kv.v + o);
+            } else {
+                *reinterpret_cast<int4 *>(k + swz(kk, ch)) = make_int4(0, 0, 0, 0);
+                *reinterpret_cast<int4 *>(v + swz(kk, ch)) = make_int4(0, 0, 0, 0);
+            }
+        }
+    };
+
+    const int nchunks = it.maxpos / kChunk + 1;
+    load_kv(0, 0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+
+    const bool active = warp * 16 < nr;
+    uint32_t qa[8][4];
+    float o[16][4];
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    int pos0 = -1, pos1 = -1;
+
+    for (int c = 0; c < nchunks; ++c) {
+        if (c + 1 < nchunks) {
+            load_kv(c + 1, (c + 1) & 1);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        if (c == 0 && active) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const int r = warp * 16 + (lane & 15), ch = 2 * kk + (lane >> 4);
+                ldsm_x4(smem_u32(sQ + swz(r, ch)), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+            }
+            pos0 = rowpos[warp * 16 + (lane >> 2)];
+            pos1 = rowpos[warp * 16 + (lane >> 2) + 8];
+        }
+        if (active) {
+            const uint8_t *k = sK + (c & 1) * kTileBytes, *v = sV + (c & 1) * kTileBytes;
+            float s[8][4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+#pragma unroll
+            for (int jp = 0; jp < 4; ++jp) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int key = 16 * jp + (lane & 7) + ((lane >> 4) << 3), ch = 2 * kk + ((lane >> 3) & 1);
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4(smem_u32(k + swz(key, ch)), b0, b1, b2, b3);
+                    mma16816(s[2 * jp], qa[kk], b0, b1);
+                    mma16816(s[2 * jp + 1], qa[kk], b2, b3);
+                }
+            }
+            // causal / tree mask + online softmax (base-2, pre-scaled)
+            float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+                const int p = c * kChunk + nt * 8 + 2 * (lane & 3);
+                s[nt][0] = p <= pos0 ? s[nt][0] * scale_log2 : -INFINITY;
+                s[nt][1] = p + 1 <= pos0 ? s[nt][1] * scale_log2 : -INFINITY;
+                s[nt][2] = p <= pos1 ? s[nt][2] * scale_log2 : -INFINITY;
+                s[nt][3] = p + 1 <= pos1 ? s[nt][3] * scale_log2 : -INFINITY;
+                mx0 = fmaxf(mx0, fmaxf(s[nt][0], s[nt][1]));
+                mx1 = fmaxf(mx1, fmaxf(s[nt][2], s[nt][3]));
+            }
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+            const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);
+            const float base0 = n0 == -INFINITY ? 0.f : n0, base1 = n1 == -INFINITY ? 0.f : n1;
+            const float a0 = exp2f(m0 - base0), a1 = exp2f(m1 - base1);
+            m0 = n0;
+            m1 = n1;
+            l0 *= a0;
+            l1 *= a1;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                o[i][0] *= a0;
+                o[i][1] *= a0;
+                o[i][2] *= a1;
+                o[i][3] *= a1;
+            }
+            uint32_t pa[4][4];
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+                const float p0 = exp2f(s[nt][0] - base0), p1 = exp2f(s[nt][1] - base0);
+                const float p2 = exp2f(s[nt][2] - base1), p3 = exp2f(s[nt][3] - base1);
+                l0 += p0 + p1;
+                l1 += p2 + p3;
+                pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
+                pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
+            }
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+#pragma unroll
+                for (int dp = 0; dp < 8; ++dp) {
+                    const int key = 16 * kk + (lane & 7) + (((lane >> 3) & 1) << 3), ch = 2 * dp + (lane >> 4);
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4_t(smem_u32(v + swz(key, ch)), b0, b1, b2, b3);
+                    mma16816(o[2 * dp], pa[kk], b0, b1);
+                    mma16816(o[2 * dp + 1], pa[kk], b2, b3);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (!active) return;
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+    const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
+    const int r0 = warp * 16 + (lane >> 2), r1 = r0 + 8;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        const int r = half ? r1 : r0;
+        if (r >= nr) continue;
+        const int tok = it.row0 + r / G, head = kvh * G + r % G;
+        bf16 *dst = out + ((size_t)tok * H + head) * kHD + 2 * (lane & 3);
+        const float inv = half ? inv1 : inv0;
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt) {
+            const float x = o[nt][half * 2 + 0] * inv, y = o[nt][half * 2 + 1] * inv;
+            *reinterpret_cast<__nv_bfloat162 *>(dst + nt * 8) = __floats2bfloat162_rn(x, y);
+        }
+    }
+}
+
+}  // namespace
+
+void k_attention(const bf16 *q, const RowDesc *rows, const AttnItem *items, int n_items, const KvCache &kv, int layer,
+                 const TfShape &s, bf16 *out, cudaStream_t st) {
+    if (n_items <= 0) return;
+    if (s.hd != kHD) throw std::invalid_argument("attention: head_dim must be 128");
+    static bool attr = false;
+    if (!attr) {
+        RS_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        attr = true;
+    }
+    const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(s.hd));
+    attn_kernel<<<dim3(n_items, s.KV), 128, kSmem, st>>>(q, rows, items, kv, layer, s.H, s.KV, scale_log2, out);
+    RS_LAUNCHED();
+}
+
+}  // namespace rs

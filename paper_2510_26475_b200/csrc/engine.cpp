@@ -166,6 +166,8 @@ SdDev rs_engine::dev(const rs_sdconfig &cfg, int nact) {
     d.drafted = c + 6 * n;
     d.emitted = c + 7 * n;
     d.n_rounds = c + 8 * n;
+    d.rsel = c + 9 * n;
+    d.racc = c + 10 * n;
     d.round_cost = d_round_cost.p;
     const size_t ch = (size_t)n * t_max;
     d.chain_tok = d_chain.p;
@@ -275,6 +277,7 @@ void rs_engine::step(rs_step_info *info) {
     drafter_versions.push_back(drafter ? drafter->version : -1);
 
     cudaStream_t st = ctx->stream;
+    pair->begin_step();
     for (int a = 0; a < batch; ++a) h_active[a] = active[a];
     RS_CUDA(cudaMemcpyAsync(d_active.p, h_active, batch * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     RS_CUDA(cudaEventRecord(ctx->ev0, st));
@@ -307,12 +310,14 @@ void rs_engine::step(rs_step_info *info) {
             pair->after_accept(d, false, st);
             if (round + 1 < mode.rounds) {
                 // any request continuing into the next round? (lockstep, server.cpp:154-178)
-                std::vector<int32_t> cont(n);
+                std::vector<int32_t> cont(n), lens(n);
                 RS_CUDA(cudaMemcpyAsync(cont.data(), d.cont, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+                RS_CUDA(cudaMemcpyAsync(lens.data(), d.len, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
                 RS_CUDA(cudaStreamSynchronize(st));
                 bool any = false;
                 for (int r : active) any |= cont[r] != 0;
                 if (!any) break;
+                for (int r : active) len[r] = lens[r];  // next round's forwards start from here
             }
         }
     } else {

@@ -112,11 +112,16 @@ struct ModelPair {
     virtual void after_accept(const SdDev &, bool /*naive*/, cudaStream_t) {}
     virtual void on_spec_enable(const SdDev &, cudaStream_t) {}
     virtual void set_drafter(const rs_model *) {}
+    virtual void begin_step() {}
 };
 
 std::unique_ptr<ModelPair> make_tabular_pair(const TabularModel *target, const TabularModel *drafter);
-std::unique_ptr<ModelPair> make_transformer_pair(rs_ctx *ctx, const rs_model *target, const rs_model *drafter,
-                                                 int n_req, int slots_max, const std::vector<int> &prompt_lens,
+}  // namespace rs
+struct rs_engine;
+namespace rs {
+std::unique_ptr<ModelPair> make_transformer_pair(rs_ctx *ctx, rs_engine *eng, const rs_model *target,
+                                                 const rs_model *drafter, int n_req, int slots_max,
+                                                 const std::vector<int> &prompt_lens,
                                                  const std::vector<std::vector<int>> &prompts, int tok_cap);
 
 }  // namespace rs

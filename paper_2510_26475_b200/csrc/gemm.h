@@ -12,6 +12,7 @@ struct GemmEpi {
     int ldo = 0;
     const void *bias = nullptr;  // bf16 [N] (kEpiBF16 only)
     float scale = 1.0f;          // kEpiF32 only
+    const int *row_map = nullptr;  // kEpiF32 only: output row of A-row m (-1 = drop); null = identity
 };
 
 struct GemmArgs {

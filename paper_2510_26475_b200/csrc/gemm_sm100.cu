@@ -169,7 +169,9 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi &ep, uint32_t tbase
                 }
             }
         } else if constexpr (EPI == kEpiF32) {
-            float *out = static_cast<float *>(ep.out) + static_cast<size_t>(row) * ep.ldo + n0;
+            const int orow = ep.row_map ? ep.row_map[row] : row;
+            if (orow < 0) return;
+            float *out = static_cast<float *>(ep.out) + static_cast<size_t>(orow) * ep.ldo + n0;
             if (n0 + 32 <= N) {
 #pragma unroll
                 for (int j = 0; j < 32; j += 4) {

@@ -1,0 +1,333 @@
+// model.cu -- weights, synthetic init and the elementwise kernels of the transformer forwards
+// (embedding gather, RMSNorm, RoPE + KV-cache store, EAGLE feature capture/gather) and K4, the
+// in-place KV-cache compaction of accepted tree paths.
+#include <cmath>
+
+#include "common.cuh"
+#include "model.h"
+#include "rng.cuh"
+
+namespace rs {
+
+namespace {
+
+__global__ void init_normal_kernel(bf16 *p, size_t n, uint64_t seed, uint64_t tid, float std) {
+    // Portable generator: splitmix64(seed, tensor, index) -> two uniforms -> Box-Muller.
+    const size_t i = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 2;
+    if (i >= n) return;
+    uint64_t s = seed ^ (tid * 0x9E3779B97F4A7C15ULL) ^ (i * 0xD1B54A32D192ED03ULL);
+    const uint64_t a = splitmix64(s), b = splitmix64(s);
+    const double u1 = (static_cast<double>(a >> 11) + 1.0) * 0x1.0p-53;  // (0, 1]
+    const double u2 = static_cast<double>(b >> 11) * 0x1.0p-53;
+    const double r = sqrt(-2.0 * log(u1));
+    p[i] = __float2bfloat16(static_cast<float>(r * cos(2.0 * M_PI * u2)) * std);
+    if (i + 1 < n) p[i + 1] = __float2bfloat16(static_cast<float>(r * sin(2.0 * M_PI * u2)) * std);
+}
+
+__global__ void fill_f32_kernel(float *p, size_t n, float v) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ void rope_table_kernel(float *rope, int max_ctx, int hd, float theta) {
+    const int pos = blockIdx.x, i = threadIdx.x;
+    if (i >= hd / 2) return;
+    const double inv = pow(static_cast<double>(theta), -2.0 * i / hd);
+    const double ang = pos * inv;
+    rope[((size_t)pos * (hd / 2) + i) * 2 + 0] = static_cast<float>(cos(ang));
+    rope[((size_t)pos * (hd / 2) + i) * 2 + 1] = static_cast<float>(sin(ang));
+}
+
+__global__ void embed_kernel(const RowDesc *rows, int M, const int32_t *tok, int tok_cap, const int32_t *chain_tok,
+                             int t_max, int n_max, const bf16 *emb, int V, int d, float *x) {
+    const int m = blockIdx.x;
+    if (m >= M) return;
+    const RowDesc r = rows[m];
+    int t = r.kind == 0 ? tok[(size_t)r.seq * tok_cap + r.pos]
+                        : chain_tok[((size_t)r.seq * t_max + r.chain) * n_max + r.cj];
+    t = min(max(t, 0), V - 1);
+    const bf16 *e = emb + (size_t)t * d;
+    float *o = x + (size_t)m * d;
+    for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
+        const int4 raw = *reinterpret_cast<const int4 *>(e + i);
+        const bf16 *h = reinterpret_cast<const bf16 *>(&raw);
+        float4 a = make_float4(__bfloat162float(h[0]), __bfloat162float(h[1]), __bfloat162float(h[2]),
+                               __bfloat162float(h[3]));
+        float4 b = make_float4(__bfloat162float(h[4]), __bfloat162float(h[5]), __bfloat162float(h[6]),
+                               __bfloat162float(h[7]));
+        *reinterpret_cast<float4 *>(o + i) = a;
+        *reinterpret_cast<float4 *>(o + i + 4) = b;
+    }
+}
+
+// One warp per row; y = x * rsqrt(mean(x^2) + eps) * w (Qwen2RMSNorm, fp32 math).
+template <class T>
+__global__ void rmsnorm_kernel(const T *x, int ldx, const float *w, int M, int d, float eps, bf16 *out, int ldo) {
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (row >= M) return;
+    const T *xr = x + (size_t)row * ldx;
+    float ss = 0.f;
+    for (int i = lane; i < d; i += 32) {
+        const float v = static_cast<float>(xr[i]);
+        ss += v * v;
+    }
+    ss = warp_sumf(ss);
+    const float inv = rsqrtf(ss / d + eps);
+    bf16 *o = out + (size_t)row * ldo;
+    for (int i = lane; i < d; i += 32) o[i] = __float2bfloat16(static_cast<float>(xr[i]) * inv * w[i]);
+}
+
+// RoPE (rotate-half, Qwen2) on q and k; q -> qbuf [M][H][hd]; k, v -> cache at the row's slot.
+__global__ void rope_store_kernel(const bf16 *qkv, const RowDesc *rows, int M, int H, int KV, int hd,
+                                  const float *rope, KvCache kv, int layer, bf16 *q) {
+    const int m = blockIdx.x;
+    const RowDesc r = rows[m];
+    const int qd = (H + 2 * KV) * hd;
+    const bf16 *src = qkv + (size_t)m * qd;
+    const int half = hd / 2;
+    const float *cs = rope + (size_t)r.pos * half * 2;
+    for (int idx = threadIdx.x; idx < (H + KV) * half; idx += blockDim.x) {
+        const int head = idx / half, i = idx % half;
+        const bf16 *h = src + head * hd;
+        const float x1 = __bfloat162float(h[i]), x2 = __bfloat162float(h[i + half]);
+        const float c = cs[2 * i], s = cs[2 * i + 1];
+        const bf16 o1 = __float2bfloat16(x1 * c - x2 * s), o2 = __float2bfloat16(x2 * c + x1 * s);
+        if (head < H) {
+            bf16 *dst = q + ((size_t)m * H + head) * hd;
+            dst[i] = o1;
+            dst[i + half] = o2;
+        } else {
+            bf16 *dst = kv.k + kv.off(layer, r.seq, head - H, r.phys);
+            dst[i] = o1;
+            dst[i + half] = o2;
+        }
+    }
+    for (int idx = threadIdx.x; idx < KV * hd; idx += blockDim.x) {
+        const int head = idx / hd, i = idx % hd;
+        kv.v[kv.off(layer, r.seq, head, r.phys) + i] = src[(H + KV) * hd + idx];
+    }
+}
+
+__global__ void store_features_kernel(const float *x, const RowDesc *rows, int M, int d, bf16 *feat, int max_ctx,
+                                      int slot) {
+    const int m = blockIdx.x;
+    const RowDesc r = rows[m];
+    bf16 *dst = feat + (((size_t)r.seq * max_ctx + r.phys) * 3 + slot) * d;
+    const float *src = x + (size_t)m * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = __float2bfloat16(src[i]);
+}
+
+// fin[m] = [g_low, g_mid, g_high] of the target at logical position pos-1 (zeros at pos 0).
+__global__ void gather_features_kernel(const RowDesc *rows, int M, int d, const bf16 *feat, int max_ctx, bf16 *fin) {
+    const int m = blockIdx.x;
+    const RowDesc r = rows[m];
+    bf16 *dst = fin + (size_t)m * 3 * d;
+    if (r.pos == 0) {
+        for (int i = threadIdx.x; i < 3 * d; i += blockDim.x) dst[i] = __float2bfloat16(0.f);
+        return;
+    }
+    const bf16 *src = feat + ((size_t)r.seq * max_ctx + (r.pos - 1)) * 3 * d;
+    for (int i = threadIdx.x * 8; i < 3 * d; i += blockDim.x * 8)
+        *reinterpret_cast<int4 *>(dst + i) = *reinterpret_cast<const int4 *>(src + i);
+}
+
+__global__ void rows_copy_kernel(const float *src, int lds, const int *srows, float *dst, int ldd, const int *drows,
+                                 int d) {
+    const int k = blockIdx.x;
+    const int sr = srows ? srows[k] : k, dr = drows ? drows[k] : k;
+    if (sr < 0 || dr < 0) return;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) dst[(size_t)dr * ldd + i] = src[(size_t)sr * lds + i];
+}
+
+// K4: move the accepted path of the selected chain from its tree slots to contiguous
+// positions, for every layer's K and V and the EAGLE features. One CTA per (sequence, token);
+// 16-byte vector moves, each warp streams whole 256-byte head rows.
+__global__ void compact_kernel(SdDev d, const int32_t *rsel, const int32_t *racc, const int32_t *rbase, KvCache kv,
+                               bf16 *feat, int feat_w, int max_ctx) {
+    const int a = blockIdx.x, j = blockIdx.y;
+    const int r = d.active[a];
+    const int sel = rsel[r], acc = racc[r];
+    if (sel <= 0 || j >= acc) return;  // chain 0 already sits at the contiguous positions
+    const int L0 = rbase[r];
+    const int src = L0 + sel * d.n + j, dst = L0 + j;
+    const int vec = kv.hd / 8;  // int4 per head row
+    const int per_layer = kv.KV * vec;
+    for (int idx = threadIdx.x; idx < kv.layers * per_layer; idx += blockDim.x) {
+        const int layer = idx / per_layer, rem = idx % per_layer, h = rem / vec, c = rem % vec;
+        const int4 *ks = reinterpret_cast<const int4 *>(kv.k + kv.off(layer, r, h, src)) + c;
+        const int4 *vs = reinterpret_cast<const int4 *>(kv.v + kv.off(layer, r, h, src)) + c;
+        reinterpret_cast<int4 *>(kv.k + kv.off(layer, r, h, dst))[c] = *ks;
+        reinterpret_cast<int4 *>(kv.v + kv.off(layer, r, h, dst))[c] = *vs;
+    }
+    if (feat) {
+        const int4 *fs = reinterpret_cast<const int4 *>(feat + ((size_t)r * max_ctx + src) * feat_w);
+        int4 *fd = reinterpret_cast<int4 *>(feat + ((size_t)r * max_ctx + dst) * feat_w);
+        for (int i = threadIdx.x; i < feat_w / 8; i += blockDim.x) fd[i] = fs[i];
+    }
+}
+
+}  // namespace
+
+void k_init_normal(bf16 *p, size_t n, uint64_t seed, uint64_t tid, float std, cudaStream_t st) {
+    if (!n) return;
+    const size_t pairs = (n + 1) / 2;
+    init_normal_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, st>>>(p, n, seed, tid, std);
+    RS_LAUNCHED();
+}
+
+void k_fill_f32(float *p, size_t n, float v, cudaStream_t st) {
+    if (!n) return;
+    fill_f32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, n, v);
+    RS_LAUNCHED();
+}
+
+void k_rope_table(float *rope, int max_ctx, int hd, float theta, cudaStream_t st) {
+    rope_table_kernel<<<max_ctx, std::max(32, hd / 2), 0, st>>>(rope, max_ctx, hd, theta);
+    RS_LAUNCHED();
+}
+
+void k_embed(const RowDesc *rows, int M, const int32_t *tok, int tok_cap, const int32_t *chain_tok, int t_max,
+             int n_max, const bf16 *emb, int V, int d, float *x, cudaStream_t st) {
+    if (M <= 0) return;
+    embed_kernel<<<M, 128, 0, st>>>(rows, M, tok, tok_cap, chain_tok, t_max, n_max, emb, V, d, x);
+    RS_LAUNCHED();
+}
+
+void k_rmsnorm(const float *x, int ldx, const float *w, int M, int d, float eps, bf16 *out, int ldo, cudaStream_t st) {
+    if (M <= 0) return;
+    rmsnorm_kernel<float><<<(M + 7) / 8, 256, 0, st>>>(x, ldx, w, M, d, eps, out, ldo);
+    RS_LAUNCHED();
+}
+
+void k_rmsnorm_bf16(const bf16 *x, int ldx, const float *w, int M, int d, float eps, bf16 *out, int ldo,
+                    cudaStream_t st) {
+    if (M <= 0) return;
+    rmsnorm_kernel<bf16><<<(M + 7) / 8, 256, 0, st>>>(x, ldx, w, M, d, eps, out, ldo);
+    RS_LAUNCHED();
+}
+
+void k_rope_store(const bf16 *qkv, const RowDesc *rows, int M, const TfShape &s, const float *rope, const KvCache &kv,
+                  int layer, bf16 *q, cudaStream_t st) {
+    if (M <= 0) return;
+    rope_store_kernel<<<M, 256, 0, st>>>(qkv, rows, M, s.H, s.KV, s.hd, rope, kv, layer, q);
+    RS_LAUNCHED();
+}
+
+void k_store_features(const float *x, const RowDesc *rows, int M, int d, bf16 *feat, int max_ctx, int slot,
+                      cudaStream_t st) {
+    if (M <= 0) return;
+    store_features_kernel<<<M, 256, 0, st>>>(x, rows, M, d, feat, max_ctx, slot);
+    RS_LAUNCHED();
+}
+
+void k_gather_features(const RowDesc *rows, int M, int d, const bf16 *feat, int max_ctx, const float *, bf16 *fin,
+                       int *, cudaStream_t st) {
+    if (M <= 0) return;
+    gather_features_kernel<<<M, 256, 0, st>>>(rows, M, d, feat, max_ctx, fin);
+    RS_LAUNCHED();
+}
+
+void k_rows_copy_f32(const float *src, int ld_src, const int *src_rows, float *dst, int ld_dst, const int *dst_rows,
+                     int n, int d, cudaStream_t st) {
+    if (n <= 0) return;
+    rows_copy_kernel<<<n, 256, 0, st>>>(src, ld_src, src_rows, dst, ld_dst, dst_rows, d);
+    RS_LAUNCHED();
+}
+
+void k_compact(const SdDev &d, const int32_t *rsel, const int32_t *racc, const int32_t *rbase, const KvCache &kv,
+               bf16 *feat, int feat_w, int max_ctx, cudaStream_t st) {
+    if (d.nact <= 0) return;
+    compact_kernel<<<dim3(d.nact, d.n), 256, 0, st>>>(d, rsel, racc, rbase, kv, feat, feat_w, max_ctx);
+    RS_LAUNCHED();
+}
+
+// ---- weights ------------------------------------------------------------------------------------
+namespace {
+struct Carver {
+    char *base;
+    size_t off = 0;
+    template <class T>
+    T *take(size_t n) {
+        off = (off + 255) & ~size_t(255);
+        T *p = reinterpret_cast<T *>(base + off);
+        off += n * sizeof(T);
+        return p;
+    }
+};
+
+size_t layer_bytes(const TfShape &s, int d_in) {
+    const size_t q = s.qkv_dim();
+    return (q * d_in + q + (size_t)s.d * s.H * s.hd + 2 * (size_t)s.dff * s.d + (size_t)s.d * s.dff) * 2 +
+           (size_t)(d_in + s.d) * 4 + 8 * 256;
+}
+
+void carve_layer(Carver &c, LayerW &w, const TfShape &s, int d_in) {
+    const size_t q = s.qkv_dim();
+    w.qkv_w = c.take<bf16>(q * d_in);
+    w.qkv_b = c.take<bf16>(q);
+    w.o_w = c.take<bf16>((size_t)s.d * s.H * s.hd);
+    w.gu_w = c.take<bf16>(2 * (size_t)s.dff * s.d);
+    w.down_w = c.take<bf16>((size_t)s.d * s.dff);
+    w.ln1 = c.take<float>(d_in);
+    w.ln2 = c.take<float>(s.d);
+}
+
+void init_layer(LayerW &w, const TfShape &s, int d_in, uint64_t seed, uint64_t tid, cudaStream_t st) {
+    const size_t q = s.qkv_dim();
+    k_init_normal(w.qkv_w, q * d_in, seed, tid + 0, s.std, st);
+    k_init_normal(w.qkv_b, q, seed, tid + 1, s.std, st);
+    k_init_normal(w.o_w, (size_t)s.d * s.H * s.hd, seed, tid + 2, s.std, st);
+    k_init_normal(w.gu_w, 2 * (size_t)s.dff * s.d, seed, tid + 3, s.std, st);
+    k_init_normal(w.down_w, (size_t)s.d * s.dff, seed, tid + 4, s.std, st);
+    k_fill_f32(w.ln1, d_in, 1.0f, st);
+    k_fill_f32(w.ln2, s.d, 1.0f, st);
+}
+}  // namespace
+
+void init_transformer(TransformerModel &m, uint64_t seed, cudaStream_t st) {
+    const TfShape &s = m.s;
+    size_t bytes = (size_t)s.V * s.d * 2 + (size_t)s.L * layer_bytes(s, s.d) + (size_t)s.d * 4 +
+                   (size_t)s.max_ctx * s.hd * 4 + 4096;
+    m.arena.alloc(bytes);
+    Carver c{m.arena.p};
+    m.emb = c.take<bf16>((size_t)s.V * s.d);
+    m.layers.resize(s.L);
+    for (auto &l : m.layers) carve_layer(c, l, s, s.d);
+    m.final_norm = c.take<float>(s.d);
+    m.rope = c.take<float>((size_t)s.max_ctx * s.hd);
+    k_init_normal(m.emb, (size_t)s.V * s.d, seed, 1, s.std, st);
+    for (int l = 0; l < s.L; ++l) init_layer(m.layers[l], s, s.d, seed, 16 + 8 * l, st);
+    k_fill_f32(m.final_norm, s.d, 1.0f, st);
+    k_rope_table(m.rope, s.max_ctx, s.hd, s.rope_theta, st);
+    // EAGLE-3 feature layers: low / mid / high hidden states
+    m.feat_layers[0] = std::min(1, s.L - 1);
+    m.feat_layers[1] = s.L / 2;
+    m.feat_layers[2] = s.L - 1;
+    const size_t q = s.qkv_dim();
+    m.n_params = (size_t)s.V * s.d + (size_t)s.L * (q * s.d + q + (size_t)s.d * s.H * s.hd + 3 * (size_t)s.dff * s.d);
+}
+
+void init_drafter(DrafterModel &m, uint64_t seed, cudaStream_t st) {
+    const TfShape &s = m.s;
+    size_t bytes = (size_t)s.d * 3 * s.d * 2 + 2 * (size_t)s.d * 4 + layer_bytes(s, 2 * s.d) + (size_t)s.d * 4 +
+                   (size_t)s.V * s.d * 2 + 4096;
+    m.arena.alloc(bytes);
+    Carver c{m.arena.p};
+    m.fc_w = c.take<bf16>((size_t)s.d * 3 * s.d);
+    m.norm_emb = c.take<float>(s.d);
+    m.norm_hid = c.take<float>(s.d);
+    carve_layer(c, m.layer, s, 2 * s.d);
+    m.final_norm = c.take<float>(s.d);
+    m.lm_w = c.take<bf16>((size_t)s.V * s.d);
+    k_init_normal(m.fc_w, (size_t)s.d * 3 * s.d, seed, 1001, s.std, st);
+    k_fill_f32(m.norm_emb, s.d, 1.0f, st);
+    k_fill_f32(m.norm_hid, s.d, 1.0f, st);
+    init_layer(m.layer, s, 2 * s.d, seed, 1010, st);
+    k_fill_f32(m.final_norm, s.d, 1.0f, st);
+    k_init_normal(m.lm_w, (size_t)s.V * s.d, seed, 1020, s.std, st);
+    const size_t q = s.qkv_dim();
+    m.n_params = (size_t)s.d * 3 * s.d + q * 2 * s.d + q + (size_t)s.d * s.H * s.hd + 3 * (size_t)s.dff * s.d +
+                 (size_t)s.V * s.d;
+}
+
+}  // namespace rs

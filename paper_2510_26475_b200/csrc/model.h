@@ -1,0 +1,113 @@
+// model.h -- Qwen2-shaped target and EAGLE-3-style drafter held in HBM (bf16 weights), and
+// the device kernels of their forwards (model.cu, attention.cu).
+#pragma once
+#include <cuda_bf16.h>
+
+#include <vector>
+
+#include "engine.h"
+
+namespace rs {
+
+using bf16 = __nv_bfloat16;
+
+struct TfShape {
+    int V = 0, d = 0, L = 0, H = 0, KV = 0, hd = 0, dff = 0, max_ctx = 0;
+    float rope_theta = 1e6f, eps = 1e-6f, std = 0.02f, logit_scale = 1.0f;
+    int qkv_dim() const { return (H + 2 * KV) * hd; }
+};
+
+struct LayerW {
+    bf16 *qkv_w = nullptr;   // [(H+2KV)*hd, d_in]
+    bf16 *qkv_b = nullptr;   // [(H+2KV)*hd]
+    bf16 *o_w = nullptr;     // [d, H*hd]
+    bf16 *gu_w = nullptr;    // [2*dff, d], 256-row blocks of [128 gate, 128 up]
+    bf16 *down_w = nullptr;  // [d, dff]
+    float *ln1 = nullptr;    // [d_in]
+    float *ln2 = nullptr;    // [d]
+};
+
+// Qwen2 decoder stack: embed -> L x (RMSNorm, QKV+bias, RoPE, GQA attention, O, RMSNorm,
+// SwiGLU MLP) -> RMSNorm -> tied LM head. Hidden states after three layers (low/mid/high)
+// are the EAGLE-3 features the drafter consumes.
+struct TransformerModel : rs_model {
+    TfShape s;
+    DBuf<char> arena;          // all weights
+    bf16 *emb = nullptr;       // [V, d] (tied LM head)
+    std::vector<LayerW> layers;
+    float *final_norm = nullptr;
+    float *rope = nullptr;     // [max_ctx][hd/2][2] cos, sin
+    int feat_layers[3] = {0, 0, 0};
+    size_t n_params = 0;
+    TransformerModel() : rs_model(Transformer) {}
+};
+
+// EAGLE-3-style drafter: f = fc([g_low, g_mid, g_high]) (or its own previous hidden state
+// when drafting deeper), one decoder layer over [RMSNorm(emb(tok)), RMSNorm(f)], own LM head.
+struct DrafterModel : rs_model {
+    TfShape s;                 // same d / heads as the target, L = 1
+    const TransformerModel *target = nullptr;
+    DBuf<char> arena;
+    bf16 *fc_w = nullptr;      // [d, 3d]
+    float *norm_emb = nullptr, *norm_hid = nullptr;  // [d]
+    LayerW layer;              // qkv_w: [(H+2KV)*hd, 2d]
+    float *final_norm = nullptr;
+    bf16 *lm_w = nullptr;      // [V, d]
+    size_t n_params = 0;
+    DrafterModel() : rs_model(Drafter) {}
+};
+
+void init_transformer(TransformerModel &m, uint64_t seed, cudaStream_t st);
+TransformerModel *create_transformer(rs_ctx *ctx, const rs_transformer_shape &sh, uint64_t seed);
+DrafterModel *create_drafter(rs_ctx *ctx, const rs_model *target, uint64_t seed, int version);
+void init_drafter(DrafterModel &m, uint64_t seed, cudaStream_t st);
+
+// One query/update row of a forward pass.
+struct RowDesc {
+    int seq;     // request id
+    int pos;     // logical position (RoPE, causal mask)
+    int phys;    // physical KV slot written by this row
+    int kind;    // 0: token = tok[seq][pos]; 1: token = chain_tok[seq][chain][cj]
+    int chain;   // chain for kind 1 / key mapping (-1: plain causal over the cache)
+    int cj;      // chain index of the token for kind 1
+    int fsrc;    // drafter feature source: 0 target features at pos-1, 1 drafter hidden (seq, chain) slot
+    int fidx;    // hidden-slot index for fsrc == 1
+};
+
+// One attention work item: up to 64/G consecutive rows sharing a key mapping.
+struct AttnItem {
+    int seq, row0, nrows, maxpos;
+    int chain, ltree, tbase, nstride;  // keys at logical p >= ltree map to tbase + chain*nstride + (p-ltree)
+};
+
+struct KvCache {
+    bf16 *k = nullptr, *v = nullptr;  // [layer][B][KV][max_ctx][hd]
+    int layers = 0, B = 0, KV = 0, max_ctx = 0, hd = 0;
+    __host__ __device__ size_t off(int layer, int seq, int kvh, int phys) const {
+        return ((((size_t)layer * B + seq) * KV + kvh) * max_ctx + phys) * hd;
+    }
+};
+
+// kernels (model.cu)
+void k_embed(const RowDesc *rows, int M, const int32_t *tok, int tok_cap, const int32_t *chain_tok, int t_max,
+             int n_max, const bf16 *emb, int V, int d, float *x, cudaStream_t st);
+void k_rmsnorm(const float *x, int ldx, const float *w, int M, int d, float eps, bf16 *out, int ldo, cudaStream_t st);
+void k_rmsnorm_bf16(const bf16 *x, int ldx, const float *w, int M, int d, float eps, bf16 *out, int ldo,
+                    cudaStream_t st);
+void k_rope_store(const bf16 *qkv, const RowDesc *rows, int M, const TfShape &s, const float *rope, const KvCache &kv,
+                  int layer, bf16 *q, cudaStream_t st);
+void k_attention(const bf16 *q, const RowDesc *rows, const AttnItem *items, int n_items, const KvCache &kv, int layer,
+                 const TfShape &s, bf16 *out, cudaStream_t st);
+void k_store_features(const float *x, const RowDesc *rows, int M, int d, bf16 *feat, int max_ctx, int slot,
+                      cudaStream_t st);
+void k_gather_features(const RowDesc *rows, int M, int d, const bf16 *feat, int max_ctx, const float *hid, bf16 *fin,
+                       int *use_hidden, cudaStream_t st);
+void k_rows_copy_f32(const float *src, int ld_src, const int *src_rows, float *dst, int ld_dst, const int *dst_rows,
+                     int n, int d, cudaStream_t st);
+void k_init_normal(bf16 *p, size_t n, uint64_t seed, uint64_t tensor_id, float std, cudaStream_t st);
+void k_fill_f32(float *p, size_t n, float v, cudaStream_t st);
+void k_rope_table(float *rope, int max_ctx, int hd, float theta, cudaStream_t st);
+void k_compact(const SdDev &d, const int32_t *rsel, const int32_t *racc, const int32_t *rbase, const KvCache &kv,
+               bf16 *feat, int feat_w, int max_ctx, cudaStream_t st);
+
+}  // namespace rs

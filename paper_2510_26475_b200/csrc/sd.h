@@ -38,6 +38,7 @@ struct SdDev {
     // cycle state [B]
     int32_t *n_eff, *d_used, *a_used, *cont, *ended, *accept_len, *drafted, *emitted, *n_rounds;
     int32_t *round_cost;     // [B][kMaxRounds][3]
+    int32_t *rsel, *racc;    // this round's selected chain (-1 none) and accepted drafted count (K4)
     // draft tree [B][t_max][n_max]
     int32_t *chain_tok, *chain_len, *chain_stop, *chain_off;
     int32_t t_max, n_max;

@@ -248,6 +248,8 @@ __global__ void round_setup_kernel(SdDev d, int round) {
         ne = rem < 2 ? (round == 0 ? 0 : -1) : min(d.n, rem - 1);
     }
     d.n_eff[r] = ne;
+    d.rsel[r] = -1;
+    d.racc[r] = 0;
     for (int i = 0; i < d.t; ++i) {
         const size_t ci = (size_t)r * d.t_max + i;
         d.chain_len[ci] = 0;
@@ -368,6 +370,8 @@ __global__ void __launch_bounds__(1024, 1) accept_kernel(SdDev d, int round, int
     if (ne < 0) return;
     int acur = d.a_used[r];
     int alen = d.accept_len[r];
+    const int alen0 = alen;
+    int sel_out = -1;
     int cont = 0;
     const int t = d.t, n = d.n;
     const int *ctok = d.chain_tok + (size_t)r * d.t_max * d.n_max;
@@ -445,6 +449,7 @@ __global__ void __launch_bounds__(1024, 1) accept_kernel(SdDev d, int round, int
                 goto done;
             }
         }
+        sel_out = sel;
         const int *chain = ctok + (size_t)sel * d.n_max;
         const int L = clen[sel];
         emit(d, q, chain[0], p1, s1, true, log(prob(q1, t1, chain[0])), ended);
@@ -509,6 +514,8 @@ done:
         d.emitted[r] += emitted;
         d.ended[r] = ended;
         d.cont[r] = cont && !ended;
+        d.rsel[r] = sel_out;
+        d.racc[r] = alen - alen0;
     }
 }
 

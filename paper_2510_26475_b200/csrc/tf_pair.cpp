@@ -1,0 +1,458 @@
+// tf_pair.cpp -- the transformer ModelPair: drafter tree expansion (K1), tree-verify forward
+// (K2) and KV compaction (K4) for one BatchEngine, plus the constructors of the transformer
+// target and the EAGLE-3-style drafter.
+//
+// KV invariant per request: after every engine step the target cache holds positions
+// 0..len-2 and the newest token (the root of the next round) is not yet processed. A round's
+// verify forward writes the root at len-1 and chain i's depth-j token at the tree slot
+// len + i*n + j (logical position len + j); K4 then moves the accepted chain's slots to
+// len..len+a-1. The drafter cache is caught up lazily: its depth-0 forward processes every
+// position it has not seen (all of them at the first spec cycle -- the reference's "drafter
+// prefill on off->on", server.cpp:280-290) with the target's low/mid/high features at p-1.
+//
+// Row / attention-item descriptors are built on the host (the host knows every request's
+// length from the previous step's summary) and staged through a pinned arena that is only
+// recycled after the engine's end-of-step synchronisation, so no async copy ever reads a
+// host buffer that has been overwritten.
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+
+#include "common.cuh"
+#include "gemm.h"
+#include "model.h"
+
+namespace rs {
+
+namespace {
+
+struct Staging {
+    char *base = nullptr;
+    size_t cap = 0, off = 0;
+    void alloc(size_t bytes) {
+        cap = bytes;
+        RS_CUDA(cudaMallocHost(&base, bytes));
+    }
+    ~Staging() {
+        if (base) cudaFreeHost(base);
+    }
+    template <class T>
+    void upload(T *dst_dev, const std::vector<T> &v, cudaStream_t st) {
+        if (v.empty()) return;
+        const size_t bytes = v.size() * sizeof(T);
+        off = (off + 15) & ~size_t(15);
+        if (off + bytes > cap) {  // arena full: drain the stream, then recycle
+            RS_CUDA(cudaStreamSynchronize(st));
+            off = 0;
+            if (bytes > cap) throw std::runtime_error("staging arena too small");
+        }
+        std::memcpy(base + off, v.data(), bytes);
+        RS_CUDA(cudaMemcpyAsync(dst_dev, base + off, bytes, cudaMemcpyHostToDevice, st));
+        off += bytes;
+    }
+};
+
+struct Workspace {
+    int Mcap = 0;
+    DBuf<float> x, e32;
+    DBuf<bf16> xn, qkv, q, ao, h, fin;
+    DBuf<RowDesc> rows;
+    DBuf<AttnItem> items;
+    DBuf<int32_t> map_a, map_b, idx;
+    void alloc(int M, const TfShape &s) {
+        Mcap = M;
+        x.alloc((size_t)M * s.d);
+        e32.alloc((size_t)M * s.d);
+        xn.alloc((size_t)M * 2 * s.d);
+        qkv.alloc((size_t)M * s.qkv_dim());
+        q.alloc((size_t)M * s.H * s.hd);
+        ao.alloc((size_t)M * s.H * s.hd);
+        h.alloc((size_t)M * s.dff);
+        fin.alloc((size_t)M * 3 * s.d);
+        rows.alloc(M);
+        items.alloc(M);
+        map_a.alloc(M);
+        map_b.alloc(M);
+        idx.alloc((size_t)2 * M);
+    }
+};
+
+void gemm(const void *A, int lda, const void *B, int M, int N, int K, GemmEpi epi, cudaStream_t st) {
+    GemmArgs g;
+    g.A = A;
+    g.B = B;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.lda = lda;
+    g.ldb = K;
+    g.epi = epi;
+    gemm_bf16(g, st);
+}
+
+GemmEpi epi_bf16(void *out, int ldo, const void *bias = nullptr) {
+    GemmEpi e;
+    e.kind = kEpiBF16;
+    e.out = out;
+    e.ldo = ldo;
+    e.bias = bias;
+    return e;
+}
+GemmEpi epi_resid(float *out, int ldo) {
+    GemmEpi e;
+    e.kind = kEpiResidual;
+    e.out = out;
+    e.ldo = ldo;
+    return e;
+}
+GemmEpi epi_swiglu(void *out, int ldo) {
+    GemmEpi e;
+    e.kind = kEpiSwiGLU;
+    e.out = out;
+    e.ldo = ldo;
+    return e;
+}
+GemmEpi epi_f32(float *out, int ldo, float scale, const int *row_map) {
+    GemmEpi e;
+    e.kind = kEpiF32;
+    e.out = out;
+    e.ldo = ldo;
+    e.scale = scale;
+    e.row_map = row_map;
+    return e;
+}
+
+// Host-side description of one forward launch.
+struct Batch {
+    std::vector<RowDesc> rows;
+    std::vector<AttnItem> items;
+    std::vector<int32_t> map_a, map_b;
+    void clear() {
+        rows.clear();
+        items.clear();
+        map_a.clear();
+        map_b.clear();
+    }
+    // attention items over rows [r0, r1) of one sequence sharing one key mapping
+    void add_items(int r0, int r1, int per, int chain, int ltree, int tbase, int nstride) {
+        for (int a = r0; a < r1; a += per) {
+            const int b = std::min(r1, a + per);
+            int maxpos = 0;
+            for (int k = a; k < b; ++k) maxpos = std::max(maxpos, rows[k].pos);
+            items.push_back(AttnItem{rows[a].seq, a, b - a, maxpos, chain, ltree, tbase, nstride});
+        }
+    }
+    int M() const { return static_cast<int>(rows.size()); }
+};
+
+struct TransformerPair : ModelPair {
+    rs_ctx *ctx;
+    rs_engine *eng;
+    const TransformerModel *tgt;
+    const DrafterModel *drf = nullptr;
+    TfShape s;
+    int B = 0, slots_max = 1, max_ctx = 0, per_item = 8;
+    KvCache kv_t, kv_d;
+    DBuf<bf16> kt, vt, kd, vd, feat;
+    DBuf<float> dh;  // drafter hidden per (request, chain) [B][t_max][d]
+    DBuf<int32_t> rbase;
+    Workspace w;
+    Staging stage;
+    Batch bt;
+    std::vector<int> dkv_len;  // drafter cache valid for positions < dkv_len
+
+    TransformerPair(rs_ctx *c, rs_engine *e, const TransformerModel *t, const DrafterModel *d)
+        : ctx(c), eng(e), tgt(t), drf(d), s(t->s) {}
+
+    RowType row_type() const override { return RowType::F32; }
+    void begin_step() override { stage.off = 0; }
+
+    void set_drafter(const rs_model *m) override {
+        if (m && m->kind != rs_model::Drafter) throw std::invalid_argument("transformer target needs an EAGLE drafter");
+        const auto *dm = static_cast<const DrafterModel *>(m);
+        if (dm && dm->target != tgt) throw std::invalid_argument("drafter is bound to a different target");
+        if (dm != drf) std::fill(dkv_len.begin(), dkv_len.end(), 0);  // new snapshot: rebuild its cache
+        drf = dm;
+    }
+
+    void setup(int n_req, int slots, const std::vector<int> &plen, int tok_cap, int t_max) {
+        B = std::max(n_req, 1);
+        slots_max = slots;
+        max_ctx = s.max_ctx;
+        per_item = std::max(1, 64 / (s.H / s.KV));
+        for (int i = 0; i < n_req; ++i)
+            if (plen[i] < 1) throw std::invalid_argument("transformer engine: prompts must be non-empty");
+        if (tok_cap + slots > max_ctx)
+            throw std::invalid_argument("transformer engine: prompt + max_len + draft tree exceeds max_ctx");
+        const size_t kv_elems = (size_t)s.L * B * s.KV * max_ctx * s.hd;
+        kt.alloc(kv_elems);
+        vt.alloc(kv_elems);
+        kv_t = KvCache{kt.p, vt.p, s.L, B, s.KV, max_ctx, s.hd};
+        const size_t kvd = (size_t)B * s.KV * max_ctx * s.hd;
+        kd.alloc(kvd);
+        vd.alloc(kvd);
+        kv_d = KvCache{kd.p, vd.p, 1, B, s.KV, max_ctx, s.hd};
+        feat.alloc((size_t)B * max_ctx * 3 * s.d);
+        dh.alloc((size_t)B * t_max * s.d);
+        rbase.alloc(B);
+        w.alloc(std::max(B * slots_max, 2048), s);
+        stage.alloc(std::max<size_t>(16u << 20, (size_t)w.Mcap * 64 * 8));
+        dkv_len.assign(n_req, 0);
+    }
+
+    void upload(const Batch &b, cudaStream_t st) {
+        if (b.M() > w.Mcap) throw std::runtime_error("forward batch exceeds workspace");
+        stage.upload(w.rows.p, b.rows, st);
+        stage.upload(w.items.p, b.items, st);
+        stage.upload(w.map_a.p, b.map_a, st);
+        stage.upload(w.map_b.p, b.map_b, st);
+    }
+
+    // Target decoder stack over rows embedded in w.x; optional LM head (row m -> map_a[m]).
+    void target_forward(const SdDev &d, int M, int ni, float *logits, bool use_map, cudaStream_t st) {
+        const int qd = s.qkv_dim(), HD = s.H * s.hd;
+        k_embed(w.rows.p, M, d.tok, d.tok_cap, d.chain_tok, d.t_max, d.n_max, tgt->emb, s.V, s.d, w.x.p, st);
+        int fslot = 0;
+        for (int l = 0; l < s.L; ++l) {
+            const LayerW &lw = tgt->layers[l];
+            k_rmsnorm(w.x.p, s.d, lw.ln1, M, s.d, s.eps, w.xn.p, s.d, st);
+            gemm(w.xn.p, s.d, lw.qkv_w, M, qd, s.d, epi_bf16(w.qkv.p, qd, lw.qkv_b), st);
+            k_rope_store(w.qkv.p, w.rows.p, M, s, tgt->rope, kv_t, l, w.q.p, st);
+            k_attention(w.q.p, w.rows.p, w.items.p, ni, kv_t, l, s, w.ao.p, st);
+            gemm(w.ao.p, HD, lw.o_w, M, s.d, HD, epi_resid(w.x.p, s.d), st);
+            k_rmsnorm(w.x.p, s.d, lw.ln2, M, s.d, s.eps, w.xn.p, s.d, st);
+            gemm(w.xn.p, s.d, lw.gu_w, M, 2 * s.dff, s.d, epi_swiglu(w.h.p, s.dff), st);
+            gemm(w.h.p, s.dff, lw.down_w, M, s.d, s.dff, epi_resid(w.x.p, s.d), st);
+            while (fslot < 3 && tgt->feat_layers[fslot] == l)
+                k_store_features(w.x.p, w.rows.p, M, s.d, feat.p, max_ctx, fslot++, st);
+        }
+        if (logits) {
+            k_rmsnorm(w.x.p, s.d, tgt->final_norm, M, s.d, s.eps, w.xn.p, s.d, st);
+            gemm(w.xn.p, s.d, tgt->emb, M, s.V, s.d,
+                 epi_f32(logits, s.V, s.logit_scale, use_map ? w.map_a.p : nullptr), st);
+        }
+    }
+
+    // EAGLE drafter layer over rows whose residual input f is in w.x.
+    void drafter_layer(const SdDev &d, int M, int ni, cudaStream_t st) {
+        const int qd = s.qkv_dim(), HD = s.H * s.hd, d2 = 2 * s.d;
+        k_embed(w.rows.p, M, d.tok, d.tok_cap, d.chain_tok, d.t_max, d.n_max, tgt->emb, s.V, s.d, w.e32.p, st);
+        k_rmsnorm(w.e32.p, s.d, drf->norm_emb, M, s.d, s.eps, w.xn.p, d2, st);
+        k_rmsnorm(w.x.p, s.d, drf->norm_hid, M, s.d, s.eps, w.xn.p + s.d, d2, st);
+        gemm(w.xn.p, d2, drf->layer.qkv_w, M, qd, d2, epi_bf16(w.qkv.p, qd, drf->layer.qkv_b), st);
+        k_rope_store(w.qkv.p, w.rows.p, M, drf->s, tgt->rope, kv_d, 0, w.q.p, st);
+        k_attention(w.q.p, w.rows.p, w.items.p, ni, kv_d, 0, drf->s, w.ao.p, st);
+        gemm(w.ao.p, HD, drf->layer.o_w, M, s.d, HD, epi_resid(w.x.p, s.d), st);
+        k_rmsnorm(w.x.p, s.d, drf->layer.ln2, M, s.d, s.eps, w.xn.p, s.d, st);
+        gemm(w.xn.p, s.d, drf->layer.gu_w, M, 2 * s.dff, s.d, epi_swiglu(w.h.p, s.dff), st);
+        gemm(w.h.p, s.dff, drf->layer.down_w, M, s.d, s.dff, epi_resid(w.x.p, s.d), st);
+    }
+
+    // LM head of the drafter on n selected rows of w.x (src rows, Q destination rows).
+    void drafter_head(const int32_t *src_dev, const int32_t *dst_dev, int n, float *Q, cudaStream_t st) {
+        float *g = w.e32.p;  // gathered rows
+        k_rows_copy_f32(w.x.p, s.d, src_dev, g, s.d, nullptr, n, s.d, st);
+        k_rmsnorm(g, s.d, drf->final_norm, n, s.d, s.eps, w.xn.p, s.d, st);
+        gemm(w.xn.p, s.d, drf->lm_w, n, s.V, s.d, epi_f32(Q, s.V, s.logit_scale, dst_dev), st);
+    }
+
+    // ---- ModelPair hooks ---------------------------------------------------------------------
+    void draft_rows(const SdDev &d, int depth, cudaStream_t st) override {
+        if (!drf) throw std::runtime_error("BatchEngine: spec mode requires a drafter snapshot");
+        const int nact = d.nact;
+        float *Q = static_cast<float *>(const_cast<void *>(d.Q));
+        if (depth == 0) {
+            // catch-up rows [dkv_len, len-1] per request; the last one is the round root.
+            int a0 = 0;
+            while (a0 < nact) {
+                bt.clear();
+                std::vector<int32_t> head_src, head_dst, hid_src, hid_dst;
+                int a = a0;
+                for (; a < nact; ++a) {
+                    const int r = eng->active[a];
+                    const int L = eng->len[r];
+                    const int from = std::min(dkv_len[r], L - 1);
+                    if (bt.M() + (L - from) > w.Mcap) {
+                        if (bt.M() == 0) throw std::runtime_error("drafter catch-up exceeds workspace");
+                        break;
+                    }
+                    const int r0 = bt.M();
+                    for (int p = from; p < L; ++p) bt.rows.push_back(RowDesc{r, p, p, 0, -1, 0, 0, 0});
+                    bt.add_items(r0, bt.M(), per_item, -1, 0, 0, 0);
+                    head_src.push_back(bt.M() - 1);
+                    head_dst.push_back(a * d.slots);
+                    for (int i = 0; i < d.t; ++i) {
+                        hid_src.push_back(bt.M() - 1);
+                        hid_dst.push_back(r * d.t_max + i);
+                    }
+                    dkv_len[r] = L;
+                }
+                bt.map_a = head_src;
+                bt.map_b = head_dst;
+                upload(bt, st);
+                std::vector<int32_t> hid(hid_src);
+                hid.insert(hid.end(), hid_dst.begin(), hid_dst.end());
+                stage.upload(w.idx.p, hid, st);
+                const int M = bt.M();
+                k_gather_features(w.rows.p, M, s.d, feat.p, max_ctx, nullptr, w.fin.p, nullptr, st);
+                gemm(w.fin.p, 3 * s.d, drf->fc_w, M, s.d, 3 * s.d, epi_f32(w.x.p, s.d, 1.0f, nullptr), st);
+                drafter_layer(d, M, (int)bt.items.size(), st);
+                drafter_head(w.map_a.p, w.map_b.p, (int)head_src.size(), Q, st);
+                const int nh = (int)hid_src.size();
+                k_rows_copy_f32(w.x.p, s.d, w.idx.p, dh.p, s.d, w.idx.p + nh, nh, s.d, st);
+                a0 = a;
+            }
+            return;
+        }
+        // depth j: one row per (request, chain); token chain_i[j-1] at logical len-1+j
+        bt.clear();
+        for (int a = 0; a < nact; ++a) {
+            const int r = eng->active[a];
+            const int L = eng->len[r];
+            for (int i = 0; i < d.t; ++i) {
+                bt.rows.push_back(RowDesc{r, L - 1 + depth, L + i * d.n + depth - 1, 1, i, depth - 1, 1, r * d.t_max + i});
+                bt.add_items(bt.M() - 1, bt.M(), 1, i, L, L, d.n);
+                bt.map_a.push_back(r * d.t_max + i);                 // hidden slot in / out
+                bt.map_b.push_back(a * d.slots + 1 + i * d.n + depth);  // Q row
+            }
+        }
+        upload(bt, st);
+        const int M = bt.M();
+        k_rows_copy_f32(dh.p, s.d, w.map_a.p, w.x.p, s.d, nullptr, M, s.d, st);
+        drafter_layer(d, M, (int)bt.items.size(), st);
+        k_rmsnorm(w.x.p, s.d, drf->final_norm, M, s.d, s.eps, w.xn.p, s.d, st);
+        gemm(w.xn.p, s.d, drf->lm_w, M, s.V, s.d, epi_f32(Q, s.V, s.logit_scale, w.map_b.p), st);
+        k_rows_copy_f32(w.x.p, s.d, nullptr, dh.p, s.d, w.map_a.p, M, s.d, st);
+    }
+
+    void verify_rows(const SdDev &d, bool naive, cudaStream_t st) override {
+        const int nact = d.nact;
+        float *P = static_cast<float *>(const_cast<void *>(d.P));
+        bt.clear();
+        std::vector<int32_t> base(B, 0);
+        for (int a = 0; a < nact; ++a) {
+            const int r = eng->active[a];
+            const int L = eng->len[r];
+            base[r] = L;
+            const int r0 = bt.M();
+            bt.rows.push_back(RowDesc{r, L - 1, L - 1, 0, -1, 0, 0, 0});
+            bt.map_a.push_back(a * d.slots);
+            if (naive) {
+                bt.add_items(r0, bt.M(), per_item, -1, 0, 0, 0);
+                continue;
+            }
+            for (int i = 0; i < d.t; ++i) {
+                const int c0 = bt.M();
+                for (int j = 0; j < d.n; ++j) {
+                    bt.rows.push_back(RowDesc{r, L + j, L + i * d.n + j, 1, i, j, 0, 0});
+                    bt.map_a.push_back(a * d.slots + 1 + i * d.n + j);
+                }
+                // the root rides with chain 0 (identical mapping below ltree)
+                bt.add_items(i == 0 ? r0 : c0, bt.M(), per_item, i, L, L, d.n);
+            }
+        }
+        upload(bt, st);
+        if (!naive) stage.upload(rbase.p, base, st);
+        target_forward(d, bt.M(), (int)bt.items.size(), P, true, st);
+    }
+
+    void after_accept(const SdDev &d, bool naive, cudaStream_t st) override {
+        if (naive) return;
+        k_compact(d, d.rsel, d.racc, rbase.p, kv_t, feat.p, 3 * s.d, max_ctx, st);
+    }
+
+    // Target prefill of prompt positions 0..P-2 (the last prompt token is the first root).
+    void prefill(const std::vector<std::vector<int>> &prompts, const SdDev &d) {
+        cudaStream_t st = ctx->stream;
+        size_t r = 0;
+        int p = 0;
+        while (r < prompts.size()) {
+            bt.clear();
+            while (r < prompts.size() && bt.M() < w.Mcap) {
+                const int P = (int)prompts[r].size();
+                if (p >= P - 1) {
+                    ++r;
+                    p = 0;
+                    continue;
+                }
+                const int take = std::min(P - 1 - p, w.Mcap - bt.M());
+                const int r0 = bt.M();
+                for (int k = 0; k < take; ++k, ++p) bt.rows.push_back(RowDesc{(int)r, p, p, 0, -1, 0, 0, 0});
+                bt.add_items(r0, bt.M(), per_item, -1, 0, 0, 0);
+            }
+            if (bt.M() == 0) break;
+            upload(bt, st);
+            target_forward(d, bt.M(), (int)bt.items.size(), nullptr, false, st);
+            RS_CUDA(cudaStreamSynchronize(st));
+            stage.off = 0;
+        }
+    }
+};
+
+}  // namespace
+
+std::unique_ptr<ModelPair> make_transformer_pair(rs_ctx *ctx, rs_engine *eng, const rs_model *target,
+                                                 const rs_model *drafter, int n_req, int slots_max,
+                                                 const std::vector<int> &prompt_lens,
+                                                 const std::vector<std::vector<int>> &prompts, int tok_cap) {
+    if (target->kind != rs_model::Transformer) throw std::invalid_argument("transformer pair: bad target");
+    if (drafter && drafter->kind != rs_model::Drafter)
+        throw std::invalid_argument("transformer target needs an EAGLE drafter");
+    auto p = std::make_unique<TransformerPair>(ctx, eng, static_cast<const TransformerModel *>(target),
+                                               static_cast<const DrafterModel *>(drafter));
+    if (drafter && static_cast<const DrafterModel *>(drafter)->target != p->tgt)
+        throw std::invalid_argument("drafter is bound to a different target");
+    p->setup(n_req, slots_max, prompt_lens, tok_cap, eng->t_max);
+    p->prefill(prompts, eng->dev(rs_sdconfig{1, 1, 1, 0}, 0));
+    return p;
+}
+
+TransformerModel *create_transformer(rs_ctx *ctx, const rs_transformer_shape &sh, uint64_t seed) {
+    TfShape s;
+    s.V = sh.vocab;
+    s.d = sh.d_model;
+    s.L = sh.n_layers;
+    s.H = sh.n_heads;
+    s.KV = sh.n_kv_heads;
+    s.hd = sh.head_dim;
+    s.dff = sh.d_ff;
+    s.max_ctx = sh.max_ctx;
+    s.rope_theta = sh.rope_theta > 0 ? sh.rope_theta : 1e6f;
+    s.eps = sh.rms_eps > 0 ? sh.rms_eps : 1e-6f;
+    s.std = sh.init_std > 0 ? sh.init_std : 0.02f;
+    s.logit_scale = sh.logit_scale > 0 ? sh.logit_scale : 1.0f;
+    if (s.V < 2 || s.d <= 0 || s.L <= 0 || s.H <= 0 || s.KV <= 0 || s.max_ctx <= 0)
+        throw std::invalid_argument("transformer shape: non-positive dimension");
+    if (s.hd != 128) throw std::invalid_argument("transformer shape: head_dim must be 128");
+    if (s.H % s.KV || s.H / s.KV > 64)
+        throw std::invalid_argument("transformer shape: n_heads must be a multiple of n_kv_heads (group <= 64)");
+    if (s.d % 64 || s.dff % 128) throw std::invalid_argument("transformer shape: d_model % 64 and d_ff % 128 required");
+    if (!(sh.temperature > 0.0)) throw std::invalid_argument("TabularARModel: temperature must be positive");
+    auto m = std::make_unique<TransformerModel>();
+    m->ctx = ctx;
+    m->vocab = s.V;
+    m->temperature = sh.temperature;
+    m->version = 0;
+    m->s = s;
+    init_transformer(*m, seed, ctx->stream);
+    RS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return m.release();
+}
+
+DrafterModel *create_drafter(rs_ctx *ctx, const rs_model *target, uint64_t seed, int version) {
+    if (target->kind != rs_model::Transformer) throw std::invalid_argument("rs_drafter_create: target must be a transformer");
+    const auto *t = static_cast<const TransformerModel *>(target);
+    auto m = std::make_unique<DrafterModel>();
+    m->ctx = ctx;
+    m->vocab = t->vocab;
+    m->temperature = t->temperature;
+    m->version = version;
+    m->target = t;
+    m->s = t->s;
+    m->s.L = 1;
+    init_drafter(*m, seed, ctx->stream);
+    RS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return m.release();
+}
+
+}  // namespace rs
