@@ -183,7 +183,7 @@ SdDev rs_engine::dev(const rs_sdconfig &cfg, int nact) {
     d.eos = V - 1;
     d.tau_p = target->temperature;
     d.tau_q = pending_drafter ? pending_drafter->temperature : target->temperature;
-    d.slots = 1 + d.t * d.n;
+    d.slots = cfg.enabled ? 1 + d.t * d.n : 1;  // rows per active sequence in P / Q
     d.P = d_P.p;
     d.Q = d_Q.p;
     d.verify_mode = verify_mode;

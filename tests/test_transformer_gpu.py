@@ -197,6 +197,6 @@ def test_mode_switch_and_adaptive_table(models):
     while not eng.all_done():
         eng.step()
     assert eng.switches() and eng.prefill_events() >= 1
-    base = run(models, rb.SDConfig.off(), verify_mode="greedy", reqs=make_requests(n=4, max_len=12))
+    base = run(models, rb.SDConfig.off(), verify_mode="greedy", reqs=make_requests(n=4, max_len=16))
     for r, b in zip(eng.requests(), base.requests()):
         assert r.generated == b.generated[:len(r.generated)]
