@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark of the batched speculative-decode rollout step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "cfg2"): Qwen2.5-3B-shaped target + EAGLE-3-style
+drafter with synthetic N(0, 0.02) bf16 weights, 64 rollouts per GPU, tree(s=1, t=4, n=5),
+lossless rejection sampling at T = 1 (the reference's verification rule). A "step" is one
+BatchEngine::step -- one speculative cycle over the whole batch (drafting 5 depths, one tree
+verify forward, fused acceptance, KV compaction). Contexts start at 1664 tokens (128-token
+prompt + 1536 tokens already generated = the mean context of a 3072-token rollout).
+
+Timing: W untimed warm-up steps, then K steps bracketed by barrier + synchronize, device
+time from CUDA events on the engine's stream, max over ranks. Every step streams the 6.2 GB
+of target weights and the KV cache, far more than the 126 MB L2, so no flush is needed.
+N > 1 (torchrun): each rank is an independent engine on its own prompt shard (no
+collective on the generation path); value = total tokens of all ranks / max time.
+"""
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "generated tokens/sec per box (1/2/4/8 B200) + mean accept length vs CPU ref"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--batch", type=int, default=64)
+    p.add_argument("--ctx", type=int, default=1664)
+    p.add_argument("--sd", default="1,4,5", help="s,t,n")
+    p.add_argument("--verify", default="sample", choices=["sample", "greedy"])
+    p.add_argument("--model", default="3b", choices=["3b", "7b", "14b", "tiny"])
+    p.add_argument("--no-profile", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+# ---- clocks (B200_PROFILING.md recipe) -------------------------------------------------------
+class ClockSampler:
+    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for n, v in zip(names, s[5:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ---- CPU reference arm ------------------------------------------------------------------------
+def _cpu_lib():
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_client import Oracle, Reference
+    try:
+        return Reference(), "reference"
+    except (FileNotFoundError, OSError):
+        return Oracle(), "port"
+
+
+def cpu_workload(batch, s, t, n):
+    """The reference's own CPU engine on its own models (tabular V=8 actor + KD-warmed
+    drafter from make_env, the only models the reference implements), same batch and SD
+    config as the GPU arm, eos_bias -3 so rollouts run long (SURVEY.md §6 / BASELINE.md §3)."""
+    lib, kind = _cpu_lib()
+    if kind == "reference":
+        env = lib("make_env", seed=1)
+        target, drafter = env["actor"], env["drafter"]
+        prompts = env["task"]["prompts"]
+    else:  # oracle port: deterministic tabular stand-ins of the same shape
+        import random
+        rng = random.Random(1)
+        target = {"vocab": 8, "order": 2, "logits": [rng.gauss(0, 0.5) for _ in range(512)]}
+        drafter = {"vocab": 8, "order": 1, "logits": [rng.gauss(0, 0.5) for _ in range(64)]}
+        prompts = [[0, 1], [2, 3], [4, 5], [0, 2]]
+    reqs = [{"id": i, "prompt": prompts[i % len(prompts)], "eos_bias": -3.0, "max_len": 256, "seed": 1, "stream": i}
+            for i in range(batch)]
+    forced = {"s": s, "t": t, "n": n, "enabled": True}
+    return lib, kind, target, drafter, reqs, forced
+
+
+def cpu_time(lib, kind, target, drafter, reqs, forced, threads, budget_s):
+    """Repeat the reference run_generation until ~budget_s of wall time; tokens/s."""
+    tok = secs = als = aln = 0
+    runs = 0
+    while secs < budget_s or runs == 0:
+        if kind == "reference":
+            out = lib("time_generation", target=target, drafter=drafter, requests=reqs, forced=forced, threads=threads)
+            tok += out["tokens"]
+            secs += out["seconds"]
+            als += out["accept_len_sum"]
+            aln += out["accept_len_cycles"]
+        else:
+            t0 = time.perf_counter()
+            out = lib("run_generation", target=target, drafter=drafter, requests=reqs, forced=forced,
+                      record_logprobs=False)
+            secs += time.perf_counter() - t0
+            tok += sum(len(x["response"]) for x in out["samples"])
+            als += sum(out["accept_lens"])
+            aln += len(out["accept_lens"])
+        runs += 1
+    return tok / secs, (als / aln if aln else 0.0), runs, secs
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    s, t, n = map(int, args.sd.split(","))
+    lib, kind, target, drafter, reqs, forced = cpu_workload(args.batch, s, t, n)
+    threads = os.cpu_count() if kind == "reference" else 1
+    for _ in range(args.warmup):
+        cpu_time(lib, kind, target, drafter, reqs, forced, threads, 0.0)
+    tok = secs = 0.0
+    al = []
+    for _ in range(args.steps):
+        v, a, runs, sec = cpu_time(lib, kind, target, drafter, reqs, forced, threads, 0.0)
+        tok += v * sec
+        secs += sec
+        al.append(a)
+    value = tok / secs
+    sample = (f"reference run_generation (oracle/_ref, compiled reference core) on TabularARModel V=8 "
+              f"(make_env seed 1: order-2 actor, KD-warmed order-1 drafter), batch {args.batch}, "
+              f"tree({s},{t},{n}), max_len 256, eos_bias -3, {threads} host threads, one generation per step")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "mean_accept_len": statistics.mean(al) if al else 0.0,
+            "config": {"workload": "cfg2 on the reference's CPU engine (tabular models)", "batch_per_gpu": args.batch,
+                       "sd_config": f"s{s}_t{t}_n{n}", "verify": "rejection sampling T=1"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---- GPU arm -------------------------------------------------------------------------------------
+def measured_peaks():
+    for p in [os.path.join(ROOT, "MEASURED_PEAKS.json")]:
+        if os.path.exists(p):
+            with open(p) as f:
+                return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2510_26475_b200 as rb
+
+    s, t, n = map(int, args.sd.split(","))
+    cfg = rb.SDConfig.tree(s, t, n)
+    steps_total = args.warmup + 3 * args.steps + 8
+    max_len = steps_total * (s * n + 1) + 8
+    max_ctx = args.ctx + max_len + s * t * n + 16
+    shape = {"3b": rb.TransformerShape.qwen2_5_3b, "7b": rb.TransformerShape.qwen2_5_7b,
+             "14b": rb.TransformerShape.qwen2_5_14b}.get(args.model)
+    shape = shape(max_ctx=max_ctx) if shape else rb.TransformerShape.tiny(max_ctx=max_ctx)
+    dev = rb.Device(local)
+    stream = torch.cuda.Stream()
+    dev.set_stream(stream.cuda_stream)
+    target = rb.TransformerModel(shape, seed=20251026, device=dev)
+    drafter = rb.EagleDrafter(target, seed=4242, version=1)
+    import random
+    rng = random.Random(1000 + rank)
+    reqs = [rb.RequestState(i, [rng.randrange(shape.vocab - 1) for _ in range(args.ctx)], -20.0, max_len,
+                            rb.DecodeRng.from_seed(7 + rank, i)) for i in range(args.batch)]
+    t_pre = time.perf_counter()
+    eng = rb.BatchEngine(target, lambda: drafter, None, rb.TimingModel(), reqs, cfg, args.verify,
+                         record_full_logprobs=False, device=dev)
+    prefill_s = time.perf_counter() - t_pre
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        eng.step()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    rb.reset_launch_count()
+    e0.record(stream)
+    tokens = accepted = drafted = 0
+    for _ in range(args.steps):
+        info = eng.step()
+        tokens += info.emitted_tokens
+        accepted += info.accepted_drafted
+        drafted += info.drafted_cycles
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = rb.launch_count()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+
+    # end to end through the public API: every step's descriptor uploads + summary readback
+    # (inside step) and a host read of every request's newly generated tokens.
+    barrier()
+    torch.cuda.synchronize()
+    buf = (ctypes.c_int32 * (max_len + 8))()
+    n_out = ctypes.c_int32()
+    seen = [len(r) for r in [[]] * args.batch]
+    for i in range(args.batch):
+        rb._check(rb.lib().rs_engine_response(eng.handle, i, None, 0, ctypes.byref(n_out)))
+        seen[i] = n_out.value
+    t0 = time.perf_counter()
+    e2e_tok = h2d = d2h = 0
+    for _ in range(args.steps):
+        info = eng.step()
+        e2e_tok += info.emitted_tokens
+        h2d += info.h2d_bytes
+        d2h += info.d2h_bytes
+        for i in range(args.batch):
+            rb._check(rb.lib().rs_engine_response(eng.handle, i, buf, max_len + 8, ctypes.byref(n_out)))
+            d2h += 4 * n_out.value
+            seen[i] = n_out.value
+    e2e_s = time.perf_counter() - t0
+
+    prof = {}
+    if not args.no_profile:
+        rb.profile(enable=True, reset=True)
+        for _ in range(min(args.steps, 5)):
+            eng.step()
+        prof = rb.profile(enable=False)
+
+    if world > 1:
+        import torch.distributed as dist
+        vals = torch.tensor([ms, e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        sums = torch.tensor([tokens, accepted, drafted, e2e_tok], dtype=torch.float64, device="cuda")
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        ms, e2e_s = vals.tolist()
+        tokens, accepted, drafted, e2e_tok = sums.tolist()
+    if rank != 0:
+        return
+
+    peaks, peak_kind = measured_peaks()
+    value = tokens / (ms / 1000.0)
+    gemm = {k: v for k, v in prof.items() if k.endswith(".gemm")}
+    roof = None
+    if "verify.gemm" in prof:
+        g = prof["verify.gemm"]
+        achieved = g["flops"] / (g["ms"] / 1000.0) / 1e12
+        peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+        if os.path.exists(tpath):
+            with open(tpath) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": "verify GEMMs (tcgen05 gemm_kernel: QKV, O, gate/up, down, LM head)",
+                "flops_per_launch": g["flops"] / g["launches"], "ms_per_launch": g["ms"] / g["launches"],
+                "peak_source": f"{peak_kind} bf16_tflops_sustained (kernel timed inside a long step)"}
+    breakdown = {k: {"ms_per_step": round(v["ms"] / max(1, min(args.steps, 5)), 3), "launches": v["launches"]}
+                 for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        lib, kind, tgt_j, drf_j, creqs, forced = cpu_workload(args.batch, s, t, n)
+        threads = os.cpu_count() if kind == "reference" else 1
+        v, al, runs, secs = cpu_time(lib, kind, tgt_j, drf_j, creqs, forced, threads, args.cpu_seconds)
+        cpu = {"value": round(v, 1), "unit": "tokens/s", "cores": threads, "kind": kind, "mean_accept_len": al,
+               "sample": f"{runs} x reference run_generation, TabularARModel V=8 (make_env seed 1), batch "
+                         f"{args.batch}, tree({s},{t},{n}), max_len 256, eos_bias -3, {secs:.1f} s wall on "
+                         f"{threads} host threads"}
+
+    line = {"metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "mean_accept_len": round(accepted / drafted, 4) if drafted else 0.0,
+            "tokens_per_step": round(tokens / args.steps, 2),
+            "config": {"workload": "cfg2: Qwen2.5-3B-shaped target + EAGLE-3-style drafter, random init, "
+                                   f"batch {args.batch}/GPU, tree depth {n} top-k {t} (s={s})" if args.model == "3b"
+                                   else f"{args.model} target, batch {args.batch}/GPU, tree({s},{t},{n})",
+                       "model": args.model, "batch_per_gpu": args.batch, "global_batch": args.batch * world,
+                       "sd_config": cfg.key(), "verify": "rejection sampling T=1" if args.verify == "sample"
+                       else "greedy", "ctx_len_start": args.ctx, "parallelism": f"prompt-sharded dp{world}",
+                       "l2": "no flush: each step streams 6.2 GB of weights + KV (>> 126 MB L2)",
+                       "prefill_s": round(prefill_s, 2)},
+            "roofline": roof, "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_tok / e2e_s, 1), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps)},
+            "gpu_launches": launches, "clocks": clk, "breakdown_ms_per_step": breakdown}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

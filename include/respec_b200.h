@@ -91,6 +91,8 @@ typedef struct {
     int32_t accepted_drafted; /* sum of accept_len over those sequences */
     int32_t redraft_passes;   /* extra drafting passes for EOS-truncated chains (sampling) */
     float step_ms;            /* device time of the step, CUDA events on the engine stream */
+    int64_t h2d_bytes;        /* host->device bytes copied during the step (descriptors, active set) */
+    int64_t d2h_bytes;        /* device->host bytes copied during the step (summary, flags) */
 } rs_step_info;
 
 /* Transformer shape (Qwen2-style target; EAGLE-3-style drafter uses the same d/heads). */
@@ -236,6 +238,11 @@ int rs_model_tensor(const rs_model *m, const char *name, int32_t layer, void **d
 int rs_memcpy_d2d(rs_ctx *ctx, void *dst_dev, const void *src_dev, int64_t bytes);
 /* Parameter count of a model (tabular: table size). */
 int rs_model_params(const rs_model *m, int64_t *out);
+/* Per-kernel-class device timing (CUDA events around each launch, this thread only):
+   JSON {"<scope>.<kernel>": {"launches", "ms", "flops", "bytes"}} with algorithmic work. */
+void rs_prof_enable(int32_t on);
+void rs_prof_reset(void);
+int rs_prof_json(char *buf, int64_t cap, int64_t *len);
 
 /* mt19937_64 state helper for rs_kd_update_tabular: 313 uint64 (312 words + index). */
 int rs_mt19937_64_seed(uint64_t seed, uint64_t *state313);

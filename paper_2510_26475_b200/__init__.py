@@ -76,7 +76,8 @@ class _ForwardEvent(ctypes.Structure):
 class _StepInfo(ctypes.Structure):
     _fields_ = [("active_batch", ctypes.c_int32), ("mode", _SDConfig), ("drafter_version", ctypes.c_int32),
                 ("emitted_tokens", ctypes.c_int32), ("drafted_cycles", ctypes.c_int32),
-                ("accepted_drafted", ctypes.c_int32), ("redraft_passes", ctypes.c_int32), ("step_ms", ctypes.c_float)]
+                ("accepted_drafted", ctypes.c_int32), ("redraft_passes", ctypes.c_int32), ("step_ms", ctypes.c_float),
+                ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64)]
 
 
 class _TransformerShape(ctypes.Structure):
@@ -119,7 +120,7 @@ EXPORTED_SYMBOLS = [
     "rs_engine_steps", "rs_engine_step_logprobs", "rs_engine_accept_lens", "rs_engine_destroy",
     "rs_engine_set_capture", "rs_engine_capture_count", "rs_engine_capture_read",
     "rs_kd_weight", "rs_kd_update_tabular", "rs_mt19937_64_seed", "rs_gemm_bf16",
-    "rs_model_tensor", "rs_memcpy_d2d", "rs_model_params",
+    "rs_model_tensor", "rs_memcpy_d2d", "rs_model_params", "rs_prof_enable", "rs_prof_reset", "rs_prof_json",
 ]
 
 _lib = None
@@ -188,6 +189,9 @@ def lib():
             "rs_model_tensor": ([vp, ctypes.c_char_p, i32, P(vp), P(i64)], ctypes.c_int),
             "rs_memcpy_d2d": ([vp, vp, vp, i64], ctypes.c_int),
             "rs_model_params": ([vp, P(i64)], ctypes.c_int),
+            "rs_prof_enable": ([i32], None),
+            "rs_prof_reset": ([], None),
+            "rs_prof_json": ([ctypes.c_char_p, i64, P(i64)], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -251,6 +255,20 @@ def default_device() -> Device:
     if _default_device is None:
         _default_device = Device(0)
     return _default_device
+
+
+def profile(enable: Optional[bool] = None, reset: bool = False):
+    """Per-kernel-class device timings (see rs_prof_json); returns the current totals."""
+    import json
+    if reset:
+        lib().rs_prof_reset()
+    if enable is not None:
+        lib().rs_prof_enable(1 if enable else 0)
+    n = ctypes.c_int64()
+    _check(lib().rs_prof_json(None, 0, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value + 1)
+    _check(lib().rs_prof_json(buf, n.value + 1, ctypes.byref(n)))
+    return json.loads(buf.value.decode())
 
 
 def launch_count() -> int:

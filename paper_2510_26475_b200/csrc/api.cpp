@@ -11,6 +11,7 @@
 #include "gemm.h"
 #include "kd.h"
 #include "model.h"
+#include "prof.h"
 
 namespace {
 thread_local std::string g_err;
@@ -71,7 +72,11 @@ void copy_out(const std::vector<T> &v, T *out, int32_t cap, int32_t *n) {
 }  // namespace
 
 namespace rs {
+thread_local int64_t g_h2d = 0, g_d2h = 0;
 void note_launch() { ++g_launches; }
+void note_copy(bool h2d, size_t bytes) { (h2d ? g_h2d : g_d2h) += (int64_t)bytes; }
+int64_t copy_bytes(bool h2d) { return h2d ? g_h2d : g_d2h; }
+void reset_copy_bytes() { g_h2d = g_d2h = 0; }
 }  // namespace rs
 
 using namespace rs;
@@ -543,6 +548,20 @@ int rs_model_tensor(const rs_model *m, const char *name, int32_t layer, void **p
         if (!p) throw std::invalid_argument("rs_model_tensor: unknown tensor " + nm);
         *ptr = p;
         *bytes = (int64_t)b;
+    });
+}
+
+void rs_prof_enable(int32_t on) { prof_enable(on != 0); }
+void rs_prof_reset(void) { prof_reset(); }
+int rs_prof_json(char *buf, int64_t cap, int64_t *len) {
+    return guard([&] {
+        const std::string s = prof_json();
+        if (len) *len = (int64_t)s.size();
+        if (buf && cap > 0) {
+            const size_t k = std::min<size_t>(s.size(), (size_t)cap - 1);
+            std::memcpy(buf, s.data(), k);
+            buf[k] = 0;
+        }
     });
 }
 

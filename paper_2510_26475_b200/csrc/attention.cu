@@ -15,6 +15,7 @@
 
 #include "common.cuh"
 #include "model.h"
+#include "prof.h"
 
 namespace rs {
 
@@ -224,8 +225,9 @@ __global__ void __launch_bounds__(128) attn_kernel(const bf16 *q, const RowDesc 
 }  // namespace
 
 void k_attention(const bf16 *q, const RowDesc *rows, const AttnItem *items, int n_items, const KvCache &kv, int layer,
-                 const TfShape &s, bf16 *out, cudaStream_t st) {
+                 const TfShape &s, bf16 *out, cudaStream_t st, double flops, double bytes) {
     if (n_items <= 0) return;
+    ProfScope prof("attn", flops, bytes, st);
     if (s.hd != kHD) throw std::invalid_argument("attention: head_dim must be 128");
     static bool attr = false;
     if (!attr) {

@@ -12,6 +12,9 @@ namespace rs {
 struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
 
 void note_launch();  // counts kernel launches (rs_launch_count)
+void note_copy(bool h2d, size_t bytes);  // host<->device traffic accounting (rs_step_info)
+int64_t copy_bytes(bool h2d);
+void reset_copy_bytes();
 
 #define RS_CUDA(call)                                                                              \
     do {                                                                                           \

@@ -10,6 +10,7 @@
 #include <stdexcept>
 
 #include "common.cuh"
+#include "prof.h"
 
 namespace rs {
 
@@ -278,8 +279,10 @@ void rs_engine::step(rs_step_info *info) {
 
     cudaStream_t st = ctx->stream;
     pair->begin_step();
+    reset_copy_bytes();
     for (int a = 0; a < batch; ++a) h_active[a] = active[a];
     RS_CUDA(cudaMemcpyAsync(d_active.p, h_active, batch * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    note_copy(true, batch * sizeof(int32_t));
     RS_CUDA(cudaEventRecord(ctx->ev0, st));
     SdDev d = dev(mode, batch);
     if (enabling) pair->on_spec_enable(d, st);
@@ -292,6 +295,7 @@ void rs_engine::step(rs_step_info *info) {
             sd_round_setup(d, round, st);
             for (;;) {
                 for (int depth = 0; depth < mode.draft_len; ++depth) {
+                    prof_set_scope("draft");
                     pair->draft_rows(d, depth, st);
                     sd_draft_sample(d, depth, rt, st);
                     if (capture) capture_rows(d, false, depth);
@@ -299,13 +303,16 @@ void rs_engine::step(rs_step_info *info) {
                 if (verify_mode == RS_VERIFY_GREEDY || mode.branching == 1) break;
                 sd_redraft_check(d, st);
                 RS_CUDA(cudaMemcpyAsync(h_misc + 1, d_flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+                note_copy(false, sizeof(int32_t));
                 RS_CUDA(cudaStreamSynchronize(st));
                 if (!h_misc[1]) break;
                 RS_CUDA(cudaMemsetAsync(d_flag.p, 0, sizeof(int32_t), st));
                 ++redraft_passes;
             }
+            prof_set_scope("verify");
             pair->verify_rows(d, false, st);
             if (capture) capture_rows(d, true, 0);
+            prof_set_scope("accept");
             sd_accept(d, round, false, rt, st);
             pair->after_accept(d, false, st);
             if (round + 1 < mode.rounds) {
@@ -313,6 +320,7 @@ void rs_engine::step(rs_step_info *info) {
                 std::vector<int32_t> cont(n), lens(n);
                 RS_CUDA(cudaMemcpyAsync(cont.data(), d.cont, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
                 RS_CUDA(cudaMemcpyAsync(lens.data(), d.len, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+                note_copy(false, 2 * n * sizeof(int32_t));
                 RS_CUDA(cudaStreamSynchronize(st));
                 bool any = false;
                 for (int r : active) any |= cont[r] != 0;
@@ -321,6 +329,7 @@ void rs_engine::step(rs_step_info *info) {
             }
         }
     } else {
+        prof_set_scope("naive");
         pair->verify_rows(d, true, st);
         if (capture) capture_rows(d, true, 0);
         sd_accept(d, 0, true, rt, st);
@@ -331,7 +340,10 @@ void rs_engine::step(rs_step_info *info) {
     const int sw = kSummaryFixed + 3 * kMaxRounds;
     RS_CUDA(cudaMemcpyAsync(h_summary, d_summary.p, (size_t)batch * sw * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     RS_CUDA(cudaMemcpyAsync(h_misc, d_err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    note_copy(false, (size_t)batch * sw * sizeof(int32_t) + sizeof(int32_t));
     RS_CUDA(cudaStreamSynchronize(st));
+    prof_collect();
+    prof_set_scope("step");
     if (h_misc[0] != 0) {
         const int code = h_misc[0];
         h_misc[0] = 0;
@@ -385,5 +397,7 @@ void rs_engine::step(rs_step_info *info) {
         info->accepted_drafted = accepted;
         info->redraft_passes = redraft_passes;
         info->step_ms = ms;
+        info->h2d_bytes = copy_bytes(true);
+        info->d2h_bytes = copy_bytes(false);
     }
 }

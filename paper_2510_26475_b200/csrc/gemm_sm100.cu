@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "gemm.h"
+#include "prof.h"
 
 namespace rs {
 
@@ -386,6 +387,9 @@ void gemm_bf16(const GemmArgs &g, cudaStream_t st) {
     if (g.K % 8 || g.lda % 8 || g.ldb % 8) throw std::invalid_argument("gemm_bf16: K and leading dims must be multiples of 8");
     if (g.epi.kind == kEpiSwiGLU && (g.N % 256)) throw std::invalid_argument("gemm_bf16: SwiGLU needs N % 256 == 0");
     const int bn = g.block_n ? g.block_n : 256;
+    const double out_el = g.epi.kind == kEpiSwiGLU ? 0.5 * g.M * g.N : (double)g.M * g.N;
+    const double out_b = g.epi.kind == kEpiBF16 || g.epi.kind == kEpiSwiGLU ? 2.0 : g.epi.kind == kEpiF32 ? 4.0 : 8.0;
+    ProfScope prof("gemm", 2.0 * g.M * g.N * g.K, 2.0 * ((double)g.M * g.K + (double)g.N * g.K) + out_el * out_b, st);
     switch (g.epi.kind) {
         case kEpiBF16: bn == 128 ? launch<128, kEpiBF16>(g, st) : launch<256, kEpiBF16>(g, st); break;
         case kEpiF32: bn == 128 ? launch<128, kEpiF32>(g, st) : launch<256, kEpiF32>(g, st); break;

@@ -96,8 +96,9 @@ void k_rmsnorm_bf16(const bf16 *x, int ldx, const float *w, int M, int d, float 
                     cudaStream_t st);
 void k_rope_store(const bf16 *qkv, const RowDesc *rows, int M, const TfShape &s, const float *rope, const KvCache &kv,
                   int layer, bf16 *q, cudaStream_t st);
+// flops / bytes: algorithmic work of the launch (profiling only)
 void k_attention(const bf16 *q, const RowDesc *rows, const AttnItem *items, int n_items, const KvCache &kv, int layer,
-                 const TfShape &s, bf16 *out, cudaStream_t st);
+                 const TfShape &s, bf16 *out, cudaStream_t st, double flops = 0, double bytes = 0);
 void k_store_features(const float *x, const RowDesc *rows, int M, int d, bf16 *feat, int max_ctx, int slot,
                       cudaStream_t st);
 void k_gather_features(const RowDesc *rows, int M, int d, const bf16 *feat, int max_ctx, const float *hid, bf16 *fin,

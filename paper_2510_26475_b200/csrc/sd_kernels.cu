@@ -18,6 +18,7 @@
 #include <climits>
 
 #include "common.cuh"
+#include "prof.h"
 #include "sd.h"
 
 namespace rs {
@@ -615,6 +616,8 @@ void sd_draft_sample(const SdDev &d, int depth, RowType rt, cudaStream_t st) {
     if (d.nact <= 0) return;
     dim3 grid(d.nact, depth == 0 ? 1 : d.t);
     const int th = sd_threads(d.V);
+    const double es = rt == RowType::F64 ? 8.0 : 4.0;
+    ProfScope prof("sample", 0, (double)d.nact * (depth == 0 ? 1 : d.t) * d.V * es, st);
     if (rt == RowType::F64) draft_sample_kernel<double><<<grid, th, 0, st>>>(d, depth);
     else draft_sample_kernel<float><<<grid, th, 0, st>>>(d, depth);
     RS_LAUNCHED();
@@ -629,6 +632,9 @@ void sd_redraft_check(const SdDev &d, cudaStream_t st) {
 void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t st) {
     if (d.nact <= 0) return;
     const int th = sd_threads(d.V);
+    // algorithmic bytes: every target row of the round plus every drafter row
+    const double es = rt == RowType::F64 ? 8.0 : 4.0;
+    ProfScope prof("accept", 0, (double)d.nact * (naive ? 1 : 2 * d.slots - 1) * d.V * es, st);
     if (rt == RowType::F64) accept_kernel<double><<<d.nact, th, 0, st>>>(d, round, naive ? 1 : 0);
     else accept_kernel<float><<<d.nact, th, 0, st>>>(d, round, naive ? 1 : 0);
     RS_LAUNCHED();

@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "gemm.h"
 #include "model.h"
+#include "prof.h"
 
 namespace rs {
 
@@ -48,6 +49,7 @@ struct Staging {
         }
         std::memcpy(base + off, v.data(), bytes);
         RS_CUDA(cudaMemcpyAsync(dst_dev, base + off, bytes, cudaMemcpyHostToDevice, st));
+        note_copy(true, bytes);
         off += bytes;
     }
 };
@@ -143,6 +145,18 @@ struct Batch {
         }
     }
     int M() const { return static_cast<int>(rows.size()); }
+    // algorithmic attention work: every query head attends to pos+1 keys (QK^T and PV);
+    // K/V bytes read once per item and kv head
+    double attn_flops(const TfShape &s) const {
+        double f = 0;
+        for (const auto &r : rows) f += 4.0 * s.H * s.hd * (r.pos + 1);
+        return f;
+    }
+    double attn_bytes(const TfShape &s) const {
+        double b = 0;
+        for (const auto &it : items) b += 4.0 * s.KV * s.hd * (it.maxpos + 1);
+        return b;
+    }
 };
 
 struct TransformerPair : ModelPair {
@@ -211,6 +225,7 @@ struct TransformerPair : ModelPair {
     // Target decoder stack over rows embedded in w.x; optional LM head (row m -> map_a[m]).
     void target_forward(const SdDev &d, int M, int ni, float *logits, bool use_map, cudaStream_t st) {
         const int qd = s.qkv_dim(), HD = s.H * s.hd;
+        const double attn_f = prof_enabled() ? bt.attn_flops(s) : 0, attn_b = prof_enabled() ? bt.attn_bytes(s) : 0;
         k_embed(w.rows.p, M, d.tok, d.tok_cap, d.chain_tok, d.t_max, d.n_max, tgt->emb, s.V, s.d, w.x.p, st);
         int fslot = 0;
         for (int l = 0; l < s.L; ++l) {
@@ -218,7 +233,7 @@ struct TransformerPair : ModelPair {
             k_rmsnorm(w.x.p, s.d, lw.ln1, M, s.d, s.eps, w.xn.p, s.d, st);
             gemm(w.xn.p, s.d, lw.qkv_w, M, qd, s.d, epi_bf16(w.qkv.p, qd, lw.qkv_b), st);
             k_rope_store(w.qkv.p, w.rows.p, M, s, tgt->rope, kv_t, l, w.q.p, st);
-            k_attention(w.q.p, w.rows.p, w.items.p, ni, kv_t, l, s, w.ao.p, st);
+            k_attention(w.q.p, w.rows.p, w.items.p, ni, kv_t, l, s, w.ao.p, st, attn_f, attn_b);
             gemm(w.ao.p, HD, lw.o_w, M, s.d, HD, epi_resid(w.x.p, s.d), st);
             k_rmsnorm(w.x.p, s.d, lw.ln2, M, s.d, s.eps, w.xn.p, s.d, st);
             gemm(w.xn.p, s.d, lw.gu_w, M, 2 * s.dff, s.d, epi_swiglu(w.h.p, s.dff), st);
@@ -241,7 +256,8 @@ struct TransformerPair : ModelPair {
         k_rmsnorm(w.x.p, s.d, drf->norm_hid, M, s.d, s.eps, w.xn.p + s.d, d2, st);
         gemm(w.xn.p, d2, drf->layer.qkv_w, M, qd, d2, epi_bf16(w.qkv.p, qd, drf->layer.qkv_b), st);
         k_rope_store(w.qkv.p, w.rows.p, M, drf->s, tgt->rope, kv_d, 0, w.q.p, st);
-        k_attention(w.q.p, w.rows.p, w.items.p, ni, kv_d, 0, drf->s, w.ao.p, st);
+        k_attention(w.q.p, w.rows.p, w.items.p, ni, kv_d, 0, drf->s, w.ao.p, st,
+                    prof_enabled() ? bt.attn_flops(s) : 0, prof_enabled() ? bt.attn_bytes(s) : 0);
         gemm(w.ao.p, HD, drf->layer.o_w, M, s.d, HD, epi_resid(w.x.p, s.d), st);
         k_rmsnorm(w.x.p, s.d, drf->layer.ln2, M, s.d, s.eps, w.xn.p, s.d, st);
         gemm(w.xn.p, s.d, drf->layer.gu_w, M, 2 * s.dff, s.d, epi_swiglu(w.h.p, s.dff), st);
@@ -358,6 +374,7 @@ struct TransformerPair : ModelPair {
 
     void after_accept(const SdDev &d, bool naive, cudaStream_t st) override {
         if (naive) return;
+        ProfScope prof("compact", 0, 0, st);
         k_compact(d, d.rsel, d.racc, rbase.p, kv_t, feat.p, 3 * s.d, max_ctx, st);
     }
 
