@@ -340,6 +340,9 @@ int rs_engine_create(rs_ctx *ctx, const rs_model *target, const rs_model *drafte
             const size_t rows = (size_t)N * e->slots_max * e->V * sizeof(float);
             e->d_P.alloc(rows);
             e->d_Q.alloc(rows);
+            const size_t nst = (size_t)N * e->slots_max * ((e->V + 255) / 256) * 2;
+            e->d_Pst.alloc(nst);
+            e->d_Qst.alloc(nst);
             e->pair = make_transformer_pair(ctx, e.get(), target, drafter, n, e->slots_max, e->prompt_len, prompts, tok_cap);
         }
         if (drafter && drafter->vocab != e->V) throw std::invalid_argument("BatchEngine: drafter vocabulary differs from target");

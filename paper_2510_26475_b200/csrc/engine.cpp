@@ -187,6 +187,9 @@ SdDev rs_engine::dev(const rs_sdconfig &cfg, int nact) {
     d.slots = cfg.enabled ? 1 + d.t * d.n : 1;  // rows per active sequence in P / Q
     d.P = d_P.p;
     d.Q = d_Q.p;
+    d.Pst = d_Pst.n ? d_Pst.p : nullptr;
+    d.Qst = d_Qst.n ? d_Qst.p : nullptr;
+    d.ntiles = (V + 255) / 256;
     d.verify_mode = verify_mode;
     d.record_full = record_full ? 1 : 0;
     d.err = d_err.p;

@@ -13,6 +13,11 @@ struct GemmEpi {
     const void *bias = nullptr;  // bf16 [N] (kEpiBF16 only)
     float scale = 1.0f;          // kEpiF32 only
     const int *row_map = nullptr;  // kEpiF32 only: output row of A-row m (-1 = drop); null = identity
+    // kEpiF32 only, BN = 256: per (output row, 256-column tile) softmax partials of
+    // y = out / tau over the tile's columns except the last global column (EOS):
+    // stats[(orow * ntiles + tile) * 2] = max y, [.. + 1] = sum exp(y - max)   (fp64)
+    double *stats = nullptr;
+    double tau = 1.0;
 };
 
 struct GemmArgs {

@@ -109,7 +109,7 @@ __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g));
 // Epilogue for one thread = one output row, 32 consecutive accumulator columns.
 template <int EPI, int BN>
 __device__ __forceinline__ void epilogue_chunk(const GemmEpi &ep, uint32_t tbase, int row, int col0, int chunk, int M,
-                                               int N) {
+                                               int N, double &rm, double &rs) {
     uint32_t v[32];
     if constexpr (EPI == kEpiSwiGLU) {
         // accumulator columns [0, BN/2) are gate, [BN/2, BN) are up, for BN/2 outputs
@@ -173,17 +173,41 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi &ep, uint32_t tbase
             const int orow = ep.row_map ? ep.row_map[row] : row;
             if (orow < 0) return;
             float *out = static_cast<float *>(ep.out) + static_cast<size_t>(orow) * ep.ldo + n0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * ep.scale);
             if (n0 + 32 <= N) {
 #pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                    float4 f = make_float4(__uint_as_float(v[j]) * ep.scale, __uint_as_float(v[j + 1]) * ep.scale,
-                                           __uint_as_float(v[j + 2]) * ep.scale, __uint_as_float(v[j + 3]) * ep.scale);
-                    *reinterpret_cast<float4 *>(out + j) = f;
-                }
+                for (int j = 0; j < 32; j += 4)
+                    *reinterpret_cast<float4 *>(out + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                                                      __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
             } else {
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
-                    if (n0 + j < N) out[j] = __uint_as_float(v[j]) * ep.scale;
+                    if (n0 + j < N) out[j] = __uint_as_float(v[j]);
+            }
+            if (ep.stats) {
+                // online (max, sum exp) of y = out / tau over this chunk's columns except the
+                // global last one (EOS, whose bias is request-specific and folded in later)
+                const bool unit = ep.tau == 1.0;
+                float cm = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (n0 + j < N - 1) cm = fmaxf(cm, __uint_as_float(v[j]));
+                if (cm != -INFINITY) {
+                    const double cmd = unit ? (double)cm : (double)cm / ep.tau;
+                    if (cmd > rm) {
+                        rs = rm == -INFINITY ? 0.0 : rs * exp(rm - cmd);
+                        rm = cmd;
+                    }
+                    double acc = 0.0;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        if (n0 + j >= N - 1) continue;
+                        const double y = unit ? (double)__uint_as_float(v[j]) : (double)__uint_as_float(v[j]) / ep.tau;
+                        acc += exp(y - rm);
+                    }
+                    rs += acc;
+                }
             }
         } else {  // kEpiResidual: out (fp32) += acc
             float *out = static_cast<float *>(ep.out) + static_cast<size_t>(row) * ep.ldo + n0;
@@ -309,10 +333,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t tb = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
             const int row = m0 + q * 32 + lane;
             constexpr int kChunks = (EPI == kEpiSwiGLU ? BN / 2 : BN) / 32;
+            double rm = -INFINITY, rs = 0.0;
 #pragma unroll 1
-            for (int c = 0; c < kChunks; ++c) epilogue_chunk<EPI, BN>(ep, tb, row, n0, c, M, N);
+            for (int c = 0; c < kChunks; ++c) epilogue_chunk<EPI, BN>(ep, tb, row, n0, c, M, N, rm, rs);
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
+            if constexpr (EPI == kEpiF32) {
+                if (ep.stats && row < M) {
+                    const int orow = ep.row_map ? ep.row_map[row] : row;
+                    if (orow >= 0) {
+                        const int ntiles = (N + BN - 1) / BN;
+                        double *st = ep.stats + ((size_t)orow * ntiles + n0 / BN) * 2;
+                        st[0] = rm;
+                        st[1] = rs;
+                    }
+                }
+            }
         }
     }
     __syncthreads();
@@ -392,7 +428,10 @@ void gemm_bf16(const GemmArgs &g, cudaStream_t st) {
     ProfScope prof("gemm", 2.0 * g.M * g.N * g.K, 2.0 * ((double)g.M * g.K + (double)g.N * g.K) + out_el * out_b, st);
     switch (g.epi.kind) {
         case kEpiBF16: bn == 128 ? launch<128, kEpiBF16>(g, st) : launch<256, kEpiBF16>(g, st); break;
-        case kEpiF32: bn == 128 ? launch<128, kEpiF32>(g, st) : launch<256, kEpiF32>(g, st); break;
+        case kEpiF32:
+            if (g.epi.stats && bn != 256) throw std::invalid_argument("gemm_bf16: row stats need block_n 256");
+            bn == 128 ? launch<128, kEpiF32>(g, st) : launch<256, kEpiF32>(g, st);
+            break;
         case kEpiResidual: bn == 128 ? launch<128, kEpiResidual>(g, st) : launch<256, kEpiResidual>(g, st); break;
         case kEpiSwiGLU: launch<256, kEpiSwiGLU>(g, st); break;
         default: throw std::invalid_argument("gemm_bf16: unknown epilogue");

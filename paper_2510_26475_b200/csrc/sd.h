@@ -50,6 +50,9 @@ struct SdDev {
     int32_t slots;           // 1 + t*n rows per active sequence
     const void *P;           // target logits rows  [nact][slots][V]
     const void *Q;           // drafter logits rows [nact][slots][V]
+    const double *Pst;       // LM-head epilogue tile partials for P rows [nact][slots][ntiles][2], or null
+    const double *Qst;       // same for Q rows
+    int32_t ntiles;          // ceil(V / 256)
     int32_t verify_mode;     // RS_VERIFY_SAMPLE / RS_VERIFY_GREEDY
     int32_t record_full;
     int32_t *err;            // device error word (first error wins)
@@ -66,6 +69,10 @@ void sd_draft_sample(const SdDev &d, int depth, RowType rt, cudaStream_t st);
 void sd_redraft_check(const SdDev &d, cudaStream_t st);
 void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t st);
 void sd_cycle_end(const SdDev &d, bool naive, cudaStream_t st);
+
+// Exact fp64 softmax tile partials of fp32 logit rows (rowstats.cu); row_ids null = rows 0..n-1.
+void row_stats(const float *rows, const int32_t *row_ids, int nrows, int V, double tau, double *stats,
+               cudaStream_t st);
 
 // Tabular model "forwards": gather logit rows by row_index (model.cpp:113-139).
 struct TabDev {

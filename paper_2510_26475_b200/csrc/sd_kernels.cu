@@ -1,19 +1,23 @@
 // sd_kernels.cu -- model-agnostic speculative-decoding kernels (sm_100a).
 //
 // K3 "fused softmax + acceptance": one CTA per active sequence walks the reference's
-// acceptance algorithm (specdec.cpp:197-267) over the logit rows the model forwards
-// produced, with block-wide max/sum reductions for the softmax normaliser, warp-segmented
-// prefix scans for the inverse CDF (model.cpp:23-40) and argmax reductions for greedy
-// verification. All probability arithmetic is fp64, exactly the reference's formula
-// p = exp(z/tau - max) / sum (model.cpp:53-68); only the summation ORDER differs (parallel
-// tree instead of sequential), i.e. ulp-level differences that can flip a token only when a
-// uniform lands within ~1e-16 of a CDF boundary.
+// acceptance algorithm (specdec.cpp:197-267) over the logit rows the model forwards produced.
+// All probability arithmetic is fp64 with exactly the reference's formula
+// p = exp(z/tau - max) / sum (model.cpp:53-68); only summation ORDER differs (ulp-level, a
+// token can flip only if a uniform lands within ~1e-16 of a CDF boundary).
 //
-// The drafting sampler draws each chain's tokens from the drafter rows with the request's
-// own draft stream at the offsets the reference's sequential loop would use
-// (specdec.cpp:177-192); chains are drafted level-synchronously (all chains of all requests
-// at depth j in one launch) and an EOS-shortened chain triggers a redraft pass with
-// corrected offsets (sd_redraft_check), so the stream order is preserved exactly.
+// Softmax statistics are hierarchical. Rows produced by the LM-head GEMM arrive with
+// per-256-column tile partials (max, sum exp) computed in the GEMM epilogue, so a row's
+// normaliser costs ~600 fp64 terms instead of a 152K-element pass, and an inverse-CDF draw
+// (model.cpp:23-40) is a warp prefix over tile masses followed by a warp scan inside the one
+// tile that brackets the uniform. Residual distributions max(0, p - q) / Z (specdec.cpp:35-52)
+// need one CTA-wide pass that yields Z and the tile masses together. Rows without GEMM
+// statistics (the fp64 tabular parity path) compute the same quantities in-kernel.
+//
+// The drafting sampler draws each chain's tokens with the request's own draft stream at the
+// offsets the reference's sequential loop would use (specdec.cpp:177-192); chains are drafted
+// level-synchronously and an EOS-shortened chain triggers a redraft pass with corrected
+// offsets (sd_redraft_check), so the stream order is preserved exactly.
 #include <cfloat>
 #include <climits>
 
@@ -25,39 +29,62 @@ namespace rs {
 
 namespace {
 
+constexpr int kTileW = 256;     // = the LM-head GEMM's BLOCK_N
+constexpr int kMaxTiles = 2048; // V <= 524288
+constexpr int kMaxCand = 16;
+
 template <class T>
 struct RowRef {
     const T *z;
     int V;
     double bias;
     double tau;
+    const double *gst;  // GEMM tile partials (max, sum) of z/tau excluding column V-1, or null
     // z'/tau with the EOS bias added to the last logit before the temperature division
-    // (model.cpp:137-138, model.cpp:58-61)
+    // (model.cpp:137-138, :58-61); tau == 1 skips the (exact anyway) division.
     __device__ __forceinline__ double v(int x) const {
         double y = static_cast<double>(z[x]);
         if (x == V - 1) y += bias;
-        return y / tau;
+        return tau == 1.0 ? y : y / tau;
     }
 };
 
 struct Stats {
-    double m, S;
+    double m, S, inv;  // inv = 1 / S (multiply instead of a per-element fp64 divide)
 };
+
+__device__ __forceinline__ int ntiles_of(int V) { return (V + kTileW - 1) / kTileW; }
+__device__ __forceinline__ int tile_lo(int t) { return t * kTileW; }
+__device__ __forceinline__ int tile_hi(int t, int V) { return min((t + 1) * kTileW, V - 1); }  // EOS excluded
 
 template <class T>
 __device__ Stats row_stats(const RowRef<T> &r, double *red) {
+    if (r.gst) {
+        const int nt = ntiles_of(r.V);
+        double m = -INFINITY;
+        for (int t = threadIdx.x; t < nt; t += blockDim.x) m = fmax(m, r.gst[2 * t]);
+        const double ve = r.v(r.V - 1);
+        m = fmax(block_max(m, red), ve);
+        double s = 0.0;
+        for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+            const double st = r.gst[2 * t + 1];
+            if (st > 0.0) s += st * exp(r.gst[2 * t] - m);
+        }
+        s = block_sum(s, red) + exp(ve - m);
+        return {m, s, 1.0 / s};
+    }
     double m = -INFINITY;
     for (int x = threadIdx.x; x < r.V; x += blockDim.x) m = fmax(m, r.v(x));
     m = block_max(m, red);
     double s = 0.0;
     for (int x = threadIdx.x; x < r.V; x += blockDim.x) s += exp(r.v(x) - m);
     s = block_sum(s, red);
-    return {m, s};
+    return {m, s, 1.0 / s};
 }
 
 template <class T>
 __device__ __forceinline__ double prob(const RowRef<T> &r, const Stats &s, int x) {
-    return exp(r.v(x) - s.m) / s.S;
+    return exp(r.v(x) - s.m) * s.inv;
 }
 
 template <class T>
@@ -80,73 +107,141 @@ struct PCurFn {
         double r = prob(p, sp, x);
         if (k > 0) {
             const double qq = prob(q, sq, x);
-            for (int j = 0; j < k; ++j) r = fmax(0.0, r - qq) / Z[j];
+            for (int j = 0; j < k; ++j) r = fmax(0.0, r - qq) * Z[j];  // Z holds 1 / Z_j
         }
         return r;
     }
 };
 
-// Chain-position residual max(0, pd - qd) / Z (specdec.cpp:238)
-template <class T>
-struct ResidFn {
-    RowRef<T> p;
-    Stats sp;
-    RowRef<T> q;
-    Stats sq;
-    double Z;
-    __device__ __forceinline__ double operator()(int x) const {
-        return fmax(0.0, prob(p, sp, x) - prob(q, sq, x)) / Z;
-    }
-};
-
+// Per-tile sums of f over the tile partition (tiles over [0, V-1) plus the EOS pseudo-tile at
+// index nt) into `mass`; returns the total. One warp per tile, coalesced lanes.
 template <class F>
-__device__ double block_total(const F &f, int V, double *red) {
+__device__ double tile_sums(const F &f, int V, double *mass, double *red) {
+    const int nt = ntiles_of(V);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int t = w; t < nt; t += nw) {
+        double s = 0.0;
+        for (int x = tile_lo(t) + lane; x < tile_hi(t, V); x += 32) s += f(x);
+        s = warp_sum(s);
+        if (lane == 0) mass[t] = s;
+    }
+    if (threadIdx.x == 0) mass[nt] = f(V - 1);
+    __syncthreads();
     double s = 0.0;
-    for (int x = threadIdx.x; x < V; x += blockDim.x) s += f(x);
+    for (int t = threadIdx.x; t <= nt; t += blockDim.x) s += mass[t];
     return block_sum(s, red);
 }
 
-// Inverse-CDF draw (model.cpp:23-40): first x with u < cum(x); on rounding slack the last
-// x with nonzero mass. Warp w owns the contiguous segment [w*Sw, (w+1)*Sw); pass A sums the
-// segments, pass B rescans only the segment(s) whose range brackets u.
-template <class F>
-__device__ int inv_cdf(const F &f, int V, double u, double *red, long long *redl, int *err) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int Sw = (V + nw - 1) / nw;
-    const int lo = min(V, w * Sw), hi = min(V, lo + Sw);
-    double s = 0.0;
-    for (int x = lo + lane; x < hi; x += 32) s += f(x);
-    s = warp_sum(s);
-    __syncthreads();
-    if (lane == 0) red[w] = s;
-    __syncthreads();
-    double prefix = 0.0;
-    for (int k = 0; k < w; ++k) prefix += red[k];
-    long long cand = LLONG_MAX;
-    if (hi > lo && u >= prefix - 1e-9 && u < prefix + s + 1e-9) {
-        double cum = prefix;
-        for (int base = lo; base < hi; base += 32) {
-            const int x = base + lane;
-            const double vx = x < hi ? f(x) : 0.0;
-            double sc = vx;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double y = __shfl_up_sync(0xffffffffu, sc, o);
-                if (lane >= o) sc += y;
-            }
-            const bool hit = x < hi && u < cum + sc;
-            const unsigned b = __ballot_sync(0xffffffffu, hit);
-            if (b) {
-                cand = base + (__ffs(b) - 1);
-                break;
-            }
-            cum += __shfl_sync(0xffffffffu, sc, 31);
-        }
+// Tile masses of a probability row straight from the GEMM partials.
+template <class T>
+__device__ void gemm_masses(const RowRef<T> &r, const Stats &st, double *mass) {
+    const int nt = ntiles_of(r.V);
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+        const double s = r.gst[2 * t + 1];
+        mass[t] = s > 0.0 ? s * exp(r.gst[2 * t] - st.m) * st.inv : 0.0;
     }
-    cand = block_min_ll(cand, redl);
-    if (cand != LLONG_MAX) return static_cast<int>(cand);
+    if (threadIdx.x == 0) mass[nt] = exp(r.v(r.V - 1) - st.m) * st.inv;
+    __syncthreads();
+}
+
+struct CdfScratch {
+    int cand_t[kMaxCand];
+    double cand_c[kMaxCand];
+    int ncand;
+    int result;
+};
+
+// Inverse-CDF draw (model.cpp:23-40): first x with u < cum(x); on rounding slack the last x
+// with nonzero mass. masses[t] * scale = mass of tile t; the tile whose cumulative range
+// brackets u (within 1e-10) is rescanned element by element by warp 0.
+template <class F>
+__device__ int inv_cdf(const F &f, int V, const double *mass, double scale, double u, CdfScratch &cs,
+                       long long *redl, int *err) {
+    const int nt = ntiles_of(V);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        cs.ncand = 0;
+        cs.result = -1;
+    }
+    __syncthreads();
+    if (w == 0) {
+        const int per = (nt + 1 + 31) / 32;
+        const int t0 = min(lane * per, nt + 1), t1 = min(t0 + per, nt + 1);
+        double ls = 0.0;
+        for (int t = t0; t < t1; ++t) ls += mass[t] * scale;
+        double incl = ls;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        double c = incl - ls;
+        for (int t = t0; t < t1; ++t) {
+            const double wt = mass[t] * scale;
+            if (u >= c - 1e-10 && u < c + wt + 1e-10) {
+                const int k = atomicAdd(&cs.ncand, 1);
+                if (k < kMaxCand) {
+                    cs.cand_t[k] = t;
+                    cs.cand_c[k] = c;
+                }
+            }
+            c += wt;
+        }
+        __syncwarp();
+        const int nc = min(cs.ncand, kMaxCand);
+        if (lane == 0) {  // candidates in increasing tile order
+            for (int i = 1; i < nc; ++i)
+                for (int j = i; j > 0 && cs.cand_t[j - 1] > cs.cand_t[j]; --j) {
+                    const int tt = cs.cand_t[j];
+                    cs.cand_t[j] = cs.cand_t[j - 1];
+                    cs.cand_t[j - 1] = tt;
+                    const double cc = cs.cand_c[j];
+                    cs.cand_c[j] = cs.cand_c[j - 1];
+                    cs.cand_c[j - 1] = cc;
+                }
+        }
+        __syncwarp();
+        int found = -1;  // warp-uniform
+        for (int k = 0; k < nc && found < 0; ++k) {
+            const int t = cs.cand_t[k];
+            const double c0 = cs.cand_c[k];
+            if (t == nt) {  // EOS pseudo-tile
+                if (u < c0 + f(V - 1)) found = V - 1;
+            } else {
+                const int lo = tile_lo(t) + lane * 8, hi = tile_hi(t, V);
+                double vals[8];
+                double s = 0.0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    vals[k] = lo + k < hi ? f(lo + k) : 0.0;
+                    s += vals[k];
+                }
+                double in2 = s;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double y = __shfl_up_sync(0xffffffffu, in2, o);
+                    if (lane >= o) in2 += y;
+                }
+                double cum = c0 + (in2 - s);
+                int mine = -1;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (lo + k >= hi) break;
+                    cum += vals[k];
+                    if (mine < 0 && u < cum) mine = lo + k;
+                }
+                const unsigned b = __ballot_sync(0xffffffffu, mine >= 0);
+                if (b) found = __shfl_sync(0xffffffffu, mine, __ffs(b) - 1);
+            }
+        }
+        if (lane == 0) cs.result = found;
+    }
+    __syncthreads();
+    int res = cs.result;
+    if (res >= 0 && res < V) return res;
+    // rounding slack at the top of the CDF: the last token with nonzero mass
     long long last = -1;
-    for (int x = threadIdx.x; x < V; x += blockDim.x)
+    for (int x = V - 1 - (int)threadIdx.x; x >= 0 && last < 0; x -= blockDim.x)
         if (f(x) > 0.0) last = x;
     last = block_max_ll(last, redl);
     if (last < 0) {
@@ -156,7 +251,9 @@ __device__ int inv_cdf(const F &f, int V, double u, double *red, long long *redl
     return static_cast<int>(last);
 }
 
-// argmax of p with lowest-index tie break, skipping `excl` (greedy verification / top-k).
+// Argmax of p with lowest-index tie break. For fp32 rows p is strictly monotone in the logit
+// (distinct fp32 logits give distinct fp64 probabilities), so the GEMM tile maxima locate
+// the winner; fp64 rows (tabular parity path) compare the probabilities themselves.
 template <class T>
 __device__ int row_argmax(const RowRef<T> &r, const Stats &st, double *red, long long *redl, const int *excl,
                           int n_excl) {
@@ -166,22 +263,22 @@ __device__ int row_argmax(const RowRef<T> &r, const Stats &st, double *red, long
         bool skip = false;
         for (int e = 0; e < n_excl; ++e) skip |= excl[e] == x;
         if (skip) continue;
-        const double p = prob(r, st, x);
-        if (p > best) {
+        const double p = sizeof(T) == 4 ? r.v(x) : prob(r, st, x);
+        if (p > best || bi == INT_MAX) {
             best = p;
             bi = x;
         }
     }
-    const double m = block_max(best, red);
-    long long key = (best == m) ? bi : LLONG_MAX;
+    const double m = block_max(bi == INT_MAX ? -INFINITY : best, red);
+    long long key = (bi != INT_MAX && best == m) ? bi : LLONG_MAX;
     key = block_min_ll(key, redl);
     return static_cast<int>(key);
 }
 
 struct Seq {
-    int r;        // request id
-    int a;        // active slot
-    int len;      // current token count (prompt + generated)
+    int r;  // request id
+    int a;  // active slot
+    int len;
     int plen;
     int maxlen;
     double bias;
@@ -216,11 +313,28 @@ __device__ void emit(const SdDev &d, Seq &q, int tok, const RowRef<T> &row, cons
 
 template <class T>
 __device__ __forceinline__ RowRef<T> prow(const SdDev &d, const Seq &q, int slot) {
-    return RowRef<T>{static_cast<const T *>(d.P) + ((size_t)q.a * d.slots + slot) * d.V, d.V, q.bias, d.tau_p};
+    const size_t row = (size_t)q.a * d.slots + slot;
+    return RowRef<T>{static_cast<const T *>(d.P) + row * d.V, d.V, q.bias, d.tau_p,
+                     d.Pst ? d.Pst + row * d.ntiles * 2 : nullptr};
 }
 template <class T>
 __device__ __forceinline__ RowRef<T> qrow(const SdDev &d, const Seq &q, int slot) {
-    return RowRef<T>{static_cast<const T *>(d.Q) + ((size_t)q.a * d.slots + slot) * d.V, d.V, q.bias, d.tau_q};
+    const size_t row = (size_t)q.a * d.slots + slot;
+    return RowRef<T>{static_cast<const T *>(d.Q) + row * d.V, d.V, q.bias, d.tau_q,
+                     d.Qst ? d.Qst + row * d.ntiles * 2 : nullptr};
+}
+
+// Draw from a plain probability row (masses from the GEMM partials when present).
+template <class T>
+__device__ int sample_row(const RowRef<T> &r, const Stats &st, double u, double *mass, CdfScratch &cs, double *red,
+                          long long *redl, int *err) {
+    const ProbFn<T> f{r, st};
+    if (r.gst) {
+        gemm_masses(r, st, mass);
+        return inv_cdf(f, r.V, mass, 1.0, u, cs, redl, err);
+    }
+    tile_sums(f, r.V, mass, red);
+    return inv_cdf(f, r.V, mass, 1.0, u, cs, redl, err);
 }
 
 __global__ void cycle_begin_kernel(SdDev d) {
@@ -260,10 +374,12 @@ __global__ void round_setup_kernel(SdDev d, int round) {
 }
 
 template <class T>
-__global__ void __launch_bounds__(1024, 1) draft_sample_kernel(SdDev d, int depth) {
+__global__ void __launch_bounds__(512) draft_sample_kernel(SdDev d, int depth) {
     __shared__ double red[32];
     __shared__ long long redl[32];
     __shared__ int picked[kMaxBranch];
+    __shared__ double mass[kMaxTiles + 1];
+    __shared__ CdfScratch cs;
     const int a = blockIdx.x;
     const int r = d.active[a];
     const int ne = d.n_eff[r];
@@ -272,15 +388,20 @@ __global__ void __launch_bounds__(1024, 1) draft_sample_kernel(SdDev d, int dept
     const MtStream &D = d.rng[2 * r];
     const bool greedy = d.verify_mode == 1;
     if (depth == 0) {
+        if (d.chain_len[(size_t)r * d.t_max] != 0) return;  // already drafted (redraft pass)
         const RowRef<T> row = qrow<T>(d, q, 0);
         const Stats st = row_stats(row, red);
+        if (!greedy) {
+            if (row.gst) gemm_masses(row, st, mass);
+            else tile_sums(ProbFn<T>{row, st}, row.V, mass, red);
+        }
         for (int i = 0; i < d.t; ++i) {
             int c;
             if (greedy) {
                 c = row_argmax(row, st, red, redl, picked, i);
             } else {
                 const double u = u_of(D, d.chain_off[(size_t)r * d.t_max + i]);
-                c = inv_cdf(ProbFn<T>{row, st}, d.V, u, red, redl, d.err);
+                c = inv_cdf(ProbFn<T>{row, st}, d.V, mass, 1.0, u, cs, redl, d.err);
             }
             if (threadIdx.x == 0) {
                 picked[i] = c;
@@ -300,7 +421,7 @@ __global__ void __launch_bounds__(1024, 1) draft_sample_kernel(SdDev d, int dept
     const Stats st = row_stats(row, red);
     int c;
     if (greedy) c = row_argmax(row, st, red, redl, picked, 0);
-    else c = inv_cdf(ProbFn<T>{row, st}, d.V, u_of(D, d.chain_off[ci] + depth), red, redl, d.err);
+    else c = sample_row(row, st, u_of(D, d.chain_off[ci] + depth), mass, cs, red, redl, d.err);
     if (threadIdx.x == 0) {
         d.chain_tok[ci * d.n_max + depth] = c;
         d.chain_len[ci] = depth + 1;
@@ -336,10 +457,12 @@ __global__ void redraft_check_kernel(SdDev d) {
 }
 
 template <class T>
-__global__ void __launch_bounds__(1024, 1) accept_kernel(SdDev d, int round, int naive) {
+__global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int naive) {
     __shared__ double red[32];
     __shared__ long long redl[32];
     __shared__ double Z[kMaxBranch];
+    __shared__ double mass[kMaxTiles + 1];
+    __shared__ CdfScratch cs;
     const int a = blockIdx.x;
     const int r = d.active[a];
     Seq q{r, a, d.len[r], d.prompt_len[r], d.max_len[r], d.eos_bias[r]};
@@ -355,7 +478,7 @@ __global__ void __launch_bounds__(1024, 1) accept_kernel(SdDev d, int round, int
         const Stats sp = row_stats(p, red);
         int x;
         if (greedy) x = row_argmax(p, sp, red, redl, nullptr, 0);
-        else x = inv_cdf(ProbFn<T>{p, sp}, d.V, u_of(D, d.d_used[r]), red, redl, d.err);
+        else x = sample_row(p, sp, u_of(D, d.d_used[r]), mass, cs, red, redl, d.err);
         emit(d, q, x, p, sp, false, 0.0, ended);
         if (threadIdx.x == 0) {
             if (!greedy) d.d_used[r] += 1;
@@ -384,12 +507,14 @@ __global__ void __launch_bounds__(1024, 1) accept_kernel(SdDev d, int round, int
         const RowRef<T> p = prow<T>(d, q, 0);
         const Stats sp = row_stats(p, red);
         const int x = greedy ? row_argmax(p, sp, red, redl, nullptr, 0)
-                             : inv_cdf(ProbFn<T>{p, sp}, d.V, u_of(A, acur++), red, redl, d.err);
+                             : sample_row(p, sp, u_of(A, acur++), mass, cs, red, redl, d.err);
         emit(d, q, x, p, sp, false, 0.0, ended);
         ++emitted;
         if (threadIdx.x == 0) {
             int *rc = d.round_cost + ((size_t)r * kMaxRounds + 0) * 3;
-            rc[0] = 0; rc[1] = 0; rc[2] = 1;
+            rc[0] = 0;
+            rc[1] = 0;
+            rc[2] = 1;
             d.n_rounds[r] = 1;
         }
         goto done;
@@ -404,7 +529,9 @@ __global__ void __launch_bounds__(1024, 1) accept_kernel(SdDev d, int round, int
         }
         if (threadIdx.x == 0) {
             int *rc = d.round_cost + ((size_t)r * kMaxRounds + round) * 3;
-            rc[0] = longest; rc[1] = t; rc[2] = tree + 1;
+            rc[0] = longest;
+            rc[1] = t;
+            rc[2] = tree + 1;
             d.n_rounds[r] = round + 1;
             d.drafted[r] = 1;
             d.d_used[r] += tree;
@@ -427,6 +554,7 @@ __global__ void __launch_bounds__(1024, 1) accept_kernel(SdDev d, int round, int
         } else {
             // Branch point: recursive rejection over the t siblings (specdec.cpp:197-217).
             int k = 0;
+            double zlast = 1.0;
             for (int i = 0; i < t; ++i) {
                 const int cand = ctok[(size_t)i * d.n_max];
                 PCurFn<T> pc{p1, s1, q1, t1, Z, k};
@@ -436,15 +564,18 @@ __global__ void __launch_bounds__(1024, 1) accept_kernel(SdDev d, int round, int
                     sel = i;
                     break;
                 }
-                const double z = block_total(
-                    [&](int x) { return fmax(0.0, pc(x) - prob(q1, t1, x)); }, d.V, red);
+                // residual normaliser and its tile masses in one pass
+                const double z = tile_sums([&](int x) { return fmax(0.0, pc(x) - prob(q1, t1, x)); }, d.V, mass, red);
                 if (z <= 1e-12 && threadIdx.x == 0) atomicCAS(d.err, 0, kErrResidual);
-                if (threadIdx.x == 0) Z[k] = z;
+                if (threadIdx.x == 0) Z[k] = 1.0 / z;
                 __syncthreads();
+                zlast = z;
                 ++k;
             }
             if (sel < 0) {
-                const int x = inv_cdf(PCurFn<T>{p1, s1, q1, t1, Z, k}, d.V, u_of(A, acur++), red, redl, d.err);
+                // all siblings rejected: draw from the final residual (masses of the last pass / Z_k)
+                const PCurFn<T> fk{p1, s1, q1, t1, Z, k};
+                const int x = inv_cdf(fk, d.V, mass, 1.0 / zlast, u_of(A, acur++), cs, redl, d.err);
                 emit(d, q, x, p1, s1, false, 0.0, ended);  // StepRecord keeps p1 (specdec.cpp:214)
                 ++emitted;
                 goto done;
@@ -484,10 +615,12 @@ __global__ void __launch_bounds__(1024, 1) accept_kernel(SdDev d, int round, int
             } else {
                 int x = repl;
                 if (!greedy) {
-                    const double z = block_total([&](int y) { return fmax(0.0, prob(pd, sp, y) - prob(qd, sq, y)); },
-                                                 d.V, red);
+                    auto res = [&](int y) { return fmax(0.0, prob(pd, sp, y) - prob(qd, sq, y)); };
+                    const double z = tile_sums(res, d.V, mass, red);
                     if (z <= 1e-12 && threadIdx.x == 0) atomicCAS(d.err, 0, kErrResidual);
-                    x = inv_cdf(ResidFn<T>{pd, sp, qd, sq, z}, d.V, u_of(A, acur++), red, redl, d.err);
+                    const double zi = 1.0 / z;
+                    auto rn = [&](int y) { return fmax(0.0, prob(pd, sp, y) - prob(qd, sq, y)) * zi; };
+                    x = inv_cdf(rn, d.V, mass, 1.0 / z, u_of(A, acur++), cs, redl, d.err);
                 }
                 emit(d, q, x, pd, sp, false, 0.0, ended);
                 ++emitted;
@@ -502,7 +635,7 @@ __global__ void __launch_bounds__(1024, 1) accept_kernel(SdDev d, int round, int
             const RowRef<T> pb = prow<T>(d, q, 1 + sel * n + L - 1);
             const Stats sb = row_stats(pb, red);
             const int x = greedy ? row_argmax(pb, sb, red, redl, nullptr, 0)
-                                 : inv_cdf(ProbFn<T>{pb, sb}, d.V, u_of(A, acur++), red, redl, d.err);
+                                 : sample_row(pb, sb, u_of(A, acur++), mass, cs, red, redl, d.err);
             emit(d, q, x, pb, sb, false, 0.0, ended);
             ++emitted;
         }
@@ -596,7 +729,7 @@ __global__ void tab_rows_kernel(SdDev d, TabDev m, int depth, int verify, int na
     for (int x = threadIdx.x; x < m.V; x += blockDim.x) dst[x] = src[x];
 }
 
-inline int sd_threads(int V) { return V <= 256 ? 32 : V <= 4096 ? 256 : 1024; }
+inline int sd_threads(int V, bool) { return V <= 256 ? 32 : V <= 4096 ? 256 : 512; }
 
 }  // namespace
 
@@ -614,8 +747,9 @@ void sd_round_setup(const SdDev &d, int round, cudaStream_t st) {
 
 void sd_draft_sample(const SdDev &d, int depth, RowType rt, cudaStream_t st) {
     if (d.nact <= 0) return;
+    if ((d.V + kTileW - 1) / kTileW > kMaxTiles) throw std::invalid_argument("vocabulary too large for the sampler");
     dim3 grid(d.nact, depth == 0 ? 1 : d.t);
-    const int th = sd_threads(d.V);
+    const int th = std::min(512, sd_threads(d.V, d.Qst != nullptr));
     const double es = rt == RowType::F64 ? 8.0 : 4.0;
     ProfScope prof("sample", 0, (double)d.nact * (depth == 0 ? 1 : d.t) * d.V * es, st);
     if (rt == RowType::F64) draft_sample_kernel<double><<<grid, th, 0, st>>>(d, depth);
@@ -631,7 +765,7 @@ void sd_redraft_check(const SdDev &d, cudaStream_t st) {
 
 void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t st) {
     if (d.nact <= 0) return;
-    const int th = sd_threads(d.V);
+    const int th = sd_threads(d.V, false);
     // algorithmic bytes: every target row of the round plus every drafter row
     const double es = rt == RowType::F64 ? 8.0 : 4.0;
     ProfScope prof("accept", 0, (double)d.nact * (naive ? 1 : 2 * d.slots - 1) * d.V * es, st);

@@ -114,13 +114,15 @@ GemmEpi epi_swiglu(void *out, int ldo) {
     e.ldo = ldo;
     return e;
 }
-GemmEpi epi_f32(float *out, int ldo, float scale, const int *row_map) {
+GemmEpi epi_f32(float *out, int ldo, float scale, const int *row_map, double *stats = nullptr, double tau = 1.0) {
     GemmEpi e;
     e.kind = kEpiF32;
     e.out = out;
     e.ldo = ldo;
     e.scale = scale;
     e.row_map = row_map;
+    e.stats = stats;
+    e.tau = tau;
     return e;
 }
 
@@ -223,7 +225,8 @@ struct TransformerPair : ModelPair {
     }
 
     // Target decoder stack over rows embedded in w.x; optional LM head (row m -> map_a[m]).
-    void target_forward(const SdDev &d, int M, int ni, float *logits, bool use_map, cudaStream_t st) {
+    void target_forward(const SdDev &d, int M, int ni, float *logits, bool use_map, cudaStream_t st,
+                        double *stats = nullptr) {
         const int qd = s.qkv_dim(), HD = s.H * s.hd;
         const double attn_f = prof_enabled() ? bt.attn_flops(s) : 0, attn_b = prof_enabled() ? bt.attn_bytes(s) : 0;
         k_embed(w.rows.p, M, d.tok, d.tok_cap, d.chain_tok, d.t_max, d.n_max, tgt->emb, s.V, s.d, w.x.p, st);
@@ -243,8 +246,9 @@ struct TransformerPair : ModelPair {
         }
         if (logits) {
             k_rmsnorm(w.x.p, s.d, tgt->final_norm, M, s.d, s.eps, w.xn.p, s.d, st);
-            gemm(w.xn.p, s.d, tgt->emb, M, s.V, s.d,
-                 epi_f32(logits, s.V, s.logit_scale, use_map ? w.map_a.p : nullptr), st);
+            gemm(w.xn.p, s.d, tgt->emb, M, s.V, s.d, epi_f32(logits, s.V, s.logit_scale, use_map ? w.map_a.p : nullptr),
+                 st);
+            if (stats) row_stats(logits, use_map ? w.map_a.p : nullptr, M, s.V, tgt->temperature, stats, st);
         }
     }
 
@@ -265,11 +269,12 @@ struct TransformerPair : ModelPair {
     }
 
     // LM head of the drafter on n selected rows of w.x (src rows, Q destination rows).
-    void drafter_head(const int32_t *src_dev, const int32_t *dst_dev, int n, float *Q, cudaStream_t st) {
+    void drafter_head(const int32_t *src_dev, const int32_t *dst_dev, int n, float *Q, double *qst, cudaStream_t st) {
         float *g = w.e32.p;  // gathered rows
         k_rows_copy_f32(w.x.p, s.d, src_dev, g, s.d, nullptr, n, s.d, st);
         k_rmsnorm(g, s.d, drf->final_norm, n, s.d, s.eps, w.xn.p, s.d, st);
         gemm(w.xn.p, s.d, drf->lm_w, n, s.V, s.d, epi_f32(Q, s.V, s.logit_scale, dst_dev), st);
+        if (qst) row_stats(Q, dst_dev, n, s.V, drf->temperature, qst, st);
     }
 
     // ---- ModelPair hooks ---------------------------------------------------------------------
@@ -313,7 +318,7 @@ struct TransformerPair : ModelPair {
                 k_gather_features(w.rows.p, M, s.d, feat.p, max_ctx, nullptr, w.fin.p, nullptr, st);
                 gemm(w.fin.p, 3 * s.d, drf->fc_w, M, s.d, 3 * s.d, epi_f32(w.x.p, s.d, 1.0f, nullptr), st);
                 drafter_layer(d, M, (int)bt.items.size(), st);
-                drafter_head(w.map_a.p, w.map_b.p, (int)head_src.size(), Q, st);
+                drafter_head(w.map_a.p, w.map_b.p, (int)head_src.size(), Q, const_cast<double *>(d.Qst), st);
                 const int nh = (int)hid_src.size();
                 k_rows_copy_f32(w.x.p, s.d, w.idx.p, dh.p, s.d, w.idx.p + nh, nh, s.d, st);
                 a0 = a;
@@ -338,6 +343,7 @@ struct TransformerPair : ModelPair {
         drafter_layer(d, M, (int)bt.items.size(), st);
         k_rmsnorm(w.x.p, s.d, drf->final_norm, M, s.d, s.eps, w.xn.p, s.d, st);
         gemm(w.xn.p, s.d, drf->lm_w, M, s.V, s.d, epi_f32(Q, s.V, s.logit_scale, w.map_b.p), st);
+        if (d.Qst) row_stats(Q, w.map_b.p, M, s.V, drf->temperature, const_cast<double *>(d.Qst), st);
         k_rows_copy_f32(w.x.p, s.d, nullptr, dh.p, s.d, w.map_a.p, M, s.d, st);
     }
 
@@ -369,7 +375,7 @@ struct TransformerPair : ModelPair {
         }
         upload(bt, st);
         if (!naive) stage.upload(rbase.p, base, st);
-        target_forward(d, bt.M(), (int)bt.items.size(), P, true, st);
+        target_forward(d, bt.M(), (int)bt.items.size(), P, true, st, const_cast<double *>(d.Pst));
     }
 
     void after_accept(const SdDev &d, bool naive, cudaStream_t st) override {
