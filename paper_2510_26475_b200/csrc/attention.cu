@@ -1,16 +1,18 @@
-// attention.cu -- tree-causal GQA attention over the paged-by-sequence KV cache.
+// attention.cu -- tree-causal GQA attention over the per-sequence KV cache.
 //
-// A work item is up to 64/G query tokens of one sequence that share one key mapping; the CTA
-// for (item, kv head) holds those tokens x G query heads as 64 rows (4 warps x 16). Keys are
-// visited in LOGICAL position order in 64-key chunks from position 0 up to the item's last
-// query position; a key at logical position p >= ltree of a tree row lives in the row's own
-// chain slots (tbase + chain*nstride + p - ltree), so a drafted token sees the context, the
-// root and exactly its own chain prefix -- the tree-causal mask of SURVEY.md §8 A3 -- and
-// nothing else. Because the chunking and the online-softmax merge order depend only on
-// logical positions, a row's result does not depend on which other rows share its CTA: the
-// same token gives the same output whether it is verified inside a tree or decoded alone.
-// Q.K^T and P.V run on the tensor cores with mma.sync m16n8k16 (bf16 in, fp32 accumulate),
-// K/V chunks are double-buffered with cp.async into XOR-swizzled shared memory.
+// A work item is a run of query tokens of one sequence; the CTA for (item, kv head) owns those
+// tokens x G query heads as rows (row = token * G + head). Tokens are grouped by key mapping:
+// a drafted token of chain i sees the context, the root and exactly its own chain prefix --
+// the tree-causal mask of SURVEY.md §8 A3 -- i.e. logical positions 0..pos where positions
+// >= ltree live in the chain's own slots (tbase + chain * nstride + p - ltree). Each warp owns
+// 16 rows of one group. Keys are visited in LOGICAL order in 64-key chunks: chunks wholly
+// below ltree are shared by every group (one K/V tile for all 8 x 21 rows of a tree), the
+// 1-2 chunks that reach into the tree are replayed once per group with that group's tile.
+// Because every row walks the same chunk sequence with the same key values whatever CTA it
+// sits in, a token's output is bit-identical whether it is verified inside a tree, decoded
+// alone or prefilled (checked by tests/test_transformer_gpu.py).
+// Q.K^T and P.V run on the tensor cores with mma.sync m16n8k16 (bf16 in, fp32 accumulate);
+// K/V tiles are double-buffered with cp.async into XOR-swizzled shared memory.
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -23,10 +25,12 @@ namespace {
 
 constexpr int kHD = 128;
 constexpr int kChunk = 64;
-constexpr int kRows = 64;
-constexpr int kRowBytes = kHD * 2;                 // 256
-constexpr int kTileBytes = kChunk * kRowBytes;     // 16 KB
-constexpr int kSmem = kTileBytes * 5 + kRows * 4;  // Q + 2x(K,V) + row positions
+constexpr int kMaxWarps = 12;  // one 21-token tree at GQA 8; 384 threads -> 170 registers/thread
+constexpr int kRowBytes = kHD * 2;                       // 256
+constexpr int kTileBytes = kChunk * kRowBytes;           // 16 KB
+constexpr int kQBytes = kMaxWarps * 16 * kRowBytes;      // 64 KB
+constexpr int kMaxPasses = 256;
+constexpr int kSmem = kQBytes + 4 * kTileBytes + 4096;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ int swz(int row, int chunk) { return row * kRowBytes + ((chunk ^ (row & 7)) << 4); }
@@ -56,82 +60,150 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<uint32_t *>(&h);
 }
 
-__global__ void __launch_bounds__(128) attn_kernel(const bf16 *q, const RowDesc *rows, const AttnItem *items,
-                                                   KvCache kv, int layer, int H, int KV, float scale_log2,
-                                                   bf16 *out) {
+struct Plan {
+    int ngroups, nwarps, npasses;
+    int g_chain[kMaxWarps], g_maxpos[kMaxWarps];
+    int w_group[kMaxWarps], w_r0[kMaxWarps], w_nr[kMaxWarps], w_maxpos[kMaxWarps];
+    short p_chunk[kMaxPasses], p_group[kMaxPasses];  // group -1: shared pass (all warps)
+};
+
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) attn_kernel(const bf16 *q, const RowDesc *rows,
+                                                                 const AttnItem *items, KvCache kv, int layer, int H,
+                                                                 int KV, float scale_log2, bf16 *out) {
     extern __shared__ __align__(128) uint8_t sm[];
     uint8_t *sQ = sm;
-    uint8_t *sK = sm + kTileBytes;
-    uint8_t *sV = sK + 2 * kTileBytes;
-    int *rowpos = reinterpret_cast<int *>(sV + 2 * kTileBytes);
+    uint8_t *sKV = sm + kQBytes;  // 2 buffers x (K, V)
+    Plan &pl = *reinterpret_cast<Plan *>(sm + kQBytes + 4 * kTileBytes);
+    __shared__ int rowpos[kMaxWarps * 16];
 
     const AttnItem it = items[blockIdx.x];
     const int kvh = blockIdx.y;
     const int G = H / KV;
-    const int nr = it.nrows * G;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    for (int idx = tid; idx < kRows * 16; idx += 128) {
-        const int r = idx >> 4, c = idx & 15;
-        uint8_t *dst = sQ + swz(r, c);
-        if (r < nr) {
-            const int tok = it.row0 + r / G, head = kvh * G + r % G;
-            cp16(dst, q + ((size_t)tok * H + head) * kHD + c * 8);
-        } else {
-            *reinterpret_cast<int4 *>(dst) = make_int4(0, 0, 0, 0);
-        }
-    }
-    if (tid < kRows) rowpos[tid] = tid < nr ? rows[it.row0 + tid / G].pos : -1;
-
-    auto load_kv = [&](int c, int buf) {
-        uint8_t *k = sK + buf * kTileBytes, *v = sV + buf * kTileBytes;
-        for (int idx = tid; idx < kChunk * 16; idx += 128) {
-            const int kk = idx >> 4, ch = idx & 15;
-            const int p = c * kChunk + kk;
-            if (p <= it.maxpos) {
-                const int phys = (it.chain < 0 || p < it.ltree) ? p : it.tbase + it.chain * it.nstride + (p - it.ltree);
-                const size_t o = kv.off(layer, it.seq, kvh, phys) + ch * 8;
-                cp16(k + swz(kk, ch), kv.k + o);
-                cp16(v + swz(kk, ch), kv.v + o);
+    // ---- plan: groups of tokens sharing a key mapping, warps, pass list --------------------
+    if (tid == 0) {
+        int ng = 0, nw = 0;
+        int k = 0;
+        while (k < it.nrows) {
+            int ch = rows[it.row0 + k].chain;
+            int k1 = k + 1;
+            if (it.chain == -2) {  // tree item: consecutive tokens of one chain (root joins chain 0)
+                if (ch < 0 && k1 < it.nrows && rows[it.row0 + k1].chain == 0) ch = 0;
+                while (k1 < it.nrows && rows[it.row0 + k1].chain == ch) ++k1;
             } else {
-                *reinterpret_cast<int4 *>(k + swz(kk, ch)) = make_int4(0, 0, 0, 0);
-                *reinterpret_cast<int4 *>(v + swz(kk, ch)) = make_int4(0, 0, 0, 0);
+                ch = it.chain;
+                k1 = it.nrows;
+            }
+            int gmax = 0;
+            for (int j = k; j < k1; ++j) gmax = max(gmax, rows[it.row0 + j].pos);
+            pl.g_chain[ng] = ch;
+            pl.g_maxpos[ng] = gmax;
+            for (int r = k * G; r < k1 * G; r += 16) {
+                pl.w_group[nw] = ng;
+                pl.w_r0[nw] = r;
+                pl.w_nr[nw] = min(16, k1 * G - r);
+                int wm = 0;
+                for (int rr = r; rr < r + pl.w_nr[nw]; ++rr) wm = max(wm, rows[it.row0 + rr / G].pos);
+                pl.w_maxpos[nw] = wm;
+                ++nw;
+            }
+            ++ng;
+            k = k1;
+        }
+        pl.ngroups = ng;
+        pl.nwarps = nw;
+        int np = 0;
+        const int cmax = it.maxpos / kChunk;
+        for (int c = 0; c <= cmax; ++c) {
+            const bool tail = it.chain != -1 && c * kChunk + kChunk - 1 >= it.ltree;
+            if (!tail) {
+                pl.p_chunk[np] = c;
+                pl.p_group[np++] = -1;
+            } else {
+                for (int g = 0; g < ng; ++g)
+                    if (pl.g_maxpos[g] >= c * kChunk) {
+                        pl.p_chunk[np] = c;
+                        pl.p_group[np++] = g;
+                    }
+            }
+        }
+        pl.npasses = np;
+    }
+    __syncthreads();
+
+    // ---- Q rows of this warp -> smem (warp-private 16 x 128) --------------------------------
+    const bool has_rows = warp < pl.nwarps;
+    const int my_group = has_rows ? pl.w_group[warp] : -1;
+    const int my_r0 = has_rows ? pl.w_r0[warp] : 0, my_nr = has_rows ? pl.w_nr[warp] : 0;
+    uint8_t *qw = sQ + warp * 16 * kRowBytes;
+    if (has_rows) {
+        for (int idx = lane; idx < 16 * 16; idx += 32) {
+            const int r = idx >> 4, c = idx & 15;
+            uint8_t *dst = qw + swz(r, c);
+            if (r < my_nr) {
+                const int rr = my_r0 + r;
+                const int tok = it.row0 + rr / G, head = kvh * G + rr % G;
+                cp16(dst, q + ((size_t)tok * H + head) * kHD + c * 8);
+            } else {
+                *reinterpret_cast<int4 *>(dst) = make_int4(0, 0, 0, 0);
+            }
+        }
+        if (lane < 16) rowpos[warp * 16 + lane] = lane < my_nr ? rows[it.row0 + (my_r0 + lane) / G].pos : -1;
+    }
+
+    auto load_pass = [&](int pi, int buf) {
+        const int c = pl.p_chunk[pi], g = pl.p_group[pi];
+        const int ch = g < 0 ? -1 : pl.g_chain[g];
+        const int lim = g < 0 ? it.maxpos : pl.g_maxpos[g];
+        uint8_t *k = sKV + buf * 2 * kTileBytes, *v = k + kTileBytes;
+        for (int idx = tid; idx < kChunk * 16; idx += blockDim.x) {
+            const int kk = idx >> 4, cc = idx & 15;
+            const int p = c * kChunk + kk;
+            if (p <= lim) {
+                const int phys = (ch < 0 || p < it.ltree) ? p : it.tbase + ch * it.nstride + (p - it.ltree);
+                const size_t o = kv.off(layer, it.seq, kvh, phys) + cc * 8;
+                cp16(k + swz(kk, cc), kv.k + o);
+                cp16(v + swz(kk, cc), kv.v + o);
+            } else {
+                *reinterpret_cast<int4 *>(k + swz(kk, cc)) = make_int4(0, 0, 0, 0);
+                *reinterpret_cast<int4 *>(v + swz(kk, cc)) = make_int4(0, 0, 0, 0);
             }
         }
     };
 
-    const int nchunks = it.maxpos / kChunk + 1;
-    load_kv(0, 0);
+    load_pass(0, 0);
     asm volatile("cp.async.commit_group;" ::: "memory");
 
-    const bool active = warp * 16 < nr;
     uint32_t qa[8][4];
     float o[16][4];
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 #pragma unroll
     for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
     int pos0 = -1, pos1 = -1;
+    const int wmax = has_rows ? pl.w_maxpos[warp] : -1;
 
-    for (int c = 0; c < nchunks; ++c) {
-        if (c + 1 < nchunks) {
-            load_kv(c + 1, (c + 1) & 1);
+    for (int pi = 0; pi < pl.npasses; ++pi) {
+        if (pi + 1 < pl.npasses) {
+            load_pass(pi + 1, (pi + 1) & 1);
             asm volatile("cp.async.commit_group;" ::: "memory");
             asm volatile("cp.async.wait_group 1;" ::: "memory");
         } else {
             asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncthreads();
-        if (c == 0 && active) {
+        if (pi == 0 && has_rows) {
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
-                const int r = warp * 16 + (lane & 15), ch = 2 * kk + (lane >> 4);
-                ldsm_x4(smem_u32(sQ + swz(r, ch)), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+                const int r = lane & 15, ch = 2 * kk + (lane >> 4);
+                ldsm_x4(smem_u32(qw + swz(r, ch)), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
             }
             pos0 = rowpos[warp * 16 + (lane >> 2)];
             pos1 = rowpos[warp * 16 + (lane >> 2) + 8];
         }
-        if (active) {
-            const uint8_t *k = sK + (c & 1) * kTileBytes, *v = sV + (c & 1) * kTileBytes;
+        const int c = pl.p_chunk[pi], g = pl.p_group[pi];
+        if (has_rows && (g < 0 || g == my_group) && wmax >= c * kChunk) {
+            const uint8_t *k = sKV + (pi & 1) * 2 * kTileBytes, *v = k + kTileBytes;
             float s[8][4];
 #pragma unroll
             for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
@@ -146,7 +218,6 @@ __global__ void __launch_bounds__(128) attn_kernel(const bf16 *q, const RowDesc 
                     mma16816(s[2 * jp + 1], qa[kk], b2, b3);
                 }
             }
-            // causal / tree mask + online softmax (base-2, pre-scaled)
             float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
             for (int nt = 0; nt < 8; ++nt) {
@@ -200,18 +271,18 @@ __global__ void __launch_bounds__(128) attn_kernel(const bf16 *q, const RowDesc 
         }
         __syncthreads();
     }
-    if (!active) return;
+    if (!has_rows) return;
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
     l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
     l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
     const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
-    const int r0 = warp * 16 + (lane >> 2), r1 = r0 + 8;
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
-        const int r = half ? r1 : r0;
-        if (r >= nr) continue;
-        const int tok = it.row0 + r / G, head = kvh * G + r % G;
+        const int r = (lane >> 2) + half * 8;
+        if (r >= my_nr) continue;
+        const int rr = my_r0 + r;
+        const int tok = it.row0 + rr / G, head = kvh * G + rr % G;
         bf16 *dst = out + ((size_t)tok * H + head) * kHD + 2 * (lane & 3);
         const float inv = half ? inv1 : inv0;
 #pragma unroll
@@ -224,6 +295,9 @@ __global__ void __launch_bounds__(128) attn_kernel(const bf16 *q, const RowDesc 
 
 }  // namespace
 
+int attn_max_tokens(int G) { return kMaxWarps * 16 / G; }
+int attn_max_warps() { return kMaxWarps; }
+
 void k_attention(const bf16 *q, const RowDesc *rows, const AttnItem *items, int n_items, const KvCache &kv, int layer,
                  const TfShape &s, bf16 *out, cudaStream_t st, double flops, double bytes) {
     if (n_items <= 0) return;
@@ -231,11 +305,13 @@ void k_attention(const bf16 *q, const RowDesc *rows, const AttnItem *items, int 
     if (s.hd != kHD) throw std::invalid_argument("attention: head_dim must be 128");
     static bool attr = false;
     if (!attr) {
+        static_assert(sizeof(Plan) <= 4096, "plan");
         RS_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
         attr = true;
     }
     const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(s.hd));
-    attn_kernel<<<dim3(n_items, s.KV), 128, kSmem, st>>>(q, rows, items, kv, layer, s.H, s.KV, scale_log2, out);
+    attn_kernel<<<dim3(n_items, s.KV), kMaxWarps * 32, kSmem, st>>>(q, rows, items, kv, layer, s.H, s.KV, scale_log2,
+                                                                   out);
     RS_LAUNCHED();
 }
 

@@ -137,7 +137,7 @@ struct Batch {
         map_a.clear();
         map_b.clear();
     }
-    // attention items over rows [r0, r1) of one sequence sharing one key mapping
+    // plain causal attention items over rows [r0, r1) of one sequence (keys = its cache)
     void add_items(int r0, int r1, int per, int chain, int ltree, int tbase, int nstride) {
         for (int a = r0; a < r1; a += per) {
             const int b = std::min(r1, a + per);
@@ -145,6 +145,28 @@ struct Batch {
             for (int k = a; k < b; ++k) maxpos = std::max(maxpos, rows[k].pos);
             items.push_back(AttnItem{rows[a].seq, a, b - a, maxpos, chain, ltree, tbase, nstride});
         }
+    }
+    // tree items over rows [r0, r1) of one sequence: groups of consecutive tokens of one chain
+    // (the root joins chain 0), packed into CTAs of at most 16 warps of 16 rows (G rows/token).
+    void add_tree_items(int r0, int r1, int G, int ltree, int tbase, int nstride) {
+        int a = r0, warps = 0, maxpos = 0;
+        int k = r0;
+        while (k < r1) {
+            int ch = rows[k].chain, k1 = k + 1;
+            if (ch < 0 && k1 < r1 && rows[k1].chain == 0) ch = 0;
+            while (k1 < r1 && rows[k1].chain == ch) ++k1;
+            const int gw = ((k1 - k) * G + 15) / 16;
+            if (warps + gw > attn_max_warps() && k > a) {
+                items.push_back(AttnItem{rows[a].seq, a, k - a, maxpos, -2, ltree, tbase, nstride});
+                a = k;
+                warps = 0;
+                maxpos = 0;
+            }
+            warps += gw;
+            for (int j = k; j < k1; ++j) maxpos = std::max(maxpos, rows[j].pos);
+            k = k1;
+        }
+        if (k > a) items.push_back(AttnItem{rows[a].seq, a, k - a, maxpos, -2, ltree, tbase, nstride});
     }
     int M() const { return static_cast<int>(rows.size()); }
     // algorithmic attention work: every query head attends to pos+1 keys (QK^T and PV);
@@ -195,7 +217,9 @@ struct TransformerPair : ModelPair {
         B = std::max(n_req, 1);
         slots_max = slots;
         max_ctx = s.max_ctx;
-        per_item = std::max(1, 64 / (s.H / s.KV));
+        per_item = attn_max_tokens(s.H / s.KV);
+        if ((eng->n_max + 1) * (s.H / s.KV) > 16 * attn_max_warps())
+            throw std::invalid_argument("transformer engine: (draft_len + 1) * GQA group must be <= 192");
         for (int i = 0; i < n_req; ++i)
             if (plen[i] < 1) throw std::invalid_argument("transformer engine: prompts must be non-empty");
         if (tok_cap + slots > max_ctx)
@@ -330,12 +354,13 @@ struct TransformerPair : ModelPair {
         for (int a = 0; a < nact; ++a) {
             const int r = eng->active[a];
             const int L = eng->len[r];
+            const int r0 = bt.M();
             for (int i = 0; i < d.t; ++i) {
                 bt.rows.push_back(RowDesc{r, L - 1 + depth, L + i * d.n + depth - 1, 1, i, depth - 1, 1, r * d.t_max + i});
-                bt.add_items(bt.M() - 1, bt.M(), 1, i, L, L, d.n);
                 bt.map_a.push_back(r * d.t_max + i);                 // hidden slot in / out
                 bt.map_b.push_back(a * d.slots + 1 + i * d.n + depth);  // Q row
             }
+            bt.add_tree_items(r0, bt.M(), s.H / s.KV, L, L, d.n);
         }
         upload(bt, st);
         const int M = bt.M();
@@ -363,15 +388,13 @@ struct TransformerPair : ModelPair {
                 bt.add_items(r0, bt.M(), per_item, -1, 0, 0, 0);
                 continue;
             }
-            for (int i = 0; i < d.t; ++i) {
-                const int c0 = bt.M();
+            for (int i = 0; i < d.t; ++i)
                 for (int j = 0; j < d.n; ++j) {
                     bt.rows.push_back(RowDesc{r, L + j, L + i * d.n + j, 1, i, j, 0, 0});
                     bt.map_a.push_back(a * d.slots + 1 + i * d.n + j);
                 }
-                // the root rides with chain 0 (identical mapping below ltree)
-                bt.add_items(i == 0 ? r0 : c0, bt.M(), per_item, i, L, L, d.n);
-            }
+            // one CTA per (sequence, kv head) for the whole tree; the root rides with chain 0
+            bt.add_tree_items(r0, bt.M(), s.H / s.KV, L, L, d.n);
         }
         upload(bt, st);
         if (!naive) stage.upload(rbase.p, base, st);
@@ -450,6 +473,7 @@ TransformerModel *create_transformer(rs_ctx *ctx, const rs_transformer_shape &sh
     if (s.H % s.KV || s.H / s.KV > 64)
         throw std::invalid_argument("transformer shape: n_heads must be a multiple of n_kv_heads (group <= 64)");
     if (s.d % 64 || s.dff % 128) throw std::invalid_argument("transformer shape: d_model % 64 and d_ff % 128 required");
+    if (s.max_ctx > 14000) throw std::invalid_argument("transformer shape: max_ctx must be <= 14000");
     if (!(sh.temperature > 0.0)) throw std::invalid_argument("TabularARModel: temperature must be positive");
     auto m = std::make_unique<TransformerModel>();
     m->ctx = ctx;
