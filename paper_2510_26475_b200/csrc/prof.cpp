@@ -1,6 +1,8 @@
 // prof.cpp -- see prof.h.
 #include "prof.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <cstdio>
 #include <map>
 #include <vector>
@@ -40,7 +42,15 @@ cudaEvent_t take() {
 
 bool prof_enabled() { return g_on && g_depth == 0; }
 void prof_enable(bool on) { g_on = on; }
-void prof_set_scope(const char *s) { g_scope = s; }
+// Scopes double as NVTX ranges ("draft", "verify", "accept", ...) so ncu can target a phase:
+// ncu --nvtx --nvtx-include "verify/" ...
+void prof_set_scope(const char *s) {
+    static thread_local bool open = false;
+    if (open) nvtxRangePop();
+    nvtxRangePushA(s);
+    open = true;
+    g_scope = s;
+}
 
 void prof_begin(const char *kind, double flops, double bytes, cudaStream_t st) {
     Rec r{g_scope + "." + kind, flops, bytes, take(), take()};
