@@ -227,9 +227,10 @@ int rs_kd_update_tabular(rs_ctx *ctx, const rs_model *drafter, const rs_kd_sampl
 /* ---- kernels exposed for tests / microbenchmarks (device pointers) ------------------------ */
 /* C = A . B^T on tcgen05 tensor cores; A [M,K] bf16, B [N,K] bf16 (K-major), epilogue:
    0 = bf16 out (+ bias[N] bf16), 1 = fp32 out * scale, 2 = fp32 out += acc, 3 = SwiGLU bf16 out [M, N/2].
-   block_n: 0 (auto) | 128 | 256. Runs on the context stream. */
+   block_n: 0 (auto) | 128 | 256; splits: deterministic split-K (epilogue 2 only).
+   Runs on the context stream. */
 int rs_gemm_bf16(rs_ctx *ctx, const void *A_dev, const void *B_dev, void *C_dev, const void *bias_dev, int32_t M,
-                 int32_t N, int32_t K, int32_t epilogue, float scale, int32_t block_n);
+                 int32_t N, int32_t K, int32_t epilogue, float scale, int32_t block_n, int32_t splits);
 /* Device pointer + byte size of a named weight tensor of a transformer target / drafter
    ("emb", "final_norm", "rope", per layer "qkv_w", "qkv_b", "o_w", "gu_w", "down_w", "ln1",
    "ln2"; drafter "fc_w", "norm_emb", "norm_hid", "lm_w"), for export / test references. */

@@ -185,7 +185,7 @@ def lib():
             "rs_kd_update_tabular": ([vp, vp, P(_KDSample), i32, _KDPolicy, P(u64), dbl, P(vp), P(_KDResult)],
                                      ctypes.c_int),
             "rs_mt19937_64_seed": ([u64, P(u64)], ctypes.c_int),
-            "rs_gemm_bf16": ([vp, vp, vp, vp, vp, i32, i32, i32, i32, ctypes.c_float, i32], ctypes.c_int),
+            "rs_gemm_bf16": ([vp, vp, vp, vp, vp, i32, i32, i32, i32, ctypes.c_float, i32, i32], ctypes.c_int),
             "rs_model_tensor": ([vp, ctypes.c_char_p, i32, P(vp), P(i64)], ctypes.c_int),
             "rs_memcpy_d2d": ([vp, vp, vp, i64], ctypes.c_int),
             "rs_model_params": ([vp, P(i64)], ctypes.c_int),

@@ -586,7 +586,7 @@ int rs_model_params(const rs_model *m, int64_t *out) {
 }
 
 int rs_gemm_bf16(rs_ctx *ctx, const void *A, const void *B, void *Cp, const void *bias, int32_t M, int32_t N, int32_t K,
-                 int32_t epilogue, float scale, int32_t block_n) {
+                 int32_t epilogue, float scale, int32_t block_n, int32_t splits) {
     return guard([&] {
         need(ctx, "rs_gemm_bf16");
         GemmArgs g;
@@ -598,6 +598,7 @@ int rs_gemm_bf16(rs_ctx *ctx, const void *A, const void *B, void *Cp, const void
         g.lda = K;
         g.ldb = K;
         g.block_n = block_n;
+        g.splits = std::max(1, (int)splits);
         g.epi.kind = epilogue;
         g.epi.out = Cp;
         g.epi.ldo = epilogue == kEpiSwiGLU ? N / 2 : N;

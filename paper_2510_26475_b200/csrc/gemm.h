@@ -25,6 +25,10 @@ struct GemmArgs {
     const void *B = nullptr;  // bf16 [N, ldb], K-major (weights)
     int M = 0, N = 0, K = 0, lda = 0, ldb = 0;
     int block_n = 0;          // 0 = auto (256)
+    // kEpiResidual only: K split into `splits` balanced ranges whose partials are added to the
+    // output in split order (deterministic; keep it a function of (N, K) only so a row's
+    // result stays independent of M).
+    int splits = 1;
     GemmEpi epi;
 };
 

@@ -94,10 +94,10 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 
 template <int BN>
 struct Cfg {
-    static constexpr int kStages = BN >= 256 ? 4 : 6;
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
     static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
     static constexpr int kSmem = 1024 + kStages * kStageBytes + 256;
     static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
@@ -209,12 +209,12 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi &ep, uint32_t tbase
                     rs += acc;
                 }
             }
-        } else {  // kEpiResidual: out (fp32) += acc
+        } else {  // kEpiResidual: out (fp32) += acc (L2-coherent loads: split-K partials of other SMs)
             float *out = static_cast<float *>(ep.out) + static_cast<size_t>(row) * ep.ldo + n0;
             if (n0 + 32 <= N) {
 #pragma unroll
                 for (int j = 0; j < 32; j += 4) {
-                    float4 f = *reinterpret_cast<float4 *>(out + j);
+                    float4 f = __ldcg(reinterpret_cast<const float4 *>(out + j));
                     f.x += __uint_as_float(v[j]);
                     f.y += __uint_as_float(v[j + 1]);
                     f.z += __uint_as_float(v[j + 2]);
@@ -224,7 +224,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi &ep, uint32_t tbase
             } else {
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
-                    if (n0 + j < N) out[j] += __uint_as_float(v[j]);
+                    if (n0 + j < N) out[j] = __ldcg(out + j) + __uint_as_float(v[j]);
             }
         }
     }
@@ -233,7 +233,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi &ep, uint32_t tbase
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmEpi ep, int M,
-                int N, int K) {
+                int N, int K, int splits, int *sem) {
     using C = Cfg<BN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -249,6 +249,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
     const int num_tiles = num_m * num_n;
     const int num_k = (K + BK - 1) / BK;
+    // work unit = (tile, K split); splits of one tile are adjacent units, K ranges balanced
+    const int num_units = num_tiles * splits;
+    auto krange = [&](int s, int &kb0, int &kb1) {
+        kb0 = s * num_k / splits;
+        kb1 = (s + 1) * num_k / splits;
+    };
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -280,9 +286,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x) {
+                const int tile = unit / splits;
                 const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
-                for (int kb = 0; kb < num_k; ++kb) {
+                int kb0, kb1;
+                krange(unit % splits, kb0, kb1);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
                     tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK, m0);
@@ -299,20 +308,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+            for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++it) {
                 const int acc = it & 1;
                 const uint32_t aphase = (it >> 1) & 1;
+                int kb0, kb1;
+                krange(unit % splits, kb0, kb1);
                 mbar_wait(&tempty[acc], aphase ^ 1);
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + acc * BN;
-                for (int kb = 0; kb < num_k; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint64_t ad = sw128_desc(sA + stage * C::kABytes);
                     const uint64_t bd = sw128_desc(sB + stage * C::kBBytes);
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)  // +32 bytes per 16-wide K step inside the swizzle atom
-                        tc_mma(tmem_d, ad + 2 * k, bd + 2 * k, C::kIdesc, (kb | k) != 0);
+                        tc_mma(tmem_d, ad + 2 * k, bd + 2 * k, C::kIdesc, (kb != kb0) || k != 0);
                     tc_commit(&empty[stage]);
                     if (++stage == C::kStages) {
                         stage = 0;
@@ -325,11 +336,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= 4) {
         const int q = warp - 4;  // TMEM lane quadrant == warp % 4
         int it = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++it) {
+            const int tile = unit / splits, split = unit % splits;
             const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
             const int acc = it & 1;
             mbar_wait(&tfull[acc], (it >> 1) & 1);
             tc_fence_after();
+            if (EPI == kEpiResidual && splits > 1) {
+                // deterministic split-K: partials are added in split order (each split's
+                // read-modify-write waits for its predecessor), so a row's result does not
+                // depend on which SM ran which split -- nor on M.
+                int v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(sem + tile) : "memory");
+                    if (v < split) __nanosleep(32);
+                } while (v < split);
+            }
             const uint32_t tb = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
             const int row = m0 + q * 32 + lane;
             constexpr int kChunks = (EPI == kEpiSwiGLU ? BN / 2 : BN) / 32;
@@ -338,6 +360,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = 0; c < kChunks; ++c) epilogue_chunk<EPI, BN>(ep, tb, row, n0, c, M, N, rm, rs);
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
+            if (EPI == kEpiResidual && splits > 1) {
+                __threadfence();
+                asm volatile("bar.sync 1, 128;" ::: "memory");  // all 4 epilogue warps wrote their rows
+                if (q == 0 && lane == 0)
+                    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sem + tile), "r"(split + 1) : "memory");
+            }
             if constexpr (EPI == kEpiF32) {
                 if (ep.stats && row < M) {
                     const int orow = ep.row_map ? ep.row_map[row] : row;
@@ -411,8 +439,23 @@ void launch(const GemmArgs &g, cudaStream_t st) {
     const CUtensorMap ta = make_map(g.A, g.M, g.K, g.lda, BM);
     const CUtensorMap tb = make_map(g.B, g.N, g.K, g.ldb, BN);
     const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
-    const int grid = std::min(tiles, num_sms());
-    gemm_kernel<BN, EPI><<<grid, kThreads, C::kSmem, st>>>(ta, tb, g.epi, g.M, g.N, g.K);
+    const int num_k = (g.K + BK - 1) / BK;
+    int splits = EPI == kEpiResidual ? std::max(1, std::min(g.splits, num_k)) : 1;
+    int *sem = nullptr;
+    if (splits > 1) {
+        // per-tile split counters, zeroed before every launch (grid <= #SMs, all CTAs resident)
+        static thread_local int *sems = nullptr;
+        static thread_local int sems_n = 0;
+        if (sems_n < tiles) {
+            if (sems) cudaFree(sems);
+            sems_n = std::max(tiles, 4096);
+            RS_CUDA(cudaMalloc(&sems, (size_t)sems_n * sizeof(int)));
+        }
+        RS_CUDA(cudaMemsetAsync(sems, 0, (size_t)tiles * sizeof(int), st));
+        sem = sems;
+    }
+    const int grid = std::min(tiles * splits, num_sms());
+    gemm_kernel<BN, EPI><<<grid, kThreads, C::kSmem, st>>>(ta, tb, g.epi, g.M, g.N, g.K, splits, sem);
     RS_LAUNCHED();
 }
 
@@ -422,17 +465,40 @@ void gemm_bf16(const GemmArgs &g, cudaStream_t st) {
     if (g.M <= 0 || g.N <= 0) return;
     if (g.K % 8 || g.lda % 8 || g.ldb % 8) throw std::invalid_argument("gemm_bf16: K and leading dims must be multiples of 8");
     if (g.epi.kind == kEpiSwiGLU && (g.N % 256)) throw std::invalid_argument("gemm_bf16: SwiGLU needs N % 256 == 0");
-    const int bn = g.block_n ? g.block_n : 256;
+    int bn = g.block_n;
+    if (!bn) {
+        // tile width that best fills the SMs: wave count x per-tile time (proportional to BN)
+        const int tm = (g.M + BM - 1) / BM;
+        double best = 1e30;
+        bn = 256;
+        for (int cand : {256, 224, 192, 160, 128}) {
+            const int tiles = tm * ((g.N + cand - 1) / cand);
+            const double cost = (double)((tiles + num_sms() - 1) / num_sms()) * cand * (cand < 256 ? 1.02 : 1.0);
+            if (cost < best) {
+                best = cost;
+                bn = cand;
+            }
+        }
+    }
+    if (g.epi.kind == kEpiSwiGLU || g.epi.stats) bn = 256;
     const double out_el = g.epi.kind == kEpiSwiGLU ? 0.5 * g.M * g.N : (double)g.M * g.N;
     const double out_b = g.epi.kind == kEpiBF16 || g.epi.kind == kEpiSwiGLU ? 2.0 : g.epi.kind == kEpiF32 ? 4.0 : 8.0;
     ProfScope prof("gemm", 2.0 * g.M * g.N * g.K, 2.0 * ((double)g.M * g.K + (double)g.N * g.K) + out_el * out_b, st);
+    auto by_bn = [&](auto epi_tag) {
+        constexpr int E = decltype(epi_tag)::value;
+        switch (bn) {
+            case 128: launch<128, E>(g, st); break;
+            case 160: launch<160, E>(g, st); break;
+            case 192: launch<192, E>(g, st); break;
+            case 224: launch<224, E>(g, st); break;
+            case 256: launch<256, E>(g, st); break;
+            default: throw std::invalid_argument("gemm_bf16: block_n must be 128/160/192/224/256");
+        }
+    };
     switch (g.epi.kind) {
-        case kEpiBF16: bn == 128 ? launch<128, kEpiBF16>(g, st) : launch<256, kEpiBF16>(g, st); break;
-        case kEpiF32:
-            if (g.epi.stats && bn != 256) throw std::invalid_argument("gemm_bf16: row stats need block_n 256");
-            bn == 128 ? launch<128, kEpiF32>(g, st) : launch<256, kEpiF32>(g, st);
-            break;
-        case kEpiResidual: bn == 128 ? launch<128, kEpiResidual>(g, st) : launch<256, kEpiResidual>(g, st); break;
+        case kEpiBF16: by_bn(std::integral_constant<int, kEpiBF16>{}); break;
+        case kEpiF32: by_bn(std::integral_constant<int, kEpiF32>{}); break;
+        case kEpiResidual: by_bn(std::integral_constant<int, kEpiResidual>{}); break;
         case kEpiSwiGLU: launch<256, kEpiSwiGLU>(g, st); break;
         default: throw std::invalid_argument("gemm_bf16: unknown epilogue");
     }

@@ -12,13 +12,13 @@ import paper_2510_26475_b200 as rb
 pytestmark = pytest.mark.gpu
 
 
-def _run(A, B, out, bias=None, epi=0, scale=1.0, block_n=0):
+def _run(A, B, out, bias=None, epi=0, scale=1.0, block_n=0, splits=1):
     dev = rb.default_device()
     torch.cuda.synchronize()
     rb._check(rb.lib().rs_gemm_bf16(dev.handle, ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
                                     ctypes.c_void_p(out.data_ptr()),
                                     ctypes.c_void_p(bias.data_ptr()) if bias is not None else None,
-                                    A.shape[0], B.shape[0], A.shape[1], epi, scale, block_n))
+                                    A.shape[0], B.shape[0], A.shape[1], epi, scale, block_n, splits))
     dev.sync()
 
 
@@ -57,6 +57,49 @@ def test_gemm_residual_add():
     _run(A, B, out, None, 2)
     ref = R + A.float() @ B.float().t()
     assert (out - ref).abs().max().item() <= 2e-3 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("epi", [0, 1, 2])
+def test_gemm_tile_width_does_not_change_results(epi):
+    """Every supported BLOCK_N gives bitwise-identical outputs (same K order per element), so
+    the M-dependent automatic tile choice keeps rows invariant to the batch they sit in."""
+    torch.manual_seed(5)
+    M, N, K = 700, 2560, 2048
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    B = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
+    bias = (torch.randn(N, device="cuda") * 0.1).bfloat16()
+    outs = []
+    for bn in (256, 224, 192, 160, 128):
+        if epi == 0:
+            out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        else:
+            out = torch.ones(M, N, device="cuda", dtype=torch.float32)
+        _run(A, B, out, bias if epi == 0 else None, epi, 1.0, bn)
+        outs.append(out)
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+
+
+@pytest.mark.parametrize("splits", [2, 3, 5])
+def test_gemm_residual_split_k_deterministic_and_row_invariant(splits):
+    """Split-K partials are added in split order: repeated runs are bitwise identical and a
+    row's result does not depend on M (the same rows inside a larger batch)."""
+    torch.manual_seed(4)
+    M, N, K = 1344, 2048, 11008
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    B = (torch.randn(N, K, device="cuda") * 0.01).bfloat16()
+    R = torch.randn(M, N, device="cuda")
+    outs = []
+    for _ in range(2):
+        out = R.clone()
+        _run(A, B, out, None, 2, splits=splits)
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
+    ref = R + A.float() @ B.float().t()
+    assert (outs[0] - ref).abs().max().item() <= 2e-3 * ref.abs().max().item()
+    small = R[:64].clone()
+    _run(A[:64].contiguous(), B, small, None, 2, splits=splits)
+    assert torch.equal(small, outs[0][:64])
 
 
 def test_gemm_swiglu():

@@ -27,7 +27,7 @@ for name, (N, K, epi) in shapes.items():
             rb._check(rb.lib().rs_gemm_bf16(dev.handle, ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
                                             ctypes.c_void_p(out.data_ptr()),
                                             ctypes.c_void_p(bias.data_ptr()) if epi == 0 else None, M, N, K, epi, 1.0,
-                                            bn))
+                                            bn, 1))
         torch.cuda.synchronize()
         for _ in range(3):
             run()
