@@ -5,6 +5,7 @@
 
 #include "common.cuh"
 #include "model.h"
+#include "prof.h"
 #include "rng.cuh"
 
 namespace rs {
@@ -60,51 +61,105 @@ __global__ void embed_kernel(const RowDesc *rows, int M, const int32_t *tok, int
     }
 }
 
-// One warp per row; y = x * rsqrt(mean(x^2) + eps) * w (Qwen2RMSNorm, fp32 math).
+__device__ __forceinline__ void load8(const float *p, float (&v)[8]) {
+    const float4 a = *reinterpret_cast<const float4 *>(p), b = *reinterpret_cast<const float4 *>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load8(const bf16 *p, float (&v)[8]) {
+    const int4 raw = *reinterpret_cast<const int4 *>(p);
+    const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&raw);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(h[k]);
+        v[2 * k] = f.x;
+        v[2 * k + 1] = f.y;
+    }
+}
+__device__ __forceinline__ void store8(bf16 *p, const float (&v)[8]) {
+    __align__(16) __nv_bfloat162 h[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+    *reinterpret_cast<int4 *>(p) = *reinterpret_cast<const int4 *>(h);
+}
+
+// One CTA per row, 16-byte vectors held in registers: y = x * rsqrt(mean(x^2) + eps) * w
+// (Qwen2RMSNorm, fp32 math). d % 8 == 0, d <= 8 * 4 * blockDim.
 template <class T>
-__global__ void rmsnorm_kernel(const T *x, int ldx, const float *w, int M, int d, float eps, bf16 *out, int ldo) {
-    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (row >= M) return;
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const T *x, int ldx, const float *w, int M, int d, float eps,
+                                                      bf16 *out, int ldo) {
+    __shared__ float red[32];
+    const int row = blockIdx.x;
     const T *xr = x + (size_t)row * ldx;
+    float v[4][8];
     float ss = 0.f;
-    for (int i = lane; i < d; i += 32) {
-        const float v = static_cast<float>(xr[i]);
-        ss += v * v;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int i = (threadIdx.x + k * blockDim.x) * 8;
+        if (i < d) {
+            load8(xr + i, v[k]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ss += v[k][j] * v[k][j];
+        }
     }
     ss = warp_sumf(ss);
-    const float inv = rsqrtf(ss / d + eps);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    ss = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    if (threadIdx.x < 32) {
+        ss = warp_sumf(ss);
+        if (threadIdx.x == 0) red[0] = ss;
+    }
+    __syncthreads();
+    const float inv = rsqrtf(red[0] / d + eps);
     bf16 *o = out + (size_t)row * ldo;
-    for (int i = lane; i < d; i += 32) o[i] = __float2bfloat16(static_cast<float>(xr[i]) * inv * w[i]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int i = (threadIdx.x + k * blockDim.x) * 8;
+        if (i < d) {
+            float wv[8];
+            load8(w + i, wv);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[k][j] = v[k][j] * inv * wv[j];
+            store8(o + i, v[k]);
+        }
+    }
 }
 
 // RoPE (rotate-half, Qwen2) on q and k; q -> qbuf [M][H][hd]; k, v -> cache at the row's slot.
-__global__ void rope_store_kernel(const bf16 *qkv, const RowDesc *rows, int M, int H, int KV, int hd,
-                                  const float *rope, KvCache kv, int layer, bf16 *q) {
+// One CTA per row; a thread rotates 8 dimension pairs (i, i + hd/2) with 16-byte accesses.
+__global__ void __launch_bounds__(256) rope_store_kernel(const bf16 *qkv, const RowDesc *rows, int M, int H, int KV,
+                                                         int hd, const float *rope, KvCache kv, int layer, bf16 *q) {
     const int m = blockIdx.x;
     const RowDesc r = rows[m];
     const int qd = (H + 2 * KV) * hd;
     const bf16 *src = qkv + (size_t)m * qd;
-    const int half = hd / 2;
+    const int half = hd / 2, groups = half / 8;
     const float *cs = rope + (size_t)r.pos * half * 2;
-    for (int idx = threadIdx.x; idx < (H + KV) * half; idx += blockDim.x) {
-        const int head = idx / half, i = idx % half;
+    for (int idx = threadIdx.x; idx < (H + KV) * groups; idx += blockDim.x) {
+        const int head = idx / groups, i = (idx % groups) * 8;
         const bf16 *h = src + head * hd;
-        const float x1 = __bfloat162float(h[i]), x2 = __bfloat162float(h[i + half]);
-        const float c = cs[2 * i], s = cs[2 * i + 1];
-        const bf16 o1 = __float2bfloat16(x1 * c - x2 * s), o2 = __float2bfloat16(x2 * c + x1 * s);
-        if (head < H) {
-            bf16 *dst = q + ((size_t)m * H + head) * hd;
-            dst[i] = o1;
-            dst[i + half] = o2;
-        } else {
-            bf16 *dst = kv.k + kv.off(layer, r.seq, head - H, r.phys);
-            dst[i] = o1;
-            dst[i + half] = o2;
+        float x1[8], x2[8], c[8], s[8], o1[8], o2[8];
+        load8(h + i, x1);
+        load8(h + i + half, x2);
+        float t[16];
+        load8(cs + 2 * i, *reinterpret_cast<float(*)[8]>(t));
+        load8(cs + 2 * i + 8, *reinterpret_cast<float(*)[8]>(t + 8));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            c[j] = t[2 * j];
+            s[j] = t[2 * j + 1];
+            o1[j] = x1[j] * c[j] - x2[j] * s[j];
+            o2[j] = x2[j] * c[j] + x1[j] * s[j];
         }
+        bf16 *dst = head < H ? q + ((size_t)m * H + head) * hd : kv.k + kv.off(layer, r.seq, head - H, r.phys);
+        store8(dst + i, o1);
+        store8(dst + i + half, o2);
     }
-    for (int idx = threadIdx.x; idx < KV * hd; idx += blockDim.x) {
-        const int head = idx / hd, i = idx % hd;
-        kv.v[kv.off(layer, r.seq, head, r.phys) + i] = src[(H + KV) * hd + idx];
+    const int vec = hd / 8;
+    for (int idx = threadIdx.x; idx < KV * vec; idx += blockDim.x) {
+        const int head = idx / vec, c8 = idx % vec;
+        *reinterpret_cast<int4 *>(kv.v + kv.off(layer, r.seq, head, r.phys) + c8 * 8) =
+            *reinterpret_cast<const int4 *>(src + (H + KV) * hd + head * hd + c8 * 8);
     }
 }
 
@@ -189,26 +244,34 @@ void k_rope_table(float *rope, int max_ctx, int hd, float theta, cudaStream_t st
 void k_embed(const RowDesc *rows, int M, const int32_t *tok, int tok_cap, const int32_t *chain_tok, int t_max,
              int n_max, const bf16 *emb, int V, int d, float *x, cudaStream_t st) {
     if (M <= 0) return;
+    ProfScope prof("embed", 0, (double)M * d * 6.0, st);
     embed_kernel<<<M, 128, 0, st>>>(rows, M, tok, tok_cap, chain_tok, t_max, n_max, emb, V, d, x);
     RS_LAUNCHED();
 }
 
 void k_rmsnorm(const float *x, int ldx, const float *w, int M, int d, float eps, bf16 *out, int ldo, cudaStream_t st) {
     if (M <= 0) return;
-    rmsnorm_kernel<float><<<(M + 7) / 8, 256, 0, st>>>(x, ldx, w, M, d, eps, out, ldo);
+    ProfScope prof("norm", 0, (double)M * d * 6.0, st);
+    if (d % 8 || d > 8192) throw std::invalid_argument("rmsnorm: d must be a multiple of 8 and <= 8192");
+    rmsnorm_kernel<float><<<M, std::min(256, std::max(32, (d / 8 + 31) / 32 * 32)), 0, st>>>(x, ldx, w, M, d, eps,
+                                                                                            out, ldo);
     RS_LAUNCHED();
 }
 
 void k_rmsnorm_bf16(const bf16 *x, int ldx, const float *w, int M, int d, float eps, bf16 *out, int ldo,
                     cudaStream_t st) {
     if (M <= 0) return;
-    rmsnorm_kernel<bf16><<<(M + 7) / 8, 256, 0, st>>>(x, ldx, w, M, d, eps, out, ldo);
+    ProfScope prof("norm", 0, (double)M * d * 4.0, st);
+    if (d % 8 || d > 8192) throw std::invalid_argument("rmsnorm: d must be a multiple of 8 and <= 8192");
+    rmsnorm_kernel<bf16><<<M, std::min(256, std::max(32, (d / 8 + 31) / 32 * 32)), 0, st>>>(x, ldx, w, M, d, eps, out,
+                                                                                           ldo);
     RS_LAUNCHED();
 }
 
 void k_rope_store(const bf16 *qkv, const RowDesc *rows, int M, const TfShape &s, const float *rope, const KvCache &kv,
                   int layer, bf16 *q, cudaStream_t st) {
     if (M <= 0) return;
+    ProfScope prof("rope", 0, (double)M * s.qkv_dim() * 4.0, st);
     rope_store_kernel<<<M, 256, 0, st>>>(qkv, rows, M, s.H, s.KV, s.hd, rope, kv, layer, q);
     RS_LAUNCHED();
 }
@@ -216,6 +279,7 @@ void k_rope_store(const bf16 *qkv, const RowDesc *rows, int M, const TfShape &s,
 void k_store_features(const float *x, const RowDesc *rows, int M, int d, bf16 *feat, int max_ctx, int slot,
                       cudaStream_t st) {
     if (M <= 0) return;
+    ProfScope prof("feat", 0, (double)M * d * 6.0, st);
     store_features_kernel<<<M, 256, 0, st>>>(x, rows, M, d, feat, max_ctx, slot);
     RS_LAUNCHED();
 }
@@ -223,6 +287,7 @@ void k_store_features(const float *x, const RowDesc *rows, int M, int d, bf16 *f
 void k_gather_features(const RowDesc *rows, int M, int d, const bf16 *feat, int max_ctx, const float *, bf16 *fin,
                        int *, cudaStream_t st) {
     if (M <= 0) return;
+    ProfScope prof("feat", 0, (double)M * d * 12.0, st);
     gather_features_kernel<<<M, 256, 0, st>>>(rows, M, d, feat, max_ctx, fin);
     RS_LAUNCHED();
 }
@@ -230,6 +295,7 @@ void k_gather_features(const RowDesc *rows, int M, int d, const bf16 *feat, int 
 void k_rows_copy_f32(const float *src, int ld_src, const int *src_rows, float *dst, int ld_dst, const int *dst_rows,
                      int n, int d, cudaStream_t st) {
     if (n <= 0) return;
+    ProfScope prof("copy", 0, (double)n * d * 8.0, st);
     rows_copy_kernel<<<n, 256, 0, st>>>(src, ld_src, src_rows, dst, ld_dst, dst_rows, d);
     RS_LAUNCHED();
 }
