@@ -247,6 +247,16 @@ int rs_prof_json(char *buf, int64_t cap, int64_t *len);
 
 /* mt19937_64 state helper for rs_kd_update_tabular: 313 uint64 (312 words + index). */
 int rs_mt19937_64_seed(uint64_t seed, uint64_t *state313);
+/* The pieces of kd_update for a prompt-sharded learner:
+   rs_kd_select   -- host: ceil(n / interval) partial Fisher-Yates indices (learner.cpp:107-121),
+                     replicated on every rank from the same selection state;
+   rs_kd_grad_tabular -- device: sum_i w_i * (q - p~)/tau per visited row (learner.cpp:62-82) and
+                     sum_i w_i * KL_i (learner.cpp:33-60) over this rank's selected samples;
+   rs_tabular_apply_delta -- logits + grad * scale into a new model, version + 1 (model.cpp:161-170). */
+int rs_kd_select(int32_t n, int32_t interval, uint64_t *selection_rng_state, int32_t *out_idx, int32_t *take);
+int rs_kd_grad_tabular(rs_ctx *ctx, const rs_model *drafter, const rs_kd_sample *samples, int32_t n,
+                       const double *weights, double *grad_out, double *loss_out);
+int rs_tabular_apply_delta(rs_ctx *ctx, const rs_model *m, const double *grad, double scale, rs_model **out);
 
 #ifdef __cplusplus
 }

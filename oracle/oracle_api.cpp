@@ -180,6 +180,30 @@ json op_kd_update(const json & req) {
             {"selected", r.selected}, {"per_sample_loss_w1", losses}};
 }
 
+// kd_loss_gradient + weighted kd_loss over an explicit (sample, weight) list (learner.cpp:58-82).
+json op_kd_grad(const json & req) {
+    auto dm = model_of(req.at("drafter"));
+    auto * drafter = dynamic_cast<TabularModel *>(dm.get());
+    if (!drafter) throw std::invalid_argument("kd_grad: tabular drafter required");
+    std::vector<Rollout> buf;
+    for (const auto & s : req.at("samples")) {
+        Rollout r;
+        r.prompt = s.at("prompt").get<std::vector<int>>();
+        r.response = s.at("response").get<std::vector<int>>();
+        for (const auto & st : s.at("steps")) r.target_logprobs.push_back(st.at("target_logprobs").get<std::vector<double>>());
+        r.eos_bias = s.value("eos_bias", 0.0);
+        buf.push_back(std::move(r));
+    }
+    const std::vector<double> w = req.at("weights").get<std::vector<double>>();
+    std::vector<std::pair<const Rollout *, double>> ws;
+    double loss = 0.0;
+    for (size_t i = 0; i < buf.size(); ++i) {
+        ws.emplace_back(&buf[i], w.at(i));
+        loss += kd_loss(*drafter, buf[i], w[i]);
+    }
+    return {{"grad", kd_loss_gradient(*drafter, ws)}, {"loss", loss}};
+}
+
 json op_profile_table(const json & req) {
     ProfileTable t(req.at("buckets").get<std::vector<int>>());
     for (const auto & e : req.at("entries")) t.set_entry(e.at("bucket"), cfg_of(e), e.at("time_per_token"));
@@ -197,6 +221,7 @@ json dispatch(const json & req) {
     if (op == "spec_step_tree") return op_spec_step_tree(req);
     if (op == "kd_update") return op_kd_update(req);
     if (op == "profile_table") return op_profile_table(req);
+    if (op == "kd_grad") return op_kd_grad(req);
     throw std::invalid_argument("oracle: unknown op " + op);
 }
 

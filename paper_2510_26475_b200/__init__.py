@@ -121,6 +121,7 @@ EXPORTED_SYMBOLS = [
     "rs_engine_set_capture", "rs_engine_capture_count", "rs_engine_capture_read",
     "rs_kd_weight", "rs_kd_update_tabular", "rs_mt19937_64_seed", "rs_gemm_bf16",
     "rs_model_tensor", "rs_memcpy_d2d", "rs_model_params", "rs_prof_enable", "rs_prof_reset", "rs_prof_json",
+    "rs_kd_select", "rs_kd_grad_tabular", "rs_tabular_apply_delta",
 ]
 
 _lib = None
@@ -192,6 +193,9 @@ def lib():
             "rs_prof_enable": ([i32], None),
             "rs_prof_reset": ([], None),
             "rs_prof_json": ([ctypes.c_char_p, i64, P(i64)], ctypes.c_int),
+            "rs_kd_select": ([i32, i32, P(u64), P(i32), P(i32)], ctypes.c_int),
+            "rs_kd_grad_tabular": ([vp, vp, P(_KDSample), i32, P(dbl), P(dbl), P(dbl)], ctypes.c_int),
+            "rs_tabular_apply_delta": ([vp, vp, P(dbl), dbl, P(vp)], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

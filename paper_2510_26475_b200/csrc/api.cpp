@@ -626,6 +626,52 @@ int rs_drafter_create(rs_ctx *ctx, const rs_model *target, uint64_t seed, int32_
     });
 }
 
+int rs_kd_select(int32_t n, int32_t interval, uint64_t *state, int32_t *out_idx, int32_t *take) {
+    return guard([&] {
+        need(state, "rs_kd_select: selection rng");
+        const std::vector<int> idx = kd_select(n, interval, state);
+        if (take) *take = (int32_t)idx.size();
+        if (out_idx) std::copy(idx.begin(), idx.end(), out_idx);
+    });
+}
+
+int rs_kd_grad_tabular(rs_ctx *ctx, const rs_model *drafter, const rs_kd_sample *samples, int32_t n,
+                       const double *weights, double *grad_out, double *loss_out) {
+    return guard([&] {
+        need(ctx, "rs_kd_grad_tabular");
+        need(drafter, "rs_kd_grad_tabular: drafter");
+        if (drafter->kind != rs_model::Tabular) throw std::invalid_argument("rs_kd_grad_tabular: tabular drafter required");
+        const auto *t = static_cast<const TabularModel *>(drafter);
+        std::vector<const rs_kd_sample *> sel;
+        std::vector<double> w;
+        for (int i = 0; i < n; ++i) {
+            sel.push_back(&samples[i]);
+            w.push_back(weights[i]);
+        }
+        DBuf<double> g(t->host.size());
+        const double loss = kd_core(ctx, t, sel, w, g.p, true, 1.0);
+        if (grad_out) RS_CUDA(cudaMemcpy(grad_out, g.p, g.bytes(), cudaMemcpyDeviceToHost));
+        if (loss_out) *loss_out = loss;
+    });
+}
+
+int rs_tabular_apply_delta(rs_ctx *ctx, const rs_model *m, const double *grad, double scale, rs_model **out) {
+    return guard([&] {
+        need(ctx, "rs_tabular_apply_delta");
+        need(m, "rs_tabular_apply_delta: model");
+        need(out, "rs_tabular_apply_delta: out");
+        if (m->kind != rs_model::Tabular) throw std::invalid_argument("rs_tabular_apply_delta: tabular model required");
+        const auto *t = static_cast<const TabularModel *>(m);
+        // with_logits_delta (model.cpp:161-170): z[i] += delta[i], delta = grad * scale
+        std::vector<double> z = t->host;
+        for (size_t i = 0; i < z.size(); ++i) z[i] += grad[i] * scale;
+        rs_model *nm = nullptr;
+        const int rc = rs_tabular_create(ctx, t->vocab, t->order, t->temperature, z.data(), t->version + 1, &nm);
+        if (rc != RS_OK) throw std::runtime_error(rs_last_error());
+        *out = nm;
+    });
+}
+
 int rs_mt19937_64_seed(uint64_t seed, uint64_t *state) {
     return guard([&] {
         need(state, "rs_mt19937_64_seed");

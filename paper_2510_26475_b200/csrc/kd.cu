@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(1024, 1) kd_job_kernel(const double *table, in
 // (learner.cpp:62-82, :146-151, model.cpp:161-170).
 __global__ void __launch_bounds__(1024, 1) kd_row_kernel(const double *table, double *out, int V, double tau, const Job *jobs,
                               const int *row_jobs, const int *row_ptr, const long long *rows, const double *lp,
-                              const double *job_m, const double *job_s, const double *w, double neg_lr) {
+                              const double *job_m, const double *job_s, const double *w, double neg_lr,
+                              int grad_only) {
     const long long row = rows[blockIdx.x];
     const double inv_tau = 1.0 / tau;
     for (int x = threadIdx.x; x < V; x += blockDim.x) {
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(1024, 1) kd_row_kernel(const double *table, do
             const double p = isinf(l) ? 0.0 : exp(l);
             g += w[jb.sample] * (q - p) * inv_tau;
         }
-        out[row * V + x] = table[row * V + x] + g * neg_lr;
+        out[row * V + x] = grad_only ? g : table[row * V + x] + g * neg_lr;
     }
 }
 
@@ -140,6 +141,105 @@ void kd_rows_loss_grad(const float *target_rows, const float *drafter_rows, cons
     RS_LAUNCHED();
 }
 
+std::vector<int> kd_select(int n, int interval, uint64_t *sel_state) {
+    // learner.cpp:107-121: partial Fisher-Yates with selection_rng() % (n - i)
+    if (interval < 1) throw std::invalid_argument("kd_update: interval must be >= 1");
+    HostMt rng;
+    std::copy(sel_state, sel_state + kMtN, rng.mt);
+    rng.idx = static_cast<int>(sel_state[kMtN]);
+    const size_t N = static_cast<size_t>(std::max(n, 0));
+    const size_t take = (N + static_cast<size_t>(interval) - 1) / static_cast<size_t>(interval);
+    std::vector<size_t> idx(N);
+    std::iota(idx.begin(), idx.end(), size_t{0});
+    for (size_t i = 0; i < take; ++i) {
+        const size_t j = i + static_cast<size_t>(rng.next() % (N - i));
+        std::swap(idx[i], idx[j]);
+    }
+    std::copy(rng.mt, rng.mt + kMtN, sel_state);
+    sel_state[kMtN] = static_cast<uint64_t>(rng.idx);
+    return std::vector<int>(idx.begin(), idx.begin() + static_cast<long>(take));
+}
+
+// Device K5 over the given (sample, weight) list: per-row gradient accumulated in the list's
+// order (learner.cpp:62-82). grad_only: out = grad (rows untouched by any sample = 0);
+// else out = table + grad * scale (the SGD step, model.cpp:161-170). Returns sum_i w_i KL_i.
+double kd_core(rs_ctx *ctx, const TabularModel *drafter, const std::vector<const rs_kd_sample *> &sel,
+               const std::vector<double> &w, double *out_dev, bool grad_only, double scale) {
+    const int V = drafter->vocab;
+    cudaStream_t st = ctx->stream;
+    std::vector<int32_t> tokens;
+    std::vector<double> lp;
+    std::vector<Job> jobs;
+    std::vector<std::vector<int>> per_sample(sel.size());
+    for (size_t i = 0; i < sel.size(); ++i) {
+        const rs_kd_sample &s = *sel[i];
+        const int seq_off = static_cast<int>(tokens.size());
+        tokens.insert(tokens.end(), s.prompt, s.prompt + s.prompt_len);
+        tokens.insert(tokens.end(), s.response, s.response + s.response_len);
+        for (int t = 0; t < s.response_len; ++t) {
+            const int lp_off = static_cast<int>(lp.size() / V);
+            lp.insert(lp.end(), s.target_logprobs + (size_t)t * V, s.target_logprobs + (size_t)(t + 1) * V);
+            per_sample[i].push_back(static_cast<int>(jobs.size()));
+            jobs.push_back(Job{seq_off, s.prompt_len + t, lp_off, static_cast<int>(i), s.eos_bias});
+        }
+    }
+    for (int v : tokens)
+        if (v < 0 || v >= V) throw std::invalid_argument("row_index: token out of vocabulary");
+    const size_t cells = drafter->host.size();
+    if (grad_only) RS_CUDA(cudaMemsetAsync(out_dev, 0, cells * 8, st));
+    else RS_CUDA(cudaMemcpyAsync(out_dev, drafter->table.p, cells * 8, cudaMemcpyDeviceToDevice, st));
+    const int J = static_cast<int>(jobs.size());
+    if (J == 0) {
+        RS_CUDA(cudaStreamSynchronize(st));
+        return 0.0;
+    }
+    std::vector<double> kl(J);
+    std::vector<long long> rows(J);
+    DBuf<int32_t> d_tok(tokens.size());
+    DBuf<double> d_lp(lp.size()), d_m(J), d_s(J), d_kl(J), d_w(std::max<size_t>(w.size(), 1));
+    DBuf<Job> d_jobs(J);
+    DBuf<long long> d_row(J);
+    RS_CUDA(cudaMemcpyAsync(d_tok.p, tokens.data(), tokens.size() * 4, cudaMemcpyHostToDevice, st));
+    RS_CUDA(cudaMemcpyAsync(d_lp.p, lp.data(), lp.size() * 8, cudaMemcpyHostToDevice, st));
+    RS_CUDA(cudaMemcpyAsync(d_jobs.p, jobs.data(), J * sizeof(Job), cudaMemcpyHostToDevice, st));
+    RS_CUDA(cudaMemcpyAsync(d_w.p, w.data(), w.size() * 8, cudaMemcpyHostToDevice, st));
+    const int th = V <= 256 ? 32 : V <= 4096 ? 256 : 1024;
+    kd_job_kernel<<<J, th, 0, st>>>(drafter->table.p, drafter->order, V, drafter->temperature, d_tok.p, d_jobs.p,
+                                    d_lp.p, d_m.p, d_s.p, d_kl.p, d_row.p);
+    RS_LAUNCHED();
+    RS_CUDA(cudaMemcpyAsync(kl.data(), d_kl.p, J * 8, cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaMemcpyAsync(rows.data(), d_row.p, J * 8, cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaStreamSynchronize(st));
+    // group jobs by row, keeping job order (= sample order, then position)
+    std::map<long long, std::vector<int>> by_row;
+    for (int j = 0; j < J; ++j) by_row[rows[j]].push_back(j);
+    std::vector<int> row_jobs, row_ptr{0};
+    std::vector<long long> urows;
+    for (auto &[r, js] : by_row) {
+        urows.push_back(r);
+        row_jobs.insert(row_jobs.end(), js.begin(), js.end());
+        row_ptr.push_back(static_cast<int>(row_jobs.size()));
+    }
+    DBuf<int32_t> d_rj(row_jobs.size()), d_rp(row_ptr.size());
+    DBuf<long long> d_ur(urows.size());
+    RS_CUDA(cudaMemcpyAsync(d_rj.p, row_jobs.data(), row_jobs.size() * 4, cudaMemcpyHostToDevice, st));
+    RS_CUDA(cudaMemcpyAsync(d_rp.p, row_ptr.data(), row_ptr.size() * 4, cudaMemcpyHostToDevice, st));
+    RS_CUDA(cudaMemcpyAsync(d_ur.p, urows.data(), urows.size() * 8, cudaMemcpyHostToDevice, st));
+    kd_row_kernel<<<(int)urows.size(), th, 0, st>>>(drafter->table.p, out_dev, V, drafter->temperature, d_jobs.p,
+                                                    d_rj.p, d_rp.p, d_ur.p, d_lp.p, d_m.p, d_s.p, d_w.p, scale,
+                                                    grad_only ? 1 : 0);
+    RS_LAUNCHED();
+    RS_CUDA(cudaStreamSynchronize(st));
+    // loss on the pre-update drafter: sum_i w_i * sum_t KL_t (learner.cpp:142-145)
+    double loss = 0.0;
+    for (size_t i = 0; i < sel.size(); ++i) {
+        double total = 0.0;
+        for (int j : per_sample[i]) total += kl[j];
+        loss += w[i] * total;
+    }
+    return loss;
+}
+
 void kd_update_tabular(rs_ctx *ctx, const TabularModel *drafter, const rs_kd_sample *buf, int n,
                        const rs_kd_policy &policy, uint64_t *sel_state, double cost, rs_model **out_model,
                        rs_kd_result *out) {
@@ -166,102 +266,24 @@ void kd_update_tabular(rs_ctx *ctx, const TabularModel *drafter, const rs_kd_sam
         if (out) *out = res;
         return;
     }
-    // selection (learner.cpp:107-121): partial Fisher-Yates with selection_rng() % (n - i)
-    HostMt rng;
-    std::copy(sel_state, sel_state + kMtN, rng.mt);
-    rng.idx = static_cast<int>(sel_state[kMtN]);
-    const size_t N = static_cast<size_t>(n);
-    const size_t take = (N + static_cast<size_t>(policy.interval) - 1) / static_cast<size_t>(policy.interval);
-    std::vector<size_t> idx(N);
-    std::iota(idx.begin(), idx.end(), size_t{0});
-    for (size_t i = 0; i < take; ++i) {
-        const size_t j = i + static_cast<size_t>(rng.next() % (N - i));
-        std::swap(idx[i], idx[j]);
-    }
-    std::copy(rng.mt, rng.mt + kMtN, sel_state);
-    sel_state[kMtN] = static_cast<uint64_t>(rng.idx);
-
+    const std::vector<int> idx = kd_select(n, policy.interval, sel_state);
+    const size_t take = idx.size();
     std::vector<double> br(take), w(take);
     for (size_t i = 0; i < take; ++i) br[i] = buf[idx[i]].reward;
     double wsum = 0, wmin = 0, wmax = 0;
     size_t distilled = 0;
-    std::vector<int32_t> tokens;
-    std::vector<double> lp;
-    std::vector<Job> jobs;
-    std::vector<std::vector<int>> per_sample_jobs(take);
+    std::vector<const rs_kd_sample *> sel(take);
     for (size_t i = 0; i < take; ++i) {
-        const rs_kd_sample &s = buf[idx[i]];
-        w[i] = kd_weight(s.reward, br, policy);
+        sel[i] = &buf[idx[i]];
+        w[i] = kd_weight(sel[i]->reward, br, policy);
         wsum += w[i];
         wmin = i == 0 ? w[i] : std::min(wmin, w[i]);
         wmax = i == 0 ? w[i] : std::max(wmax, w[i]);
-        distilled += static_cast<size_t>(s.response_len);
-        const int seq_off = static_cast<int>(tokens.size());
-        tokens.insert(tokens.end(), s.prompt, s.prompt + s.prompt_len);
-        tokens.insert(tokens.end(), s.response, s.response + s.response_len);
-        for (int t = 0; t < s.response_len; ++t) {
-            const int lp_off = static_cast<int>(lp.size() / V);
-            lp.insert(lp.end(), s.target_logprobs + (size_t)t * V, s.target_logprobs + (size_t)(t + 1) * V);
-            per_sample_jobs[i].push_back(static_cast<int>(jobs.size()));
-            jobs.push_back(Job{seq_off, s.prompt_len + t, lp_off, static_cast<int>(i), s.eos_bias});
-        }
+        distilled += static_cast<size_t>(sel[i]->response_len);
     }
-    for (int v : tokens)
-        if (v < 0 || v >= V) throw std::invalid_argument("row_index: token out of vocabulary");
-
     auto m = copy_model(true);
-    cudaStream_t st = ctx->stream;
-    const int J = static_cast<int>(jobs.size());
-    std::vector<double> kl(J);
-    std::vector<long long> rows(J);
-    if (J > 0) {
-        DBuf<int32_t> d_tok(tokens.size());
-        DBuf<double> d_lp(lp.size()), d_m(J), d_s(J), d_kl(J), d_w(take);
-        DBuf<Job> d_jobs(J);
-        DBuf<long long> d_row(J);
-        RS_CUDA(cudaMemcpyAsync(d_tok.p, tokens.data(), tokens.size() * 4, cudaMemcpyHostToDevice, st));
-        RS_CUDA(cudaMemcpyAsync(d_lp.p, lp.data(), lp.size() * 8, cudaMemcpyHostToDevice, st));
-        RS_CUDA(cudaMemcpyAsync(d_jobs.p, jobs.data(), J * sizeof(Job), cudaMemcpyHostToDevice, st));
-        RS_CUDA(cudaMemcpyAsync(d_w.p, w.data(), take * 8, cudaMemcpyHostToDevice, st));
-        const int th = V <= 256 ? 32 : V <= 4096 ? 256 : 1024;
-        kd_job_kernel<<<J, th, 0, st>>>(drafter->table.p, drafter->order, V, drafter->temperature, d_tok.p, d_jobs.p,
-                                        d_lp.p, d_m.p, d_s.p, d_kl.p, d_row.p);
-        RS_LAUNCHED();
-        RS_CUDA(cudaMemcpyAsync(kl.data(), d_kl.p, J * 8, cudaMemcpyDeviceToHost, st));
-        RS_CUDA(cudaMemcpyAsync(rows.data(), d_row.p, J * 8, cudaMemcpyDeviceToHost, st));
-        RS_CUDA(cudaStreamSynchronize(st));
-        // group jobs by row, keeping job order (= sample order, then position)
-        std::map<long long, std::vector<int>> by_row;
-        for (int j = 0; j < J; ++j) by_row[rows[j]].push_back(j);
-        std::vector<int> row_jobs, row_ptr{0};
-        std::vector<long long> urows;
-        for (auto &[r, js] : by_row) {
-            urows.push_back(r);
-            row_jobs.insert(row_jobs.end(), js.begin(), js.end());
-            row_ptr.push_back(static_cast<int>(row_jobs.size()));
-        }
-        DBuf<int32_t> d_rj(row_jobs.size()), d_rp(row_ptr.size());
-        DBuf<long long> d_ur(urows.size());
-        RS_CUDA(cudaMemcpyAsync(d_rj.p, row_jobs.data(), row_jobs.size() * 4, cudaMemcpyHostToDevice, st));
-        RS_CUDA(cudaMemcpyAsync(d_rp.p, row_ptr.data(), row_ptr.size() * 4, cudaMemcpyHostToDevice, st));
-        RS_CUDA(cudaMemcpyAsync(d_ur.p, urows.data(), urows.size() * 8, cudaMemcpyHostToDevice, st));
-        RS_CUDA(cudaMemcpyAsync(m->table.p, drafter->table.p, m->host.size() * 8, cudaMemcpyDeviceToDevice, st));
-        kd_row_kernel<<<(int)urows.size(), th, 0, st>>>(drafter->table.p, m->table.p, V, drafter->temperature,
-                                                        d_jobs.p, d_rj.p, d_rp.p, d_ur.p, d_lp.p, d_m.p, d_s.p, d_w.p,
-                                                        -policy.lr);
-        RS_LAUNCHED();
-        RS_CUDA(cudaMemcpyAsync(m->host.data(), m->table.p, m->host.size() * 8, cudaMemcpyDeviceToHost, st));
-        RS_CUDA(cudaStreamSynchronize(st));
-    } else {
-        RS_CUDA(cudaMemcpy(m->table.p, drafter->table.p, m->host.size() * 8, cudaMemcpyDeviceToDevice));
-    }
-    // loss on the pre-update drafter: sum_i w_i * sum_t KL_t (learner.cpp:142-145)
-    double loss = 0.0;
-    for (size_t i = 0; i < take; ++i) {
-        double total = 0.0;
-        for (int j : per_sample_jobs[i]) total += kl[j];
-        loss += w[i] * total;
-    }
+    const double loss = kd_core(ctx, drafter, sel, w, m->table.p, false, -policy.lr);
+    RS_CUDA(cudaMemcpy(m->host.data(), m->table.p, m->host.size() * 8, cudaMemcpyDeviceToHost));
     res.updated = 1;
     res.samples_used = static_cast<int>(take);
     res.loss = loss;

@@ -17,6 +17,10 @@ void kd_update_tabular(rs_ctx *ctx, const TabularModel *drafter, const rs_kd_sam
                        const rs_kd_policy &policy, uint64_t *sel_state, double cost, rs_model **out_model,
                        rs_kd_result *out);
 
+std::vector<int> kd_select(int n, int interval, uint64_t *sel_state);
+double kd_core(rs_ctx *ctx, const TabularModel *drafter, const std::vector<const rs_kd_sample *> &sel,
+               const std::vector<double> &w, double *out_dev, bool grad_only, double scale);
+
 // K5 for large vocabularies: per position, loss_i = w_i * sum_x p(x)(log p(x) - log q(x)) and
 // dZ_i(x) = w_i * (q(x) - p(x)) / tau, with p given as target logits rows (softmax at tau_p)
 // and q as drafter logits rows (softmax at tau_q), fp32 rows, fp64 accumulation.

@@ -114,6 +114,32 @@ def test_engine_errors_match_reference():
         assert all(a == min(3, a) for a in r.accept_lens)
 
 
+def test_distributed_kd_step_on_gpu():
+    """The prompt-sharded KD step with the device K5 gradient (rs_kd_grad_tabular), two shards
+    summed on the host (the all-reduce), then rs_tabular_apply_delta == reference kd_update."""
+    from paper_2510_26475_b200.distributed import apply_delta, kd_grad_tabular, kd_step_distributed, shard_requests
+    g = load_golden("kd_update.json")
+    drafter = model_of(g["drafter"])
+    buf = [rb.RolloutSample(s["prompt"], s["response"],
+                            [rb.StepRecord(st["token"], st["logp"], st["drafted"], st["logq"], st["target_logprobs"])
+                             for st in s["steps"]], s["eos_bias"], s["reward"]) for s in g["buffer"]]
+    c = g["cases"][0]
+    p = c["policy"]
+    pol = rb.KDPolicy(p["interval"], rb.WeightMode.Reward, p["clip_lo"], p["clip_hi"], p["lr"])
+    results = []
+    for rank in range(2):
+        mine = shard_requests(list(range(len(buf))), rank, 2, group_size=8)
+        results.append(kd_step_distributed([s.reward for s in buf], [len(s.response) for s in buf],
+                                           [buf[i] for i in mine], mine, pol, rb.SelectionRng(c["selection_seed"]),
+                                           0.02, lambda ss, ww: kd_grad_tabular(drafter, ss, ww)))
+    grad = [a + b for a, b in zip(results[0].grad, results[1].grad)]
+    loss = results[0].loss + results[1].loss
+    new = apply_delta(drafter, grad, -p["lr"])
+    assert new.version == drafter.version + 1
+    assert loss == pytest.approx(c["out"]["loss"], rel=1e-10)
+    assert max(abs(a - b) for a, b in zip(new.logits(), c["out"]["logits"])) < 1e-12
+
+
 def test_kd_update_matches_reference():
     g = load_golden("kd_update.json")
     drafter = model_of(g["drafter"])
