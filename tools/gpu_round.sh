@@ -1,0 +1,19 @@
+#!/bin/bash
+# One gpurun call: GPU tests, smoke, bench, launch list and one ncu --set full capture.
+# usage: gpurun -- bash tools/gpu_round.sh [tag]
+TAG=${1:-r01}
+O=gpurun_out/$TAG
+mkdir -p $O
+nvidia-smi > $O/nvidia-smi.txt 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"
+timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest_gpu.log
+timeout 600 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"; cat $O/bench.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "draft/" --nvtx-include "verify/" --nvtx-include "accept/" \
+  --csv --log-file $O/launches.csv python tools/profile_step.py 3 > $O/launches.log 2>&1; echo "ncu launches rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "verify/" -k regex:gemm -s 0 -c 4 \
+  -o $O/gemm_full python tools/profile_step.py 2 > $O/gemm_full.log 2>&1; echo "ncu full rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "verify/" -k regex:gemm -s 144 -c 1 \
+  -o $O/lmhead_full python tools/profile_step.py 2 > $O/lmhead_full.log 2>&1; echo "ncu lmhead rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "accept/" -k regex:"accept|compact" -s 0 -c 4 \
+  -o $O/accept_full python tools/profile_step.py 2 > $O/accept_full.log 2>&1; echo "ncu accept rc=$?"
+ls -la $O
