@@ -231,6 +231,13 @@ int rs_kd_update_tabular(rs_ctx *ctx, const rs_model *drafter, const rs_kd_sampl
    Runs on the context stream. */
 int rs_gemm_bf16(rs_ctx *ctx, const void *A_dev, const void *B_dev, void *C_dev, const void *bias_dev, int32_t M,
                  int32_t N, int32_t K, int32_t epilogue, float scale, int32_t block_n, int32_t splits);
+/* LM-head GEMM: C_f32[M, N] = scale * A[M, K] . B[N, K]^T with, when stats_dev is non-null,
+   the fused fp64 softmax tile partials of C / tau (per 256-column tile, EOS column N-1
+   excluded): stats[(m * ceil(N/256) + t) * 2] = max, [.. + 1] = sum exp(. - max). */
+int rs_lm_head_bf16(rs_ctx *ctx, const void *A_dev, const void *B_dev, float *C_dev, double *stats_dev, int32_t M,
+                    int32_t N, int32_t K, float scale, double tau);
+/* The same tile partials from fp32 rows already in HBM (stand-alone full-chip kernel). */
+int rs_row_stats(rs_ctx *ctx, const float *rows_dev, int32_t nrows, int32_t V, double tau, double *stats_dev);
 /* Device pointer + byte size of a named weight tensor of a transformer target / drafter
    ("emb", "final_norm", "rope", per layer "qkv_w", "qkv_b", "o_w", "gu_w", "down_w", "ln1",
    "ln2"; drafter "fc_w", "norm_emb", "norm_hid", "lm_w"), for export / test references. */
@@ -242,6 +249,11 @@ int rs_model_params(const rs_model *m, int64_t *out);
 /* Per-kernel-class device timing (CUDA events around each launch, this thread only):
    JSON {"<scope>.<kernel>": {"launches", "ms", "flops", "bytes"}} with algorithmic work. */
 void rs_prof_enable(int32_t on);
+/* Process-wide kernel tuning knobs (0 = automatic). Keys: "accept_cluster" -- CTAs per
+   sequence in the fused acceptance kernel (1, 2, 4, 8); "fused_stats" -- drafter LM-head softmax
+   partials in the GEMM epilogue (1) or a separate row-stats kernel (0); results are bitwise
+   independent of both. */
+int rs_set_tuning(const char *key, int64_t value);
 void rs_prof_reset(void);
 int rs_prof_json(char *buf, int64_t cap, int64_t *len);
 

@@ -120,7 +120,7 @@ EXPORTED_SYMBOLS = [
     "rs_engine_steps", "rs_engine_step_logprobs", "rs_engine_accept_lens", "rs_engine_destroy",
     "rs_engine_set_capture", "rs_engine_capture_count", "rs_engine_capture_read",
     "rs_kd_weight", "rs_kd_update_tabular", "rs_mt19937_64_seed", "rs_gemm_bf16",
-    "rs_model_tensor", "rs_memcpy_d2d", "rs_model_params", "rs_prof_enable", "rs_prof_reset", "rs_prof_json",
+    "rs_model_tensor", "rs_memcpy_d2d", "rs_model_params", "rs_prof_enable", "rs_prof_reset", "rs_prof_json", "rs_set_tuning", "rs_lm_head_bf16", "rs_row_stats",
     "rs_kd_select", "rs_kd_grad_tabular", "rs_tabular_apply_delta",
 ]
 
@@ -192,6 +192,9 @@ def lib():
             "rs_model_params": ([vp, P(i64)], ctypes.c_int),
             "rs_prof_enable": ([i32], None),
             "rs_prof_reset": ([], None),
+            "rs_set_tuning": ([ctypes.c_char_p, i64], ctypes.c_int),
+            "rs_lm_head_bf16": ([vp, vp, vp, vp, vp, i32, i32, i32, ctypes.c_float, dbl], ctypes.c_int),
+            "rs_row_stats": ([vp, vp, i32, i32, dbl, vp], ctypes.c_int),
             "rs_prof_json": ([ctypes.c_char_p, i64, P(i64)], ctypes.c_int),
             "rs_kd_select": ([i32, i32, P(u64), P(i32), P(i32)], ctypes.c_int),
             "rs_kd_grad_tabular": ([vp, vp, P(_KDSample), i32, P(dbl), P(dbl), P(dbl)], ctypes.c_int),
@@ -273,6 +276,11 @@ def profile(enable: Optional[bool] = None, reset: bool = False):
     buf = ctypes.create_string_buffer(n.value + 1)
     _check(lib().rs_prof_json(buf, n.value + 1, ctypes.byref(n)))
     return json.loads(buf.value.decode())
+
+
+def set_tuning(key: str, value: int) -> None:
+    """Process-wide kernel knobs (rs_set_tuning); 0 restores the automatic choice."""
+    _check(lib().rs_set_tuning(key.encode(), int(value)))
 
 
 def launch_count() -> int:

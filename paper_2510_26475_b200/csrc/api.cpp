@@ -345,6 +345,7 @@ int rs_engine_create(rs_ctx *ctx, const rs_model *target, const rs_model *drafte
             e->d_Qst.alloc(nst);
             e->pair = make_transformer_pair(ctx, e.get(), target, drafter, n, e->slots_max, e->prompt_len, prompts, tok_cap);
         }
+        e->d_pq.alloc((size_t)N * 2 * e->V);
         if (drafter && drafter->vocab != e->V) throw std::invalid_argument("BatchEngine: drafter vocabulary differs from target");
         RS_CUDA(cudaStreamSynchronize(ctx->stream));
         *out = e.release();
@@ -555,6 +556,20 @@ int rs_model_tensor(const rs_model *m, const char *name, int32_t layer, void **p
 }
 
 void rs_prof_enable(int32_t on) { prof_enable(on != 0); }
+int rs_set_tuning(const char *key, int64_t value) {
+    return guard([&] {
+        const std::string k = key ? key : "";
+        if (k == "accept_cluster") {
+            if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8)
+                throw std::invalid_argument("accept_cluster must be 0, 1, 2, 4 or 8");
+            rs::tuning().accept_cluster = static_cast<int>(value);
+        } else if (k == "fused_stats") {
+            rs::tuning().fused_stats = value != 0 ? 1 : -1;
+        } else {
+            throw std::invalid_argument("unknown tuning key: " + k);
+        }
+    });
+}
 void rs_prof_reset(void) { prof_reset(); }
 int rs_prof_json(char *buf, int64_t cap, int64_t *len) {
     return guard([&] {
@@ -605,6 +620,35 @@ int rs_gemm_bf16(rs_ctx *ctx, const void *A, const void *B, void *Cp, const void
         g.epi.bias = bias;
         g.epi.scale = scale;
         gemm_bf16(g, ctx->stream);
+    });
+}
+
+int rs_lm_head_bf16(rs_ctx *ctx, const void *A, const void *B, float *Cp, double *stats, int32_t M, int32_t N,
+                    int32_t K, float scale, double tau) {
+    return guard([&] {
+        need(ctx, "rs_lm_head_bf16");
+        GemmArgs g;
+        g.A = A;
+        g.B = B;
+        g.M = M;
+        g.N = N;
+        g.K = K;
+        g.lda = K;
+        g.ldb = K;
+        g.epi.kind = kEpiF32;
+        g.epi.out = Cp;
+        g.epi.ldo = N;
+        g.epi.scale = scale;
+        g.epi.stats = stats;
+        g.epi.tau = tau;
+        gemm_bf16(g, ctx->stream);
+    });
+}
+
+int rs_row_stats(rs_ctx *ctx, const float *rows, int32_t nrows, int32_t V, double tau, double *stats) {
+    return guard([&] {
+        need(ctx, "rs_row_stats");
+        row_stats(rows, nullptr, nrows, V, tau, stats, ctx->stream);
     });
 }
 

@@ -45,6 +45,13 @@ enum DevErr : int {
 };
 const char *dev_err_message(int code);
 
+// Process-wide tuning knobs set through rs_set_tuning (0 = automatic).
+struct Tuning {
+    int accept_cluster = 0;
+    int fused_stats = 0;  // drafter LM-head stats: 1 fused GEMM epilogue; 0 / -1 separate row-stats kernel
+};
+Tuning &tuning();
+
 #ifdef __CUDACC__
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

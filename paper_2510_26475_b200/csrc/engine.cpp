@@ -2,6 +2,7 @@
 // ProfileTable follows server.cpp:21-145; rs_engine::step follows BatchEngine::step
 // (server.cpp:266-349) with the per-request spec_step_tree calls replaced by batched device
 // launches (drafting by depth, one verify forward, one fused acceptance per round).
+#include <cstdlib>
 #include "engine.h"
 
 #include <algorithm>
@@ -17,6 +18,32 @@ namespace rs {
 std::string cfg_key(const rs_sdconfig &c) {
     if (!c.enabled) return "off";
     return "s" + std::to_string(c.rounds) + "_t" + std::to_string(c.branching) + "_n" + std::to_string(c.draft_len);
+}
+
+// Defaults can be overridden for A/B measurements with RS_TUNE="key=value,key=value".
+Tuning &tuning() {
+    static Tuning t = [] {
+        Tuning x;
+        if (const char *env = std::getenv("RS_TUNE")) {
+            std::string s(env);
+            size_t p = 0;
+            while (p < s.size()) {
+                size_t e = s.find(',', p);
+                if (e == std::string::npos) e = s.size();
+                const std::string kv = s.substr(p, e - p);
+                const size_t eq = kv.find('=');
+                if (eq != std::string::npos) {
+                    const std::string k = kv.substr(0, eq);
+                    const int v = std::atoi(kv.c_str() + eq + 1);
+                    if (k == "accept_cluster") x.accept_cluster = v;
+                    else if (k == "fused_stats") x.fused_stats = v;
+                }
+                p = e + 1;
+            }
+        }
+        return x;
+    }();
+    return t;
 }
 
 const char *dev_err_message(int code) {
@@ -190,6 +217,8 @@ SdDev rs_engine::dev(const rs_sdconfig &cfg, int nact) {
     d.Pst = d_Pst.n ? d_Pst.p : nullptr;
     d.Qst = d_Qst.n ? d_Qst.p : nullptr;
     d.ntiles = (V + 255) / 256;
+    d.lazy_pst = d.Pst ? 1 : 0;
+    d.pq_cache = d_pq.n ? d_pq.p : nullptr;  // target rows: stats on demand inside the acceptance kernel
     d.verify_mode = verify_mode;
     d.record_full = record_full ? 1 : 0;
     d.err = d_err.p;

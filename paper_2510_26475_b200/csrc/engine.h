@@ -168,6 +168,7 @@ struct rs_engine {
     rs::DBuf<int32_t> d_round_cost, d_chain;  // chain_tok, chain_len, chain_stop, chain_off
     rs::DBuf<int32_t> d_err, d_flag, d_summary;
     rs::DBuf<char> d_P, d_Q;
+    rs::DBuf<double> d_pq;          // acceptance scratch: fp64 p1 / q1 rows per active sequence
     rs::DBuf<double> d_Pst, d_Qst;  // LM-head tile softmax partials (transformer engines)
     int32_t *h_summary = nullptr;  // pinned
     int32_t *h_active = nullptr;   // pinned

@@ -185,29 +185,12 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi &ep, uint32_t tbase
                 for (int j = 0; j < 32; ++j)
                     if (n0 + j < N) out[j] = __uint_as_float(v[j]);
             }
-            if (ep.stats) {
-                // online (max, sum exp) of y = out / tau over this chunk's columns except the
-                // global last one (EOS, whose bias is request-specific and folded in later)
-                const bool unit = ep.tau == 1.0;
+            if (ep.stats) {  // running fp32 max of the tile's columns except the global last (EOS)
                 float cm = -INFINITY;
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
                     if (n0 + j < N - 1) cm = fmaxf(cm, __uint_as_float(v[j]));
-                if (cm != -INFINITY) {
-                    const double cmd = unit ? (double)cm : (double)cm / ep.tau;
-                    if (cmd > rm) {
-                        rs = rm == -INFINITY ? 0.0 : rs * exp(rm - cmd);
-                        rm = cmd;
-                    }
-                    double acc = 0.0;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        if (n0 + j >= N - 1) continue;
-                        const double y = unit ? (double)__uint_as_float(v[j]) : (double)__uint_as_float(v[j]) / ep.tau;
-                        acc += exp(y - rm);
-                    }
-                    rs += acc;
-                }
+                rm = fmax(rm, (double)cm);
             }
         } else {  // kEpiResidual: out (fp32) += acc (L2-coherent loads: split-K partials of other SMs)
             float *out = static_cast<float *>(ep.out) + static_cast<size_t>(row) * ep.ldo + n0;
@@ -226,6 +209,46 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi &ep, uint32_t tbase
                 for (int j = 0; j < 32; ++j)
                     if (n0 + j < N) out[j] = __ldcg(out + j) + __uint_as_float(v[j]);
             }
+        }
+    }
+}
+
+// Second epilogue pass of the LM head (kEpiF32 with stats, BN = 256 = one stats tile): the
+// tile's fp64 softmax partials in EXACTLY tilestat.cuh's order -- "lane" l of the canonical
+// warp owns columns l + 32 j, partials summed in j order, then the xor-butterfly -- so a row's
+// statistics are bitwise those of the stand-alone row-stats kernel. The accumulator is
+// re-read from TMEM (and re-scaled) instead of being held in registers.
+__device__ __forceinline__ void stats_pass(const GemmEpi &ep, uint32_t tb, int row, int n0, int M, int N, float mx) {
+    const bool live = mx != -INFINITY;
+    const bool unit = ep.tau == 1.0;
+    const double m = !live ? -INFINITY : unit ? (double)mx : (double)mx / ep.tau;
+    double acc[32];
+#pragma unroll
+    for (int l = 0; l < 32; ++l) acc[l] = 0.0;
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tb + c * 32, v);  // warp-collective: every lane, live or not
+#pragma unroll
+        for (int l = 0; l < 32; ++l) {
+            const float f = __uint_as_float(v[l]) * ep.scale;
+            if (live && n0 + c * 32 + l < N - 1 && f != -INFINITY) {
+                const double y = unit ? (double)f : (double)f / ep.tau;
+                acc[l] += exp(y - m);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int l = 0; l < o; ++l) acc[l] = acc[l] + acc[l + o];
+    if (row < M) {
+        const int orow = ep.row_map ? ep.row_map[row] : row;
+        if (orow >= 0) {
+            const int ntiles = (N + 255) / 256;
+            double *st = ep.stats + ((size_t)orow * ntiles + n0 / 256) * 2;
+            st[0] = m;
+            st[1] = live ? acc[0] : 0.0;
         }
     }
 }
@@ -358,6 +381,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             double rm = -INFINITY, rs = 0.0;
 #pragma unroll 1
             for (int c = 0; c < kChunks; ++c) epilogue_chunk<EPI, BN>(ep, tb, row, n0, c, M, N, rm, rs);
+            if constexpr (EPI == kEpiF32 && BN == 256) {
+                // the tile max is warp-uniform only per row; every lane joins the TMEM loads
+                if (ep.stats) stats_pass(ep, tb, row, n0, M, N, (float)rm);
+            }
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
             if (EPI == kEpiResidual && splits > 1) {
@@ -365,17 +392,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 asm volatile("bar.sync 1, 128;" ::: "memory");  // all 4 epilogue warps wrote their rows
                 if (q == 0 && lane == 0)
                     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sem + tile), "r"(split + 1) : "memory");
-            }
-            if constexpr (EPI == kEpiF32) {
-                if (ep.stats && row < M) {
-                    const int orow = ep.row_map ? ep.row_map[row] : row;
-                    if (orow >= 0) {
-                        const int ntiles = (N + BN - 1) / BN;
-                        double *st = ep.stats + ((size_t)orow * ntiles + n0 / BN) * 2;
-                        st[0] = rm;
-                        st[1] = rs;
-                    }
-                }
             }
         }
     }

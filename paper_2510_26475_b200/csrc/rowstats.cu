@@ -9,6 +9,7 @@
 #include "common.cuh"
 #include "prof.h"
 #include "sd.h"
+#include "tilestat.cuh"
 
 namespace rs {
 
@@ -23,28 +24,8 @@ __global__ void __launch_bounds__(256) row_stats_kernel(const float *rows, const
     const int k = static_cast<int>(gw / ntiles), t = static_cast<int>(gw % ntiles);
     const int row = row_ids ? row_ids[k] : k;
     if (row < 0) return;
-    const float *z = rows + (size_t)row * V;
-    const int lo = t * 256, hi = min(lo + 256, V - 1);  // EOS excluded
-    float v[8];
-    float mx = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const int x = lo + lane + 32 * j;
-        v[j] = x < hi ? z[x] : -INFINITY;
-        mx = fmaxf(mx, v[j]);
-    }
-    mx = warp_maxf(mx);
-    double m = -INFINITY, s = 0.0;
-    if (mx != -INFINITY) {
-        m = tau == 1.0 ? (double)mx : (double)mx / tau;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            if (v[j] == -INFINITY) continue;
-            const double y = tau == 1.0 ? (double)v[j] : (double)v[j] / tau;
-            s += exp(y - m);
-        }
-        s = warp_sum(s);
-    }
+    double m, s;
+    tile_stat(rows + (size_t)row * V, V, t, tau, lane, m, s);
     if (lane == 0) {
         double *o = stats + ((size_t)row * ntiles + t) * 2;
         o[0] = m;

@@ -53,6 +53,8 @@ struct SdDev {
     const double *Pst;       // LM-head epilogue tile partials for P rows [nact][slots][ntiles][2], or null
     const double *Qst;       // same for Q rows
     int32_t ntiles;          // ceil(V / 256)
+    int32_t lazy_pst;
+    double *pq_cache;        // [nact][2][V] fp64 p1 / q1 of the branch point (sibling residual passes)        // Pst is scratch: the acceptance kernel fills the rows it touches
     int32_t verify_mode;     // RS_VERIFY_SAMPLE / RS_VERIFY_GREEDY
     int32_t record_full;
     int32_t *err;            // device error word (first error wins)

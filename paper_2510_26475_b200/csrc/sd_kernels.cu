@@ -21,9 +21,12 @@
 #include <cfloat>
 #include <climits>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "prof.h"
 #include "sd.h"
+#include "tilestat.cuh"
 
 namespace rs {
 
@@ -32,6 +35,46 @@ namespace {
 constexpr int kTileW = 256;     // = the LM-head GEMM's BLOCK_N
 constexpr int kMaxTiles = 2048; // V <= 524288
 constexpr int kMaxCand = 16;
+constexpr int kMaxCluster = 8;
+
+namespace cg = cooperative_groups;
+
+// A sequence's acceptance runs on a thread-block CLUSTER of `size` CTAs (1 when the batch
+// alone fills the chip). Every CTA walks the same control flow on the same data; the only
+// split work is the full-vocabulary passes (residual tile sums, argmax, full-row records),
+// whose tile partials are exchanged through distributed shared memory. Tile t is always
+// summed by one warp in the same lane order, so results are bitwise independent of `size`.
+struct Cl {
+    unsigned rank, size;
+    __device__ __forceinline__ bool lead() const { return rank == 0 && threadIdx.x == 0; }
+};
+__device__ __forceinline__ void cl_sync(const Cl &cl) {
+    if (cl.size > 1) cg::this_cluster().sync();
+    else __syncthreads();
+}
+// Combine one (value, key) pair per CTA across the cluster: max value, then min key.
+__device__ void cl_maxkey(const Cl &cl, double &best, long long &key, double *slot_v, long long *slot_k) {
+    if (cl.size == 1) return;
+    if (threadIdx.x == 0) {
+        *slot_v = best;
+        *slot_k = key;
+    }
+    cl_sync(cl);
+    auto cluster = cg::this_cluster();
+    double b = -INFINITY;
+    long long k = LLONG_MAX;
+    for (unsigned r = 0; r < cl.size; ++r) {
+        const double v = *cluster.map_shared_rank(slot_v, r);
+        const long long kk = *cluster.map_shared_rank(slot_k, r);
+        if (v > b || (v == b && kk < k)) {
+            b = v;
+            k = kk;
+        }
+    }
+    best = b;
+    key = k;
+    cl_sync(cl);
+}
 
 template <class T>
 struct RowRef {
@@ -43,7 +86,7 @@ struct RowRef {
     // z'/tau with the EOS bias added to the last logit before the temperature division
     // (model.cpp:137-138, :58-61); tau == 1 skips the (exact anyway) division.
     __device__ __forceinline__ double v(int x) const {
-        double y = static_cast<double>(z[x]);
+        double y = static_cast<double>(__ldg(z + x));  // rows are read-only here: loads may run ahead of stores
         if (x == V - 1) y += bias;
         return tau == 1.0 ? y : y / tau;
     }
@@ -62,13 +105,13 @@ __device__ Stats row_stats(const RowRef<T> &r, double *red) {
     if (r.gst) {
         const int nt = ntiles_of(r.V);
         double m = -INFINITY;
-        for (int t = threadIdx.x; t < nt; t += blockDim.x) m = fmax(m, r.gst[2 * t]);
+        for (int t = threadIdx.x; t < nt; t += blockDim.x) m = fmax(m, __ldcg(r.gst + 2 * t));
         const double ve = r.v(r.V - 1);
         m = fmax(block_max(m, red), ve);
         double s = 0.0;
         for (int t = threadIdx.x; t < nt; t += blockDim.x) {
-            const double st = r.gst[2 * t + 1];
-            if (st > 0.0) s += st * exp(r.gst[2 * t] - m);
+            const double st = __ldcg(r.gst + 2 * t + 1);
+            if (st > 0.0) s += st * exp(__ldcg(r.gst + 2 * t) - m);
         }
         s = block_sum(s, red) + exp(ve - m);
         return {m, s, 1.0 / s};
@@ -113,23 +156,85 @@ struct PCurFn {
     }
 };
 
-// Per-tile sums of f over the tile partition (tiles over [0, V-1) plus the EOS pseudo-tile at
-// index nt) into `mass`; returns the total. One warp per tile, coalesced lanes.
-template <class F>
-__device__ double tile_sums(const F &f, int V, double *mass, double *red) {
-    const int nt = ntiles_of(V);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int t = w; t < nt; t += nw) {
-        double s = 0.0;
-        for (int x = tile_lo(t) + lane; x < tile_hi(t, V); x += 32) s += f(x);
-        s = warp_sum(s);
-        if (lane == 0) mass[t] = s;
+// Contiguous tile range of cluster rank c: [c * nt / C, (c + 1) * nt / C).
+__device__ __forceinline__ int cl_tile0(const Cl &cl, unsigned c, int nt) { return (int)((long)c * nt / cl.size); }
+__device__ __forceinline__ unsigned cl_owner(const Cl &cl, int t, int nt) {
+    unsigned c = 0;
+    while (c + 1 < cl.size && cl_tile0(cl, c + 1, nt) <= t) ++c;
+    return c;
+}
+
+// Warm L2 with this CTA's share of a logit row (TMA bulk prefetch, 16 B granules).
+__device__ __forceinline__ void l2_prefetch_share(const void *row, size_t bytes, const Cl &cl) {
+    if (threadIdx.x >= 32 || bytes < 65536 || (reinterpret_cast<uintptr_t>(row) & 15)) return;
+    const size_t per = ((bytes + cl.size - 1) / cl.size + 15) & ~size_t(15);
+    const size_t b0 = per * cl.rank;
+    if (b0 >= bytes) return;
+    const size_t n = (bytes - b0 < per ? bytes - b0 : per) & ~size_t(15);
+    const char *p = static_cast<const char *>(row) + b0;
+    constexpr size_t kChunk = 32768;
+    for (size_t off = (size_t)threadIdx.x * kChunk; off < n; off += 32 * kChunk) {
+        const uint32_t len = (uint32_t)(n - off < kChunk ? n - off : kChunk);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + off), "r"(len) : "memory");
     }
-    if (threadIdx.x == 0) mass[nt] = f(V - 1);
-    __syncthreads();
+}
+
+// Gather the other ranks' tile values into every CTA's `mass`, then the total.
+__device__ double gather_masses(int nt, double *mass, double *red, const Cl &cl) {
+    if (cl.size > 1) __threadfence();  // tile functors may have written global scratch read by peers
+    cl_sync(cl);
+    if (cl.size > 1) {
+        auto cluster = cg::this_cluster();
+        for (int t = threadIdx.x; t <= nt; t += blockDim.x) {
+            const unsigned own = t == nt ? 0u : cl_owner(cl, t, nt);
+            if (own != cl.rank) mass[t] = *cluster.map_shared_rank(mass + t, own);
+        }
+        cl_sync(cl);  // peers have read our tiles before anyone overwrites `mass` again
+    }
     double s = 0.0;
     for (int t = threadIdx.x; t <= nt; t += blockDim.x) s += mass[t];
     return block_sum(s, red);
+}
+
+// Per-tile sums of f over the tile partition (tiles over [0, V-1) plus the EOS pseudo-tile at
+// index nt) into `mass`; returns the total. One warp per tile, lane l summing columns
+// l + 32 j in j order, then the warp butterfly -- whichever warp / CTA owns the tile. Each CTA
+// of the cluster takes a contiguous tile range; a warp handles two tiles per iteration with
+// all 16 column values fetched before any is summed (memory-level parallelism).
+template <class F>
+__device__ double tile_sums(const F &f, int V, double *mass, double *red, const Cl &cl) {
+    const int nt = ntiles_of(V);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int t0 = cl_tile0(cl, cl.rank, nt), t1 = cl_tile0(cl, cl.rank + 1, nt);
+    for (int t = t0 + w; t < t1; t += 2 * nw) {
+        const int u = t + nw;
+        const int hi = tile_hi(t, V), hu = u < t1 ? tile_hi(u, V) : 0;
+        double va[8], vb[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int x = tile_lo(t) + lane + 32 * j;
+            va[j] = x < hi ? f(x) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int x = tile_lo(u) + lane + 32 * j;
+            vb[j] = x < hu ? f(x) : 0.0;
+        }
+        double sa = 0.0, sb = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            sa += va[j];
+            sb += vb[j];
+        }
+        sa = warp_sum(sa);
+        sb = warp_sum(sb);
+        if (lane == 0) {
+            mass[t] = sa;
+            if (u < t1) mass[u] = sb;
+        }
+    }
+    if (cl.rank == 0 && threadIdx.x == 0) mass[nt] = f(V - 1);
+    return gather_masses(nt, mass, red, cl);
 }
 
 // Tile masses of a probability row straight from the GEMM partials.
@@ -137,8 +242,8 @@ template <class T>
 __device__ void gemm_masses(const RowRef<T> &r, const Stats &st, double *mass) {
     const int nt = ntiles_of(r.V);
     for (int t = threadIdx.x; t < nt; t += blockDim.x) {
-        const double s = r.gst[2 * t + 1];
-        mass[t] = s > 0.0 ? s * exp(r.gst[2 * t] - st.m) * st.inv : 0.0;
+        const double s = __ldcg(r.gst + 2 * t + 1);
+        mass[t] = s > 0.0 ? s * exp(__ldcg(r.gst + 2 * t) - st.m) * st.inv : 0.0;
     }
     if (threadIdx.x == 0) mass[nt] = exp(r.v(r.V - 1) - st.m) * st.inv;
     __syncthreads();
@@ -256,10 +361,10 @@ __device__ int inv_cdf(const F &f, int V, const double *mass, double scale, doub
 // the winner; fp64 rows (tabular parity path) compare the probabilities themselves.
 template <class T>
 __device__ int row_argmax(const RowRef<T> &r, const Stats &st, double *red, long long *redl, const int *excl,
-                          int n_excl) {
+                          int n_excl, const Cl &cl, double *slot_v, long long *slot_k) {
     double best = -1.0;
     int bi = INT_MAX;
-    for (int x = threadIdx.x; x < r.V; x += blockDim.x) {
+    for (int x = cl.rank * blockDim.x + threadIdx.x; x < r.V; x += cl.size * blockDim.x) {
         bool skip = false;
         for (int e = 0; e < n_excl; ++e) skip |= excl[e] == x;
         if (skip) continue;
@@ -269,9 +374,10 @@ __device__ int row_argmax(const RowRef<T> &r, const Stats &st, double *red, long
             bi = x;
         }
     }
-    const double m = block_max(bi == INT_MAX ? -INFINITY : best, red);
+    double m = block_max(bi == INT_MAX ? -INFINITY : best, red);
     long long key = (bi != INT_MAX && best == m) ? bi : LLONG_MAX;
     key = block_min_ll(key, redl);
+    cl_maxkey(cl, m, key, slot_v, slot_k);
     return static_cast<int>(key);
 }
 
@@ -289,9 +395,9 @@ __device__ __forceinline__ double u_of(const MtStream &ms, int k) { return to_un
 // Append one emitted token with its StepRecord (specdec.cpp:62-74, :276-283).
 template <class T>
 __device__ void emit(const SdDev &d, Seq &q, int tok, const RowRef<T> &row, const Stats &st, bool drafted,
-                     double logq, bool &ended) {
+                     double logq, bool &ended, const Cl &cl) {
     const int gen = q.len - q.plen;
-    if (threadIdx.x == 0) {
+    if (cl.lead()) {
         if (q.len < d.tok_cap && gen < d.steps_cap) {
             d.tok[(size_t)q.r * d.tok_cap + q.len] = tok;
             const size_t si = (size_t)q.r * d.steps_cap + gen;
@@ -305,7 +411,8 @@ __device__ void emit(const SdDev &d, Seq &q, int tok, const RowRef<T> &row, cons
     }
     if (d.st_full && gen < d.steps_cap) {
         double *dst = d.st_full + ((size_t)q.r * d.steps_cap + gen) * d.V;
-        for (int x = threadIdx.x; x < d.V; x += blockDim.x) dst[x] = log(prob(row, st, x));
+        for (int x = cl.rank * blockDim.x + threadIdx.x; x < d.V; x += cl.size * blockDim.x)
+            dst[x] = log(prob(row, st, x));
     }
     q.len += 1;
     if (tok == d.eos) ended = true;
@@ -324,16 +431,43 @@ __device__ __forceinline__ RowRef<T> qrow(const SdDev &d, const Seq &q, int slot
                      d.Qst ? d.Qst + row * d.ntiles * 2 : nullptr};
 }
 
+// Target rows without precomputed statistics (SdDev::lazy_pst): the acceptance kernel fills a
+// row's tile partials the first time it touches the row -- typically 2-3 of the 1 + t*n
+// verified rows per sequence -- split over the cluster's warps, with the same tile_stat the
+// full-chip row-stats kernel uses.
+template <class T>
+__device__ RowRef<T> prow_ready(const SdDev &d, const Seq &q, int slot, const Cl &cl) {
+    RowRef<T> r = prow<T>(d, q, slot);
+    if constexpr (sizeof(T) == 4) {
+        if (d.lazy_pst && r.gst) {
+            double *g = const_cast<double *>(r.gst);
+            const int nt = ntiles_of(r.V), lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+            const int t1 = cl_tile0(cl, cl.rank + 1, nt);
+            for (int t = cl_tile0(cl, cl.rank, nt) + (threadIdx.x >> 5); t < t1; t += nw) {
+                double m, s;
+                tile_stat(reinterpret_cast<const float *>(r.z), r.V, t, r.tau, lane, m, s);
+                if (lane == 0) {
+                    g[2 * t] = m;
+                    g[2 * t + 1] = s;
+                }
+            }
+            __threadfence();
+            cl_sync(cl);
+        }
+    }
+    return r;
+}
+
 // Draw from a plain probability row (masses from the GEMM partials when present).
 template <class T>
 __device__ int sample_row(const RowRef<T> &r, const Stats &st, double u, double *mass, CdfScratch &cs, double *red,
-                          long long *redl, int *err) {
+                          long long *redl, int *err, const Cl &cl) {
     const ProbFn<T> f{r, st};
     if (r.gst) {
         gemm_masses(r, st, mass);
         return inv_cdf(f, r.V, mass, 1.0, u, cs, redl, err);
     }
-    tile_sums(f, r.V, mass, red);
+    tile_sums(f, r.V, mass, red, cl);
     return inv_cdf(f, r.V, mass, 1.0, u, cs, redl, err);
 }
 
@@ -380,6 +514,9 @@ __global__ void __launch_bounds__(512) draft_sample_kernel(SdDev d, int depth) {
     __shared__ int picked[kMaxBranch];
     __shared__ double mass[kMaxTiles + 1];
     __shared__ CdfScratch cs;
+    __shared__ double slot_v;
+    __shared__ long long slot_k;
+    const Cl cl{0u, 1u};
     const int a = blockIdx.x;
     const int r = d.active[a];
     const int ne = d.n_eff[r];
@@ -393,12 +530,12 @@ __global__ void __launch_bounds__(512) draft_sample_kernel(SdDev d, int depth) {
         const Stats st = row_stats(row, red);
         if (!greedy) {
             if (row.gst) gemm_masses(row, st, mass);
-            else tile_sums(ProbFn<T>{row, st}, row.V, mass, red);
+            else tile_sums(ProbFn<T>{row, st}, row.V, mass, red, cl);
         }
         for (int i = 0; i < d.t; ++i) {
             int c;
             if (greedy) {
-                c = row_argmax(row, st, red, redl, picked, i);
+                c = row_argmax(row, st, red, redl, picked, i, cl, &slot_v, &slot_k);
             } else {
                 const double u = u_of(D, d.chain_off[(size_t)r * d.t_max + i]);
                 c = inv_cdf(ProbFn<T>{row, st}, d.V, mass, 1.0, u, cs, redl, d.err);
@@ -420,8 +557,8 @@ __global__ void __launch_bounds__(512) draft_sample_kernel(SdDev d, int depth) {
     const RowRef<T> row = qrow<T>(d, q, 1 + i * d.n + depth);
     const Stats st = row_stats(row, red);
     int c;
-    if (greedy) c = row_argmax(row, st, red, redl, picked, 0);
-    else c = sample_row(row, st, u_of(D, d.chain_off[ci] + depth), mass, cs, red, redl, d.err);
+    if (greedy) c = row_argmax(row, st, red, redl, picked, 0, cl, &slot_v, &slot_k);
+    else c = sample_row(row, st, u_of(D, d.chain_off[ci] + depth), mass, cs, red, redl, d.err, cl);
     if (threadIdx.x == 0) {
         d.chain_tok[ci * d.n_max + depth] = c;
         d.chain_len[ci] = depth + 1;
@@ -463,7 +600,10 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
     __shared__ double Z[kMaxBranch];
     __shared__ double mass[kMaxTiles + 1];
     __shared__ CdfScratch cs;
-    const int a = blockIdx.x;
+    __shared__ double slot_v;
+    __shared__ long long slot_k;
+    const Cl cl{cg::this_cluster().block_rank(), cg::this_cluster().num_blocks()};
+    const int a = blockIdx.x / cl.size;
     const int r = d.active[a];
     Seq q{r, a, d.len[r], d.prompt_len[r], d.max_len[r], d.eos_bias[r]};
     const bool greedy = d.verify_mode == 1;
@@ -474,13 +614,13 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
 
     if (naive) {
         // Non-spec step (server.cpp:328-347): one target sample on the DRAFT stream.
-        const RowRef<T> p = prow<T>(d, q, 0);
+        const RowRef<T> p = prow_ready<T>(d, q, 0, cl);
         const Stats sp = row_stats(p, red);
         int x;
-        if (greedy) x = row_argmax(p, sp, red, redl, nullptr, 0);
-        else x = sample_row(p, sp, u_of(D, d.d_used[r]), mass, cs, red, redl, d.err);
-        emit(d, q, x, p, sp, false, 0.0, ended);
-        if (threadIdx.x == 0) {
+        if (greedy) x = row_argmax(p, sp, red, redl, nullptr, 0, cl, &slot_v, &slot_k);
+        else x = sample_row(p, sp, u_of(D, d.d_used[r]), mass, cs, red, redl, d.err, cl);
+        emit(d, q, x, p, sp, false, 0.0, ended, cl);
+        if (cl.lead()) {
             if (!greedy) d.d_used[r] += 1;
             d.len[r] = q.len;
             d.emitted[r] += 1;
@@ -504,13 +644,13 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
     if (ne == 0) {
         // max_emit == 1: no round runs, the single token is the bonus from the target on the
         // ACCEPT stream (specdec.cpp:256-266; SURVEY App. A "Engine != generate()").
-        const RowRef<T> p = prow<T>(d, q, 0);
+        const RowRef<T> p = prow_ready<T>(d, q, 0, cl);
         const Stats sp = row_stats(p, red);
-        const int x = greedy ? row_argmax(p, sp, red, redl, nullptr, 0)
-                             : sample_row(p, sp, u_of(A, acur++), mass, cs, red, redl, d.err);
-        emit(d, q, x, p, sp, false, 0.0, ended);
+        const int x = greedy ? row_argmax(p, sp, red, redl, nullptr, 0, cl, &slot_v, &slot_k)
+                             : sample_row(p, sp, u_of(A, acur++), mass, cs, red, redl, d.err, cl);
+        emit(d, q, x, p, sp, false, 0.0, ended, cl);
         ++emitted;
-        if (threadIdx.x == 0) {
+        if (cl.lead()) {
             int *rc = d.round_cost + ((size_t)r * kMaxRounds + 0) * 3;
             rc[0] = 0;
             rc[1] = 0;
@@ -527,7 +667,7 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
             longest = max(longest, clen[i]);
             tree += clen[i];
         }
-        if (threadIdx.x == 0) {
+        if (cl.lead()) {
             int *rc = d.round_cost + ((size_t)r * kMaxRounds + round) * 3;
             rc[0] = longest;
             rc[1] = t;
@@ -537,17 +677,22 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
             d.d_used[r] += tree;
         }
 
-        const RowRef<T> p1 = prow<T>(d, q, 0);
+        {
+            const size_t rb = (size_t)d.V * sizeof(T);
+            l2_prefetch_share(prow<T>(d, q, 0).z, rb, cl);
+            l2_prefetch_share(qrow<T>(d, q, 0).z, rb, cl);
+        }
+        const RowRef<T> p1 = prow_ready<T>(d, q, 0, cl);
         const RowRef<T> q1 = qrow<T>(d, q, 0);
         const Stats s1 = row_stats(p1, red);
         const Stats t1 = row_stats(q1, red);
         int sel = -1;
         if (greedy) {
-            const int a1 = row_argmax(p1, s1, red, redl, nullptr, 0);
+            const int a1 = row_argmax(p1, s1, red, redl, nullptr, 0, cl, &slot_v, &slot_k);
             for (int i = 0; i < t && sel < 0; ++i)
                 if (ctok[(size_t)i * d.n_max] == a1) sel = i;
             if (sel < 0) {
-                emit(d, q, a1, p1, s1, false, 0.0, ended);
+                emit(d, q, a1, p1, s1, false, 0.0, ended, cl);
                 ++emitted;
                 goto done;
             }
@@ -555,6 +700,7 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
             // Branch point: recursive rejection over the t siblings (specdec.cpp:197-217).
             int k = 0;
             double zlast = 1.0;
+            double *cache = d.pq_cache && t > 1 ? d.pq_cache + (size_t)a * 2 * d.V : nullptr;
             for (int i = 0; i < t; ++i) {
                 const int cand = ctok[(size_t)i * d.n_max];
                 PCurFn<T> pc{p1, s1, q1, t1, Z, k};
@@ -565,8 +711,26 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
                     break;
                 }
                 // residual normaliser and its tile masses in one pass
-                const double z = tile_sums([&](int x) { return fmax(0.0, pc(x) - prob(q1, t1, x)); }, d.V, mass, red);
-                if (z <= 1e-12 && threadIdx.x == 0) atomicCAS(d.err, 0, kErrResidual);
+                // The first residual pass caches p1(x), q1(x) in fp64 (the same bits prob()
+                // returns); later sibling passes stream them instead of redoing two fp64 exps.
+                auto res_k = [&](int x) {
+                    double rr, qq;
+                    if (k == 0 || !cache) {
+                        rr = prob(p1, s1, x);
+                        qq = prob(q1, t1, x);
+                        if (cache) {
+                            cache[x] = rr;
+                            cache[d.V + x] = qq;
+                        }
+                    } else {
+                        rr = __ldcg(cache + x);
+                        qq = __ldcg(cache + d.V + x);
+                    }
+                    for (int j = 0; j < k; ++j) rr = fmax(0.0, rr - qq) * Z[j];
+                    return fmax(0.0, rr - qq);
+                };
+                const double z = tile_sums(res_k, d.V, mass, red, cl);
+                if (z <= 1e-12 && cl.lead()) atomicCAS(d.err, 0, kErrResidual);
                 if (threadIdx.x == 0) Z[k] = 1.0 / z;
                 __syncthreads();
                 zlast = z;
@@ -576,7 +740,7 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
                 // all siblings rejected: draw from the final residual (masses of the last pass / Z_k)
                 const PCurFn<T> fk{p1, s1, q1, t1, Z, k};
                 const int x = inv_cdf(fk, d.V, mass, 1.0 / zlast, u_of(A, acur++), cs, redl, d.err);
-                emit(d, q, x, p1, s1, false, 0.0, ended);  // StepRecord keeps p1 (specdec.cpp:214)
+                emit(d, q, x, p1, s1, false, 0.0, ended, cl);  // StepRecord keeps p1 (specdec.cpp:214)
                 ++emitted;
                 goto done;
             }
@@ -584,13 +748,22 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
         sel_out = sel;
         const int *chain = ctok + (size_t)sel * d.n_max;
         const int L = clen[sel];
-        emit(d, q, chain[0], p1, s1, true, log(prob(q1, t1, chain[0])), ended);
+        emit(d, q, chain[0], p1, s1, true, log(prob(q1, t1, chain[0])), ended, cl);
         ++emitted;
         ++alen;
         if (ended) goto done;
         // Chain-style verification of the selected chain (specdec.cpp:226-245).
         for (int pos = 1; pos < L; ++pos) {
-            const RowRef<T> pd = prow<T>(d, q, 1 + sel * n + pos - 1);
+            {  // this position's pair and the next target row (next position or bonus)
+                const size_t rb = (size_t)d.V * sizeof(T);
+                if (pos == 1) {
+                    l2_prefetch_share(prow<T>(d, q, 1 + sel * n).z, rb, cl);
+                    l2_prefetch_share(qrow<T>(d, q, 1 + sel * n + 1).z, rb, cl);
+                }
+                l2_prefetch_share(prow<T>(d, q, 1 + sel * n + pos).z, rb, cl);
+                if (pos + 1 < L) l2_prefetch_share(qrow<T>(d, q, 1 + sel * n + pos + 1).z, rb, cl);
+            }
+            const RowRef<T> pd = prow_ready<T>(d, q, 1 + sel * n + pos - 1, cl);
             const RowRef<T> qd = qrow<T>(d, q, 1 + sel * n + pos);
             const Stats sp = row_stats(pd, red);
             const Stats sq = row_stats(qd, red);
@@ -599,7 +772,7 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
             int repl = -1;
             const double qv = prob(qd, sq, dt);
             if (greedy) {
-                repl = row_argmax(pd, sp, red, redl, nullptr, 0);
+                repl = row_argmax(pd, sp, red, redl, nullptr, 0, cl, &slot_v, &slot_k);
                 ok = dt == repl;
             } else {
                 const double pv = prob(pd, sp, dt);
@@ -608,7 +781,7 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
                 ok = u_of(A, acur++) < fmin(1.0, pv / qv);
             }
             if (ok) {
-                emit(d, q, dt, pd, sp, true, log(qv), ended);
+                emit(d, q, dt, pd, sp, true, log(qv), ended, cl);
                 ++emitted;
                 ++alen;
                 if (ended) goto done;
@@ -616,13 +789,13 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
                 int x = repl;
                 if (!greedy) {
                     auto res = [&](int y) { return fmax(0.0, prob(pd, sp, y) - prob(qd, sq, y)); };
-                    const double z = tile_sums(res, d.V, mass, red);
-                    if (z <= 1e-12 && threadIdx.x == 0) atomicCAS(d.err, 0, kErrResidual);
+                    const double z = tile_sums(res, d.V, mass, red, cl);
+                    if (z <= 1e-12 && cl.lead()) atomicCAS(d.err, 0, kErrResidual);
                     const double zi = 1.0 / z;
                     auto rn = [&](int y) { return fmax(0.0, prob(pd, sp, y) - prob(qd, sq, y)) * zi; };
                     x = inv_cdf(rn, d.V, mass, 1.0 / z, u_of(A, acur++), cs, redl, d.err);
                 }
-                emit(d, q, x, pd, sp, false, 0.0, ended);
+                emit(d, q, x, pd, sp, false, 0.0, ended, cl);
                 ++emitted;
                 goto done;
             }
@@ -632,16 +805,16 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
         if (round + 1 < d.s && rem_after >= 2) {
             cont = 1;
         } else {
-            const RowRef<T> pb = prow<T>(d, q, 1 + sel * n + L - 1);
+            const RowRef<T> pb = prow_ready<T>(d, q, 1 + sel * n + L - 1, cl);
             const Stats sb = row_stats(pb, red);
-            const int x = greedy ? row_argmax(pb, sb, red, redl, nullptr, 0)
-                                 : sample_row(pb, sb, u_of(A, acur++), mass, cs, red, redl, d.err);
-            emit(d, q, x, pb, sb, false, 0.0, ended);
+            const int x = greedy ? row_argmax(pb, sb, red, redl, nullptr, 0, cl, &slot_v, &slot_k)
+                                 : sample_row(pb, sb, u_of(A, acur++), mass, cs, red, redl, d.err, cl);
+            emit(d, q, x, pb, sb, false, 0.0, ended, cl);
             ++emitted;
         }
     }
 done:
-    if (threadIdx.x == 0) {
+    if (cl.lead()) {
         d.len[r] = q.len;
         d.a_used[r] = acur;
         d.accept_len[r] = alen;
@@ -769,8 +942,35 @@ void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t s
     // algorithmic bytes: every target row of the round plus every drafter row
     const double es = rt == RowType::F64 ? 8.0 : 4.0;
     ProfScope prof("accept", 0, (double)d.nact * (naive ? 1 : 2 * d.slots - 1) * d.V * es, st);
-    if (rt == RowType::F64) accept_kernel<double><<<d.nact, th, 0, st>>>(d, round, naive ? 1 : 0);
-    else accept_kernel<float><<<d.nact, th, 0, st>>>(d, round, naive ? 1 : 0);
+    // Large vocabularies: a cluster of up to 8 CTAs per sequence, sized so the whole batch is
+    // co-resident (2 x 256-thread CTAs per SM) -- the residual passes are fp64-exp bound.
+    unsigned C = 1;
+    int threads = th;
+    if (d.V > 4096) {
+        threads = 256;
+        int sms = 148;
+        RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+        while (C < kMaxCluster && (long)d.nact * C * 2 <= 2L * sms) C *= 2;
+    }
+    if (tuning().accept_cluster > 0) {
+        C = static_cast<unsigned>(tuning().accept_cluster);
+        threads = std::min(th, 256);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(d.nact * C);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const int nv = naive ? 1 : 0;
+    if (rt == RowType::F64) RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<double>, d, round, nv));
+    else RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<float>, d, round, nv));
     RS_LAUNCHED();
 }
 

@@ -293,13 +293,25 @@ struct TransformerPair : ModelPair {
         gemm(w.h.p, s.dff, drf->layer.down_w, M, s.d, s.dff, epi_resid(w.x.p, s.d), st);
     }
 
+    // Drafter LM head over n normalised rows in w.xn -> Q rows dst[m]; every drafted row is
+    // sampled, so its softmax tile partials come out of the GEMM epilogue (the fp64 exps run
+    // on the epilogue warps while the next tile accumulates) unless tuned off.
+    void lm_head_q(float *Q, double *qst, const int32_t *dst, int n, cudaStream_t st) {
+        // Measured on B200 (cfg2): the fp64 exps do NOT hide under the next tile's MMAs with
+        // four epilogue warps (drafter GEMMs 1.76 -> 2.78 ms/step vs 0.41 ms for the separate
+        // full-chip kernel), so the separate kernel is the default.
+        const bool fused = qst && tuning().fused_stats > 0;
+        gemm(w.xn.p, s.d, drf->lm_w, n, s.V, s.d,
+             epi_f32(Q, s.V, s.logit_scale, dst, fused ? qst : nullptr, drf->temperature), st);
+        if (qst && !fused) row_stats(Q, dst, n, s.V, drf->temperature, qst, st);
+    }
+
     // LM head of the drafter on n selected rows of w.x (src rows, Q destination rows).
     void drafter_head(const int32_t *src_dev, const int32_t *dst_dev, int n, float *Q, double *qst, cudaStream_t st) {
         float *g = w.e32.p;  // gathered rows
         k_rows_copy_f32(w.x.p, s.d, src_dev, g, s.d, nullptr, n, s.d, st);
         k_rmsnorm(g, s.d, drf->final_norm, n, s.d, s.eps, w.xn.p, s.d, st);
-        gemm(w.xn.p, s.d, drf->lm_w, n, s.V, s.d, epi_f32(Q, s.V, s.logit_scale, dst_dev), st);
-        if (qst) row_stats(Q, dst_dev, n, s.V, drf->temperature, qst, st);
+        lm_head_q(Q, qst, dst_dev, n, st);
     }
 
     // ---- ModelPair hooks ---------------------------------------------------------------------
@@ -368,8 +380,7 @@ struct TransformerPair : ModelPair {
         k_rows_copy_f32(dh.p, s.d, w.map_a.p, w.x.p, s.d, nullptr, M, s.d, st);
         drafter_layer(d, M, (int)bt.items.size(), st);
         k_rmsnorm(w.x.p, s.d, drf->final_norm, M, s.d, s.eps, w.xn.p, s.d, st);
-        gemm(w.xn.p, s.d, drf->lm_w, M, s.V, s.d, epi_f32(Q, s.V, s.logit_scale, w.map_b.p), st);
-        if (d.Qst) row_stats(Q, w.map_b.p, M, s.V, drf->temperature, const_cast<double *>(d.Qst), st);
+        lm_head_q(Q, const_cast<double *>(d.Qst), w.map_b.p, M, st);
         k_rows_copy_f32(w.x.p, s.d, nullptr, dh.p, s.d, w.map_a.p, M, s.d, st);
     }
 
@@ -399,7 +410,8 @@ struct TransformerPair : ModelPair {
         }
         upload(bt, st);
         if (!naive) stage.upload(rbase.p, base, st);
-        target_forward(d, bt.M(), (int)bt.items.size(), P, true, st, const_cast<double *>(d.Pst));
+        // no stats pass over the verified rows: acceptance computes the 2-3 rows it touches
+        target_forward(d, bt.M(), (int)bt.items.size(), P, true, st, d.lazy_pst ? nullptr : const_cast<double *>(d.Pst));
     }
 
     void after_accept(const SdDev &d, bool naive, cudaStream_t st) override {

@@ -114,3 +114,36 @@ def test_gemm_swiglu():
     g, u = A.float() @ G.float().t(), A.float() @ U.float().t()
     ref = torch.nn.functional.silu(g) * u
     assert (out.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item() + 1e-3
+
+
+@pytest.mark.parametrize("M,N,K,tau", [(256, 151936, 2048, 1.0), (37, 4104, 256, 0.7), (130, 1024, 128, 1.3)])
+def test_lm_head_fused_stats_bitwise(M, N, K, tau):
+    """LM-head epilogue softmax partials == the stand-alone row-stats kernel, BITWISE (same
+    tile order, tilestat.cuh), and == a torch fp64 restatement within 1e-12 relative."""
+    torch.manual_seed(N)
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    B = (torch.randn(N, K, device="cuda") * 0.05).bfloat16()
+    B[5] = 0  # a constant column (ties inside one tile)
+    nt = (N + 255) // 256
+    out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    fused = torch.full((M, nt, 2), float("nan"), device="cuda", dtype=torch.float64)
+    sep = torch.full_like(fused, float("nan"))
+    dev = rb.default_device()
+    torch.cuda.synchronize()
+    rb._check(rb.lib().rs_lm_head_bf16(dev.handle, ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
+                                       ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(fused.data_ptr()),
+                                       M, N, K, 2.0, tau))
+    rb._check(rb.lib().rs_row_stats(dev.handle, ctypes.c_void_p(out.data_ptr()), M, N, tau,
+                                    ctypes.c_void_p(sep.data_ptr())))
+    dev.sync()
+    ref = (A.float() @ B.float().t()) * 2.0
+    assert (out - ref).abs().max().item() <= 2e-3 * ref.abs().max().item()
+    assert torch.equal(fused, sep)
+    y = out.double()[:, : N - 1]
+    y = y / torch.full_like(y, tau)  # true division (a python-scalar divisor may become a reciprocal multiply)
+    pad = nt * 256 - (N - 1)
+    y = torch.nn.functional.pad(y, (0, pad), value=float("-inf")).view(M, nt, 256)
+    m = y.max(-1).values
+    s = torch.exp(y - m[..., None]).sum(-1)
+    assert torch.equal(fused[..., 0], m)
+    assert torch.allclose(fused[..., 1], s, rtol=1e-12, atol=0)
