@@ -229,6 +229,7 @@ def main():
     eng = rb.BatchEngine(target, lambda: drafter, None, rb.TimingModel(), reqs, cfg, args.verify,
                          record_full_logprobs=False, device=dev)
     prefill_s = time.perf_counter() - t_pre
+    print(f"[bench] prefill {prefill_s:.2f} s", file=sys.stderr, flush=True)
 
     def barrier():
         if world > 1:
@@ -236,6 +237,7 @@ def main():
 
     for _ in range(args.warmup):
         eng.step()
+    print("[bench] warm-up done", file=sys.stderr, flush=True)
 
     clocks = ClockSampler(local)
     clocks.start()

@@ -48,6 +48,7 @@ const char *dev_err_message(int code);
 // Process-wide tuning knobs set through rs_set_tuning (0 = automatic).
 struct Tuning {
     int accept_cluster = 0;
+    int attn_tc = 0;      // target attention: 0 / 1 tcgen05 kernel, -1 legacy mma.sync kernel
     int fused_stats = 0;  // drafter LM-head stats: 1 fused GEMM epilogue; 0 / -1 separate row-stats kernel
 };
 Tuning &tuning();

@@ -37,6 +37,7 @@ Tuning &tuning() {
                     const int v = std::atoi(kv.c_str() + eq + 1);
                     if (k == "accept_cluster") x.accept_cluster = v;
                     else if (k == "fused_stats") x.fused_stats = v;
+                    else if (k == "attn_tc") x.attn_tc = v;
                 }
                 p = e + 1;
             }

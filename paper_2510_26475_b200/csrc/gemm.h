@@ -1,5 +1,6 @@
 // gemm.h -- tcgen05 bf16 GEMM launcher (gemm_sm100.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace rs {
@@ -35,5 +36,9 @@ struct GemmArgs {
 // SwiGLU layout: B rows are interleaved per 256-row block as [128 gate rows, 128 up rows];
 // output column j = silu(gate_j) * up_j, N_out = N / 2.
 void gemm_bf16(const GemmArgs &g, cudaStream_t st);
+
+// 2D bf16 TMA map over a row-major [rows, cols] matrix (leading dim `ld` elements), box of
+// 64 columns x box_rows rows, 128B swizzle (gemm_sm100.cu).
+CUtensorMap make_tma_map_bf16(const void *base, int rows, int cols, int ld, int box_rows);
 
 }  // namespace rs

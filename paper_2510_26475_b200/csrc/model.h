@@ -78,7 +78,29 @@ struct RowDesc {
 struct AttnItem {
     int seq, row0, nrows, maxpos;
     int chain, ltree, tbase, nstride;  // keys at logical p >= ltree map to tbase + chain*nstride + (p-ltree)
+    int pass0 = 0, npass = 0, grp0 = 0, ngrp = 0;  // tensor-core attention plan (AttnPlan slices)
 };
+
+// Host-built pass plan of the tensor-core attention (attention_tc.cu): per item, the key
+// chunks it visits in logical order and, for chunks reaching into a draft tree, one replay per
+// group of tokens sharing a key mapping (one draft chain; the root rides with chain 0).
+struct AttnPass {
+    int16_t chunk, grp;  // grp -1: shared by every row of the item
+    uint8_t tiles;       // bit i: 128-row M-tile i takes part
+    uint8_t manual;      // 1: keys remapped to a chain's slots (cp.async), 0: contiguous (TMA)
+    int16_t pad;
+};
+struct AttnGroup {
+    int chain, maxpos;
+};
+struct AttnPlan {
+    const AttnPass *passes = nullptr;
+    const AttnGroup *groups = nullptr;
+    const int16_t *tok_grp = nullptr;  // per forward row: group index within its item
+};
+constexpr int kAttnChunk = 128;     // keys per chunk of the tensor-core attention
+constexpr int kAttnMaxPasses = 192;
+constexpr int kAttnMaxGroups = 64;
 
 struct KvCache {
     bf16 *k = nullptr, *v = nullptr;  // [layer][B][KV][max_ctx][hd]
@@ -103,6 +125,12 @@ int attn_max_warps();
 // flops / bytes: algorithmic work of the launch (profiling only)
 void k_attention(const bf16 *q, const RowDesc *rows, const AttnItem *items, int n_items, const KvCache &kv, int layer,
                  const TfShape &s, bf16 *out, cudaStream_t st, double flops = 0, double bytes = 0);
+// Target attention on tcgen05/TMEM (attention_tc.cu): same items (chain -1 plain, -2 tree),
+// at most attn_tc_max_tokens(G) tokens per item.
+int attn_tc_max_tokens(int G);
+void k_attention_tc(const bf16 *q, const RowDesc *rows, const AttnItem *items, const AttnPlan &plan, int n_items,
+                    const KvCache &kv, int layer, const TfShape &s, bf16 *out, cudaStream_t st, double flops = 0,
+                    double bytes = 0);
 void k_store_features(const float *x, const RowDesc *rows, int M, int d, bf16 *feat, int max_ctx, int slot,
                       cudaStream_t st);
 void k_gather_features(const RowDesc *rows, int M, int d, const bf16 *feat, int max_ctx, const float *hid, bf16 *fin,

@@ -61,6 +61,14 @@ struct Workspace {
     DBuf<RowDesc> rows;
     DBuf<AttnItem> items;
     DBuf<int32_t> map_a, map_b, idx;
+    DBuf<AttnGroup> groups;
+    DBuf<int16_t> tok_grp;
+    DBuf<AttnPass> passes;
+    void ensure_passes(size_t n, cudaStream_t st) {
+        if (n <= passes.n) return;
+        RS_CUDA(cudaStreamSynchronize(st));
+        passes.alloc(std::max(n, 2 * passes.n));
+    }
     void alloc(int M, const TfShape &s) {
         Mcap = M;
         x.alloc((size_t)M * s.d);
@@ -76,6 +84,9 @@ struct Workspace {
         map_a.alloc(M);
         map_b.alloc(M);
         idx.alloc((size_t)2 * M);
+        groups.alloc(M);
+        tok_grp.alloc(M);
+        passes.alloc((size_t)M * 8);
     }
 };
 
@@ -132,11 +143,66 @@ struct Batch {
     std::vector<RowDesc> rows;
     std::vector<AttnItem> items;
     std::vector<int32_t> map_a, map_b;
+    std::vector<AttnPass> passes;
+    std::vector<AttnGroup> groups;
+    std::vector<int16_t> tok_grp;
     void clear() {
         rows.clear();
         items.clear();
         map_a.clear();
         map_b.clear();
+        passes.clear();
+        groups.clear();
+        tok_grp.clear();
+    }
+    // Pass plan of every item for the tensor-core attention (G query heads per kv head).
+    void plan_tc(int G) {
+        passes.clear();
+        groups.clear();
+        tok_grp.assign(rows.size(), 0);
+        const int T = 128 / G;
+        for (auto &it : items) {
+            it.pass0 = (int)passes.size();
+            it.grp0 = (int)groups.size();
+            const int ntok = it.nrows;
+            int ng = 0;
+            for (int k = 0; k < ntok;) {
+                int ch = rows[it.row0 + k].chain, k1 = k + 1;
+                if (it.chain == -2) {  // consecutive tokens of one chain; the root joins chain 0
+                    if (ch < 0 && k1 < ntok && rows[it.row0 + k1].chain == 0) ch = 0;
+                    while (k1 < ntok && rows[it.row0 + k1].chain == ch) ++k1;
+                } else {
+                    ch = -1;
+                    k1 = ntok;
+                }
+                int gmax = 0;
+                for (int j = k; j < k1; ++j) {
+                    tok_grp[it.row0 + j] = (int16_t)ng;
+                    gmax = std::max(gmax, rows[it.row0 + j].pos);
+                }
+                groups.push_back(AttnGroup{ch, gmax});
+                ++ng;
+                k = k1;
+            }
+            for (int c = 0; c <= it.maxpos / kAttnChunk; ++c) {
+                const int c0 = c * kAttnChunk;
+                const bool tail = it.chain == -2 && c0 + kAttnChunk - 1 >= it.ltree;
+                for (int g = tail ? 0 : -1; g < (tail ? ng : 0); ++g) {
+                    uint8_t tiles = 0;
+                    for (int k = 0; k < ntok; ++k)
+                        if ((g < 0 || tok_grp[it.row0 + k] == g) && rows[it.row0 + k].pos >= c0)
+                            tiles |= (uint8_t)(1u << (k / T));
+                    if (!tiles) continue;
+                    const int ch = g < 0 ? -1 : groups[it.grp0 + g].chain;
+                    const bool contiguous = ch < 0 || (ch == 0 && it.tbase == it.ltree);
+                    passes.push_back(AttnPass{(int16_t)c, (int16_t)g, tiles, (uint8_t)(contiguous ? 0 : 1), 0});
+                }
+            }
+            it.npass = (int)passes.size() - it.pass0;
+            it.ngrp = ng;
+            if (it.npass > kAttnMaxPasses || ng > kAttnMaxGroups || ntok > 2 * T)
+                throw std::runtime_error("attention plan exceeds the kernel's limits");
+        }
     }
     // plain causal attention items over rows [r0, r1) of one sequence (keys = its cache)
     void add_items(int r0, int r1, int per, int chain, int ltree, int tbase, int nstride) {
@@ -169,6 +235,16 @@ struct Batch {
         }
         if (k > a) items.push_back(AttnItem{rows[a].seq, a, k - a, maxpos, -2, ltree, tbase, nstride});
     }
+    // tree items for the tensor-core attention: consecutive runs of at most max_tok tokens (two
+    // 128-row M-tiles); the kernel regroups tokens by chain inside an item.
+    void add_tree_items_tc(int r0, int r1, int max_tok, int ltree, int tbase, int nstride) {
+        for (int a = r0; a < r1; a += max_tok) {
+            const int b = std::min(r1, a + max_tok);
+            int maxpos = 0;
+            for (int k = a; k < b; ++k) maxpos = std::max(maxpos, rows[k].pos);
+            items.push_back(AttnItem{rows[a].seq, a, b - a, maxpos, -2, ltree, tbase, nstride});
+        }
+    }
     int M() const { return static_cast<int>(rows.size()); }
     // algorithmic attention work: every query head attends to pos+1 keys (QK^T and PV);
     // K/V bytes read once per item and kv head
@@ -190,7 +266,8 @@ struct TransformerPair : ModelPair {
     const TransformerModel *tgt;
     const DrafterModel *drf = nullptr;
     TfShape s;
-    int B = 0, slots_max = 1, max_ctx = 0, per_item = 8;
+    int B = 0, slots_max = 1, max_ctx = 0, per_item = 8, per_item_t = 8;
+    bool tc_attn = true;  // target attention on tcgen05 (attention_tc.cu); fixed for the engine's life
     KvCache kv_t, kv_d;
     DBuf<bf16> kt, vt, kd, vd, feat;
     DBuf<float> dh;  // drafter hidden per (request, chain) [B][t_max][d]
@@ -219,6 +296,8 @@ struct TransformerPair : ModelPair {
         slots_max = slots;
         max_ctx = s.max_ctx;
         per_item = attn_max_tokens(s.H / s.KV);
+        tc_attn = tuning().attn_tc >= 0;
+        per_item_t = tc_attn ? attn_tc_max_tokens(s.H / s.KV) : per_item;
         if ((eng->n_max + 1) * (s.H / s.KV) > 16 * attn_max_warps())
             throw std::invalid_argument("transformer engine: (draft_len + 1) * GQA group must be <= 192");
         for (int i = 0; i < n_req; ++i)
@@ -229,6 +308,10 @@ struct TransformerPair : ModelPair {
         kt.alloc(kv_elems);
         vt.alloc(kv_elems);
         kv_t = KvCache{kt.p, vt.p, s.L, B, s.KV, max_ctx, s.hd};
+        // never-written slots must hold finite values: whole 128-key chunks are multiplied by
+        // probabilities that are exactly 0 past a row's position (0 * NaN would poison O)
+        RS_CUDA(cudaMemsetAsync(kt.p, 0, kv_elems * sizeof(bf16), ctx->stream));
+        RS_CUDA(cudaMemsetAsync(vt.p, 0, kv_elems * sizeof(bf16), ctx->stream));
         const size_t kvd = (size_t)B * s.KV * max_ctx * s.hd;
         kd.alloc(kvd);
         vd.alloc(kvd);
@@ -241,8 +324,15 @@ struct TransformerPair : ModelPair {
         dkv_len.assign(n_req, 0);
     }
 
-    void upload(const Batch &b, cudaStream_t st) {
+    void upload(Batch &b, cudaStream_t st, bool tc_plan = false) {
         if (b.M() > w.Mcap) throw std::runtime_error("forward batch exceeds workspace");
+        if (tc_plan) {
+            b.plan_tc(s.H / s.KV);
+            w.ensure_passes(b.passes.size(), st);
+            stage.upload(w.passes.p, b.passes, st);
+            stage.upload(w.groups.p, b.groups, st);
+            stage.upload(w.tok_grp.p, b.tok_grp, st);
+        }
         stage.upload(w.rows.p, b.rows, st);
         stage.upload(w.items.p, b.items, st);
         stage.upload(w.map_a.p, b.map_a, st);
@@ -261,7 +351,10 @@ struct TransformerPair : ModelPair {
             k_rmsnorm(w.x.p, s.d, lw.ln1, M, s.d, s.eps, w.xn.p, s.d, st);
             gemm(w.xn.p, s.d, lw.qkv_w, M, qd, s.d, epi_bf16(w.qkv.p, qd, lw.qkv_b), st);
             k_rope_store(w.qkv.p, w.rows.p, M, s, tgt->rope, kv_t, l, w.q.p, st);
-            k_attention(w.q.p, w.rows.p, w.items.p, ni, kv_t, l, s, w.ao.p, st, attn_f, attn_b);
+            if (tc_attn)
+                k_attention_tc(w.q.p, w.rows.p, w.items.p, AttnPlan{w.passes.p, w.groups.p, w.tok_grp.p}, ni, kv_t, l, s,
+                               w.ao.p, st, attn_f, attn_b);
+            else k_attention(w.q.p, w.rows.p, w.items.p, ni, kv_t, l, s, w.ao.p, st, attn_f, attn_b);
             gemm(w.ao.p, HD, lw.o_w, M, s.d, HD, epi_resid(w.x.p, s.d), st);
             k_rmsnorm(w.x.p, s.d, lw.ln2, M, s.d, s.eps, w.xn.p, s.d, st);
             gemm(w.xn.p, s.d, lw.gu_w, M, 2 * s.dff, s.d, epi_swiglu(w.h.p, s.dff), st);
@@ -397,7 +490,7 @@ struct TransformerPair : ModelPair {
             bt.rows.push_back(RowDesc{r, L - 1, L - 1, 0, -1, 0, 0, 0});
             bt.map_a.push_back(a * d.slots);
             if (naive) {
-                bt.add_items(r0, bt.M(), per_item, -1, 0, 0, 0);
+                bt.add_items(r0, bt.M(), per_item_t, -1, 0, 0, 0);
                 continue;
             }
             for (int i = 0; i < d.t; ++i)
@@ -406,9 +499,10 @@ struct TransformerPair : ModelPair {
                     bt.map_a.push_back(a * d.slots + 1 + i * d.n + j);
                 }
             // one CTA per (sequence, kv head) for the whole tree; the root rides with chain 0
-            bt.add_tree_items(r0, bt.M(), s.H / s.KV, L, L, d.n);
+            if (tc_attn) bt.add_tree_items_tc(r0, bt.M(), per_item_t, L, L, d.n);
+            else bt.add_tree_items(r0, bt.M(), s.H / s.KV, L, L, d.n);
         }
-        upload(bt, st);
+        upload(bt, st, tc_attn);
         if (!naive) stage.upload(rbase.p, base, st);
         // no stats pass over the verified rows: acceptance computes the 2-3 rows it touches
         target_forward(d, bt.M(), (int)bt.items.size(), P, true, st, d.lazy_pst ? nullptr : const_cast<double *>(d.Pst));
@@ -437,10 +531,10 @@ struct TransformerPair : ModelPair {
                 const int take = std::min(P - 1 - p, w.Mcap - bt.M());
                 const int r0 = bt.M();
                 for (int k = 0; k < take; ++k, ++p) bt.rows.push_back(RowDesc{(int)r, p, p, 0, -1, 0, 0, 0});
-                bt.add_items(r0, bt.M(), per_item, -1, 0, 0, 0);
+                bt.add_items(r0, bt.M(), per_item_t, -1, 0, 0, 0);
             }
             if (bt.M() == 0) break;
-            upload(bt, st);
+            upload(bt, st, tc_attn);
             target_forward(d, bt.M(), (int)bt.items.size(), nullptr, false, st);
             RS_CUDA(cudaStreamSynchronize(st));
             stage.off = 0;
