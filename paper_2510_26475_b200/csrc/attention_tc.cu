@@ -24,6 +24,7 @@
 //               TMEM (tcgen05.st), rescales O in TMEM when the running max moves, and finally
 //               writes O / l as bf16.
 // TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512) columns.
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -47,7 +48,7 @@ constexpr int kQBytes = 2 * kTileBytes;        // two M-tiles
 constexpr int kMaxPasses = kAttnMaxPasses;
 constexpr int kMaxGroups = kAttnMaxGroups;
 constexpr int kMaxTok = 256;
-constexpr int kThreads = 384;
+constexpr int kThreads = 640;  // 4 control warps + 2 x 8 softmax warps
 constexpr uint32_t kIdescS = (1u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
 constexpr uint32_t kIdescPV = kIdescS | (1u << 16);  // B (= V) is MN-major
 
@@ -59,6 +60,7 @@ struct Plan {
     short tok_grp[kMaxTok];
     int tok_pos[kMaxTok];
     Pass pass[kMaxPasses];
+    float xch[2 * 4 * 2 * 32];  // softmax pair exchange [tile][quadrant][half][lane]
 };
 
 constexpr int kBarBytes = 256;
@@ -84,14 +86,20 @@ __device__ __forceinline__ uint32_t swz_off(int r, int c) {
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, const bf16 *q,
                    const RowDesc *rows, const AttnItem *items, AttnPlan plan, KvCache kv, int layer, int H, int KV,
-                   float scale_log2, bf16 *out) {
+                   float scale_log2, bf16 *out, long long *trace) {
+    // trace (diagnostics, CTA (0,0) only): [0] start, per pass j: [1+4j] fullK ok, [2+4j] p0 ok,
+    // [3+4j] p1 ok (MMA thread), [4+4j] softmax tile 0 s_full ok
+    const bool tr = trace && blockIdx.x == 0 && blockIdx.y == 0;
+    if (tr && threadIdx.x == 0) trace[0] = clock64();
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sQ = smem;
     uint8_t *sKV = smem + kQBytes;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sKV + kStages * kStageBytes);
-    uint64_t *full = bars, *empty = bars + kStages;
-    uint64_t *s_full = bars + 2 * kStages, *p_full = s_full + 2, *o_done = p_full + 2;
+    // K and V halves of a stage fill and drain separately: S = Q K^T can start while V is in
+    // flight, and K(j + 2) loads as soon as the S MMAs of pass j are done.
+    uint64_t *fullK = bars, *fullV = bars + kStages, *emptyK = bars + 2 * kStages, *emptyV = bars + 3 * kStages;
+    uint64_t *s_full = bars + 4 * kStages, *p_full = s_full + 2, *o_done = p_full + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_done + 1);
     Plan &pl = *reinterpret_cast<Plan *>(reinterpret_cast<uint8_t *>(bars) + kBarBytes);
 
@@ -121,12 +129,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&fullK[s], 1);
+            mbar_init(&fullV[s], 1);
+            mbar_init(&emptyK[s], 1);
+            mbar_init(&emptyV[s], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], 4);
+            mbar_init(&p_full[i], 8);
         }
         mbar_init(o_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -138,19 +148,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                      "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
     }
-    // ---- Q tiles -> smem (softmax warps: one row each, zero rows beyond the item) -------------
+    // ---- Q tiles -> smem (softmax warps: half a row each, zero rows beyond the item) ----------
     if (warp >= 4) {
         const int T0 = 128 / G;
-        const int tile = (warp - 4) >> 2, r = ((warp - 4) & 3) * 32 + lane;
+        const int tile = (warp - 4) >> 3, half = ((warp - 4) >> 2) & 1, r = (warp & 3) * 32 + lane;
         const int k = tile * T0 + r / G;
         const bool valid = r < T0 * G && k < it.nrows;
         uint8_t *base = sQ + tile * kTileBytes;
-        const bf16 *src = q + ((size_t)(it.row0 + k) * H + kvh * G + r % G) * kHD;
-        int4 v[16];
+        const bf16 *src = q + ((size_t)(it.row0 + k) * H + kvh * G + r % G) * kHD + half * 64;
+        int4 v[8];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) v[c] = valid ? *reinterpret_cast<const int4 *>(src + c * 8) : make_int4(0, 0, 0, 0);
+        for (int c = 0; c < 8; ++c) v[c] = valid ? *reinterpret_cast<const int4 *>(src + c * 8) : make_int4(0, 0, 0, 0);
 #pragma unroll
-        for (int c = 0; c < 16; ++c) *reinterpret_cast<int4 *>(base + swz_off(r, c)) = v[c];
+        for (int c = 0; c < 8; ++c) *reinterpret_cast<int4 *>(base + swz_off(r, half * 8 + c)) = v[c];
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     const int T = 128 / G;
@@ -169,19 +179,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < np; ++j) {
             const Pass ps = pl.pass[j];
             const int s = j % kStages;
-            mbar_wait(&empty[s], ((j / kStages) & 1) ^ 1);
+            const uint32_t par = ((j / kStages) & 1) ^ 1;
             uint8_t *dst = sKV + s * kStageBytes;
             if (!ps.manual) {
+                const int y = (int)(kvrow0 + ps.chunk * kCk);
+                mbar_wait(&emptyK[s], par);
                 if (t == 0) {
-                    mbar_arrive_expect_tx(&full[s], kStageBytes);
-                    const int y = (int)(kvrow0 + ps.chunk * kCk);
-                    tma_load_2d(dst, &tmK, &full[s], 0, y);
-                    tma_load_2d(dst + kHalfBytes, &tmK, &full[s], 64, y);
-                    tma_load_2d(dst + kTileBytes, &tmV, &full[s], 0, y);
-                    tma_load_2d(dst + kTileBytes + kHalfBytes, &tmV, &full[s], 64, y);
+                    mbar_arrive_expect_tx(&fullK[s], kTileBytes);
+                    tma_load_2d(dst, &tmK, &fullK[s], 0, y);
+                    tma_load_2d(dst + kHalfBytes, &tmK, &fullK[s], 64, y);
+                }
+                mbar_wait(&emptyV[s], par);
+                if (t == 0) {
+                    mbar_arrive_expect_tx(&fullV[s], kTileBytes);
+                    tma_load_2d(dst + kTileBytes, &tmV, &fullV[s], 0, y);
+                    tma_load_2d(dst + kTileBytes + kHalfBytes, &tmV, &fullV[s], 64, y);
                 }
                 continue;
             }
+            mbar_wait(&emptyK[s], par);
+            mbar_wait(&emptyV[s], par);
             const int ch = pl.g_chain[ps.grp], lim = pl.g_maxpos[ps.grp];
             for (int idx = t; idx < kCk * 16; idx += 64) {
                 const int r = idx >> 4, c = idx & 15;
@@ -200,7 +217,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             asm volatile("cp.async.wait_all;" ::: "memory");
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("bar.sync 1, 64;" ::: "memory");
-            if (t == 0) mbar_arrive(&full[s]);
+            if (t == 0) {
+                mbar_arrive(&fullK[s]);
+                mbar_arrive(&fullV[s]);
+            }
         }
     } else if (warp == 1) {
         // ---- MMA issuer ---------------------------------------------------------------------------
@@ -211,7 +231,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < np; ++j) users[j] = (uint8_t)__popc(pl.pass[j].tiles);
             auto issue_pv = [&](int i) {
                 const int jp = pend[i];
+                mbar_wait(&fullV[jp % kStages], (jp / kStages) & 1);
                 mbar_wait(&p_full[i], pv_n[i] & 1);
+                if (tr) trace[2 + 4 * jp + i] = clock64();
                 tc_fence_after();
                 const uint8_t *v = sKV + (jp % kStages) * kStageBytes + kTileBytes;
                 const uint32_t d_o = tmem + 256 + i * 128, a_p = tmem + i * 128;
@@ -221,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                               (pv_n[i] > 0 || k > 0) ? 1u : 0u);
                 ++pv_n[i];
                 pend[i] = -1;
-                if (--users[jp] == 0) tc_commit(&empty[jp % kStages]);
+                if (--users[jp] == 0) tc_commit(&emptyV[jp % kStages]);
             };
             for (int j = 0; j < np; ++j) {
                 const Pass ps = pl.pass[j];
@@ -229,7 +251,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < 2; ++i)
                     if (pend[i] >= 0 && pend[i] <= j - kStages) issue_pv(i);
                 const int s = j % kStages;
-                mbar_wait(&full[s], (j / kStages) & 1);
+                mbar_wait(&fullK[s], (j / kStages) & 1);
+                if (tr) trace[1 + 4 * j] = clock64();
                 tc_fence_after();
                 const uint8_t *kt = sKV + s * kStageBytes;
                 for (int i = 0; i < 2; ++i) {
@@ -246,19 +269,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_commit(&s_full[i]);
                     pend[i] = j;
                 }
+                tc_commit(&emptyK[s]);
             }
             for (int i = 0; i < 2; ++i)
                 if (pend[i] >= 0) issue_pv(i);
             tc_commit(o_done);
         }
     } else if (warp >= 4) {
-        // ---- softmax: one thread per row of M-tile `tile` ----------------------------------------
-        // Per pass: row max over the visible columns (TMEM read #1), then p = 2^(s*scale - m)
-        // written as bf16 over the consumed S columns (TMEM read #2). The running max m only
-        // moves when the chunk max exceeds it by more than 2^8 (so p <= 256): O in TMEM is then
-        // rescaled. The row sum is kept as 8 interleaved partials. Every choice depends only on
-        // the row's own scores, so the arithmetic is identical whatever item the row sits in.
-        const int tile = (warp - 4) >> 2, qd = (warp - 4) & 3;
+        // ---- softmax: two threads per row of M-tile `tile` (column halves) --------------------
+        // Per pass: one TMEM read of the thread's 64 scores, the row max combined with the
+        // partner thread (same TMEM lane, other half) through shared memory, p = 2^(s*scale - m)
+        // written as bf16 over the consumed S columns. The running max m only moves when the
+        // chunk max exceeds it by more than 2^8 (so p <= 256): O in TMEM is then rescaled. Row
+        // sums are kept as 8 interleaved partials per half. Every choice depends only on the
+        // row's own scores, so the arithmetic is identical whatever item the row sits in.
+        const int tile = (warp - 4) >> 3, half = ((warp - 4) >> 2) & 1, qd = warp & 3;
         const int r = qd * 32 + lane;
         const int k = tile * T + r / G;
         const bool valid = r < T * G && k < pl.ntok;
@@ -266,7 +291,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int pos = valid ? pl.tok_pos[k] : -1;
         const int grp = valid ? pl.tok_grp[k] : -2;
         const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-        const uint32_t tS = tmem + lane_off + tile * 128, tO = tmem + lane_off + 256 + tile * 128;
+        const uint32_t tS = tmem + lane_off + tile * 128, tO = tmem + lane_off + 256 + tile * 128 + half * 64;
+        float *xch = reinterpret_cast<float *>(pl.xch) + ((tile * 4 + qd) * 2) * 32;  // [half][lane]
+        const int bar_id = 2 + tile * 4 + qd;
         float m = -INFINITY;
         float lp[8];
 #pragma unroll
@@ -276,83 +303,74 @@ __global__ void __launch_bounds__(kThreads, 1)
             const Pass ps = pl.pass[j];
             if (!(ps.tiles & (1 << tile))) continue;
             mbar_wait(&s_full[tile], n & 1);
+            if (tr && tile == 0 && warp == 4 && lane == 0) trace[4 + 4 * j] = clock64();
             tc_fence_after();
-            const int c0 = ps.chunk * kCk;
+            const int c0 = ps.chunk * kCk + half * 64;
             const bool mine = valid && (ps.grp < 0 || ps.grp == grp);
-            const int lim = mine ? pos - c0 : -1;  // columns x <= lim are visible
+            const int lim = mine ? pos - c0 : -1;  // own columns x <= lim are visible
+            // both halves of a pair see the same rows, so this branch is pair-uniform
             if (warp_valid) {
-                if (!__any_sync(0xffffffffu, lim >= 0)) {
-                    // no visible key in this warp: P rows = 0 (O unchanged)
-                    uint32_t z[16];
+                uint32_t v[64];
+                tmem_ld32_nw(tS + half * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+                tmem_ld32_nw(tS + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+                tmem_ld_wait();
+                float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+                if (lim >= 63) {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) z[i] = 0u;
-#pragma unroll 1
-                    for (int cc = 0; cc < 4; ++cc) tmem_st16(tS + cc * 16, z);
+                    for (int x = 0; x < 64; x += 4) {
+                        mx0 = fmaxf(mx0, __uint_as_float(v[x]));
+                        mx1 = fmaxf(mx1, __uint_as_float(v[x + 1]));
+                        mx2 = fmaxf(mx2, __uint_as_float(v[x + 2]));
+                        mx3 = fmaxf(mx3, __uint_as_float(v[x + 3]));
+                    }
                 } else {
-                    float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-#pragma unroll 1
-                    for (int cc = 0; cc < 4; ++cc) {
-                        uint32_t v[32];
-                        tmem_ld32(tS + cc * 32, v);
-                        if (lim >= cc * 32 + 31) {
 #pragma unroll
-                            for (int x = 0; x < 32; x += 4) {
-                                mx0 = fmaxf(mx0, __uint_as_float(v[x]));
-                                mx1 = fmaxf(mx1, __uint_as_float(v[x + 1]));
-                                mx2 = fmaxf(mx2, __uint_as_float(v[x + 2]));
-                                mx3 = fmaxf(mx3, __uint_as_float(v[x + 3]));
-                            }
-                        } else {
+                    for (int x = 0; x < 64; ++x)
+                        if (x <= lim) mx0 = fmaxf(mx0, __uint_as_float(v[x]));
+                }
+                xch[half * 32 + lane] = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+                asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");  // both halves loaded S
+                float mx = fmaxf(xch[lane], xch[32 + lane]);
+                mx = mx == -INFINITY ? mx : mx * scale_log2;  // scale > 0: max commutes with it
+                bool resc = false;
+                float alpha = 1.f;
+                if (mx > m) {
+                    if (m == -INFINITY) {
+                        m = mx;  // first visible keys of the row: O row and l are still 0
+                    } else if (mx > m + 8.f) {
+                        alpha = ex2(m - mx);
+                        m = mx;
+                        resc = true;
 #pragma unroll
-                            for (int x = 0; x < 32; ++x)
-                                if (cc * 32 + x <= lim) mx0 = fmaxf(mx0, __uint_as_float(v[x]));
-                        }
+                        for (int i = 0; i < 8; ++i) lp[i] *= alpha;
                     }
-                    float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-                    mx = mx == -INFINITY ? mx : mx * scale_log2;  // scale > 0: max commutes with it
-                    bool resc = false;
-                    float alpha = 1.f;
-                    if (mx > m) {
-                        if (m == -INFINITY) {
-                            m = mx;  // first visible keys of the row: O row and l are still 0
-                        } else if (mx > m + 8.f) {
-                            alpha = ex2(m - mx);
-                            m = mx;
-                            resc = true;
+                }
+                const float nb = m == -INFINITY ? 0.f : -m;
+                uint32_t pk[32];
+                const bool all = lim >= 63;
 #pragma unroll
-                            for (int i = 0; i < 8; ++i) lp[i] *= alpha;
-                        }
+                for (int x = 0; x < 64; x += 2) {
+                    float p0 = ex2(fmaf(__uint_as_float(v[x]), scale_log2, nb));
+                    float p1 = ex2(fmaf(__uint_as_float(v[x + 1]), scale_log2, nb));
+                    if (!all) {
+                        p0 = x <= lim ? p0 : 0.f;
+                        p1 = x + 1 <= lim ? p1 : 0.f;
                     }
-                    const float nb = m == -INFINITY ? 0.f : -m;
+                    lp[x & 7] += p0;
+                    lp[(x + 1) & 7] += p1;
+                    pk[x >> 1] = pack_bf16(p0, p1);
+                }
+                // P (bf16) of this half over S columns [32 half, 32 half + 32), already read by both
+                tmem_st16(tS + half * 32, *reinterpret_cast<uint32_t(*)[16]>(pk));
+                tmem_st16(tS + half * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(pk + 16));
+                if (n > 0 && __any_sync(0xffffffffu, resc)) {
 #pragma unroll 1
-                    for (int cc = 0; cc < 4; ++cc) {
-                        uint32_t v[32];
-                        tmem_ld32(tS + cc * 32, v);
-                        uint32_t pk[16];
-                        const bool all = lim >= cc * 32 + 31;
+                    for (int cc = 0; cc < 2; ++cc) {
+                        uint32_t o[32];
+                        tmem_ld32(tO + cc * 32, o);
 #pragma unroll
-                        for (int x = 0; x < 32; x += 2) {
-                            float p0 = ex2(fmaf(__uint_as_float(v[x]), scale_log2, nb));
-                            float p1 = ex2(fmaf(__uint_as_float(v[x + 1]), scale_log2, nb));
-                            if (!all) {
-                                p0 = cc * 32 + x <= lim ? p0 : 0.f;
-                                p1 = cc * 32 + x + 1 <= lim ? p1 : 0.f;
-                            }
-                            lp[x & 7] += p0;
-                            lp[(x + 1) & 7] += p1;
-                            pk[x >> 1] = pack_bf16(p0, p1);
-                        }
-                        tmem_st16(tS + cc * 16, pk);  // P (bf16) over the S columns already consumed
-                    }
-                    if (n > 0 && __any_sync(0xffffffffu, resc)) {
-#pragma unroll 1
-                        for (int cc = 0; cc < 4; ++cc) {
-                            uint32_t v[32];
-                            tmem_ld32(tO + cc * 32, v);
-#pragma unroll
-                            for (int x = 0; x < 32; ++x) v[x] = __float_as_uint(__uint_as_float(v[x]) * alpha);
-                            tmem_st32(tO + cc * 32, v);
-                        }
+                        for (int x = 0; x < 32; ++x) o[x] = __float_as_uint(__uint_as_float(o[x]) * alpha);
+                        tmem_st32(tO + cc * 32, o);
                     }
                 }
                 tmem_st_wait();
@@ -363,23 +381,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++n;
         }
         if (n > 0 && warp_valid) {
+            float lh = ((lp[0] + lp[1]) + (lp[2] + lp[3])) + ((lp[4] + lp[5]) + (lp[6] + lp[7]));
+            xch[half * 32 + lane] = lh;
+            asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+            const float l = xch[lane] + xch[32 + lane];
             mbar_wait(o_done, 0);
             tc_fence_after();
-            const float l = ((lp[0] + lp[1]) + (lp[2] + lp[3])) + ((lp[4] + lp[5]) + (lp[6] + lp[7]));
             const float inv = l > 0.f ? 1.f / l : 0.f;
-            bf16 *dst = out + ((size_t)(it.row0 + (valid ? k : 0)) * H + kvh * G + r % G) * kHD;
+            bf16 *dst = out + ((size_t)(it.row0 + (valid ? k : 0)) * H + kvh * G + r % G) * kHD + half * 64;
 #pragma unroll 1
-            for (int cc = 0; cc < 4; ++cc) {
-                uint32_t v[32];
-                tmem_ld32(tO + cc * 32, v);
+            for (int cc = 0; cc < 2; ++cc) {
+                uint32_t o[32];
+                tmem_ld32(tO + cc * 32, o);
                 if (valid) {
 #pragma unroll
                     for (int x = 0; x < 32; x += 8) {
                         uint4 w;
-                        w.x = pack_bf16(__uint_as_float(v[x]) * inv, __uint_as_float(v[x + 1]) * inv);
-                        w.y = pack_bf16(__uint_as_float(v[x + 2]) * inv, __uint_as_float(v[x + 3]) * inv);
-                        w.z = pack_bf16(__uint_as_float(v[x + 4]) * inv, __uint_as_float(v[x + 5]) * inv);
-                        w.w = pack_bf16(__uint_as_float(v[x + 6]) * inv, __uint_as_float(v[x + 7]) * inv);
+                        w.x = pack_bf16(__uint_as_float(o[x]) * inv, __uint_as_float(o[x + 1]) * inv);
+                        w.y = pack_bf16(__uint_as_float(o[x + 2]) * inv, __uint_as_float(o[x + 3]) * inv);
+                        w.z = pack_bf16(__uint_as_float(o[x + 4]) * inv, __uint_as_float(o[x + 5]) * inv);
+                        w.w = pack_bf16(__uint_as_float(o[x + 6]) * inv, __uint_as_float(o[x + 7]) * inv);
                         *reinterpret_cast<uint4 *>(dst + cc * 32 + x) = w;
                     }
                 }
@@ -415,8 +436,22 @@ void k_attention_tc(const bf16 *q, const RowDesc *rows, const AttnItem *items, c
     const CUtensorMap tk = make_tma_map_bf16(kv.k, total_rows, kHD, kHD, kCk);
     const CUtensorMap tv = make_tma_map_bf16(kv.v, total_rows, kHD, kHD, kCk);
     const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(s.hd));
+    static long long *trace = nullptr;
+    if (tuning().attn_trace && !trace) RS_CUDA(cudaMalloc(&trace, 8 * (1 + 4 * kMaxPasses)));
     attn_tc_kernel<<<dim3(n_items, s.KV), kThreads, kSmem, st>>>(tk, tv, q, rows, items, plan, kv, layer, s.H,
-                                                                 s.KV, scale_log2, out);
+                                                                 s.KV, scale_log2, out,
+                                                                 tuning().attn_trace ? trace : nullptr);
+    if (tuning().attn_trace) {
+        RS_CUDA(cudaStreamSynchronize(st));
+        static long long host[1 + 4 * kMaxPasses];
+        RS_CUDA(cudaMemcpy(host, trace, sizeof(host), cudaMemcpyDeviceToHost));
+        if (tuning().attn_trace == layer + 1 && n_items >= 32) {
+            fprintf(stderr, "attn trace layer %d items %d passes %d:\n", layer, n_items, 0);
+            for (int j = 0; j < 24; ++j)
+                fprintf(stderr, "  pass %2d fullK %8lld p0 %8lld p1 %8lld sm0 %8lld\n", j, host[1 + 4 * j] - host[0],
+                        host[2 + 4 * j] - host[0], host[3 + 4 * j] - host[0], host[4 + 4 * j] - host[0]);
+        }
+    }
     RS_LAUNCHED();
 }
 

@@ -49,7 +49,8 @@ const char *dev_err_message(int code);
 struct Tuning {
     int accept_cluster = 0;
     int attn_tc = 0;      // target attention: 0 / 1 tcgen05 kernel, -1 legacy mma.sync kernel
-    int fused_stats = 0;  // drafter LM-head stats: 1 fused GEMM epilogue; 0 / -1 separate row-stats kernel
+    int fused_stats = 0;
+    int attn_trace = 0;   // diagnostics: layer + 1 whose attention pass timeline is printed  // drafter LM-head stats: 1 fused GEMM epilogue; 0 / -1 separate row-stats kernel
 };
 Tuning &tuning();
 

@@ -38,6 +38,7 @@ Tuning &tuning() {
                     if (k == "accept_cluster") x.accept_cluster = v;
                     else if (k == "fused_stats") x.fused_stats = v;
                     else if (k == "attn_tc") x.attn_tc = v;
+                    else if (k == "attn_trace") x.attn_trace = v;
                 }
                 p = e + 1;
             }
