@@ -270,6 +270,23 @@ int rs_kd_grad_tabular(rs_ctx *ctx, const rs_model *drafter, const rs_kd_sample 
                        const double *weights, double *grad_out, double *loss_out);
 int rs_tabular_apply_delta(rs_ctx *ctx, const rs_model *m, const double *grad, double scale, rs_model **out);
 
+/* Transformer drafters (EAGLE-3-style) -- the same kd_update (learner.cpp:98-160) with the
+   drafter's distribution q recomputed by its forward and the target rows p~ recomputed by a
+   teacher-forced target forward over prompt + response (StepRecord::target_logprobs are not
+   materialised at V = 152K; rs_kd_sample.target_logprobs is ignored and may be NULL). The
+   trained parameters are the drafter's LM head: dL/dW_lm = logit_scale * sum_t dZ_t^T h_t with
+   dZ_t = w (q_t - p~_t) / tau (learner.cpp:62-82) and h_t the final-normed drafter hidden state.
+   rs_kd_grad_transformer   -- the per-rank piece: sum_i w_i KL_i and the fp32 [V][d] gradient of
+                               the given samples (accumulated into grad_dev unless zero_grad);
+   rs_drafter_apply_grad    -- new snapshot (version + 1) with lm_w + scale * grad;
+   rs_kd_update_transformer -- single-process kd_update: select, weight, gradient, SGD (-lr). */
+int rs_kd_grad_transformer(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const rs_kd_sample *samples,
+                           int32_t n, const double *weights, float *grad_dev, int32_t zero_grad, double *loss_out);
+int rs_drafter_apply_grad(rs_ctx *ctx, const rs_model *drafter, const float *grad_dev, double scale, rs_model **out);
+int rs_kd_update_transformer(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const rs_kd_sample *buf,
+                             int32_t n, rs_kd_policy policy, uint64_t *selection_rng_state, double cost,
+                             rs_model **new_drafter, rs_kd_result *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -120,7 +120,8 @@ EXPORTED_SYMBOLS = [
     "rs_engine_steps", "rs_engine_step_logprobs", "rs_engine_accept_lens", "rs_engine_destroy",
     "rs_engine_set_capture", "rs_engine_capture_count", "rs_engine_capture_read",
     "rs_kd_weight", "rs_kd_update_tabular", "rs_mt19937_64_seed", "rs_gemm_bf16",
-    "rs_model_tensor", "rs_memcpy_d2d", "rs_model_params", "rs_prof_enable", "rs_prof_reset", "rs_prof_json", "rs_set_tuning", "rs_lm_head_bf16", "rs_row_stats",
+    "rs_model_tensor", "rs_memcpy_d2d", "rs_model_params", "rs_prof_enable", "rs_prof_reset", "rs_prof_json", "rs_set_tuning", "rs_lm_head_bf16", "rs_row_stats", "rs_kd_grad_transformer", "rs_drafter_apply_grad",
+    "rs_kd_update_transformer",
     "rs_kd_select", "rs_kd_grad_tabular", "rs_tabular_apply_delta",
 ]
 
@@ -195,6 +196,10 @@ def lib():
             "rs_set_tuning": ([ctypes.c_char_p, i64], ctypes.c_int),
             "rs_lm_head_bf16": ([vp, vp, vp, vp, vp, i32, i32, i32, ctypes.c_float, dbl], ctypes.c_int),
             "rs_row_stats": ([vp, vp, i32, i32, dbl, vp], ctypes.c_int),
+            "rs_kd_grad_transformer": ([vp, vp, vp, P(_KDSample), i32, P(dbl), vp, i32, P(dbl)], ctypes.c_int),
+            "rs_drafter_apply_grad": ([vp, vp, vp, dbl, P(vp)], ctypes.c_int),
+            "rs_kd_update_transformer": ([vp, vp, vp, P(_KDSample), i32, _KDPolicy, P(u64), dbl, P(vp),
+                                          P(_KDResult)], ctypes.c_int),
             "rs_prof_json": ([ctypes.c_char_p, i64, P(i64)], ctypes.c_int),
             "rs_kd_select": ([i32, i32, P(u64), P(i32), P(i32)], ctypes.c_int),
             "rs_kd_grad_tabular": ([vp, vp, P(_KDSample), i32, P(dbl), P(dbl), P(dbl)], ctypes.c_int),
@@ -520,6 +525,20 @@ class EagleDrafter(_NeuralModel):
         _check(lib().rs_drafter_create(self.device.handle, target.handle, seed & (2 ** 64 - 1), version,
                                        ctypes.byref(h)))
         self.handle = h
+
+    @staticmethod
+    def _wrap(handle, target: TransformerModel) -> "EagleDrafter":
+        m = EagleDrafter.__new__(EagleDrafter)
+        m.handle, m.target, m.shape, m.device = handle, target, target.shape, target.device
+        return m
+
+    def apply_grad(self, grad, scale: float) -> "EagleDrafter":
+        """New snapshot (version + 1): lm_w + scale * grad (fp32 [V][d] device tensor / pointer)."""
+        h = ctypes.c_void_p()
+        ptr = grad.data_ptr() if hasattr(grad, "data_ptr") else grad
+        _check(lib().rs_drafter_apply_grad(self.device.handle, self.handle, ctypes.c_void_p(ptr), scale,
+                                           ctypes.byref(h)))
+        return EagleDrafter._wrap(h, self.target)
 
 
 # ---- ProfileTable (server.hpp:21-49) ------------------------------------------------------------------
@@ -891,9 +910,55 @@ class KDUpdateResult:
     sim_time: float
 
 
-def kd_update(drafter: TabularARModel, buffer: Sequence[RolloutSample], policy: KDPolicy, selection_rng: SelectionRng,
+def _kd_samples(buffer: Sequence[RolloutSample], with_logprobs: bool):
+    keep = []
+    arr = (_KDSample * max(1, len(buffer)))()
+    for i, s in enumerate(buffer):
+        p, r = _i32arr(s.prompt), _i32arr(s.response)
+        lp = None
+        if with_logprobs:
+            if len(s.steps) != len(s.response):
+                raise InvalidArgument("kd_loss: steps/response length mismatch")
+            lp = _f64arr([x for st in s.steps for x in st.target_logprobs])
+        keep += [p, r, lp]
+        arr[i] = _KDSample(ctypes.cast(p, ctypes.POINTER(ctypes.c_int32)), len(s.prompt),
+                           ctypes.cast(r, ctypes.POINTER(ctypes.c_int32)), len(s.response),
+                           ctypes.cast(lp, ctypes.POINTER(ctypes.c_double)) if lp is not None else None,
+                           s.eos_bias, s.reward)
+    return arr, keep
+
+
+def kd_grad_transformer(drafter: "EagleDrafter", samples: Sequence[RolloutSample], weights: Sequence[float],
+                        grad=None, zero_grad: bool = True):
+    """Per-rank K5 for a transformer drafter: (sum_i w_i KL_i, fp32 [V, d] LM-head gradient as a
+    torch CUDA tensor). The gradient is what the prompt-sharded learner all-reduces."""
+    import torch
+    V, d = drafter.shape.vocab, drafter.shape.d_model
+    if grad is None:
+        grad = torch.zeros(V, d, dtype=torch.float32, device="cuda")
+    arr, keep = _kd_samples(samples, False)
+    loss = ctypes.c_double()
+    torch.cuda.synchronize()
+    _check(lib().rs_kd_grad_transformer(drafter.device.handle, drafter.target.handle, drafter.handle, arr,
+                                        len(samples), _f64arr(weights), ctypes.c_void_p(grad.data_ptr()),
+                                        1 if zero_grad else 0, ctypes.byref(loss)))
+    return loss.value, grad
+
+
+def kd_update(drafter, buffer: Sequence[RolloutSample], policy: KDPolicy, selection_rng: SelectionRng,
               sim_cost_per_token: float) -> KDUpdateResult:
-    """kd_update (learner.cpp:98-160): loss + analytic gradient + SGD step on the device."""
+    """kd_update (learner.cpp:98-160): loss + analytic gradient + SGD step on the device.
+    Tabular drafters follow the reference bit-for-bit; EAGLE drafters train their LM head with
+    p~ recomputed by the target (rs_kd_update_transformer)."""
+    if isinstance(drafter, EagleDrafter):
+        arr, keep = _kd_samples(buffer, False)
+        h = ctypes.c_void_p()
+        res = _KDResult()
+        _check(lib().rs_kd_update_transformer(drafter.device.handle, drafter.target.handle, drafter.handle, arr,
+                                              len(buffer), policy._c(), selection_rng.state, sim_cost_per_token,
+                                              ctypes.byref(h), ctypes.byref(res)))
+        return KDUpdateResult(EagleDrafter._wrap(h, drafter.target), bool(res.updated), res.loss, res.samples_used,
+                              res.weight_mean, res.weight_min, res.weight_max, res.sim_time)
     V = drafter.vocab_size
     keep = []
     arr = (_KDSample * max(1, len(buffer)))()

@@ -510,6 +510,102 @@ int rs_kd_update_tabular(rs_ctx *ctx, const rs_model *drafter, const rs_kd_sampl
     });
 }
 
+namespace {
+std::vector<rs::KdSeq> kd_seqs(const rs_kd_sample *buf, const std::vector<int> &idx, const std::vector<double> &w) {
+    std::vector<rs::KdSeq> seqs;
+    for (size_t i = 0; i < idx.size(); ++i) {
+        const rs_kd_sample &x = buf[idx[i]];
+        if (x.response_len <= 0) continue;  // nothing to distil (learner.cpp:40-53 sums over steps)
+        rs::KdSeq q;
+        q.tokens.assign(x.prompt, x.prompt + x.prompt_len);
+        q.tokens.insert(q.tokens.end(), x.response, x.response + x.response_len);
+        q.prompt_len = x.prompt_len;
+        q.eos_bias = x.eos_bias;
+        q.weight = w[i];
+        seqs.push_back(std::move(q));
+    }
+    return seqs;
+}
+const rs::TransformerModel *as_target(const rs_model *m) {
+    if (!m || m->kind != rs_model::Transformer) throw std::invalid_argument("kd: transformer target required");
+    return static_cast<const rs::TransformerModel *>(m);
+}
+const rs::DrafterModel *as_drafter(const rs_model *m) {
+    if (!m || m->kind != rs_model::Drafter) throw std::invalid_argument("kd: EAGLE drafter required");
+    return static_cast<const rs::DrafterModel *>(m);
+}
+}  // namespace
+
+int rs_kd_grad_transformer(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const rs_kd_sample *samples,
+                           int32_t n, const double *weights, float *grad_dev, int32_t zero_grad, double *loss_out) {
+    return guard([&] {
+        need(ctx, "rs_kd_grad_transformer");
+        need(grad_dev, "rs_kd_grad_transformer: grad");
+        if (n > 0) need(samples, "rs_kd_grad_transformer: samples");
+        std::vector<int> idx(std::max(n, 0));
+        std::vector<double> w(std::max(n, 0), 1.0);
+        for (int i = 0; i < n; ++i) {
+            idx[i] = i;
+            if (weights) w[i] = weights[i];
+        }
+        const double loss = rs::kd_grad_transformer(ctx, as_target(target), as_drafter(drafter),
+                                                    kd_seqs(samples, idx, w), grad_dev, zero_grad != 0);
+        if (loss_out) *loss_out = loss;
+    });
+}
+
+int rs_drafter_apply_grad(rs_ctx *ctx, const rs_model *drafter, const float *grad_dev, double scale, rs_model **out) {
+    return guard([&] {
+        need(ctx, "rs_drafter_apply_grad");
+        need(out, "rs_drafter_apply_grad: out");
+        *out = rs::drafter_apply_lm_grad(ctx, as_drafter(drafter), grad_dev, scale);
+    });
+}
+
+int rs_kd_update_transformer(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const rs_kd_sample *buf,
+                             int32_t n, rs_kd_policy policy, uint64_t *sel_state, double cost, rs_model **new_drafter,
+                             rs_kd_result *out) {
+    return guard([&] {
+        need(ctx, "rs_kd_update_transformer");
+        need(sel_state, "rs_kd_update_transformer: selection rng");
+        need(new_drafter, "rs_kd_update_transformer: out");
+        const auto *t = as_target(target);
+        const auto *d = as_drafter(drafter);
+        if (policy.mode == 2) throw std::logic_error("kd_update: frozen drafter takes no updates");
+        if (policy.interval < 1) throw std::invalid_argument("kd_update: interval must be >= 1");
+        rs_kd_result res{};
+        if (n <= 0) {  // empty buffer: no-op (learner.cpp:103-105) -- an unchanged snapshot
+            *new_drafter = rs::drafter_apply_lm_grad(ctx, d, nullptr, 0.0);
+            static_cast<rs::DrafterModel *>(*new_drafter)->version = d->version;
+            if (out) *out = res;
+            return;
+        }
+        const std::vector<int> idx = rs::kd_select(n, policy.interval, sel_state);
+        std::vector<double> br(idx.size()), w(idx.size());
+        for (size_t i = 0; i < idx.size(); ++i) br[i] = buf[idx[i]].reward;
+        double wsum = 0, wmin = 0, wmax = 0;
+        size_t distilled = 0;
+        for (size_t i = 0; i < idx.size(); ++i) {
+            w[i] = rs::kd_weight(buf[idx[i]].reward, br, policy);
+            wsum += w[i];
+            wmin = i == 0 ? w[i] : std::min(wmin, w[i]);
+            wmax = i == 0 ? w[i] : std::max(wmax, w[i]);
+            distilled += static_cast<size_t>(std::max(0, buf[idx[i]].response_len));
+        }
+        rs::DBuf<float> grad((size_t)t->s.V * t->s.d);
+        const double loss = rs::kd_grad_transformer(ctx, t, d, kd_seqs(buf, idx, w), grad.p, true);
+        *new_drafter = rs::drafter_apply_lm_grad(ctx, d, grad.p, -policy.lr);
+        res.updated = 1;
+        res.samples_used = static_cast<int>(idx.size());
+        res.loss = loss;
+        res.weight_mean = wsum / static_cast<double>(idx.size());
+        res.weight_min = wmin;
+        res.weight_max = wmax;
+        res.sim_time = cost * static_cast<double>(distilled);
+        if (out) *out = res;
+    });
+}
+
 int rs_model_tensor(const rs_model *m, const char *name, int32_t layer, void **ptr, int64_t *bytes) {
     return guard([&] {
         need(m, "rs_model_tensor");

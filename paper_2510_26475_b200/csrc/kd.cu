@@ -7,8 +7,11 @@
 
 #include "common.cuh"
 #include "kd.h"
+#include "prof.h"
 
 namespace rs {
+
+using bf16 = __nv_bfloat16;
 
 double kd_weight(double r, const std::vector<double> &br, const rs_kd_policy &p) {
     switch (p.mode) {
@@ -130,7 +133,148 @@ __global__ void __launch_bounds__(1024, 1) kd_rows_kernel(const float *trow, con
     if (threadIdx.x == 0) loss[i] = wi * kl;
 }
 
+// ---- K5 at full-chip parallelism (transformer KD) ------------------------------------------
+// Row log-normaliser log sum_x exp(z'/tau) of fp32 logit rows from their 256-column tile
+// partials (rowstats.cu; EOS column excluded) plus the EOS column with the row's bias.
+__global__ void kd_lse_kernel(const float *rows, const double *st, int nrows, int V, double tau, const double *bias,
+                              double *lse) {
+    const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (r >= nrows) return;
+    const int nt = (V + 255) / 256;
+    const double *s = st + (size_t)r * nt * 2;
+    const double ve = ((double)rows[(size_t)r * V + V - 1] + bias[r]) / tau;
+    double m = ve;
+    for (int t = lane; t < nt; t += 32) m = fmax(m, s[2 * t]);
+    m = warp_max(m);
+    double S = 0.0;
+    for (int t = lane; t < nt; t += 32)
+        if (s[2 * t + 1] > 0.0) S += s[2 * t + 1] * exp(s[2 * t] - m);
+    S = warp_sum(S) + exp(ve - m);
+    if (lane == 0) lse[r] = m + log(S);
+}
+
+// Per element of a 64-row x 256-column tile: p~ = softmax(target / tau_p), q = softmax(drafter /
+// tau_q) (EOS bias on both, model.cpp:137-138), KL term p~ (log p~ - log q) (p~ > 0 only,
+// learner.cpp:44-50) and dZ = w (q - p~) / tau_q (learner.cpp:75) times the LM-head output
+// scale -- written TRANSPOSED ([V][ldt] bf16) so it is the K-major A operand of the
+// dW = dZ^T . h GEMM. One warp per row, lane l on columns l + 32 j; KL partials per (row, tile).
+__global__ void __launch_bounds__(256) kd_elem_kernel(const float *P, const float *Q, const double *lseP,
+                                                      const double *lseQ, const double *w, const double *bias, int R,
+                                                      int V, double tau_p, double tau_q, float zscale, bf16 *dzT,
+                                                      int ldt, double *kl_part) {
+    __shared__ __align__(16) bf16 tile[64][256 + 8];
+    const int t = blockIdx.x, r0 = blockIdx.y * 64;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nt = gridDim.x;
+    for (int rr = warp; rr < 64; rr += 8) {
+        const int r = r0 + rr;
+        double kl = 0.0;
+        if (r < R) {
+            const float *zp = P + (size_t)r * V, *zq = Q + (size_t)r * V;
+            const double b = bias[r], lp0 = lseP[r], lq0 = lseQ[r], wr = w[r];
+#pragma unroll 4
+            for (int j = 0; j < 8; ++j) {
+                const int c = lane + 32 * j, x = t * 256 + c;
+                float dz = 0.f;
+                if (x < V) {
+                    double vp = zp[x], vq = zq[x];
+                    if (x == V - 1) {
+                        vp += b;
+                        vq += b;
+                    }
+                    const double lp = vp / tau_p - lp0, lq = vq / tau_q - lq0;
+                    const double p = exp(lp), q = exp(lq);
+                    if (p > 0.0) kl += p * (lp - lq);
+                    dz = (float)(wr * (q - p) / tau_q) * zscale;
+                }
+                tile[rr][c] = __float2bfloat16(dz);
+            }
+        } else {
+            for (int j = 0; j < 8; ++j) tile[rr][lane + 32 * j] = __float2bfloat16(0.f);
+        }
+        kl = warp_sum(kl);
+        if (lane == 0 && r < R) kl_part[(size_t)r * nt + t] = kl;
+    }
+    __syncthreads();
+    // transposed store: column c of the tile -> dzT[x][r0 .. r0 + 63] (128 contiguous bytes)
+    const int c = threadIdx.x, x = t * 256 + c;
+    if (x < V && r0 + 64 <= ldt) {
+        bf16 *dst = dzT + (size_t)x * ldt + r0;
+#pragma unroll
+        for (int k = 0; k < 64; k += 8) {
+            __align__(16) bf16 v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = tile[k + i][c];
+            *reinterpret_cast<int4 *>(dst + k) = *reinterpret_cast<const int4 *>(v);
+        }
+    }
+}
+
+// loss_r = w_r * sum_t kl_part[r][t] (fixed order: lane-strided partials, warp butterfly)
+__global__ void kd_rowloss_kernel(const double *kl_part, int R, int nt, const double *w, double *loss) {
+    const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (r >= R) return;
+    double s = 0.0;
+    for (int t = lane; t < nt; t += 32) s += kl_part[(size_t)r * nt + t];
+    s = warp_sum(s);
+    if (lane == 0) loss[r] = w[r] * s;
+}
+
+// out[c][r] = in[r][c] for r < R, 0 for R <= r < ldo (bf16, 32 x 32 tiles)
+__global__ void transpose_pad_kernel(const bf16 *in, int ldi, int R, int C, bf16 *out, int ldo) {
+    __shared__ bf16 t[32][33];
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (int k = ty; k < 32; k += 8) {
+        const int r = r0 + k, c = c0 + tx;
+        t[k][tx] = (r < R && c < C) ? in[(size_t)r * ldi + c] : __float2bfloat16(0.f);
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+        const int c = c0 + k, r = r0 + tx;
+        if (c < C && r < ldo) out[(size_t)c * ldo + r] = t[tx][k];
+    }
+}
+
+// w_new = bf16(w + scale * g)
+__global__ void sgd_bf16_kernel(const bf16 *w, const float *g, float scale, size_t n, bf16 *out) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = __float2bfloat16(__bfloat162float(w[i]) + scale * g[i]);
+}
+
 }  // namespace
+
+void kd_rows_lse(const float *rows, const double *stats, int nrows, int V, double tau, const double *bias, double *lse,
+                 cudaStream_t st) {
+    if (nrows <= 0) return;
+    kd_lse_kernel<<<(nrows + 7) / 8, 256, 0, st>>>(rows, stats, nrows, V, tau, bias, lse);
+    RS_LAUNCHED();
+}
+
+void kd_rows_elem(const float *P, const float *Q, const double *lseP, const double *lseQ, const double *w,
+                  const double *bias, int R, int V, double tau_p, double tau_q, float zscale, bf16 *dzT, int ldt,
+                  double *kl_part, double *loss, cudaStream_t st) {
+    if (R <= 0) return;
+    const int nt = (V + 255) / 256;
+    ProfScope prof("kd", 0, (double)R * V * (4.0 + 4.0 + 2.0), st);
+    kd_elem_kernel<<<dim3(nt, (R + 63) / 64), 256, 0, st>>>(P, Q, lseP, lseQ, w, bias, R, V, tau_p, tau_q, zscale,
+                                                              dzT, ldt, kl_part);
+    RS_LAUNCHED();
+    kd_rowloss_kernel<<<(R + 7) / 8, 256, 0, st>>>(kl_part, R, nt, w, loss);
+    RS_LAUNCHED();
+}
+
+void transpose_pad_bf16(const bf16 *in, int ldi, int R, int C, bf16 *out, int ldo, cudaStream_t st) {
+    if (C <= 0 || ldo <= 0) return;
+    transpose_pad_kernel<<<dim3((C + 31) / 32, (ldo + 31) / 32), 256, 0, st>>>(in, ldi, R, C, out, ldo);
+    RS_LAUNCHED();
+}
+
+void sgd_bf16(const bf16 *w, const float *g, float scale, size_t n, bf16 *out, cudaStream_t st) {
+    if (!n) return;
+    sgd_bf16_kernel<<<1184, 256, 0, st>>>(w, g, scale, n, out);
+    RS_LAUNCHED();
+}
 
 void kd_rows_loss_grad(const float *target_rows, const float *drafter_rows, const double *weights,
                        const double *eos_bias, int rows, int V, double tau_p, double tau_q, double *loss_out,

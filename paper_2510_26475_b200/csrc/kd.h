@@ -2,6 +2,8 @@
 #pragma once
 #include <vector>
 
+#include <cuda_bf16.h>
+
 #include "engine.h"
 
 namespace rs {
@@ -27,5 +29,16 @@ double kd_core(rs_ctx *ctx, const TabularModel *drafter, const std::vector<const
 void kd_rows_loss_grad(const float *target_rows, const float *drafter_rows, const double *weights,
                        const double *eos_bias, int rows, int V, double tau_p, double tau_q, double *loss_out,
                        float *dz_out, cudaStream_t st);
+
+// K5 at full-chip parallelism (transformer drafters): per-row log-normalisers from the rows'
+// 256-column tile partials, then one pass over 64 x 256 tiles producing the weighted KL per row
+// (loss[r] = w_r KL_r) and dZ^T = (w (q - p~) / tau_q * zscale)^T as bf16 [V][ldt].
+void kd_rows_lse(const float *rows, const double *stats, int nrows, int V, double tau, const double *bias, double *lse,
+                 cudaStream_t st);
+void kd_rows_elem(const float *P, const float *Q, const double *lseP, const double *lseQ, const double *w,
+                  const double *bias, int R, int V, double tau_p, double tau_q, float zscale, __nv_bfloat16 *dzT, int ldt,
+                  double *kl_part, double *loss, cudaStream_t st);
+void transpose_pad_bf16(const __nv_bfloat16 *in, int ldi, int R, int C, __nv_bfloat16 *out, int ldo, cudaStream_t st);
+void sgd_bf16(const __nv_bfloat16 *w, const float *g, float scale, size_t n, __nv_bfloat16 *out, cudaStream_t st);
 
 }  // namespace rs

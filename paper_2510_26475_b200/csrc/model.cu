@@ -373,7 +373,8 @@ void init_transformer(TransformerModel &m, uint64_t seed, cudaStream_t st) {
     m.n_params = (size_t)s.V * s.d + (size_t)s.L * (q * s.d + q + (size_t)s.d * s.H * s.hd + 3 * (size_t)s.dff * s.d);
 }
 
-void init_drafter(DrafterModel &m, uint64_t seed, cudaStream_t st) {
+// Allocate a drafter's weight arena and carve its tensors (no initialisation).
+void carve_drafter(DrafterModel &m) {
     const TfShape &s = m.s;
     size_t bytes = (size_t)s.d * 3 * s.d * 2 + 2 * (size_t)s.d * 4 + layer_bytes(s, 2 * s.d) + (size_t)s.d * 4 +
                    (size_t)s.V * s.d * 2 + 4096;
@@ -385,15 +386,20 @@ void init_drafter(DrafterModel &m, uint64_t seed, cudaStream_t st) {
     carve_layer(c, m.layer, s, 2 * s.d);
     m.final_norm = c.take<float>(s.d);
     m.lm_w = c.take<bf16>((size_t)s.V * s.d);
+    const size_t q = s.qkv_dim();
+    m.n_params = (size_t)s.d * 3 * s.d + q * 2 * s.d + q + (size_t)s.d * s.H * s.hd + 3 * (size_t)s.dff * s.d +
+                 (size_t)s.V * s.d;
+}
+
+void init_drafter(DrafterModel &m, uint64_t seed, cudaStream_t st) {
+    const TfShape &s = m.s;
+    carve_drafter(m);
     k_init_normal(m.fc_w, (size_t)s.d * 3 * s.d, seed, 1001, s.std, st);
     k_fill_f32(m.norm_emb, s.d, 1.0f, st);
     k_fill_f32(m.norm_hid, s.d, 1.0f, st);
     init_layer(m.layer, s, 2 * s.d, seed, 1010, st);
     k_fill_f32(m.final_norm, s.d, 1.0f, st);
     k_init_normal(m.lm_w, (size_t)s.V * s.d, seed, 1020, s.std, st);
-    const size_t q = s.qkv_dim();
-    m.n_params = (size_t)s.d * 3 * s.d + q * 2 * s.d + q + (size_t)s.d * s.H * s.hd + 3 * (size_t)s.dff * s.d +
-                 (size_t)s.V * s.d;
 }
 
 }  // namespace rs

@@ -61,6 +61,21 @@ void init_transformer(TransformerModel &m, uint64_t seed, cudaStream_t st);
 TransformerModel *create_transformer(rs_ctx *ctx, const rs_transformer_shape &sh, uint64_t seed);
 DrafterModel *create_drafter(rs_ctx *ctx, const rs_model *target, uint64_t seed, int version);
 void init_drafter(DrafterModel &m, uint64_t seed, cudaStream_t st);
+void carve_drafter(DrafterModel &m);
+
+// Transformer KD (K5 + the drafter LM-head gradient), tf_pair.cpp. One training sequence =
+// prompt + response of a RolloutSample; every response position t contributes
+// w * KL(p~_t || q_t) with p~ the target and q the drafter at context prompt + response[:t].
+struct KdSeq {
+    std::vector<int> tokens;
+    int prompt_len = 0;
+    double eos_bias = 0.0, weight = 1.0;
+};
+// Accumulates dL/dW_lm (fp32 [V][d]) into grad (zeroed first if zero_grad); returns the loss.
+double kd_grad_transformer(rs_ctx *ctx, const TransformerModel *tgt, const DrafterModel *drf,
+                           const std::vector<KdSeq> &seqs, float *grad, bool zero_grad);
+// New drafter snapshot (version + 1): lm_w + scale * grad, every other tensor copied.
+DrafterModel *drafter_apply_lm_grad(rs_ctx *ctx, const DrafterModel *drf, const float *grad, double scale);
 
 // One query/update row of a forward pass.
 struct RowDesc {

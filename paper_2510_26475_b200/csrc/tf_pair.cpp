@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "gemm.h"
+#include "kd.h"
 #include "model.h"
 #include "prof.h"
 
@@ -298,7 +299,7 @@ struct TransformerPair : ModelPair {
         per_item = attn_max_tokens(s.H / s.KV);
         tc_attn = tuning().attn_tc >= 0;
         per_item_t = tc_attn ? attn_tc_max_tokens(s.H / s.KV) : per_item;
-        if ((eng->n_max + 1) * (s.H / s.KV) > 16 * attn_max_warps())
+        if (eng && (eng->n_max + 1) * (s.H / s.KV) > 16 * attn_max_warps())
             throw std::invalid_argument("transformer engine: (draft_len + 1) * GQA group must be <= 192");
         for (int i = 0; i < n_req; ++i)
             if (plen[i] < 1) throw std::invalid_argument("transformer engine: prompts must be non-empty");
@@ -514,6 +515,100 @@ struct TransformerPair : ModelPair {
         k_compact(d, d.rsel, d.racc, rbase.p, kv_t, feat.p, 3 * s.d, max_ctx, st);
     }
 
+    // ---- transformer KD (K5 + LM-head gradient) over teacher-forced training sequences -------
+    // Rows = every position 0..len-2 of every sequence, in position order per sequence, packed
+    // into forwards of <= Mcap rows. Per forward: target stack (KV + EAGLE features; logits only
+    // for the KD rows = positions >= prompt_len - 1), drafter fc + layer over the same rows
+    // (features of position p-1, the drafter's own KV), drafter LM head on the KD rows, K5
+    // (loss, dZ^T), and dW_lm += dZ^T . h_norm on the tensor cores (fp32 accumulate).
+    double kd_pass(const SdDev &d, const std::vector<KdSeq> &seqs, float *grad) {
+        cudaStream_t st = ctx->stream;
+        const int V = s.V, Mcap = w.Mcap;
+        const int ldt = (Mcap + 63) / 64 * 64;
+        const int nt = (V + 255) / 256;
+        DBuf<float> Pb((size_t)Mcap * V), Qb((size_t)Mcap * V);
+        DBuf<double> stP((size_t)Mcap * nt * 2), stQ((size_t)Mcap * nt * 2), lseP(Mcap), lseQ(Mcap), kl((size_t)Mcap * nt),
+            lossr(Mcap), wr(Mcap), br(Mcap);
+        DBuf<bf16> dzT((size_t)V * ldt), hT((size_t)s.d * ldt);
+        std::vector<double> lh(Mcap);
+        double loss = 0.0;
+        size_t r = 0;
+        int p = 0;
+        while (r < seqs.size()) {
+            bt.clear();
+            std::vector<int32_t> kd_src;
+            std::vector<double> kd_w, kd_b;
+            std::vector<std::pair<int, int>> segs;  // (first row, end row) per sequence run
+            while (r < seqs.size() && bt.M() < Mcap) {
+                const int len = (int)seqs[r].tokens.size();
+                if (p >= len - 1) {
+                    ++r;
+                    p = 0;
+                    continue;
+                }
+                const int take = std::min(len - 1 - p, Mcap - bt.M());
+                const int r0 = bt.M();
+                for (int k = 0; k < take; ++k, ++p) {
+                    const bool kd = p >= seqs[r].prompt_len - 1;
+                    bt.map_a.push_back(kd ? (int32_t)kd_src.size() : -1);
+                    if (kd) {
+                        kd_src.push_back(bt.M());
+                        kd_w.push_back(seqs[r].weight);
+                        kd_b.push_back(seqs[r].eos_bias);
+                    }
+                    bt.rows.push_back(RowDesc{(int)r, p, p, 0, -1, 0, 0, 0});
+                }
+                segs.emplace_back(r0, bt.M());
+            }
+            if (bt.M() == 0) break;
+            const int M = bt.M(), R = (int)kd_src.size();
+            // target: tensor-core attention items
+            for (const auto &sg : segs) bt.add_items(sg.first, sg.second, per_item_t, -1, 0, 0, 0);
+            upload(bt, st, tc_attn);
+            target_forward(d, M, (int)bt.items.size(), Pb.p, true, st);
+            // drafter: legacy attention items over the same rows
+            bt.items.clear();
+            for (const auto &sg : segs) bt.add_items(sg.first, sg.second, per_item, -1, 0, 0, 0);
+            std::vector<int32_t> dst(R);
+            for (int k = 0; k < R; ++k) dst[k] = k;
+            bt.map_a = kd_src;
+            bt.map_b = dst;
+            upload(bt, st);
+            k_gather_features(w.rows.p, M, s.d, feat.p, max_ctx, nullptr, w.fin.p, nullptr, st);
+            gemm(w.fin.p, 3 * s.d, drf->fc_w, M, s.d, 3 * s.d, epi_f32(w.x.p, s.d, 1.0f, nullptr), st);
+            drafter_layer(d, M, (int)bt.items.size(), st);
+            if (R == 0) continue;
+            drafter_head(w.map_a.p, w.map_b.p, R, Qb.p, nullptr, st);  // h_norm of the KD rows stays in w.xn
+            stage.upload(wr.p, kd_w, st);
+            stage.upload(br.p, kd_b, st);
+            row_stats(Pb.p, nullptr, R, V, tgt->temperature, stP.p, st);
+            row_stats(Qb.p, nullptr, R, V, drf->temperature, stQ.p, st);
+            kd_rows_lse(Pb.p, stP.p, R, V, tgt->temperature, br.p, lseP.p, st);
+            kd_rows_lse(Qb.p, stQ.p, R, V, drf->temperature, br.p, lseQ.p, st);
+            const int Rp = (R + 63) / 64 * 64;
+            kd_rows_elem(Pb.p, Qb.p, lseP.p, lseQ.p, wr.p, br.p, R, V, tgt->temperature, drf->temperature,
+                         s.logit_scale, dzT.p, Rp, kl.p, lossr.p, st);
+            transpose_pad_bf16(w.xn.p, s.d, R, s.d, hT.p, Rp, st);
+            GemmArgs g;  // dW[V][d] += dZ^T[V][Rp] . (h^T[d][Rp])^T
+            g.A = dzT.p;
+            g.B = hT.p;
+            g.M = V;
+            g.N = s.d;
+            g.K = Rp;
+            g.lda = Rp;
+            g.ldb = Rp;
+            g.epi.kind = kEpiResidual;
+            g.epi.out = grad;
+            g.epi.ldo = s.d;
+            gemm_bf16(g, st);
+            RS_CUDA(cudaMemcpyAsync(lh.data(), lossr.p, (size_t)R * 8, cudaMemcpyDeviceToHost, st));
+            RS_CUDA(cudaStreamSynchronize(st));
+            for (int k = 0; k < R; ++k) loss += lh[k];
+            stage.off = 0;
+        }
+        return loss;
+    }
+
     // Target prefill of prompt positions 0..P-2 (the last prompt token is the first root).
     void prefill(const std::vector<std::vector<int>> &prompts, const SdDev &d) {
         cudaStream_t st = ctx->stream;
@@ -558,6 +653,56 @@ std::unique_ptr<ModelPair> make_transformer_pair(rs_ctx *ctx, rs_engine *eng, co
     p->setup(n_req, slots_max, prompt_lens, tok_cap, eng->t_max);
     p->prefill(prompts, eng->dev(rs_sdconfig{1, 1, 1, 0}, 0));
     return p;
+}
+
+double kd_grad_transformer(rs_ctx *ctx, const TransformerModel *tgt, const DrafterModel *drf,
+                           const std::vector<KdSeq> &seqs, float *grad, bool zero_grad) {
+    if (!tgt || !drf || drf->target != tgt) throw std::invalid_argument("kd: drafter is bound to a different target");
+    cudaStream_t st = ctx->stream;
+    if (zero_grad) RS_CUDA(cudaMemsetAsync(grad, 0, (size_t)tgt->s.V * tgt->s.d * sizeof(float), st));
+    if (seqs.empty()) return 0.0;
+    int tok_cap = 1;
+    std::vector<int> plen;
+    for (const auto &q : seqs) {
+        if (q.prompt_len < 1 || (int)q.tokens.size() < q.prompt_len)
+            throw std::invalid_argument("kd: prompts must be non-empty");
+        tok_cap = std::max(tok_cap, (int)q.tokens.size());
+        plen.push_back(q.prompt_len);
+    }
+    if (tok_cap + 1 > tgt->s.max_ctx) throw std::invalid_argument("kd: sequence exceeds the model's max_ctx");
+    const int n = (int)seqs.size();
+    std::vector<int32_t> htok((size_t)n * tok_cap, 0);
+    for (int i = 0; i < n; ++i) std::copy(seqs[i].tokens.begin(), seqs[i].tokens.end(), htok.begin() + (size_t)i * tok_cap);
+    DBuf<int32_t> tok(htok.size());
+    RS_CUDA(cudaMemcpyAsync(tok.p, htok.data(), htok.size() * 4, cudaMemcpyHostToDevice, st));
+    note_copy(true, htok.size() * 4);
+    TransformerPair p(ctx, nullptr, tgt, drf);
+    p.setup(n, 1, plen, tok_cap, 1);
+    SdDev d{};
+    d.tok = tok.p;
+    d.tok_cap = tok_cap;
+    d.t_max = 1;
+    d.n_max = 1;
+    const double loss = p.kd_pass(d, seqs, grad);
+    RS_CUDA(cudaStreamSynchronize(st));
+    return loss;
+}
+
+DrafterModel *drafter_apply_lm_grad(rs_ctx *ctx, const DrafterModel *drf, const float *grad, double scale) {
+    auto m = std::make_unique<DrafterModel>();
+    m->ctx = ctx;
+    m->vocab = drf->vocab;
+    m->temperature = drf->temperature;
+    m->version = drf->version + 1;
+    m->target = drf->target;
+    m->s = drf->s;
+    carve_drafter(*m);
+    if (m->arena.n != drf->arena.n) throw std::logic_error("drafter arena layout mismatch");
+    cudaStream_t st = ctx->stream;
+    RS_CUDA(cudaMemcpyAsync(m->arena.p, drf->arena.p, m->arena.n, cudaMemcpyDeviceToDevice, st));
+    if (grad && scale != 0.0) sgd_bf16(drf->lm_w, grad, (float)scale, (size_t)m->s.V * m->s.d, m->lm_w, st);
+    RS_CUDA(cudaStreamSynchronize(st));
+    return m.release();
 }
 
 TransformerModel *create_transformer(rs_ctx *ctx, const rs_transformer_shape &sh, uint64_t seed) {

@@ -16,7 +16,7 @@ from dataclasses import dataclass
 from typing import Callable, List, Optional, Sequence, Tuple
 
 from . import (KDPolicy, RolloutSample, SelectionRng, TabularARModel, _KDSample, _check, _f64arr, _i32arr,
-               kd_weight, lib)
+               kd_grad_transformer, kd_weight, lib)
 
 
 def shard_requests(requests: Sequence, rank: int, world: int, group_size: int = 1) -> List:
@@ -119,3 +119,45 @@ def torch_all_reduce(group=None, device: str = "cpu") -> Callable[[List[float]],
         return t.cpu().tolist()
 
     return fn
+
+
+@dataclass
+class TransformerKDStep:
+    drafter: object          # the new EagleDrafter snapshot (version + 1), identical on every rank
+    loss: float              # sum over ALL ranks' selected samples of w_i KL_i
+    selected: List[int]
+    weights: List[float]
+    samples_used: int
+    sim_time: float
+
+
+def kd_step_distributed_transformer(drafter, global_rewards: Sequence[float], global_lengths: Sequence[int],
+                                    local_samples: Sequence[RolloutSample], local_global_idx: Sequence[int],
+                                    policy: KDPolicy, selection_rng: SelectionRng, sim_cost_per_token: float,
+                                    group=None, reduce: bool = True) -> TransformerKDStep:
+    """Prompt-sharded kd_update for an EAGLE drafter: replicated selection + reward weights over
+    GLOBAL buffer indices (learner.cpp:107-140), this rank's K5 + LM-head gradient on its GPU,
+    ONE all-reduce of the fp32 [V, d] gradient (and the loss) with torch.distributed -- NCCL over
+    NVLink on a B200 box, the only collective of the whole rollout path -- then the same SGD
+    step (-lr) on every rank, so every rank publishes the same snapshot."""
+    import torch
+    if policy.mode == 2:
+        from . import LogicError
+        raise LogicError("kd_update: frozen drafter takes no updates")
+    sel = kd_select(len(global_rewards), policy.interval, selection_rng)
+    batch_rewards = [global_rewards[i] for i in sel]
+    weights = {i: kd_weight(global_rewards[i], batch_rewards, policy) for i in sel}
+    order = {g: k for k, g in enumerate(sel)}
+    mine = sorted([(order[g], s, weights[g]) for s, g in zip(local_samples, local_global_idx) if g in weights],
+                  key=lambda t: t[0])
+    loss, grad = kd_grad_transformer(drafter, [s for _, s, _ in mine], [w for _, _, w in mine])
+    if reduce:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
+            lt = torch.tensor([loss], dtype=torch.float64, device=grad.device)
+            dist.all_reduce(lt, op=dist.ReduceOp.SUM, group=group)
+            loss = float(lt.item())
+    new = drafter.apply_grad(grad, -policy.lr)
+    tokens = sum(global_lengths[i] for i in sel)
+    return TransformerKDStep(new, loss, sel, [weights[i] for i in sel], len(sel), sim_cost_per_token * tokens)
