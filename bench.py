@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--no-profile", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--kd", type=int, default=4, help="rollouts per GPU in the online KD update leg (0 = off)")
     return p.parse_args()
 
 
@@ -195,6 +196,53 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def kd_leg(args, rb, eng, drafter, rank, world, barrier):
+    """cfg5 leg: one online KD update of the drafter on this step's rollouts (prompt + generated
+    tokens of the first --kd requests per GPU), reward-weighted (synthetic rewards), the fp32
+    LM-head gradient all-reduced over the ranks (NCCL), the same SGD snapshot on every rank.
+    Device time of the whole update (teacher-forced target + drafter forwards, K5, gradient
+    GEMM, all-reduce, SGD), max over ranks."""
+    import random
+    import torch
+    from paper_2510_26475_b200.distributed import kd_step_distributed_transformer
+    reqs = eng.requests()[: args.kd]
+    rng = random.Random(77)
+    rewards = [rng.random() for _ in range(args.kd * world)]  # same global list on every rank
+    lengths = [0] * (args.kd * world)
+    local, gidx = [], []
+    for i, r in enumerate(reqs):
+        g = rank * args.kd + i
+        local.append(rb.RolloutSample(list(r.prompt), list(r.generated), [], eos_bias=r.eos_bias, reward=rewards[g]))
+        gidx.append(g)
+        lengths[g] = len(r.generated)
+    if world > 1:
+        import torch.distributed as dist
+        lt = torch.tensor(lengths, dtype=torch.int64, device="cuda")
+        dist.all_reduce(lt)
+        lengths = lt.tolist()
+    pol = rb.KDPolicy(interval=1, mode=0, clip_lo=0.0, clip_hi=4.0, lr=0.5)  # config.hpp:38
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    step = kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    toks = sum(lengths)
+    shape = drafter.shape
+    return {"rollouts": args.kd * world, "tokens_distilled": toks, "ms": round(ms, 2),
+            "distilled_tokens_per_s": round(toks / (ms / 1000.0), 1), "loss": step.loss,
+            "new_drafter_version": step.drafter.version, "trained": "drafter LM head (fp32 grad [V, d])",
+            "allreduce_bytes": shape.vocab * shape.d_model * 4 if world > 1 else 0,
+            "context_tokens_per_rollout": args.ctx}
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -290,6 +338,8 @@ def main():
             eng.step()
         prof = rb.profile(enable=False)
 
+    kd = kd_leg(args, rb, eng, drafter, rank, world, barrier) if args.kd > 0 else None
+
     if world > 1:
         import torch.distributed as dist
         vals = torch.tensor([ms, e2e_s], dtype=torch.float64, device="cuda")
@@ -348,7 +398,7 @@ def main():
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_tok / e2e_s, 1), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps)},
-            "gpu_launches": launches, "clocks": clk, "breakdown_ms_per_step": breakdown}
+            "gpu_launches": launches, "clocks": clk, "breakdown_ms_per_step": breakdown, "kd_update": kd}
     print(json.dumps(line), flush=True)
 
 
