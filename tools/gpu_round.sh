@@ -16,4 +16,6 @@ timeout 600 ncu --set full --clock-control none --import-source on --nvtx --nvtx
   -o $O/lmhead_full python tools/profile_step.py 2 > $O/lmhead_full.log 2>&1; echo "ncu lmhead rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "accept/" -k regex:"accept|compact" -s 0 -c 4 \
   -o $O/accept_full python tools/profile_step.py 2 > $O/accept_full.log 2>&1; echo "ncu accept rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "verify/" -k regex:attn_tc -s 2 -c 1 \
+  -o $O/attn_full python tools/profile_step.py 2 > $O/attn_full.log 2>&1; echo "ncu attn rc=$?"
 ls -la $O
