@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "model.h"
+#include "launch.cuh"
 #include "prof.h"
 
 namespace rs {
@@ -76,6 +77,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) attn_kernel(const bf16 *q, 
     Plan &pl = *reinterpret_cast<Plan *>(sm + kQBytes + 4 * kTileBytes);
     __shared__ int rowpos[kMaxWarps * 16];
 
+    pdl_trigger();
+    pdl_wait();
     const AttnItem it = items[blockIdx.x];
     const int kvh = blockIdx.y;
     const int G = H / KV;
@@ -310,8 +313,8 @@ void k_attention(const bf16 *q, const RowDesc *rows, const AttnItem *items, int 
         attr = true;
     }
     const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(s.hd));
-    attn_kernel<<<dim3(n_items, s.KV), kMaxWarps * 32, kSmem, st>>>(q, rows, items, kv, layer, s.H, s.KV, scale_log2,
-                                                                   out);
+    launch_pdl(attn_kernel, dim3(n_items, s.KV), kMaxWarps * 32, kSmem, st, q, rows, items, kv, layer, s.H, s.KV,
+               scale_log2, out);
     RS_LAUNCHED();
 }
 

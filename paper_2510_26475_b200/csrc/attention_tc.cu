@@ -32,6 +32,7 @@
 #include "gemm.h"
 #include "model.h"
 #include "prof.h"
+#include "launch.cuh"
 #include "tc.cuh"
 
 namespace rs {
@@ -103,7 +104,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_done + 1);
     Plan &pl = *reinterpret_cast<Plan *>(reinterpret_cast<uint8_t *>(bars) + kBarBytes);
 
-    const AttnItem it = items[blockIdx.x];
+    pdl_trigger();
+    const AttnItem it = items[blockIdx.x];  // host-uploaded plan: independent of the previous kernel
     const int kvh = blockIdx.y;
     const int G = H / KV;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -148,6 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
     }
+    pdl_wait();  // Q and the K/V cache come from the previous kernel (RoPE / KV store)
     // ---- Q tiles -> smem (softmax warps: half a row each, zero rows beyond the item) ----------
     if (warp >= 4) {
         const int T0 = 128 / G;
@@ -438,9 +441,8 @@ void k_attention_tc(const bf16 *q, const RowDesc *rows, const AttnItem *items, c
     const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(s.hd));
     static long long *trace = nullptr;
     if (tuning().attn_trace && !trace) RS_CUDA(cudaMalloc(&trace, 8 * (1 + 4 * kMaxPasses)));
-    attn_tc_kernel<<<dim3(n_items, s.KV), kThreads, kSmem, st>>>(tk, tv, q, rows, items, plan, kv, layer, s.H,
-                                                                 s.KV, scale_log2, out,
-                                                                 tuning().attn_trace ? trace : nullptr);
+    launch_pdl(attn_tc_kernel, dim3(n_items, s.KV), kThreads, kSmem, st, tk, tv, q, rows, items, plan, kv, layer,
+               s.H, s.KV, scale_log2, out, tuning().attn_trace ? trace : nullptr);
     if (tuning().attn_trace) {
         RS_CUDA(cudaStreamSynchronize(st));
         static long long host[1 + 4 * kMaxPasses];

@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "gemm.h"
+#include "launch.cuh"
 #include "tc.cuh"
 #include "prof.h"
 
@@ -204,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
+    pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
     const int num_tiles = num_m * num_n;
@@ -240,6 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();  // operands / residual of the previous kernel
 
     if (warp == 0) {
         if (lane == 0) {
@@ -415,7 +418,7 @@ void launch(const GemmArgs &g, cudaStream_t st) {
         sem = sems;
     }
     const int grid = std::min(tiles * splits, num_sms());
-    gemm_kernel<BN, EPI><<<grid, kThreads, C::kSmem, st>>>(ta, tb, g.epi, g.M, g.N, g.K, splits, sem);
+    launch_pdl(gemm_kernel<BN, EPI>, grid, kThreads, C::kSmem, st, ta, tb, g.epi, g.M, g.N, g.K, splits, sem);
     RS_LAUNCHED();
 }
 

@@ -5,6 +5,7 @@
 
 #include "common.cuh"
 #include "model.h"
+#include "launch.cuh"
 #include "prof.h"
 #include "rng.cuh"
 
@@ -41,6 +42,8 @@ __global__ void rope_table_kernel(float *rope, int max_ctx, int hd, float theta)
 
 __global__ void embed_kernel(const RowDesc *rows, int M, const int32_t *tok, int tok_cap, const int32_t *chain_tok,
                              int t_max, int n_max, const bf16 *emb, int V, int d, float *x) {
+    pdl_trigger();
+    pdl_wait();
     const int m = blockIdx.x;
     if (m >= M) return;
     const RowDesc r = rows[m];
@@ -87,6 +90,8 @@ __device__ __forceinline__ void store8(bf16 *p, const float (&v)[8]) {
 template <class T>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const T *x, int ldx, const float *w, int M, int d, float eps,
                                                       bf16 *out, int ldo) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ float red[32];
     const int row = blockIdx.x;
     const T *xr = x + (size_t)row * ldx;
@@ -129,6 +134,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const T *x, int ldx, const
 // One CTA per row; a thread rotates 8 dimension pairs (i, i + hd/2) with 16-byte accesses.
 __global__ void __launch_bounds__(256) rope_store_kernel(const bf16 *qkv, const RowDesc *rows, int M, int H, int KV,
                                                          int hd, const float *rope, KvCache kv, int layer, bf16 *q) {
+    pdl_trigger();
+    pdl_wait();
     const int m = blockIdx.x;
     const RowDesc r = rows[m];
     const int qd = (H + 2 * KV) * hd;
@@ -165,6 +172,8 @@ __global__ void __launch_bounds__(256) rope_store_kernel(const bf16 *qkv, const 
 
 __global__ void store_features_kernel(const float *x, const RowDesc *rows, int M, int d, bf16 *feat, int max_ctx,
                                       int slot) {
+    pdl_trigger();
+    pdl_wait();
     const int m = blockIdx.x;
     const RowDesc r = rows[m];
     bf16 *dst = feat + (((size_t)r.seq * max_ctx + r.phys) * 3 + slot) * d;
@@ -174,6 +183,8 @@ __global__ void store_features_kernel(const float *x, const RowDesc *rows, int M
 
 // fin[m] = [g_low, g_mid, g_high] of the target at logical position pos-1 (zeros at pos 0).
 __global__ void gather_features_kernel(const RowDesc *rows, int M, int d, const bf16 *feat, int max_ctx, bf16 *fin) {
+    pdl_trigger();
+    pdl_wait();
     const int m = blockIdx.x;
     const RowDesc r = rows[m];
     bf16 *dst = fin + (size_t)m * 3 * d;
@@ -188,6 +199,8 @@ __global__ void gather_features_kernel(const RowDesc *rows, int M, int d, const 
 
 __global__ void rows_copy_kernel(const float *src, int lds, const int *srows, float *dst, int ldd, const int *drows,
                                  int d) {
+    pdl_trigger();
+    pdl_wait();
     const int k = blockIdx.x;
     const int sr = srows ? srows[k] : k, dr = drows ? drows[k] : k;
     if (sr < 0 || dr < 0) return;
@@ -199,6 +212,8 @@ __global__ void rows_copy_kernel(const float *src, int lds, const int *srows, fl
 // 16-byte vector moves, each warp streams whole 256-byte head rows.
 __global__ void compact_kernel(SdDev d, const int32_t *rsel, const int32_t *racc, const int32_t *rbase, KvCache kv,
                                bf16 *feat, int feat_w, int max_ctx) {
+    pdl_trigger();
+    pdl_wait();
     const int a = blockIdx.x, j = blockIdx.y;
     const int r = d.active[a];
     const int sel = rsel[r], acc = racc[r];
@@ -245,7 +260,7 @@ void k_embed(const RowDesc *rows, int M, const int32_t *tok, int tok_cap, const 
              int n_max, const bf16 *emb, int V, int d, float *x, cudaStream_t st) {
     if (M <= 0) return;
     ProfScope prof("embed", 0, (double)M * d * 6.0, st);
-    embed_kernel<<<M, 128, 0, st>>>(rows, M, tok, tok_cap, chain_tok, t_max, n_max, emb, V, d, x);
+    launch_pdl(embed_kernel, M, 128, 0, st, rows, M, tok, tok_cap, chain_tok, t_max, n_max, emb, V, d, x);
     RS_LAUNCHED();
 }
 
@@ -253,8 +268,8 @@ void k_rmsnorm(const float *x, int ldx, const float *w, int M, int d, float eps,
     if (M <= 0) return;
     ProfScope prof("norm", 0, (double)M * d * 6.0, st);
     if (d % 8 || d > 8192) throw std::invalid_argument("rmsnorm: d must be a multiple of 8 and <= 8192");
-    rmsnorm_kernel<float><<<M, std::min(256, std::max(32, (d / 8 + 31) / 32 * 32)), 0, st>>>(x, ldx, w, M, d, eps,
-                                                                                            out, ldo);
+    launch_pdl(rmsnorm_kernel<float>, M, std::min(256, std::max(32, (d / 8 + 31) / 32 * 32)), 0, st, x, ldx, w, M, d,
+               eps, out, ldo);
     RS_LAUNCHED();
 }
 
@@ -263,8 +278,8 @@ void k_rmsnorm_bf16(const bf16 *x, int ldx, const float *w, int M, int d, float 
     if (M <= 0) return;
     ProfScope prof("norm", 0, (double)M * d * 4.0, st);
     if (d % 8 || d > 8192) throw std::invalid_argument("rmsnorm: d must be a multiple of 8 and <= 8192");
-    rmsnorm_kernel<bf16><<<M, std::min(256, std::max(32, (d / 8 + 31) / 32 * 32)), 0, st>>>(x, ldx, w, M, d, eps, out,
-                                                                                           ldo);
+    launch_pdl(rmsnorm_kernel<bf16>, M, std::min(256, std::max(32, (d / 8 + 31) / 32 * 32)), 0, st, x, ldx, w, M, d,
+               eps, out, ldo);
     RS_LAUNCHED();
 }
 
@@ -272,7 +287,7 @@ void k_rope_store(const bf16 *qkv, const RowDesc *rows, int M, const TfShape &s,
                   int layer, bf16 *q, cudaStream_t st) {
     if (M <= 0) return;
     ProfScope prof("rope", 0, (double)M * s.qkv_dim() * 4.0, st);
-    rope_store_kernel<<<M, 256, 0, st>>>(qkv, rows, M, s.H, s.KV, s.hd, rope, kv, layer, q);
+    launch_pdl(rope_store_kernel, M, 256, 0, st, qkv, rows, M, s.H, s.KV, s.hd, rope, kv, layer, q);
     RS_LAUNCHED();
 }
 
@@ -280,7 +295,7 @@ void k_store_features(const float *x, const RowDesc *rows, int M, int d, bf16 *f
                       cudaStream_t st) {
     if (M <= 0) return;
     ProfScope prof("feat", 0, (double)M * d * 6.0, st);
-    store_features_kernel<<<M, 256, 0, st>>>(x, rows, M, d, feat, max_ctx, slot);
+    launch_pdl(store_features_kernel, M, 256, 0, st, x, rows, M, d, feat, max_ctx, slot);
     RS_LAUNCHED();
 }
 
@@ -288,7 +303,7 @@ void k_gather_features(const RowDesc *rows, int M, int d, const bf16 *feat, int 
                        int *, cudaStream_t st) {
     if (M <= 0) return;
     ProfScope prof("feat", 0, (double)M * d * 12.0, st);
-    gather_features_kernel<<<M, 256, 0, st>>>(rows, M, d, feat, max_ctx, fin);
+    launch_pdl(gather_features_kernel, M, 256, 0, st, rows, M, d, feat, max_ctx, fin);
     RS_LAUNCHED();
 }
 
@@ -296,14 +311,14 @@ void k_rows_copy_f32(const float *src, int ld_src, const int *src_rows, float *d
                      int n, int d, cudaStream_t st) {
     if (n <= 0) return;
     ProfScope prof("copy", 0, (double)n * d * 8.0, st);
-    rows_copy_kernel<<<n, 256, 0, st>>>(src, ld_src, src_rows, dst, ld_dst, dst_rows, d);
+    launch_pdl(rows_copy_kernel, n, 256, 0, st, src, ld_src, src_rows, dst, ld_dst, dst_rows, d);
     RS_LAUNCHED();
 }
 
 void k_compact(const SdDev &d, const int32_t *rsel, const int32_t *racc, const int32_t *rbase, const KvCache &kv,
                bf16 *feat, int feat_w, int max_ctx, cudaStream_t st) {
     if (d.nact <= 0) return;
-    compact_kernel<<<dim3(d.nact, d.n), 256, 0, st>>>(d, rsel, racc, rbase, kv, feat, feat_w, max_ctx);
+    launch_pdl(compact_kernel, dim3(d.nact, d.n), 256, 0, st, d, rsel, racc, rbase, kv, feat, feat_w, max_ctx);
     RS_LAUNCHED();
 }
 

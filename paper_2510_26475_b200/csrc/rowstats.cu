@@ -7,6 +7,7 @@
 // consumers use. The row's normaliser is then a ~600-term combine and an inverse-CDF draw a
 // tile-prefix walk (sd_kernels.cu), instead of full 152K-element fp64 passes on one SM.
 #include "common.cuh"
+#include "launch.cuh"
 #include "prof.h"
 #include "sd.h"
 #include "tilestat.cuh"
@@ -17,6 +18,8 @@ namespace {
 
 __global__ void __launch_bounds__(256) row_stats_kernel(const float *rows, const int32_t *row_ids, int nrows, int V,
                                                         double tau, double *stats) {
+    pdl_trigger();
+    pdl_wait();
     const int ntiles = (V + 255) / 256;
     const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -40,7 +43,7 @@ void row_stats(const float *rows, const int32_t *row_ids, int nrows, int V, doub
     if (nrows <= 0) return;
     const long long warps = (long long)nrows * ((V + 255) / 256);
     ProfScope prof("rowstats", 0, (double)nrows * V * 4.0, st);
-    row_stats_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(rows, row_ids, nrows, V, tau, stats);
+    launch_pdl(row_stats_kernel, (unsigned)((warps + 7) / 8), 256, 0, st, rows, row_ids, nrows, V, tau, stats);
     RS_LAUNCHED();
 }
 

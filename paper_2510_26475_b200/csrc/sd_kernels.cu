@@ -25,6 +25,7 @@
 
 #include "common.cuh"
 #include "prof.h"
+#include "launch.cuh"
 #include "sd.h"
 #include "tilestat.cuh"
 
@@ -472,6 +473,8 @@ __device__ int sample_row(const RowRef<T> &r, const Stats &st, double u, double 
 }
 
 __global__ void cycle_begin_kernel(SdDev d) {
+    pdl_trigger();
+    pdl_wait();
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= d.nact) return;
     const int r = d.active[a];
@@ -487,6 +490,8 @@ __global__ void cycle_begin_kernel(SdDev d) {
 
 // specdec.cpp:165-171: remaining = max_emit - |accepted|; < 2 -> no drafting this round.
 __global__ void round_setup_kernel(SdDev d, int round) {
+    pdl_trigger();
+    pdl_wait();
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= d.nact) return;
     const int r = d.active[a];
@@ -509,6 +514,8 @@ __global__ void round_setup_kernel(SdDev d, int round) {
 
 template <class T>
 __global__ void __launch_bounds__(512) draft_sample_kernel(SdDev d, int depth) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double red[32];
     __shared__ long long redl[32];
     __shared__ int picked[kMaxBranch];
@@ -569,6 +576,8 @@ __global__ void __launch_bounds__(512) draft_sample_kernel(SdDev d, int depth) {
 // Offsets must equal the reference's sequential consumption: chain i starts after the
 // draws of chains 0..i-1 (specdec.cpp:177-192). Any mismatch -> fix + request a redraft.
 __global__ void redraft_check_kernel(SdDev d) {
+    pdl_trigger();
+    pdl_wait();
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= d.nact) return;
     const int r = d.active[a];
@@ -595,6 +604,8 @@ __global__ void redraft_check_kernel(SdDev d) {
 
 template <class T>
 __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int naive) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double red[32];
     __shared__ long long redl[32];
     __shared__ double Z[kMaxBranch];
@@ -827,6 +838,8 @@ done:
 }
 
 __global__ void cycle_end_kernel(SdDev d, int naive) {
+    pdl_trigger();
+    pdl_wait();
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= d.nact) return;
     const int r = d.active[a];
@@ -861,6 +874,8 @@ __device__ long long tab_row_index(const SdDev &d, const TabDev &m, int r, int l
 }
 
 __global__ void tab_rows_kernel(SdDev d, TabDev m, int depth, int verify, int naive) {
+    pdl_trigger();
+    pdl_wait();
     // blockIdx.x = active slot, blockIdx.y = tree slot
     const int a = blockIdx.x, slot = blockIdx.y;
     const int r = d.active[a];
@@ -908,13 +923,13 @@ inline int sd_threads(int V, bool) { return V <= 256 ? 32 : V <= 4096 ? 256 : 51
 
 void sd_cycle_begin(const SdDev &d, cudaStream_t st) {
     if (d.nact <= 0) return;
-    cycle_begin_kernel<<<(d.nact + 127) / 128, 128, 0, st>>>(d);
+    launch_pdl(cycle_begin_kernel, (d.nact + 127) / 128, 128, 0, st, d);
     RS_LAUNCHED();
 }
 
 void sd_round_setup(const SdDev &d, int round, cudaStream_t st) {
     if (d.nact <= 0) return;
-    round_setup_kernel<<<(d.nact + 127) / 128, 128, 0, st>>>(d, round);
+    launch_pdl(round_setup_kernel, (d.nact + 127) / 128, 128, 0, st, d, round);
     RS_LAUNCHED();
 }
 
@@ -925,14 +940,14 @@ void sd_draft_sample(const SdDev &d, int depth, RowType rt, cudaStream_t st) {
     const int th = std::min(512, sd_threads(d.V, d.Qst != nullptr));
     const double es = rt == RowType::F64 ? 8.0 : 4.0;
     ProfScope prof("sample", 0, (double)d.nact * (depth == 0 ? 1 : d.t) * d.V * es, st);
-    if (rt == RowType::F64) draft_sample_kernel<double><<<grid, th, 0, st>>>(d, depth);
-    else draft_sample_kernel<float><<<grid, th, 0, st>>>(d, depth);
+    if (rt == RowType::F64) launch_pdl(draft_sample_kernel<double>, grid, th, 0, st, d, depth);
+    else launch_pdl(draft_sample_kernel<float>, grid, th, 0, st, d, depth);
     RS_LAUNCHED();
 }
 
 void sd_redraft_check(const SdDev &d, cudaStream_t st) {
     if (d.nact <= 0) return;
-    redraft_check_kernel<<<(d.nact + 127) / 128, 128, 0, st>>>(d);
+    launch_pdl(redraft_check_kernel, (d.nact + 127) / 128, 128, 0, st, d);
     RS_LAUNCHED();
 }
 
@@ -961,13 +976,15 @@ void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t s
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = C;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = tuning().pdl >= 0 ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     const int nv = naive ? 1 : 0;
     if (rt == RowType::F64) RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<double>, d, round, nv));
     else RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<float>, d, round, nv));
@@ -976,21 +993,21 @@ void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t s
 
 void sd_cycle_end(const SdDev &d, bool naive, cudaStream_t st) {
     if (d.nact <= 0) return;
-    cycle_end_kernel<<<(d.nact + 127) / 128, 128, 0, st>>>(d, naive ? 1 : 0);
+    launch_pdl(cycle_end_kernel, (d.nact + 127) / 128, 128, 0, st, d, naive ? 1 : 0);
     RS_LAUNCHED();
 }
 
 void tab_draft_rows(const SdDev &d, const TabDev &m, int depth, cudaStream_t st) {
     if (d.nact <= 0) return;
     dim3 grid(d.nact, depth == 0 ? 1 : d.t);
-    tab_rows_kernel<<<grid, 32, 0, st>>>(d, m, depth, 0, 0);
+    launch_pdl(tab_rows_kernel, grid, 32, 0, st, d, m, depth, 0, 0);
     RS_LAUNCHED();
 }
 
 void tab_verify_rows(const SdDev &d, const TabDev &m, bool naive, cudaStream_t st) {
     if (d.nact <= 0) return;
     dim3 grid(d.nact, naive ? 1 : d.slots);
-    tab_rows_kernel<<<grid, 32, 0, st>>>(d, m, 0, 1, naive ? 1 : 0);
+    launch_pdl(tab_rows_kernel, grid, 32, 0, st, d, m, 0, 1, naive ? 1 : 0);
     RS_LAUNCHED();
 }
 
