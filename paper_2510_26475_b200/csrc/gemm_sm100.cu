@@ -86,12 +86,14 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi &ep, uint32_t tbase
 #pragma unroll
                 for (int j = 0; j < 32; j += 8) {
                     __align__(16) __nv_bfloat162 h[4];
+                    __align__(16) __nv_bfloat162 bb[4];
+                    if (bias) *reinterpret_cast<int4 *>(bb) = __ldg(reinterpret_cast<const int4 *>(bias + n0 + j));
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         float a = __uint_as_float(v[j + 2 * k]), b = __uint_as_float(v[j + 2 * k + 1]);
                         if (bias) {
-                            a += __bfloat162float(bias[n0 + j + 2 * k]);
-                            b += __bfloat162float(bias[n0 + j + 2 * k + 1]);
+                            a += __low2float(bb[k]);
+                            b += __high2float(bb[k]);
                         }
                         h[k] = __floats2bfloat162_rn(a, b);
                     }
@@ -242,22 +244,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    pdl_wait();  // operands / residual of the previous kernel
 
     if (warp == 0) {
         if (lane == 0) {
+            // The weights (B) do not depend on the previous kernel: the first ring's worth of B
+            // k-blocks is requested before the programmatic-dependency wait, so the HBM latency
+            // of the weight stream overlaps the previous kernel's tail. A (activations) follows.
+            int pre = 0;
+            if (blockIdx.x < num_units) {
+                const int tile = blockIdx.x / splits;
+                const int n0 = (tile / num_m) * BN;
+                int kb0, kb1;
+                krange(blockIdx.x % splits, kb0, kb1);
+                pre = min(C::kStages, kb1 - kb0);
+                for (int i = 0; i < pre; ++i) {
+                    mbar_arrive_expect_tx(&full[i], C::kStageBytes);
+                    tma_load_2d(sB + i * C::kBBytes, &tmB, &full[i], (kb0 + i) * BK, n0);
+                }
+            }
+            pdl_wait();  // activations / residual of the previous kernel
             int stage = 0;
             uint32_t phase = 0;
+            int issued = 0;
             for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x) {
                 const int tile = unit / splits;
                 const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
                 int kb0, kb1;
                 krange(unit % splits, kb0, kb1);
-                for (int kb = kb0; kb < kb1; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb, ++issued) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                    if (issued >= pre) {
+                        mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                        tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, n0);
+                    }
                     tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK, m0);
-                    tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, n0);
                     if (++stage == C::kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -296,6 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
+        pdl_wait();  // outputs / residual / bias reads happen after the previous kernel
         const int q = warp - 4;  // TMEM lane quadrant == warp % 4
         int it = 0;
         for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++it) {
