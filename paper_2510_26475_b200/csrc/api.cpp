@@ -661,6 +661,10 @@ int rs_set_tuning(const char *key, int64_t value) {
             rs::tuning().accept_cluster = static_cast<int>(value);
         } else if (k == "fused_stats") {
             rs::tuning().fused_stats = value != 0 ? 1 : -1;
+        } else if (k == "gemm2") {
+            rs::tuning().gemm2 = static_cast<int>(value);
+        } else if (k == "pdl") {
+            rs::tuning().pdl = static_cast<int>(value);
         } else {
             throw std::invalid_argument("unknown tuning key: " + k);
         }
@@ -712,7 +716,7 @@ int rs_gemm_bf16(rs_ctx *ctx, const void *A, const void *B, void *Cp, const void
         g.splits = std::max(1, (int)splits);
         g.epi.kind = epilogue;
         g.epi.out = Cp;
-        g.epi.ldo = epilogue == kEpiSwiGLU ? N / 2 : N;
+        g.epi.ldo = epilogue == kEpiSwiGLU || epilogue == kEpiSwiGLU2 ? N / 2 : N;
         g.epi.bias = bias;
         g.epi.scale = scale;
         gemm_bf16(g, ctx->stream);

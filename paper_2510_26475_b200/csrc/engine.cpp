@@ -40,6 +40,7 @@ Tuning &tuning() {
                     else if (k == "attn_tc") x.attn_tc = v;
                     else if (k == "attn_trace") x.attn_trace = v;
                     else if (k == "pdl") x.pdl = v;
+                    else if (k == "gemm2") x.gemm2 = v;
                 }
                 p = e + 1;
             }

@@ -5,7 +5,9 @@
 
 namespace rs {
 
-enum GemmEpiKind { kEpiBF16 = 0, kEpiF32 = 1, kEpiResidual = 2, kEpiSwiGLU = 3 };
+// kEpiSwiGLU: gate/up rows interleaved per 256-row block as [128 gate, 128 up];
+// kEpiSwiGLU2: interleaved pairwise (row 2i gate_i, row 2i+1 up_i) -- the model layout.
+enum GemmEpiKind { kEpiBF16 = 0, kEpiF32 = 1, kEpiResidual = 2, kEpiSwiGLU = 3, kEpiSwiGLU2 = 4 };
 
 struct GemmEpi {
     int kind = kEpiBF16;
@@ -30,6 +32,7 @@ struct GemmArgs {
     // output in split order (deterministic; keep it a function of (N, K) only so a row's
     // result stays independent of M).
     int splits = 1;
+    bool force_1sm = false;   // keep the single-SM kernel (e.g. fused softmax statistics tests)
     GemmEpi epi;
 };
 
@@ -40,5 +43,12 @@ void gemm_bf16(const GemmArgs &g, cudaStream_t st);
 // 2D bf16 TMA map over a row-major [rows, cols] matrix (leading dim `ld` elements), box of
 // 64 columns x box_rows rows, 128B swizzle (gemm_sm100.cu).
 CUtensorMap make_tma_map_bf16(const void *base, int rows, int cols, int ld, int box_rows);
+
+// SM-pair GEMM (gemm_2sm.cu): same contract as gemm_bf16 (C[M, N] = A . B^T, A = M token rows,
+// B = N weight rows), computed with the weights as the 256-row M operand of
+// tcgen05.mma.cta_group::2. block_n = token tile (0 = auto). No fused softmax statistics and
+// no block-interleaved SwiGLU (kEpiSwiGLU2 only).
+bool gemm2_supported(const GemmArgs &g);
+void gemm2_bf16(const GemmArgs &g, cudaStream_t st);
 
 }  // namespace rs

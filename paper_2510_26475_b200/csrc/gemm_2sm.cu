@@ -1,0 +1,446 @@
+// gemm_2sm.cu -- weight GEMMs on SM PAIRS (tcgen05.mma.cta_group::2), weights as the M operand.
+//
+//   C[T, N] = X[T, K] . W[N, K]^T     (X: T tokens of activations, W: N output features)
+//
+// computed as C^T = W . X^T: a CTA pair (thread-block cluster of 2) owns a 256-feature x BT-token
+// tile. Each CTA stages its own 128 weight rows and HALF of the token rows (BT/2) per 64-wide
+// k-block; the leader's single elected thread issues 128x... M=256 tcgen05.mma.cta_group::2 that
+// read the weight halves and the token halves of BOTH CTAs, and each CTA's TMEM receives the
+// fp32 accumulator of its own 128 features x BT tokens. Per SM and k-block this moves
+// 16 KB + BT/2 x 128 B instead of 16 KB + BT x 128 B, and the feature dimension of every Qwen
+// projection (QKV, O, gate/up, down, LM head) is a multiple of 256 while the token count (the
+// verify tree: batch x (t n + 1)) is arbitrary -- no padded 128-row tiles.
+//
+// Roles per CTA (256 threads): warp 0 lane 0 = TMA producer (both CTAs; complete_tx lands on
+// the LEADER's full barrier, the leader alone arms it with both CTAs' bytes), warp 1 lane 0 of
+// the leader = MMA issuer (commits multicast to both CTAs' empty / accumulator-full barriers),
+// warp 2 = TMEM allocator (cta_group::2, both CTAs), warps 4-7 = epilogue: thread = one feature
+// row (TMEM lane), 32 tokens per tcgen05.ld, stores C[t][f] coalesced across the warp's lanes,
+// then arrives (remotely for the peer) on the leader's accumulator-empty barrier.
+// Epilogues: bias + bf16, scaled fp32 with a token row map (LM head), fp32 residual add
+// (deterministic split-K order), SiLU(gate) * up with gate/up rows interleaved pairwise.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "gemm.h"
+#include "launch.cuh"
+#include "prof.h"
+#include "tc.cuh"
+
+namespace rs {
+
+namespace {
+
+constexpr int kBM = 128;  // weight rows per CTA (256 per pair)
+constexpr int kBK = 64;
+constexpr int kThr = 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `p` (a local shared variable) in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(const void *p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2sm(void *dst, const CUtensorMap *map, uint32_t bar_cluster, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(bar_cluster), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+// arrive on the barrier at the same offset in both CTAs of the pair once prior MMAs are done
+__device__ __forceinline__ void tc_commit2_mc(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
+template <int BT>
+struct Cfg2 {
+    static constexpr int kABytes = kBM * kBK * 2;          // own 128 weight rows
+    static constexpr int kBBytes = (BT / 2) * kBK * 2;     // own half of the token rows
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStages = (180 * 1024) / kStageBytes > 8 ? 8 : (180 * 1024) / kStageBytes;
+    static constexpr int kTmemCols = 2 * BT <= 128 ? 128 : 2 * BT <= 256 ? 256 : 512;
+    static constexpr int kStgBytes = 4 * 32 * 33 * 4;  // epilogue transpose blocks (4 warps)
+    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256 + kStgBytes;
+    // kind::f16, bf16 x bf16 -> f32, both K-major, N = BT tokens, M = 256 features (pair)
+    static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BT >> 3) << 17) |
+                                       (static_cast<uint32_t>(256 >> 4) << 24);
+};
+
+__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+
+// Epilogue of one 32-token chunk of this warp's 32 feature rows f0w .. f0w + 31 (lane = row).
+// The accumulator (thread = feature row, registers = tokens) is transposed through a
+// 32 x 33 fp32 staging block so global memory is written token-row-wise with 16-byte vectors:
+// C[t][f0w .. f0w + 31] is 128 B (fp32) / 64 B (bf16) / 32 B (SwiGLU, 16 outputs) contiguous.
+template <int EPI>
+__device__ __forceinline__ void epi2_chunk(const GemmEpi &ep, uint32_t taddr, int f0w, int t0, int F, int T,
+                                           float (*stg)[33]) {
+    uint32_t v[32];
+    tmem_ld32(taddr, v);
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) stg[j][lane] = __uint_as_float(v[j]);  // stg[token][feature]
+    __syncwarp();
+    if constexpr (EPI == kEpiF32 || EPI == kEpiResidual) {
+        // 8 lanes x float4 per token row, 4 token rows per pass
+        const int sub = lane >> 3, c4 = (lane & 7) * 4;
+        const int f = f0w + c4;
+        float4 cur[8];
+        int rowo[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int j = i * 4 + sub, t = t0 + j;
+            rowo[i] = -1;
+            if (t < T && f < F) {
+                rowo[i] = EPI == kEpiF32 ? (ep.row_map ? __ldg(ep.row_map + t) : t) : t;
+                if (EPI == kEpiResidual && rowo[i] >= 0)
+                    cur[i] = __ldcg(reinterpret_cast<const float4 *>(static_cast<float *>(ep.out) +
+                                                                     (size_t)rowo[i] * ep.ldo + f));
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (rowo[i] < 0) continue;
+            const int j = i * 4 + sub;
+            float4 o = make_float4(stg[j][c4], stg[j][c4 + 1], stg[j][c4 + 2], stg[j][c4 + 3]);
+            if (EPI == kEpiF32) {
+                o.x *= ep.scale;
+                o.y *= ep.scale;
+                o.z *= ep.scale;
+                o.w *= ep.scale;
+            } else {
+                o.x += cur[i].x;
+                o.y += cur[i].y;
+                o.z += cur[i].z;
+                o.w += cur[i].w;
+            }
+            *reinterpret_cast<float4 *>(static_cast<float *>(ep.out) + (size_t)rowo[i] * ep.ldo + f) = o;
+        }
+    } else if constexpr (EPI == kEpiBF16) {
+        // 4 lanes x 8 bf16 per token row, 8 token rows per pass
+        const int sub = lane >> 2, c8 = (lane & 3) * 8;
+        const int f = f0w + c8;
+        __align__(16) __nv_bfloat162 bb[4];
+        if (ep.bias && f < F) *reinterpret_cast<int4 *>(bb) = __ldg(reinterpret_cast<const int4 *>(
+                                  static_cast<const __nv_bfloat16 *>(ep.bias) + f));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int j = i * 8 + sub, t = t0 + j;
+            if (t >= T || f >= F) continue;
+            __align__(16) __nv_bfloat162 h[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                float a = stg[j][c8 + 2 * k], b = stg[j][c8 + 2 * k + 1];
+                if (ep.bias) {
+                    a += __low2float(bb[k]);
+                    b += __high2float(bb[k]);
+                }
+                h[k] = __floats2bfloat162_rn(a, b);
+            }
+            *reinterpret_cast<int4 *>(static_cast<__nv_bfloat16 *>(ep.out) + (size_t)t * ep.ldo + f) =
+                *reinterpret_cast<const int4 *>(h);
+        }
+    } else {  // kEpiSwiGLU2: feature rows 2i / 2i + 1 = gate_i / up_i -> 16 outputs per token
+        const int sub = lane >> 1, c16 = (lane & 1) * 16;  // 2 lanes x 8 outputs per token row
+        const int fo = (f0w >> 1) + (c16 >> 1);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int j = i * 16 + sub, t = t0 + j;
+            if (t >= T || 2 * fo >= F) continue;
+            __align__(16) __nv_bfloat162 h[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float g0 = stg[j][c16 + 4 * k], u0 = stg[j][c16 + 4 * k + 1];
+                const float g1 = stg[j][c16 + 4 * k + 2], u1 = stg[j][c16 + 4 * k + 3];
+                h[k] = __floats2bfloat162_rn(silu(g0) * u0, silu(g1) * u1);
+            }
+            *reinterpret_cast<int4 *>(static_cast<__nv_bfloat16 *>(ep.out) + (size_t)t * ep.ldo + fo) =
+                *reinterpret_cast<const int4 *>(h);
+        }
+    }
+}
+
+// F = features (rows of W), T = tokens (rows of X). Units = (feature pair-tile, token tile, split),
+// token tiles fastest so the pairs that share a weight tile run together (one HBM read).
+template <int BT, int EPI>
+__global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmEpi ep, int F,
+                 int T, int K, int splits, int *sem) {
+    using C = Cfg2<BT>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + C::kStages * C::kABytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::kStages * C::kStageBytes);
+    uint64_t *empty = full + C::kStages;
+    uint64_t *tfull = empty + C::kStages;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    float(*stg_all)[33] = reinterpret_cast<float(*)[33]>(smem + C::kStages * C::kStageBytes + 256);
+
+    pdl_trigger();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int num_f = (F + 2 * kBM - 1) / (2 * kBM), num_t = (T + BT - 1) / BT;
+    const int num_k = (K + kBK - 1) / kBK;
+    const int num_units = num_f * num_t * splits;
+    auto unit_coords = [&](int unit, int &f0, int &t0, int &kb0, int &kb1) {
+        const int split = unit % splits, tile = unit / splits;
+        f0 = (tile / num_t) * 2 * kBM + rank * kBM;
+        t0 = (tile % num_t) * BT;
+        kb0 = split * num_k / splits;
+        kb1 = (split + 1) * num_k / splits;
+    };
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 2 * 128);  // both CTAs' epilogue threads
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(C::kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::);
+    }
+    tc_fence_before();
+    cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / TMA
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint32_t lead_full = mapa(full, 0);  // full[0] of the leader; stage s at + 8 s
+            // weights do not depend on the previous kernel: the first ring's worth of W k-blocks
+            // goes out before the programmatic-dependency wait, the token rows after it
+            int pre = 0;
+            if (pair < num_units) {
+                int f0, t0, kb0, kb1;
+                unit_coords(pair, f0, t0, kb0, kb1);
+                pre = min(C::kStages, kb1 - kb0);
+                for (int i = 0; i < pre; ++i) {
+                    if (leader) mbar_arrive_expect_tx(&full[i], 2 * C::kStageBytes);
+                    tma_load_2sm(sA + i * C::kABytes, &tmW, lead_full + 8 * i, (kb0 + i) * kBK, f0);
+                }
+            }
+            pdl_wait();
+            int stage = 0;
+            uint32_t phase = 0;
+            int issued = 0;
+            for (int unit = pair; unit < num_units; unit += npairs) {
+                int f0, t0, kb0, kb1;
+                unit_coords(unit, f0, t0, kb0, kb1);
+                const int tb = t0 + (int)rank * (BT / 2);
+                for (int kb = kb0; kb < kb1; ++kb, ++issued) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (issued >= pre) {
+                        if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
+                        tma_load_2sm(sA + stage * C::kABytes, &tmW, lead_full + 8 * stage, kb * kBK, f0);
+                    }
+                    tma_load_2sm(sB + stage * C::kBBytes, &tmX, lead_full + 8 * stage, kb * kBK, tb);
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int unit = pair; unit < num_units; unit += npairs, ++it) {
+                const int acc = it & 1;
+                int f0, t0, kb0, kb1;
+                unit_coords(unit, f0, t0, kb0, kb1);
+                mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + acc * BT;
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint64_t ad = sw128_desc(sA + stage * C::kABytes);
+                    const uint64_t bd = sw128_desc(sB + stage * C::kBBytes);
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k)
+                        tc_mma2(tmem_d, ad + 2 * k, bd + 2 * k, C::kIdesc, (kb != kb0) || k != 0);
+                    tc_commit2_mc(&empty[stage]);
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit2_mc(&tfull[acc]);
+            }
+        }
+    } else if (warp >= 4) {
+        pdl_wait();
+        const int q = warp - 4;  // TMEM lane quadrant
+        const uint32_t lead_tempty = mapa(tempty, 0);
+        int it = 0;
+        for (int unit = pair; unit < num_units; unit += npairs, ++it) {
+            int f0, t0, kb0, kb1;
+            unit_coords(unit, f0, t0, kb0, kb1);
+            const int split = unit % splits, tile = unit / splits;
+            const int acc = it & 1;
+            mbar_wait(&tfull[acc], (it >> 1) & 1);
+            tc_fence_after();
+            if (EPI == kEpiResidual && splits > 1) {
+                int v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(sem + tile) : "memory");
+                    if (v < 2 * split) __nanosleep(32);
+                } while (v < 2 * split);  // both CTAs of the predecessor split are done
+            }
+            const uint32_t tb = tmem_base + acc * BT + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+            for (int c = 0; c < BT / 32; ++c)
+                epi2_chunk<EPI>(ep, tb + c * 32, f0 + q * 32, t0 + c * 32, F, T, stg_all + q * 32);
+            tc_fence_before();
+            mbar_arrive_remote(lead_tempty + 8 * acc);
+            if (EPI == kEpiResidual && splits > 1) {
+                __threadfence();
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (q == 0 && lane == 0) atomicAdd(sem + tile, 1);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();  // no CTA leaves while its peer may still signal its barriers
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::kTmemCols));
+    }
+}
+
+int num_sms2() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        RS_CUDA(cudaGetDevice(&dev));
+        RS_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return n;
+}
+
+template <int BT, int EPI>
+void launch2(const GemmArgs &g, cudaStream_t st) {
+    using C = Cfg2<BT>;
+    static bool attr = false;
+    if (!attr) {
+        RS_CUDA(cudaFuncSetAttribute(gemm2_kernel<BT, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+        attr = true;
+    }
+    const int F = g.N, T = g.M;
+    const CUtensorMap tw = make_tma_map_bf16(g.B, F, g.K, g.ldb, kBM);
+    const CUtensorMap tx = make_tma_map_bf16(g.A, T, g.K, g.lda, BT / 2);
+    const int tiles = ((F + 2 * kBM - 1) / (2 * kBM)) * ((T + BT - 1) / BT);
+    const int num_k = (g.K + kBK - 1) / kBK;
+    const int splits = EPI == kEpiResidual ? std::max(1, std::min(g.splits, num_k)) : 1;
+    int *sem = nullptr;
+    if (splits > 1) {
+        static thread_local int *sems = nullptr;
+        static thread_local int sems_n = 0;
+        if (sems_n < tiles) {
+            if (sems) cudaFree(sems);
+            sems_n = std::max(tiles, 4096);
+            RS_CUDA(cudaMalloc(&sems, (size_t)sems_n * sizeof(int)));
+        }
+        RS_CUDA(cudaMemsetAsync(sems, 0, (size_t)tiles * sizeof(int), st));
+        sem = sems;
+    }
+    const int pairs = std::min(tiles * splits, num_sms2() / 2);
+    launch_pdl(gemm2_kernel<BT, EPI>, dim3(2 * pairs), kThr, C::kSmem, st, tw, tx, g.epi, F, T, g.K, splits, sem);
+    RS_LAUNCHED();
+}
+
+}  // namespace
+
+bool gemm2_supported(const GemmArgs &g) {
+    return g.K % 8 == 0 && g.lda % 8 == 0 && g.ldb % 8 == 0 && g.epi.stats == nullptr && g.M > 0 && g.N > 0 &&
+           g.epi.kind != kEpiSwiGLU;
+}
+
+// Token tile width: the widest of {256, 224, 192, 160, 128, 96, 64} that keeps the pair-tile
+// count within one wave of SM pairs, else the one with the least wave-quantised work.
+int gemm2_pick_bt(int F, int T, int sms) {
+    const int pairs = sms / 2, nf = (F + 255) / 256;
+    double best = 1e30;
+    int bt = 256;
+    for (int cand : {256, 224, 192, 160, 128, 96, 64}) {
+        const int tiles = nf * ((T + cand - 1) / cand);
+        const double waves = (double)((tiles + pairs - 1) / pairs);
+        const double cost = waves * cand * (1.0 + 0.04 * (256 - cand) / 32.0);
+        if (cost < best) {
+            best = cost;
+            bt = cand;
+        }
+    }
+    return bt;
+}
+
+void gemm2_bf16(const GemmArgs &g, cudaStream_t st) {
+    const int bt = g.block_n ? g.block_n : gemm2_pick_bt(g.N, g.M, num_sms2());
+    auto by_bt = [&](auto tag) {
+        constexpr int E = decltype(tag)::value;
+        switch (bt) {
+            case 64: launch2<64, E>(g, st); break;
+            case 96: launch2<96, E>(g, st); break;
+            case 128: launch2<128, E>(g, st); break;
+            case 160: launch2<160, E>(g, st); break;
+            case 192: launch2<192, E>(g, st); break;
+            case 224: launch2<224, E>(g, st); break;
+            case 256: launch2<256, E>(g, st); break;
+            default: throw std::invalid_argument("gemm2: token tile must be 64..256 in steps of 32");
+        }
+    };
+    switch (g.epi.kind) {
+        case kEpiBF16: by_bt(std::integral_constant<int, kEpiBF16>{}); break;
+        case kEpiF32: by_bt(std::integral_constant<int, kEpiF32>{}); break;
+        case kEpiResidual: by_bt(std::integral_constant<int, kEpiResidual>{}); break;
+        case kEpiSwiGLU2: by_bt(std::integral_constant<int, kEpiSwiGLU2>{}); break;
+        default: throw std::invalid_argument("gemm2: unsupported epilogue");
+    }
+}
+
+}  // namespace rs

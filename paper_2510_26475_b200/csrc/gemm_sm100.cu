@@ -75,6 +75,28 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi &ep, uint32_t tbase
                 if (n0 + j < Nout) out[j] = __float2bfloat16(silu(__uint_as_float(v[j])) * __uint_as_float(u[j]));
         }
         return;
+    } else if constexpr (EPI == kEpiSwiGLU2) {
+        // pairwise interleave: accumulator columns 2i / 2i + 1 are gate_i / up_i
+        tmem_ld32(tbase + chunk * 32, v);
+        if (row >= M) return;
+        const int n0 = col0 / 2 + chunk * 16;  // output column
+        const int Nout = N / 2;
+        __nv_bfloat16 *out = static_cast<__nv_bfloat16 *>(ep.out) + static_cast<size_t>(row) * ep.ldo + n0;
+        if (n0 + 16 <= Nout) {
+            __align__(16) __nv_bfloat162 h[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                h[k] = __floats2bfloat162_rn(silu(__uint_as_float(v[4 * k])) * __uint_as_float(v[4 * k + 1]),
+                                             silu(__uint_as_float(v[4 * k + 2])) * __uint_as_float(v[4 * k + 3]));
+            reinterpret_cast<int4 *>(out)[0] = reinterpret_cast<const int4 *>(h)[0];
+            reinterpret_cast<int4 *>(out)[1] = reinterpret_cast<const int4 *>(h)[1];
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (n0 + j < Nout)
+                    out[j] = __float2bfloat16(silu(__uint_as_float(v[2 * j])) * __uint_as_float(v[2 * j + 1]));
+        }
+        return;
     } else {
         tmem_ld32(tbase + chunk * 32, v);
         if (row >= M) return;
@@ -447,6 +469,13 @@ void launch(const GemmArgs &g, cudaStream_t st) {
 
 void gemm_bf16(const GemmArgs &g, cudaStream_t st) {
     if (g.M <= 0 || g.N <= 0) return;
+    if (tuning().gemm2 >= 0 && !g.force_1sm && gemm2_supported(g)) {
+        const double out_el = g.epi.kind == kEpiSwiGLU2 ? 0.5 * g.M * g.N : (double)g.M * g.N;
+        const double out_b = g.epi.kind == kEpiBF16 || g.epi.kind == kEpiSwiGLU2 ? 2.0 : g.epi.kind == kEpiF32 ? 4.0 : 8.0;
+        ProfScope prof("gemm", 2.0 * g.M * g.N * g.K, 2.0 * ((double)g.M * g.K + (double)g.N * g.K) + out_el * out_b, st);
+        gemm2_bf16(g, st);
+        return;
+    }
     if (g.K % 8 || g.lda % 8 || g.ldb % 8) throw std::invalid_argument("gemm_bf16: K and leading dims must be multiples of 8");
     if (g.epi.kind == kEpiSwiGLU && (g.N % 256)) throw std::invalid_argument("gemm_bf16: SwiGLU needs N % 256 == 0");
     int bn = g.block_n;
@@ -465,8 +494,11 @@ void gemm_bf16(const GemmArgs &g, cudaStream_t st) {
         }
     }
     if (g.epi.kind == kEpiSwiGLU || g.epi.stats) bn = 256;
-    const double out_el = g.epi.kind == kEpiSwiGLU ? 0.5 * g.M * g.N : (double)g.M * g.N;
-    const double out_b = g.epi.kind == kEpiBF16 || g.epi.kind == kEpiSwiGLU ? 2.0 : g.epi.kind == kEpiF32 ? 4.0 : 8.0;
+    if (g.epi.kind == kEpiSwiGLU2 && (g.N % 2)) throw std::invalid_argument("gemm_bf16: SwiGLU needs an even N");
+    const double out_el = g.epi.kind == kEpiSwiGLU || g.epi.kind == kEpiSwiGLU2 ? 0.5 * g.M * g.N : (double)g.M * g.N;
+    const double out_b = g.epi.kind == kEpiBF16 || g.epi.kind == kEpiSwiGLU || g.epi.kind == kEpiSwiGLU2 ? 2.0
+                         : g.epi.kind == kEpiF32                                                        ? 4.0
+                                                                                                        : 8.0;
     ProfScope prof("gemm", 2.0 * g.M * g.N * g.K, 2.0 * ((double)g.M * g.K + (double)g.N * g.K) + out_el * out_b, st);
     auto by_bn = [&](auto epi_tag) {
         constexpr int E = decltype(epi_tag)::value;
@@ -484,6 +516,7 @@ void gemm_bf16(const GemmArgs &g, cudaStream_t st) {
         case kEpiF32: by_bn(std::integral_constant<int, kEpiF32>{}); break;
         case kEpiResidual: by_bn(std::integral_constant<int, kEpiResidual>{}); break;
         case kEpiSwiGLU: launch<256, kEpiSwiGLU>(g, st); break;
+        case kEpiSwiGLU2: by_bn(std::integral_constant<int, kEpiSwiGLU2>{}); break;
         default: throw std::invalid_argument("gemm_bf16: unknown epilogue");
     }
 }

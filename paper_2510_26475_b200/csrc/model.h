@@ -21,7 +21,7 @@ struct LayerW {
     bf16 *qkv_w = nullptr;   // [(H+2KV)*hd, d_in]
     bf16 *qkv_b = nullptr;   // [(H+2KV)*hd]
     bf16 *o_w = nullptr;     // [d, H*hd]
-    bf16 *gu_w = nullptr;    // [2*dff, d], 256-row blocks of [128 gate, 128 up]
+    bf16 *gu_w = nullptr;    // [2*dff, d], rows interleaved pairwise: 2i gate_i, 2i+1 up_i
     bf16 *down_w = nullptr;  // [d, dff]
     float *ln1 = nullptr;    // [d_in]
     float *ln2 = nullptr;    // [d]

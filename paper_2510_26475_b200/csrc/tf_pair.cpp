@@ -122,7 +122,7 @@ GemmEpi epi_resid(float *out, int ldo) {
 }
 GemmEpi epi_swiglu(void *out, int ldo) {
     GemmEpi e;
-    e.kind = kEpiSwiGLU;
+    e.kind = kEpiSwiGLU2;  // gate/up rows interleaved pairwise (model layout)
     e.out = out;
     e.ldo = ldo;
     return e;

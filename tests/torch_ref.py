@@ -21,12 +21,11 @@ class TargetRef:
         self.final = m.to_torch("final_norm").float()
         self.layers = []
         for l in range(s.n_layers):
-            gu = m.to_torch("gu_w", l).view(2 * s.d_ff, d).float()
-            blocks = gu.view(-1, 256, d)
+            gu = m.to_torch("gu_w", l).view(2 * s.d_ff, d).float()  # rows 2i gate_i, 2i+1 up_i
             self.layers.append(dict(
                 qkv_w=m.to_torch("qkv_w", l).view(q, d).float(), qkv_b=m.to_torch("qkv_b", l).float(),
                 o_w=m.to_torch("o_w", l).view(d, s.n_heads * s.head_dim).float(),
-                g_w=blocks[:, :128].reshape(-1, d), u_w=blocks[:, 128:].reshape(-1, d),
+                g_w=gu[0::2], u_w=gu[1::2],
                 down_w=m.to_torch("down_w", l).view(d, s.d_ff).float(),
                 ln1=m.to_torch("ln1", l).float(), ln2=m.to_torch("ln2", l).float()))
         self.feat_layers = (min(1, s.n_layers - 1), s.n_layers // 2, s.n_layers - 1)
@@ -99,10 +98,10 @@ class DrafterRef:
         self.fc = dm.to_torch("fc_w").view(d, 3 * d).float()
         self.ne = dm.to_torch("norm_emb").float()
         self.nh = dm.to_torch("norm_hid").float()
-        gu = dm.to_torch("gu_w").view(2 * s.d_ff, d).float().view(-1, 256, d)
+        gu = dm.to_torch("gu_w").view(2 * s.d_ff, d).float()
         self.L = dict(qkv_w=dm.to_torch("qkv_w").view(q, 2 * d).float(), qkv_b=dm.to_torch("qkv_b").float(),
                       o_w=dm.to_torch("o_w").view(d, s.n_heads * s.head_dim).float(),
-                      g_w=gu[:, :128].reshape(-1, d), u_w=gu[:, 128:].reshape(-1, d),
+                      g_w=gu[0::2], u_w=gu[1::2],
                       down_w=dm.to_torch("down_w").view(d, s.d_ff).float(), ln2=dm.to_torch("ln2").float())
         self.final = dm.to_torch("final_norm").float()
         self.lm = dm.to_torch("lm_w").view(s.vocab, d).float()

@@ -9,17 +9,18 @@ sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(_
 import paper_2510_26475_b200 as rb  # noqa: E402
 
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 1344
-shapes = {"qkv": (2560, 2048, 0), "o": (2048, 2048, 2), "gate_up": (22016, 2048, 3), "down": (2048, 11008, 2),
+shapes = {"qkv": (2560, 2048, 0), "o": (2048, 2048, 2), "gate_up": (22016, 2048, 4), "down": (2048, 11008, 2),
           "lm_head": (151936, 2048, 1)}
 dev = rb.default_device()
 s = torch.cuda.Stream()
 dev.set_stream(s.cuda_stream)
 res = {}
 for name, (N, K, epi) in shapes.items():
-    for bn in ([256, 128] if epi != 3 else [256]):
+    for bn in ("pair", "single"):
+        rb.set_tuning("gemm2", 0 if bn == "pair" else -1)
         A = torch.randn(M, K, device="cuda").bfloat16()
         B = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
-        out = torch.zeros(M, N // 2 if epi == 3 else N, device="cuda",
+        out = torch.zeros(M, N // 2 if epi in (3, 4) else N, device="cuda",
                           dtype=torch.float32 if epi in (1, 2) else torch.bfloat16)
         bias = torch.zeros(N, device="cuda").bfloat16()
 
@@ -27,7 +28,7 @@ for name, (N, K, epi) in shapes.items():
             rb._check(rb.lib().rs_gemm_bf16(dev.handle, ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
                                             ctypes.c_void_p(out.data_ptr()),
                                             ctypes.c_void_p(bias.data_ptr()) if epi == 0 else None, M, N, K, epi, 1.0,
-                                            bn, 1))
+                                            0, 1))
         torch.cuda.synchronize()
         for _ in range(3):
             run()
