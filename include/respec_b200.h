@@ -206,6 +206,11 @@ int rs_engine_active_trace(const rs_engine *e, int32_t *out, int32_t cap, int32_
 int rs_engine_drafter_versions(const rs_engine *e, int32_t *out, int32_t cap, int32_t *n);
 /* RolloutSample fields of request `req` (request order, server.cpp:365-374). */
 int rs_engine_response(rs_engine *e, int32_t req, int32_t *tokens, int32_t cap, int32_t *len);
+/* The tokens emitted by the LAST rs_engine_step, per active request of that step (host copy that
+   arrived with the step summary -- no device access): req[a], count[a] and
+   tokens[a * cap_per_req + 0 .. count[a]); n = active requests of that step. */
+int rs_engine_step_tokens(rs_engine *e, int32_t *req, int32_t *count, int32_t *tokens, int32_t cap_per_req,
+                          int32_t *n);
 int rs_engine_steps(rs_engine *e, int32_t req, double *logp, uint8_t *drafted, double *logq, int32_t cap, int32_t *n);
 int rs_engine_step_logprobs(rs_engine *e, int32_t req, double *out, int64_t cap, int32_t *rows);
 int rs_engine_accept_lens(rs_engine *e, int32_t req, int32_t *out, int32_t cap, int32_t *n);

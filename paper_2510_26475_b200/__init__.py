@@ -121,7 +121,7 @@ EXPORTED_SYMBOLS = [
     "rs_engine_set_capture", "rs_engine_capture_count", "rs_engine_capture_read",
     "rs_kd_weight", "rs_kd_update_tabular", "rs_mt19937_64_seed", "rs_gemm_bf16",
     "rs_model_tensor", "rs_memcpy_d2d", "rs_model_params", "rs_prof_enable", "rs_prof_reset", "rs_prof_json", "rs_set_tuning", "rs_lm_head_bf16", "rs_row_stats", "rs_kd_grad_transformer", "rs_drafter_apply_grad",
-    "rs_kd_update_transformer",
+    "rs_kd_update_transformer", "rs_engine_step_tokens",
     "rs_kd_select", "rs_kd_grad_tabular", "rs_tabular_apply_delta",
 ]
 
@@ -198,6 +198,7 @@ def lib():
             "rs_row_stats": ([vp, vp, i32, i32, dbl, vp], ctypes.c_int),
             "rs_kd_grad_transformer": ([vp, vp, vp, P(_KDSample), i32, P(dbl), vp, i32, P(dbl)], ctypes.c_int),
             "rs_drafter_apply_grad": ([vp, vp, vp, dbl, P(vp)], ctypes.c_int),
+            "rs_engine_step_tokens": ([vp, P(i32), P(i32), P(i32), i32, P(i32)], ctypes.c_int),
             "rs_kd_update_transformer": ([vp, vp, vp, P(_KDSample), i32, _KDPolicy, P(u64), dbl, P(vp),
                                           P(_KDResult)], ctypes.c_int),
             "rs_prof_json": ([ctypes.c_char_p, i64, P(i64)], ctypes.c_int),
@@ -807,6 +808,17 @@ class BatchEngine:
             full = [list(fb[k * V:(k + 1) * V]) for k in range(n)]
         toks = self._response(i)
         return [StepRecord(toks[k], lp[k], bool(dr[k]), lq[k], full[k] if full else None) for k in range(n)]
+
+    def step_tokens(self) -> dict:
+        """{request index: tokens emitted by the last step()} -- host data that arrived with the
+        step summary (no extra device round trip)."""
+        cap = 512
+        n = len(self._reqs)
+        req, cnt = (ctypes.c_int32 * n)(), (ctypes.c_int32 * n)()
+        toks = (ctypes.c_int32 * (n * cap))()
+        na = ctypes.c_int32()
+        _check(lib().rs_engine_step_tokens(self.handle, req, cnt, toks, cap, ctypes.byref(na)))
+        return {req[a]: list(toks[a * cap: a * cap + min(cnt[a], cap)]) for a in range(na.value)}
 
     def requests(self) -> List[RequestState]:
         V = self._target.vocab_size

@@ -326,6 +326,9 @@ int rs_engine_create(rs_ctx *ctx, const rs_model *target, const rs_model *drafte
         RS_CUDA(cudaMemset(e->d_flag.p, 0, 4));
         e->d_summary.alloc((size_t)N * (kSummaryFixed + 3 * kMaxRounds));
         RS_CUDA(cudaMallocHost(&e->h_summary, (size_t)N * (kSummaryFixed + 3 * kMaxRounds) * 4));
+        e->newtok_cap = kMaxRounds * e->n_max + 1;  // a cycle emits <= s * n + 1 tokens
+        e->d_newtok.alloc((size_t)N * e->newtok_cap);
+        RS_CUDA(cudaMallocHost(&e->h_newtok, (size_t)N * e->newtok_cap * 4));
         RS_CUDA(cudaMallocHost(&e->h_active, (size_t)N * 4));
         RS_CUDA(cudaMallocHost(&e->h_misc, 16));
         std::memset(e->h_misc, 0, 16);
@@ -416,6 +419,23 @@ int rs_engine_response(rs_engine *e, int32_t req, int32_t *tokens, int32_t cap, 
         const int k = std::min(gen, std::max(cap, 0));
         if (tokens && k > 0)
             RS_CUDA(cudaMemcpy(tokens, e->d_tok.p + (size_t)req * e->tok_cap + e->prompt_len[req], k * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+int rs_engine_step_tokens(rs_engine *e, int32_t *req, int32_t *count, int32_t *tokens, int32_t cap_per_req,
+                          int32_t *n) {
+    return guard([&] {
+        need(e, "rs_engine_step_tokens");
+        const int na = (int)e->last_active.size();
+        if (n) *n = na;
+        for (int a = 0; a < na; ++a) {
+            if (req) req[a] = e->last_active[a];
+            const int c = std::min(e->last_emitted[a], e->newtok_cap);
+            if (count) count[a] = c;
+            if (tokens)
+                for (int k = 0; k < std::min(c, cap_per_req); ++k)
+                    tokens[(size_t)a * cap_per_req + k] = e->h_newtok[(size_t)a * e->newtok_cap + k];
+        }
     });
 }
 

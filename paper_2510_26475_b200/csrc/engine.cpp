@@ -166,6 +166,7 @@ using namespace rs;
 
 rs_engine::~rs_engine() {
     if (h_summary) cudaFreeHost(h_summary);
+    if (h_newtok) cudaFreeHost(h_newtok);
     if (h_active) cudaFreeHost(h_active);
     if (h_misc) cudaFreeHost(h_misc);
 }
@@ -228,6 +229,8 @@ SdDev rs_engine::dev(const rs_sdconfig &cfg, int nact) {
     d.err = d_err.p;
     d.flag = d_flag.p;
     d.summary = d_summary.p;
+    d.newtok = d_newtok.n ? d_newtok.p : nullptr;
+    d.newtok_cap = newtok_cap;
     return d;
 }
 
@@ -326,9 +329,43 @@ void rs_engine::step(rs_step_info *info) {
     sd_cycle_begin(d, st);
     const RowType rt = pair->row_type();
     int redraft_passes = 0;
-    if (mode.enabled) {
+    // Single-round cycles run OPTIMISTICALLY with no host synchronisation inside the step: the
+    // redraft check (EOS-shortened chain -> later chains' draft-stream offsets move) only raises a
+    // device flag that turns acceptance and the cycle end into no-ops; the flag is read back
+    // with the step summary and, in that rare case, the cycle is redone synchronously below.
+    const bool optimistic = mode.enabled && mode.rounds == 1 && verify_mode != RS_VERIFY_GREEDY &&
+                            mode.branching > 1 && !capture;
+    bool redo = false;
+    if (optimistic) {
+        sd_round_setup(d, 0, st);
+        for (int depth = 0; depth < mode.draft_len; ++depth) {
+            prof_set_scope("draft");
+            pair->draft_rows(d, depth, st);
+            sd_draft_sample(d, depth, rt, st);
+        }
+        sd_redraft_check(d, st);
+        prof_set_scope("verify");
+        pair->verify_rows(d, false, st);
+        prof_set_scope("accept");
+        sd_accept(d, 0, false, rt, st);
+        pair->after_accept(d, false, st);
+        sd_cycle_end(d, false, st);
+        RS_CUDA(cudaEventRecord(ctx->ev1, st));
+        RS_CUDA(cudaMemcpyAsync(h_misc + 1, d_flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        note_copy(false, sizeof(int32_t));
+        RS_CUDA(cudaStreamSynchronize(st));
+        redo = h_misc[1] != 0;
+        if (redo) {
+            RS_CUDA(cudaMemsetAsync(d_flag.p, 0, sizeof(int32_t), st));
+            ++redraft_passes;
+        }
+    }
+    if (optimistic && !redo) {
+        // done: summary below
+    } else if (mode.enabled) {
         for (int round = 0; round < mode.rounds; ++round) {
-            sd_round_setup(d, round, st);
+            if (!redo) sd_round_setup(d, round, st);  // a redo keeps the corrected offsets
+            redo = false;
             for (;;) {
                 for (int depth = 0; depth < mode.draft_len; ++depth) {
                     prof_set_scope("draft");
@@ -371,10 +408,17 @@ void rs_engine::step(rs_step_info *info) {
         sd_accept(d, 0, true, rt, st);
         pair->after_accept(d, true, st);
     }
-    sd_cycle_end(d, !mode.enabled, st);
-    RS_CUDA(cudaEventRecord(ctx->ev1, st));
+    if (!(optimistic && !redo && redraft_passes == 0)) {
+        sd_cycle_end(d, !mode.enabled, st);
+        RS_CUDA(cudaEventRecord(ctx->ev1, st));
+    }
     const int sw = kSummaryFixed + 3 * kMaxRounds;
     RS_CUDA(cudaMemcpyAsync(h_summary, d_summary.p, (size_t)batch * sw * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    if (h_newtok) {  // this cycle's tokens ride along with the summary (one synchronisation)
+        RS_CUDA(cudaMemcpyAsync(h_newtok, d_newtok.p, (size_t)batch * newtok_cap * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, st));
+        note_copy(false, (size_t)batch * newtok_cap * sizeof(int32_t));
+    }
     RS_CUDA(cudaMemcpyAsync(h_misc, d_err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     note_copy(false, (size_t)batch * sw * sizeof(int32_t) + sizeof(int32_t));
     RS_CUDA(cudaStreamSynchronize(st));
@@ -391,9 +435,12 @@ void rs_engine::step(rs_step_info *info) {
     int emitted = 0, drafted_cycles = 0, accepted = 0;
     size_t max_rounds = 0;
     for (int a = 0; a < batch; ++a) max_rounds = std::max<size_t>(max_rounds, h_summary[a * sw + 4]);
+    last_active.assign(active.begin(), active.begin() + batch);
+    last_emitted.assign(batch, 0);
     for (int a = 0; a < batch; ++a) {
         const int32_t *s = h_summary + a * sw;
         const int r = active[a];
+        last_emitted[a] = s[1];
         done[r] = s[0];
         len[r] = s[5];
         emitted += s[1];

@@ -166,7 +166,10 @@ struct rs_engine {
     rs::DBuf<uint8_t> d_st_drafted;
     rs::DBuf<int32_t> d_cyc;  // n_eff, d_used, a_used, cont, ended, accept_len, drafted, emitted, n_rounds
     rs::DBuf<int32_t> d_round_cost, d_chain;  // chain_tok, chain_len, chain_stop, chain_off
-    rs::DBuf<int32_t> d_err, d_flag, d_summary;
+    rs::DBuf<int32_t> d_err, d_flag, d_summary, d_newtok;
+    int32_t *h_newtok = nullptr;   // pinned [B][newtok_cap]: last step's emitted tokens per active slot
+    int newtok_cap = 0;
+    std::vector<int32_t> last_active, last_emitted;  // active slots of the last step and their counts
     rs::DBuf<char> d_P, d_Q;
     rs::DBuf<double> d_pq;          // acceptance scratch: fp64 p1 / q1 rows per active sequence
     rs::DBuf<double> d_Pst, d_Qst;  // LM-head tile softmax partials (transformer engines)

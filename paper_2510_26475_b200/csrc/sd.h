@@ -60,6 +60,8 @@ struct SdDev {
     int32_t *err;            // device error word (first error wins)
     int32_t *flag;           // redraft flag
     int32_t *summary;        // [nact][kSummaryFixed + 3*kMaxRounds]
+    int32_t *newtok;         // [nact][newtok_cap] tokens emitted by this cycle (returned with the summary)
+    int32_t newtok_cap;
 };
 
 enum class RowType { F64, F32 };

@@ -606,6 +606,9 @@ template <class T>
 __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int naive) {
     pdl_trigger();
     pdl_wait();
+    // an EOS-shortened chain shifted the draft-stream offsets of later chains: this optimistic
+    // pass is void (no state change); the host redrafts with the corrected offsets and reruns
+    if (*d.flag) return;
     __shared__ double red[32];
     __shared__ long long redl[32];
     __shared__ double Z[kMaxBranch];
@@ -840,6 +843,7 @@ done:
 __global__ void cycle_end_kernel(SdDev d, int naive) {
     pdl_trigger();
     pdl_wait();
+    if (*d.flag) return;  // void optimistic pass (see accept_kernel)
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= d.nact) return;
     const int r = d.active[a];
@@ -857,6 +861,10 @@ __global__ void cycle_end_kernel(SdDev d, int naive) {
     s[5] = d.len[r];
     if (!naive)
         for (int k = 0; k < 3 * d.n_rounds[r]; ++k) s[kSummaryFixed + k] = d.round_cost[(size_t)r * kMaxRounds * 3 + k];
+    if (d.newtok) {
+        const int e = min(d.emitted[r], d.newtok_cap), l = d.len[r];
+        for (int k = 0; k < e; ++k) d.newtok[(size_t)a * d.newtok_cap + k] = d.tok[(size_t)r * d.tok_cap + l - e + k];
+    }
 }
 
 // ---- tabular model rows ------------------------------------------------------------------

@@ -200,3 +200,19 @@ def test_mode_switch_and_adaptive_table(models):
     base = run(models, rb.SDConfig.off(), verify_mode="greedy", reqs=make_requests(n=4, max_len=16))
     for r, b in zip(eng.requests(), base.requests()):
         assert r.generated == b.generated[:len(r.generated)]
+
+
+def test_step_tokens_match_responses(models):
+    """rs_engine_step_tokens (the step's tokens, returned with the summary) reassembles every
+    response exactly."""
+    tgt, drf = models
+    reqs = make_requests(n=4, max_len=12)
+    eng = rb.BatchEngine(tgt, lambda: drf, None, rb.TimingModel(), reqs, rb.SDConfig.tree(1, 3, 3), "sample",
+                         record_full_logprobs=False)
+    got = {r.id: [] for r in reqs}
+    while not eng.all_done():
+        eng.step()
+        for rid, toks in eng.step_tokens().items():
+            got[rid].extend(toks)
+    for r in eng.requests():
+        assert got[r.id] == r.generated
