@@ -47,6 +47,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--kd", type=int, default=4, help="rollouts per GPU in the online KD update leg (0 = off)")
+    p.add_argument("--tuner", action="store_true",
+                   help="dynamic SD-config tuning (cfg3): measured ProfileTable over power-of-two buckets, re-solved "
+                        "every cycle from the live batch")
     return p.parse_args()
 
 
@@ -273,8 +276,17 @@ def main():
     rng = random.Random(1000 + rank)
     reqs = [rb.RequestState(i, [rng.randrange(shape.vocab - 1) for _ in range(args.ctx)], -20.0, max_len,
                             rb.DecodeRng.from_seed(7 + rank, i)) for i in range(args.batch)]
+    table, tuner = None, None
+    if args.tuner:
+        t_prof = time.perf_counter()
+        buckets = [b for b in (1, 2, 4, 8, 16, 32, 64, 128, 256) if b <= args.batch]
+        grid = [rb.SDConfig.chain(3), rb.SDConfig.tree(1, 2, 3), rb.SDConfig.tree(1, 4, 3), cfg]
+        table = rb.profile_measured(target, drafter, buckets, grid, prompt_len=128, warmup=1, cycles=3)
+        tuner = {"profile_s": round(time.perf_counter() - t_prof, 2),
+                 "best": {b: table.best_for_bucket(b).key() for b in buckets},
+                 "grid": ["off"] + [c.key() for c in grid], "source": "measured device ms per emitted token"}
     t_pre = time.perf_counter()
-    eng = rb.BatchEngine(target, lambda: drafter, None, rb.TimingModel(), reqs, cfg, args.verify,
+    eng = rb.BatchEngine(target, lambda: drafter, table, rb.TimingModel(), reqs, cfg, args.verify,
                          record_full_logprobs=False, device=dev)
     prefill_s = time.perf_counter() - t_pre
     print(f"[bench] prefill {prefill_s:.2f} s", file=sys.stderr, flush=True)
@@ -399,6 +411,9 @@ def main():
             "e2e": {"value": round(e2e_tok / e2e_s, 1), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps)},
             "gpu_launches": launches, "clocks": clk, "breakdown_ms_per_step": breakdown, "kd_update": kd}
+    if tuner:
+        line["tuner"] = tuner
+        line["config"]["sd_config"] = "dynamic (measured ProfileTable)"
     print(json.dumps(line), flush=True)
 
 

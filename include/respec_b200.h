@@ -174,6 +174,14 @@ int rs_model_vocab(const rs_model *m, int32_t *out);
 int rs_model_destroy(rs_model *m);
 
 /* ---- ProfileTable (server.hpp:21-49, server.cpp:21-145) -------------------------------- */
+/* profile() (server.cpp:182-239) with MEASURED latency instead of ledger_time: for every bucket
+   b and config c, a wave of exactly b synthetic requests (prompt_len tokens, EOS suppressed so no
+   request finishes, as stop_at_eos = false does in the reference) runs `warmup` + `cycles` engine
+   steps with c forced; time_per_token[ib * nc + ic] = measured device ms of the `cycles` steps /
+   tokens they emitted. The caller builds the ProfileTable from it (rs_table_set_entry). */
+int rs_profile_measured(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const int32_t *buckets,
+                        int32_t nb, const rs_sdconfig *cfgs, int32_t nc, int32_t prompt_len, int32_t warmup,
+                        int32_t cycles, uint64_t seed, double *time_per_token);
 int rs_table_create(const int32_t *buckets, int32_t n, rs_table **out);
 int rs_table_set_entry(rs_table *t, int32_t bucket, rs_sdconfig cfg, double time_per_token);
 int rs_table_finalize(rs_table *t);

@@ -121,7 +121,7 @@ EXPORTED_SYMBOLS = [
     "rs_engine_set_capture", "rs_engine_capture_count", "rs_engine_capture_read",
     "rs_kd_weight", "rs_kd_update_tabular", "rs_mt19937_64_seed", "rs_gemm_bf16",
     "rs_model_tensor", "rs_memcpy_d2d", "rs_model_params", "rs_prof_enable", "rs_prof_reset", "rs_prof_json", "rs_set_tuning", "rs_lm_head_bf16", "rs_row_stats", "rs_kd_grad_transformer", "rs_drafter_apply_grad",
-    "rs_kd_update_transformer", "rs_engine_step_tokens",
+    "rs_kd_update_transformer", "rs_engine_step_tokens", "rs_profile_measured",
     "rs_kd_select", "rs_kd_grad_tabular", "rs_tabular_apply_delta",
 ]
 
@@ -199,6 +199,8 @@ def lib():
             "rs_kd_grad_transformer": ([vp, vp, vp, P(_KDSample), i32, P(dbl), vp, i32, P(dbl)], ctypes.c_int),
             "rs_drafter_apply_grad": ([vp, vp, vp, dbl, P(vp)], ctypes.c_int),
             "rs_engine_step_tokens": ([vp, P(i32), P(i32), P(i32), i32, P(i32)], ctypes.c_int),
+            "rs_profile_measured": ([vp, vp, vp, P(i32), i32, P(_SDConfig), i32, i32, i32, i32, u64, P(dbl)],
+                                    ctypes.c_int),
             "rs_kd_update_transformer": ([vp, vp, vp, P(_KDSample), i32, _KDPolicy, P(u64), dbl, P(vp),
                                           P(_KDResult)], ctypes.c_int),
             "rs_prof_json": ([ctypes.c_char_p, i64, P(i64)], ctypes.c_int),
@@ -540,6 +542,26 @@ class EagleDrafter(_NeuralModel):
         _check(lib().rs_drafter_apply_grad(self.device.handle, self.handle, ctypes.c_void_p(ptr), scale,
                                            ctypes.byref(h)))
         return EagleDrafter._wrap(h, self.target)
+
+
+def profile_measured(target, drafter, buckets: Sequence[int], configs: Sequence["SDConfig"], prompt_len: int = 128,
+                     warmup: int = 2, cycles: int = 8, seed: int = 1) -> "ProfileTable":
+    """profile() (server.cpp:182-239) from MEASURED device latency per emitted token: one wave
+    of exactly `bucket` requests per (bucket, config), `cycles` timed engine steps after
+    `warmup`. The non-spec entry is always measured (finalize requires it)."""
+    cfgs = [SDConfig.off()] + [c for c in configs if c.enabled]
+    arr = (_SDConfig * len(cfgs))(*[c._c() for c in cfgs])
+    out = (ctypes.c_double * (len(buckets) * len(cfgs)))()
+    dev = target.device
+    _check(lib().rs_profile_measured(dev.handle, target.handle, drafter.handle if drafter else None,
+                                     _i32arr(buckets), len(buckets), arr, len(cfgs), prompt_len, warmup, cycles,
+                                     seed & (2 ** 64 - 1), out))
+    table = ProfileTable(buckets)
+    for ib, b in enumerate(buckets):
+        for ic, c in enumerate(cfgs):
+            table.set_entry(b, c, out[ib * len(cfgs) + ic])
+    table.finalize()
+    return table
 
 
 # ---- ProfileTable (server.hpp:21-49) ------------------------------------------------------------------

@@ -422,6 +422,65 @@ int rs_engine_response(rs_engine *e, int32_t req, int32_t *tokens, int32_t cap, 
     });
 }
 
+int rs_profile_measured(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const int32_t *buckets,
+                        int32_t nb, const rs_sdconfig *cfgs, int32_t nc, int32_t prompt_len, int32_t warmup,
+                        int32_t cycles, uint64_t seed, double *tpt) {
+    return guard([&] {
+        need(ctx, "rs_profile_measured");
+        need(target, "rs_profile_measured: target");
+        need(tpt, "rs_profile_measured: out");
+        if (nb <= 0 || nc <= 0 || cycles <= 0 || prompt_len <= 0)
+            throw std::invalid_argument("profile: empty grid");
+        const int V = target->vocab;
+        for (int ib = 0; ib < nb; ++ib) {
+            const int b = buckets[ib];
+            if (b <= 0) throw std::invalid_argument("profile: bucket sizes must be positive");
+            // synthetic prompts (splitmix64 over [0, V-1)), the same for every config of a bucket
+            std::vector<std::vector<int32_t>> prompts(b, std::vector<int32_t>(prompt_len));
+            uint64_t x = seed * 0x9E3779B97F4A7C15ull + (uint64_t)b;
+            for (auto &p : prompts)
+                for (auto &t : p) {
+                    x += 0x9E3779B97F4A7C15ull;
+                    uint64_t z = x;
+                    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+                    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+                    t = (int32_t)((z ^ (z >> 31)) % (uint64_t)(V - 1));
+                }
+            for (int ic = 0; ic < nc; ++ic) {
+                const rs_sdconfig c = cfgs[ic];
+                if (c.enabled && !drafter) throw std::invalid_argument("profile: spec configs need a drafter");
+                const int per = c.enabled ? c.rounds * c.draft_len + 1 : 1;
+                const int max_len = (warmup + cycles) * per + 8;
+                std::vector<rs_request> reqs(b);
+                for (int i = 0; i < b; ++i)
+                    reqs[i] = {i, prompts[i].data(), prompt_len, -1e4, max_len, seed, (uint64_t)i};
+                rs_timing_model tm{{1.0, 32, 2.0}, {0.1, 32, 0.4}};
+                rs_engine *e = nullptr;
+                int rc = rs_engine_create(ctx, target, c.enabled ? drafter : nullptr, nullptr, &tm, reqs.data(), b, c,
+                                          RS_VERIFY_SAMPLE, 0, &e);
+                if (rc != RS_OK) throw std::runtime_error(std::string("profile: ") + rs_last_error());
+                double ms = 0.0;
+                long long toks = 0;
+                for (int k = 0; k < warmup + cycles; ++k) {
+                    rs_step_info info{};
+                    rc = rs_engine_step(e, &info);
+                    if (rc != RS_OK) {
+                        const std::string m = rs_last_error();
+                        rs_engine_destroy(e);
+                        throw std::runtime_error("profile: " + m);
+                    }
+                    if (k >= warmup) {
+                        ms += info.step_ms;
+                        toks += info.emitted_tokens;
+                    }
+                }
+                rs_engine_destroy(e);
+                tpt[(size_t)ib * nc + ic] = toks > 0 ? ms / (double)toks : 1e30;
+            }
+        }
+    });
+}
+
 int rs_engine_step_tokens(rs_engine *e, int32_t *req, int32_t *count, int32_t *tokens, int32_t cap_per_req,
                           int32_t *n) {
     return guard([&] {
