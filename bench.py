@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--kd", type=int, default=4, help="rollouts per GPU in the online KD update leg (0 = off)")
+    p.add_argument("--no-tuner-leg", action="store_true", help="skip the dynamic-tuning (cfg3-style) leg")
     p.add_argument("--tuner", action="store_true",
                    help="dynamic SD-config tuning (cfg3): measured ProfileTable over power-of-two buckets, re-solved "
                         "every cycle from the live batch")
@@ -197,6 +198,54 @@ def measured_peaks():
             with open(p) as f:
                 return json.load(f), "measured"
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def tuner_leg(args, rb, target, drafter, reqs, dev, stream, max_len, cfg, world, barrier):
+    """cfg3-style leg: the same rollouts with DYNAMIC SD-config tuning -- a ProfileTable measured
+    on this GPU (device ms per emitted token per power-of-two bucket and config, profile() of
+    server.cpp:182-239 with measured instead of simulated latency), re-solved every cycle from
+    the live batch (server.cpp:279). Same metric as the headline, device time, max over ranks."""
+    import torch
+    t0 = time.perf_counter()
+    buckets = [b for b in (1, 2, 4, 8, 16, 32, 64, 128, 256) if b <= args.batch]
+    grid = [rb.SDConfig.chain(3), rb.SDConfig.tree(1, 2, 3), rb.SDConfig.tree(1, 4, 3), cfg]
+    table = rb.profile_measured(target, drafter, buckets, grid, prompt_len=128, warmup=1, cycles=3)
+    prof_s = time.perf_counter() - t0
+    fresh = [rb.RequestState(r.id, list(r.prompt), r.eos_bias, max_len, rb.DecodeRng.from_seed(11, r.id))
+             for r in reqs]
+    eng = rb.BatchEngine(target, lambda: drafter, table, rb.TimingModel(), fresh, cfg, args.verify,
+                         record_full_logprobs=False, device=dev)
+    for _ in range(args.warmup):
+        eng.step()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    tokens = acc = drafted = 0
+    modes = {}
+    for _ in range(args.steps):
+        info = eng.step()
+        tokens += info.emitted_tokens
+        acc += info.accepted_drafted
+        drafted += info.drafted_cycles
+        k = rb.SDConfig._from_c(info.mode).key()
+        modes[k] = modes.get(k, 0) + 1
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        n = torch.tensor([tokens], dtype=torch.float64, device="cuda")
+        dist.all_reduce(n)
+        tokens = int(n.item())
+    return {"value": round(tokens / (ms / 1000.0), 1), "unit": "tokens/s", "ms_per_step": round(ms / args.steps, 3),
+            "mean_accept_len": round(acc / drafted, 4) if drafted else 0.0, "configs_used": modes,
+            "table_best": {b: table.best_for_bucket(b).key() for b in buckets},
+            "grid": ["off"] + [c.key() for c in grid], "profile_s": round(prof_s, 2),
+            "source": "ProfileTable of measured device ms per emitted token (this GPU)"}
 
 
 def kd_leg(args, rb, eng, drafter, rank, world, barrier):
@@ -351,6 +400,9 @@ def main():
         prof = rb.profile(enable=False)
 
     kd = kd_leg(args, rb, eng, drafter, rank, world, barrier) if args.kd > 0 else None
+    dyn = None
+    if not args.tuner and not args.no_tuner_leg:
+        dyn = tuner_leg(args, rb, target, drafter, reqs, dev, stream, max_len, cfg, world, barrier)
 
     if world > 1:
         import torch.distributed as dist
@@ -411,6 +463,8 @@ def main():
             "e2e": {"value": round(e2e_tok / e2e_s, 1), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps)},
             "gpu_launches": launches, "clocks": clk, "breakdown_ms_per_step": breakdown, "kd_update": kd}
+    if dyn:
+        line["dynamic_tuning"] = dyn
     if tuner:
         line["tuner"] = tuner
         line["config"]["sd_config"] = "dynamic (measured ProfileTable)"

@@ -7,7 +7,18 @@ namespace rs {
 
 // kEpiSwiGLU: gate/up rows interleaved per 256-row block as [128 gate, 128 up];
 // kEpiSwiGLU2: interleaved pairwise (row 2i gate_i, row 2i+1 up_i) -- the model layout.
-enum GemmEpiKind { kEpiBF16 = 0, kEpiF32 = 1, kEpiResidual = 2, kEpiSwiGLU = 3, kEpiSwiGLU2 = 4 };
+// kEpiQKVRope: QKV projection + bias, then RoPE on Q and K and the K/V cache store (SM-pair
+// kernel only; replaces the separate RoPE / KV-store kernel).
+enum GemmEpiKind { kEpiBF16 = 0, kEpiF32 = 1, kEpiResidual = 2, kEpiSwiGLU = 3, kEpiSwiGLU2 = 4, kEpiQKVRope = 5 };
+
+// Where kEpiQKVRope sends its outputs: q [T][H][hd] and the per-token K/V cache slot
+// ((layer * B + seq) * KV + kv_head) * max_ctx + phys (RowDesc of each token).
+struct QkvStore {
+    const void *rows = nullptr;  // RowDesc[T]
+    const float *rope = nullptr; // [max_ctx][hd/2][2] cos, sin
+    void *q = nullptr, *k = nullptr, *v = nullptr;
+    int H = 0, KV = 0, layer = 0, B = 0, max_ctx = 0;
+};
 
 struct GemmEpi {
     int kind = kEpiBF16;
@@ -21,6 +32,7 @@ struct GemmEpi {
     // stats[(orow * ntiles + tile) * 2] = max y, [.. + 1] = sum exp(y - max)   (fp64)
     double *stats = nullptr;
     double tau = 1.0;
+    QkvStore qkv;                // kEpiQKVRope only
 };
 
 struct GemmArgs {

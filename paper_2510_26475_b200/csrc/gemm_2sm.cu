@@ -27,6 +27,7 @@
 #include "common.cuh"
 #include "gemm.h"
 #include "launch.cuh"
+#include "model.h"
 #include "prof.h"
 #include "tc.cuh"
 
@@ -85,8 +86,8 @@ struct Cfg2 {
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStages = (180 * 1024) / kStageBytes > 8 ? 8 : (180 * 1024) / kStageBytes;
     static constexpr int kTmemCols = 2 * BT <= 128 ? 128 : 2 * BT <= 256 ? 256 : 512;
-    static constexpr int kStgBytes = 4 * 32 * 33 * 4;  // epilogue transpose blocks (4 warps)
-    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256 + kStgBytes;
+    static constexpr int kStgBytes = 32 * 132 * 4;  // epilogue transpose blocks (4 x 32 x 33 or 32 x 132 fp32)
+    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256 + kStgBytes + 256 * 16;
     // kind::f16, bf16 x bf16 -> f32, both K-major, N = BT tokens, M = 256 features (pair)
     static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BT >> 3) << 17) |
                                        (static_cast<uint32_t>(256 >> 4) << 24);
@@ -167,6 +168,8 @@ __device__ __forceinline__ void epi2_chunk(const GemmEpi &ep, uint32_t taddr, in
             *reinterpret_cast<int4 *>(static_cast<__nv_bfloat16 *>(ep.out) + (size_t)t * ep.ldo + f) =
                 *reinterpret_cast<const int4 *>(h);
         }
+    } else if constexpr (EPI == kEpiQKVRope) {
+        // handled by epi2_qkv_rope (needs the whole 128-dim head of the CTA)
     } else {  // kEpiSwiGLU2: feature rows 2i / 2i + 1 = gate_i / up_i -> 16 outputs per token
         const int sub = lane >> 1, c16 = (lane & 1) * 16;  // 2 lanes x 8 outputs per token row
         const int fo = (f0w >> 1) + (c16 >> 1);
@@ -187,6 +190,72 @@ __device__ __forceinline__ void epi2_chunk(const GemmEpi &ep, uint32_t taddr, in
     }
 }
 
+// QKV + bias + RoPE + K/V cache store for one 32-token chunk. The CTA's 128 features are one
+// head (hd = 128): the four epilogue warps stage bf16(acc + bias) of all 128 dims x 32 tokens,
+// then every thread rotates 8-dim vectors (i, i + 64 pairs, rotate-half, Qwen2) and stores 16 B
+// into q [t][head] or the K / V cache slot of the token (RowDesc::seq / phys / pos).
+__device__ __forceinline__ void epi2_qkv_rope(const GemmEpi &ep, uint32_t taddr, int head, int q_warp, int t0, int T,
+                                              float (*stg)[132], const int4 *tok, int tbase) {
+    const int lane = threadIdx.x & 31;
+    const int dim = q_warp * 32 + lane;
+    const QkvStore &s = ep.qkv;
+    const int tid = q_warp * 32 + lane;
+    const bool is_q = head < s.H, is_k = !is_q && head < s.H + s.KV;
+    // cos / sin of this thread's four 8-dim vectors first: their latency overlaps the TMEM read
+    float4 cs[4][4];
+    if (is_q || is_k) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int vi = tid + 128 * k, j = vi >> 4, g = vi & 15;
+            const int pos = t0 + j < T ? tok[t0 + j - tbase].x : 0;
+            const float4 *src = reinterpret_cast<const float4 *>(s.rope + ((size_t)pos * 64 + ((8 * g) & 63)) * 2);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) cs[k][e] = __ldg(src + e);
+        }
+    }
+    uint32_t v[32];
+    tmem_ld32(taddr, v);
+    const float b = __bfloat162float(static_cast<const __nv_bfloat16 *>(ep.bias)[head * 128 + dim]);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) stg[j][dim] = __bfloat162float(__float2bfloat16(__uint_as_float(v[j]) + b));
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int vi = tid + 128 * k, j = vi >> 4, g = vi & 15;  // token j, dims 8g .. 8g + 7
+        const int t = t0 + j;
+        if (t >= T) continue;
+        const int4 r = tok[t - tbase];  // pos, seq, phys
+        const int d0 = 8 * g;
+        float o[8];
+        if (is_q || is_k) {
+            const int i0 = d0 & 63;
+            const float *csf = reinterpret_cast<const float *>(cs[k]);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const float c = csf[2 * e], sn = csf[2 * e + 1];
+                const float x1 = stg[j][i0 + e], x2 = stg[j][i0 + 64 + e];
+                o[e] = d0 < 64 ? x1 * c - x2 * sn : x2 * c + x1 * sn;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = stg[j][d0 + e];
+        }
+        __nv_bfloat16 *dst;
+        if (is_q) {
+            dst = static_cast<__nv_bfloat16 *>(s.q) + ((size_t)t * s.H + head) * 128;
+        } else {
+            const int kvh = is_k ? head - s.H : head - s.H - s.KV;
+            const size_t off = ((((size_t)s.layer * s.B + r.y) * s.KV + kvh) * s.max_ctx + r.z) * 128;
+            dst = static_cast<__nv_bfloat16 *>(is_k ? s.k : s.v) + off;
+        }
+        __align__(16) __nv_bfloat162 h[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
+        *reinterpret_cast<int4 *>(dst + d0) = *reinterpret_cast<const int4 *>(h);
+    }
+    asm volatile("bar.sync 2, 128;" ::: "memory");  // stg is reused by the next chunk
+}
+
 // F = features (rows of W), T = tokens (rows of X). Units = (feature pair-tile, token tile, split),
 // token tiles fastest so the pairs that share a weight tile run together (one HBM read).
 template <int BT, int EPI>
@@ -204,6 +273,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
     float(*stg_all)[33] = reinterpret_cast<float(*)[33]>(smem + C::kStages * C::kStageBytes + 256);
+    int4 *tok_tab = reinterpret_cast<int4 *>(smem + C::kStages * C::kStageBytes + 256 + C::kStgBytes);  // [BT]
 
     pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -322,6 +392,17 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
             unit_coords(unit, f0, t0, kb0, kb1);
             const int split = unit % splits, tile = unit / splits;
             const int acc = it & 1;
+            if constexpr (EPI == kEpiQKVRope) {
+                // (pos, seq, phys) of the tile's tokens, staged while the MMAs still run
+                const RowDesc *rws = static_cast<const RowDesc *>(ep.qkv.rows);
+                asm volatile("bar.sync 2, 128;" ::: "memory");  // previous tile done with the table
+                for (int i = threadIdx.x - 128; i < BT; i += 128)
+                    if (t0 + i < T) {
+                        const RowDesc r = rws[t0 + i];
+                        tok_tab[i] = make_int4(r.pos, r.seq, r.phys, 0);
+                    }
+                asm volatile("bar.sync 2, 128;" ::: "memory");
+            }
             mbar_wait(&tfull[acc], (it >> 1) & 1);
             tc_fence_after();
             if (EPI == kEpiResidual && splits > 1) {
@@ -332,9 +413,16 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                 } while (v < 2 * split);  // both CTAs of the predecessor split are done
             }
             const uint32_t tb = tmem_base + acc * BT + (static_cast<uint32_t>(q * 32) << 16);
+            if constexpr (EPI == kEpiQKVRope) {
 #pragma unroll 1
-            for (int c = 0; c < BT / 32; ++c)
-                epi2_chunk<EPI>(ep, tb + c * 32, f0 + q * 32, t0 + c * 32, F, T, stg_all + q * 32);
+                for (int c = 0; c < BT / 32; ++c)
+                    epi2_qkv_rope(ep, tb + c * 32, f0 / 128, q, t0 + c * 32, T,
+                                  reinterpret_cast<float(*)[132]>(stg_all), tok_tab, t0);
+            } else {
+#pragma unroll 1
+                for (int c = 0; c < BT / 32; ++c)
+                    epi2_chunk<EPI>(ep, tb + c * 32, f0 + q * 32, t0 + c * 32, F, T, stg_all + q * 32);
+            }
             tc_fence_before();
             mbar_arrive_remote(lead_tempty + 8 * acc);
             if (EPI == kEpiResidual && splits > 1) {
@@ -439,6 +527,10 @@ void gemm2_bf16(const GemmArgs &g, cudaStream_t st) {
         case kEpiF32: by_bt(std::integral_constant<int, kEpiF32>{}); break;
         case kEpiResidual: by_bt(std::integral_constant<int, kEpiResidual>{}); break;
         case kEpiSwiGLU2: by_bt(std::integral_constant<int, kEpiSwiGLU2>{}); break;
+        case kEpiQKVRope:
+            if (g.N % 128 || !g.epi.bias) throw std::invalid_argument("gemm2: QKV+RoPE needs 128-dim heads and a bias");
+            by_bt(std::integral_constant<int, kEpiQKVRope>{});
+            break;
         default: throw std::invalid_argument("gemm2: unsupported epilogue");
     }
 }

@@ -469,6 +469,8 @@ void launch(const GemmArgs &g, cudaStream_t st) {
 
 void gemm_bf16(const GemmArgs &g, cudaStream_t st) {
     if (g.M <= 0 || g.N <= 0) return;
+    if (g.epi.kind == kEpiQKVRope && (tuning().gemm2 < 0 || g.force_1sm || !gemm2_supported(g)))
+        throw std::invalid_argument("gemm_bf16: the fused QKV+RoPE epilogue runs on the SM-pair kernel only");
     if (tuning().gemm2 >= 0 && !g.force_1sm && gemm2_supported(g)) {
         const double out_el = g.epi.kind == kEpiSwiGLU2 ? 0.5 * g.M * g.N : (double)g.M * g.N;
         const double out_b = g.epi.kind == kEpiBF16 || g.epi.kind == kEpiSwiGLU2 ? 2.0 : g.epi.kind == kEpiF32 ? 4.0 : 8.0;

@@ -127,6 +127,26 @@ GemmEpi epi_swiglu(void *out, int ldo) {
     e.ldo = ldo;
     return e;
 }
+// QKV projection + bias + RoPE + K/V cache store in one SM-pair GEMM epilogue.
+GemmEpi epi_qkv_rope(bf16 *q, const bf16 *bias, const RowDesc *rows, const float *rope, const KvCache &kv, int layer,
+                     int H) {
+    GemmEpi e;
+    e.kind = kEpiQKVRope;
+    e.bias = bias;
+    e.qkv.rows = rows;
+    e.qkv.rope = rope;
+    e.qkv.q = q;
+    e.qkv.k = kv.k;
+    e.qkv.v = kv.v;
+    e.qkv.H = H;
+    e.qkv.KV = kv.KV;
+    e.qkv.layer = layer;
+    e.qkv.B = kv.B;
+    e.qkv.max_ctx = kv.max_ctx;
+    return e;
+}
+bool fused_qkv_rope(const TfShape &s) { return tuning().gemm2 >= 0 && s.hd == 128; }
+
 GemmEpi epi_f32(float *out, int ldo, float scale, const int *row_map, double *stats = nullptr, double tau = 1.0) {
     GemmEpi e;
     e.kind = kEpiF32;
@@ -350,8 +370,13 @@ struct TransformerPair : ModelPair {
         for (int l = 0; l < s.L; ++l) {
             const LayerW &lw = tgt->layers[l];
             k_rmsnorm(w.x.p, s.d, lw.ln1, M, s.d, s.eps, w.xn.p, s.d, st);
-            gemm(w.xn.p, s.d, lw.qkv_w, M, qd, s.d, epi_bf16(w.qkv.p, qd, lw.qkv_b), st);
-            k_rope_store(w.qkv.p, w.rows.p, M, s, tgt->rope, kv_t, l, w.q.p, st);
+            if (fused_qkv_rope(s)) {
+                gemm(w.xn.p, s.d, lw.qkv_w, M, qd, s.d, epi_qkv_rope(w.q.p, lw.qkv_b, w.rows.p, tgt->rope, kv_t, l, s.H),
+                     st);
+            } else {
+                gemm(w.xn.p, s.d, lw.qkv_w, M, qd, s.d, epi_bf16(w.qkv.p, qd, lw.qkv_b), st);
+                k_rope_store(w.qkv.p, w.rows.p, M, s, tgt->rope, kv_t, l, w.q.p, st);
+            }
             if (tc_attn)
                 k_attention_tc(w.q.p, w.rows.p, w.items.p, AttnPlan{w.passes.p, w.groups.p, w.tok_grp.p}, ni, kv_t, l, s,
                                w.ao.p, st, attn_f, attn_b);
@@ -377,8 +402,13 @@ struct TransformerPair : ModelPair {
         k_embed(w.rows.p, M, d.tok, d.tok_cap, d.chain_tok, d.t_max, d.n_max, tgt->emb, s.V, s.d, w.e32.p, st);
         k_rmsnorm(w.e32.p, s.d, drf->norm_emb, M, s.d, s.eps, w.xn.p, d2, st);
         k_rmsnorm(w.x.p, s.d, drf->norm_hid, M, s.d, s.eps, w.xn.p + s.d, d2, st);
-        gemm(w.xn.p, d2, drf->layer.qkv_w, M, qd, d2, epi_bf16(w.qkv.p, qd, drf->layer.qkv_b), st);
-        k_rope_store(w.qkv.p, w.rows.p, M, drf->s, tgt->rope, kv_d, 0, w.q.p, st);
+        if (fused_qkv_rope(s)) {
+            gemm(w.xn.p, d2, drf->layer.qkv_w, M, qd, d2,
+                 epi_qkv_rope(w.q.p, drf->layer.qkv_b, w.rows.p, tgt->rope, kv_d, 0, s.H), st);
+        } else {
+            gemm(w.xn.p, d2, drf->layer.qkv_w, M, qd, d2, epi_bf16(w.qkv.p, qd, drf->layer.qkv_b), st);
+            k_rope_store(w.qkv.p, w.rows.p, M, drf->s, tgt->rope, kv_d, 0, w.q.p, st);
+        }
         k_attention(w.q.p, w.rows.p, w.items.p, ni, kv_d, 0, drf->s, w.ao.p, st,
                     prof_enabled() ? bt.attn_flops(s) : 0, prof_enabled() ? bt.attn_bytes(s) : 0);
         gemm(w.ao.p, HD, drf->layer.o_w, M, s.d, HD, epi_resid(w.x.p, s.d), st);
