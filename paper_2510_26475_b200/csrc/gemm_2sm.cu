@@ -22,6 +22,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cmath>
 #include <mutex>
 
 #include "common.cuh"
@@ -32,6 +33,8 @@
 #include "tc.cuh"
 
 namespace rs {
+
+int gemm2_splits(const GemmArgs &g);
 
 namespace {
 
@@ -464,7 +467,7 @@ void launch2(const GemmArgs &g, cudaStream_t st) {
     const CUtensorMap tx = make_tma_map_bf16(g.A, T, g.K, g.lda, BT / 2);
     const int tiles = ((F + 2 * kBM - 1) / (2 * kBM)) * ((T + BT - 1) / BT);
     const int num_k = (g.K + kBK - 1) / kBK;
-    const int splits = EPI == kEpiResidual ? std::max(1, std::min(g.splits, num_k)) : 1;
+    const int splits = EPI == kEpiResidual ? std::max(1, std::min(gemm2_splits(g), num_k)) : 1;
     int *sem = nullptr;
     if (splits > 1) {
         static thread_local int *sems = nullptr;
@@ -489,17 +492,21 @@ bool gemm2_supported(const GemmArgs &g) {
            g.epi.kind != kEpiSwiGLU;
 }
 
-// Token tile width: the widest of {256, 224, 192, 160, 128, 96, 64} that keeps the pair-tile
-// count within one wave of SM pairs, else the one with the least wave-quantised work.
-int gemm2_pick_bt(int F, int T, int sms) {
-    const int pairs = sms / 2, nf = (F + 255) / 256;
+// Token tile: the BT of {256 .. 64} with the least modelled time for the unit count of one
+// (features, tokens, splits) problem -- waves of SM pairs x k-blocks per unit x cycles per
+// k-block, where a k-block costs max(tensor time, per-SM operand traffic at ~58 B/clk) -- plus
+// a fixed charge per extra split. The result never changes a token's arithmetic (token-tile
+// invariance), only the schedule.
+int gemm2_pick_bt(int F, int T, int K, int splits, int sms) {
+    const int pairs = sms / 2, nf = (F + 255) / 256, nk = (K + 63) / 64;
     double best = 1e30;
     int bt = 256;
     for (int cand : {256, 224, 192, 160, 128, 96, 64}) {
-        const int tiles = nf * ((T + cand - 1) / cand);
-        const double waves = (double)((tiles + pairs - 1) / pairs);
-        const double cost = waves * cand * (1.0 + 0.04 * (256 - cand) / 32.0);
-        if (cost < best) {
+        const double units = (double)nf * ((T + cand - 1) / cand) * splits;
+        const double waves = std::ceil(units / pairs);
+        const double per_kb = std::max(2.12 * cand, (16384.0 + 64.0 * cand) / 58.0);
+        const double cost = waves * std::ceil((double)nk / splits) * per_kb + (splits - 1) * 2000.0;
+        if (cost < best * 0.999) {
             best = cost;
             bt = cand;
         }
@@ -507,8 +514,20 @@ int gemm2_pick_bt(int F, int T, int sms) {
     return bt;
 }
 
+// Split-K for the residual epilogue is a function of (F, K) only -- never of the token count --
+// so a token's partial-sum order, and with it its bits, does not depend on the batch it is in.
+int gemm2_splits(const GemmArgs &g) {
+    if (g.epi.kind != kEpiResidual) return 1;
+    if (g.splits > 0) return g.splits;
+    // measured on B200 (down projection, K = 11008, 1344 tokens): 3 splits at BT 224 cost more
+    // (three read-modify-write passes over the fp32 residual + ordered hand-offs) than one split
+    // at BT 160 (8.94 vs 8.45 ms/step of verify GEMMs), so the automatic choice is one split
+    return 1;
+}
+
 void gemm2_bf16(const GemmArgs &g, cudaStream_t st) {
-    const int bt = g.block_n ? g.block_n : gemm2_pick_bt(g.N, g.M, num_sms2());
+    const int splits = gemm2_splits(g);
+    const int bt = g.block_n ? g.block_n : gemm2_pick_bt(g.N, g.M, g.K, splits, num_sms2());
     auto by_bt = [&](auto tag) {
         constexpr int E = decltype(tag)::value;
         switch (bt) {

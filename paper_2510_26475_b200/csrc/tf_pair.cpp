@@ -101,6 +101,7 @@ void gemm(const void *A, int lda, const void *B, int M, int N, int K, GemmEpi ep
     g.lda = lda;
     g.ldb = K;
     g.epi = epi;
+    g.splits = 0;  // residual epilogue: split-K by (N, K) only (gemm_2sm.cu)
     // block_n auto: the tile width that best fills one wave of 148 SMs (gemm_sm100.cu)
     gemm_bf16(g, st);
 }
