@@ -261,6 +261,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < 2; ++i) {
                     if (!(ps.tiles & (1 << i))) continue;
                     if (pend[i] >= 0) issue_pv(i);
+                    // Phase offset: tile 1's first scores wait for tile 0's first softmax, so the
+                    // two softmax groups run half a period apart -- each overlaps the other
+                    // tile's MMAs instead of both contending for the MUFU at once.
+                    if (i == 1 && j == 0 && (ps.tiles & 1) && pv_n[1] == 0) mbar_wait(&p_full[0], 0);
                     const uint8_t *qt = sQ + i * kTileBytes;
                     const uint32_t d_s = tmem + i * 128;
 #pragma unroll
