@@ -18,4 +18,6 @@ timeout 600 ncu --set full --clock-control none --import-source on --nvtx --nvtx
   -o $O/accept_full python tools/profile_step.py 2 > $O/accept_full.log 2>&1; echo "ncu accept rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "verify/" -k regex:attn_tc -s 2 -c 1 \
   -o $O/attn_full python tools/profile_step.py 2 > $O/attn_full.log 2>&1; echo "ncu attn rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "verify/" -k regex:gemm -s 0 -c 4 \
+  -o $O/gemm_b256_full python tools/profile_step.py 1 1664 256 > $O/gemm_b256_full.log 2>&1; echo "ncu gemm b256 rc=$?"
 ls -la $O
