@@ -742,8 +742,6 @@ int rs_set_tuning(const char *key, int64_t value) {
             rs::tuning().fused_stats = value != 0 ? 1 : -1;
         } else if (k == "gemm2") {
             rs::tuning().gemm2 = static_cast<int>(value);
-        } else if (k == "fused_norm") {
-            rs::tuning().fused_norm = static_cast<int>(value);
         } else if (k == "pdl") {
             rs::tuning().pdl = static_cast<int>(value);
         } else {

@@ -41,7 +41,6 @@ Tuning &tuning() {
                     else if (k == "attn_trace") x.attn_trace = v;
                     else if (k == "pdl") x.pdl = v;
                     else if (k == "gemm2") x.gemm2 = v;
-                    else if (k == "fused_norm") x.fused_norm = v;
                 }
                 p = e + 1;
             }

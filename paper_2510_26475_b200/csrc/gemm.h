@@ -33,16 +33,6 @@ struct GemmEpi {
     double *stats = nullptr;
     double tau = 1.0;
     QkvStore qkv;                // kEpiQKVRope only
-    // Fused RMSNorm (SM-pair kernel). A residual epilogue (producer) may also write
-    // xb = bf16(x_new * xb_w) [M][ldo] and ss[m][f / 32] = sum of x_new^2 over 32-feature groups;
-    // a consumer of xb scales its accumulator row t by r[t] = rsqrt(sum_p ss[t][p] / (32 P) + eps)
-    // (P = ss_parts) before bias / SwiGLU / RoPE / output scale: RMSNorm(x) W^T = r (x * w) W^T.
-    void *xb_out = nullptr;
-    const float *xb_w = nullptr;
-    float *ss_out = nullptr;
-    const float *ss_in = nullptr;
-    int ss_parts = 0;
-    float eps = 1e-6f;
 };
 
 struct GemmArgs {

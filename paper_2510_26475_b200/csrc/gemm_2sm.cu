@@ -90,7 +90,7 @@ struct Cfg2 {
     static constexpr int kStages = (180 * 1024) / kStageBytes > 8 ? 8 : (180 * 1024) / kStageBytes;
     static constexpr int kTmemCols = 2 * BT <= 128 ? 128 : 2 * BT <= 256 ? 256 : 512;
     static constexpr int kStgBytes = 32 * 132 * 4;  // epilogue transpose blocks (4 x 32 x 33 or 32 x 132 fp32)
-    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256 + kStgBytes + 256 * 16 + 256 * 4;
+    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256 + kStgBytes + 256 * 16;
     // kind::f16, bf16 x bf16 -> f32, both K-major, N = BT tokens, M = 256 features (pair)
     static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BT >> 3) << 17) |
                                        (static_cast<uint32_t>(256 >> 4) << 24);
@@ -104,18 +104,13 @@ __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g));
 // C[t][f0w .. f0w + 31] is 128 B (fp32) / 64 B (bf16) / 32 B (SwiGLU, 16 outputs) contiguous.
 template <int EPI>
 __device__ __forceinline__ void epi2_chunk(const GemmEpi &ep, uint32_t taddr, int f0w, int t0, int F, int T,
-                                           float (*stg)[33], const float *rt) {
+                                           float (*stg)[33]) {
     uint32_t v[32];
     tmem_ld32(taddr, v);
     const int lane = threadIdx.x & 31;
     __syncwarp();
-    if (rt) {  // fused RMSNorm of the consumer: row scale r[t]
 #pragma unroll
-        for (int j = 0; j < 32; ++j) stg[j][lane] = __uint_as_float(v[j]) * rt[j];
-    } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) stg[j][lane] = __uint_as_float(v[j]);  // stg[token][feature]
-    }
+    for (int j = 0; j < 32; ++j) stg[j][lane] = __uint_as_float(v[j]);  // stg[token][feature]
     __syncwarp();
     if constexpr (EPI == kEpiF32 || EPI == kEpiResidual) {
         // 8 lanes x float4 per token row, 4 token rows per pass
@@ -134,41 +129,23 @@ __device__ __forceinline__ void epi2_chunk(const GemmEpi &ep, uint32_t taddr, in
                                                                      (size_t)rowo[i] * ep.ldo + f));
             }
         }
-        float4 xw = make_float4(1.f, 1.f, 1.f, 1.f);
-        if (EPI == kEpiResidual && ep.xb_out && ep.xb_w && f < F) xw = __ldg(reinterpret_cast<const float4 *>(ep.xb_w + f));
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            float ssq = 0.f;
-            if (rowo[i] >= 0) {
-                const int j = i * 4 + sub;
-                float4 o = make_float4(stg[j][c4], stg[j][c4 + 1], stg[j][c4 + 2], stg[j][c4 + 3]);
-                if (EPI == kEpiF32) {
-                    o.x *= ep.scale;
-                    o.y *= ep.scale;
-                    o.z *= ep.scale;
-                    o.w *= ep.scale;
-                } else {
-                    o.x += cur[i].x;
-                    o.y += cur[i].y;
-                    o.z += cur[i].z;
-                    o.w += cur[i].w;
-                }
-                *reinterpret_cast<float4 *>(static_cast<float *>(ep.out) + (size_t)rowo[i] * ep.ldo + f) = o;
-                if (EPI == kEpiResidual && ep.xb_out) {
-                    __align__(8) __nv_bfloat162 h[2] = {__floats2bfloat162_rn(o.x * xw.x, o.y * xw.y),
-                                                        __floats2bfloat162_rn(o.z * xw.z, o.w * xw.w)};
-                    *reinterpret_cast<uint2 *>(static_cast<__nv_bfloat16 *>(ep.xb_out) + (size_t)rowo[i] * ep.ldo + f) =
-                        *reinterpret_cast<const uint2 *>(h);
-                    ssq = ((o.x * o.x + o.y * o.y) + (o.z * o.z + o.w * o.w));
-                }
+            if (rowo[i] < 0) continue;
+            const int j = i * 4 + sub;
+            float4 o = make_float4(stg[j][c4], stg[j][c4 + 1], stg[j][c4 + 2], stg[j][c4 + 3]);
+            if (EPI == kEpiF32) {
+                o.x *= ep.scale;
+                o.y *= ep.scale;
+                o.z *= ep.scale;
+                o.w *= ep.scale;
+            } else {
+                o.x += cur[i].x;
+                o.y += cur[i].y;
+                o.z += cur[i].z;
+                o.w += cur[i].w;
             }
-            if (EPI == kEpiResidual && ep.ss_out) {
-                // sum of squares over the token row's 32 features (8 lanes x 4), fixed order
-                ssq += __shfl_xor_sync(0xffffffffu, ssq, 1);
-                ssq += __shfl_xor_sync(0xffffffffu, ssq, 2);
-                ssq += __shfl_xor_sync(0xffffffffu, ssq, 4);
-                if ((lane & 7) == 0 && rowo[i] >= 0) ep.ss_out[(size_t)rowo[i] * ep.ss_parts + (f0w >> 5)] = ssq;
-            }
+            *reinterpret_cast<float4 *>(static_cast<float *>(ep.out) + (size_t)rowo[i] * ep.ldo + f) = o;
         }
     } else if constexpr (EPI == kEpiBF16) {
         // 4 lanes x 8 bf16 per token row, 8 token rows per pass
@@ -221,7 +198,7 @@ __device__ __forceinline__ void epi2_chunk(const GemmEpi &ep, uint32_t taddr, in
 // then every thread rotates 8-dim vectors (i, i + 64 pairs, rotate-half, Qwen2) and stores 16 B
 // into q [t][head] or the K / V cache slot of the token (RowDesc::seq / phys / pos).
 __device__ __forceinline__ void epi2_qkv_rope(const GemmEpi &ep, uint32_t taddr, int head, int q_warp, int t0, int T,
-                                              float (*stg)[132], const int4 *tok, int tbase, const float *rt) {
+                                              float (*stg)[132], const int4 *tok, int tbase) {
     const int lane = threadIdx.x & 31;
     const int dim = q_warp * 32 + lane;
     const QkvStore &s = ep.qkv;
@@ -242,13 +219,8 @@ __device__ __forceinline__ void epi2_qkv_rope(const GemmEpi &ep, uint32_t taddr,
     uint32_t v[32];
     tmem_ld32(taddr, v);
     const float b = __bfloat162float(static_cast<const __nv_bfloat16 *>(ep.bias)[head * 128 + dim]);
-    if (rt) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) stg[j][dim] = __bfloat162float(__float2bfloat16(__uint_as_float(v[j]) * rt[j] + b));
-    } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) stg[j][dim] = __bfloat162float(__float2bfloat16(__uint_as_float(v[j]) + b));
-    }
+    for (int j = 0; j < 32; ++j) stg[j][dim] = __bfloat162float(__float2bfloat16(__uint_as_float(v[j]) + b));
     asm volatile("bar.sync 2, 128;" ::: "memory");
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -305,7 +277,6 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
     float(*stg_all)[33] = reinterpret_cast<float(*)[33]>(smem + C::kStages * C::kStageBytes + 256);
     int4 *tok_tab = reinterpret_cast<int4 *>(smem + C::kStages * C::kStageBytes + 256 + C::kStgBytes);  // [BT]
-    float *r_tab = reinterpret_cast<float *>(tok_tab + 256);                                             // [BT]
 
     pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -424,21 +395,6 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
             unit_coords(unit, f0, t0, kb0, kb1);
             const int split = unit % splits, tile = unit / splits;
             const int acc = it & 1;
-            if (ep.ss_in) {
-                // fused RMSNorm: r[t] of the tile's tokens, staged while the MMAs still run
-                asm volatile("bar.sync 3, 128;" ::: "memory");  // previous tile done with the table
-                for (int i = threadIdx.x - 128; i < BT; i += 128) {
-                    float r = 0.f;
-                    if (t0 + i < T) {
-                        const float *p = ep.ss_in + (size_t)(t0 + i) * ep.ss_parts;
-                        float sum = 0.f;
-                        for (int k = 0; k < ep.ss_parts; ++k) sum += p[k];
-                        r = rsqrtf(sum / (float)(32 * ep.ss_parts) + ep.eps);
-                    }
-                    r_tab[i] = r;
-                }
-                asm volatile("bar.sync 3, 128;" ::: "memory");
-            }
             if constexpr (EPI == kEpiQKVRope) {
                 // (pos, seq, phys) of the tile's tokens, staged while the MMAs still run
                 const RowDesc *rws = static_cast<const RowDesc *>(ep.qkv.rows);
@@ -464,13 +420,11 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
 #pragma unroll 1
                 for (int c = 0; c < BT / 32; ++c)
                     epi2_qkv_rope(ep, tb + c * 32, f0 / 128, q, t0 + c * 32, T,
-                                  reinterpret_cast<float(*)[132]>(stg_all), tok_tab, t0,
-                                  ep.ss_in ? r_tab + c * 32 : nullptr);
+                                  reinterpret_cast<float(*)[132]>(stg_all), tok_tab, t0);
             } else {
 #pragma unroll 1
                 for (int c = 0; c < BT / 32; ++c)
-                    epi2_chunk<EPI>(ep, tb + c * 32, f0 + q * 32, t0 + c * 32, F, T, stg_all + q * 32,
-                                    ep.ss_in ? r_tab + c * 32 : nullptr);
+                    epi2_chunk<EPI>(ep, tb + c * 32, f0 + q * 32, t0 + c * 32, F, T, stg_all + q * 32);
             }
             tc_fence_before();
             mbar_arrive_remote(lead_tempty + 8 * acc);

@@ -41,8 +41,7 @@ __global__ void rope_table_kernel(float *rope, int max_ctx, int hd, float theta)
 }
 
 __global__ void embed_kernel(const RowDesc *rows, int M, const int32_t *tok, int tok_cap, const int32_t *chain_tok,
-                             int t_max, int n_max, const bf16 *emb, int V, int d, float *x, bf16 *xb,
-                             const float *xb_w, float *ss) {
+                             int t_max, int n_max, const bf16 *emb, int V, int d, float *x) {
     pdl_trigger();
     pdl_wait();
     const int m = blockIdx.x;
@@ -62,18 +61,6 @@ __global__ void embed_kernel(const RowDesc *rows, int M, const int32_t *tok, int
                                __bfloat162float(h[7]));
         *reinterpret_cast<float4 *>(o + i) = a;
         *reinterpret_cast<float4 *>(o + i + 4) = b;
-        if (xb) {  // fused RMSNorm of the first layer (gemm.h GemmEpi::xb_out / ss_out contract)
-            const float4 wa = *reinterpret_cast<const float4 *>(xb_w + i), wb = *reinterpret_cast<const float4 *>(xb_w + i + 4);
-            __align__(16) __nv_bfloat162 hh[4] = {
-                __floats2bfloat162_rn(a.x * wa.x, a.y * wa.y), __floats2bfloat162_rn(a.z * wa.z, a.w * wa.w),
-                __floats2bfloat162_rn(b.x * wb.x, b.y * wb.y), __floats2bfloat162_rn(b.z * wb.z, b.w * wb.w)};
-            *reinterpret_cast<int4 *>(xb + (size_t)m * d + i) = *reinterpret_cast<const int4 *>(hh);
-            // 32-feature groups = 4 consecutive threads
-            float s = ((a.x * a.x + a.y * a.y) + (a.z * a.z + a.w * a.w)) + ((b.x * b.x + b.y * b.y) + (b.z * b.z + b.w * b.w));
-            s += __shfl_xor_sync(0xffffffffu, s, 1);
-            s += __shfl_xor_sync(0xffffffffu, s, 2);
-            if ((threadIdx.x & 3) == 0) ss[(size_t)m * (d / 32) + i / 32] = s;
-        }
     }
 }
 
@@ -270,12 +257,10 @@ void k_rope_table(float *rope, int max_ctx, int hd, float theta, cudaStream_t st
 }
 
 void k_embed(const RowDesc *rows, int M, const int32_t *tok, int tok_cap, const int32_t *chain_tok, int t_max,
-             int n_max, const bf16 *emb, int V, int d, float *x, cudaStream_t st, bf16 *xb, const float *xb_w,
-             float *ss) {
+             int n_max, const bf16 *emb, int V, int d, float *x, cudaStream_t st) {
     if (M <= 0) return;
     ProfScope prof("embed", 0, (double)M * d * 6.0, st);
-    if (xb && (d % 256)) throw std::invalid_argument("embed: fused norm needs d % 256 == 0");
-    launch_pdl(embed_kernel, M, 128, 0, st, rows, M, tok, tok_cap, chain_tok, t_max, n_max, emb, V, d, x, xb, xb_w, ss);
+    launch_pdl(embed_kernel, M, 128, 0, st, rows, M, tok, tok_cap, chain_tok, t_max, n_max, emb, V, d, x);
     RS_LAUNCHED();
 }
 

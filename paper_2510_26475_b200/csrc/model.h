@@ -126,11 +126,8 @@ struct KvCache {
 };
 
 // kernels (model.cu)
-// x = emb[token] (fp32); optionally the fused-RMSNorm operands of the first layer:
-// xb = bf16(x * xb_w) and ss[m][p] = sum of x^2 over features 32 p .. 32 p + 31.
 void k_embed(const RowDesc *rows, int M, const int32_t *tok, int tok_cap, const int32_t *chain_tok, int t_max,
-             int n_max, const bf16 *emb, int V, int d, float *x, cudaStream_t st, bf16 *xb = nullptr,
-             const float *xb_w = nullptr, float *ss = nullptr);
+             int n_max, const bf16 *emb, int V, int d, float *x, cudaStream_t st);
 void k_rmsnorm(const float *x, int ldx, const float *w, int M, int d, float eps, bf16 *out, int ldo, cudaStream_t st);
 void k_rmsnorm_bf16(const bf16 *x, int ldx, const float *w, int M, int d, float eps, bf16 *out, int ldo,
                     cudaStream_t st);

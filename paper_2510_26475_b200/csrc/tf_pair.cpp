@@ -65,7 +65,6 @@ struct Workspace {
     DBuf<AttnGroup> groups;
     DBuf<int16_t> tok_grp;
     DBuf<AttnPass> passes;
-    DBuf<float> ss;  // fused RMSNorm: per-token sums of x^2 over 32-feature groups [M][d / 32]
     void ensure_passes(size_t n, cudaStream_t st) {
         if (n <= passes.n) return;
         RS_CUDA(cudaStreamSynchronize(st));
@@ -88,7 +87,6 @@ struct Workspace {
         idx.alloc((size_t)2 * M);
         groups.alloc(M);
         tok_grp.alloc(M);
-        ss.alloc((size_t)M * (s.d / 32 + 1));
         passes.alloc((size_t)M * 8);
     }
 };
@@ -149,7 +147,6 @@ GemmEpi epi_qkv_rope(bf16 *q, const bf16 *bias, const RowDesc *rows, const float
     return e;
 }
 bool fused_qkv_rope(const TfShape &s) { return tuning().gemm2 >= 0 && s.hd == 128; }
-bool fused_norm(const TfShape &s) { return tuning().gemm2 >= 0 && tuning().fused_norm >= 0 && s.d % 256 == 0; }
 
 GemmEpi epi_f32(float *out, int ldo, float scale, const int *row_map, double *stats = nullptr, double tau = 1.0) {
     GemmEpi e;
@@ -369,37 +366,14 @@ struct TransformerPair : ModelPair {
                         double *stats = nullptr) {
         const int qd = s.qkv_dim(), HD = s.H * s.hd;
         const double attn_f = prof_enabled() ? bt.attn_flops(s) : 0, attn_b = prof_enabled() ? bt.attn_bytes(s) : 0;
-        // Fused RMSNorm (SM-pair GEMMs): every producer of the residual stream x (embedding, O and
-        // down epilogues) also writes xb = bf16(x * w_next) for the next norm's weight w_next and
-        // per-32-feature sums of x^2; the consuming GEMM scales its accumulator rows by
-        // r = rsqrt(mean(x^2) + eps). No separate RMSNorm pass over x.
-        const bool fn = fused_norm(s);
-        auto norm_in = [&](GemmEpi e) {
-            if (fn) {
-                e.ss_in = w.ss.p;
-                e.ss_parts = s.d / 32;
-                e.eps = s.eps;
-            }
-            return e;
-        };
-        auto norm_out = [&](GemmEpi e, const float *w_next) {
-            if (fn) {
-                e.xb_out = w.xn.p;
-                e.xb_w = w_next;
-                e.ss_out = w.ss.p;
-                e.ss_parts = s.d / 32;
-            }
-            return e;
-        };
-        k_embed(w.rows.p, M, d.tok, d.tok_cap, d.chain_tok, d.t_max, d.n_max, tgt->emb, s.V, s.d, w.x.p, st,
-                fn ? w.xn.p : nullptr, fn ? tgt->layers[0].ln1 : nullptr, fn ? w.ss.p : nullptr);
+        k_embed(w.rows.p, M, d.tok, d.tok_cap, d.chain_tok, d.t_max, d.n_max, tgt->emb, s.V, s.d, w.x.p, st);
         int fslot = 0;
         for (int l = 0; l < s.L; ++l) {
             const LayerW &lw = tgt->layers[l];
-            if (!fn) k_rmsnorm(w.x.p, s.d, lw.ln1, M, s.d, s.eps, w.xn.p, s.d, st);
+            k_rmsnorm(w.x.p, s.d, lw.ln1, M, s.d, s.eps, w.xn.p, s.d, st);
             if (fused_qkv_rope(s)) {
-                gemm(w.xn.p, s.d, lw.qkv_w, M, qd, s.d,
-                     norm_in(epi_qkv_rope(w.q.p, lw.qkv_b, w.rows.p, tgt->rope, kv_t, l, s.H)), st);
+                gemm(w.xn.p, s.d, lw.qkv_w, M, qd, s.d, epi_qkv_rope(w.q.p, lw.qkv_b, w.rows.p, tgt->rope, kv_t, l, s.H),
+                     st);
             } else {
                 gemm(w.xn.p, s.d, lw.qkv_w, M, qd, s.d, epi_bf16(w.qkv.p, qd, lw.qkv_b), st);
                 k_rope_store(w.qkv.p, w.rows.p, M, s, tgt->rope, kv_t, l, w.q.p, st);
@@ -408,18 +382,17 @@ struct TransformerPair : ModelPair {
                 k_attention_tc(w.q.p, w.rows.p, w.items.p, AttnPlan{w.passes.p, w.groups.p, w.tok_grp.p}, ni, kv_t, l, s,
                                w.ao.p, st, attn_f, attn_b);
             else k_attention(w.q.p, w.rows.p, w.items.p, ni, kv_t, l, s, w.ao.p, st, attn_f, attn_b);
-            gemm(w.ao.p, HD, lw.o_w, M, s.d, HD, norm_out(epi_resid(w.x.p, s.d), lw.ln2), st);
-            if (!fn) k_rmsnorm(w.x.p, s.d, lw.ln2, M, s.d, s.eps, w.xn.p, s.d, st);
-            gemm(w.xn.p, s.d, lw.gu_w, M, 2 * s.dff, s.d, norm_in(epi_swiglu(w.h.p, s.dff)), st);
-            const float *w_next = l + 1 < s.L ? tgt->layers[l + 1].ln1 : tgt->final_norm;
-            gemm(w.h.p, s.dff, lw.down_w, M, s.d, s.dff, norm_out(epi_resid(w.x.p, s.d), w_next), st);
+            gemm(w.ao.p, HD, lw.o_w, M, s.d, HD, epi_resid(w.x.p, s.d), st);
+            k_rmsnorm(w.x.p, s.d, lw.ln2, M, s.d, s.eps, w.xn.p, s.d, st);
+            gemm(w.xn.p, s.d, lw.gu_w, M, 2 * s.dff, s.d, epi_swiglu(w.h.p, s.dff), st);
+            gemm(w.h.p, s.dff, lw.down_w, M, s.d, s.dff, epi_resid(w.x.p, s.d), st);
             while (fslot < 3 && tgt->feat_layers[fslot] == l)
                 k_store_features(w.x.p, w.rows.p, M, s.d, feat.p, max_ctx, fslot++, st);
         }
         if (logits) {
-            if (!fn) k_rmsnorm(w.x.p, s.d, tgt->final_norm, M, s.d, s.eps, w.xn.p, s.d, st);
-            gemm(w.xn.p, s.d, tgt->emb, M, s.V, s.d,
-                 norm_in(epi_f32(logits, s.V, s.logit_scale, use_map ? w.map_a.p : nullptr)), st);
+            k_rmsnorm(w.x.p, s.d, tgt->final_norm, M, s.d, s.eps, w.xn.p, s.d, st);
+            gemm(w.xn.p, s.d, tgt->emb, M, s.V, s.d, epi_f32(logits, s.V, s.logit_scale, use_map ? w.map_a.p : nullptr),
+                 st);
             if (stats) row_stats(logits, use_map ? w.map_a.p : nullptr, M, s.V, tgt->temperature, stats, st);
         }
     }

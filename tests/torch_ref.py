@@ -13,9 +13,8 @@ def bf(x):
 
 
 class TargetRef:
-    def __init__(self, m, fused_norm=True):
+    def __init__(self, m):
         s = m.shape
-        self.fused_norm = fused_norm
         self.s = s
         d, q = s.d_model, (s.n_heads + 2 * s.n_kv_heads) * s.head_dim
         self.emb = m.to_torch("emb").view(s.vocab, d).float()
@@ -33,14 +32,6 @@ class TargetRef:
 
     def rms(self, x, w):
         return bf(x * torch.rsqrt((x * x).mean(-1, keepdim=True) + self.s.rms_eps) * w)
-
-    def normed_matmul(self, x, w, W):
-        """RMSNorm(x; w) @ W^T the way the fused SM-pair GEMM computes it (gemm.h, fused
-        RMSNorm): bf16(x * w) @ W^T, then each row scaled by rsqrt(mean(x^2) + eps)."""
-        if not self.fused_norm:
-            return self.rms(x, w) @ W.t()
-        r = torch.rsqrt((x * x).mean(-1, keepdim=True) + self.s.rms_eps)
-        return (bf(x * w) @ W.t()) * r
 
     def rope(self, x, pos):
         hd = self.s.head_dim
@@ -67,15 +58,16 @@ class TargetRef:
     def layer(self, x, L, pos):
         s = self.s
         T = x.shape[0]
-        qkv = bf(self.normed_matmul(x, L["ln1"], L["qkv_w"]) + L["qkv_b"])
+        h = self.rms(x, L["ln1"])
+        qkv = bf(h @ L["qkv_w"].t() + L["qkv_b"])
         H, KV, hd = s.n_heads, s.n_kv_heads, s.head_dim
         q = self.rope(qkv[:, :H * hd].view(T, H, hd), pos)
         k = self.rope(qkv[:, H * hd:(H + KV) * hd].view(T, KV, hd), pos)
         v = qkv[:, (H + KV) * hd:].view(T, KV, hd)
         ao = self.attend(q, k, v).reshape(T, H * hd)
         x = x + ao @ L["o_w"].t()
-        mlp = bf(torch.nn.functional.silu(self.normed_matmul(x, L["ln2"], L["g_w"])) *
-                 self.normed_matmul(x, L["ln2"], L["u_w"]))
+        h2 = self.rms(x, L["ln2"])
+        mlp = bf(torch.nn.functional.silu(h2 @ L["g_w"].t()) * (h2 @ L["u_w"].t()))
         return x + mlp @ L["down_w"].t()
 
     def forward(self, tokens):
@@ -90,7 +82,7 @@ class TargetRef:
             for f in self.feat_layers:
                 if f == l:
                     feats.append(bf(x))
-        logits = self.normed_matmul(x, self.final, self.emb) * self.s.logit_scale
+        logits = (self.rms(x, self.final) @ self.emb.t()) * self.s.logit_scale
         return logits, torch.stack(feats, 1)
 
 
