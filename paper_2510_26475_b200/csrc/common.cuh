@@ -52,7 +52,8 @@ struct Tuning {
     int fused_stats = 0;
     int attn_trace = 0;
     int pdl = 0;
-    int gemm2 = 0;        // weight GEMMs on SM pairs (gemm_2sm.cu): 0 / 1 on, -1 single-SM kernel          // programmatic dependent launch on the forward path: 0 / 1 on, -1 off   // diagnostics: layer + 1 whose attention pass timeline is printed  // drafter LM-head stats: 1 fused GEMM epilogue; 0 / -1 separate row-stats kernel
+    int gemm2 = 0;
+    int gemm_trace = 0;   // diagnostics: per-launch timeline of the SM-pair GEMM (CTA 0)        // weight GEMMs on SM pairs (gemm_2sm.cu): 0 / 1 on, -1 single-SM kernel          // programmatic dependent launch on the forward path: 0 / 1 on, -1 off   // diagnostics: layer + 1 whose attention pass timeline is printed  // drafter LM-head stats: 1 fused GEMM epilogue; 0 / -1 separate row-stats kernel
 };
 Tuning &tuning();
 

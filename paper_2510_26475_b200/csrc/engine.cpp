@@ -41,6 +41,7 @@ Tuning &tuning() {
                     else if (k == "attn_trace") x.attn_trace = v;
                     else if (k == "pdl") x.pdl = v;
                     else if (k == "gemm2") x.gemm2 = v;
+                    else if (k == "gemm_trace") x.gemm_trace = v;
                 }
                 p = e + 1;
             }

@@ -23,6 +23,7 @@
 #include <cuda_bf16.h>
 
 #include <cmath>
+#include <cstdio>
 #include <mutex>
 
 #include "common.cuh"
@@ -102,9 +103,22 @@ __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g));
 // The accumulator (thread = feature row, registers = tokens) is transposed through a
 // 32 x 33 fp32 staging block so global memory is written token-row-wise with 16-byte vectors:
 // C[t][f0w .. f0w + 31] is 128 B (fp32) / 64 B (bf16) / 32 B (SwiGLU, 16 outputs) contiguous.
+// Residual rows of one 32-token chunk (same lane mapping as epi2_chunk), loaded ahead of the
+// chunk that needs them so the L2 round trip overlaps the previous chunk's work.
+__device__ __forceinline__ void resid_prefetch(const GemmEpi &ep, int f0w, int t0, int F, int T, float4 (&cur)[8]) {
+    const int lane = threadIdx.x & 31, sub = lane >> 3, f = f0w + (lane & 7) * 4;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int t = t0 + i * 4 + sub;
+        cur[i] = (t < T && f < F) ? __ldcg(reinterpret_cast<const float4 *>(static_cast<float *>(ep.out) +
+                                                                             (size_t)t * ep.ldo + f))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
 template <int EPI>
 __device__ __forceinline__ void epi2_chunk(const GemmEpi &ep, uint32_t taddr, int f0w, int t0, int F, int T,
-                                           float (*stg)[33]) {
+                                           float (*stg)[33], const float4 *pre = nullptr) {
     uint32_t v[32];
     tmem_ld32(taddr, v);
     const int lane = threadIdx.x & 31;
@@ -125,8 +139,9 @@ __device__ __forceinline__ void epi2_chunk(const GemmEpi &ep, uint32_t taddr, in
             if (t < T && f < F) {
                 rowo[i] = EPI == kEpiF32 ? (ep.row_map ? __ldg(ep.row_map + t) : t) : t;
                 if (EPI == kEpiResidual && rowo[i] >= 0)
-                    cur[i] = __ldcg(reinterpret_cast<const float4 *>(static_cast<float *>(ep.out) +
-                                                                     (size_t)rowo[i] * ep.ldo + f));
+                    cur[i] = pre ? pre[i]
+                                 : __ldcg(reinterpret_cast<const float4 *>(static_cast<float *>(ep.out) +
+                                                                           (size_t)rowo[i] * ep.ldo + f));
             }
         }
 #pragma unroll
@@ -264,7 +279,7 @@ __device__ __forceinline__ void epi2_qkv_rope(const GemmEpi &ep, uint32_t taddr,
 template <int BT, int EPI>
 __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmEpi ep, int F,
-                 int T, int K, int splits, int *sem) {
+                 int T, int K, int splits, int *sem, long long *g2trace, int g2slot) {
     using C = Cfg2<BT>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -279,6 +294,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
     int4 *tok_tab = reinterpret_cast<int4 *>(smem + C::kStages * C::kStageBytes + 256 + C::kStgBytes);  // [BT]
 
     pdl_trigger();
+    if (g2trace && blockIdx.x == 0 && threadIdx.x == 0) g2trace[g2slot * 8 + 0] = clock64();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
@@ -335,6 +351,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                 }
             }
             pdl_wait();
+            if (g2trace && blockIdx.x == 0) g2trace[g2slot * 8 + 1] = clock64();
             int stage = 0;
             uint32_t phase = 0;
             int issued = 0;
@@ -370,6 +387,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                 const uint32_t tmem_d = tmem_base + acc * BT;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
+                    if (g2trace && blockIdx.x == 0 && it == 0 && stage == 0 && phase == 0) g2trace[g2slot * 8 + 2] = clock64();
                     tc_fence_after();
                     const uint64_t ad = sw128_desc(sA + stage * C::kABytes);
                     const uint64_t bd = sw128_desc(sB + stage * C::kBBytes);
@@ -383,6 +401,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                     }
                 }
                 tc_commit2_mc(&tfull[acc]);
+                if (g2trace && blockIdx.x == 0 && it == 0) g2trace[g2slot * 8 + 3] = clock64();
             }
         }
     } else if (warp >= 4) {
@@ -407,6 +426,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                 asm volatile("bar.sync 2, 128;" ::: "memory");
             }
             mbar_wait(&tfull[acc], (it >> 1) & 1);
+            if (g2trace && blockIdx.x == 0 && threadIdx.x == 128 && it == 0) g2trace[g2slot * 8 + 4] = clock64();
             tc_fence_after();
             if (EPI == kEpiResidual && splits > 1) {
                 int v;
@@ -421,6 +441,15 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                 for (int c = 0; c < BT / 32; ++c)
                     epi2_qkv_rope(ep, tb + c * 32, f0 / 128, q, t0 + c * 32, T,
                                   reinterpret_cast<float(*)[132]>(stg_all), tok_tab, t0);
+            } else if constexpr (EPI == kEpiResidual) {
+                // software-pipelined: chunk c + 1's residual rows are in flight while chunk c is done
+                float4 cur[2][8];
+                resid_prefetch(ep, f0 + q * 32, t0, F, T, cur[0]);
+#pragma unroll
+                for (int c = 0; c < BT / 32; ++c) {
+                    if (c + 1 < BT / 32) resid_prefetch(ep, f0 + q * 32, t0 + (c + 1) * 32, F, T, cur[(c + 1) & 1]);
+                    epi2_chunk<EPI>(ep, tb + c * 32, f0 + q * 32, t0 + c * 32, F, T, stg_all + q * 32, cur[c & 1]);
+                }
             } else {
 #pragma unroll 1
                 for (int c = 0; c < BT / 32; ++c)
@@ -428,6 +457,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
             }
             tc_fence_before();
             mbar_arrive_remote(lead_tempty + 8 * acc);
+            if (g2trace && blockIdx.x == 0 && threadIdx.x == 128 && it == 0) g2trace[g2slot * 8 + 5] = clock64();
             if (EPI == kEpiResidual && splits > 1) {
                 __threadfence();
                 asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -438,6 +468,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
     tc_fence_before();
     __syncthreads();
     cluster_sync_all();  // no CTA leaves while its peer may still signal its barriers
+    if (g2trace && blockIdx.x == 0 && threadIdx.x == 128) g2trace[g2slot * 8 + 6] = clock64();
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::kTmemCols));
@@ -481,7 +512,22 @@ void launch2(const GemmArgs &g, cudaStream_t st) {
         sem = sems;
     }
     const int pairs = std::min(tiles * splits, num_sms2() / 2);
-    launch_pdl(gemm2_kernel<BT, EPI>, dim3(2 * pairs), kThr, C::kSmem, st, tw, tx, g.epi, F, T, g.K, splits, sem);
+    // diagnostics (RS_TUNE gemm_trace=1): per launch of CTA 0: start, after the dependency wait,
+    // first full stage, last MMA commit of tile 0, epilogue start / end of tile 0, exit
+    static long long *tr = nullptr;
+    static int slot = 0;
+    if (tuning().gemm_trace && !tr) RS_CUDA(cudaMalloc(&tr, 8 * 8 * 4096));
+    launch_pdl(gemm2_kernel<BT, EPI>, dim3(2 * pairs), kThr, C::kSmem, st, tw, tx, g.epi, F, T, g.K, splits, sem,
+               tuning().gemm_trace ? tr : (long long *)nullptr, slot);
+    if (tuning().gemm_trace) {
+        RS_CUDA(cudaStreamSynchronize(st));
+        long long h[8];
+        RS_CUDA(cudaMemcpy(h, tr + slot * 8, sizeof(h), cudaMemcpyDeviceToHost));
+        if (slot < 4096 && F < 20000 && T > 1000)
+            fprintf(stderr, "gemm2 F=%d T=%d K=%d BT=%d epi=%d: wait %lld full0 %lld mma_done %lld epi %lld..%lld exit %lld\n",
+                    F, T, g.K, BT, EPI, h[1] - h[0], h[2] - h[0], h[3] - h[0], h[4] - h[0], h[5] - h[0], h[6] - h[0]);
+        slot = (slot + 1) % 4096;
+    }
     RS_LAUNCHED();
 }
 
