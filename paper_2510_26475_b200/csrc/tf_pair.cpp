@@ -338,6 +338,8 @@ struct TransformerPair : ModelPair {
         kd.alloc(kvd);
         vd.alloc(kvd);
         kv_d = KvCache{kd.p, vd.p, 1, B, s.KV, max_ctx, s.hd};
+        RS_CUDA(cudaMemsetAsync(kd.p, 0, kvd * sizeof(bf16), ctx->stream));
+        RS_CUDA(cudaMemsetAsync(vd.p, 0, kvd * sizeof(bf16), ctx->stream));
         feat.alloc((size_t)B * max_ctx * 3 * s.d);
         dh.alloc((size_t)B * t_max * s.d);
         rbase.alloc(B);
@@ -410,8 +412,13 @@ struct TransformerPair : ModelPair {
             gemm(w.xn.p, d2, drf->layer.qkv_w, M, qd, d2, epi_bf16(w.qkv.p, qd, drf->layer.qkv_b), st);
             k_rope_store(w.qkv.p, w.rows.p, M, drf->s, tgt->rope, kv_d, 0, w.q.p, st);
         }
-        k_attention(w.q.p, w.rows.p, w.items.p, ni, kv_d, 0, drf->s, w.ao.p, st,
-                    prof_enabled() ? bt.attn_flops(s) : 0, prof_enabled() ? bt.attn_bytes(s) : 0);
+        if (tc_attn)
+            k_attention_tc(w.q.p, w.rows.p, w.items.p, AttnPlan{w.passes.p, w.groups.p, w.tok_grp.p}, ni, kv_d, 0,
+                           drf->s, w.ao.p, st, prof_enabled() ? bt.attn_flops(s) : 0,
+                           prof_enabled() ? bt.attn_bytes(s) : 0);
+        else
+            k_attention(w.q.p, w.rows.p, w.items.p, ni, kv_d, 0, drf->s, w.ao.p, st,
+                        prof_enabled() ? bt.attn_flops(s) : 0, prof_enabled() ? bt.attn_bytes(s) : 0);
         gemm(w.ao.p, HD, drf->layer.o_w, M, s.d, HD, epi_resid(w.x.p, s.d), st);
         k_rmsnorm(w.x.p, s.d, drf->layer.ln2, M, s.d, s.eps, w.xn.p, s.d, st);
         gemm(w.xn.p, s.d, drf->layer.gu_w, M, 2 * s.dff, s.d, epi_swiglu(w.h.p, s.dff), st);
@@ -461,7 +468,7 @@ struct TransformerPair : ModelPair {
                     }
                     const int r0 = bt.M();
                     for (int p = from; p < L; ++p) bt.rows.push_back(RowDesc{r, p, p, 0, -1, 0, 0, 0});
-                    bt.add_items(r0, bt.M(), per_item, -1, 0, 0, 0);
+                    bt.add_items(r0, bt.M(), per_item_t, -1, 0, 0, 0);
                     head_src.push_back(bt.M() - 1);
                     head_dst.push_back(a * d.slots);
                     for (int i = 0; i < d.t; ++i) {
@@ -472,7 +479,7 @@ struct TransformerPair : ModelPair {
                 }
                 bt.map_a = head_src;
                 bt.map_b = head_dst;
-                upload(bt, st);
+                upload(bt, st, tc_attn);
                 std::vector<int32_t> hid(hid_src);
                 hid.insert(hid.end(), hid_dst.begin(), hid_dst.end());
                 stage.upload(w.idx.p, hid, st);
@@ -498,9 +505,10 @@ struct TransformerPair : ModelPair {
                 bt.map_a.push_back(r * d.t_max + i);                 // hidden slot in / out
                 bt.map_b.push_back(a * d.slots + 1 + i * d.n + depth);  // Q row
             }
-            bt.add_tree_items(r0, bt.M(), s.H / s.KV, L, L, d.n);
+            if (tc_attn) bt.add_tree_items_tc(r0, bt.M(), per_item_t, L, L, d.n);
+            else bt.add_tree_items(r0, bt.M(), s.H / s.KV, L, L, d.n);
         }
-        upload(bt, st);
+        upload(bt, st, tc_attn);
         const int M = bt.M();
         k_rows_copy_f32(dh.p, s.d, w.map_a.p, w.x.p, s.d, nullptr, M, s.d, st);
         drafter_layer(d, M, (int)bt.items.size(), st);
@@ -597,14 +605,14 @@ struct TransformerPair : ModelPair {
             for (const auto &sg : segs) bt.add_items(sg.first, sg.second, per_item_t, -1, 0, 0, 0);
             upload(bt, st, tc_attn);
             target_forward(d, M, (int)bt.items.size(), Pb.p, true, st);
-            // drafter: legacy attention items over the same rows
+            // drafter: the same attention items over the same rows
             bt.items.clear();
-            for (const auto &sg : segs) bt.add_items(sg.first, sg.second, per_item, -1, 0, 0, 0);
+            for (const auto &sg : segs) bt.add_items(sg.first, sg.second, per_item_t, -1, 0, 0, 0);
             std::vector<int32_t> dst(R);
             for (int k = 0; k < R; ++k) dst[k] = k;
             bt.map_a = kd_src;
             bt.map_b = dst;
-            upload(bt, st);
+            upload(bt, st, tc_attn);
             k_gather_features(w.rows.p, M, s.d, feat.p, max_ctx, nullptr, w.fin.p, nullptr, st);
             gemm(w.fin.p, 3 * s.d, drf->fc_w, M, s.d, 3 * s.d, epi_f32(w.x.p, s.d, 1.0f, nullptr), st);
             drafter_layer(d, M, (int)bt.items.size(), st);
