@@ -394,10 +394,10 @@ def main():
 
     prof = {}
     if not args.no_profile:
-        rb.profile(enable=True, reset=True)
+        rb.device_profile(enable=True, reset=True)
         for _ in range(min(args.steps, 5)):
             eng.step()
-        prof = rb.profile(enable=False)
+        prof = rb.device_profile(enable=False)
 
     kd = kd_leg(args, rb, eng, drafter, rank, world, barrier) if args.kd > 0 else None
     dyn = None

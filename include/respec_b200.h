@@ -35,6 +35,7 @@ typedef struct rs_ctx rs_ctx;       /* one GPU + stream + scratch */
 typedef struct rs_model rs_model;   /* immutable device-resident model (tabular or transformer) */
 typedef struct rs_table rs_table;   /* ProfileTable, server.hpp:21-49 */
 typedef struct rs_engine rs_engine; /* BatchEngine, server.hpp:98-132 */
+typedef struct rs_learner rs_learner; /* OnlineLearner, learner.hpp:87-139 */
 
 /* SDConfig (specdec.hpp:17-37). enabled=0 is the non-spec configuration. */
 typedef struct {
@@ -171,7 +172,17 @@ int rs_transformer_create(rs_ctx *ctx, const rs_transformer_shape *shape, uint64
 int rs_drafter_create(rs_ctx *ctx, const rs_model *target, uint64_t seed, int32_t version, rs_model **out);
 int rs_model_version(const rs_model *m, int32_t *out);
 int rs_model_vocab(const rs_model *m, int32_t *out);
+/* Model handles are reference-counted: destroy drops one reference (the weights are freed at
+   zero), retain adds one (learner snapshots are shared between the learner and its callers). */
 int rs_model_destroy(rs_model *m);
+/* TabularARModel::random (model.cpp:102-111): scale * N(0,1) logits from std::mt19937_64(seed)
+   through std::normal_distribution (host standard library; bit-identical to the reference build). */
+int rs_tabular_random(rs_ctx *ctx, int32_t vocab, int32_t order, double temperature, double scale, uint64_t seed,
+                      rs_model **out);
+/* make_skew_requests' per-request EOS biases (scenarios.cpp:175-189): 2.5 - 2.2 * Exp(1) draws
+   from std::exponential_distribution over std::mt19937_64(seed). */
+int rs_skew_eos_biases(uint64_t seed, int32_t n, double *out);
+int rs_model_retain(rs_model *m);
 
 /* ---- ProfileTable (server.hpp:21-49, server.cpp:21-145) -------------------------------- */
 /* profile() (server.cpp:182-239) with MEASURED latency instead of ledger_time: for every bucket
@@ -182,6 +193,16 @@ int rs_model_destroy(rs_model *m);
 int rs_profile_measured(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const int32_t *buckets,
                         int32_t nb, const rs_sdconfig *cfgs, int32_t nc, int32_t prompt_len, int32_t warmup,
                         int32_t cycles, uint64_t seed, double *time_per_token);
+/* profile() (server.cpp:182-239) with the reference's SIMULATED cost model on the GPU engine:
+   configs = {off} + grid; per bucket b and config, waves of exactly b requests over a pool of
+   num_requests (prompt rid % n_prompts from the flattened `prompts` with n_prompts + 1
+   `prompt_off` offsets, DecodeRng::from_seed(seed, rid), eos_bias 0) run cycles_per_request
+   cycles with stop_at_eos = false; time_per_token[ib * (ng + 1) + ic] = ledger_time of all
+   waves' forward events / emitted tokens. */
+int rs_profile_simulated(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const rs_sdconfig *grid,
+                         int32_t ng, const int32_t *prompts, const int32_t *prompt_off, int32_t n_prompts,
+                         const rs_timing_model *tm, const int32_t *buckets, int32_t nb, int32_t cycles_per_request,
+                         int32_t num_requests, uint64_t seed, double *time_per_token);
 int rs_table_create(const int32_t *buckets, int32_t n, rs_table **out);
 int rs_table_set_entry(rs_table *t, int32_t bucket, rs_sdconfig cfg, double time_per_token);
 int rs_table_finalize(rs_table *t);
@@ -201,6 +222,9 @@ int rs_engine_create(rs_ctx *ctx, const rs_model *target, const rs_model *drafte
                      int32_t verify_mode, int32_t record_full_logprobs, rs_engine **out);
 /* DrafterSnapshotFn (server.hpp:92): the snapshot is read once, at the next step boundary. */
 int rs_engine_set_drafter(rs_engine *e, const rs_model *drafter);
+/* stop_at_eos = 0 (before the first step): EOS neither stops a drafted chain nor ends a request
+   (spec_step_tree(..., stop_at_eos = false), as profile() runs it, server.cpp:215). */
+int rs_engine_set_stop_at_eos(rs_engine *e, int32_t stop);
 /* BatchEngine::step (server.cpp:266-349); throws "BatchEngine: empty batch" when done. */
 int rs_engine_step(rs_engine *e, rs_step_info *info);
 int rs_engine_all_done(const rs_engine *e, int32_t *out);
@@ -300,6 +324,53 @@ int rs_drafter_apply_grad(rs_ctx *ctx, const rs_model *drafter, const float *gra
 int rs_kd_update_transformer(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const rs_kd_sample *buf,
                              int32_t n, rs_kd_policy policy, uint64_t *selection_rng_state, double cost,
                              rs_model **new_drafter, rs_kd_result *out);
+
+/* ---- online learner (learner.hpp:39-139, learner.cpp:84-289) ------------------------------
+   OnlineLearner over the device kd_update: feed() copies samples into a ReplayBuffer of
+   `buffer_capacity` entries (oldest dropped when full, learner.cpp:84-89); an update fires on
+   on_iteration_boundary(it) when (it + 1) % interval == 0 and the buffer is non-empty
+   (learner.cpp:184-203), consuming the whole buffer through rs_kd_update_tabular or
+   rs_kd_update_transformer (chosen by the drafter's kind). async != 0 runs updates on a worker
+   thread with its own CUDA stream, overlapping the caller's rollouts; await_pending is the
+   rendezvous (learner.cpp:205-211), and async and synchronous learners publish identical
+   snapshot sequences. A failed asynchronous update is reported by the next await_pending /
+   on_iteration_boundary / shutdown. rs_learner_snapshot returns a NEW reference (release it
+   with rs_model_destroy). */
+typedef struct {
+    int32_t update_idx;
+    int32_t drafter_version;
+    double kd_loss;
+    int32_t samples_used;
+    double weight_mean;
+    double weight_min;
+    double weight_max;
+    double weights_l2; /* L2 of the published snapshot's trained weights (tabular logits / drafter LM head) */
+} rs_learner_metric;   /* LearnerMetrics, learner.hpp:75-84 */
+int rs_learner_create(rs_ctx *ctx, const rs_model *drafter, rs_kd_policy policy, uint64_t selection_seed,
+                      double sim_cost_per_token, int64_t buffer_capacity, int32_t async, rs_learner **out);
+int rs_learner_destroy(rs_learner *l); /* shutdown (drains queued updates) + free */
+int rs_learner_feed(rs_learner *l, const rs_kd_sample *samples, int32_t n);
+int rs_learner_on_iteration_boundary(rs_learner *l, int32_t iteration);
+int rs_learner_await_pending(rs_learner *l);
+int rs_learner_shutdown(rs_learner *l);
+int rs_learner_snapshot(const rs_learner *l, rs_model **out);
+int rs_learner_drafter_version(const rs_learner *l, int32_t *out);
+int rs_learner_total_sim_time(const rs_learner *l, double *out);
+int rs_learner_buffer_size(const rs_learner *l, int64_t *out);
+int rs_learner_metrics(const rs_learner *l, rs_learner_metric *out, int32_t cap, int32_t *n);
+
+/* ---- GRPO stage (rl.hpp:12-50, rl.cpp:8-90) ---------------------------------------------
+   rs_reward          -- fraction of adjacent (golden_a, golden_b) pairs in a response (rl.cpp:8-19);
+   rs_group_advantages -- (r - mean) / (population std + 1e-6), G >= 2 (rl.cpp:21-40);
+   rs_policy_update_tabular -- new actor (version + 1) = actor + lr * sum_i A_i grad log pi(y_i)
+                       on the device; samples' target_logprobs are ignored. actor_versions (or
+                       NULL) must all equal the actor's version, else "policy_update: off-policy
+                       update" (rl.cpp:76-80). */
+int rs_reward(const int32_t *y, int32_t n, int32_t golden_a, int32_t golden_b, double *out);
+int rs_group_advantages(const double *rewards, int32_t g, double *out);
+int rs_policy_update_tabular(rs_ctx *ctx, const rs_model *actor, const rs_kd_sample *samples,
+                             const double *advantages, const int32_t *actor_versions, int32_t n, double lr,
+                             rs_model **out);
 
 #ifdef __cplusplus
 }

@@ -260,6 +260,104 @@ json op_time_generation(const json & req) {
     return {{"seconds", secs}, {"tokens", tok}, {"accept_len_sum", as}, {"accept_len_cycles", an}, {"threads", threads}};
 }
 
+RolloutSample sample_of(const json & s) {
+    RolloutSample r;
+    r.prompt = s.at("prompt").get<std::vector<int>>();
+    r.response = s.at("response").get<std::vector<int>>();
+    if (s.contains("steps"))
+        for (const auto & st : s.at("steps")) {
+            StepRecord rec;
+            rec.token = st.value("token", 0);
+            if (st.contains("target_logprobs")) rec.target_logprobs = st.at("target_logprobs").get<std::vector<double>>();
+            r.steps.push_back(std::move(rec));
+        }
+    r.eos_bias = s.value("eos_bias", 0.0);
+    r.reward = s.value("reward", 0.0);
+    r.actor_version = s.value("actor_version", 0);
+    return r;
+}
+
+KDPolicy policy_of(const json & pj) {
+    const std::string mode = pj.value("mode", "reward");
+    return KDPolicy{pj.value("interval", 1), mode == "uniform" ? WeightMode::Uniform : mode == "frozen" ? WeightMode::Frozen : WeightMode::Reward,
+                    pj.value("clip_lo", 0.0), pj.value("clip_hi", 4.0), pj.value("lr", 0.1)};
+}
+
+json learner_metrics_json(const std::vector<LearnerMetrics> & ms) {
+    json out = json::array();
+    for (const auto & m : ms)
+        out.push_back({{"update", m.update_idx}, {"drafter_version", m.drafter_version}, {"kd_loss", m.kd_loss},
+                       {"samples", m.samples_used}, {"weight_mean", m.weight_mean}, {"weight_min", m.weight_min},
+                       {"weight_max", m.weight_max}, {"weights_l2", m.weights_l2}});
+    return out;
+}
+
+// OnlineLearner driven by a script of iterations: {"feed": [samples], "boundary": it, "await": bool}.
+json op_online_learner(const json & req) {
+    OnlineLearner l(model_of(req.at("drafter")), policy_of(req.at("policy")), req.at("selection_seed").get<uint64_t>(),
+                    req.value("cost_per_token", 0.0), req.value("capacity", size_t{4096}), req.value("async", false));
+    json states = json::array();
+    for (const auto & it : req.at("script")) {
+        std::vector<RolloutSample> batch;
+        for (const auto & s : it.value("feed", json::array())) batch.push_back(sample_of(s));
+        l.feed(std::move(batch));
+        json st = {{"buffer_after_feed", l.buffer_size()}};
+        if (it.contains("boundary")) l.on_iteration_boundary(it.at("boundary").get<int>());
+        if (it.value("await", true)) l.await_pending();
+        st["version"] = l.drafter_version();
+        st["buffer"] = l.buffer_size();
+        st["updates"] = l.metrics().size();
+        states.push_back(st);
+    }
+    l.await_pending();
+    json out = {{"states", states}, {"metrics", learner_metrics_json(l.metrics())}, {"total_sim_time", l.total_sim_time()},
+                {"logits", l.snapshot()->logits()}, {"version", l.drafter_version()}};
+    l.shutdown();
+    return out;
+}
+
+json op_policy_update(const json & req) {
+    TabularARModel actor = model_of(req.at("actor"));
+    std::vector<RolloutSample> samples;
+    for (const auto & s : req.at("samples")) samples.push_back(sample_of(s));
+    std::vector<std::pair<const RolloutSample *, double>> w;
+    const auto adv = req.at("advantages").get<std::vector<double>>();
+    for (size_t i = 0; i < samples.size(); ++i) w.emplace_back(&samples[i], adv.at(i));
+    TabularARModel next = policy_update(actor, w, req.value("lr", 0.2));
+    return {{"logits", next.logits()}, {"version", next.version()}, {"objective", policy_objective(actor, w)}};
+}
+
+json op_group_advantages(const json & req) {
+    return {{"advantages", group_advantages(req.at("rewards").get<std::vector<double>>())}};
+}
+
+json op_build_profile(const json & req) {
+    ExperimentConfig cfg = ExperimentConfig::from_json(req.at("config"));
+    Env env = make_env(cfg);
+    ProfileTable t = build_profile(cfg, env.actor, env.drafter);
+    return {{"json", t.to_json()}, {"csv", t.to_csv()}};
+}
+
+json op_make_env_cfg(const json & req) {
+    ExperimentConfig cfg = ExperimentConfig::from_json(req.at("config"));
+    Env env = make_env(cfg);
+    return {{"actor", model_json(env.actor)}, {"drafter", model_json(env.drafter)}};
+}
+
+// run_scenario (scenarios.cpp:330-341) on an ExperimentConfig JSON.
+json op_run_scenario(const json & req) {
+    ExperimentConfig cfg = ExperimentConfig::from_json(req.at("config"));
+    ScenarioResult r = run_scenario(cfg);
+    json out = {{"scenario", r.scenario}, {"summary", r.summary}, {"step_lines", r.step_lines},
+                {"learner_lines", r.learner_lines}, {"switch_lines", r.switch_lines}};
+    if (r.table) out["table"] = {{"json", r.table->to_json()}, {"csv", r.table->to_csv()}};
+    return out;
+}
+
+json op_config_roundtrip(const json & req) {
+    return ExperimentConfig::from_json(req.at("config")).to_json();
+}
+
 json dispatch(const json & req) {
     const std::string op = req.at("op");
     if (op == "run_generation") return op_run_generation(req);
@@ -270,6 +368,13 @@ json dispatch(const json & req) {
     if (op == "make_step_requests") return op_make_step_requests(req);
     if (op == "reward") return op_reward(req);
     if (op == "time_generation") return op_time_generation(req);
+    if (op == "online_learner") return op_online_learner(req);
+    if (op == "policy_update") return op_policy_update(req);
+    if (op == "group_advantages") return op_group_advantages(req);
+    if (op == "build_profile") return op_build_profile(req);
+    if (op == "make_env_cfg") return op_make_env_cfg(req);
+    if (op == "run_scenario") return op_run_scenario(req);
+    if (op == "config_roundtrip") return op_config_roundtrip(req);
     if (op == "run_verify") return {{"ok", run_verify(req.value("seed", uint64_t{1})).all_pass}};
     throw std::invalid_argument("ref: unknown op " + op);
 }

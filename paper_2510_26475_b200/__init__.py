@@ -106,6 +106,12 @@ class _KDResult(ctypes.Structure):
                 ("sim_time", ctypes.c_double)]
 
 
+class _LearnerMetric(ctypes.Structure):
+    _fields_ = [("update_idx", ctypes.c_int32), ("drafter_version", ctypes.c_int32), ("kd_loss", ctypes.c_double),
+                ("samples_used", ctypes.c_int32), ("weight_mean", ctypes.c_double), ("weight_min", ctypes.c_double),
+                ("weight_max", ctypes.c_double), ("weights_l2", ctypes.c_double)]
+
+
 # Every symbol include/respec_b200.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = [
     "rs_last_error", "rs_version", "rs_launch_count", "rs_launch_count_reset",
@@ -122,7 +128,12 @@ EXPORTED_SYMBOLS = [
     "rs_kd_weight", "rs_kd_update_tabular", "rs_mt19937_64_seed", "rs_gemm_bf16",
     "rs_model_tensor", "rs_memcpy_d2d", "rs_model_params", "rs_prof_enable", "rs_prof_reset", "rs_prof_json", "rs_set_tuning", "rs_lm_head_bf16", "rs_row_stats", "rs_kd_grad_transformer", "rs_drafter_apply_grad",
     "rs_kd_update_transformer", "rs_engine_step_tokens", "rs_profile_measured",
-    "rs_kd_select", "rs_kd_grad_tabular", "rs_tabular_apply_delta",
+    "rs_kd_select", "rs_kd_grad_tabular", "rs_tabular_apply_delta", "rs_model_retain",
+    "rs_learner_create", "rs_learner_destroy", "rs_learner_feed", "rs_learner_on_iteration_boundary",
+    "rs_learner_await_pending", "rs_learner_shutdown", "rs_learner_snapshot", "rs_learner_drafter_version",
+    "rs_learner_total_sim_time", "rs_learner_buffer_size", "rs_learner_metrics",
+    "rs_reward", "rs_group_advantages", "rs_policy_update_tabular",
+    "rs_engine_set_stop_at_eos", "rs_profile_simulated", "rs_tabular_random", "rs_skew_eos_biases",
 ]
 
 _lib = None
@@ -207,6 +218,26 @@ def lib():
             "rs_kd_select": ([i32, i32, P(u64), P(i32), P(i32)], ctypes.c_int),
             "rs_kd_grad_tabular": ([vp, vp, P(_KDSample), i32, P(dbl), P(dbl), P(dbl)], ctypes.c_int),
             "rs_tabular_apply_delta": ([vp, vp, P(dbl), dbl, P(vp)], ctypes.c_int),
+            "rs_model_retain": ([vp], ctypes.c_int),
+            "rs_learner_create": ([vp, vp, _KDPolicy, u64, dbl, i64, i32, P(vp)], ctypes.c_int),
+            "rs_learner_destroy": ([vp], ctypes.c_int),
+            "rs_learner_feed": ([vp, P(_KDSample), i32], ctypes.c_int),
+            "rs_learner_on_iteration_boundary": ([vp, i32], ctypes.c_int),
+            "rs_learner_await_pending": ([vp], ctypes.c_int),
+            "rs_learner_shutdown": ([vp], ctypes.c_int),
+            "rs_learner_snapshot": ([vp, P(vp)], ctypes.c_int),
+            "rs_learner_drafter_version": ([vp, P(i32)], ctypes.c_int),
+            "rs_learner_total_sim_time": ([vp, P(dbl)], ctypes.c_int),
+            "rs_learner_buffer_size": ([vp, P(i64)], ctypes.c_int),
+            "rs_learner_metrics": ([vp, P(_LearnerMetric), i32, P(i32)], ctypes.c_int),
+            "rs_reward": ([P(i32), i32, i32, i32, P(dbl)], ctypes.c_int),
+            "rs_group_advantages": ([P(dbl), i32, P(dbl)], ctypes.c_int),
+            "rs_policy_update_tabular": ([vp, vp, P(_KDSample), P(dbl), P(i32), i32, dbl, P(vp)], ctypes.c_int),
+            "rs_engine_set_stop_at_eos": ([vp, i32], ctypes.c_int),
+            "rs_profile_simulated": ([vp, vp, vp, P(_SDConfig), i32, P(i32), P(i32), i32, P(_TimingModel), P(i32),
+                                      i32, i32, i32, u64, P(dbl)], ctypes.c_int),
+            "rs_tabular_random": ([vp, i32, i32, dbl, dbl, u64, P(vp)], ctypes.c_int),
+            "rs_skew_eos_biases": ([u64, i32, P(dbl)], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -272,7 +303,7 @@ def default_device() -> Device:
     return _default_device
 
 
-def profile(enable: Optional[bool] = None, reset: bool = False):
+def device_profile(enable: Optional[bool] = None, reset: bool = False):
     """Per-kernel-class device timings (see rs_prof_json); returns the current totals."""
     import json
     if reset:
@@ -407,6 +438,21 @@ class TabularARModel(Model):
         _check(lib().rs_tabular_create(self.device.handle, vocab, order, temperature, _f64arr(logits), version,
                                        ctypes.byref(h)))
         self.handle = h
+
+    @staticmethod
+    def random(vocab: int, order: int, temperature: float, scale: float, seed: int,
+               device: Optional[Device] = None) -> "TabularARModel":
+        """TabularARModel::random (model.cpp:102-111) with rng = std::mt19937_64(seed)."""
+        device = device or default_device()
+        h = ctypes.c_void_p()
+        _check(lib().rs_tabular_random(device.handle, vocab, order, temperature, scale, seed & (2 ** 64 - 1),
+                                       ctypes.byref(h)))
+        return TabularARModel._wrap(h, order, temperature, device)
+
+    @staticmethod
+    def zeros(vocab: int, order: int, temperature: float = 1.0, device: Optional[Device] = None) -> "TabularARModel":
+        """TabularARModel::zeros (model.cpp:97-100)."""
+        return TabularARModel(vocab, order, [0.0] * (vocab ** order * vocab), temperature, 0, device)
 
     @staticmethod
     def from_json(j: dict, device: Optional[Device] = None) -> "TabularARModel":  # model.cpp:183-191
@@ -565,6 +611,46 @@ def profile_measured(target, drafter, buckets: Sequence[int], configs: Sequence[
 
 
 # ---- ProfileTable (server.hpp:21-49) ------------------------------------------------------------------
+@dataclass
+class ProfileOptions:
+    """ProfileOptions (server.hpp:51-56)."""
+    batch_sizes: List[int] = field(default_factory=lambda: [1, 2, 4, 8, 16, 32, 64])
+    cycles_per_request: int = 64
+    num_requests: int = 64
+    seed: int = 1
+
+
+def profile(target: Model, drafter: Optional[Model], config_grid: Sequence["SDConfig"],
+            eval_prompts: Sequence[Sequence[int]], tm: "TimingModel", opts: ProfileOptions = None) -> "ProfileTable":
+    """profile() (server.cpp:182-239): the offline Solver under the SIMULATED timing model, run on
+    the GPU engine (fixed-width waves, stop_at_eos = false, one ledger per bucket x config).
+    For measured B200 latency use profile_measured()."""
+    opts = opts or ProfileOptions()
+    if not eval_prompts:
+        raise InvalidArgument("profile: no eval prompts")
+    grid = [c for c in config_grid]
+    garr = (_SDConfig * max(1, len(grid)))(*[c._c() for c in grid])
+    flat = [t for p in eval_prompts for t in p]
+    off = [0]
+    for p in eval_prompts:
+        off.append(off[-1] + len(p))
+    nc = len(grid) + 1
+    out = (ctypes.c_double * max(1, len(opts.batch_sizes) * nc))()
+    tmc = tm._c()
+    _check(lib().rs_profile_simulated(target.device.handle, target.handle, drafter.handle if drafter else None, garr,
+                                      len(grid), _i32arr(flat), _i32arr(off), len(eval_prompts), ctypes.byref(tmc),
+                                      _i32arr(opts.batch_sizes), len(opts.batch_sizes), opts.cycles_per_request,
+                                      opts.num_requests, opts.seed & (2 ** 64 - 1), out))
+    table = ProfileTable(opts.batch_sizes)
+    cfgs = [SDConfig.off()] + grid
+    for ib, b in enumerate(opts.batch_sizes):
+        for ic, c in enumerate(cfgs):
+            table.set_entry(b, c, out[ib * nc + ic])
+    table.finalize()
+    return table
+
+
+
 class ProfileTable:
     def __init__(self, buckets: Sequence[int]):
         h = ctypes.c_void_p()
@@ -944,13 +1030,18 @@ class KDUpdateResult:
     sim_time: float
 
 
-def _kd_samples(buffer: Sequence[RolloutSample], with_logprobs: bool):
+def _kd_samples(buffer: Sequence[RolloutSample], with_logprobs):
+    """ctypes rs_kd_sample array (+ the arrays it points into). with_logprobs: True (required),
+    False (omitted) or "auto" (passed when every step carries its target_logprobs row)."""
     keep = []
     arr = (_KDSample * max(1, len(buffer)))()
     for i, s in enumerate(buffer):
         p, r = _i32arr(s.prompt), _i32arr(s.response)
         lp = None
-        if with_logprobs:
+        want = with_logprobs
+        if want == "auto":
+            want = len(s.steps) == len(s.response) and all(st.target_logprobs is not None for st in s.steps)
+        if want:
             if len(s.steps) != len(s.response):
                 raise InvalidArgument("kd_loss: steps/response length mismatch")
             lp = _f64arr([x for st in s.steps for x in st.target_logprobs])
@@ -1013,3 +1104,269 @@ def kd_update(drafter, buffer: Sequence[RolloutSample], policy: KDPolicy, select
     new = TabularARModel._wrap(h, drafter.order, drafter.temperature, drafter.device)
     return KDUpdateResult(new, bool(res.updated), res.loss, res.samples_used, res.weight_mean, res.weight_min,
                           res.weight_max, res.sim_time)
+
+
+# ---- online learner (learner.hpp:39-139) -------------------------------------------------------------------
+class ReplayBuffer:
+    """ReplayBuffer (learner.hpp:39-51): FIFO of RolloutSamples, the oldest dropped when full."""
+
+    def __init__(self, capacity: int = 4096):
+        self._capacity = capacity
+        self._entries: List[RolloutSample] = []
+
+    def push(self, sample: RolloutSample) -> None:  # learner.cpp:84-89
+        if self._capacity <= 0:
+            return
+        if len(self._entries) == self._capacity:
+            self._entries.pop(0)
+        self._entries.append(sample)
+
+    def take_all(self) -> List[RolloutSample]:  # learner.cpp:91-96
+        out, self._entries = self._entries, []
+        return out
+
+    def size(self) -> int:
+        return len(self._entries)
+
+    def capacity(self) -> int:
+        return self._capacity
+
+
+@dataclass
+class LearnerMetrics:
+    """LearnerMetrics (learner.hpp:75-84)."""
+    update_idx: int
+    drafter_version: int
+    kd_loss: float
+    samples_used: int
+    weight_mean: float
+    weight_min: float
+    weight_max: float
+    weights_l2: float
+
+
+class OnlineLearner:
+    """OnlineLearner (learner.hpp:87-139) over the device kd_update (rs_learner_*).
+
+    feed() copies samples into the native replay buffer; on_iteration_boundary(it) fires an
+    update when (it + 1) % interval == 0 and consumes the whole buffer. With async_=True the
+    update runs on a native worker thread with its own CUDA stream, overlapping the caller's
+    rollouts; await_pending() is the rendezvous. Async and synchronous learners publish identical
+    snapshot sequences (learner.hpp:91-97). Works for tabular and EAGLE drafters."""
+
+    def __init__(self, drafter: Model, policy: KDPolicy, selection_seed: int, sim_cost_per_token: float,
+                 buffer_capacity: int = 4096, async_: bool = False):
+        self._proto = drafter
+        self._policy = policy
+        self.device = drafter.device
+        h = ctypes.c_void_p()
+        _check(lib().rs_learner_create(self.device.handle, drafter.handle, policy._c(),
+                                       selection_seed & (2 ** 64 - 1), sim_cost_per_token, buffer_capacity,
+                                       1 if async_ else 0, ctypes.byref(h)))
+        self.handle = h
+
+    def feed(self, samples: Sequence[RolloutSample]) -> None:
+        samples = list(samples)
+        if not samples:
+            return
+        arr, keep = _kd_samples(samples, "auto")
+        _check(lib().rs_learner_feed(self.handle, arr, len(samples)))
+
+    def on_iteration_boundary(self, iteration: int) -> None:
+        _check(lib().rs_learner_on_iteration_boundary(self.handle, iteration))
+
+    def await_pending(self) -> None:
+        _check(lib().rs_learner_await_pending(self.handle))
+
+    def shutdown(self) -> None:
+        _check(lib().rs_learner_shutdown(self.handle))
+
+    def snapshot(self) -> Model:
+        h = ctypes.c_void_p()
+        _check(lib().rs_learner_snapshot(self.handle, ctypes.byref(h)))
+        d = self._proto
+        if isinstance(d, EagleDrafter):
+            return EagleDrafter._wrap(h, d.target)
+        return TabularARModel._wrap(h, d.order, d.temperature, d.device)
+
+    def drafter_version(self) -> int:
+        v = ctypes.c_int32()
+        _check(lib().rs_learner_drafter_version(self.handle, ctypes.byref(v)))
+        return v.value
+
+    def total_sim_time(self) -> float:
+        v = ctypes.c_double()
+        _check(lib().rs_learner_total_sim_time(self.handle, ctypes.byref(v)))
+        return v.value
+
+    def buffer_size(self) -> int:
+        v = ctypes.c_int64()
+        _check(lib().rs_learner_buffer_size(self.handle, ctypes.byref(v)))
+        return v.value
+
+    def metrics(self) -> List[LearnerMetrics]:
+        n = ctypes.c_int32()
+        _check(lib().rs_learner_metrics(self.handle, None, 0, ctypes.byref(n)))
+        buf = (_LearnerMetric * max(1, n.value))()
+        _check(lib().rs_learner_metrics(self.handle, buf, n.value, ctypes.byref(n)))
+        return [LearnerMetrics(m.update_idx, m.drafter_version, m.kd_loss, m.samples_used, m.weight_mean,
+                               m.weight_min, m.weight_max, m.weights_l2) for m in buf[:n.value]]
+
+    def policy(self) -> KDPolicy:
+        return self._policy
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            lib().rs_learner_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---- GRPO stage + training loop (rl.hpp, trainer.cpp) ------------------------------------------------------
+@dataclass
+class RewardSpec:
+    golden_a: int = 1
+    golden_b: int = 2
+
+
+def reward(y: Sequence[int], spec: RewardSpec = RewardSpec()) -> float:
+    """reward (rl.cpp:8-19)."""
+    out = ctypes.c_double()
+    _check(lib().rs_reward(_i32arr(y), len(y), spec.golden_a, spec.golden_b, ctypes.byref(out)))
+    return out.value
+
+
+def group_advantages(rewards: Sequence[float]) -> List[float]:
+    """group_advantages (rl.cpp:21-40)."""
+    out = (ctypes.c_double * max(1, len(rewards)))()
+    _check(lib().rs_group_advantages(_f64arr(rewards), len(rewards), out))
+    return list(out[:len(rewards)])
+
+
+def policy_update(actor: TabularARModel, weighted: Sequence[tuple], lr: float) -> TabularARModel:
+    """policy_update (rl.cpp:74-88) on the device: weighted = [(RolloutSample, advantage)]."""
+    samples = [s for s, _ in weighted]
+    arr, keep = _kd_samples(samples, False)
+    h = ctypes.c_void_p()
+    _check(lib().rs_policy_update_tabular(actor.device.handle, actor.handle, arr, _f64arr([a for _, a in weighted]),
+                                          _i32arr([s.actor_version for s in samples]), len(samples), lr,
+                                          ctypes.byref(h)))
+    return TabularARModel._wrap(h, actor.order, actor.temperature, actor.device)
+
+
+@dataclass
+class Task:
+    """Task (rl.hpp:23-29)."""
+    prompts: List[List[int]]
+    eos_biases: List[float]
+    reward_spec: RewardSpec = field(default_factory=RewardSpec)
+    group_size: int = 8
+    max_len: int = 24
+
+
+def make_step_requests(task: Task, seed: int, step: int) -> List[RequestState]:
+    """make_step_requests (rl.cpp:92-111): G requests per prompt, stream (step << 24) | idx."""
+    if len(task.prompts) != len(task.eos_biases):
+        raise InvalidArgument("make_step_requests: prompts/eos_biases length mismatch")
+    out, idx = [], 0
+    for p, prompt in enumerate(task.prompts):
+        for _ in range(task.group_size):
+            out.append(RequestState(idx, list(prompt), task.eos_biases[p], task.max_len,
+                                    DecodeRng.from_seed(seed, (step << 24) | idx)))
+            idx += 1
+    return out
+
+
+class SDTrainMode:
+    Off, Fixed, Adaptive = 0, 1, 2
+
+
+@dataclass
+class TrainOptions:
+    """TrainOptions (rl.hpp:54-64)."""
+    steps: int = 200
+    sd: int = SDTrainMode.Off
+    fixed_cfg: SDConfig = field(default_factory=SDConfig.off)
+    table: Optional[ProfileTable] = None
+    policy_lr: float = 0.2
+    seed: int = 1
+    count_learner_time: bool = False
+
+
+@dataclass
+class StepMetrics:
+    """StepMetrics (rl.hpp:66-75)."""
+    step: int = 0
+    mean_reward: float = 0.0
+    mean_accept_len: float = 0.0
+    sim_time: float = 0.0
+    actor_version: int = 0
+    drafter_version: int = -1
+    cycles: int = 0
+    switches: int = 0
+    wall_ms: float = 0.0  # measured device time of the step's rollout
+
+
+@dataclass
+class TrainResult:
+    metrics: List[StepMetrics]
+    actor: TabularARModel
+    total_sim_time: float = 0.0
+
+
+def train_loop(actor: TabularARModel, learner: Optional[OnlineLearner], task: Task, tm: TimingModel,
+               opts: TrainOptions) -> TrainResult:
+    """train_loop (trainer.cpp:9-90): per step, rendezvous with the learner and read its snapshot
+    once, generate one group per prompt with the GPU BatchEngine, score, take one policy step on
+    the device, then hand the rollouts to the learner at the iteration boundary (async learners
+    overlap their update with the next step's rollout)."""
+    if opts.sd == SDTrainMode.Adaptive and opts.table is None:
+        raise InvalidArgument("train_loop: adaptive mode needs a profile table")
+    if opts.sd != SDTrainMode.Off and learner is None:
+        raise InvalidArgument("train_loop: spec decoding needs a drafter learner")
+    result = TrainResult([], actor, 0.0)
+    for step in range(opts.steps):
+        drafter = None
+        if learner is not None:
+            learner.await_pending()
+            drafter = learner.snapshot()
+        drafter_fn = (lambda d=drafter: d) if opts.sd != SDTrainMode.Off else None
+        forced = opts.fixed_cfg if opts.sd == SDTrainMode.Fixed else SDConfig.off()
+        table = opts.table if opts.sd == SDTrainMode.Adaptive else None
+        run = run_generation(make_step_requests(task, opts.seed, step), result.actor, drafter_fn, table, tm, forced,
+                             result.actor.version, record_full_logprobs=learner is not None)
+        G = task.group_size
+        weighted, reward_sum = [], 0.0
+        for p in range(len(task.prompts)):
+            rewards = []
+            for g in range(G):
+                smp = run.samples[p * G + g]
+                smp.reward = reward(smp.response, task.reward_spec)
+                smp.drafter_version = drafter.version if drafter is not None else -1
+                rewards.append(smp.reward)
+                reward_sum += smp.reward
+            adv = group_advantages(rewards)
+            weighted += [(run.samples[p * G + g], adv[g]) for g in range(G)]
+        next_actor = policy_update(result.actor, weighted, opts.policy_lr)
+        m = StepMetrics(step, reward_sum / len(run.samples),
+                        (sum(run.accept_lens) / len(run.accept_lens)) if run.accept_lens else 0.0, run.total_time,
+                        result.actor.version, drafter.version if drafter is not None else -1, run.cycles,
+                        len(run.switches), run.wall_ms)
+        if learner is not None:
+            before = learner.total_sim_time()
+            learner.feed(run.samples)
+            learner.on_iteration_boundary(step)
+            if opts.count_learner_time:
+                learner.await_pending()
+                m.sim_time += learner.total_sim_time() - before
+        result.total_sim_time += m.sim_time
+        result.metrics.append(m)
+        result.actor = next_actor
+    if learner is not None:
+        learner.await_pending()
+    return result

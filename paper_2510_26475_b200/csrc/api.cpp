@@ -2,10 +2,13 @@
 // internal C++ exception into the status code of the reference's exception class and
 // keeps the message in a thread-local buffer for rs_last_error().
 #include <algorithm>
+#include <memory>
+#include <random>
 #include <cstring>
 #include <stdexcept>
 #include <string>
 
+#include "abi.h"
 #include "common.cuh"
 #include "engine.h"
 #include "gemm.h"
@@ -13,42 +16,17 @@
 #include "model.h"
 #include "prof.h"
 
+namespace rs_abi {
+std::string &last_error() {
+    thread_local std::string e;
+    return e;
+}
+}  // namespace rs_abi
+
 namespace {
-thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
-
-template <class F>
-int guard(F &&f) {
-    try {
-        f();
-        return RS_OK;
-    } catch (const rs::CudaError &e) {
-        g_err = e.what();
-        return RS_ECUDA;
-    } catch (const std::bad_alloc &e) {
-        g_err = "out of memory";
-        return RS_ENOMEM;
-    } catch (const std::invalid_argument &e) {
-        g_err = e.what();
-        return RS_EINVAL;
-    } catch (const std::out_of_range &e) {
-        g_err = e.what();
-        return RS_EINVAL;
-    } catch (const std::logic_error &e) {
-        g_err = e.what();
-        return RS_ELOGIC;
-    } catch (const std::runtime_error &e) {
-        g_err = e.what();
-        return RS_ESTATE;
-    } catch (const std::exception &e) {
-        g_err = e.what();
-        return RS_ESTATE;
-    }
-}
-
-void need(const void *p, const char *what) {
-    if (!p) throw std::invalid_argument(std::string(what) + ": null pointer");
-}
+using rs_abi::guard;
+using rs_abi::need;
 
 void check_cfg(const rs_sdconfig &c) {
     if (!c.enabled) return;
@@ -83,7 +61,7 @@ using namespace rs;
 
 extern "C" {
 
-const char *rs_last_error(void) { return g_err.c_str(); }
+const char *rs_last_error(void) { return rs_abi::last_error().c_str(); }
 int rs_version(void) { return 10000; }
 int64_t rs_launch_count(void) { return g_launches; }
 void rs_launch_count_reset(void) { g_launches = 0; }
@@ -175,7 +153,15 @@ int rs_model_vocab(const rs_model *m, int32_t *out) {
     return guard([&] { need(m, "rs_model_vocab"); *out = m->vocab; });
 }
 int rs_model_destroy(rs_model *m) {
-    return guard([&] { delete m; });
+    return guard([&] {
+        if (m && m->refs.fetch_sub(1, std::memory_order_acq_rel) == 1) delete m;
+    });
+}
+int rs_model_retain(rs_model *m) {
+    return guard([&] {
+        need(m, "rs_model_retain");
+        m->refs.fetch_add(1, std::memory_order_relaxed);
+    });
 }
 
 // ---- ProfileTable ----------------------------------------------------------------------------
@@ -538,6 +524,108 @@ int rs_engine_destroy(rs_engine *e) {
     return guard([&] {
         if (e && e->ctx) cudaStreamSynchronize(e->ctx->stream);
         delete e;
+    });
+}
+
+int rs_engine_set_stop_at_eos(rs_engine *e, int32_t stop) {
+    return guard([&] {
+        need(e, "rs_engine_set_stop_at_eos");
+        if (e->cycle > 0) throw std::runtime_error("rs_engine_set_stop_at_eos: engine already stepped");
+        e->stop_at_eos = stop != 0;
+    });
+}
+
+// profile() (server.cpp:182-239) on the GPU engine with the SIMULATED cost model: per bucket and
+// config (the non-spec entry first), waves of exactly `batch` requests over a pool of
+// num_requests (prompt rid % n_prompts, DecodeRng::from_seed(seed, rid), eos_bias 0), each
+// running cycles_per_request engine cycles with stop_at_eos = false; every wave's forward
+// events are appended to one ledger, and time_per_token = ledger_time / emitted tokens.
+int rs_profile_simulated(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const rs_sdconfig *grid,
+                         int32_t ng, const int32_t *prompts, const int32_t *prompt_off, int32_t n_prompts,
+                         const rs_timing_model *tm, const int32_t *buckets, int32_t nb, int32_t cycles_per_request,
+                         int32_t num_requests, uint64_t seed, double *time_per_token) {
+    return guard([&] {
+        need(ctx, "rs_profile_simulated");
+        need(target, "rs_profile_simulated: target");
+        need(tm, "rs_profile_simulated: timing");
+        need(time_per_token, "rs_profile_simulated: out");
+        if (n_prompts <= 0) throw std::invalid_argument("profile: no eval prompts");
+        need(prompts, "rs_profile_simulated: prompts");
+        need(prompt_off, "rs_profile_simulated: prompt offsets");
+        if (nb > 0) need(buckets, "rs_profile_simulated: buckets");
+        std::vector<rs_sdconfig> cfgs{rs_sdconfig{1, 1, 1, 0}};
+        for (int i = 0; i < ng; ++i) {
+            check_cfg(grid[i]);
+            cfgs.push_back(grid[i]);
+        }
+        const int nc = (int)cfgs.size();
+        for (int ib = 0; ib < nb; ++ib) {
+            const int batch = buckets[ib];
+            if (batch < 1) throw std::invalid_argument("profile: batch sizes must be >= 1");
+            for (int ic = 0; ic < nc; ++ic) {
+                const rs_sdconfig c = cfgs[ic];
+                if (c.enabled && !drafter) throw std::invalid_argument("profile: spec configs need a drafter");
+                const int per = c.enabled ? c.rounds * c.draft_len + 1 : 1;
+                const int max_len = cycles_per_request * per + (c.enabled ? c.draft_len : 0) + 8;
+                std::vector<rs_forward_event> ledger;
+                long long tokens = 0;
+                for (int base = 0; base < num_requests; base += batch) {
+                    std::vector<rs_request> reqs(batch);
+                    for (int i = 0; i < batch; ++i) {
+                        const int rid = base + i;
+                        const int p = rid % n_prompts;
+                        reqs[i] = {i, prompts + prompt_off[p], prompt_off[p + 1] - prompt_off[p], 0.0, max_len, seed,
+                                   (uint64_t)rid};
+                    }
+                    rs_engine *e = nullptr;
+                    rs_abi::rethrow(rs_engine_create(ctx, target, c.enabled ? drafter : nullptr, nullptr, tm,
+                                                     reqs.data(), batch, c, RS_VERIFY_SAMPLE, 0, &e));
+                    std::unique_ptr<rs_engine, int (*)(rs_engine *)> hold(e, rs_engine_destroy);
+                    e->stop_at_eos = false;
+                    for (int k = 0; k < cycles_per_request; ++k) {
+                        rs_step_info info{};
+                        rs_abi::rethrow(rs_engine_step(e, &info));
+                        tokens += info.emitted_tokens;
+                    }
+                    ledger.insert(ledger.end(), e->ledger.begin(), e->ledger.end());
+                }
+                double total = 0.0;  // ledger_time (costsim.cpp:13-27) over the whole pool, in order
+                for (const auto &ev : ledger) {
+                    const rs_role_timing &t = ev.role ? tm->target : tm->drafter;
+                    total += t.latency_floor + t.unit_cost * (double)std::max(ev.batch_tokens, t.saturation_tokens);
+                }
+                time_per_token[(size_t)ib * nc + ic] = total / (double)tokens;
+            }
+        }
+    });
+}
+
+// TabularARModel::random (model.cpp:102-111): scale * N(0, 1) logits drawn with
+// std::normal_distribution from std::mt19937_64(seed) -- the host standard library's own
+// algorithms (the same libstdc++ as the reference build), so the table is bit-identical.
+int rs_tabular_random(rs_ctx *ctx, int32_t vocab, int32_t order, double temperature, double scale, uint64_t seed,
+                      rs_model **out) {
+    return guard([&] {
+        need(out, "rs_tabular_random");
+        if (vocab < 2 || order < 0) throw std::invalid_argument("TabularARModel: bad vocab/order");
+        size_t rows = 1;
+        for (int i = 0; i < order; ++i) rows *= (size_t)vocab;
+        std::vector<double> logits(rows * (size_t)vocab);
+        std::mt19937_64 rng(seed);
+        std::normal_distribution<double> gauss(0.0, 1.0);
+        for (double &z : logits) z = scale * gauss(rng);
+        rs_abi::rethrow(rs_tabular_create(ctx, vocab, order, temperature, logits.data(), 0, out));
+    });
+}
+
+// make_skew_requests' EOS hazards (scenarios.cpp:175-189): 2.5 - 2.2 * Exp(1) draws from
+// std::exponential_distribution over std::mt19937_64(seed).
+int rs_skew_eos_biases(uint64_t seed, int32_t n, double *out) {
+    return guard([&] {
+        if (n > 0) need(out, "rs_skew_eos_biases");
+        std::mt19937_64 rng(seed);
+        std::exponential_distribution<double> tail(1.0);
+        for (int i = 0; i < n; ++i) out[i] = 2.5 - 2.2 * tail(rng);
     });
 }
 

@@ -306,12 +306,12 @@ void k_attention(const bf16 *q, const RowDesc *rows, const AttnItem *items, int 
     if (n_items <= 0) return;
     ProfScope prof("attn", flops, bytes, st);
     if (s.hd != kHD) throw std::invalid_argument("attention: head_dim must be 128");
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [] {  // thread-safe one-time init (engine + learner threads)
         static_assert(sizeof(Plan) <= 4096, "plan");
         RS_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(s.hd));
     launch_pdl(attn_kernel, dim3(n_items, s.KV), kMaxWarps * 32, kSmem, st, q, rows, items, kv, layer, s.H, s.KV,
                scale_log2, out);

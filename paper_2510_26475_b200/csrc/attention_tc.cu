@@ -433,12 +433,12 @@ void k_attention_tc(const bf16 *q, const RowDesc *rows, const AttnItem *items, c
     ProfScope prof("attn", flops, bytes, st);
     if (s.hd != kHD) throw std::invalid_argument("attention: head_dim must be 128");
     if (s.H / s.KV > 128) throw std::invalid_argument("attention: GQA group too large");
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [] {  // thread-safe one-time init (engine + learner threads)
         static_assert(sizeof(Plan) + kBarBytes + 1024 + kQBytes + kStages * kStageBytes <= 232448, "smem");
         RS_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     const int total_rows = kv.layers * kv.B * kv.KV * kv.max_ctx;
     const CUtensorMap tk = make_tma_map_bf16(kv.k, total_rows, kHD, kHD, kCk);
     const CUtensorMap tv = make_tma_map_bf16(kv.v, total_rows, kHD, kHD, kCk);

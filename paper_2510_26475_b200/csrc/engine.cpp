@@ -214,7 +214,7 @@ SdDev rs_engine::dev(const rs_sdconfig &cfg, int nact) {
     d.t = cfg.enabled ? cfg.branching : 1;
     d.n = cfg.enabled ? cfg.draft_len : 1;
     d.V = V;
-    d.eos = V - 1;
+    d.eos = stop_at_eos ? V - 1 : -1;  // -1 matches no token: spec_step_tree(stop_at_eos = false)
     d.tau_p = target->temperature;
     d.tau_q = pending_drafter ? pending_drafter->temperature : target->temperature;
     d.slots = cfg.enabled ? 1 + d.t * d.n : 1;  // rows per active sequence in P / Q

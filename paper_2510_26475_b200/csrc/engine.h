@@ -2,6 +2,7 @@
 // ProfileTable / BatchEngine / run_generation (server.hpp:21-148) and drives the device
 // kernels through the launchers in sd.h (tabular) and model.h (transformer).
 #pragma once
+#include <atomic>
 
 #include <cuda_runtime.h>
 
@@ -68,6 +69,9 @@ struct rs_model {
     int vocab = 0;
     double temperature = 1.0;
     int version = 0;
+    // Handles are reference-counted: rs_model_retain adds one, rs_model_destroy drops one and
+    // frees the weights at zero (learner snapshots are shared between the learner and callers).
+    std::atomic<int> refs{1};
     explicit rs_model(Kind k) : kind(k) {}
     virtual ~rs_model() = default;
 };
@@ -139,6 +143,7 @@ struct rs_engine {
     rs_sdconfig mode{};
     int verify_mode = RS_VERIFY_SAMPLE;
     bool record_full = false;
+    bool stop_at_eos = true;  // false: EOS neither stops a chain nor ends a request (profile waves)
     bool mode_init = false;
     int cycle = 0;
     int prefill_events = 0;

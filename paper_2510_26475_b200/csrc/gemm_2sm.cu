@@ -476,23 +476,23 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
 }
 
 int num_sms2() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
+    static const int n = [] {
+        int dev = 0, v = 0;
         RS_CUDA(cudaGetDevice(&dev));
-        RS_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-    }
+        RS_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+        return v;
+    }();
     return n;
 }
 
 template <int BT, int EPI>
 void launch2(const GemmArgs &g, cudaStream_t st) {
     using C = Cfg2<BT>;
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [] {  // thread-safe one-time init (engine + learner threads)
         RS_CUDA(cudaFuncSetAttribute(gemm2_kernel<BT, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     const int F = g.N, T = g.M;
     const CUtensorMap tw = make_tma_map_bf16(g.B, F, g.K, g.ldb, kBM);
     const CUtensorMap tx = make_tma_map_bf16(g.A, T, g.K, g.lda, BT / 2);

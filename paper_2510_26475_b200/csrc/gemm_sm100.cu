@@ -425,23 +425,23 @@ CUtensorMap make_tma_map_bf16(const void *base, int rows, int cols, int ld, int 
 namespace {
 
 int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
+    static const int n = [] {
+        int dev = 0, v = 0;
         RS_CUDA(cudaGetDevice(&dev));
-        RS_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-    }
+        RS_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+        return v;
+    }();
     return n;
 }
 
 template <int BN, int EPI>
 void launch(const GemmArgs &g, cudaStream_t st) {
     using C = Cfg<BN>;
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [] {  // thread-safe one-time init (engine + learner threads)
         RS_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     const CUtensorMap ta = make_map(g.A, g.M, g.K, g.lda, BM);
     const CUtensorMap tb = make_map(g.B, g.N, g.K, g.ldb, BN);
     const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);

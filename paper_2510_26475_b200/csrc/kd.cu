@@ -55,9 +55,9 @@ __global__ void __launch_bounds__(1024, 1) kd_job_kernel(const double *table, in
     double s = 0.0;
     for (int x = threadIdx.x; x < V; x += blockDim.x) s += exp(zv(x) - m);
     s = block_sum(s, red);
-    const double *l = lp + (size_t)jb.lp_off * V;
     double kl = 0.0;
-    for (int x = threadIdx.x; x < V; x += blockDim.x) {
+    const double *l = lp ? lp + (size_t)jb.lp_off * V : nullptr;
+    for (int x = threadIdx.x; l && x < V; x += blockDim.x) {
         if (isinf(l[x])) continue;  // p = 0 contributes nothing
         const double logq = log(exp(zv(x) - m) / s);
         kl += exp(l[x]) * (l[x] - logq);
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(1024, 1) kd_job_kernel(const double *table, in
 __global__ void __launch_bounds__(1024, 1) kd_row_kernel(const double *table, double *out, int V, double tau, const Job *jobs,
                               const int *row_jobs, const int *row_ptr, const long long *rows, const double *lp,
                               const double *job_m, const double *job_s, const double *w, double neg_lr,
-                              int grad_only) {
+                              int grad_only, const int *tokens) {
     const long long row = rows[blockIdx.x];
     const double inv_tau = 1.0 / tau;
     for (int x = threadIdx.x; x < V; x += blockDim.x) {
@@ -88,6 +88,11 @@ __global__ void __launch_bounds__(1024, 1) kd_row_kernel(const double *table, do
             double y = table[row * V + x];
             if (x == V - 1) y += jb.bias;
             const double q = exp(y / tau - job_m[j]) / job_s[j];
+            if (tokens) {  // policy gradient: A * (onehot(y_t) - pi) / tau, in rl.cpp:66-72's order
+                g -= w[jb.sample] * q * inv_tau;
+                if (x == tokens[jb.seq_off + jb.ctx_len]) g += w[jb.sample] * inv_tau;
+                continue;
+            }
             const double l = lp[(size_t)jb.lp_off * V + x];
             const double p = isinf(l) ? 0.0 : exp(l);
             g += w[jb.sample] * (q - p) * inv_tau;
@@ -308,7 +313,7 @@ std::vector<int> kd_select(int n, int interval, uint64_t *sel_state) {
 // order (learner.cpp:62-82). grad_only: out = grad (rows untouched by any sample = 0);
 // else out = table + grad * scale (the SGD step, model.cpp:161-170). Returns sum_i w_i KL_i.
 double kd_core(rs_ctx *ctx, const TabularModel *drafter, const std::vector<const rs_kd_sample *> &sel,
-               const std::vector<double> &w, double *out_dev, bool grad_only, double scale) {
+               const std::vector<double> &w, double *out_dev, bool grad_only, double scale, bool policy) {
     const int V = drafter->vocab;
     cudaStream_t st = ctx->stream;
     std::vector<int32_t> tokens;
@@ -322,7 +327,10 @@ double kd_core(rs_ctx *ctx, const TabularModel *drafter, const std::vector<const
         tokens.insert(tokens.end(), s.response, s.response + s.response_len);
         for (int t = 0; t < s.response_len; ++t) {
             const int lp_off = static_cast<int>(lp.size() / V);
-            lp.insert(lp.end(), s.target_logprobs + (size_t)t * V, s.target_logprobs + (size_t)(t + 1) * V);
+            if (!policy) {
+                if (!s.target_logprobs) throw std::invalid_argument("kd_loss: target log-probabilities required");
+                lp.insert(lp.end(), s.target_logprobs + (size_t)t * V, s.target_logprobs + (size_t)(t + 1) * V);
+            }
             per_sample[i].push_back(static_cast<int>(jobs.size()));
             jobs.push_back(Job{seq_off, s.prompt_len + t, lp_off, static_cast<int>(i), s.eos_bias});
         }
@@ -340,7 +348,7 @@ double kd_core(rs_ctx *ctx, const TabularModel *drafter, const std::vector<const
     std::vector<double> kl(J);
     std::vector<long long> rows(J);
     DBuf<int32_t> d_tok(tokens.size());
-    DBuf<double> d_lp(lp.size()), d_m(J), d_s(J), d_kl(J), d_w(std::max<size_t>(w.size(), 1));
+    DBuf<double> d_lp(std::max<size_t>(lp.size(), 1)), d_m(J), d_s(J), d_kl(J), d_w(std::max<size_t>(w.size(), 1));
     DBuf<Job> d_jobs(J);
     DBuf<long long> d_row(J);
     RS_CUDA(cudaMemcpyAsync(d_tok.p, tokens.data(), tokens.size() * 4, cudaMemcpyHostToDevice, st));
@@ -349,7 +357,7 @@ double kd_core(rs_ctx *ctx, const TabularModel *drafter, const std::vector<const
     RS_CUDA(cudaMemcpyAsync(d_w.p, w.data(), w.size() * 8, cudaMemcpyHostToDevice, st));
     const int th = V <= 256 ? 32 : V <= 4096 ? 256 : 1024;
     kd_job_kernel<<<J, th, 0, st>>>(drafter->table.p, drafter->order, V, drafter->temperature, d_tok.p, d_jobs.p,
-                                    d_lp.p, d_m.p, d_s.p, d_kl.p, d_row.p);
+                                    policy ? nullptr : d_lp.p, d_m.p, d_s.p, d_kl.p, d_row.p);
     RS_LAUNCHED();
     RS_CUDA(cudaMemcpyAsync(kl.data(), d_kl.p, J * 8, cudaMemcpyDeviceToHost, st));
     RS_CUDA(cudaMemcpyAsync(rows.data(), d_row.p, J * 8, cudaMemcpyDeviceToHost, st));
@@ -371,7 +379,7 @@ double kd_core(rs_ctx *ctx, const TabularModel *drafter, const std::vector<const
     RS_CUDA(cudaMemcpyAsync(d_ur.p, urows.data(), urows.size() * 8, cudaMemcpyHostToDevice, st));
     kd_row_kernel<<<(int)urows.size(), th, 0, st>>>(drafter->table.p, out_dev, V, drafter->temperature, d_jobs.p,
                                                     d_rj.p, d_rp.p, d_ur.p, d_lp.p, d_m.p, d_s.p, d_w.p, scale,
-                                                    grad_only ? 1 : 0);
+                                                    grad_only ? 1 : 0, policy ? d_tok.p : nullptr);
     RS_LAUNCHED();
     RS_CUDA(cudaStreamSynchronize(st));
     // loss on the pre-update drafter: sum_i w_i * sum_t KL_t (learner.cpp:142-145)
@@ -437,6 +445,53 @@ void kd_update_tabular(rs_ctx *ctx, const TabularModel *drafter, const rs_kd_sam
     res.sim_time = cost * static_cast<double>(distilled);
     *out_model = m.release();
     if (out) *out = res;
+}
+
+namespace {
+// Deterministic sum of squares: a fixed grid of CTAs each reduces a fixed strided slice, then
+// one CTA adds the partials in index order (same bits run to run, independent of timing).
+constexpr int kL2Blocks = 1184;
+__global__ void __launch_bounds__(256) sumsq_partial_kernel(const bf16 *w, size_t n, double *part) {
+    __shared__ double red[32];
+    double s = 0.0;
+    const size_t n8 = n / 8;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (size_t)gridDim.x * blockDim.x) {
+        const uint4 u = *reinterpret_cast<const uint4 *>(w + i * 8);
+        const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float2 f = __bfloat1622float2(h[j]);
+            s += (double)f.x * f.x;
+            s += (double)f.y * f.y;
+        }
+    }
+    if (blockIdx.x == 0)
+        for (size_t i = n8 * 8 + threadIdx.x; i < n; i += blockDim.x) {
+            const double v = __bfloat162float(w[i]);
+            s += v * v;
+        }
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+__global__ void __launch_bounds__(256) sumsq_final_kernel(const double *part, int n, double *out) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) *out = s;
+}
+}  // namespace
+
+double weights_l2_bf16(const bf16 *w, size_t n, cudaStream_t st) {
+    DBuf<double> part(kL2Blocks + 1);
+    sumsq_partial_kernel<<<kL2Blocks, 256, 0, st>>>(w, n, part.p);
+    RS_LAUNCHED();
+    sumsq_final_kernel<<<1, 256, 0, st>>>(part.p, kL2Blocks, part.p + kL2Blocks);
+    RS_LAUNCHED();
+    double h = 0.0;
+    RS_CUDA(cudaMemcpyAsync(&h, part.p + kL2Blocks, sizeof(double), cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaStreamSynchronize(st));
+    return std::sqrt(h);
 }
 
 }  // namespace rs

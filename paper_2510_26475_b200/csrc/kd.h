@@ -21,7 +21,7 @@ void kd_update_tabular(rs_ctx *ctx, const TabularModel *drafter, const rs_kd_sam
 
 std::vector<int> kd_select(int n, int interval, uint64_t *sel_state);
 double kd_core(rs_ctx *ctx, const TabularModel *drafter, const std::vector<const rs_kd_sample *> &sel,
-               const std::vector<double> &w, double *out_dev, bool grad_only, double scale);
+               const std::vector<double> &w, double *out_dev, bool grad_only, double scale, bool policy = false);
 
 // K5 for large vocabularies: per position, loss_i = w_i * sum_x p(x)(log p(x) - log q(x)) and
 // dZ_i(x) = w_i * (q(x) - p(x)) / tau, with p given as target logits rows (softmax at tau_p)
@@ -40,5 +40,9 @@ void kd_rows_elem(const float *P, const float *Q, const double *lseP, const doub
                   double *kl_part, double *loss, cudaStream_t st);
 void transpose_pad_bf16(const __nv_bfloat16 *in, int ldi, int R, int C, __nv_bfloat16 *out, int ldo, cudaStream_t st);
 void sgd_bf16(const __nv_bfloat16 *w, const float *g, float scale, size_t n, __nv_bfloat16 *out, cudaStream_t st);
+
+// L2 norm of a bf16 weight tensor (fp64 accumulation, deterministic order) -- the learner's
+// LearnerMetrics::weights_l2 for transformer drafters (learner.cpp:268-272).
+double weights_l2_bf16(const __nv_bfloat16 *w, size_t n, cudaStream_t st);
 
 }  // namespace rs

@@ -100,8 +100,68 @@ def main():
         kd_cases.append({"policy": pol, "selection_seed": seed, "out": out})
     with open(os.path.join(HERE, "kd_update.json"), "w") as f:
         json.dump({"drafter": env["drafter"], "buffer": buf, "cases": kd_cases}, f)
-    for name in ["appendix_b.json", "tabular_engine.json", "kd_update.json"]:
+    learner_and_scenarios(env)
+    for name in ["appendix_b.json", "tabular_engine.json", "kd_update.json", "learner_scenarios.json"]:
         print(name, os.path.getsize(os.path.join(HERE, name)))
+
+
+# Small profiling grid for the scenario fixtures (the full default grid is checked separately
+# through build_profile's best-config list).
+SMALL_PROFILE = {"batch_sizes": [1, 2, 4, 8, 16, 32], "profile_cycles": 16, "profile_requests": 32}
+
+
+def learner_and_scenarios(env):
+    """OnlineLearner scripts (learner.cpp:162-289), policy_update (rl.cpp:74-88), the default
+    build_profile, and run_scenario for every scenario (scenarios.cpp:28-341) at small sizes."""
+    out = {"drafter": env["drafter"], "actor": env["actor"]}
+    # rollout batches with rewards: SD-off generations of steps 0..5, 8 samples each
+    batches = []
+    for step in range(6):
+        reqs = R("make_step_requests", seed=1, step=step)["requests"][step * 4: step * 4 + 8]
+        gen = R("run_generation", target=env["actor"], drafter=None, requests=reqs, forced=OFF, record_logprobs=True)
+        rewards = R("reward", responses=[s["response"] for s in gen["samples"]])["rewards"]
+        batches.append([{"prompt": s["prompt"], "response": s["response"],
+                         "steps": [{"token": t, "target_logprobs": st["target_logprobs"]}
+                                   for t, st in zip(s["response"], s["steps"])],
+                         "eos_bias": s["eos_bias"], "reward": r} for s, r in zip(gen["samples"], rewards)])
+    out["batches"] = batches
+    learners = []
+    for name, pol, cap, seed in [
+            ("interval2_reward_evict", {"interval": 2, "mode": "reward", "clip_lo": 0.0, "clip_hi": 4.0, "lr": 0.3}, 12, 31),
+            ("interval1_uniform", {"interval": 1, "mode": "uniform", "clip_lo": 0.0, "clip_hi": 4.0, "lr": 0.5}, 4096, 7),
+            ("interval3_clip", {"interval": 3, "mode": "reward", "clip_lo": 0.5, "clip_hi": 2.0, "lr": 0.2}, 4096, 5),
+            ("frozen", {"interval": 1, "mode": "frozen", "clip_lo": 0.0, "clip_hi": 4.0, "lr": 0.5}, 64, 7)]:
+        script = [{"feed": b, "boundary": it, "await": True} for it, b in enumerate(batches)]
+        res = {}
+        for mode in (False, True):
+            res["async" if mode else "sync"] = R("online_learner", drafter=env["drafter"], policy=pol, selection_seed=seed,
+                                                   cost_per_token=0.02, capacity=cap, script=script, **{"async": mode})
+        assert res["sync"] == res["async"], name  # learner.hpp:91-97: async changes timing, not semantics
+        learners.append({"name": name, "policy": pol, "capacity": cap, "selection_seed": seed, "out": res["sync"]})
+    out["learners"] = learners
+    # policy_update on one group-structured batch (step-0 requests, all 32)
+    reqs = R("make_step_requests", seed=1, step=0)["requests"]
+    gen = R("run_generation", target=env["actor"], drafter=None, requests=reqs, forced=OFF, record_logprobs=False)
+    rewards = R("reward", responses=[s["response"] for s in gen["samples"]])["rewards"]
+    adv = []
+    for g in range(0, len(rewards), 8):
+        adv += R("group_advantages", rewards=rewards[g:g + 8])["advantages"]
+    samples = [{"prompt": s["prompt"], "response": s["response"], "eos_bias": s["eos_bias"], "actor_version": 0}
+               for s in gen["samples"]]
+    out["policy_update"] = {"samples": samples, "rewards": rewards, "advantages": adv, "lr": 0.2,
+                            "out": R("policy_update", actor=env["actor"], samples=samples, advantages=adv, lr=0.2)}
+    out["default_profile"] = R("build_profile", config={})
+    out["config_default"] = R("config_roundtrip", config={})
+    scen = []
+    for name, over in [("baseline", {"steps": 6}), ("naive-spec", {"steps": 6}), ("frozen", {"steps": 5}),
+                       ("uniform-kd", {"steps": 6, "async_learner": False}), ("respec", dict(SMALL_PROFILE, steps=6)),
+                       ("async-ablation", {"steps": 6}), ("skew-demo", dict(SMALL_PROFILE)),
+                       ("respec", dict(SMALL_PROFILE, steps=4, kd_interval=2, async_learner=False, seed=3))]:
+        c = dict(over, scenario=name)
+        scen.append({"config": c, "out": R("run_scenario", config=c)})
+    out["scenarios"] = scen
+    with open(os.path.join(HERE, "learner_scenarios.json"), "w") as f:
+        json.dump(out, f)
 
 
 if __name__ == "__main__":
