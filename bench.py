@@ -252,8 +252,9 @@ def kd_leg(args, rb, eng, drafter, rank, world, barrier):
     """cfg5 leg: one online KD update of the drafter on this step's rollouts (prompt + generated
     tokens of the first --kd requests per GPU), reward-weighted (synthetic rewards), the fp32
     LM-head gradient all-reduced over the ranks (NCCL), the same SGD snapshot on every rank.
-    Device time of the whole update (teacher-forced target + drafter forwards, K5, gradient
-    GEMM, all-reduce, SGD), max over ranks."""
+    Device time of the whole update (target over the response positions from the engine's
+    resident KV cache, teacher-forced drafter, K5, gradient GEMM, all-reduce, SGD), max over
+    ranks; the teacher-forced recompute of prompt + response is timed beside it."""
     import random
     import torch
     from paper_2510_26475_b200.distributed import kd_step_distributed_transformer
@@ -277,10 +278,19 @@ def kd_leg(args, rb, eng, drafter, rank, world, barrier):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    step = kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02)
+    step = kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02,
+                                           engine=eng, local_req_ids=list(range(len(local))))
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    # the same update with the target recomputed teacher-forced over prompt + response
+    barrier()
+    torch.cuda.synchronize()
+    e0.record()
+    kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02)
+    e1.record()
+    torch.cuda.synchronize()
+    ms_recompute = e0.elapsed_time(e1)
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -289,6 +299,8 @@ def kd_leg(args, rb, eng, drafter, rank, world, barrier):
     toks = sum(lengths)
     shape = drafter.shape
     return {"rollouts": args.kd * world, "tokens_distilled": toks, "ms": round(ms, 2),
+            "source": "engine-resident target KV cache + features (rs_engine_kd_grad)",
+            "ms_teacher_forced_recompute": round(ms_recompute, 2),
             "distilled_tokens_per_s": round(toks / (ms / 1000.0), 1), "loss": step.loss,
             "new_drafter_version": step.drafter.version, "trained": "drafter LM head (fp32 grad [V, d])",
             "allreduce_bytes": shape.vocab * shape.d_model * 4 if world > 1 else 0,

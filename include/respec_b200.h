@@ -321,6 +321,16 @@ int rs_tabular_apply_delta(rs_ctx *ctx, const rs_model *m, const double *grad, d
 int rs_kd_grad_transformer(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const rs_kd_sample *samples,
                            int32_t n, const double *weights, float *grad_dev, int32_t zero_grad, double *loss_out);
 int rs_drafter_apply_grad(rs_ctx *ctx, const rs_model *drafter, const float *grad_dev, double scale, rs_model **out);
+/* The same per-rank K5 + LM-head gradient as rs_kd_grad_transformer over requests of a live
+   transformer engine (prompt = the request's prompt, response = its generated tokens, eos_bias
+   its own), computed from the engine's RESIDENT target KV cache and features: only the response
+   positions go through the target (no teacher-forced recompute of the prompt); the given drafter
+   runs teacher-forced into a private cache (the engine's drafter state is untouched).
+   Per-row losses and dZ are bit-identical to rs_kd_grad_transformer on the same sequences; the
+   gradient is too whenever both accumulate the KD rows in the same groups (one group when they
+   fit the workspace), else it differs only by fp32 summation grouping. */
+int rs_engine_kd_grad(rs_engine *e, const rs_model *drafter, const int32_t *req, int32_t n, const double *weights,
+                      float *grad_dev, int32_t zero_grad, double *loss_out);
 int rs_kd_update_transformer(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const rs_kd_sample *buf,
                              int32_t n, rs_kd_policy policy, uint64_t *selection_rng_state, double cost,
                              rs_model **new_drafter, rs_kd_result *out);

@@ -134,6 +134,7 @@ EXPORTED_SYMBOLS = [
     "rs_learner_total_sim_time", "rs_learner_buffer_size", "rs_learner_metrics",
     "rs_reward", "rs_group_advantages", "rs_policy_update_tabular",
     "rs_engine_set_stop_at_eos", "rs_profile_simulated", "rs_tabular_random", "rs_skew_eos_biases",
+    "rs_engine_kd_grad",
 ]
 
 _lib = None
@@ -238,6 +239,7 @@ def lib():
                                       i32, i32, i32, u64, P(dbl)], ctypes.c_int),
             "rs_tabular_random": ([vp, i32, i32, dbl, dbl, u64, P(vp)], ctypes.c_int),
             "rs_skew_eos_biases": ([u64, i32, P(dbl)], ctypes.c_int),
+            "rs_engine_kd_grad": ([vp, vp, P(i32), i32, P(dbl), vp, i32, P(dbl)], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -927,6 +929,22 @@ class BatchEngine:
         na = ctypes.c_int32()
         _check(lib().rs_engine_step_tokens(self.handle, req, cnt, toks, cap, ctypes.byref(na)))
         return {req[a]: list(toks[a * cap: a * cap + min(cnt[a], cap)]) for a in range(na.value)}
+
+    def kd_grad(self, drafter: "EagleDrafter", req_ids: Sequence[int], weights: Sequence[float], grad=None,
+                zero_grad: bool = True):
+        """Per-rank K5 + drafter LM-head gradient over these requests' generated tokens, from the
+        engine's resident target KV cache and features (rs_engine_kd_grad): (loss, fp32 [V, d]
+        torch CUDA tensor). Same result as kd_grad_transformer on the same rollouts without the
+        teacher-forced recompute of the prompts."""
+        import torch
+        V, d = drafter.shape.vocab, drafter.shape.d_model
+        if grad is None:
+            grad = torch.zeros(V, d, dtype=torch.float32, device="cuda")
+        loss = ctypes.c_double()
+        torch.cuda.synchronize()
+        _check(lib().rs_engine_kd_grad(self.handle, drafter.handle, _i32arr(req_ids), len(req_ids), _f64arr(weights),
+                                       ctypes.c_void_p(grad.data_ptr()), 1 if zero_grad else 0, ctypes.byref(loss)))
+        return loss.value, grad
 
     def requests(self) -> List[RequestState]:
         V = self._target.vocab_size

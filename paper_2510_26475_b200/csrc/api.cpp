@@ -729,6 +729,29 @@ int rs_drafter_apply_grad(rs_ctx *ctx, const rs_model *drafter, const float *gra
     });
 }
 
+int rs_engine_kd_grad(rs_engine *e, const rs_model *drafter, const int32_t *req, int32_t n, const double *weights,
+                      float *grad_dev, int32_t zero_grad, double *loss_out) {
+    return guard([&] {
+        need(e, "rs_engine_kd_grad");
+        need(grad_dev, "rs_engine_kd_grad: grad");
+        if (n > 0) need(req, "rs_engine_kd_grad: requests");
+        if (!e->pair) throw std::runtime_error("rs_engine_kd_grad: engine has no model pair");
+        const auto *t = static_cast<const rs::TransformerModel *>(e->target);
+        if (e->target->kind != rs_model::Transformer) throw std::invalid_argument("kd from the engine needs a transformer target");
+        if (zero_grad) RS_CUDA(cudaMemsetAsync(grad_dev, 0, (size_t)t->s.V * t->s.d * sizeof(float), e->ctx->stream));
+        std::vector<rs::KdRef> refs;
+        for (int i = 0; i < n; ++i) {
+            if (req[i] < 0 || req[i] >= e->n) throw std::invalid_argument("kd: request index out of range");
+            if (e->len[req[i]] - e->prompt_len[req[i]] <= 0) continue;  // nothing generated: nothing to distil
+            refs.push_back(rs::KdRef{req[i], weights ? weights[i] : 1.0, e->eos_bias[req[i]]});
+        }
+        const double loss = refs.empty() ? 0.0 : e->pair->kd_cached(refs, drafter, grad_dev);
+        RS_CUDA(cudaStreamSynchronize(e->ctx->stream));
+        rs::prof_collect();
+        if (loss_out) *loss_out = loss;
+    });
+}
+
 int rs_kd_update_transformer(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const rs_kd_sample *buf,
                              int32_t n, rs_kd_policy policy, uint64_t *sel_state, double cost, rs_model **new_drafter,
                              rs_kd_result *out) {
@@ -832,6 +855,9 @@ int rs_set_tuning(const char *key, int64_t value) {
             rs::tuning().gemm2 = static_cast<int>(value);
         } else if (k == "pdl") {
             rs::tuning().pdl = static_cast<int>(value);
+        } else if (k == "kd_rows") {
+            if (value < 0) throw std::invalid_argument("kd_rows must be >= 0");
+            rs::tuning().kd_rows = static_cast<int>(value);
         } else {
             throw std::invalid_argument("unknown tuning key: " + k);
         }

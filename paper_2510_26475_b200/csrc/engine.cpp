@@ -42,6 +42,7 @@ Tuning &tuning() {
                     else if (k == "pdl") x.pdl = v;
                     else if (k == "gemm2") x.gemm2 = v;
                     else if (k == "gemm_trace") x.gemm_trace = v;
+                    else if (k == "kd_rows") x.kd_rows = v;
                 }
                 p = e + 1;
             }

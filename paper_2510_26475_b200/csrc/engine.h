@@ -3,6 +3,7 @@
 // kernels through the launchers in sd.h (tabular) and model.h (transformer).
 #pragma once
 #include <atomic>
+#include <stdexcept>
 
 #include <cuda_runtime.h>
 
@@ -42,6 +43,9 @@ struct DBuf {
         release();
         n = count;
         if (count) RS_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void ensure(size_t count) {  // grow-only: keeps the allocation when it is large enough
+        if (count > n) alloc(count);
     }
     void release() {
         if (p) cudaFree(p);
@@ -108,6 +112,11 @@ private:
 };
 
 // Model-side hooks of one engine (the forwards that produce logit rows).
+struct KdRef {  // one request of a finished (or running) engine taking part in a KD update
+    int req = 0;
+    double weight = 1.0, eos_bias = 0.0;
+};
+
 struct ModelPair {
     virtual ~ModelPair() = default;
     virtual RowType row_type() const = 0;
@@ -117,6 +126,11 @@ struct ModelPair {
     virtual void on_spec_enable(const SdDev &, cudaStream_t) {}
     virtual void set_drafter(const rs_model *) {}
     virtual void begin_step() {}
+    // Online-KD loss + drafter LM-head gradient over requests' generated tokens from the
+    // resident caches (transformer pairs only).
+    virtual double kd_cached(const std::vector<KdRef> &, const rs_model *, float *) {
+        throw std::invalid_argument("kd from the engine needs a transformer target");
+    }
 };
 
 std::unique_ptr<ModelPair> make_tabular_pair(const TabularModel *target, const TabularModel *drafter);

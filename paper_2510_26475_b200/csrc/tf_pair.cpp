@@ -298,6 +298,11 @@ struct TransformerPair : ModelPair {
     Staging stage;
     Batch bt;
     std::vector<int> dkv_len;  // drafter cache valid for positions < dkv_len
+    struct KdScratch {         // kd_cached buffers (rows x V logits, stats, dZ^T, h, private drafter KV)
+        DBuf<float> Pb, Qb;
+        DBuf<double> stP, stQ, lseP, lseQ, kl, lossr, wr, br;
+        DBuf<bf16> dzT, hT, hG, tk, tv;
+    } kd_scr;
 
     TransformerPair(rs_ctx *c, rs_engine *e, const TransformerModel *t, const DrafterModel *d)
         : ctx(c), eng(e), tgt(t), drf(d), s(t->s) {}
@@ -563,13 +568,16 @@ struct TransformerPair : ModelPair {
     double kd_pass(const SdDev &d, const std::vector<KdSeq> &seqs, float *grad) {
         cudaStream_t st = ctx->stream;
         const int V = s.V, Mcap = w.Mcap;
-        const int ldt = (Mcap + 63) / 64 * 64;
+        long long need = 0;  // KD rows in total (one per response token)
+        for (const auto &q : seqs) need += std::max(0, (int)q.tokens.size() - q.prompt_len);
+        const int Rcap = (int)std::max<long long>(1, std::min<long long>(Mcap, need));
+        const int ldt = (Rcap + 63) / 64 * 64;
         const int nt = (V + 255) / 256;
-        DBuf<float> Pb((size_t)Mcap * V), Qb((size_t)Mcap * V);
-        DBuf<double> stP((size_t)Mcap * nt * 2), stQ((size_t)Mcap * nt * 2), lseP(Mcap), lseQ(Mcap), kl((size_t)Mcap * nt),
-            lossr(Mcap), wr(Mcap), br(Mcap);
+        DBuf<float> Pb((size_t)Rcap * V), Qb((size_t)Rcap * V);
+        DBuf<double> stP((size_t)Rcap * nt * 2), stQ((size_t)Rcap * nt * 2), lseP(Rcap), lseQ(Rcap), kl((size_t)Rcap * nt),
+            lossr(Rcap), wr(Rcap), br(Rcap);
         DBuf<bf16> dzT((size_t)V * ldt), hT((size_t)s.d * ldt);
-        std::vector<double> lh(Mcap);
+        std::vector<double> lh(Rcap);
         double loss = 0.0;
         size_t r = 0;
         int p = 0;
@@ -604,7 +612,9 @@ struct TransformerPair : ModelPair {
             // target: tensor-core attention items
             for (const auto &sg : segs) bt.add_items(sg.first, sg.second, per_item_t, -1, 0, 0, 0);
             upload(bt, st, tc_attn);
+            prof_set_scope("kd_target");
             target_forward(d, M, (int)bt.items.size(), Pb.p, true, st);
+            prof_set_scope("kd_drafter");
             // drafter: the same attention items over the same rows
             bt.items.clear();
             for (const auto &sg : segs) bt.add_items(sg.first, sg.second, per_item_t, -1, 0, 0, 0);
@@ -620,6 +630,7 @@ struct TransformerPair : ModelPair {
             drafter_head(w.map_a.p, w.map_b.p, R, Qb.p, nullptr, st);  // h_norm of the KD rows stays in w.xn
             stage.upload(wr.p, kd_w, st);
             stage.upload(br.p, kd_b, st);
+            prof_set_scope("kd_k5");
             row_stats(Pb.p, nullptr, R, V, tgt->temperature, stP.p, st);
             row_stats(Qb.p, nullptr, R, V, drf->temperature, stQ.p, st);
             kd_rows_lse(Pb.p, stP.p, R, V, tgt->temperature, br.p, lseP.p, st);
@@ -627,7 +638,179 @@ struct TransformerPair : ModelPair {
             const int Rp = (R + 63) / 64 * 64;
             kd_rows_elem(Pb.p, Qb.p, lseP.p, lseQ.p, wr.p, br.p, R, V, tgt->temperature, drf->temperature,
                          s.logit_scale, dzT.p, Rp, kl.p, lossr.p, st);
+            prof_set_scope("kd_grad");
             transpose_pad_bf16(w.xn.p, s.d, R, s.d, hT.p, Rp, st);
+            GemmArgs g;  // dW[V][d] += dZ^T[V][Rp] . (h^T[d][Rp])^T
+            g.A = dzT.p;
+            g.B = hT.p;
+            g.M = V;
+            g.N = s.d;
+            g.K = Rp;
+            g.lda = Rp;
+            g.ldb = Rp;
+            g.epi.kind = kEpiResidual;
+            g.epi.out = grad;
+            g.epi.ldo = s.d;
+            gemm_bf16(g, st);
+            RS_CUDA(cudaMemcpyAsync(lh.data(), lossr.p, (size_t)R * 8, cudaMemcpyDeviceToHost, st));
+            RS_CUDA(cudaStreamSynchronize(st));
+            for (int k = 0; k < R; ++k) loss += lh[k];
+            stage.off = 0;
+        }
+        return loss;
+    }
+
+    // K5 + LM-head gradient from the engine's RESIDENT state instead of a teacher-forced
+    // recompute of prompt + response: the target runs only over the response positions
+    // [plen - 1, len - 2] of each selected request (its prompt keys are already in kv_t from the
+    // prefill; the response keys are rewritten bit-identically by the rows themselves -- every
+    // kernel on the path is row-invariant), storing their EAGLE features next to the prompt's.
+    // The drafter (the given snapshot, not the engine's) then runs teacher-forced over every
+    // position from those features into a private drafter KV cache, so the engine's own drafter
+    // state is untouched. Rows are grouped so a group holds <= Mcap KD rows; the drafter
+    // advances through each request only as far as the group needs. Same loss / gradient as
+    // kd_pass on the same sequences.
+    double kd_cached(const std::vector<KdRef> &refs, const rs_model *m, float *grad) override {
+        if (!m || m->kind != rs_model::Drafter) throw std::invalid_argument("kd: EAGLE drafter required");
+        const auto *kd_drf = static_cast<const DrafterModel *>(m);
+        if (kd_drf->target != tgt) throw std::invalid_argument("kd: drafter is bound to a different target");
+        for (const auto &x : refs)
+            if (x.req < 0 || x.req >= eng->n) throw std::invalid_argument("kd: request index out of range");
+        SdDev d{};
+        d.tok = eng->d_tok.p;
+        d.tok_cap = eng->tok_cap;
+        d.t_max = 1;
+        d.n_max = 1;
+        cudaStream_t st = ctx->stream;
+        const int V = s.V;
+        const int Mcap = tuning().kd_rows > 0 ? std::min(w.Mcap, tuning().kd_rows) : w.Mcap;
+        long long need = 0;  // KD rows in total: every generated token of every selected request
+        for (const auto &x : refs) need += std::max(0, eng->len[x.req] - eng->prompt_len[x.req]);
+        const int Rcap = (int)std::max<long long>(1, std::min<long long>(Mcap, need));
+        const int ldt = (Rcap + 63) / 64 * 64;
+        const int nt = (V + 255) / 256;
+        // scratch kept on the engine (grow-only): repeated updates allocate nothing
+        KdScratch &k = kd_scr;
+        k.Pb.ensure((size_t)Rcap * V);
+        k.Qb.ensure((size_t)Rcap * V);
+        k.stP.ensure((size_t)Rcap * nt * 2);
+        k.stQ.ensure((size_t)Rcap * nt * 2);
+        k.kl.ensure((size_t)Rcap * nt);
+        for (DBuf<double> *b : {&k.lseP, &k.lseQ, &k.lossr, &k.wr, &k.br}) b->ensure(Rcap);
+        k.dzT.ensure((size_t)V * ldt);
+        k.hT.ensure((size_t)s.d * ldt);
+        k.hG.ensure((size_t)Rcap * s.d);
+        const size_t kvd = (size_t)B * s.KV * max_ctx * s.hd;
+        k.tk.ensure(kvd);
+        k.tv.ensure(kvd);
+        RS_CUDA(cudaMemsetAsync(k.tk.p, 0, kvd * sizeof(bf16), st));
+        RS_CUDA(cudaMemsetAsync(k.tv.p, 0, kvd * sizeof(bf16), st));
+        DBuf<float> &Pb = k.Pb, &Qb = k.Qb;
+        DBuf<double> &stP = k.stP, &stQ = k.stQ, &lseP = k.lseP, &lseQ = k.lseQ, &kl = k.kl, &lossr = k.lossr, &wr = k.wr,
+                     &br = k.br;
+        DBuf<bf16> &dzT = k.dzT, &hT = k.hT, &hG = k.hG, &tk = k.tk, &tv = k.tv;
+        struct Swap {  // private drafter cache + the KD snapshot for the duration of the pass
+            TransformerPair &t;
+            KvCache kv;
+            const DrafterModel *m;
+            ~Swap() {
+                t.kv_d = kv;
+                t.drf = m;
+            }
+        } swap{*this, kv_d, drf};
+        kv_d = KvCache{tk.p, tv.p, 1, B, s.KV, max_ctx, s.hd};
+        drf = kd_drf;
+        std::vector<int> dp(refs.size(), 0);  // drafter positions computed per selected request
+        std::vector<double> lh(Rcap);
+        double loss = 0.0;
+        size_t i = 0;
+        int p = refs.empty() ? 0 : eng->prompt_len[refs[0].req] - 1;
+        while (i < refs.size()) {
+            // ---- one group of <= Mcap KD rows: (request i, positions [first, last]) spans ----
+            struct Span {
+                size_t i;
+                int first, last, kd0;
+            };
+            std::vector<Span> spans;
+            std::vector<double> kd_w, kd_b;
+            bt.clear();
+            while (i < refs.size() && bt.M() < Mcap) {
+                const int r = refs[i].req, last = eng->len[r] - 2;
+                if (p > last) {
+                    if (++i < refs.size()) p = eng->prompt_len[refs[i].req] - 1;
+                    continue;
+                }
+                const int take = std::min(last - p + 1, Mcap - bt.M());
+                const int r0 = bt.M();
+                spans.push_back(Span{i, p, p + take - 1, r0});
+                for (int k = 0; k < take; ++k, ++p) {
+                    bt.rows.push_back(RowDesc{r, p, p, 0, -1, 0, 0, 0});
+                    kd_w.push_back(refs[i].weight);
+                    kd_b.push_back(refs[i].eos_bias);
+                }
+                bt.add_items(r0, bt.M(), per_item_t, -1, 0, 0, 0);
+            }
+            const int R = bt.M();
+            if (R == 0) break;
+            prof_set_scope("kd_target");
+            upload(bt, st, tc_attn);
+            target_forward(d, R, (int)bt.items.size(), Pb.p, false, st);
+            // ---- drafter: teacher-forced from dp[i] through each span's last position ----
+            prof_set_scope("kd_drafter");
+            size_t sp = 0;
+            while (sp < spans.size()) {
+                bt.clear();
+                std::vector<int32_t> src;
+                int dst0 = -1;
+                for (; sp < spans.size(); ++sp) {
+                    const Span &sn = spans[sp];
+                    const int r = refs[sn.i].req;
+                    const int from = dp[sn.i];
+                    if (from > sn.last) continue;
+                    const int room = Mcap - bt.M();
+                    if (room <= 0) break;
+                    const int upto = std::min(sn.last, from + room - 1);
+                    const int r0 = bt.M();
+                    for (int q = from; q <= upto; ++q) {
+                        if (q >= sn.first) {
+                            if (dst0 < 0) dst0 = sn.kd0 + (q - sn.first);
+                            src.push_back(bt.M());
+                        }
+                        bt.rows.push_back(RowDesc{r, q, q, 0, -1, 0, 0, 0});
+                    }
+                    bt.add_items(r0, bt.M(), per_item_t, -1, 0, 0, 0);
+                    dp[sn.i] = upto + 1;
+                    if (upto < sn.last) break;  // chunk full mid-span: resume this span next chunk
+                }
+                const int M = bt.M();
+                if (M == 0) break;
+                const int n = (int)src.size();
+                std::vector<int32_t> dst(n);
+                for (int k = 0; k < n; ++k) dst[k] = dst0 + k;
+                bt.map_a = src;
+                bt.map_b = dst;
+                upload(bt, st, tc_attn);
+                k_gather_features(w.rows.p, M, s.d, feat.p, max_ctx, nullptr, w.fin.p, nullptr, st);
+                gemm(w.fin.p, 3 * s.d, drf->fc_w, M, s.d, 3 * s.d, epi_f32(w.x.p, s.d, 1.0f, nullptr), st);
+                drafter_layer(d, M, (int)bt.items.size(), st);
+                if (n == 0) continue;
+                drafter_head(w.map_a.p, w.map_b.p, n, Qb.p, nullptr, st);
+                RS_CUDA(cudaMemcpyAsync(hG.p + (size_t)dst0 * s.d, w.xn.p, (size_t)n * s.d * sizeof(bf16),
+                                        cudaMemcpyDeviceToDevice, st));
+            }
+            // ---- K5 + dW_lm over the group's R rows ----
+            prof_set_scope("kd_k5");
+            stage.upload(wr.p, kd_w, st);
+            stage.upload(br.p, kd_b, st);
+            row_stats(Pb.p, nullptr, R, V, tgt->temperature, stP.p, st);
+            row_stats(Qb.p, nullptr, R, V, drf->temperature, stQ.p, st);
+            kd_rows_lse(Pb.p, stP.p, R, V, tgt->temperature, br.p, lseP.p, st);
+            kd_rows_lse(Qb.p, stQ.p, R, V, drf->temperature, br.p, lseQ.p, st);
+            const int Rp = (R + 63) / 64 * 64;
+            kd_rows_elem(Pb.p, Qb.p, lseP.p, lseQ.p, wr.p, br.p, R, V, tgt->temperature, drf->temperature,
+                         s.logit_scale, dzT.p, Rp, kl.p, lossr.p, st);
+            prof_set_scope("kd_grad");
+            transpose_pad_bf16(hG.p, s.d, R, s.d, hT.p, Rp, st);
             GemmArgs g;  // dW[V][d] += dZ^T[V][Rp] . (h^T[d][Rp])^T
             g.A = dzT.p;
             g.B = hT.p;
@@ -724,6 +907,8 @@ double kd_grad_transformer(rs_ctx *ctx, const TransformerModel *tgt, const Draft
     d.n_max = 1;
     const double loss = p.kd_pass(d, seqs, grad);
     RS_CUDA(cudaStreamSynchronize(st));
+    prof_collect();
+    prof_set_scope("step");
     return loss;
 }
 

@@ -134,12 +134,17 @@ class TransformerKDStep:
 def kd_step_distributed_transformer(drafter, global_rewards: Sequence[float], global_lengths: Sequence[int],
                                     local_samples: Sequence[RolloutSample], local_global_idx: Sequence[int],
                                     policy: KDPolicy, selection_rng: SelectionRng, sim_cost_per_token: float,
-                                    group=None, reduce: bool = True) -> TransformerKDStep:
+                                    group=None, reduce: bool = True, engine=None,
+                                    local_req_ids: Optional[Sequence[int]] = None) -> TransformerKDStep:
     """Prompt-sharded kd_update for an EAGLE drafter: replicated selection + reward weights over
     GLOBAL buffer indices (learner.cpp:107-140), this rank's K5 + LM-head gradient on its GPU,
     ONE all-reduce of the fp32 [V, d] gradient (and the loss) with torch.distributed -- NCCL over
     NVLink on a B200 box, the only collective of the whole rollout path -- then the same SGD
-    step (-lr) on every rank, so every rank publishes the same snapshot."""
+    step (-lr) on every rank, so every rank publishes the same snapshot.
+
+    With `engine` (this rank's BatchEngine that generated the local rollouts; local_req_ids[k] =
+    its request index of local_samples[k]) the gradient comes from the engine's resident KV cache
+    and features (BatchEngine.kd_grad) instead of a teacher-forced recompute of the prompts."""
     import torch
     if policy.mode == 2:
         from . import LogicError
@@ -148,9 +153,13 @@ def kd_step_distributed_transformer(drafter, global_rewards: Sequence[float], gl
     batch_rewards = [global_rewards[i] for i in sel]
     weights = {i: kd_weight(global_rewards[i], batch_rewards, policy) for i in sel}
     order = {g: k for k, g in enumerate(sel)}
-    mine = sorted([(order[g], s, weights[g]) for s, g in zip(local_samples, local_global_idx) if g in weights],
-                  key=lambda t: t[0])
-    loss, grad = kd_grad_transformer(drafter, [s for _, s, _ in mine], [w for _, _, w in mine])
+    rids = list(local_req_ids) if local_req_ids is not None else list(range(len(local_samples)))
+    mine = sorted([(order[g], s, weights[g], q) for s, g, q in zip(local_samples, local_global_idx, rids)
+                   if g in weights], key=lambda t: t[0])
+    if engine is not None:
+        loss, grad = engine.kd_grad(drafter, [q for *_, q in mine], [w for _, _, w, _ in mine])
+    else:
+        loss, grad = kd_grad_transformer(drafter, [s for _, s, _, _ in mine], [w for _, _, w, _ in mine])
     if reduce:
         import torch.distributed as dist
         if dist.is_available() and dist.is_initialized():

@@ -141,3 +141,55 @@ def test_distributed_step_single_rank(models):
     ref = rb.kd_update(drf, ss, pol, rb.SelectionRng(9), 0.01)
     assert st.loss == pytest.approx(ref.loss, rel=1e-12)
     assert torch.equal(st.drafter.to_torch("lm_w"), ref.drafter.to_torch("lm_w"))
+
+
+def _engine_rollouts(tgt, drf, n=4, seed=3, max_len=9):
+    rng = random.Random(seed)
+    reqs = [rb.RequestState(i, [rng.randrange(SHAPE.vocab - 1) for _ in range(4 + 3 * i)], -2.0 + 0.5 * i,
+                            max_len + i, rb.DecodeRng.from_seed(17, i)) for i in range(n)]
+    return rb.BatchEngine(tgt, lambda: drf, None, rb.TimingModel(), reqs, rb.SDConfig.tree(1, 2, 3), "sample",
+                          record_full_logprobs=False)
+
+
+@pytest.mark.parametrize("kd_rows", [0, 7])
+def test_engine_kd_grad_matches_recompute(models, kd_rows):
+    """rs_engine_kd_grad (resident KV cache + features, response positions only through the
+    target) == kd_grad_transformer (teacher-forced recompute of prompt + response): identical
+    per-row losses (so an identical total), the same gradient -- bitwise when both use one group,
+    to fp32 grouping otherwise (kd_rows=7 forces several groups and drafter chunks)."""
+    tgt, drf = models
+    other = rb.EagleDrafter(tgt, seed=77, version=9)  # KD drafter != the engine's drafter
+    eng = _engine_rollouts(tgt, drf)
+    while not eng.all_done():
+        eng.step()
+    reqs = eng.requests()
+    ids = [0, 2, 3, 1]
+    ws = [0.5, 1.5, 1.0, 2.0]
+    ss = [rb.RolloutSample(list(reqs[i].prompt), list(reqs[i].generated), [], reqs[i].eos_bias) for i in ids]
+    rb.set_tuning("kd_rows", kd_rows)
+    try:
+        loss_e, g_e = eng.kd_grad(other, ids, ws)
+    finally:
+        rb.set_tuning("kd_rows", 0)
+    loss_r, g_r = rb.kd_grad_transformer(other, ss, ws)
+    assert loss_e == loss_r
+    if kd_rows == 0:
+        assert torch.equal(g_e, g_r)
+    else:
+        assert (g_e - g_r).abs().max().item() <= 1e-5 * g_r.abs().max().item()
+
+
+def test_engine_kd_grad_leaves_engine_state(models):
+    """A KD pass in the middle of a rollout does not perturb the rollout (private drafter cache;
+    target keys rewritten bit-identically)."""
+    tgt, drf = models
+    a, b = _engine_rollouts(tgt, drf, max_len=14), _engine_rollouts(tgt, drf, max_len=14)
+    for _ in range(2):
+        a.step()
+        b.step()
+    a.kd_grad(rb.EagleDrafter(tgt, seed=78), [0, 1, 2, 3], [1.0] * 4)
+    while not a.all_done():
+        a.step()
+    while not b.all_done():
+        b.step()
+    assert [r.generated for r in a.requests()] == [r.generated for r in b.requests()]
