@@ -567,27 +567,32 @@ int rs_profile_simulated(rs_ctx *ctx, const rs_model *target, const rs_model *dr
                 if (c.enabled && !drafter) throw std::invalid_argument("profile: spec configs need a drafter");
                 const int per = c.enabled ? c.rounds * c.draft_len + 1 : 1;
                 const int max_len = cycles_per_request * per + (c.enabled ? c.draft_len : 0) + 8;
+                // Every wave of the pool runs side by side in ONE engine (a request's trajectory
+                // depends only on its own RNG streams and context); the engine charges each wave's
+                // lockstep cycles into that wave's own ledger, concatenated in wave order below --
+                // the reference's single ledger, event for event.
                 std::vector<rs_forward_event> ledger;
                 long long tokens = 0;
-                for (int base = 0; base < num_requests; base += batch) {
-                    std::vector<rs_request> reqs(batch);
-                    for (int i = 0; i < batch; ++i) {
-                        const int rid = base + i;
+                const int waves = num_requests > 0 ? (num_requests + batch - 1) / batch : 0;
+                if (waves > 0) {
+                    std::vector<rs_request> reqs((size_t)waves * batch);
+                    for (int rid = 0; rid < waves * batch; ++rid) {
                         const int p = rid % n_prompts;
-                        reqs[i] = {i, prompts + prompt_off[p], prompt_off[p + 1] - prompt_off[p], 0.0, max_len, seed,
-                                   (uint64_t)rid};
+                        reqs[rid] = {rid, prompts + prompt_off[p], prompt_off[p + 1] - prompt_off[p], 0.0, max_len,
+                                     seed, (uint64_t)rid};
                     }
                     rs_engine *e = nullptr;
                     rs_abi::rethrow(rs_engine_create(ctx, target, c.enabled ? drafter : nullptr, nullptr, tm,
-                                                     reqs.data(), batch, c, RS_VERIFY_SAMPLE, 0, &e));
+                                                     reqs.data(), (int32_t)reqs.size(), c, RS_VERIFY_SAMPLE, 0, &e));
                     std::unique_ptr<rs_engine, int (*)(rs_engine *)> hold(e, rs_engine_destroy);
                     e->stop_at_eos = false;
+                    e->ledger_group = batch;
                     for (int k = 0; k < cycles_per_request; ++k) {
                         rs_step_info info{};
                         rs_abi::rethrow(rs_engine_step(e, &info));
                         tokens += info.emitted_tokens;
                     }
-                    ledger.insert(ledger.end(), e->ledger.begin(), e->ledger.end());
+                    for (const auto &gl : e->group_ledgers) ledger.insert(ledger.end(), gl.begin(), gl.end());
                 }
                 double total = 0.0;  // ledger_time (costsim.cpp:13-27) over the whole pool, in order
                 for (const auto &ev : ledger) {

@@ -452,24 +452,45 @@ void rs_engine::step(rs_step_info *info) {
             accepted += s[2];
         }
     }
-    if (mode.enabled) {
-        for (size_t rr = 0; rr < max_rounds; ++rr) {
-            int max_fw = 0, each = 0, max_target = 0;
-            for (int a = 0; a < batch; ++a) {
-                const int32_t *s = h_summary + a * sw;
-                if ((size_t)s[4] > rr) {
-                    const int32_t *rc = s + kSummaryFixed + 3 * rr;
-                    max_fw = std::max(max_fw, rc[0]);
-                    each = std::max(each, rc[1]);
-                    max_target = std::max(max_target, rc[2]);
+    // charge_batched_cycle over the whole active batch, or -- ledger_group > 0 (the profiler's
+    // fixed-width waves run side by side) -- separately per group of ledger_group requests into
+    // that group's own ledger.
+    auto charge = [&](std::vector<rs_forward_event> &out, int a0, int a1) {
+        const int width = a1 - a0;
+        if (mode.enabled) {
+            size_t rounds = 0;
+            for (int a = a0; a < a1; ++a) rounds = std::max<size_t>(rounds, h_summary[a * sw + 4]);
+            for (size_t rr = 0; rr < rounds; ++rr) {
+                int max_fw = 0, each = 0, max_target = 0;
+                for (int a = a0; a < a1; ++a) {
+                    const int32_t *s = h_summary + a * sw;
+                    if ((size_t)s[4] > rr) {
+                        const int32_t *rc = s + kSummaryFixed + 3 * rr;
+                        max_fw = std::max(max_fw, rc[0]);
+                        each = std::max(each, rc[1]);
+                        max_target = std::max(max_target, rc[2]);
+                    }
                 }
+                for (int f = 0; f < max_fw; ++f) out.push_back({0, width * each, width * each});
+                if (max_target > 0) out.push_back({1, width * max_target, width * max_target});
             }
-            for (int f = 0; f < max_fw; ++f) ledger.push_back({0, batch * each, batch * each});
-            if (max_target > 0) ledger.push_back({1, batch * max_target, batch * max_target});
+        } else {
+            out.push_back({1, width, width});
+        }
+    };
+    if (ledger_group > 0) {
+        group_ledgers.resize((n + ledger_group - 1) / ledger_group);
+        for (int a0 = 0; a0 < batch;) {
+            const int g = active[a0] / ledger_group;
+            int a1 = a0;
+            while (a1 < batch && active[a1] / ledger_group == g) ++a1;
+            charge(group_ledgers[g], a0, a1);
+            a0 = a1;
         }
     } else {
-        ledger.push_back({1, batch, batch});
+        charge(ledger, 0, batch);
     }
+    (void)max_rounds;
     ++cycle;
     if (info) {
         float ms = 0.f;

@@ -172,6 +172,8 @@ struct rs_engine {
     std::vector<double> eos_bias;
     std::vector<std::vector<int>> accept_lens;
     std::vector<rs_forward_event> ledger;
+    int ledger_group = 0;  // > 0: charge cycles per group of this many requests (profile waves)
+    std::vector<std::vector<rs_forward_event>> group_ledgers;
     std::vector<rs_switch_event> switches;
     std::vector<int> active_trace, drafter_versions;
     std::vector<int> active;
