@@ -20,4 +20,10 @@ timeout 600 ncu --set full --clock-control none --import-source on --nvtx --nvtx
   -o $O/attn_full python tools/profile_step.py 2 > $O/attn_full.log 2>&1; echo "ncu attn rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "verify/" -k regex:gemm -s 0 -c 4 \
   -o $O/gemm_b256_full python tools/profile_step.py 1 1664 256 > $O/gemm_b256_full.log 2>&1; echo "ncu gemm b256 rc=$?"
+timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --nvtx \
+  --nvtx-include "verify/" -k regex:gemm --csv --log-file $O/gemm_traffic.csv python tools/profile_step.py 1 > $O/gemm_traffic.log 2>&1
+echo "ncu traffic rc=$?"
+python tools/gemm_traffic.py $O/gemm_traffic.csv > $O/gemm_traffic.json; head -3 $O/gemm_traffic.json
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"kd_elem|kd_lse|row_stats" -s 0 -c 4 \
+  -o $O/kd_full python tools/profile_kd.py 1 1664 65 > $O/kd_full.log 2>&1; echo "ncu kd rc=$?"
 ls -la $O
