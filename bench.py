@@ -274,6 +274,12 @@ def kd_leg(args, rb, eng, drafter, rank, world, barrier):
         dist.all_reduce(lt)
         lengths = lt.tolist()
     pol = rb.KDPolicy(interval=1, mode=0, clip_lo=0.0, clip_hi=4.0, lr=0.5)  # config.hpp:38
+    # untimed warm-up of both paths: first-use allocations (the engine's grow-only KD scratch,
+    # the recompute path's workspaces) stay out of the timed region, as for an online learner
+    # that updates every iteration
+    kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02,
+                                    engine=eng, local_req_ids=list(range(len(local))))
+    kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

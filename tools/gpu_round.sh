@@ -26,4 +26,7 @@ echo "ncu traffic rc=$?"
 python tools/gemm_traffic.py $O/gemm_traffic.csv > $O/gemm_traffic.json; head -3 $O/gemm_traffic.json
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"kd_elem|kd_lse|row_stats" -s 0 -c 4 \
   -o $O/kd_full python tools/profile_kd.py 1 1664 65 > $O/kd_full.log 2>&1; echo "ncu kd rc=$?"
+python tools/ncu_summary.py $O > $O/ncu_summary.md 2> $O/ncu_summary.err; echo "summary rc=$?"
+# keep the copy-back under gpurun's 64 MiB: summaries stay, the large reports go
+find $O -name "*.ncu-rep" -size +6M -delete
 ls -la $O
