@@ -85,22 +85,32 @@ __device__ __forceinline__ void store8(bf16 *p, const float (&v)[8]) {
     *reinterpret_cast<int4 *>(p) = *reinterpret_cast<const int4 *>(h);
 }
 
-// One CTA per row, 16-byte vectors held in registers: y = x * rsqrt(mean(x^2) + eps) * w
-// (Qwen2RMSNorm, fp32 math). d % 8 == 0, d <= 8 * 4 * blockDim.
-template <class T>
-__global__ void __launch_bounds__(256) rmsnorm_kernel(const T *x, int ldx, const float *w, int M, int d, float eps,
-                                                      bf16 *out, int ldo) {
+// Two rows per 256-thread CTA (128 threads per row, NG groups of 8 elements per thread), so a
+// verify batch of ~1.3K rows is a single wave of resident CTAs; the gain vector is read before
+// the programmatic-dependency wait (weights never depend on the previous kernel).
+// y = x * rsqrt(mean(x^2) + eps) * w (Qwen2RMSNorm, fp32 math); d % 8 == 0, d <= 8192.
+template <class T, int NG>
+__global__ void __launch_bounds__(256) rmsnorm2_kernel(const T *x, int ldx, const float *w, int M, int d, float eps,
+                                                       bf16 *out, int ldo) {
     pdl_trigger();
+    const int half = threadIdx.x >> 7, t = threadIdx.x & 127;
+    float wv[NG][8];
+#pragma unroll
+    for (int k = 0; k < NG; ++k) {
+        const int i = (t + k * 128) * 8;
+        if (i < d) load8(w + i, wv[k]);
+    }
     pdl_wait();
-    __shared__ float red[32];
-    const int row = blockIdx.x;
-    const T *xr = x + (size_t)row * ldx;
-    float v[4][8];
+    __shared__ float red[8];
+    const int row = blockIdx.x * 2 + half;
+    const bool live = row < M;
+    const T *xr = x + (size_t)(live ? row : 0) * ldx;
+    float v[NG][8];
     float ss = 0.f;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int i = (threadIdx.x + k * blockDim.x) * 8;
-        if (i < d) {
+    for (int k = 0; k < NG; ++k) {
+        const int i = (t + k * 128) * 8;
+        if (live && i < d) {
             load8(xr + i, v[k]);
 #pragma unroll
             for (int j = 0; j < 8; ++j) ss += v[k][j] * v[k][j];
@@ -109,24 +119,31 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const T *x, int ldx, const
     ss = warp_sumf(ss);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
     __syncthreads();
-    ss = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    if (threadIdx.x < 32) {
-        ss = warp_sumf(ss);
-        if (threadIdx.x == 0) red[0] = ss;
-    }
-    __syncthreads();
-    const float inv = rsqrtf(red[0] / d + eps);
+    const float tot = (red[half * 4] + red[half * 4 + 1]) + (red[half * 4 + 2] + red[half * 4 + 3]);
+    if (!live) return;
+    const float inv = rsqrtf(tot / d + eps);
     bf16 *o = out + (size_t)row * ldo;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int i = (threadIdx.x + k * blockDim.x) * 8;
+    for (int k = 0; k < NG; ++k) {
+        const int i = (t + k * 128) * 8;
         if (i < d) {
-            float wv[8];
-            load8(w + i, wv);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[k][j] = v[k][j] * inv * wv[j];
+            for (int j = 0; j < 8; ++j) v[k][j] = v[k][j] * inv * wv[k][j];
             store8(o + i, v[k]);
         }
+    }
+}
+
+template <class T>
+void launch_rmsnorm2(const T *x, int ldx, const float *w, int M, int d, float eps, bf16 *out, int ldo, cudaStream_t st) {
+    const int ng = (d / 8 + 127) / 128;
+    const int grid = (M + 1) / 2;
+    switch (ng) {
+#define RS_NG(n) \
+    case n: launch_pdl(rmsnorm2_kernel<T, n>, grid, 256, 0, st, x, ldx, w, M, d, eps, out, ldo); break;
+        RS_NG(1) RS_NG(2) RS_NG(3) RS_NG(4) RS_NG(5) RS_NG(6) RS_NG(7) RS_NG(8)
+#undef RS_NG
+        default: throw std::invalid_argument("rmsnorm: d must be <= 8192");
     }
 }
 
@@ -268,8 +285,7 @@ void k_rmsnorm(const float *x, int ldx, const float *w, int M, int d, float eps,
     if (M <= 0) return;
     ProfScope prof("norm", 0, (double)M * d * 6.0, st);
     if (d % 8 || d > 8192) throw std::invalid_argument("rmsnorm: d must be a multiple of 8 and <= 8192");
-    launch_pdl(rmsnorm_kernel<float>, M, std::min(256, std::max(32, (d / 8 + 31) / 32 * 32)), 0, st, x, ldx, w, M, d,
-               eps, out, ldo);
+    launch_rmsnorm2(x, ldx, w, M, d, eps, out, ldo, st);
     RS_LAUNCHED();
 }
 
@@ -278,8 +294,7 @@ void k_rmsnorm_bf16(const bf16 *x, int ldx, const float *w, int M, int d, float 
     if (M <= 0) return;
     ProfScope prof("norm", 0, (double)M * d * 4.0, st);
     if (d % 8 || d > 8192) throw std::invalid_argument("rmsnorm: d must be a multiple of 8 and <= 8192");
-    launch_pdl(rmsnorm_kernel<bf16>, M, std::min(256, std::max(32, (d / 8 + 31) / 32 * 32)), 0, st, x, ldx, w, M, d,
-               eps, out, ldo);
+    launch_rmsnorm2(x, ldx, w, M, d, eps, out, ldo, st);
     RS_LAUNCHED();
 }
 
