@@ -279,7 +279,7 @@ __device__ __forceinline__ void epi2_qkv_rope(const GemmEpi &ep, uint32_t taddr,
 template <int BT, int EPI>
 __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmEpi ep, int F,
-                 int T, int K, int splits, int *sem, long long *g2trace, int g2slot) {
+                 int T, int K, int splits, int *sem, float *ws, long long *g2trace, int g2slot) {
     using C = Cfg2<BT>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -293,6 +293,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
     float(*stg_all)[33] = reinterpret_cast<float(*)[33]>(smem + C::kStages * C::kStageBytes + 256);
     int4 *tok_tab = reinterpret_cast<int4 *>(smem + C::kStages * C::kStageBytes + 256 + C::kStgBytes);  // [BT]
 
+    __shared__ int s_last;  // split-K: this CTA holds the last partial of its tile
     pdl_trigger();
     if (g2trace && blockIdx.x == 0 && threadIdx.x == 0) g2trace[g2slot * 8 + 0] = clock64();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -428,14 +429,71 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
             mbar_wait(&tfull[acc], (it >> 1) & 1);
             if (g2trace && blockIdx.x == 0 && threadIdx.x == 128 && it == 0) g2trace[g2slot * 8 + 4] = clock64();
             tc_fence_after();
-            if (EPI == kEpiResidual && splits > 1) {
-                int v;
-                do {
-                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(sem + tile) : "memory");
-                    if (v < 2 * split) __nanosleep(32);
-                } while (v < 2 * split);  // both CTAs of the predecessor split are done
-            }
             const uint32_t tb = tmem_base + acc * BT + (static_cast<uint32_t>(q * 32) << 16);
+            if (EPI == kEpiResidual && splits > 1) {
+                // Split-K without hand-offs: every split parks its fp32 partial (this CTA's 128
+                // features x BT tokens, token-major) in the workspace; the split that arrives last
+                // sums ALL partials in split order -- the same order whichever split is last -- back
+                // into its accumulator and runs the one residual epilogue.
+                const int slot = tile * 2 + (int)rank;
+                float *mine = ws + ((size_t)slot * splits + split) * (128 * BT);
+                const int f = q * 32 + lane;
+                // feature-major: thread f owns ws[f][0 .. BT), 16-byte stores / loads
+                float4 *mrow = reinterpret_cast<float4 *>(mine + (size_t)f * BT);
+#pragma unroll 1
+                for (int c = 0; c < BT / 32; ++c) {
+                    uint32_t v[32];
+                    tmem_ld32(tb + c * 32, v);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        __stcg(mrow + c * 8 + j, make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                             __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])));
+                }
+                __threadfence();
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (q == 0 && lane == 0) s_last = atomicAdd(sem + slot, 1) == splits - 1;
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (!s_last) {
+                    tc_fence_before();
+                    mbar_arrive_remote(lead_tempty + 8 * acc);
+                    continue;
+                }
+                __threadfence();
+                const float4 *base = reinterpret_cast<const float4 *>(ws + (size_t)slot * splits * (128 * BT) + (size_t)f * BT);
+                constexpr int kSplitStride = 128 * BT / 4;  // float4s between consecutive splits
+#pragma unroll 1
+                for (int c = 0; c < BT / 32; ++c) {
+                    float4 a[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) a[j] = __ldcg(base + c * 8 + j);
+#pragma unroll 1
+                    for (int sp = 1; sp < splits; ++sp) {
+                        float4 b[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) b[j] = __ldcg(base + (size_t)sp * kSplitStride + c * 8 + j);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            a[j].x += b[j].x;
+                            a[j].y += b[j].y;
+                            a[j].z += b[j].z;
+                            a[j].w += b[j].w;
+                        }
+                    }
+                    uint32_t v[32];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        v[4 * j] = __float_as_uint(a[j].x);
+                        v[4 * j + 1] = __float_as_uint(a[j].y);
+                        v[4 * j + 2] = __float_as_uint(a[j].z);
+                        v[4 * j + 3] = __float_as_uint(a[j].w);
+                    }
+                    tmem_st32(tb + c * 32, v);
+                }
+                tmem_st_wait();
+                tc_fence_before();
+                if (q == 0 && lane == 0) sem[slot] = 0;  // ready for the next launch
+                tc_fence_after();
+            }
             if constexpr (EPI == kEpiQKVRope) {
 #pragma unroll 1
                 for (int c = 0; c < BT / 32; ++c)
@@ -458,11 +516,6 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
             tc_fence_before();
             mbar_arrive_remote(lead_tempty + 8 * acc);
             if (g2trace && blockIdx.x == 0 && threadIdx.x == 128 && it == 0) g2trace[g2slot * 8 + 5] = clock64();
-            if (EPI == kEpiResidual && splits > 1) {
-                __threadfence();
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (q == 0 && lane == 0) atomicAdd(sem + tile, 1);
-            }
         }
     }
     tc_fence_before();
@@ -500,16 +553,28 @@ void launch2(const GemmArgs &g, cudaStream_t st) {
     const int num_k = (g.K + kBK - 1) / kBK;
     const int splits = EPI == kEpiResidual ? std::max(1, std::min(gemm2_splits(g), num_k)) : 1;
     int *sem = nullptr;
+    float *ws = nullptr;
     if (splits > 1) {
+        // per host thread (engine / learner streams never share them): arrival counters, zero
+        // between launches (the last split resets its own), and the partial-tile workspace
         static thread_local int *sems = nullptr;
         static thread_local int sems_n = 0;
-        if (sems_n < tiles) {
+        static thread_local float *wsb = nullptr;
+        static thread_local size_t ws_n = 0;
+        if (sems_n < 2 * tiles) {
             if (sems) cudaFree(sems);
-            sems_n = std::max(tiles, 4096);
+            sems_n = std::max(2 * tiles, 8192);
             RS_CUDA(cudaMalloc(&sems, (size_t)sems_n * sizeof(int)));
+            RS_CUDA(cudaMemsetAsync(sems, 0, (size_t)sems_n * sizeof(int), st));
         }
-        RS_CUDA(cudaMemsetAsync(sems, 0, (size_t)tiles * sizeof(int), st));
+        const size_t need = (size_t)2 * tiles * splits * 128 * BT;
+        if (ws_n < need) {
+            if (wsb) cudaFree(wsb);
+            ws_n = need;
+            RS_CUDA(cudaMalloc(&wsb, ws_n * sizeof(float)));
+        }
         sem = sems;
+        ws = wsb;
     }
     const int pairs = std::min(tiles * splits, num_sms2() / 2);
     // diagnostics (RS_TUNE gemm_trace=1): per launch of CTA 0: start, after the dependency wait,
@@ -517,7 +582,7 @@ void launch2(const GemmArgs &g, cudaStream_t st) {
     static long long *tr = nullptr;
     static int slot = 0;
     if (tuning().gemm_trace && !tr) RS_CUDA(cudaMalloc(&tr, 8 * 8 * 4096));
-    launch_pdl(gemm2_kernel<BT, EPI>, dim3(2 * pairs), kThr, C::kSmem, st, tw, tx, g.epi, F, T, g.K, splits, sem,
+    launch_pdl(gemm2_kernel<BT, EPI>, dim3(2 * pairs), kThr, C::kSmem, st, tw, tx, g.epi, F, T, g.K, splits, sem, ws,
                tuning().gemm_trace ? tr : (long long *)nullptr, slot);
     if (tuning().gemm_trace) {
         RS_CUDA(cudaStreamSynchronize(st));

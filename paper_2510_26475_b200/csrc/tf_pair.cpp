@@ -91,7 +91,7 @@ struct Workspace {
     }
 };
 
-void gemm(const void *A, int lda, const void *B, int M, int N, int K, GemmEpi epi, cudaStream_t st) {
+void gemm(const void *A, int lda, const void *B, int M, int N, int K, GemmEpi epi, cudaStream_t st, int splits = 0) {
     GemmArgs g;
     g.A = A;
     g.B = B;
@@ -101,7 +101,7 @@ void gemm(const void *A, int lda, const void *B, int M, int N, int K, GemmEpi ep
     g.lda = lda;
     g.ldb = K;
     g.epi = epi;
-    g.splits = 0;  // residual epilogue: split-K by (N, K) only (gemm_2sm.cu)
+    g.splits = splits;  // residual epilogue: 0 = split-K by (N, K) only (gemm_2sm.cu), else fixed per weight
     // block_n auto: the tile width that best fills one wave of 148 SMs (gemm_sm100.cu)
     gemm_bf16(g, st);
 }
@@ -121,6 +121,14 @@ GemmEpi epi_resid(float *out, int ldo) {
     e.ldo = ldo;
     return e;
 }
+
+// Split-K of the DRAFTER's residual GEMMs (fc, O, down). The drafter runs at 256-ish rows, where
+// a 2048-feature output is only 8 SM-pair tiles: without splitting, 8 of 74 pairs walk the whole
+// K (down: 172 k-blocks). The count is fixed per weight matrix (a function of K only), never of
+// the row count, so a row's partial-sum order -- and its bits -- does not depend on its batch.
+// Measured at 256 rows (tools/gemm_split_sweep.py): down 49.8 -> 33.6 us and fc 30.4 -> 24.0 us
+// at 2 splits; more splits lose to the last-arriving CTA's reduction of the partials.
+int drafter_splits(int K) { return K >= 4096 ? 2 : 1; }
 GemmEpi epi_swiglu(void *out, int ldo) {
     GemmEpi e;
     e.kind = kEpiSwiGLU2;  // gate/up rows interleaved pairwise (model layout)
@@ -404,6 +412,12 @@ struct TransformerPair : ModelPair {
         }
     }
 
+    // EAGLE fc: w.x = fin . fc_w^T over the gathered low/mid/high features (split-K into zeroed rows).
+    void drafter_fc(int M, cudaStream_t st) {
+        RS_CUDA(cudaMemsetAsync(w.x.p, 0, (size_t)M * s.d * sizeof(float), st));
+        gemm(w.fin.p, 3 * s.d, drf->fc_w, M, s.d, 3 * s.d, epi_resid(w.x.p, s.d), st, drafter_splits(3 * s.d));
+    }
+
     // EAGLE drafter layer over rows whose residual input f is in w.x.
     void drafter_layer(const SdDev &d, int M, int ni, cudaStream_t st) {
         const int qd = s.qkv_dim(), HD = s.H * s.hd, d2 = 2 * s.d;
@@ -424,10 +438,10 @@ struct TransformerPair : ModelPair {
         else
             k_attention(w.q.p, w.rows.p, w.items.p, ni, kv_d, 0, drf->s, w.ao.p, st,
                         prof_enabled() ? bt.attn_flops(s) : 0, prof_enabled() ? bt.attn_bytes(s) : 0);
-        gemm(w.ao.p, HD, drf->layer.o_w, M, s.d, HD, epi_resid(w.x.p, s.d), st);
+        gemm(w.ao.p, HD, drf->layer.o_w, M, s.d, HD, epi_resid(w.x.p, s.d), st, drafter_splits(HD));
         k_rmsnorm(w.x.p, s.d, drf->layer.ln2, M, s.d, s.eps, w.xn.p, s.d, st);
         gemm(w.xn.p, s.d, drf->layer.gu_w, M, 2 * s.dff, s.d, epi_swiglu(w.h.p, s.dff), st);
-        gemm(w.h.p, s.dff, drf->layer.down_w, M, s.d, s.dff, epi_resid(w.x.p, s.d), st);
+        gemm(w.h.p, s.dff, drf->layer.down_w, M, s.d, s.dff, epi_resid(w.x.p, s.d), st, drafter_splits(s.dff));
     }
 
     // Drafter LM head over n normalised rows in w.xn -> Q rows dst[m]; every drafted row is
@@ -490,7 +504,7 @@ struct TransformerPair : ModelPair {
                 stage.upload(w.idx.p, hid, st);
                 const int M = bt.M();
                 k_gather_features(w.rows.p, M, s.d, feat.p, max_ctx, nullptr, w.fin.p, nullptr, st);
-                gemm(w.fin.p, 3 * s.d, drf->fc_w, M, s.d, 3 * s.d, epi_f32(w.x.p, s.d, 1.0f, nullptr), st);
+                drafter_fc(M, st);
                 drafter_layer(d, M, (int)bt.items.size(), st);
                 drafter_head(w.map_a.p, w.map_b.p, (int)head_src.size(), Q, const_cast<double *>(d.Qst), st);
                 const int nh = (int)hid_src.size();
@@ -624,7 +638,7 @@ struct TransformerPair : ModelPair {
             bt.map_b = dst;
             upload(bt, st, tc_attn);
             k_gather_features(w.rows.p, M, s.d, feat.p, max_ctx, nullptr, w.fin.p, nullptr, st);
-            gemm(w.fin.p, 3 * s.d, drf->fc_w, M, s.d, 3 * s.d, epi_f32(w.x.p, s.d, 1.0f, nullptr), st);
+            drafter_fc(M, st);
             drafter_layer(d, M, (int)bt.items.size(), st);
             if (R == 0) continue;
             drafter_head(w.map_a.p, w.map_b.p, R, Qb.p, nullptr, st);  // h_norm of the KD rows stays in w.xn
@@ -791,7 +805,7 @@ struct TransformerPair : ModelPair {
                 bt.map_b = dst;
                 upload(bt, st, tc_attn);
                 k_gather_features(w.rows.p, M, s.d, feat.p, max_ctx, nullptr, w.fin.p, nullptr, st);
-                gemm(w.fin.p, 3 * s.d, drf->fc_w, M, s.d, 3 * s.d, epi_f32(w.x.p, s.d, 1.0f, nullptr), st);
+                drafter_fc(M, st);
                 drafter_layer(d, M, (int)bt.items.size(), st);
                 if (n == 0) continue;
                 drafter_head(w.map_a.p, w.map_b.p, n, Qb.p, nullptr, st);
