@@ -131,11 +131,20 @@ __device__ __forceinline__ double prob(const RowRef<T> &r, const Stats &s, int x
     return exp(r.v(x) - s.m) * s.inv;
 }
 
+// L1 prefetch of a logit element's line: issued a tile-pair ahead in the full-vocabulary passes
+// so the loads of the next tiles are in flight while this pair's fp64 exps run (the passes are
+// otherwise bound by load latency -- long-scoreboard stalls on the fp32 -> fp64 converts).
+__device__ __forceinline__ void pf_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+struct NoPrefetch {
+    __device__ __forceinline__ void operator()(int) const {}
+};
+
 template <class T>
 struct ProbFn {
     RowRef<T> r;
     Stats s;
     __device__ __forceinline__ double operator()(int x) const { return prob(r, s, x); }
+    __device__ __forceinline__ void pf(int x) const { pf_l1(r.z + x); }
 };
 
 // p_cur after k sibling rejections: r_j = max(0, r_{j-1} - q1) / Z_j (specdec.cpp:209 -> :35-52)
@@ -154,6 +163,10 @@ struct PCurFn {
             for (int j = 0; j < k; ++j) r = fmax(0.0, r - qq) * Z[j];  // Z holds 1 / Z_j
         }
         return r;
+    }
+    __device__ __forceinline__ void pf(int x) const {
+        pf_l1(p.z + x);
+        if (k > 0) pf_l1(q.z + x);
     }
 };
 
@@ -202,13 +215,26 @@ __device__ double gather_masses(int nt, double *mass, double *red, const Cl &cl)
 // l + 32 j in j order, then the warp butterfly -- whichever warp / CTA owns the tile. Each CTA
 // of the cluster takes a contiguous tile range; a warp handles two tiles per iteration with
 // all 16 column values fetched before any is summed (memory-level parallelism).
-template <class F>
-__device__ double tile_sums(const F &f, int V, double *mass, double *red, const Cl &cl) {
+template <class F, class P>
+__device__ double tile_sums(const F &f, const P &pf, int V, double *mass, double *red, const Cl &cl) {
     const int nt = ntiles_of(V);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int t0 = cl_tile0(cl, cl.rank, nt), t1 = cl_tile0(cl, cl.rank + 1, nt);
+    auto touch = [&](int tt) {
+        if (tt >= t1) return;
+        const int hi = tile_hi(tt, V);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int x = tile_lo(tt) + lane + 32 * j;
+            if (x < hi) pf(x);
+        }
+    };
+    touch(t0 + w);
+    touch(t0 + w + nw);
     for (int t = t0 + w; t < t1; t += 2 * nw) {
         const int u = t + nw;
+        touch(t + 2 * nw);
+        touch(u + 2 * nw);
         const int hi = tile_hi(t, V), hu = u < t1 ? tile_hi(u, V) : 0;
         double va[8], vb[8];
 #pragma unroll
@@ -236,6 +262,10 @@ __device__ double tile_sums(const F &f, int V, double *mass, double *red, const 
     }
     if (cl.rank == 0 && threadIdx.x == 0) mass[nt] = f(V - 1);
     return gather_masses(nt, mass, red, cl);
+}
+template <class F>
+__device__ __forceinline__ double tile_sums(const F &f, int V, double *mass, double *red, const Cl &cl) {
+    return tile_sums(f, NoPrefetch{}, V, mass, red, cl);
 }
 
 // Tile masses of a probability row straight from the GEMM partials.
@@ -444,7 +474,15 @@ __device__ RowRef<T> prow_ready(const SdDev &d, const Seq &q, int slot, const Cl
             double *g = const_cast<double *>(r.gst);
             const int nt = ntiles_of(r.V), lane = threadIdx.x & 31, nw = blockDim.x >> 5;
             const int t1 = cl_tile0(cl, cl.rank + 1, nt);
+            const float *zf = reinterpret_cast<const float *>(r.z);
+            auto touch = [&](int tt) {
+                if (tt >= t1) return;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (tile_lo(tt) + lane + 32 * j < tile_hi(tt, r.V)) pf_l1(zf + tile_lo(tt) + lane + 32 * j);
+            };
             for (int t = cl_tile0(cl, cl.rank, nt) + (threadIdx.x >> 5); t < t1; t += nw) {
+                touch(t + nw);
                 double m, s;
                 tile_stat(reinterpret_cast<const float *>(r.z), r.V, t, r.tau, lane, m, s);
                 if (lane == 0) {
@@ -468,7 +506,7 @@ __device__ int sample_row(const RowRef<T> &r, const Stats &st, double u, double 
         gemm_masses(r, st, mass);
         return inv_cdf(f, r.V, mass, 1.0, u, cs, redl, err);
     }
-    tile_sums(f, r.V, mass, red, cl);
+    tile_sums(f, [&](int x) { f.pf(x); }, r.V, mass, red, cl);
     return inv_cdf(f, r.V, mass, 1.0, u, cs, redl, err);
 }
 
@@ -537,7 +575,10 @@ __global__ void __launch_bounds__(512) draft_sample_kernel(SdDev d, int depth) {
         const Stats st = row_stats(row, red);
         if (!greedy) {
             if (row.gst) gemm_masses(row, st, mass);
-            else tile_sums(ProbFn<T>{row, st}, row.V, mass, red, cl);
+            else {
+                const ProbFn<T> pfn{row, st};
+                tile_sums(pfn, [&](int x) { pfn.pf(x); }, row.V, mass, red, cl);
+            }
         }
         for (int i = 0; i < d.t; ++i) {
             int c;
@@ -743,7 +784,13 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
                     for (int j = 0; j < k; ++j) rr = fmax(0.0, rr - qq) * Z[j];
                     return fmax(0.0, rr - qq);
                 };
-                const double z = tile_sums(res_k, d.V, mass, red, cl);
+                auto res_pf = [&](int x) {
+                    if (k == 0 || !cache) {
+                        pf_l1(p1.z + x);
+                        pf_l1(q1.z + x);
+                    }
+                };
+                const double z = tile_sums(res_k, res_pf, d.V, mass, red, cl);
                 if (z <= 1e-12 && cl.lead()) atomicCAS(d.err, 0, kErrResidual);
                 if (threadIdx.x == 0) Z[k] = 1.0 / z;
                 __syncthreads();
@@ -803,7 +850,7 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
                 int x = repl;
                 if (!greedy) {
                     auto res = [&](int y) { return fmax(0.0, prob(pd, sp, y) - prob(qd, sq, y)); };
-                    const double z = tile_sums(res, d.V, mass, red, cl);
+                    const double z = tile_sums(res, [&](int y) { pf_l1(pd.z + y); pf_l1(qd.z + y); }, d.V, mass, red, cl);
                     if (z <= 1e-12 && cl.lead()) atomicCAS(d.err, 0, kErrResidual);
                     const double zi = 1.0 / z;
                     auto rn = [&](int y) { return fmax(0.0, prob(pd, sp, y) - prob(qd, sq, y)) * zi; };
