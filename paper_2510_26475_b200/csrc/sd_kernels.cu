@@ -768,6 +768,9 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
                 // residual normaliser and its tile masses in one pass
                 // The first residual pass caches p1(x), q1(x) in fp64 (the same bits prob()
                 // returns); later sibling passes stream them instead of redoing two fp64 exps.
+                // With the cache, cache[x] holds p_k(x) -- the residual after k rejections,
+                // memoised pass by pass: one step of the recursion per pass instead of k, the
+                // same operations in the same order as the loop (so the same bits).
                 auto res_k = [&](int x) {
                     double rr, qq;
                     if (k == 0 || !cache) {
@@ -776,12 +779,14 @@ __global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int 
                         if (cache) {
                             cache[x] = rr;
                             cache[d.V + x] = qq;
+                        } else {
+                            for (int j = 0; j < k; ++j) rr = fmax(0.0, rr - qq) * Z[j];
                         }
                     } else {
-                        rr = __ldcg(cache + x);
                         qq = __ldcg(cache + d.V + x);
+                        rr = fmax(0.0, __ldcg(cache + x) - qq) * Z[k - 1];
+                        cache[x] = rr;
                     }
-                    for (int j = 0; j < k; ++j) rr = fmax(0.0, rr - qq) * Z[j];
                     return fmax(0.0, rr - qq);
                 };
                 auto res_pf = [&](int x) {
