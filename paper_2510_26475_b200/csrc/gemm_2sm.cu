@@ -41,7 +41,8 @@ namespace {
 
 constexpr int kBM = 128;  // weight rows per CTA (256 per pair)
 constexpr int kBK = 64;
-constexpr int kThr = 256;
+constexpr int kThr = 384;   // warps 0-3 control (TMA, MMA, TMEM), 4-11 epilogue
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quadrant, alternate 32-token chunks
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -90,7 +91,7 @@ struct Cfg2 {
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStages = (180 * 1024) / kStageBytes > 8 ? 8 : (180 * 1024) / kStageBytes;
     static constexpr int kTmemCols = 2 * BT <= 128 ? 128 : 2 * BT <= 256 ? 256 : 512;
-    static constexpr int kStgBytes = 32 * 132 * 4;  // epilogue transpose blocks (4 x 32 x 33 or 32 x 132 fp32)
+    static constexpr int kStgBytes = 2 * 32 * 132 * 4;  // per epilogue group: 4 x 32 x 33 or 32 x 132 fp32
     static constexpr int kSmem = 1024 + kStages * kStageBytes + 256 + kStgBytes + 256 * 16;
     // kind::f16, bf16 x bf16 -> f32, both K-major, N = BT tokens, M = 256 features (pair)
     static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BT >> 3) << 17) |
@@ -213,7 +214,7 @@ __device__ __forceinline__ void epi2_chunk(const GemmEpi &ep, uint32_t taddr, in
 // then every thread rotates 8-dim vectors (i, i + 64 pairs, rotate-half, Qwen2) and stores 16 B
 // into q [t][head] or the K / V cache slot of the token (RowDesc::seq / phys / pos).
 __device__ __forceinline__ void epi2_qkv_rope(const GemmEpi &ep, uint32_t taddr, int head, int q_warp, int t0, int T,
-                                              float (*stg)[132], const int4 *tok, int tbase) {
+                                              float (*stg)[132], const int4 *tok, int tbase, int bar) {
     const int lane = threadIdx.x & 31;
     const int dim = q_warp * 32 + lane;
     const QkvStore &s = ep.qkv;
@@ -236,7 +237,7 @@ __device__ __forceinline__ void epi2_qkv_rope(const GemmEpi &ep, uint32_t taddr,
     const float b = __bfloat162float(static_cast<const __nv_bfloat16 *>(ep.bias)[head * 128 + dim]);
 #pragma unroll
     for (int j = 0; j < 32; ++j) stg[j][dim] = __bfloat162float(__float2bfloat16(__uint_as_float(v[j]) + b));
-    asm volatile("bar.sync 2, 128;" ::: "memory");
+    asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int vi = tid + 128 * k, j = vi >> 4, g = vi & 15;  // token j, dims 8g .. 8g + 7
@@ -271,7 +272,7 @@ __device__ __forceinline__ void epi2_qkv_rope(const GemmEpi &ep, uint32_t taddr,
         for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
         *reinterpret_cast<int4 *>(dst + d0) = *reinterpret_cast<const int4 *>(h);
     }
-    asm volatile("bar.sync 2, 128;" ::: "memory");  // stg is reused by the next chunk
+    asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");  // stg is reused by the next chunk
 }
 
 // F = features (rows of W), T = tokens (rows of X). Units = (feature pair-tile, token tile, split),
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 2 * 128);  // both CTAs' epilogue threads
+            mbar_init(&tempty[a], 2 * 32 * kEpiWarps);  // both CTAs' epilogue threads
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -407,7 +408,10 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
         }
     } else if (warp >= 4) {
         pdl_wait();
-        const int q = warp - 4;  // TMEM lane quadrant
+        const int q = warp & 3;          // TMEM lane quadrant
+        const int grp = (warp - 4) >> 2;  // chunk parity of this warp's group
+        const int ebar = 2 + grp;         // named barrier of the group (QKV epilogue)
+        float(*stg_grp)[33] = stg_all + grp * 4 * 32;
         const uint32_t lead_tempty = mapa(tempty, 0);
         int it = 0;
         for (int unit = pair; unit < num_units; unit += npairs, ++it) {
@@ -418,13 +422,13 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
             if constexpr (EPI == kEpiQKVRope) {
                 // (pos, seq, phys) of the tile's tokens, staged while the MMAs still run
                 const RowDesc *rws = static_cast<const RowDesc *>(ep.qkv.rows);
-                asm volatile("bar.sync 2, 128;" ::: "memory");  // previous tile done with the table
-                for (int i = threadIdx.x - 128; i < BT; i += 128)
+                asm volatile("bar.sync 4, 256;" ::: "memory");  // previous tile done with the table
+                for (int i = threadIdx.x - 128; i < BT; i += 256)
                     if (t0 + i < T) {
                         const RowDesc r = rws[t0 + i];
                         tok_tab[i] = make_int4(r.pos, r.seq, r.phys, 0);
                     }
-                asm volatile("bar.sync 2, 128;" ::: "memory");
+                asm volatile("bar.sync 4, 256;" ::: "memory");
             }
             mbar_wait(&tfull[acc], (it >> 1) & 1);
             if (g2trace && blockIdx.x == 0 && threadIdx.x == 128 && it == 0) g2trace[g2slot * 8 + 4] = clock64();
@@ -441,7 +445,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                 // feature-major: thread f owns ws[f][0 .. BT), 16-byte stores / loads
                 float4 *mrow = reinterpret_cast<float4 *>(mine + (size_t)f * BT);
 #pragma unroll 1
-                for (int c = 0; c < BT / 32; ++c) {
+                for (int c = grp; c < BT / 32; c += 2) {
                     uint32_t v[32];
                     tmem_ld32(tb + c * 32, v);
 #pragma unroll
@@ -450,9 +454,9 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                                                              __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])));
                 }
                 __threadfence();
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (q == 0 && lane == 0) s_last = atomicAdd(sem + slot, 1) == splits - 1;
-                asm volatile("bar.sync 1, 128;" ::: "memory");
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (warp == 4 && lane == 0) s_last = atomicAdd(sem + slot, 1) == splits - 1;
+                asm volatile("bar.sync 1, 256;" ::: "memory");
                 if (!s_last) {
                     tc_fence_before();
                     mbar_arrive_remote(lead_tempty + 8 * acc);
@@ -462,7 +466,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                 const float4 *base = reinterpret_cast<const float4 *>(ws + (size_t)slot * splits * (128 * BT) + (size_t)f * BT);
                 constexpr int kSplitStride = 128 * BT / 4;  // float4s between consecutive splits
 #pragma unroll 1
-                for (int c = 0; c < BT / 32; ++c) {
+                for (int c = grp; c < BT / 32; c += 2) {
                     float4 a[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) a[j] = __ldcg(base + c * 8 + j);
@@ -491,27 +495,27 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                 }
                 tmem_st_wait();
                 tc_fence_before();
-                if (q == 0 && lane == 0) sem[slot] = 0;  // ready for the next launch
+                if (warp == 4 && lane == 0) sem[slot] = 0;  // ready for the next launch
                 tc_fence_after();
             }
             if constexpr (EPI == kEpiQKVRope) {
 #pragma unroll 1
-                for (int c = 0; c < BT / 32; ++c)
+                for (int c = grp; c < BT / 32; c += 2)
                     epi2_qkv_rope(ep, tb + c * 32, f0 / 128, q, t0 + c * 32, T,
-                                  reinterpret_cast<float(*)[132]>(stg_all), tok_tab, t0);
+                                  reinterpret_cast<float(*)[132]>(stg_grp), tok_tab, t0, ebar);
             } else if constexpr (EPI == kEpiResidual) {
                 // software-pipelined: chunk c + 1's residual rows are in flight while chunk c is done
                 float4 cur[2][8];
-                resid_prefetch(ep, f0 + q * 32, t0, F, T, cur[0]);
+                if (grp < BT / 32) resid_prefetch(ep, f0 + q * 32, t0 + grp * 32, F, T, cur[0]);
 #pragma unroll
-                for (int c = 0; c < BT / 32; ++c) {
-                    if (c + 1 < BT / 32) resid_prefetch(ep, f0 + q * 32, t0 + (c + 1) * 32, F, T, cur[(c + 1) & 1]);
-                    epi2_chunk<EPI>(ep, tb + c * 32, f0 + q * 32, t0 + c * 32, F, T, stg_all + q * 32, cur[c & 1]);
+                for (int i = 0, c = grp; c < BT / 32; ++i, c += 2) {
+                    if (c + 2 < BT / 32) resid_prefetch(ep, f0 + q * 32, t0 + (c + 2) * 32, F, T, cur[(i + 1) & 1]);
+                    epi2_chunk<EPI>(ep, tb + c * 32, f0 + q * 32, t0 + c * 32, F, T, stg_grp + q * 32, cur[i & 1]);
                 }
             } else {
 #pragma unroll 1
-                for (int c = 0; c < BT / 32; ++c)
-                    epi2_chunk<EPI>(ep, tb + c * 32, f0 + q * 32, t0 + c * 32, F, T, stg_all + q * 32);
+                for (int c = grp; c < BT / 32; c += 2)
+                    epi2_chunk<EPI>(ep, tb + c * 32, f0 + q * 32, t0 + c * 32, F, T, stg_grp + q * 32);
             }
             tc_fence_before();
             mbar_arrive_remote(lead_tempty + 8 * acc);
