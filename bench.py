@@ -48,6 +48,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--kd", type=int, default=4, help="rollouts per GPU in the online KD update leg (0 = off)")
     p.add_argument("--no-tuner-leg", action="store_true", help="skip the dynamic-tuning (cfg3-style) leg")
+    p.add_argument("--no-b256-leg", action="store_true", help="skip the batch-256 north-star leg")
     p.add_argument("--tuner", action="store_true",
                    help="dynamic SD-config tuning (cfg3): measured ProfileTable over power-of-two buckets, re-solved "
                         "every cycle from the live batch")
@@ -198,6 +199,46 @@ def measured_peaks():
             with open(p) as f:
                 return json.load(f), "measured"
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def batch256_leg(args, rb, target, drafter, dev, stream, cfg, peaks):
+    """North-star check (BASELINE.json north_star): the same SD step at batch 256 on one GPU --
+    tokens/s and the verify GEMM family's achieved TFLOP/s against the measured sustained peak
+    (target >= 60 % tensor utilisation). Device time of 4 steps after 2 warm-up steps; the GEMM
+    figure from the per-kernel profiler over 2 further steps."""
+    import random
+    import torch
+    rng = random.Random(256)
+    n_steps, n_warm = 4, 2
+    s, t, n = map(int, args.sd.split(","))
+    max_len = (n_warm + 2 * n_steps + 4) * (s * n + 1) + 8
+    reqs = [rb.RequestState(i, [rng.randrange(target.shape.vocab - 1) for _ in range(args.ctx)], -20.0, max_len,
+                            rb.DecodeRng.from_seed(99, i)) for i in range(256)]
+    eng = rb.BatchEngine(target, lambda: drafter, None, rb.TimingModel(), reqs, cfg, args.verify,
+                         record_full_logprobs=False, device=dev)
+    for _ in range(n_warm):
+        eng.step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    tokens = 0
+    for _ in range(n_steps):
+        tokens += eng.step().emitted_tokens
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    rb.device_profile(enable=True, reset=True)
+    for _ in range(2):
+        eng.step()
+    prof = rb.device_profile(enable=False)
+    g = prof.get("verify.gemm")
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    ach = g["flops"] / (g["ms"] / 1000.0) / 1e12 if g else None
+    del eng
+    return {"batch": 256, "value": round(tokens / (ms / 1000.0), 1), "unit": "tokens/s",
+            "ms_per_step": round(ms / n_steps, 3), "verify_gemm_tflops": round(ach, 1) if ach else None,
+            "verify_gemm_frac_of_sustained_peak": round(ach / peak, 4) if ach else None,
+            "north_star_target": ">= 0.60 tensor utilisation in verification"}
 
 
 def tuner_leg(args, rb, target, drafter, reqs, dev, stream, max_len, cfg, world, barrier):
@@ -421,6 +462,9 @@ def main():
     dyn = None
     if not args.tuner and not args.no_tuner_leg:
         dyn = tuner_leg(args, rb, target, drafter, reqs, dev, stream, max_len, cfg, world, barrier)
+    b256 = None
+    if world == 1 and args.model == "3b" and args.batch != 256 and not args.no_b256_leg:
+        b256 = batch256_leg(args, rb, target, drafter, dev, stream, cfg, measured_peaks()[0])
 
     if world > 1:
         import torch.distributed as dist
@@ -480,7 +524,7 @@ def main():
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_tok / e2e_s, 1), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps)},
-            "gpu_launches": launches, "clocks": clk, "breakdown_ms_per_step": breakdown, "kd_update": kd}
+            "gpu_launches": launches, "clocks": clk, "breakdown_ms_per_step": breakdown, "kd_update": kd, "north_star_batch256": b256}
     if dyn:
         line["dynamic_tuning"] = dyn
     if tuner:
