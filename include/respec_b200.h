@@ -225,6 +225,11 @@ int rs_engine_set_drafter(rs_engine *e, const rs_model *drafter);
 /* stop_at_eos = 0 (before the first step): EOS neither stops a drafted chain nor ends a request
    (spec_step_tree(..., stop_at_eos = false), as profile() runs it, server.cpp:215). */
 int rs_engine_set_stop_at_eos(rs_engine *e, int32_t stop);
+/* A request's DecodeRng (draft + accept mt19937_64 streams) as an opaque image of `n` words
+   (query n with out = NULL): export after a step, import into a new engine before its first
+   step -- spec_step_tree's DecodeRng& continuation across calls (rng.hpp:33-47). */
+int rs_engine_rng_export(const rs_engine *e, int32_t req, uint64_t *out, int64_t cap, int64_t *n);
+int rs_engine_rng_import(rs_engine *e, int32_t req, const uint64_t *in, int64_t n);
 /* BatchEngine::step (server.cpp:266-349); throws "BatchEngine: empty batch" when done. */
 int rs_engine_step(rs_engine *e, rs_step_info *info);
 int rs_engine_all_done(const rs_engine *e, int32_t *out);

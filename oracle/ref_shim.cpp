@@ -293,6 +293,22 @@ json learner_metrics_json(const std::vector<LearnerMetrics> & ms) {
 }
 
 // OnlineLearner driven by a script of iterations: {"feed": [samples], "boundary": it, "await": bool}.
+// generate (specdec.cpp:271-316) on one sequence, plus mean_accept_len.
+json op_generate(const json & req) {
+    TabularARModel target = model_of(req.at("target"));
+    TabularARModel drafter = model_of(req.at("drafter"));
+    DecodeRng rng = DecodeRng::from_seed(req.at("seed").get<uint64_t>(), req.value("stream", uint64_t{0}));
+    GenerateResult g = generate(target, drafter, Context{req.at("prompt").get<std::vector<int>>()}, cfg_of(req.at("cfg")),
+                                req.at("max_len").get<int>(), rng, req.value("eos_bias", 0.0), req.value("stop_at_eos", true));
+    json steps = json::array();
+    for (const auto & st : g.steps) steps.push_back(step_json(st, false));
+    json ledger = json::array();
+    for (const auto & e : g.ledger.events) ledger.push_back({e.role == ModelRole::Target ? 1 : 0, e.positions_evaluated, e.concurrent_batch_tokens});
+    json out = {{"tokens", g.tokens}, {"steps", steps}, {"accept_lens", g.accept_lens}, {"ledger", ledger}, {"ended_eos", g.ended_eos}};
+    if (!g.accept_lens.empty()) out["mean_accept_len"] = mean_accept_len(g.accept_lens);
+    return out;
+}
+
 json op_online_learner(const json & req) {
     OnlineLearner l(model_of(req.at("drafter")), policy_of(req.at("policy")), req.at("selection_seed").get<uint64_t>(),
                     req.value("cost_per_token", 0.0), req.value("capacity", size_t{4096}), req.value("async", false));
@@ -369,6 +385,7 @@ json dispatch(const json & req) {
     if (op == "reward") return op_reward(req);
     if (op == "time_generation") return op_time_generation(req);
     if (op == "online_learner") return op_online_learner(req);
+    if (op == "generate") return op_generate(req);
     if (op == "policy_update") return op_policy_update(req);
     if (op == "group_advantages") return op_group_advantages(req);
     if (op == "build_profile") return op_build_profile(req);

@@ -134,7 +134,7 @@ EXPORTED_SYMBOLS = [
     "rs_learner_total_sim_time", "rs_learner_buffer_size", "rs_learner_metrics",
     "rs_reward", "rs_group_advantages", "rs_policy_update_tabular",
     "rs_engine_set_stop_at_eos", "rs_profile_simulated", "rs_tabular_random", "rs_skew_eos_biases",
-    "rs_engine_kd_grad",
+    "rs_engine_kd_grad", "rs_engine_rng_export", "rs_engine_rng_import",
 ]
 
 _lib = None
@@ -240,6 +240,8 @@ def lib():
             "rs_tabular_random": ([vp, i32, i32, dbl, dbl, u64, P(vp)], ctypes.c_int),
             "rs_skew_eos_biases": ([u64, i32, P(dbl)], ctypes.c_int),
             "rs_engine_kd_grad": ([vp, vp, P(i32), i32, P(dbl), vp, i32, P(dbl)], ctypes.c_int),
+            "rs_engine_rng_export": ([vp, i32, P(u64), i64, P(i64)], ctypes.c_int),
+            "rs_engine_rng_import": ([vp, i32, P(u64), i64], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -731,11 +733,14 @@ class ProfileTable:
 
 
 # ---- requests / records ------------------------------------------------------------------------------------
-@dataclass(frozen=True)
+@dataclass
 class DecodeRng:
-    """DecodeRng::from_seed(seed, stream_id) (rng.hpp:37-43); the streams live on the device."""
+    """DecodeRng::from_seed(seed, stream_id) (rng.hpp:37-43); the streams live on the device.
+    `state` is the advanced stream image after spec_step_tree / generate consumed draws from it
+    (None = freshly seeded); an engine created with this rng continues where it stopped."""
     seed: int = 0
     stream_id: int = 0
+    state: Optional[object] = field(default=None, compare=False, repr=False)
 
     @staticmethod
     def from_seed(seed: int, stream_id: int = 0) -> "DecodeRng":
@@ -841,6 +846,21 @@ class BatchEngine:
                                       forced._c(), self._vmode, 1 if record_full_logprobs else 0, ctypes.byref(h)))
         self.handle = h
         self.last_info = None
+        for i, r in enumerate(self._reqs):  # continue advanced DecodeRng streams
+            if r.rng.state is not None:
+                _check(lib().rs_engine_rng_import(self.handle, i, r.rng.state, len(r.rng.state)))
+
+    def set_stop_at_eos(self, stop: bool) -> None:
+        """stop_at_eos = False (before the first step): EOS is an ordinary token (server.cpp:215)."""
+        _check(lib().rs_engine_set_stop_at_eos(self.handle, 1 if stop else 0))
+
+    def rng_state(self, req: int):
+        """The request's advanced DecodeRng stream image (rs_engine_rng_export)."""
+        n = ctypes.c_int64()
+        _check(lib().rs_engine_rng_export(self.handle, req, None, 0, ctypes.byref(n)))
+        buf = (ctypes.c_uint64 * n.value)()
+        _check(lib().rs_engine_rng_export(self.handle, req, buf, n.value, ctypes.byref(n)))
+        return buf
 
     def step(self):
         """One engine cycle (server.cpp:266-349); raises EngineError on an empty batch."""
@@ -1002,6 +1022,137 @@ def run_generation(requests: Sequence[RequestState], target: Model, drafter: Opt
     al = [a for r in reqs for a in r.accept_lens]
     return GenerationRun(samples, eng.ledger_time(), al, eng.switches(), eng.active_trace(), eng.ledger(),
                          eng.cycles(), eng.prefill_events(), wall)
+
+
+# ---- single-sequence API (specdec.hpp:58-131) -------------------------------------------------------------------
+@dataclass
+class RoundCost:
+    """RoundCost (specdec.hpp:58-63)."""
+    drafter_forwards: int = 0
+    drafter_tokens_each: int = 0
+    target_tokens: int = 0
+
+
+@dataclass
+class VerifyOutcome:
+    """VerifyOutcome (specdec.hpp:65-75). draft_records holds the number of drafted positions
+    (one DraftPosRecord each in the reference)."""
+    accepted_tokens: List[int]
+    accept_len: int
+    bonus_token: int
+    steps: List[StepRecord]
+    rounds: List[RoundCost]
+    ended: bool
+    draft_records: int = 0
+
+
+def _rounds_of(ledger) -> List[RoundCost]:
+    """Per-round costs of a single-sequence cycle from its forward events (charge_batched_cycle
+    over one outcome, server.cpp:154-178): `drafter_forwards` drafter passes of t tokens, then one
+    target pass of t*n_eff + 1 tokens."""
+    out, fw, each = [], 0, 0
+    for role, _, tokens in ledger:
+        if role == 0:
+            fw += 1
+            each = tokens
+        else:
+            out.append(RoundCost(fw, each, tokens))
+            fw, each = 0, 0
+    return out
+
+
+def spec_step_tree(target: Model, drafter: Model, ctx: Sequence[int], cfg: SDConfig, rng: DecodeRng,
+                   eos_bias: float = 0.0, stop_at_eos: bool = True, max_emit: int = 2 ** 31 - 1,
+                   record_full_logprobs: bool = True) -> VerifyOutcome:
+    """spec_step_tree (specdec.cpp:146-269): ONE verification cycle of one sequence on the GPU
+    engine. `rng` is advanced in place (DecodeRng& in the reference), so consecutive calls
+    continue the same draft / accept streams."""
+    if not cfg.enabled:
+        raise InvalidArgument("spec_step_tree: SD config must be enabled")
+    cap = cfg.rounds * cfg.draft_len + 1  # the most one cycle can emit
+    req = RequestState(0, list(ctx), eos_bias, max(1, min(max_emit, cap)), rng)
+    eng = BatchEngine(target, lambda: drafter, None, TimingModel(), [req], cfg, "sample", record_full_logprobs,
+                      getattr(target, "device", None))
+    eng.set_stop_at_eos(stop_at_eos)
+    eng.step()
+    r = eng.requests()[0]
+    rng.state = eng.rng_state(0)
+    steps = r.steps
+    eos = target.vocab_size - 1
+    ended = bool(stop_at_eos and r.generated and r.generated[-1] == eos)
+    bonus = steps[-1].token if steps and not steps[-1].drafted else -1
+    rounds = _rounds_of(eng.ledger())
+    return VerifyOutcome(list(r.generated), r.accept_lens[0] if r.accept_lens else 0, bonus, steps, rounds, ended,
+                         sum(x.target_tokens - 1 for x in rounds))
+
+
+def spec_step_chain(target: Model, drafter: Model, ctx: Sequence[int], k: int, rng: DecodeRng,
+                    eos_bias: float = 0.0, stop_at_eos: bool = True) -> VerifyOutcome:
+    """spec_step_chain (specdec.cpp:78-144) == spec_step_tree with tree(1, 1, k) (specdec.hpp:108-113)."""
+    return spec_step_tree(target, drafter, ctx, SDConfig.chain(k), rng, eos_bias, stop_at_eos)
+
+
+@dataclass
+class GenerateResult:
+    """GenerateResult (specdec.hpp:117-123)."""
+    tokens: List[int]
+    steps: List[StepRecord]
+    accept_lens: List[int]
+    ledger: List[tuple]
+    ended_eos: bool = False
+
+
+def _naive_step(target: Model, ctx: Sequence[int], rng: DecodeRng, eos_bias: float) -> StepRecord:
+    """One target sample on the DRAFT stream (specdec.cpp:281-291 / server.cpp:328-347)."""
+    eng = BatchEngine(target, None, None, TimingModel(), [RequestState(0, list(ctx), eos_bias, 1, rng)],
+                      SDConfig.off(), "sample", True, getattr(target, "device", None))
+    eng.set_stop_at_eos(True)
+    eng.step()
+    rng.state = eng.rng_state(0)
+    return eng.requests()[0].steps[0]
+
+
+def generate(target: Model, drafter: Optional[Model], prompt: Sequence[int], cfg: SDConfig, max_len: int,
+             rng: DecodeRng, eos_bias: float = 0.0, stop_at_eos: bool = True) -> GenerateResult:
+    """generate (specdec.cpp:271-316): one sequence to EOS or max_len -- naive target steps on the
+    DRAFT stream when the config is off or one token is left (specdec.cpp:293-297), otherwise a
+    spec_step_tree cycle capped at the remaining budget -- every cycle on the GPU engine."""
+    if max_len < 1:
+        raise InvalidArgument("generate: max_len must be >= 1")
+    eos = target.vocab_size - 1
+    res = GenerateResult([], [], [], [], False)
+    ctx = list(prompt)
+    while len(res.tokens) < max_len and not res.ended_eos:
+        remaining = max_len - len(res.tokens)
+        if not cfg.enabled or remaining == 1:
+            st = _naive_step(target, ctx, rng, eos_bias)
+            res.steps.append(st)
+            res.tokens.append(st.token)
+            res.ledger.append((1, 1, 1))
+            ctx.append(st.token)
+            if stop_at_eos and st.token == eos:
+                res.ended_eos = True
+            continue
+        out = spec_step_tree(target, drafter, ctx, cfg, rng, eos_bias, stop_at_eos, remaining)
+        for rc in out.rounds:
+            res.ledger += [(0, rc.drafter_tokens_each, rc.drafter_tokens_each)] * rc.drafter_forwards
+            res.ledger.append((1, rc.target_tokens, rc.target_tokens))
+        res.accept_lens.append(out.accept_len)
+        res.tokens += out.accepted_tokens
+        ctx += out.accepted_tokens
+        res.steps += out.steps
+        res.ended_eos = out.ended
+    return res
+
+
+def mean_accept_len(accept_lens: Sequence[int]) -> float:
+    """mean_accept_len (specdec.cpp:318-327)."""
+    if not accept_lens:
+        raise InvalidArgument("mean_accept_len: no verification cycles recorded")
+    s = 0.0
+    for a in accept_lens:
+        s += a
+    return s / len(accept_lens)
 
 
 # ---- KD learner (learner.hpp:15-69) --------------------------------------------------------------------------

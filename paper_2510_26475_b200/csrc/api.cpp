@@ -634,6 +634,33 @@ int rs_skew_eos_biases(uint64_t seed, int32_t n, double *out) {
     });
 }
 
+// DecodeRng continuation (rng.hpp:33-47): the two mt19937_64 streams of a request as an opaque
+// image -- exported after a step, imported into a fresh engine before its first step -- so a
+// caller can run spec_step_tree cycle by cycle on one DecodeRng& like the reference.
+int rs_engine_rng_export(const rs_engine *e, int32_t req, uint64_t *out, int64_t cap, int64_t *n) {
+    return guard([&] {
+        need(e, "rs_engine_rng_export");
+        check_req(e, req);
+        const int64_t words = (int64_t)(2 * sizeof(rs::MtStream) / 8);
+        if (n) *n = words;
+        if (!out || cap <= 0) return;
+        if (cap < words) throw std::invalid_argument("rs_engine_rng_export: buffer too small");
+        RS_CUDA(cudaStreamSynchronize(e->ctx->stream));
+        RS_CUDA(cudaMemcpy(out, e->d_rng.p + 2 * (size_t)req, 2 * sizeof(rs::MtStream), cudaMemcpyDeviceToHost));
+    });
+}
+int rs_engine_rng_import(rs_engine *e, int32_t req, const uint64_t *in, int64_t n) {
+    return guard([&] {
+        need(e, "rs_engine_rng_import");
+        need(in, "rs_engine_rng_import: state");
+        check_req(e, req);
+        if (e->cycle > 0) throw std::runtime_error("rs_engine_rng_import: engine already stepped");
+        if (n != (int64_t)(2 * sizeof(rs::MtStream) / 8)) throw std::invalid_argument("rs_engine_rng_import: bad state size");
+        RS_CUDA(cudaStreamSynchronize(e->ctx->stream));
+        RS_CUDA(cudaMemcpy(e->d_rng.p + 2 * (size_t)req, in, 2 * sizeof(rs::MtStream), cudaMemcpyHostToDevice));
+    });
+}
+
 int rs_engine_set_capture(rs_engine *e, int32_t enable) {
     return guard([&] { need(e, "rs_engine_set_capture"); e->capture = enable != 0; });
 }
