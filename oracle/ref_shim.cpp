@@ -294,6 +294,21 @@ json learner_metrics_json(const std::vector<LearnerMetrics> & ms) {
 
 // OnlineLearner driven by a script of iterations: {"feed": [samples], "boundary": it, "await": bool}.
 // generate (specdec.cpp:271-316) on one sequence, plus mean_accept_len.
+// kd_loss_gradient + per-sample kd_loss over an explicit (sample, weight) list (learner.cpp:33-82).
+json op_kd_grad(const json & req) {
+    TabularARModel drafter = model_of(req.at("drafter"));
+    std::vector<RolloutSample> samples;
+    for (const auto & s : req.at("samples")) samples.push_back(sample_of(s));
+    const auto w = req.at("weights").get<std::vector<double>>();
+    std::vector<std::pair<const RolloutSample *, double>> ws;
+    json losses = json::array();
+    for (size_t i = 0; i < samples.size(); ++i) {
+        ws.emplace_back(&samples[i], w.at(i));
+        losses.push_back(kd_loss(drafter, samples[i], w.at(i)));
+    }
+    return {{"grad", kd_loss_gradient(drafter, ws)}, {"losses", losses}};
+}
+
 json op_generate(const json & req) {
     TabularARModel target = model_of(req.at("target"));
     TabularARModel drafter = model_of(req.at("drafter"));
@@ -386,6 +401,7 @@ json dispatch(const json & req) {
     if (op == "time_generation") return op_time_generation(req);
     if (op == "online_learner") return op_online_learner(req);
     if (op == "generate") return op_generate(req);
+    if (op == "kd_grad") return op_kd_grad(req);
     if (op == "policy_update") return op_policy_update(req);
     if (op == "group_advantages") return op_group_advantages(req);
     if (op == "build_profile") return op_build_profile(req);

@@ -1239,6 +1239,27 @@ def kd_grad_transformer(drafter: "EagleDrafter", samples: Sequence[RolloutSample
     return loss.value, grad
 
 
+def kd_loss(drafter, sample: RolloutSample, w: float) -> float:
+    """kd_loss (learner.cpp:33-60): w * sum_t KL(p~_t || q_theta(.|ctx_t)) for one sample, on the device
+    (tabular: from the sample's target_logprobs; EAGLE drafter: p~ recomputed by its target)."""
+    if isinstance(drafter, EagleDrafter):
+        loss, _ = kd_grad_transformer(drafter, [sample], [w])
+        return loss
+    from .distributed import kd_grad_tabular
+    return kd_grad_tabular(drafter, [sample], [w])[1]
+
+
+def kd_loss_gradient(drafter, weighted: Sequence[tuple]):
+    """kd_loss_gradient (learner.cpp:62-82): the drafter-logit gradient of sum_i w_i L_KD(sample_i),
+    weighted = [(RolloutSample, w)]. Tabular: the full logit-table gradient (list of V^(order+1)
+    floats, reference order); EAGLE drafter: the fp32 [V, d] LM-head gradient (torch CUDA tensor)."""
+    samples, ws = [x for x, _ in weighted], [w for _, w in weighted]
+    if isinstance(drafter, EagleDrafter):
+        return kd_grad_transformer(drafter, samples, ws)[1]
+    from .distributed import kd_grad_tabular
+    return kd_grad_tabular(drafter, samples, ws)[0]
+
+
 def kd_update(drafter, buffer: Sequence[RolloutSample], policy: KDPolicy, selection_rng: SelectionRng,
               sim_cost_per_token: float) -> KDUpdateResult:
     """kd_update (learner.cpp:98-160): loss + analytic gradient + SGD step on the device.

@@ -104,3 +104,21 @@ def test_generate_matches_reference(reference, cfg, max_len, bias, stop):
         assert rb.mean_accept_len(g.accept_lens) == exp["mean_accept_len"]
     with pytest.raises(rb.InvalidArgument, match="no verification cycles"):
         rb.mean_accept_len([])
+
+
+def test_kd_loss_and_gradient_match_reference(reference):
+    """kd_loss / kd_loss_gradient (learner.hpp:32-37) on the device vs the reference (1e-10 / 1e-12,
+    test_learner.cpp:93-110)."""
+    from conftest import load_golden
+    g = load_golden("kd_update.json")
+    buf = g["buffer"][:6]
+    ws = [0.5, 1.0, 2.0, 0.0, 1.5, 3.0]
+    exp = reference("kd_grad", drafter=g["drafter"], samples=buf, weights=ws)
+    drafter = model_of(g["drafter"])
+    samples = [rb.RolloutSample(s["prompt"], s["response"],
+                                [rb.StepRecord(st["token"], st["logp"], st["drafted"], st["logq"], st["target_logprobs"])
+                                 for st in s["steps"]], s["eos_bias"], s["reward"]) for s in buf]
+    for smp, w, e in zip(samples, ws, exp["losses"]):
+        assert rb.kd_loss(drafter, smp, w) == pytest.approx(e, rel=1e-10, abs=1e-12)
+    grad = rb.kd_loss_gradient(drafter, list(zip(samples, ws)))
+    assert max(abs(a - b) for a, b in zip(grad, exp["grad"])) < 1e-12
