@@ -497,6 +497,24 @@ def main():
                 "peak_source": f"{peak_kind} bf16_tflops_sustained (kernel timed inside a long step)"}
     breakdown = {k: {"ms_per_step": round(v["ms"] / max(1, min(args.steps, 5)), 3), "launches": v["launches"]}
                  for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
+    # HBM view of the two byte-moving stages (north star: achieved GB/s of acceptance and KV
+    # compaction), per-kernel profiler time; bytes per SURVEY §8(d)
+    hbm = {}
+    nprof = max(1, min(args.steps, 5))
+    if "accept.accept" in prof and prof["accept.accept"]["ms"] > 0:
+        a = prof["accept.accept"]
+        hbm["acceptance"] = {"algorithmic_bytes_per_step": a["bytes"] / nprof, "ms_per_step": a["ms"] / nprof,
+                             "GB_s": round(a["bytes"] / (a["ms"] / 1000.0) / 1e9, 1),
+                             "bytes": "(t*n_eff+1) target + t*n_eff drafter fp32 logit rows of V per sequence, "
+                                      "as if materialised; lazy tile statistics read ~3 rows"}
+    if "accept.compact" in prof and prof["accept.compact"]["ms"] > 0 and args.steps > 0:
+        c = prof["accept.compact"]
+        per_tok = shape.kv_bytes_per_token() + 2 * shape.n_kv_heads * shape.head_dim * 2 + 3 * shape.d_model * 2
+        moved = 2.0 * per_tok * (accepted / args.steps)  # read + write of every accepted drafted token
+        hbm["kv_compaction"] = {"algorithmic_bytes_per_step": moved, "ms_per_step": c["ms"] / nprof,
+                                "GB_s": round(moved / (c["ms"] / nprof / 1000.0) / 1e9, 1),
+                                "bytes": "2 x accepted drafted tokens x (target K/V all layers + drafter K/V + "
+                                         "EAGLE features)"}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -524,7 +542,7 @@ def main():
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_tok / e2e_s, 1), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps)},
-            "gpu_launches": launches, "clocks": clk, "breakdown_ms_per_step": breakdown, "kd_update": kd, "north_star_batch256": b256}
+            "gpu_launches": launches, "clocks": clk, "breakdown_ms_per_step": breakdown, "kd_update": kd, "north_star_batch256": b256, "hbm": hbm or None}
     if dyn:
         line["dynamic_tuning"] = dyn
     if tuner:
