@@ -295,7 +295,8 @@ void rs_prof_enable(int32_t on);
    sequence in the fused acceptance kernel (1, 2, 4, 8); "fused_stats" -- drafter LM-head softmax
    partials in the GEMM epilogue (1) or a separate row-stats kernel (0); results are bitwise
    independent of both; "gemm2" -- weight GEMMs on SM pairs (0 auto/on, -1 single-SM kernel);
-   "pdl" -- programmatic dependent launch on the forward path (0 on, -1 off). */
+   "pdl" -- programmatic dependent launch on the forward path (0 on, -1 off); "kd_rows" -- cap on
+   the KD rows per group of rs_engine_kd_grad (tests of the grouping; 0 = workspace size). */
 int rs_set_tuning(const char *key, int64_t value);
 void rs_prof_reset(void);
 int rs_prof_json(char *buf, int64_t cap, int64_t *len);
