@@ -534,7 +534,7 @@ def main():
             "config": {"workload": "cfg2: Qwen2.5-3B-shaped target + EAGLE-3-style drafter, random init, "
                                    f"batch {args.batch}/GPU, tree depth {n} top-k {t} (s={s})" if args.model == "3b"
                                    else f"{args.model} target, batch {args.batch}/GPU, tree({s},{t},{n})",
-                       "model": args.model, "batch_per_gpu": args.batch, "global_batch": args.batch * world,
+                       "target_shape": f"qwen2.5-{args.model}", "batch_per_gpu": args.batch, "global_batch": args.batch * world,
                        "sd_config": cfg.key(), "verify": "rejection sampling T=1" if args.verify == "sample"
                        else "greedy", "ctx_len_start": args.ctx, "parallelism": f"prompt-sharded dp{world}",
                        "l2": "no flush: each step streams 6.2 GB of weights + KV (>> 126 MB L2)",
