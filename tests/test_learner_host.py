@@ -51,3 +51,13 @@ def test_replay_buffer_eviction():
     for i in range(3):
         b.push(rb.RolloutSample([i], [], []))
     assert b.size() == 2 and [s.prompt for s in b.take_all()] == [[1], [2]] and b.size() == 0
+
+
+def test_round_costs_from_single_sequence_ledger():
+    """spec_step_tree's RoundCost list is read back from the one-request engine's forward events
+    (charge_batched_cycle over one outcome, server.cpp:154-178)."""
+    ledger = [(0, 2, 2), (0, 2, 2), (1, 7, 7), (0, 2, 2), (1, 5, 5), (1, 1, 1)]
+    rounds = rb._rounds_of(ledger)
+    assert [(r.drafter_forwards, r.drafter_tokens_each, r.target_tokens) for r in rounds] == \
+        [(2, 2, 7), (1, 2, 5), (0, 0, 1)]
+    assert rb.mean_accept_len([1, 0, 3, 3]) == 1.75
