@@ -389,6 +389,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (n > 0 && warp_valid) {
             float lh = ((lp[0] + lp[1]) + (lp[2] + lp[3])) + ((lp[4] + lp[5]) + (lp[6] + lp[7]));
+            // the partner half may still be reading the last pass's maxima from xch: no pass
+            // follows to order it through the S / P barriers, so the pair syncs before reuse
+            asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
             xch[half * 32 + lane] = lh;
             asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
             const float l = xch[lane] + xch[32 + lane];
