@@ -1017,15 +1017,17 @@ void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t s
     // algorithmic bytes: every target row of the round plus every drafter row
     const double es = rt == RowType::F64 ? 8.0 : 4.0;
     ProfScope prof("accept", 0, (double)d.nact * (naive ? 1 : 2 * d.slots - 1) * d.V * es, st);
-    // Large vocabularies: a cluster of up to 8 CTAs per sequence, sized so the whole batch is
-    // co-resident (2 x 256-thread CTAs per SM) -- the residual passes are fp64-exp bound.
+    // Large vocabularies: a cluster of up to 8 CTAs per sequence -- the residual passes are fp64 /
+    // load-latency bound, so more CTAs in flight win even past one resident wave. Measured (cfg2,
+    // V = 152K): batch 32 / 64 -> 8 CTAs (0.39 / 0.62 ms vs 0.57 / 0.68 at 4); batch 256 -> 4
+    // (2.25 ms vs 2.39 at 2, 2.88 at 1). Results are bitwise independent of the cluster size.
     unsigned C = 1;
     int threads = th;
     if (d.V > 4096) {
         threads = 256;
         int sms = 148;
         RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-        while (C < kMaxCluster && (long)d.nact * C * 2 <= 2L * sms) C *= 2;
+        while (C < kMaxCluster && (long)d.nact * C * 2 <= 8L * sms) C *= 2;
     }
     if (tuning().accept_cluster > 0) {
         C = static_cast<unsigned>(tuning().accept_cluster);
