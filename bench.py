@@ -185,7 +185,10 @@ def reference_arm(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * secs / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "mean_accept_len": statistics.mean(al) if al else 0.0,
-            "config": {"workload": "cfg2 on the reference's CPU engine (tabular models)", "batch_per_gpu": args.batch,
+            "config": {"workload": "cfg2 on the reference's CPU engine (tabular models)",
+                       "model_family": "TabularARModel V=8 -- the only model family the reference implements; the "
+                                       "GPU arm runs a Qwen2.5-3B-shaped transformer, so the model compute differs",
+                       "batch_per_gpu": args.batch,
                        "sd_config": f"s{s}_t{t}_n{n}", "verify": "rejection sampling T=1"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
