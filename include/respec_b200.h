@@ -366,6 +366,11 @@ int rs_learner_create(rs_ctx *ctx, const rs_model *drafter, rs_kd_policy policy,
                       double sim_cost_per_token, int64_t buffer_capacity, int32_t async, rs_learner **out);
 int rs_learner_destroy(rs_learner *l); /* shutdown (drains queued updates) + free */
 int rs_learner_feed(rs_learner *l, const rs_kd_sample *samples, int32_t n);
+/* Samples backed by a live transformer engine (EAGLE drafter learners): request req[i] of `e`
+   with reward[i]; updates read the engine's resident KV cache and features (as
+   rs_engine_kd_grad) instead of recomputing the prompts. The engine must outlive the update and
+   must not be stepped while it is pending. */
+int rs_learner_feed_engine(rs_learner *l, rs_engine *e, const int32_t *req, const double *reward, int32_t n);
 int rs_learner_on_iteration_boundary(rs_learner *l, int32_t iteration);
 int rs_learner_await_pending(rs_learner *l);
 int rs_learner_shutdown(rs_learner *l);

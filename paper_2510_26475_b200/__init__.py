@@ -134,7 +134,7 @@ EXPORTED_SYMBOLS = [
     "rs_learner_total_sim_time", "rs_learner_buffer_size", "rs_learner_metrics",
     "rs_reward", "rs_group_advantages", "rs_policy_update_tabular",
     "rs_engine_set_stop_at_eos", "rs_profile_simulated", "rs_tabular_random", "rs_skew_eos_biases",
-    "rs_engine_kd_grad", "rs_engine_rng_export", "rs_engine_rng_import",
+    "rs_engine_kd_grad", "rs_engine_rng_export", "rs_engine_rng_import", "rs_learner_feed_engine",
 ]
 
 _lib = None
@@ -242,6 +242,7 @@ def lib():
             "rs_engine_kd_grad": ([vp, vp, P(i32), i32, P(dbl), vp, i32, P(dbl)], ctypes.c_int),
             "rs_engine_rng_export": ([vp, i32, P(u64), i64, P(i64)], ctypes.c_int),
             "rs_engine_rng_import": ([vp, i32, P(u64), i64], ctypes.c_int),
+            "rs_learner_feed_engine": ([vp, vp, P(i32), P(dbl), i32], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -1348,6 +1349,7 @@ class OnlineLearner:
                  buffer_capacity: int = 4096, async_: bool = False):
         self._proto = drafter
         self._policy = policy
+        self._engines = []
         self.device = drafter.device
         h = ctypes.c_void_p()
         _check(lib().rs_learner_create(self.device.handle, drafter.handle, policy._c(),
@@ -1362,11 +1364,24 @@ class OnlineLearner:
         arr, keep = _kd_samples(samples, "auto")
         _check(lib().rs_learner_feed(self.handle, arr, len(samples)))
 
+    def feed_engine(self, engine: "BatchEngine", req_ids: Sequence[int], rewards: Sequence[float]) -> None:
+        """Samples backed by a live transformer engine (rs_learner_feed_engine): updates read its
+        resident KV cache and features instead of recomputing the prompts. The engine is kept
+        alive here until no update can still read it; do not step it while one is pending."""
+        req_ids = list(req_ids)
+        if not req_ids:
+            return
+        self._engines.append(engine)
+        _check(lib().rs_learner_feed_engine(self.handle, engine.handle, _i32arr(req_ids), _f64arr(rewards),
+                                            len(req_ids)))
+
     def on_iteration_boundary(self, iteration: int) -> None:
         _check(lib().rs_learner_on_iteration_boundary(self.handle, iteration))
 
     def await_pending(self) -> None:
         _check(lib().rs_learner_await_pending(self.handle))
+        if self.buffer_size() == 0:
+            self._engines = []  # no buffered or pending update reads them any more
 
     def shutdown(self) -> None:
         _check(lib().rs_learner_shutdown(self.handle))

@@ -32,6 +32,8 @@ struct Sample {  // RolloutSample fields the learner reads (rollout.hpp:12-20)
     std::vector<int32_t> prompt, response;
     std::vector<double> lp;  // response_len x V target log-probabilities, or empty
     double eos_bias = 0.0, reward = 0.0;
+    rs_engine *eng = nullptr;  // or: request `req` of a live transformer engine (resident caches)
+    int req = -1, response_len = 0;
 };
 
 struct ModelRef {  // one counted reference to an rs_model
@@ -80,6 +82,72 @@ struct rs_learner {
         buffer.push_back(std::move(s));
     }
 
+    // kd_update (learner.cpp:98-160) for an EAGLE drafter when samples come from live engines:
+    // the same selection and reward weights, the gradient of each engine's selected requests from
+    // its resident KV cache / features (rs_engine_kd_grad), detached samples by the teacher-forced
+    // recompute; contributions in selection order, grouped by source.
+    rs_model *update_from_engines(const std::vector<Sample> &batch, const rs::DrafterModel *d, rs_ctx *c,
+                                  rs_kd_result &res) {
+        if (policy.mode == 2) throw std::logic_error("kd_update: frozen drafter takes no updates");
+        if (policy.interval < 1) throw std::invalid_argument("kd_update: interval must be >= 1");
+        const std::vector<int> idx = rs::kd_select((int)batch.size(), policy.interval, sel);
+        std::vector<double> br(idx.size()), w(idx.size());
+        for (size_t i = 0; i < idx.size(); ++i) br[i] = batch[idx[i]].reward;
+        double wsum = 0, wmin = 0, wmax = 0;
+        size_t distilled = 0;
+        for (size_t i = 0; i < idx.size(); ++i) {
+            w[i] = rs::kd_weight(batch[idx[i]].reward, br, policy);
+            wsum += w[i];
+            wmin = i == 0 ? w[i] : std::min(wmin, w[i]);
+            wmax = i == 0 ? w[i] : std::max(wmax, w[i]);
+            distilled += (size_t)std::max(0, batch[idx[i]].response_len);
+        }
+        const auto *t = d->target;
+        rs::DBuf<float> grad((size_t)t->s.V * t->s.d);
+        RS_CUDA(cudaMemsetAsync(grad.p, 0, grad.bytes(), c->stream));
+        RS_CUDA(cudaStreamSynchronize(c->stream));
+        double loss = 0.0;
+        size_t i = 0;
+        while (i < idx.size()) {
+            const Sample &s0 = batch[idx[i]];
+            size_t j = i;
+            if (s0.eng) {
+                std::vector<rs::KdRef> refs;
+                for (; j < idx.size() && batch[idx[j]].eng == s0.eng; ++j)
+                    if (batch[idx[j]].response_len > 0)
+                        refs.push_back(rs::KdRef{batch[idx[j]].req, w[j], batch[idx[j]].eos_bias});
+                if (!refs.empty()) {
+                    if (!s0.eng->pair) throw std::runtime_error("OnlineLearner: engine has no model pair");
+                    loss += s0.eng->pair->kd_cached(refs, d, grad.p);
+                }
+            } else {
+                std::vector<rs::KdSeq> seqs;
+                for (; j < idx.size() && !batch[idx[j]].eng; ++j) {
+                    const Sample &x = batch[idx[j]];
+                    if (x.response.empty()) continue;
+                    rs::KdSeq q;
+                    q.tokens = x.prompt;
+                    q.tokens.insert(q.tokens.end(), x.response.begin(), x.response.end());
+                    q.prompt_len = (int)x.prompt.size();
+                    q.eos_bias = x.eos_bias;
+                    q.weight = w[j];
+                    seqs.push_back(std::move(q));
+                }
+                if (!seqs.empty()) loss += rs::kd_grad_transformer(c, t, d, seqs, grad.p, false);
+            }
+            i = j;
+        }
+        rs_model *out = rs::drafter_apply_lm_grad(c, d, grad.p, -policy.lr);
+        res.updated = 1;
+        res.samples_used = (int)idx.size();
+        res.loss = loss;
+        res.weight_mean = idx.empty() ? 0.0 : wsum / (double)idx.size();
+        res.weight_min = wmin;
+        res.weight_max = wmax;
+        res.sim_time = cost * (double)distilled;
+        return out;
+    }
+
     // OnlineLearner::do_update (learner.cpp:256-289).
     void do_update(const std::vector<Sample> &batch, rs_ctx *c) {
         ModelRef base;
@@ -87,6 +155,9 @@ struct rs_learner {
             std::lock_guard<std::mutex> lock(mu);
             base = snapshot;
         }
+        const bool from_engines =
+            base.m->kind == rs_model::Drafter &&
+            std::any_of(batch.begin(), batch.end(), [](const Sample &x) { return x.eng != nullptr; });
         std::vector<rs_kd_sample> arr(batch.size());
         for (size_t i = 0; i < batch.size(); ++i) {
             const Sample &s = batch[i];
@@ -96,8 +167,10 @@ struct rs_learner {
         }
         rs_model *out = nullptr;
         rs_kd_result res{};
-        int st;
-        if (base.m->kind == rs_model::Tabular) {
+        int st = RS_OK;
+        if (from_engines) {
+            out = update_from_engines(batch, static_cast<const rs::DrafterModel *>(base.m), c, res);
+        } else if (base.m->kind == rs_model::Tabular) {
             st = rs_kd_update_tabular(c, base.m, arr.data(), (int32_t)arr.size(), policy, sel, cost, &out, &res);
         } else {
             const auto *d = static_cast<const rs::DrafterModel *>(base.m);
@@ -225,6 +298,34 @@ int rs_learner_feed(rs_learner *l, const rs_kd_sample *samples, int32_t n) {
             if (x.target_logprobs) s.lp.assign(x.target_logprobs, x.target_logprobs + (size_t)x.response_len * V);
             s.eos_bias = x.eos_bias;
             s.reward = x.reward;
+            s.response_len = x.response_len;
+            l->push(std::move(s));
+        }
+    });
+}
+
+// Samples backed by a live transformer engine: request req[i] (prompt = its prompt, response =
+// its generated tokens, its EOS bias) with reward[i]. Updates then read the engine's resident
+// caches instead of recomputing the prompts; the engine must outlive them and must not be
+// stepped while one is pending.
+int rs_learner_feed_engine(rs_learner *l, rs_engine *e, const int32_t *req, const double *reward, int32_t n) {
+    return guard([&] {
+        need(l, "rs_learner_feed_engine");
+        need(e, "rs_learner_feed_engine: engine");
+        if (n > 0) {
+            need(req, "rs_learner_feed_engine: requests");
+            need(reward, "rs_learner_feed_engine: rewards");
+        }
+        if (l->snapshot.m->kind != rs_model::Drafter || e->target->kind != rs_model::Transformer)
+            throw std::invalid_argument("OnlineLearner: engine samples need an EAGLE drafter and a transformer engine");
+        for (int i = 0; i < n; ++i) {
+            if (req[i] < 0 || req[i] >= e->n) throw std::invalid_argument("feed: request index out of range");
+            Sample s;
+            s.eng = e;
+            s.req = req[i];
+            s.response_len = e->len[req[i]] - e->prompt_len[req[i]];
+            s.eos_bias = e->eos_bias[req[i]];
+            s.reward = reward[i];
             l->push(std::move(s));
         }
     });

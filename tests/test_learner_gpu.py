@@ -185,3 +185,41 @@ def test_transformer_learner_async_equals_sync():
         L.close()
     assert mets[0] == mets[1] and all(math.isfinite(x[1]) and x[1] > 0 for x in mets[0])
     assert (heads[0] == heads[1]).all()
+
+
+def test_transformer_learner_from_engine_caches():
+    """OnlineLearner fed with engine-backed samples (rs_learner_feed_engine) == the same learner fed
+    with the detached rollouts: same selection, samples and version; the loss to 1e-9 and the LM
+    head to bf16 rounding (the gradient is summed in a different grouping)."""
+    import random
+    import torch
+    shape = rb.TransformerShape.tiny(vocab=512, max_ctx=128)
+    tgt = rb.TransformerModel(shape, seed=7)
+    drf = rb.EagleDrafter(tgt, seed=8)
+    rng = random.Random(5)
+    reqs = [rb.RequestState(i, [rng.randrange(511) for _ in range(5 + i)], -1.0, 7 + i, rb.DecodeRng.from_seed(3, i))
+            for i in range(5)]
+    eng = rb.BatchEngine(tgt, lambda: drf, None, rb.TimingModel(), reqs, rb.SDConfig.tree(1, 2, 3), "sample",
+                         record_full_logprobs=False)
+    while not eng.all_done():
+        eng.step()
+    rewards = [rng.random() for _ in range(5)]
+    done = eng.requests()
+    pol = rb.KDPolicy(1, rb.WeightMode.Reward, 0.0, 4.0, 0.5)
+    outs = []
+    for mode in ("engine", "detached", "engine_async"):
+        L = rb.OnlineLearner(drf, pol, 11, 0.01, 64, mode == "engine_async")
+        if mode == "detached":
+            L.feed([rb.RolloutSample(list(r.prompt), list(r.generated), [], r.eos_bias, w) for r, w in zip(done, rewards)])
+        else:
+            L.feed_engine(eng, list(range(5)), rewards)
+        L.on_iteration_boundary(0)
+        L.await_pending()
+        m = L.metrics()[0]
+        outs.append((L.drafter_version(), m.samples_used, m.kd_loss, L.snapshot().to_torch("lm_w").float()))
+        L.close()
+    (v0, n0, l0, h0), (v1, n1, l1, h1), (v2, n2, l2, h2) = outs
+    assert v0 == v1 == v2 == drf.version + 1 and n0 == n1 == n2
+    assert l0 == pytest.approx(l1, rel=1e-9) and l0 == l2
+    assert torch.equal(h0, h2)
+    assert (h0 - h1).abs().max().item() <= 2e-2 * h1.abs().max().item()
