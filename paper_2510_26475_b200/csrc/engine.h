@@ -128,7 +128,8 @@ struct ModelPair {
     virtual void begin_step() {}
     // Online-KD loss + drafter LM-head gradient over requests' generated tokens from the
     // resident caches (transformer pairs only).
-    virtual double kd_cached(const std::vector<KdRef> &, const rs_model *, float *) {
+    // `stream` (or null: the engine's) carries the pass -- an asynchronous learner runs it on its own.
+    virtual double kd_cached(const std::vector<KdRef> &, const rs_model *, float *, cudaStream_t = nullptr) {
         throw std::invalid_argument("kd from the engine needs a transformer target");
     }
 };

@@ -105,7 +105,6 @@ struct rs_learner {
         const auto *t = d->target;
         rs::DBuf<float> grad((size_t)t->s.V * t->s.d);
         RS_CUDA(cudaMemsetAsync(grad.p, 0, grad.bytes(), c->stream));
-        RS_CUDA(cudaStreamSynchronize(c->stream));
         double loss = 0.0;
         size_t i = 0;
         while (i < idx.size()) {
@@ -118,7 +117,7 @@ struct rs_learner {
                         refs.push_back(rs::KdRef{batch[idx[j]].req, w[j], batch[idx[j]].eos_bias});
                 if (!refs.empty()) {
                     if (!s0.eng->pair) throw std::runtime_error("OnlineLearner: engine has no model pair");
-                    loss += s0.eng->pair->kd_cached(refs, d, grad.p);
+                    loss += s0.eng->pair->kd_cached(refs, d, grad.p, c->stream);
                 }
             } else {
                 std::vector<rs::KdSeq> seqs;

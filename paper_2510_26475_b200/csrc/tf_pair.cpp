@@ -684,7 +684,8 @@ struct TransformerPair : ModelPair {
     // state is untouched. Rows are grouped so a group holds <= Mcap KD rows; the drafter
     // advances through each request only as far as the group needs. Same loss / gradient as
     // kd_pass on the same sequences.
-    double kd_cached(const std::vector<KdRef> &refs, const rs_model *m, float *grad) override {
+    double kd_cached(const std::vector<KdRef> &refs, const rs_model *m, float *grad,
+                     cudaStream_t on = nullptr) override {
         if (!m || m->kind != rs_model::Drafter) throw std::invalid_argument("kd: EAGLE drafter required");
         const auto *kd_drf = static_cast<const DrafterModel *>(m);
         if (kd_drf->target != tgt) throw std::invalid_argument("kd: drafter is bound to a different target");
@@ -695,7 +696,7 @@ struct TransformerPair : ModelPair {
         d.tok_cap = eng->tok_cap;
         d.t_max = 1;
         d.n_max = 1;
-        cudaStream_t st = ctx->stream;
+        cudaStream_t st = on ? on : ctx->stream;
         const int V = s.V;
         const int Mcap = tuning().kd_rows > 0 ? std::min(w.Mcap, tuning().kd_rows) : w.Mcap;
         long long need = 0;  // KD rows in total: every generated token of every selected request

@@ -223,3 +223,42 @@ def test_transformer_learner_from_engine_caches():
     assert l0 == pytest.approx(l1, rel=1e-9) and l0 == l2
     assert torch.equal(h0, h2)
     assert (h0 - h1).abs().max().item() <= 2e-2 * h1.abs().max().item()
+
+
+def test_async_engine_backed_update_overlaps_a_rollout():
+    """An asynchronous engine-backed update runs on the learner's own stream while a second engine
+    generates on the caller's stream: both results are bitwise those of running them apart."""
+    import random
+    import torch
+    shape = rb.TransformerShape.tiny(vocab=512, max_ctx=128)
+    tgt = rb.TransformerModel(shape, seed=9)
+    drf = rb.EagleDrafter(tgt, seed=10)
+
+    def engine(seed):
+        rng = random.Random(seed)
+        reqs = [rb.RequestState(i, [rng.randrange(511) for _ in range(6)], -1.0, 10, rb.DecodeRng.from_seed(seed, i))
+                for i in range(6)]
+        return rb.BatchEngine(tgt, lambda: drf, None, rb.TimingModel(), reqs, rb.SDConfig.tree(1, 2, 3), "sample",
+                              record_full_logprobs=False)
+
+    def run(e):
+        while not e.all_done():
+            e.step()
+        return [r.generated for r in e.requests()]
+
+    a = engine(1)
+    run(a)
+    pol = rb.KDPolicy(1, rb.WeightMode.Uniform, 0.0, 4.0, 0.5)
+    ref = rb.OnlineLearner(drf, pol, 3, 0.0, 64, False)
+    ref.feed_engine(a, list(range(6)), [1.0] * 6)
+    ref.on_iteration_boundary(0)
+    want_head = ref.snapshot().to_torch("lm_w")
+    want_b = run(engine(2))
+    L = rb.OnlineLearner(drf, pol, 3, 0.0, 64, True)
+    L.feed_engine(a, list(range(6)), [1.0] * 6)
+    L.on_iteration_boundary(0)   # the worker starts distilling from engine a ...
+    got_b = run(engine(2))       # ... while engine b generates on the main stream
+    L.await_pending()
+    assert got_b == want_b
+    assert torch.equal(L.snapshot().to_torch("lm_w"), want_head)
+    assert L.metrics()[0].kd_loss == ref.metrics()[0].kd_loss
