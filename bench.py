@@ -204,6 +204,62 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def kd_overlap_leg(args, rb, target, drafter, eng, dev, stream, cfg):
+    """cfg5 interleaving: an ASYNCHRONOUS OnlineLearner update distilling the first --kd rollouts of
+    the measured engine from its resident caches (rs_learner_feed_engine) on the learner's own
+    stream, while a second engine keeps generating on the caller's stream. Reports the second
+    engine's device ms/step alone and with the update in flight, and the update's wall time."""
+    import random
+    import time as _t
+    import torch
+    s, t, n = map(int, args.sd.split(","))
+    rng = random.Random(4242)
+    max_len = 16 * (s * n + 1) + 8
+    reqs = [rb.RequestState(i, [rng.randrange(target.shape.vocab - 1) for _ in range(args.ctx)], -20.0, max_len,
+                            rb.DecodeRng.from_seed(77, i)) for i in range(args.batch)]
+    b = rb.BatchEngine(target, lambda: drafter, None, rb.TimingModel(), reqs, cfg, args.verify,
+                       record_full_logprobs=False, device=dev)
+    for _ in range(2):
+        b.step()
+
+    def timed(k):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            b.step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / k
+
+    alone = timed(4)
+    pol = rb.KDPolicy(interval=1, mode=0, clip_lo=0.0, clip_hi=4.0, lr=0.5)
+    rewards = [random.Random(77).random() for _ in range(args.kd)]
+    warm = rb.OnlineLearner(drafter, pol, 123, 0.02, 64, False)  # first-use allocations, untimed
+    warm.feed_engine(eng, list(range(args.kd)), rewards)
+    warm.on_iteration_boundary(0)
+    t0 = _t.perf_counter()
+    sync = rb.OnlineLearner(drafter, pol, 123, 0.02, 64, False)
+    sync.feed_engine(eng, list(range(args.kd)), rewards)
+    sync.on_iteration_boundary(0)
+    kd_alone_ms = (_t.perf_counter() - t0) * 1e3
+    L = rb.OnlineLearner(drafter, pol, 123, 0.02, 64, True)
+    L.feed_engine(eng, list(range(args.kd)), rewards)
+    t0 = _t.perf_counter()
+    L.on_iteration_boundary(0)
+    with_kd = timed(4)
+    L.await_pending()
+    kd_wall_ms = (_t.perf_counter() - t0) * 1e3
+    same = L.snapshot().version == sync.snapshot().version and L.metrics()[0].kd_loss == sync.metrics()[0].kd_loss
+    for x in (warm, sync, L):
+        x.close()
+    del b
+    return {"rollouts_distilled": args.kd, "rollout_ms_per_step_alone": round(alone, 3),
+            "rollout_ms_per_step_with_async_kd": round(with_kd, 3), "kd_update_ms_sync": round(kd_alone_ms, 2),
+            "kd_update_wall_ms_async": round(kd_wall_ms, 2), "async_equals_sync": bool(same),
+            "source": "OnlineLearner(async) fed from the measured engine's resident caches, on its own stream"}
+
+
 def batch256_leg(args, rb, target, drafter, dev, stream, cfg, peaks):
     """North-star check (BASELINE.json north_star): the same SD step at batch 256 on one GPU --
     tokens/s and the verify GEMM family's achieved TFLOP/s against the measured sustained peak
@@ -465,6 +521,9 @@ def main():
     dyn = None
     if not args.tuner and not args.no_tuner_leg:
         dyn = tuner_leg(args, rb, target, drafter, reqs, dev, stream, max_len, cfg, world, barrier)
+    overlap = None
+    if world == 1 and args.kd > 0 and args.model != "tiny":
+        overlap = kd_overlap_leg(args, rb, target, drafter, eng, dev, stream, cfg)
     b256 = None
     if world == 1 and args.model == "3b" and args.batch != 256 and not args.no_b256_leg:
         b256 = batch256_leg(args, rb, target, drafter, dev, stream, cfg, measured_peaks()[0])
@@ -545,7 +604,8 @@ def main():
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_tok / e2e_s, 1), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps)},
-            "gpu_launches": launches, "clocks": clk, "breakdown_ms_per_step": breakdown, "kd_update": kd, "north_star_batch256": b256, "hbm": hbm or None}
+            "gpu_launches": launches, "clocks": clk, "breakdown_ms_per_step": breakdown, "kd_update": kd, "kd_async_overlap": overlap, "north_star_batch256": b256,
+            "hbm": hbm or None}
     if dyn:
         line["dynamic_tuning"] = dyn
     if tuner:
