@@ -89,9 +89,11 @@ struct Cfg2 {
     static constexpr int kABytes = kBM * kBK * 2;          // own 128 weight rows
     static constexpr int kBBytes = (BT / 2) * kBK * 2;     // own half of the token rows
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = (180 * 1024) / kStageBytes > 8 ? 8 : (180 * 1024) / kStageBytes;
-    static constexpr int kTmemCols = 2 * BT <= 128 ? 128 : 2 * BT <= 256 ? 256 : 512;
     static constexpr int kStgBytes = 2 * 32 * 132 * 4;  // per epilogue group: 4 x 32 x 33 or 32 x 132 fp32
+    // as many ring stages as the 227 KB opt-in shared memory leaves after the fixed parts (max 8)
+    static constexpr int kFixed = 1024 + 256 + kStgBytes + 256 * 16 + 2048;  // + static smem / slack
+    static constexpr int kStages = (232448 - kFixed) / kStageBytes > 8 ? 8 : (232448 - kFixed) / kStageBytes;
+    static constexpr int kTmemCols = 2 * BT <= 128 ? 128 : 2 * BT <= 256 ? 256 : 512;
     static constexpr int kSmem = 1024 + kStages * kStageBytes + 256 + kStgBytes + 256 * 16;
     // kind::f16, bf16 x bf16 -> f32, both K-major, N = BT tokens, M = 256 features (pair)
     static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BT >> 3) << 17) |
