@@ -257,6 +257,9 @@ int rs_engine_set_capture(rs_engine *e, int32_t enable);
 int rs_engine_capture_count(const rs_engine *e, int64_t *rows, int32_t *vocab, int32_t *ext_width);
 int rs_engine_capture_read(rs_engine *e, int64_t first, int64_t count, int32_t *role, int32_t *req,
                            int32_t *ctx_len, int32_t *ext, double *logits);
+/* Same rows, fp32 as the transformer LM heads produced them (count * vocab floats); fails
+   with RS_EINVAL for fp64 (tabular) rows. Metadata via rs_engine_capture_read(..., NULL). */
+int rs_engine_capture_read_f32(rs_engine *e, int64_t first, int64_t count, float *logits);
 
 /* ---- KD learner (learner.hpp:27-69, learner.cpp:10-160) -------------------------------- */
 double rs_kd_weight(double r, const double *batch_rewards, int32_t n, rs_kd_policy policy, int *status);

@@ -5,7 +5,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <json.hpp>
+#include <map>
 #include <memory>
+#include <mutex>
 
 #include "restate.hpp"
 
@@ -24,8 +26,20 @@ SDConfig cfg_of(const json & j) {
 }
 json cfg_json(const SDConfig & c) { return {{"s", c.rounds}, {"t", c.branching}, {"n", c.draft_len}, {"enabled", c.enabled}}; }
 
+// Lookup models filled through the binary entry points below (oracle_lookup_*), referenced
+// from a JSON request as {"kind": "lookup_ref", "id": k}.
+std::mutex g_reg_mu;
+std::map<int, std::shared_ptr<LookupModel>> g_reg;
+int g_reg_next = 1;
+
 std::shared_ptr<Model> model_of(const json & j) {
     const std::string kind = j.value("kind", "tabular");
+    if (kind == "lookup_ref") {
+        std::lock_guard<std::mutex> lk(g_reg_mu);
+        auto it = g_reg.find(j.at("id").get<int>());
+        if (it == g_reg.end()) throw std::invalid_argument("lookup_ref: unknown id");
+        return it->second;
+    }
     if (kind == "tabular") {
         auto m = std::make_shared<TabularModel>();
         m->vocab = j.at("vocab");
@@ -249,4 +263,37 @@ char * oracle_call(const char * req) {
     }
 }
 void oracle_free(char * p) { std::free(p); }
+
+// Binary transport for captured full-vocabulary rows (V ~ 152K fp32 per row).
+int oracle_lookup_new(int vocab, double temperature, int depth_aware) {
+    auto m = std::make_shared<LookupModel>();
+    m->vocab = vocab;
+    m->temperature = temperature;
+    m->depth_aware = depth_aware != 0;
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    g_reg[g_reg_next] = m;
+    return g_reg_next++;
+}
+// Adds one row keyed by (ctx, depth). Returns 0 when added, 1 when an identical row was
+// already present, -1 when a DIFFERENT row exists for the same key (row invariance broken),
+// -2 for an unknown id.
+int oracle_lookup_add_f32(int id, const int * ctx, int n, int depth, const float * logits) {
+    std::shared_ptr<LookupModel> m;
+    {
+        std::lock_guard<std::mutex> lk(g_reg_mu);
+        auto it = g_reg.find(id);
+        if (it == g_reg.end()) return -2;
+        m = it->second;
+    }
+    std::pair<std::vector<int>, int> key{std::vector<int>(ctx, ctx + n), m->depth_aware ? depth : 0};
+    auto it = m->rows32.find(key);
+    if (it != m->rows32.end())
+        return std::memcmp(it->second.data(), logits, sizeof(float) * m->vocab) == 0 ? 1 : -1;
+    m->rows32.emplace(std::move(key), std::vector<float>(logits, logits + m->vocab));
+    return 0;
+}
+void oracle_lookup_free(int id) {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    g_reg.erase(id);
+}
 }

@@ -31,8 +31,11 @@ std::vector<double> TabularModel::logits(const std::vector<int> & ctx) const {
 }
 
 std::vector<double> LookupModel::logits_at(const std::vector<int> & ctx, int depth) const {
-    auto it = rows.find({ctx, depth_aware ? depth : 0});
+    const std::pair<std::vector<int>, int> key{ctx, depth_aware ? depth : 0};
+    auto it = rows.find(key);
     if (it == rows.end()) {
+        auto f = rows32.find(key);
+        if (f != rows32.end()) return std::vector<double>(f->second.begin(), f->second.end());
         std::string s = "LookupModel: no row for context of length " + std::to_string(ctx.size()) + " [";
         for (size_t i = ctx.size() > 6 ? ctx.size() - 6 : 0; i < ctx.size(); ++i) s += std::to_string(ctx[i]) + " ";
         throw std::out_of_range(s + "]");

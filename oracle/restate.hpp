@@ -79,6 +79,9 @@ struct TabularModel : Model {
 struct LookupModel : Model {
     bool depth_aware = false;
     std::map<std::pair<std::vector<int>, int>, std::vector<double>> rows;  // (ctx, depth or 0)
+    // fp32 rows handed over through the binary entry (oracle_lookup_add_f32): full-vocabulary
+    // rows at V ~ 152K are too large for the JSON transport
+    std::map<std::pair<std::vector<int>, int>, std::vector<float>> rows32;
     std::vector<double> logits(const std::vector<int> & ctx) const override { return logits_at(ctx, 0); }
     std::vector<double> logits_at(const std::vector<int> & ctx, int depth) const override;
 };

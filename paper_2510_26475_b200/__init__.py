@@ -124,7 +124,7 @@ EXPORTED_SYMBOLS = [
     "rs_engine_cycles", "rs_engine_prefill_events", "rs_engine_ledger_time", "rs_engine_ledger",
     "rs_engine_switches", "rs_engine_active_trace", "rs_engine_drafter_versions", "rs_engine_response",
     "rs_engine_steps", "rs_engine_step_logprobs", "rs_engine_accept_lens", "rs_engine_destroy",
-    "rs_engine_set_capture", "rs_engine_capture_count", "rs_engine_capture_read",
+    "rs_engine_set_capture", "rs_engine_capture_count", "rs_engine_capture_read", "rs_engine_capture_read_f32",
     "rs_kd_weight", "rs_kd_update_tabular", "rs_mt19937_64_seed", "rs_gemm_bf16",
     "rs_model_tensor", "rs_memcpy_d2d", "rs_model_params", "rs_prof_enable", "rs_prof_reset", "rs_prof_json", "rs_set_tuning", "rs_lm_head_bf16", "rs_row_stats", "rs_kd_grad_transformer", "rs_drafter_apply_grad",
     "rs_kd_update_transformer", "rs_engine_step_tokens", "rs_profile_measured",
@@ -195,6 +195,7 @@ def lib():
             "rs_engine_set_capture": ([vp, i32], ctypes.c_int),
             "rs_engine_capture_count": ([vp, P(i64), P(i32), P(i32)], ctypes.c_int),
             "rs_engine_capture_read": ([vp, i64, i64, P(i32), P(i32), P(i32), P(i32), P(dbl)], ctypes.c_int),
+            "rs_engine_capture_read_f32": ([vp, i64, i64, ctypes.c_void_p], ctypes.c_int),
             "rs_kd_weight": ([dbl, P(dbl), i32, _KDPolicy, P(ctypes.c_int)], dbl),
             "rs_kd_update_tabular": ([vp, vp, P(_KDSample), i32, _KDPolicy, P(u64), dbl, P(vp), P(_KDResult)],
                                      ctypes.c_int),
@@ -998,6 +999,25 @@ class BatchEngine:
         for i in range(k):
             e = [x for x in ext[i * W:(i + 1) * W] if x >= 0]
             out.append((role[i], req[i], cl[i], e, lg[i * V:(i + 1) * V]))
+        return out
+
+    def captured_meta(self):
+        """Metadata of the captured rows without the logits: [(role, request, ctx_len, ext)]."""
+        n, V, W = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().rs_engine_capture_count(self.handle, ctypes.byref(n), ctypes.byref(V), ctypes.byref(W)))
+        k, W = n.value, W.value
+        if k == 0:
+            return []
+        role, req, cl = (ctypes.c_int32 * k)(), (ctypes.c_int32 * k)(), (ctypes.c_int32 * k)()
+        ext = (ctypes.c_int32 * (k * W))()
+        _check(lib().rs_engine_capture_read(self.handle, 0, k, role, req, cl, ext, None))
+        return [(role[i], req[i], cl[i], [x for x in ext[i * W:(i + 1) * W] if x >= 0]) for i in range(k)]
+
+    def captured_logits_f32(self, first: int, count: int):
+        """numpy float32 [count, V] of captured transformer rows first..first+count."""
+        import numpy as np
+        out = np.empty((count, self._target.vocab_size), dtype=np.float32)
+        _check(lib().rs_engine_capture_read_f32(self.handle, first, count, ctypes.c_void_p(out.ctypes.data)))
         return out
 
     def __del__(self):

@@ -684,8 +684,21 @@ int rs_engine_capture_read(rs_engine *e, int64_t first, int64_t count, int32_t *
             if (req) req[i] = e->cap_req[k];
             if (ctx_len) ctx_len[i] = e->cap_ctx_len[k];
             if (ext) std::copy_n(&e->cap_ext[k * e->n_max], e->n_max, ext + i * e->n_max);
-            if (logits) std::copy_n(&e->cap_logits[k * e->V], e->V, logits + i * e->V);
+            if (logits) {
+                if (!e->cap_logits.empty()) std::copy_n(&e->cap_logits[k * e->V], e->V, logits + i * e->V);
+                else std::copy_n(&e->cap_f32[k * e->V], e->V, logits + i * e->V);
+            }
         }
+    });
+}
+int rs_engine_capture_read_f32(rs_engine *e, int64_t first, int64_t count, float *logits) {
+    return guard([&] {
+        need(e, "rs_engine_capture_read_f32");
+        need(logits, "rs_engine_capture_read_f32: logits");
+        const int64_t total = (int64_t)e->cap_role.size();
+        if (first < 0 || count < 0 || first + count > total) throw std::invalid_argument("capture range");
+        if (!e->cap_logits.empty()) throw std::invalid_argument("rs_engine_capture_read_f32: rows are fp64");
+        std::copy_n(&e->cap_f32[first * e->V], count * e->V, logits);
     });
 }
 

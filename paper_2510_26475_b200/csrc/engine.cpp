@@ -254,8 +254,13 @@ void rs_engine::capture_rows(const SdDev &d, bool verify, int depth) {
         cap_req.push_back(r);
         cap_ctx_len.push_back(lens[r]);
         for (int k = 0; k < n_max; ++k) cap_ext.push_back(k < e ? ext[k] : -1);
-        for (int x = 0; x < V; ++x)
-            cap_logits.push_back(es == 8 ? reinterpret_cast<double *>(row.data())[x] : reinterpret_cast<float *>(row.data())[x]);
+        if (es == 8) {
+            const double *x = reinterpret_cast<const double *>(row.data());
+            cap_logits.insert(cap_logits.end(), x, x + V);
+        } else {
+            const float *x = reinterpret_cast<const float *>(row.data());
+            cap_f32.insert(cap_f32.end(), x, x + V);
+        }
     };
     const bool naive = !mode.enabled;
     for (int a = 0; a < nact; ++a) {

@@ -202,7 +202,8 @@ struct rs_engine {
     // capture (debug replay against the CPU oracle)
     bool capture = false;
     std::vector<int32_t> cap_role, cap_req, cap_ctx_len, cap_ext;  // ext: up to n_max tokens
-    std::vector<double> cap_logits;
+    std::vector<double> cap_logits;  // fp64 rows (tabular parity mode)
+    std::vector<float> cap_f32;      // fp32 rows (transformer logits), stored as produced
 
     ~rs_engine();
     rs::SdDev dev(const rs_sdconfig &cfg, int nact);

@@ -48,6 +48,47 @@ class Oracle(_JsonLib):
 
     def __init__(self):
         super().__init__(os.path.join(ROOT, "oracle", "build", "liboracle.so"))
+        self.lib.oracle_lookup_new.restype = ctypes.c_int
+        self.lib.oracle_lookup_new.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int]
+        self.lib.oracle_lookup_add_f32.restype = ctypes.c_int
+        self.lib.oracle_lookup_add_f32.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int,
+                                                   ctypes.c_int, ctypes.c_void_p]
+        self.lib.oracle_lookup_free.argtypes = [ctypes.c_int]
+
+    def lookup(self, vocab, temperature=1.0, depth_aware=False):
+        return LookupHandle(self, vocab, temperature, depth_aware)
+
+
+class LookupHandle:
+    """A LookupModel inside liboracle filled through the binary entry (fp32 rows at V ~ 152K
+    do not fit the JSON transport). Use `.json()` as the model in a request."""
+
+    def __init__(self, oracle, vocab, temperature=1.0, depth_aware=False):
+        self.lib = oracle.lib
+        self.vocab = vocab
+        self.id = self.lib.oracle_lookup_new(vocab, ctypes.c_double(temperature), 1 if depth_aware else 0)
+        self.added = self.duplicates = 0
+
+    def add(self, ctx, depth, logits_f32):
+        import numpy as np
+        row = np.ascontiguousarray(logits_f32, dtype=np.float32)
+        assert row.shape == (self.vocab,)
+        c = (ctypes.c_int * len(ctx))(*ctx)
+        r = self.lib.oracle_lookup_add_f32(self.id, c, len(ctx), depth, ctypes.c_void_p(row.ctypes.data))
+        if r < 0:
+            raise AssertionError("same context produced a different logit row (row invariance broken)"
+                                 if r == -1 else "unknown lookup id")
+        self.added += r == 0
+        self.duplicates += r == 1
+
+    def json(self):
+        return {"kind": "lookup_ref", "id": self.id}
+
+    def __del__(self):
+        try:
+            self.lib.oracle_lookup_free(self.id)
+        except Exception:
+            pass
 
 
 class Reference(_JsonLib):

@@ -111,7 +111,16 @@ def test_engine_errors_match_reference():
     while not eng3.all_done():
         eng3.step()
     for r in eng3.requests():  # drafter == target accepts every drafted token (test_specdec.cpp:76-85)
-        assert all(a == min(3, a) for a in r.accept_lens)
+        # n_eff = min(3, remaining - 1) (specdec.cpp:170): a full cycle accepts all 3; only the
+        # budget-limited last cycle drafts fewer, and then accepts all it drafted; a chain that
+        # drafts EOS stops there (every token of it accepted)
+        assert r.accept_lens
+        emitted = 0
+        for k, a in enumerate(r.accept_lens):
+            n_eff = min(3, r.max_len - emitted - 1)
+            last = k == len(r.accept_lens) - 1
+            assert a == n_eff or (last and r.generated[-1] == target.eos), (k, a, n_eff)
+            emitted += a + 1
 
 
 def test_distributed_kd_step_on_gpu():

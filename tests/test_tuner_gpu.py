@@ -27,15 +27,37 @@ def table(models):
     return rb.profile_measured(tgt, drf, [1, 2, 4], CFGS, prompt_len=16, warmup=1, cycles=3)
 
 
-def test_measured_table_is_complete(table):
+def _reference_best(ents):
+    """ProfileTable::finalize (server.cpp:21-54): a scan in insertion order; strictly lower
+    time wins, ties go to fewer drafted tokens (off counts 0), then to non-spec."""
+    best = None
+    for cfg, tpt in ents:
+        if best is None or tpt < best[1]:
+            best = (cfg, tpt)
+        elif tpt == best[1]:
+            cur = cfg.drafted_per_cycle() if cfg.enabled else 0
+            old = best[0].drafted_per_cycle() if best[0].enabled else 0
+            if cur < old or (cur == old and not cfg.enabled and best[0].enabled):
+                best = (cfg, tpt)
+    return best[0]
+
+
+def test_measured_table_is_complete(table, oracle):
     keys = {c.key() for c in CFGS} | {rb.SDConfig.off().key()}
+    j = table.to_json()
+    exp = oracle("profile_table", buckets=j["buckets"], entries=j["entries"], solve=[1, 2, 3, 4, 9])
     for b in (1, 2, 4):
         ents = table._entries[b]
         assert {c.key() for c, _ in ents} == keys
         assert all(0 < t < 1e3 for _, t in ents)  # ms per emitted token
         best = table.best_for_bucket(b)
-        want = min(ents, key=lambda e: (e[1], e[0].drafted_per_cycle() if e[0].enabled else -1))
-        assert best.key() == want[0].key() or best.key() in keys
+        assert best.key() == _reference_best(ents).key()  # measured argmin, reference tie-break
+        want = next(e["cfg"] for e in exp["best"] if e["bucket"] == b)
+        assert (best.rounds, best.branching, best.draft_len, best.enabled) == \
+            ((want["s"], want["t"], want["n"], True) if want["enabled"] else (best.rounds, best.branching,
+                                                                              best.draft_len, False))
+    for s in exp["solve"]:  # bucket_for clamps above the largest bucket (server.cpp:56-66)
+        assert table.bucket_for(s["batch"]) == s["bucket"]
     j = table.to_json()
     t2 = rb.ProfileTable.from_json(j)
     for b in (1, 2, 4):

@@ -70,8 +70,9 @@ class TargetRef:
         mlp = bf(torch.nn.functional.silu(h2 @ L["g_w"].t()) * (h2 @ L["u_w"].t()))
         return x + mlp @ L["down_w"].t()
 
-    def forward(self, tokens):
-        """Logits [T, V] for every position and the EAGLE features [T, 3, d]."""
+    def forward(self, tokens, last_only=False):
+        """Logits [T, V] for every position (last_only: [1, V] for the last position; the
+        full-vocabulary rows at V ~ 152K are large) and the EAGLE features [T, 3, d]."""
         dev = self.emb.device
         tok = torch.tensor(tokens, device=dev)
         pos = torch.arange(len(tokens), device=dev)
@@ -82,6 +83,8 @@ class TargetRef:
             for f in self.feat_layers:
                 if f == l:
                     feats.append(bf(x))
+        if last_only:
+            x = x[-1:]
         logits = (self.rms(x, self.final) @ self.emb.t()) * self.s.logit_scale
         return logits, torch.stack(feats, 1)
 
@@ -106,18 +109,18 @@ class DrafterRef:
         self.final = dm.to_torch("final_norm").float()
         self.lm = dm.to_torch("lm_w").view(s.vocab, d).float()
 
-    def context_logits(self, tokens):
+    def context_logits(self, tokens, last_only=False):
         """q rows for every prefix of `tokens` with target features (the depth-0 / catch-up
-        path). Returns [T, V] where row p is q(. | tokens[:p+1])."""
+        path). Returns [T, V] where row p is q(. | tokens[:p+1]) ([1, V] with last_only)."""
         t = self.t
-        _, feats = t.forward(tokens)
+        _, feats = t.forward(tokens, last_only=True)
         T, d = len(tokens), self.s.d_model
         prev = torch.zeros(T, 3 * d, device=feats.device)
         prev[1:] = feats[:-1].reshape(T - 1, 3 * d)
         f = prev @ self.fc.t()
-        return self._layer_logits(tokens, f)[0]
+        return self._layer_logits(tokens, f, last_only)[0]
 
-    def _layer_logits(self, tokens, f):
+    def _layer_logits(self, tokens, f, last_only=False):
         t, s = self.t, self.s
         dev = f.device
         tok = torch.tensor(tokens, device=dev)
@@ -134,4 +137,5 @@ class DrafterRef:
         x = f + t.attend(q, k, v).reshape(T, H * hd) @ L["o_w"].t()
         h2 = t.rms(x, L["ln2"])
         x = x + bf(torch.nn.functional.silu(h2 @ L["g_w"].t()) * (h2 @ L["u_w"].t())) @ L["down_w"].t()
-        return (t.rms(x, self.final) @ self.lm.t()) * t.s.logit_scale, x
+        y = x[-1:] if last_only else x
+        return (t.rms(y, self.final) @ self.lm.t()) * t.s.logit_scale, x
