@@ -36,6 +36,7 @@ typedef struct rs_model rs_model;   /* immutable device-resident model (tabular 
 typedef struct rs_table rs_table;   /* ProfileTable, server.hpp:21-49 */
 typedef struct rs_engine rs_engine; /* BatchEngine, server.hpp:98-132 */
 typedef struct rs_learner rs_learner; /* OnlineLearner, learner.hpp:87-139 */
+typedef struct rs_comm rs_comm;     /* one rank of an NCCL communicator (drafter-gradient all-reduce) */
 
 /* SDConfig (specdec.hpp:17-37). enabled=0 is the non-spec configuration. */
 typedef struct {
@@ -395,6 +396,36 @@ int rs_group_advantages(const double *rewards, int32_t g, double *out);
 int rs_policy_update_tabular(rs_ctx *ctx, const rs_model *actor, const rs_kd_sample *samples,
                              const double *advantages, const int32_t *actor_versions, int32_t n, double lr,
                              rs_model **out);
+
+/* ---- multi-GPU: the KD gradient all-reduce ---------------------------
+   Replaces the cross-sample sum of kd_loss_gradient (learner.cpp:68-80) when the rollouts are
+   sharded by prompt over the GPUs of a box (one process or thread per GPU); the
+   generation path itself has no collective. NCCL is loaded at run time (libnccl.so.2).
+   rs_comm_unique_id -- rank 0 creates the 128-byte id, the caller ships it to the other ranks;
+   rs_comm_create    -- ncclCommInitRank on the context's device (collective over all ranks);
+   rs_comm_allreduce -- in-place all-reduce of a device buffer on the context's stream;
+   rs_comm_allreduce_host -- synchronous all-reduce of <= 64 host doubles (losses, token
+                       counts, max-over-ranks device times). */
+#define RS_COMM_ID_BYTES 128
+#define RS_DT_F32 0
+#define RS_DT_F64 1
+#define RS_DT_I64 2
+#define RS_OP_SUM 0
+#define RS_OP_MAX 1
+int rs_nccl_version(int32_t *out);
+int rs_comm_unique_id(uint8_t *id);
+int rs_comm_create(rs_ctx *ctx, int32_t nranks, int32_t rank, const uint8_t *id, rs_comm **out);
+int rs_comm_destroy(rs_comm *c);
+int rs_comm_size(const rs_comm *c, int32_t *nranks, int32_t *rank);
+int rs_comm_allreduce(rs_comm *c, rs_ctx *ctx, void *buf_dev, int64_t count, int32_t dtype, int32_t op);
+int rs_comm_allreduce_host(rs_comm *c, rs_ctx *ctx, double *vals, int32_t n, int32_t op);
+/* Library-owned device memory (gradient buffers) and copies on the context's stream; the
+   h2d / d2h copies are synchronous. */
+int rs_device_alloc(rs_ctx *ctx, int64_t bytes, void **out);
+int rs_device_free(rs_ctx *ctx, void *p);
+int rs_memset_async(rs_ctx *ctx, void *p, int32_t value, int64_t bytes);
+int rs_memcpy_h2d(rs_ctx *ctx, void *dst_dev, const void *src, int64_t bytes);
+int rs_memcpy_d2h(rs_ctx *ctx, void *dst, const void *src_dev, int64_t bytes);
 
 #ifdef __cplusplus
 }

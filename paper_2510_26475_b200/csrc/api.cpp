@@ -345,7 +345,13 @@ int rs_engine_set_drafter(rs_engine *e, const rs_model *drafter) {
     return guard([&] { need(e, "rs_engine_set_drafter"); e->pending_drafter = drafter; });
 }
 int rs_engine_step(rs_engine *e, rs_step_info *info) {
-    return guard([&] { need(e, "rs_engine_step"); e->step(info); });
+    return guard([&] {
+        need(e, "rs_engine_step");
+        e->check_unpinned("BatchEngine::step");
+        std::unique_lock<std::mutex> lk(e->use_mu, std::try_to_lock);
+        if (!lk) throw std::runtime_error("BatchEngine::step: engine in use by another thread");
+        e->step(info);
+    });
 }
 int rs_engine_all_done(const rs_engine *e, int32_t *out) {
     return guard([&] {
@@ -779,6 +785,8 @@ int rs_engine_kd_grad(rs_engine *e, const rs_model *drafter, const int32_t *req,
     return guard([&] {
         need(e, "rs_engine_kd_grad");
         need(grad_dev, "rs_engine_kd_grad: grad");
+        std::unique_lock<std::mutex> lk(e->use_mu, std::try_to_lock);
+        if (!lk) throw std::runtime_error("rs_engine_kd_grad: engine in use by another thread");
         if (n > 0) need(req, "rs_engine_kd_grad: requests");
         if (!e->pair) throw std::runtime_error("rs_engine_kd_grad: engine has no model pair");
         const auto *t = static_cast<const rs::TransformerModel *>(e->target);

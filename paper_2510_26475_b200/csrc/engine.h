@@ -3,6 +3,7 @@
 // kernels through the launchers in sd.h (tabular) and model.h (transformer).
 #pragma once
 #include <atomic>
+#include <mutex>
 #include <stdexcept>
 
 #include <cuda_runtime.h>
@@ -76,7 +77,14 @@ struct rs_model {
     // Handles are reference-counted: rs_model_retain adds one, rs_model_destroy drops one and
     // frees the weights at zero (learner snapshots are shared between the learner and callers).
     std::atomic<int> refs{1};
+    // Process-unique id: a snapshot allocated at a freed snapshot's address is still a new
+    // snapshot (engines key their drafter-cache invalidation on it, not on the pointer).
+    const uint64_t uid = next_uid();
     explicit rs_model(Kind k) : kind(k) {}
+    static uint64_t next_uid() {
+        static std::atomic<uint64_t> n{1};
+        return n.fetch_add(1);
+    }
     virtual ~rs_model() = default;
 };
 
@@ -151,6 +159,17 @@ struct rs_table {
 
 struct rs_engine {
     rs_ctx *ctx = nullptr;
+    // Held while the engine's device state is in use: by step() / kd_grad on the caller's
+    // thread and by a KD update that reads the engine's resident caches (possibly on an
+    // asynchronous learner's worker). Overlap raises instead of corrupting the rollout.
+    std::mutex use_mu;
+    // Scheduled KD updates that will read this engine's resident caches: step() refuses to run
+    // while any is pending (the rollout state they read must stay as it was fed).
+    std::atomic<int> kd_pins{0};
+    void check_unpinned(const char *what) const {
+        if (kd_pins.load() > 0)
+            throw std::runtime_error(std::string(what) + ": engine is read by a pending KD update (await_pending first)");
+    }
     const rs_model *target = nullptr;
     const rs_model *pending_drafter = nullptr;  // snapshot read at the next step
     const rs::ProfileTable *table = nullptr;

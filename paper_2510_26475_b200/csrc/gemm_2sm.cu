@@ -98,6 +98,11 @@ struct Cfg2 {
     // kind::f16, bf16 x bf16 -> f32, both K-major, N = BT tokens, M = 256 features (pair)
     static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BT >> 3) << 17) |
                                        (static_cast<uint32_t>(256 >> 4) << 24);
+    // dynamic + static (s_last) shared memory within the 227 KB opt-in limit, and the barrier
+    // area (full/empty per stage, tfull/tempty x 2, the TMEM slot) within its 256 bytes
+    static_assert(kSmem + 1024 <= 232448, "gemm2: shared memory over the 227 KB opt-in budget");
+    static_assert((2 * kStages + 4) * 8 + 4 <= 256, "gemm2: barrier area overflow");
+    static_assert(kStages >= 2, "gemm2: ring needs at least two stages");
 };
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }

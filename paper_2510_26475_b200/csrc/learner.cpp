@@ -54,6 +54,13 @@ struct ModelRef {  // one counted reference to an rs_model
 
 }  // namespace
 
+// Engines whose resident caches a scheduled update reads are pinned (one count per sample)
+// from on_iteration_boundary until that update ends; rs_engine_step refuses to run meanwhile.
+void pin_engines(const std::vector<Sample> &batch, int delta) {
+    for (const Sample &x : batch)
+        if (x.eng) x.eng->kd_pins.fetch_add(delta);
+}
+
 struct rs_learner {
     rs_ctx *ctx = nullptr;      // caller's context (synchronous updates run on its stream)
     rs_ctx *own = nullptr;      // async worker's context (its own stream)
@@ -67,6 +74,8 @@ struct rs_learner {
     mutable std::mutex mu;
     std::condition_variable cv;
     ModelRef snapshot;
+    int vocab = 0;                      // of every snapshot version (fixed at creation; read
+    rs_model::Kind kind = rs_model::Tabular;  // without `mu` by feed / feed_engine)
     std::vector<rs_learner_metric> metrics;
     double sim_time = 0.0;
     std::deque<std::vector<Sample>> jobs;
@@ -117,7 +126,9 @@ struct rs_learner {
                         refs.push_back(rs::KdRef{batch[idx[j]].req, w[j], batch[idx[j]].eos_bias});
                 if (!refs.empty()) {
                     if (!s0.eng->pair) throw std::runtime_error("OnlineLearner: engine has no model pair");
+                    std::lock_guard<std::mutex> lk(s0.eng->use_mu);  // kd_cached uses the engine's scratch
                     loss += s0.eng->pair->kd_cached(refs, d, grad.p, c->stream);
+                    RS_CUDA(cudaStreamSynchronize(c->stream));  // its caches are read before the engine moves on
                 }
             } else {
                 std::vector<rs::KdSeq> seqs;
@@ -210,6 +221,7 @@ struct rs_learner {
                 busy = true;
             }
             int st = guard([&] { do_update(batch, own); });
+            pin_engines(batch, -1);
             {
                 std::lock_guard<std::mutex> lock(mu);
                 busy = false;
@@ -268,6 +280,8 @@ int rs_learner_create(rs_ctx *ctx, const rs_model *drafter, rs_kd_policy policy,
         auto *m = const_cast<rs_model *>(drafter);
         m->refs.fetch_add(1, std::memory_order_relaxed);
         l->snapshot = ModelRef(m);
+        l->vocab = m->vocab;
+        l->kind = m->kind;
         l->async = async != 0;
         if (l->async) {
             rs_abi::rethrow(rs_ctx_create(ctx->device, &l->own));
@@ -287,7 +301,7 @@ int rs_learner_feed(rs_learner *l, const rs_kd_sample *samples, int32_t n) {
     return guard([&] {
         need(l, "rs_learner_feed");
         if (n > 0) need(samples, "rs_learner_feed: samples");
-        const int V = l->snapshot.m->vocab;
+        const int V = l->vocab;
         for (int i = 0; i < n; ++i) {
             const rs_kd_sample &x = samples[i];
             if (x.prompt_len < 0 || x.response_len < 0) throw std::invalid_argument("feed: negative length");
@@ -315,7 +329,7 @@ int rs_learner_feed_engine(rs_learner *l, rs_engine *e, const int32_t *req, cons
             need(req, "rs_learner_feed_engine: requests");
             need(reward, "rs_learner_feed_engine: rewards");
         }
-        if (l->snapshot.m->kind != rs_model::Drafter || e->target->kind != rs_model::Transformer)
+        if (l->kind != rs_model::Drafter || e->target->kind != rs_model::Transformer)
             throw std::invalid_argument("OnlineLearner: engine samples need an EAGLE drafter and a transformer engine");
         for (int i = 0; i < n; ++i) {
             if (req[i] < 0 || req[i] >= e->n) throw std::invalid_argument("feed: request index out of range");
@@ -341,7 +355,12 @@ int rs_learner_on_iteration_boundary(rs_learner *l, int32_t iteration) {
         std::vector<Sample> batch(std::make_move_iterator(l->buffer.begin()), std::make_move_iterator(l->buffer.end()));
         l->buffer.clear();
         if (batch.empty()) return;
+        pin_engines(batch, +1);
         if (!l->async) {
+            struct Unpin {
+                std::vector<Sample> &b;
+                ~Unpin() { pin_engines(b, -1); }
+            } unpin{batch};
             l->do_update(batch, l->ctx);
             return;
         }

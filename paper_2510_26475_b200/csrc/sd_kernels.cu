@@ -1025,8 +1025,12 @@ void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t s
     int threads = th;
     if (d.V > 4096) {
         threads = 256;
-        int sms = 148;
-        RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+        static const int sms = [] {  // of the current device, queried once (hot path)
+            int dev = 0, v = 148;
+            RS_CUDA(cudaGetDevice(&dev));
+            RS_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+            return v;
+        }();
         while (C < kMaxCluster && (long)d.nact * C * 2 <= 8L * sms) C *= 2;
     }
     if (tuning().accept_cluster > 0) {

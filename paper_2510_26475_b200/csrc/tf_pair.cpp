@@ -295,6 +295,7 @@ struct TransformerPair : ModelPair {
     rs_engine *eng;
     const TransformerModel *tgt;
     const DrafterModel *drf = nullptr;
+    uint64_t drf_uid = 0;
     TfShape s;
     int B = 0, slots_max = 1, max_ctx = 0, per_item = 8, per_item_t = 8;
     bool tc_attn = true;  // target attention on tcgen05 (attention_tc.cu); fixed for the engine's life
@@ -313,7 +314,7 @@ struct TransformerPair : ModelPair {
     } kd_scr;
 
     TransformerPair(rs_ctx *c, rs_engine *e, const TransformerModel *t, const DrafterModel *d)
-        : ctx(c), eng(e), tgt(t), drf(d), s(t->s) {}
+        : ctx(c), eng(e), tgt(t), drf(d), drf_uid(d ? d->uid : 0), s(t->s) {}
 
     RowType row_type() const override { return RowType::F32; }
     void begin_step() override { stage.off = 0; }
@@ -322,8 +323,11 @@ struct TransformerPair : ModelPair {
         if (m && m->kind != rs_model::Drafter) throw std::invalid_argument("transformer target needs an EAGLE drafter");
         const auto *dm = static_cast<const DrafterModel *>(m);
         if (dm && dm->target != tgt) throw std::invalid_argument("drafter is bound to a different target");
-        if (dm != drf) std::fill(dkv_len.begin(), dkv_len.end(), 0);  // new snapshot: rebuild its cache
+        // new snapshot (by id: a fresh one can reuse a freed one's address): rebuild its cache
+        const uint64_t uid = dm ? dm->uid : 0;
+        if (uid != drf_uid) std::fill(dkv_len.begin(), dkv_len.end(), 0);
         drf = dm;
+        drf_uid = uid;
     }
 
     void setup(int n_req, int slots, const std::vector<int> &plen, int tok_cap, int t_max) {

@@ -262,3 +262,28 @@ def test_async_engine_backed_update_overlaps_a_rollout():
     assert got_b == want_b
     assert torch.equal(L.snapshot().to_torch("lm_w"), want_head)
     assert L.metrics()[0].kd_loss == ref.metrics()[0].kd_loss
+
+
+def test_engine_pins_are_released_after_updates():
+    """Engines read by a scheduled KD update are pinned until it ends (stepping one meanwhile
+    raises instead of corrupting what the update reads); after the update -- sync, or async
+    after await_pending -- the engine steps again."""
+    import random
+    shape = rb.TransformerShape.tiny(vocab=512, max_ctx=128)
+    tgt = rb.TransformerModel(shape, seed=9)
+    drf = rb.EagleDrafter(tgt, seed=10)
+    rng = random.Random(3)
+    reqs = [rb.RequestState(i, [rng.randrange(511) for _ in range(6)], -1.0, 12, rb.DecodeRng.from_seed(3, i))
+            for i in range(4)]
+    e = rb.BatchEngine(tgt, lambda: drf, None, rb.TimingModel(), reqs, rb.SDConfig.tree(1, 2, 3), "sample",
+                       record_full_logprobs=False)
+    e.step()
+    pol = rb.KDPolicy(1, rb.WeightMode.Uniform, 0.0, 4.0, 0.5)
+    for async_ in (False, True):
+        L = rb.OnlineLearner(drf, pol, 3, 0.0, 64, async_)
+        L.feed_engine(e, [0, 1], [1.0, 0.5])
+        L.on_iteration_boundary(0)
+        L.await_pending()
+        assert L.drafter_version() == drf.version + 1
+        e.step()  # unpinned
+        L.close()

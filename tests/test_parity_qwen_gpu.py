@@ -87,44 +87,65 @@ def test_greedy_sd_equals_greedy_decode(models, cfg):
     assert got == want
 
 
+def _ref_row(tref, dref, role, toks, cl, ext):
+    d = tref.s.d_model
+    if role == 1:
+        return tref.forward(toks, last_only=True)[0][-1]
+    if not ext:
+        return dref.context_logits(toks, last_only=True)[-1]
+    # deeper drafter rows: feature = the drafter's own hidden state one depth up
+    _, feats = tref.forward(toks[:cl], last_only=True)
+    prev = torch.zeros(cl, 3 * d, device="cuda")
+    prev[1:] = feats[:-1].reshape(cl - 1, 3 * d)
+    f = tref.mm(prev, dref.fc)
+    for p in range(cl, len(toks)):
+        _, x = dref._layer_logits(toks[:p], f, last_only=True)
+        f = torch.cat([f, x[-1:]], 0)
+    return dref._layer_logits(toks, f, last_only=True)[0][-1]
+
+
+def _err(a, ref):
+    dz = a - ref
+    sd = ref.std().item()
+    return dz.abs().max().item() / sd, dz.pow(2).mean().sqrt().item() / sd
+
+
 def test_logits_match_torch_reference(models):
-    """Target verify rows (root and in-tree), depth-0 and deeper drafter rows vs fp32 torch."""
+    """Target verify rows (root and in-tree), depth-0 and deeper drafter rows vs fp32 torch.
+
+    Tolerance, self-calibrated: the fp32 reference and the same reference with bf16-operand
+    matmuls (fp32 accumulation; a second valid bf16 implementation) differ by the flips of the
+    bf16 rounding points, which grow with d and depth (rms ~1e-2 of the logit std at 4 layers,
+    d = 2048..5120; the max over V ~ 152K columns sits ~5 rms out). The CUDA rows must stay
+    within 2x that floor (rms and max), and below absolute bars of 2e-2 rms / 1e-1 max."""
     name, tgt, drf = models
     eng = run(tgt, drf, make_requests(tgt.shape, 2, 6), rb.SDConfig.tree(1, 4, 5), "sample", capture=True)
     reqs = eng.requests()
     full = [r.prompt + r.generated for r in reqs]
     meta = eng.captured_meta()
-    tref = TargetRef(tgt)
-    dref = DrafterRef(drf, tref)
-    d = tgt.shape.d_model
+    t32, tbf = TargetRef(tgt), TargetRef(tgt, bf16_mm=True)
+    d32, dbf = DrafterRef(drf, t32), DrafterRef(drf, tbf)
     picked = {"t_root": [], "t_tree": [], "d_root": [], "d_deep": []}
     for i, (role, req, cl, ext) in enumerate(meta):
         k = ("t_" if role == 1 else "d_") + (("tree" if role == 1 else "deep") if ext else "root")
         if len(picked[k]) < 4:
             picked[k].append(i)
     assert all(len(v) >= 2 for v in picked.values()), {k: len(v) for k, v in picked.items()}
-    worst = {}
+    got_e, floor_e = [0.0, 0.0], [0.0, 0.0]
     for kind, idx in picked.items():
         for i in idx:
             role, req, cl, ext = meta[i]
             got = torch.from_numpy(eng.captured_logits_f32(i, 1)[0]).cuda()
             toks = full[req][:cl] + ext
-            if role == 1:
-                ref = tref.forward(toks, last_only=True)[0][-1]
-            elif not ext:
-                ref = dref.context_logits(toks, last_only=True)[-1]
-            else:  # deeper drafter rows: feature = the drafter's own hidden state one depth up
-                _, feats = tref.forward(toks[:cl], last_only=True)
-                prev = torch.zeros(cl, 3 * d, device="cuda")
-                prev[1:] = feats[:-1].reshape(cl - 1, 3 * d)
-                f = prev @ dref.fc.t()
-                for p in range(cl, len(toks)):
-                    _, x = dref._layer_logits(toks[:p], f, last_only=True)
-                    f = torch.cat([f, x[-1:]], 0)
-                ref = dref._layer_logits(toks, f, last_only=True)[0][-1]
-            err = (got - ref).abs().max().item() / ref.std().item()
-            worst[kind] = max(worst.get(kind, 0.0), err)
-    assert max(worst.values()) < 3e-2, worst
+            ref = _ref_row(t32, d32, role, toks, cl, ext)
+            alt = _ref_row(tbf, dbf, role, toks, cl, ext)
+            g, f = _err(got, ref), _err(alt, ref)
+            got_e = [max(got_e[0], g[0]), max(got_e[1], g[1])]
+            floor_e = [max(floor_e[0], f[0]), max(floor_e[1], f[1])]
+    print(name, "cuda vs fp32 (max, rms)/std:", [round(x, 4) for x in got_e],
+          "bf16-matmul torch vs fp32:", [round(x, 4) for x in floor_e])
+    assert got_e[0] < max(2 * floor_e[0], 2e-2) and got_e[0] < 1e-1, (got_e, floor_e)
+    assert got_e[1] < max(2 * floor_e[1], 4e-3) and got_e[1] < 2e-2, (got_e, floor_e)
 
 
 def _replay(oracle, eng, vocab, mode, cfg):

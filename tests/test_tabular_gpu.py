@@ -119,7 +119,7 @@ def test_engine_errors_match_reference():
         for k, a in enumerate(r.accept_lens):
             n_eff = min(3, r.max_len - emitted - 1)
             last = k == len(r.accept_lens) - 1
-            assert a == n_eff or (last and r.generated[-1] == target.eos), (k, a, n_eff)
+            assert a == n_eff or (last and r.generated[-1] == target.vocab_size - 1), (k, a, n_eff)
             emitted += a + 1
 
 

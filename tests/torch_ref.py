@@ -13,9 +13,14 @@ def bf(x):
 
 
 class TargetRef:
-    def __init__(self, m):
+    """bf16_mm=True: every matmul takes bf16 operands with fp32 accumulation (cuBLAS bf16
+    GEMMs) instead of fp32 -- a second, equally valid bf16 implementation whose distance to
+    the fp32 one calibrates the noise floor of the bf16 rounding points."""
+
+    def __init__(self, m, bf16_mm=False):
         s = m.shape
         self.s = s
+        self.bf16_mm = bf16_mm
         d, q = s.d_model, (s.n_heads + 2 * s.n_kv_heads) * s.head_dim
         self.emb = m.to_torch("emb").view(s.vocab, d).float()
         self.final = m.to_torch("final_norm").float()
@@ -29,6 +34,11 @@ class TargetRef:
                 down_w=m.to_torch("down_w", l).view(d, s.d_ff).float(),
                 ln1=m.to_torch("ln1", l).float(), ln2=m.to_torch("ln2", l).float()))
         self.feat_layers = (min(1, s.n_layers - 1), s.n_layers // 2, s.n_layers - 1)
+
+    def mm(self, a, w):
+        if self.bf16_mm:
+            return (a.to(torch.bfloat16) @ w.to(torch.bfloat16).t()).float()
+        return a @ w.t()
 
     def rms(self, x, w):
         return bf(x * torch.rsqrt((x * x).mean(-1, keepdim=True) + self.s.rms_eps) * w)
@@ -59,16 +69,16 @@ class TargetRef:
         s = self.s
         T = x.shape[0]
         h = self.rms(x, L["ln1"])
-        qkv = bf(h @ L["qkv_w"].t() + L["qkv_b"])
+        qkv = bf(self.mm(h, L["qkv_w"]) + L["qkv_b"])
         H, KV, hd = s.n_heads, s.n_kv_heads, s.head_dim
         q = self.rope(qkv[:, :H * hd].view(T, H, hd), pos)
         k = self.rope(qkv[:, H * hd:(H + KV) * hd].view(T, KV, hd), pos)
         v = qkv[:, (H + KV) * hd:].view(T, KV, hd)
         ao = self.attend(q, k, v).reshape(T, H * hd)
-        x = x + ao @ L["o_w"].t()
+        x = x + self.mm(ao, L["o_w"])
         h2 = self.rms(x, L["ln2"])
-        mlp = bf(torch.nn.functional.silu(h2 @ L["g_w"].t()) * (h2 @ L["u_w"].t()))
-        return x + mlp @ L["down_w"].t()
+        mlp = bf(torch.nn.functional.silu(self.mm(h2, L["g_w"])) * self.mm(h2, L["u_w"]))
+        return x + self.mm(mlp, L["down_w"])
 
     def forward(self, tokens, last_only=False):
         """Logits [T, V] for every position (last_only: [1, V] for the last position; the
@@ -85,7 +95,7 @@ class TargetRef:
                     feats.append(bf(x))
         if last_only:
             x = x[-1:]
-        logits = (self.rms(x, self.final) @ self.emb.t()) * self.s.logit_scale
+        logits = self.mm(self.rms(x, self.final), self.emb) * self.s.logit_scale
         return logits, torch.stack(feats, 1)
 
 
@@ -117,7 +127,7 @@ class DrafterRef:
         T, d = len(tokens), self.s.d_model
         prev = torch.zeros(T, 3 * d, device=feats.device)
         prev[1:] = feats[:-1].reshape(T - 1, 3 * d)
-        f = prev @ self.fc.t()
+        f = t.mm(prev, self.fc)
         return self._layer_logits(tokens, f, last_only)[0]
 
     def _layer_logits(self, tokens, f, last_only=False):
@@ -130,12 +140,12 @@ class DrafterRef:
         L = self.L
         T = len(tokens)
         H, KV, hd = s.n_heads, s.n_kv_heads, s.head_dim
-        qkv = bf(h @ L["qkv_w"].t() + L["qkv_b"])
+        qkv = bf(t.mm(h, L["qkv_w"]) + L["qkv_b"])
         q = t.rope(qkv[:, :H * hd].view(T, H, hd), pos)
         k = t.rope(qkv[:, H * hd:(H + KV) * hd].view(T, KV, hd), pos)
         v = qkv[:, (H + KV) * hd:].view(T, KV, hd)
-        x = f + t.attend(q, k, v).reshape(T, H * hd) @ L["o_w"].t()
+        x = f + t.mm(t.attend(q, k, v).reshape(T, H * hd), L["o_w"])
         h2 = t.rms(x, L["ln2"])
-        x = x + bf(torch.nn.functional.silu(h2 @ L["g_w"].t()) * (h2 @ L["u_w"].t())) @ L["down_w"].t()
+        x = x + t.mm(bf(torch.nn.functional.silu(t.mm(h2, L["g_w"])) * t.mm(h2, L["u_w"])), L["down_w"])
         y = x[-1:] if last_only else x
-        return (t.rms(y, self.final) @ self.lm.t()) * t.s.logit_scale, x
+        return t.mm(t.rms(y, self.final), self.lm) * t.s.logit_scale, x
