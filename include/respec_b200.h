@@ -321,13 +321,22 @@ int rs_tabular_apply_delta(rs_ctx *ctx, const rs_model *m, const double *grad, d
 /* Transformer drafters (EAGLE-3-style) -- the same kd_update (learner.cpp:98-160) with the
    drafter's distribution q recomputed by its forward and the target rows p~ recomputed by a
    teacher-forced target forward over prompt + response (StepRecord::target_logprobs are not
-   materialised at V = 152K; rs_kd_sample.target_logprobs is ignored and may be NULL). The
-   trained parameters are the drafter's LM head: dL/dW_lm = logit_scale * sum_t dZ_t^T h_t with
-   dZ_t = w (q_t - p~_t) / tau (learner.cpp:62-82) and h_t the final-normed drafter hidden state.
-   rs_kd_grad_transformer   -- the per-rank piece: sum_i w_i KL_i and the fp32 [V][d] gradient of
-                               the given samples (accumulated into grad_dev unless zero_grad);
-   rs_drafter_apply_grad    -- new snapshot (version + 1) with lm_w + scale * grad;
+   materialised at V = 152K; rs_kd_sample.target_logprobs is ignored and may be NULL). As in the
+   reference, where the gradient covers the whole model (learner.cpp:62-82) and the update moves
+   every parameter (with_logits_delta, :146-151), EVERY drafter tensor is trained: dZ_t =
+   w (q_t - p~_t) / tau at the response positions, backpropagated through the LM head, final
+   norm, SwiGLU MLP, post-attention norm, O projection, causal attention (into every position's
+   keys / values), RoPE, QKV (+ bias), the two input norms and fc. The target (and the shared
+   embedding) is frozen.
+   rs_drafter_grad_layout   -- the fp32 gradient buffer: total floats (name NULL) or the
+                               (offset, count) of one tensor ("lm_w", "fc_w", "norm_emb",
+                               "norm_hid", "qkv_w", "qkv_b", "o_w", "ln2", "gu_w", "down_w",
+                               "final_norm"); the LM head comes first ([V][d] at offset 0);
+   rs_kd_grad_transformer   -- the per-rank piece: sum_i w_i KL_i and the gradient of the given
+                               samples (accumulated into grad_dev unless zero_grad);
+   rs_drafter_apply_grad    -- new snapshot (version + 1): every tensor w + scale * grad;
    rs_kd_update_transformer -- single-process kd_update: select, weight, gradient, SGD (-lr). */
+int rs_drafter_grad_layout(const rs_model *drafter, const char *name, int64_t *offset, int64_t *count);
 int rs_kd_grad_transformer(rs_ctx *ctx, const rs_model *target, const rs_model *drafter, const rs_kd_sample *samples,
                            int32_t n, const double *weights, float *grad_dev, int32_t zero_grad, double *loss_out);
 int rs_drafter_apply_grad(rs_ctx *ctx, const rs_model *drafter, const float *grad_dev, double scale, rs_model **out);

@@ -135,6 +135,9 @@ EXPORTED_SYMBOLS = [
     "rs_reward", "rs_group_advantages", "rs_policy_update_tabular",
     "rs_engine_set_stop_at_eos", "rs_profile_simulated", "rs_tabular_random", "rs_skew_eos_biases",
     "rs_engine_kd_grad", "rs_engine_rng_export", "rs_engine_rng_import", "rs_learner_feed_engine",
+    "rs_drafter_grad_layout", "rs_nccl_version", "rs_comm_unique_id", "rs_comm_create", "rs_comm_destroy",
+    "rs_comm_size", "rs_comm_allreduce", "rs_comm_allreduce_host", "rs_device_alloc", "rs_device_free",
+    "rs_memset_async", "rs_memcpy_h2d", "rs_memcpy_d2h",
 ]
 
 _lib = None
@@ -244,6 +247,19 @@ def lib():
             "rs_engine_rng_export": ([vp, i32, P(u64), i64, P(i64)], ctypes.c_int),
             "rs_engine_rng_import": ([vp, i32, P(u64), i64], ctypes.c_int),
             "rs_learner_feed_engine": ([vp, vp, P(i32), P(dbl), i32], ctypes.c_int),
+            "rs_drafter_grad_layout": ([vp, ctypes.c_char_p, P(i64), P(i64)], ctypes.c_int),
+            "rs_nccl_version": ([P(i32)], ctypes.c_int),
+            "rs_comm_unique_id": ([P(ctypes.c_uint8)], ctypes.c_int),
+            "rs_comm_create": ([vp, i32, i32, P(ctypes.c_uint8), P(vp)], ctypes.c_int),
+            "rs_comm_destroy": ([vp], ctypes.c_int),
+            "rs_comm_size": ([vp, P(i32), P(i32)], ctypes.c_int),
+            "rs_comm_allreduce": ([vp, vp, vp, i64, i32, i32], ctypes.c_int),
+            "rs_comm_allreduce_host": ([vp, vp, P(dbl), i32, i32], ctypes.c_int),
+            "rs_device_alloc": ([vp, i64, P(vp)], ctypes.c_int),
+            "rs_device_free": ([vp, vp], ctypes.c_int),
+            "rs_memset_async": ([vp, vp, i32, i64], ctypes.c_int),
+            "rs_memcpy_h2d": ([vp, vp, vp, i64], ctypes.c_int),
+            "rs_memcpy_d2h": ([vp, vp, vp, i64], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -307,6 +323,68 @@ def default_device() -> Device:
     if _default_device is None:
         _default_device = Device(0)
     return _default_device
+
+
+class DeviceBuffer:
+    """Library-owned device memory (rs_device_alloc): the drafter gradient of the KD update and
+    its all-reduce need no tensor framework. fp32 elements unless stated."""
+
+    def __init__(self, nbytes: int, device: Optional["Device"] = None, zero: bool = True):
+        self.device = device or default_device()
+        self.nbytes = int(nbytes)
+        p = ctypes.c_void_p()
+        _check(lib().rs_device_alloc(self.device.handle, self.nbytes, ctypes.byref(p)))
+        self.ptr = p.value or 0
+        if zero:
+            self.zero()
+
+    @staticmethod
+    def floats(n: int, device: Optional["Device"] = None) -> "DeviceBuffer":
+        return DeviceBuffer(4 * int(n), device)
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+    @property
+    def numel(self) -> int:
+        return self.nbytes // 4
+
+    def zero(self) -> "DeviceBuffer":
+        _check(lib().rs_memset_async(self.device.handle, ctypes.c_void_p(self.ptr), 0, self.nbytes))
+        return self
+
+    def clone(self) -> "DeviceBuffer":
+        out = DeviceBuffer(self.nbytes, self.device, zero=False)
+        _check(lib().rs_memcpy_d2d(self.device.handle, ctypes.c_void_p(out.ptr), ctypes.c_void_p(self.ptr),
+                                   self.nbytes))
+        return out
+
+    def to_numpy(self, offset: int = 0, count: Optional[int] = None):
+        """fp32 elements [offset, offset + count) copied to the host."""
+        import numpy as np
+        count = self.numel - offset if count is None else count
+        out = np.empty(count, dtype=np.float32)
+        _check(lib().rs_memcpy_d2h(self.device.handle, ctypes.c_void_p(out.ctypes.data),
+                                   ctypes.c_void_p(self.ptr + 4 * offset), 4 * count))
+        return out
+
+    def to_torch(self, offset: int = 0, count: Optional[int] = None):
+        """A torch CUDA copy (tests only)."""
+        import torch
+        count = self.numel - offset if count is None else count
+        t = torch.empty(count, dtype=torch.float32, device="cuda")
+        torch.cuda.synchronize()
+        _check(lib().rs_memcpy_d2d(self.device.handle, ctypes.c_void_p(t.data_ptr()),
+                                   ctypes.c_void_p(self.ptr + 4 * offset), 4 * count))
+        return t
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                lib().rs_device_free(self.device.handle, ctypes.c_void_p(self.ptr))
+                self.ptr = 0
+        except Exception:
+            pass
 
 
 def device_profile(enable: Optional[bool] = None, reset: bool = False):
@@ -587,8 +665,23 @@ class EagleDrafter(_NeuralModel):
         m.handle, m.target, m.shape, m.device = handle, target, target.shape, target.device
         return m
 
+    GRAD_TENSORS = ("lm_w", "fc_w", "norm_emb", "norm_hid", "qkv_w", "qkv_b", "o_w", "ln2", "gu_w", "down_w",
+                    "final_norm")
+
+    def grad_layout(self, name: Optional[str] = None):
+        """(offset, count) of one tensor in the fp32 drafter gradient (name None: (0, total))."""
+        o, n = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().rs_drafter_grad_layout(self.handle, name.encode() if name else None, ctypes.byref(o),
+                                            ctypes.byref(n)))
+        return o.value, n.value
+
+    def new_grad(self) -> DeviceBuffer:
+        """A zeroed fp32 gradient buffer covering every drafter tensor."""
+        return DeviceBuffer.floats(self.grad_layout()[1], self.device)
+
     def apply_grad(self, grad, scale: float) -> "EagleDrafter":
-        """New snapshot (version + 1): lm_w + scale * grad (fp32 [V][d] device tensor / pointer)."""
+        """New snapshot (version + 1): every tensor w + scale * grad (the fp32 layout of
+        grad_layout; a DeviceBuffer, a tensor with data_ptr, or a raw pointer)."""
         h = ctypes.c_void_p()
         ptr = grad.data_ptr() if hasattr(grad, "data_ptr") else grad
         _check(lib().rs_drafter_apply_grad(self.device.handle, self.handle, ctypes.c_void_p(ptr), scale,
@@ -954,16 +1047,14 @@ class BatchEngine:
 
     def kd_grad(self, drafter: "EagleDrafter", req_ids: Sequence[int], weights: Sequence[float], grad=None,
                 zero_grad: bool = True):
-        """Per-rank K5 + drafter LM-head gradient over these requests' generated tokens, from the
-        engine's resident target KV cache and features (rs_engine_kd_grad): (loss, fp32 [V, d]
-        torch CUDA tensor). Same result as kd_grad_transformer on the same rollouts without the
-        teacher-forced recompute of the prompts."""
-        import torch
-        V, d = drafter.shape.vocab, drafter.shape.d_model
+        """Per-rank K5 + whole-drafter gradient over these requests' generated tokens, from the
+        engine's resident target KV cache and features (rs_engine_kd_grad): (loss, DeviceBuffer
+        in the drafter's grad_layout). Same result as kd_grad_transformer on the same rollouts
+        without the teacher-forced recompute of the prompts."""
         if grad is None:
-            grad = torch.zeros(V, d, dtype=torch.float32, device="cuda")
+            grad = drafter.new_grad()
         loss = ctypes.c_double()
-        torch.cuda.synchronize()
+        self.device.sync()
         _check(lib().rs_engine_kd_grad(self.handle, drafter.handle, _i32arr(req_ids), len(req_ids), _f64arr(weights),
                                        ctypes.c_void_p(grad.data_ptr()), 1 if zero_grad else 0, ctypes.byref(loss)))
         return loss.value, grad
@@ -1245,15 +1336,14 @@ def _kd_samples(buffer: Sequence[RolloutSample], with_logprobs):
 
 def kd_grad_transformer(drafter: "EagleDrafter", samples: Sequence[RolloutSample], weights: Sequence[float],
                         grad=None, zero_grad: bool = True):
-    """Per-rank K5 for a transformer drafter: (sum_i w_i KL_i, fp32 [V, d] LM-head gradient as a
-    torch CUDA tensor). The gradient is what the prompt-sharded learner all-reduces."""
-    import torch
-    V, d = drafter.shape.vocab, drafter.shape.d_model
+    """Per-rank K5 + backward for a transformer drafter: (sum_i w_i KL_i, gradient of every
+    drafter tensor as a DeviceBuffer in drafter.grad_layout()). The gradient is what the
+    prompt-sharded learner all-reduces."""
     if grad is None:
-        grad = torch.zeros(V, d, dtype=torch.float32, device="cuda")
+        grad = drafter.new_grad()
     arr, keep = _kd_samples(samples, False)
     loss = ctypes.c_double()
-    torch.cuda.synchronize()
+    drafter.device.sync()
     _check(lib().rs_kd_grad_transformer(drafter.device.handle, drafter.target.handle, drafter.handle, arr,
                                         len(samples), _f64arr(weights), ctypes.c_void_p(grad.data_ptr()),
                                         1 if zero_grad else 0, ctypes.byref(loss)))
@@ -1273,7 +1363,8 @@ def kd_loss(drafter, sample: RolloutSample, w: float) -> float:
 def kd_loss_gradient(drafter, weighted: Sequence[tuple]):
     """kd_loss_gradient (learner.cpp:62-82): the drafter-logit gradient of sum_i w_i L_KD(sample_i),
     weighted = [(RolloutSample, w)]. Tabular: the full logit-table gradient (list of V^(order+1)
-    floats, reference order); EAGLE drafter: the fp32 [V, d] LM-head gradient (torch CUDA tensor)."""
+    floats, reference order); EAGLE drafter: the gradient of every drafter tensor (DeviceBuffer,
+    drafter.grad_layout())."""
     samples, ws = [x for x, _ in weighted], [w for _, w in weighted]
     if isinstance(drafter, EagleDrafter):
         return kd_grad_transformer(drafter, samples, ws)[1]

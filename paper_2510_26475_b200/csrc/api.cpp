@@ -772,6 +772,35 @@ int rs_kd_grad_transformer(rs_ctx *ctx, const rs_model *target, const rs_model *
     });
 }
 
+int rs_drafter_grad_layout(const rs_model *drafter, const char *name, int64_t *offset, int64_t *count) {
+    return guard([&] {
+        need(drafter, "rs_drafter_grad_layout");
+        if (drafter->kind != rs_model::Drafter) throw std::invalid_argument("rs_drafter_grad_layout: EAGLE drafter required");
+        const auto *d = static_cast<const rs::DrafterModel *>(drafter);
+        const rs::TfShape &s = d->s;
+        const rs::DrafterGradLayout g = rs::drafter_grad_layout(s);
+        const size_t q = s.qkv_dim(), HD = (size_t)s.H * s.hd;
+        size_t off = 0, n = g.total;
+        if (name) {
+            const std::string nm(name);
+            if (nm == "lm_w") { off = g.lm; n = (size_t)s.V * s.d; }
+            else if (nm == "fc_w") { off = g.fc; n = (size_t)s.d * 3 * s.d; }
+            else if (nm == "norm_emb") { off = g.norm_emb; n = s.d; }
+            else if (nm == "norm_hid") { off = g.norm_hid; n = s.d; }
+            else if (nm == "qkv_w") { off = g.qkv_w; n = q * 2 * s.d; }
+            else if (nm == "qkv_b") { off = g.qkv_b; n = q; }
+            else if (nm == "o_w") { off = g.o_w; n = (size_t)s.d * HD; }
+            else if (nm == "ln2") { off = g.ln2; n = s.d; }
+            else if (nm == "gu_w") { off = g.gu_w; n = (size_t)2 * s.dff * s.d; }
+            else if (nm == "down_w") { off = g.down_w; n = (size_t)s.d * s.dff; }
+            else if (nm == "final_norm") { off = g.final_norm; n = s.d; }
+            else throw std::invalid_argument("rs_drafter_grad_layout: unknown tensor " + nm);
+        }
+        if (offset) *offset = (int64_t)off;
+        if (count) *count = (int64_t)n;
+    });
+}
+
 int rs_drafter_apply_grad(rs_ctx *ctx, const rs_model *drafter, const float *grad_dev, double scale, rs_model **out) {
     return guard([&] {
         need(ctx, "rs_drafter_apply_grad");
@@ -791,7 +820,8 @@ int rs_engine_kd_grad(rs_engine *e, const rs_model *drafter, const int32_t *req,
         if (!e->pair) throw std::runtime_error("rs_engine_kd_grad: engine has no model pair");
         const auto *t = static_cast<const rs::TransformerModel *>(e->target);
         if (e->target->kind != rs_model::Transformer) throw std::invalid_argument("kd from the engine needs a transformer target");
-        if (zero_grad) RS_CUDA(cudaMemsetAsync(grad_dev, 0, (size_t)t->s.V * t->s.d * sizeof(float), e->ctx->stream));
+        if (zero_grad)
+            RS_CUDA(cudaMemsetAsync(grad_dev, 0, rs::drafter_grad_layout(t->s).total * sizeof(float), e->ctx->stream));
         std::vector<rs::KdRef> refs;
         for (int i = 0; i < n; ++i) {
             if (req[i] < 0 || req[i] >= e->n) throw std::invalid_argument("kd: request index out of range");
@@ -835,7 +865,7 @@ int rs_kd_update_transformer(rs_ctx *ctx, const rs_model *target, const rs_model
             wmax = i == 0 ? w[i] : std::max(wmax, w[i]);
             distilled += static_cast<size_t>(std::max(0, buf[idx[i]].response_len));
         }
-        rs::DBuf<float> grad((size_t)t->s.V * t->s.d);
+        rs::DBuf<float> grad(rs::drafter_grad_layout(t->s).total);
         const double loss = rs::kd_grad_transformer(ctx, t, d, kd_seqs(buf, idx, w), grad.p, true);
         *new_drafter = rs::drafter_apply_lm_grad(ctx, d, grad.p, -policy.lr);
         res.updated = 1;

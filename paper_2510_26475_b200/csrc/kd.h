@@ -41,6 +41,24 @@ void kd_rows_elem(const float *P, const float *Q, const double *lseP, const doub
 void transpose_pad_bf16(const __nv_bfloat16 *in, int ldi, int R, int C, __nv_bfloat16 *out, int ldo, cudaStream_t st);
 void sgd_bf16(const __nv_bfloat16 *w, const float *g, float scale, size_t n, __nv_bfloat16 *out, cudaStream_t st);
 
+// Whole-drafter KD backward (kd_train.cu): element-wise / reduction pieces around the GEMMs.
+// rms_bwd: dx = base + dRMSNorm/dx . dy (base / dx / gterm optional), gterm = dy * x * r (the
+// per-row gain gradient terms); colsum_f32: out[c] (+)= sum over rows in a fixed order
+// (partial needs max_chunks * C floats); swiglu_bwd: pairwise-interleaved gate/up gradient;
+// rope_bwd: inverse rotation in place; softmax_bwd: causal rows, P and dS (times scale) in
+// bf16; cast_bf16: fp32 -> bf16 sub-matrix; sgd_f32: out = w + scale * g.
+void rms_bwd(const float *x, int ldx, const float *g, const float *dy, int lddy, int M, int d, float eps,
+             const float *base, int ldb, float *dx, int lddx, float *gterm, int ldg, cudaStream_t st);
+void colsum_f32(const float *in, int ld, int M, int C, float *out, bool accumulate, float *partial, int max_chunks,
+                cudaStream_t st);
+void swiglu_bwd(const __nv_bfloat16 *gu, int ldgu, const float *dh, int lddh, int M, int F, __nv_bfloat16 *dgu,
+                int lddgu, cudaStream_t st);
+void rope_bwd(float *x, int ldx, int M, int heads, int hd, const int *pos, const float *rope, cudaStream_t st);
+void softmax_bwd(const float *S, const float *dP, int lds, int T, float scale, __nv_bfloat16 *P, __nv_bfloat16 *dS,
+                 int ldo, cudaStream_t st);
+void cast_bf16(const float *in, int ldi, int M, int C, __nv_bfloat16 *out, int ldo, cudaStream_t st);
+void sgd_f32(const float *w, const float *g, float scale, size_t n, float *out, cudaStream_t st);
+
 // L2 norm of a bf16 weight tensor (fp64 accumulation, deterministic order) -- the learner's
 // LearnerMetrics::weights_l2 for transformer drafters (learner.cpp:268-272).
 double weights_l2_bf16(const __nv_bfloat16 *w, size_t n, cudaStream_t st);

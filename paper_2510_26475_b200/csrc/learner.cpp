@@ -112,7 +112,7 @@ struct rs_learner {
             distilled += (size_t)std::max(0, batch[idx[i]].response_len);
         }
         const auto *t = d->target;
-        rs::DBuf<float> grad((size_t)t->s.V * t->s.d);
+        rs::DBuf<float> grad(rs::drafter_grad_layout(t->s).total);
         RS_CUDA(cudaMemsetAsync(grad.p, 0, grad.bytes(), c->stream));
         double loss = 0.0;
         size_t i = 0;

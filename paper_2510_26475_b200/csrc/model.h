@@ -74,8 +74,18 @@ struct KdSeq {
 // Accumulates dL/dW_lm (fp32 [V][d]) into grad (zeroed first if zero_grad); returns the loss.
 double kd_grad_transformer(rs_ctx *ctx, const TransformerModel *tgt, const DrafterModel *drf,
                            const std::vector<KdSeq> &seqs, float *grad, bool zero_grad);
-// New drafter snapshot (version + 1): lm_w + scale * grad, every other tensor copied.
+// New drafter snapshot (version + 1): every tensor w + scale * grad (grad in the layout below).
 DrafterModel *drafter_apply_lm_grad(rs_ctx *ctx, const DrafterModel *drf, const float *grad, double scale);
+
+// The drafter gradient (fp32, one buffer): every trainable tensor of the EAGLE drafter, LM head
+// first (so a [V][d] prefix is the LM-head gradient), then fc, the two input-norm gains, the
+// decoder layer (QKV weight + bias, O, post-attention norm gain, gate/up, down) and the final
+// norm gain. The target's embedding (shared by the drafter's input) is frozen.
+struct DrafterGradLayout {
+    size_t lm = 0, fc = 0, norm_emb = 0, norm_hid = 0, qkv_w = 0, qkv_b = 0, o_w = 0, ln2 = 0, gu_w = 0, down_w = 0,
+           final_norm = 0, total = 0;
+};
+DrafterGradLayout drafter_grad_layout(const TfShape &s);
 
 // One query/update row of a forward pass.
 struct RowDesc {

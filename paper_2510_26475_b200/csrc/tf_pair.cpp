@@ -106,6 +106,24 @@ void gemm(const void *A, int lda, const void *B, int M, int N, int K, GemmEpi ep
     gemm_bf16(g, st);
 }
 
+// C[M, N] (+)= A[M, K] . B[N, K]^T with explicit leading dimensions (backward-pass GEMMs:
+// transposed activations as operands, K = rows of the training batch).
+void gemm_ld(const void *A, int lda, const void *B, int ldb, int M, int N, int K, GemmEpi epi, cudaStream_t st) {
+    GemmArgs g;
+    g.A = A;
+    g.B = B;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.lda = lda;
+    g.ldb = ldb;
+    g.epi = epi;
+    g.splits = 1;
+    gemm_bf16(g, st);
+}
+
+int round64(int x) { return (x + 63) / 64 * 64; }
+
 GemmEpi epi_bf16(void *out, int ldo, const void *bias = nullptr) {
     GemmEpi e;
     e.kind = kEpiBF16;
@@ -577,117 +595,386 @@ struct TransformerPair : ModelPair {
         k_compact(d, d.rsel, d.racc, rbase.p, kv_t, feat.p, 3 * s.d, max_ctx, st);
     }
 
-    // ---- transformer KD (K5 + LM-head gradient) over teacher-forced training sequences -------
-    // Rows = every position 0..len-2 of every sequence, in position order per sequence, packed
-    // into forwards of <= Mcap rows. Per forward: target stack (KV + EAGLE features; logits only
-    // for the KD rows = positions >= prompt_len - 1), drafter fc + layer over the same rows
-    // (features of position p-1, the drafter's own KV), drafter LM head on the KD rows, K5
-    // (loss, dZ^T), and dW_lm += dZ^T . h_norm on the tensor cores (fp32 accumulate).
+    // ---- whole-drafter KD (kd_update, learner.cpp:62-82 / :146-151) ---------------------------
+    // One training sequence = a request slot r of this pair's batch (tokens in d.tok row r) with
+    // prompt length plen and length len; its rows are positions 0..len-2, the KD rows (one per
+    // response token) positions plen-1..len-2: w * KL(p~ || q) of the next token's distribution.
+    struct KdTrainSeq {
+        int r, plen, len;
+        double w, bias;
+    };
+    // Activations of the teacher-forced drafter forward, one row per (sequence, position), kept
+    // for the backward pass; plus the backward's scratch. Grow-only (repeated updates allocate
+    // nothing).
+    struct TrainStore {
+        DBuf<bf16> fin, hc, q, ao, h2, hs, hf;  // [P][3d] [P][2d] [P][HD] [P][HD] [P][d] [P][dff] [P][d]
+        DBuf<float> f, x1, x2;                   // [P][d] fp32 residual stream
+        DBuf<float> dhf, dx2, dx1, gterm, wide;  // [P][d] x3, [P][2d], [P][max(dff, 2d, qd)]
+        DBuf<bf16> gu, dgu, nb, tA, tB;          // [P][2dff] x2, [P][max(d, HD, qd)], transposes
+        DBuf<float> partial;                     // column-sum partials
+        DBuf<bf16> WdT, WguT, WoT, WqkvT, lmT;   // transposed drafter weights
+        DBuf<float> S, dP;                       // attention backward, per (sequence, head)
+        DBuf<bf16> P, dS, PT, dST, KT, QT, dOT;
+        DBuf<int32_t> pos, rowmap;
+        DBuf<bf16> dz;                           // [Rp][V] dZ row-major
+    } trs;
+
+    // Teacher-forced drafter forward over M rows (in w.rows / w.items) whose first global row is
+    // o: the drafter_fc + drafter_layer + final-norm ops with every activation the backward pass
+    // needs written to the store (same kernels, same arithmetic as the drafting path).
+    void drafter_forward_train(const SdDev &d, int M, int ni, size_t o, cudaStream_t st) {
+        TrainStore &T = trs;
+        const int qd = s.qkv_dim(), HD = s.H * s.hd, d2 = 2 * s.d;
+        bf16 *fin = T.fin.p + o * 3 * s.d, *hc = T.hc.p + o * d2, *q = T.q.p + o * HD, *ao = T.ao.p + o * HD;
+        bf16 *h2 = T.h2.p + o * s.d, *hs = T.hs.p + o * s.dff, *hf = T.hf.p + o * s.d;
+        float *f = T.f.p + o * s.d, *x1 = T.x1.p + o * s.d, *x2 = T.x2.p + o * s.d;
+        k_gather_features(w.rows.p, M, s.d, feat.p, max_ctx, nullptr, fin, nullptr, st);
+        RS_CUDA(cudaMemsetAsync(f, 0, (size_t)M * s.d * sizeof(float), st));
+        gemm(fin, 3 * s.d, drf->fc_w, M, s.d, 3 * s.d, epi_resid(f, s.d), st, drafter_splits(3 * s.d));
+        k_embed(w.rows.p, M, d.tok, d.tok_cap, d.chain_tok, d.t_max, d.n_max, tgt->emb, s.V, s.d, w.e32.p, st);
+        k_rmsnorm(w.e32.p, s.d, drf->norm_emb, M, s.d, s.eps, hc, d2, st);
+        k_rmsnorm(f, s.d, drf->norm_hid, M, s.d, s.eps, hc + s.d, d2, st);
+        if (fused_qkv_rope(s)) {
+            gemm(hc, d2, drf->layer.qkv_w, M, qd, d2, epi_qkv_rope(q, drf->layer.qkv_b, w.rows.p, tgt->rope, kv_d, 0, s.H),
+                 st);
+        } else {
+            gemm(hc, d2, drf->layer.qkv_w, M, qd, d2, epi_bf16(w.qkv.p, qd, drf->layer.qkv_b), st);
+            k_rope_store(w.qkv.p, w.rows.p, M, drf->s, tgt->rope, kv_d, 0, q, st);
+        }
+        if (tc_attn)
+            k_attention_tc(q, w.rows.p, w.items.p, AttnPlan{w.passes.p, w.groups.p, w.tok_grp.p}, ni, kv_d, 0, drf->s, ao,
+                           st);
+        else k_attention(q, w.rows.p, w.items.p, ni, kv_d, 0, drf->s, ao, st);
+        RS_CUDA(cudaMemcpyAsync(x1, f, (size_t)M * s.d * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        gemm(ao, HD, drf->layer.o_w, M, s.d, HD, epi_resid(x1, s.d), st, drafter_splits(HD));
+        k_rmsnorm(x1, s.d, drf->layer.ln2, M, s.d, s.eps, h2, s.d, st);
+        gemm(h2, s.d, drf->layer.gu_w, M, 2 * s.dff, s.d, epi_swiglu(hs, s.dff), st);
+        RS_CUDA(cudaMemcpyAsync(x2, x1, (size_t)M * s.d * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        gemm(hs, s.dff, drf->layer.down_w, M, s.d, s.dff, epi_resid(x2, s.d), st, drafter_splits(s.dff));
+        k_rmsnorm(x2, s.d, drf->final_norm, M, s.d, s.eps, hf, s.d, st);
+    }
+
+    // Whole-drafter KD over `seqs`: (1) the drafter forward over every row, teacher-forced from
+    // the target's EAGLE features (which must already be in `feat`, with the target KV cache
+    // holding every row's keys); (2) per group of <= Mcap KD rows: target logits (P), drafter
+    // logits from the stored final-norm rows (Q), K5 (loss, dZ), dW_lm += dZ^T h and dh_final =
+    // dZ W_lm; (3) the backward pass of the drafter layer, fc and norms over every row, the
+    // causal attention backward per (sequence, head) on the tensor cores. Accumulates into
+    // `grad` (drafter_grad_layout); returns sum_rows w KL.
+    double kd_train(const SdDev &d, const std::vector<KdTrainSeq> &seqs, float *grad, int Mcap, cudaStream_t st) {
+        TrainStore &T = trs;
+        const int V = s.V, qd = s.qkv_dim(), HD = s.H * s.hd, d2 = 2 * s.d, G = s.H / s.KV, hd = s.hd;
+        const DrafterGradLayout gl = drafter_grad_layout(s);
+        std::vector<size_t> row0(seqs.size());
+        size_t P = 0;
+        long long nkd = 0;
+        int Tmax = 1;
+        for (size_t j = 0; j < seqs.size(); ++j) {
+            row0[j] = P;
+            P += (size_t)std::max(0, seqs[j].len - 1);
+            nkd += std::max(0, seqs[j].len - seqs[j].plen);
+            Tmax = std::max(Tmax, seqs[j].len - 1);
+        }
+        if (P == 0 || nkd == 0) return 0.0;
+        const int Pp = round64((int)P), Tp = round64(Tmax);
+        const int Rcap = (int)std::max<long long>(1, std::min<long long>(Mcap, nkd)), Rp = round64(Rcap);
+        const int nt = (V + 255) / 256;
+        const int wide = std::max({s.dff, d2, qd});
+        const int nbw = std::max({s.d, HD, qd});
+        const size_t tcols = (size_t)std::max({2 * s.dff, 3 * s.d, qd, HD}) * Pp;
+        T.fin.ensure(P * 3 * s.d);
+        T.hc.ensure(P * d2);
+        T.q.ensure(P * HD);
+        T.ao.ensure(P * HD);
+        T.h2.ensure(P * s.d);
+        T.hs.ensure(P * s.dff);
+        T.hf.ensure(P * s.d);
+        for (DBuf<float> *b : {&T.f, &T.x1, &T.x2, &T.dhf, &T.dx2, &T.dx1}) b->ensure(P * s.d);
+        T.gterm.ensure(P * d2);
+        T.wide.ensure(P * wide);
+        T.gu.ensure(P * 2 * s.dff);
+        T.dgu.ensure(P * 2 * s.dff);
+        T.nb.ensure(P * nbw);
+        T.tA.ensure(tcols);
+        T.tB.ensure(tcols);
+        T.partial.ensure((size_t)64 * std::max(qd, d2));
+        T.WdT.ensure((size_t)s.dff * s.d);
+        T.WguT.ensure((size_t)s.d * 2 * s.dff);
+        T.WoT.ensure((size_t)HD * s.d);
+        T.WqkvT.ensure((size_t)d2 * qd);
+        T.lmT.ensure((size_t)s.d * V);
+        T.S.ensure((size_t)Tmax * Tp);
+        T.dP.ensure((size_t)Tmax * Tp);
+        for (DBuf<bf16> *b : {&T.P, &T.dS, &T.PT, &T.dST}) b->ensure((size_t)Tmax * Tp);
+        for (DBuf<bf16> *b : {&T.KT, &T.QT, &T.dOT}) b->ensure((size_t)hd * Tp);
+        T.pos.ensure(P);
+        T.rowmap.ensure(Rcap);
+        T.dz.ensure((size_t)Rp * V);
+        KdScratch &k = kd_scr;
+        k.Pb.ensure((size_t)Rcap * V);
+        k.Qb.ensure((size_t)Rcap * V);
+        k.stP.ensure((size_t)Rcap * nt * 2);
+        k.stQ.ensure((size_t)Rcap * nt * 2);
+        k.kl.ensure((size_t)Rcap * nt);
+        for (DBuf<double> *b : {&k.lseP, &k.lseQ, &k.lossr, &k.wr, &k.br}) b->ensure(Rcap);
+        k.dzT.ensure((size_t)V * Rp);
+        k.hT.ensure((size_t)s.d * Rp);
+        k.hG.ensure((size_t)Rcap * s.d);
+
+        // ---- (1) drafter forward over every row, chunks of <= Mcap rows ----
+        prof_set_scope("kd_drafter");
+        {
+            size_t j = 0;
+            int p = 0;
+            size_t o = 0;
+            while (j < seqs.size()) {
+                bt.clear();
+                while (j < seqs.size() && bt.M() < Mcap) {
+                    const int last = seqs[j].len - 2;
+                    if (p > last) {
+                        ++j;
+                        p = 0;
+                        continue;
+                    }
+                    const int take = std::min(last - p + 1, Mcap - bt.M());
+                    const int r0 = bt.M();
+                    for (int q = 0; q < take; ++q, ++p) bt.rows.push_back(RowDesc{seqs[j].r, p, p, 0, -1, 0, 0, 0});
+                    bt.add_items(r0, bt.M(), per_item_t, -1, 0, 0, 0);
+                }
+                const int M = bt.M();
+                if (M == 0) break;
+                upload(bt, st, tc_attn);
+                drafter_forward_train(d, M, (int)bt.items.size(), o, st);
+                o += (size_t)M;
+                RS_CUDA(cudaStreamSynchronize(st));
+                stage.off = 0;
+            }
+        }
+        std::vector<int32_t> hpos(P);
+        for (size_t j = 0; j < seqs.size(); ++j)
+            for (int p = 0; p < seqs[j].len - 1; ++p) hpos[row0[j] + p] = p;
+        stage.upload(T.pos.p, hpos, st);
+
+        // weights transposed once per update (the input-gradient GEMMs take W^T as operand)
+        transpose_pad_bf16(drf->lm_w, s.d, V, s.d, T.lmT.p, V, st);
+        transpose_pad_bf16(drf->layer.down_w, s.dff, s.d, s.dff, T.WdT.p, s.d, st);
+        transpose_pad_bf16(drf->layer.gu_w, s.d, 2 * s.dff, s.d, T.WguT.p, 2 * s.dff, st);
+        transpose_pad_bf16(drf->layer.o_w, HD, s.d, HD, T.WoT.p, s.d, st);
+        transpose_pad_bf16(drf->layer.qkv_w, d2, qd, d2, T.WqkvT.p, qd, st);
+        RS_CUDA(cudaMemsetAsync(T.dhf.p, 0, P * s.d * sizeof(float), st));
+
+        // ---- (2) K5 per group of KD rows ----
+        double loss = 0.0;
+        std::vector<double> lh(Rcap);
+        size_t j = 0;
+        int p = seqs.empty() ? 0 : seqs[0].plen - 1;
+        while (j < seqs.size()) {
+            struct Run {
+                size_t grow;  // first global row
+                int n, k0;    // rows, first group row
+            };
+            std::vector<Run> runs;
+            std::vector<double> kd_w, kd_b;
+            std::vector<int32_t> gmap;
+            bt.clear();
+            while (j < seqs.size() && bt.M() < Mcap) {
+                const int last = seqs[j].len - 2;
+                if (p > last) {
+                    if (++j < seqs.size()) p = seqs[j].plen - 1;
+                    continue;
+                }
+                const int take = std::min(last - p + 1, Mcap - bt.M());
+                const int r0 = bt.M();
+                runs.push_back(Run{row0[j] + (size_t)p, take, r0});
+                for (int q = 0; q < take; ++q, ++p) {
+                    bt.rows.push_back(RowDesc{seqs[j].r, p, p, 0, -1, 0, 0, 0});
+                    kd_w.push_back(seqs[j].w);
+                    kd_b.push_back(seqs[j].bias);
+                    gmap.push_back((int32_t)(row0[j] + (size_t)p));
+                }
+                bt.add_items(r0, bt.M(), per_item_t, -1, 0, 0, 0);
+            }
+            const int R = bt.M();
+            if (R == 0) break;
+            prof_set_scope("kd_target");
+            upload(bt, st, tc_attn);
+            target_forward(d, R, (int)bt.items.size(), k.Pb.p, false, st);
+            prof_set_scope("kd_k5");
+            for (const Run &u : runs) {  // drafter logits and the final-norm rows of the group
+                gemm(T.hf.p + u.grow * s.d, s.d, drf->lm_w, u.n, V, s.d,
+                     epi_f32(k.Qb.p + (size_t)u.k0 * V, V, s.logit_scale, nullptr), st);
+                RS_CUDA(cudaMemcpyAsync(k.hG.p + (size_t)u.k0 * s.d, T.hf.p + u.grow * s.d, (size_t)u.n * s.d * sizeof(bf16),
+                                        cudaMemcpyDeviceToDevice, st));
+            }
+            stage.upload(k.wr.p, kd_w, st);
+            stage.upload(k.br.p, kd_b, st);
+            stage.upload(T.rowmap.p, gmap, st);
+            row_stats(k.Pb.p, nullptr, R, V, tgt->temperature, k.stP.p, st);
+            row_stats(k.Qb.p, nullptr, R, V, drf->temperature, k.stQ.p, st);
+            kd_rows_lse(k.Pb.p, k.stP.p, R, V, tgt->temperature, k.br.p, k.lseP.p, st);
+            kd_rows_lse(k.Qb.p, k.stQ.p, R, V, drf->temperature, k.br.p, k.lseQ.p, st);
+            const int Rq = round64(R);
+            kd_rows_elem(k.Pb.p, k.Qb.p, k.lseP.p, k.lseQ.p, k.wr.p, k.br.p, R, V, tgt->temperature, drf->temperature,
+                         s.logit_scale, k.dzT.p, Rq, k.kl.p, k.lossr.p, st);
+            prof_set_scope("kd_grad");
+            transpose_pad_bf16(k.hG.p, s.d, R, s.d, k.hT.p, Rq, st);
+            // dW_lm[V][d] += dZ^T[V][Rq] . (h^T[d][Rq])^T
+            gemm_ld(k.dzT.p, Rq, k.hT.p, Rq, V, s.d, Rq, epi_resid(grad + gl.lm, s.d), st);
+            // dh_final[row] = dZ[row] . W_lm  (dZ row-major from dZ^T; W_lm^T as the operand)
+            transpose_pad_bf16(k.dzT.p, Rq, V, R, T.dz.p, V, st);
+            gemm_ld(T.dz.p, V, T.lmT.p, V, R, s.d, V, epi_f32(T.dhf.p, s.d, 1.0f, T.rowmap.p), st);
+            RS_CUDA(cudaMemcpyAsync(lh.data(), k.lossr.p, (size_t)R * 8, cudaMemcpyDeviceToHost, st));
+            RS_CUDA(cudaStreamSynchronize(st));
+            for (int q = 0; q < R; ++q) loss += lh[q];
+            stage.off = 0;
+        }
+
+        // ---- (3) backward over every row ----
+        prof_set_scope("kd_backward");
+        const int Pi = (int)P;
+        float *dqkv = T.wide.p;  // [P][qd] fp32 (reused below: dhs [P][dff], dh [P][2d])
+        // final norm: dx2 = dRMS(x2) . dh_final; d final_norm
+        rms_bwd(T.x2.p, s.d, drf->final_norm, T.dhf.p, s.d, Pi, s.d, s.eps, nullptr, 0, T.dx2.p, s.d, T.gterm.p, s.d,
+                st);
+        colsum_f32(T.gterm.p, s.d, Pi, s.d, grad + gl.final_norm, true, T.partial.p, 64, st);
+        // down projection: dhs = dx2 . W_d, dW_d += dx2^T hs
+        cast_bf16(T.dx2.p, s.d, Pi, s.d, T.nb.p, s.d, st);
+        gemm_ld(T.nb.p, s.d, T.WdT.p, s.d, Pi, s.dff, s.d, epi_f32(T.wide.p, s.dff, 1.0f, nullptr), st);
+        transpose_pad_bf16(T.nb.p, s.d, Pi, s.d, T.tA.p, Pp, st);
+        transpose_pad_bf16(T.hs.p, s.dff, Pi, s.dff, T.tB.p, Pp, st);
+        gemm_ld(T.tA.p, Pp, T.tB.p, Pp, s.d, s.dff, Pp, epi_resid(grad + gl.down_w, s.dff), st);
+        // SwiGLU: recompute gate/up, dgu
+        gemm(T.h2.p, s.d, drf->layer.gu_w, Pi, 2 * s.dff, s.d, epi_bf16(T.gu.p, 2 * s.dff), st);
+        swiglu_bwd(T.gu.p, 2 * s.dff, T.wide.p, s.dff, Pi, s.dff, T.dgu.p, 2 * s.dff, st);
+        // gate/up projection: dh2 = dgu . W_gu, dW_gu += dgu^T h2
+        gemm_ld(T.dgu.p, 2 * s.dff, T.WguT.p, 2 * s.dff, Pi, s.d, 2 * s.dff, epi_f32(T.wide.p, s.d, 1.0f, nullptr), st);
+        transpose_pad_bf16(T.dgu.p, 2 * s.dff, Pi, 2 * s.dff, T.tA.p, Pp, st);
+        transpose_pad_bf16(T.h2.p, s.d, Pi, s.d, T.tB.p, Pp, st);
+        gemm_ld(T.tA.p, Pp, T.tB.p, Pp, 2 * s.dff, s.d, Pp, epi_resid(grad + gl.gu_w, s.d), st);
+        // post-attention norm: dx1 = dx2 + dRMS(x1) . dh2; d ln2
+        rms_bwd(T.x1.p, s.d, drf->layer.ln2, T.wide.p, s.d, Pi, s.d, s.eps, T.dx2.p, s.d, T.dx1.p, s.d, T.gterm.p, s.d,
+                st);
+        colsum_f32(T.gterm.p, s.d, Pi, s.d, grad + gl.ln2, true, T.partial.p, 64, st);
+        // O projection: da = dx1 . W_o (bf16, the attention backward's dO), dW_o += dx1^T ao
+        cast_bf16(T.dx1.p, s.d, Pi, s.d, T.nb.p, s.d, st);
+        transpose_pad_bf16(T.nb.p, s.d, Pi, s.d, T.tA.p, Pp, st);
+        transpose_pad_bf16(T.ao.p, HD, Pi, HD, T.tB.p, Pp, st);
+        gemm_ld(T.tA.p, Pp, T.tB.p, Pp, s.d, HD, Pp, epi_resid(grad + gl.o_w, HD), st);
+        bf16 *da = T.gu.p;  // gate/up no longer needed: [P][HD] bf16
+        gemm_ld(T.nb.p, s.d, T.WoT.p, s.d, Pi, HD, s.d, epi_bf16(da, HD), st);
+        // attention backward per (sequence, query head): S = Q K^T, dP = dO V^T, softmax
+        // backward, dV += P^T dO, dK += dS^T Q, dQ = dS K (K / V post-RoPE from the private
+        // drafter cache; GQA heads of one kv head accumulate in head order)
+        RS_CUDA(cudaMemsetAsync(dqkv, 0, P * qd * sizeof(float), st));
+        const float scale = 1.0f / sqrtf((float)hd);
+        for (size_t jj = 0; jj < seqs.size(); ++jj) {
+            const int Tn = seqs[jj].len - 1;
+            if (Tn <= 0) continue;
+            const int Tq = round64(Tn);
+            const size_t g0 = row0[jj];
+            for (int h = 0; h < s.H; ++h) {
+                const int g = h / G;
+                const bf16 *Kg = kv_d.k + kv_d.off(0, seqs[jj].r, g, 0), *Vg = kv_d.v + kv_d.off(0, seqs[jj].r, g, 0);
+                const bf16 *Qh = T.q.p + g0 * HD + (size_t)h * hd, *dOh = da + g0 * HD + (size_t)h * hd;
+                if (h % G == 0) transpose_pad_bf16(Kg, hd, Tn, hd, T.KT.p, Tq, st);
+                gemm_ld(Qh, HD, Kg, hd, Tn, Tn, hd, epi_f32(T.S.p, Tq, 1.0f, nullptr), st);
+                gemm_ld(dOh, HD, Vg, hd, Tn, Tn, hd, epi_f32(T.dP.p, Tq, 1.0f, nullptr), st);
+                softmax_bwd(T.S.p, T.dP.p, Tq, Tn, scale, T.P.p, T.dS.p, Tq, st);
+                transpose_pad_bf16(T.P.p, Tq, Tn, Tn, T.PT.p, Tq, st);
+                transpose_pad_bf16(T.dS.p, Tq, Tn, Tn, T.dST.p, Tq, st);
+                transpose_pad_bf16(dOh, HD, Tn, hd, T.dOT.p, Tq, st);
+                transpose_pad_bf16(Qh, HD, Tn, hd, T.QT.p, Tq, st);
+                float *rowq = dqkv + g0 * qd;
+                gemm_ld(T.PT.p, Tq, T.dOT.p, Tq, Tn, hd, Tq, epi_resid(rowq + HD + s.KV * hd + g * hd, qd), st);
+                gemm_ld(T.dST.p, Tq, T.QT.p, Tq, Tn, hd, Tq, epi_resid(rowq + HD + g * hd, qd), st);
+                gemm_ld(T.dS.p, Tq, T.KT.p, Tq, Tn, hd, Tq, epi_f32(rowq + h * hd, qd, 1.0f, nullptr), st);
+            }
+        }
+        // RoPE backward on dq, dk; QKV bias; dh = dqkv . W_qkv; dW_qkv += dqkv^T h
+        rope_bwd(dqkv, qd, Pi, s.H, hd, T.pos.p, tgt->rope, st);
+        rope_bwd(dqkv + HD, qd, Pi, s.KV, hd, T.pos.p, tgt->rope, st);
+        colsum_f32(dqkv, qd, Pi, qd, grad + gl.qkv_b, true, T.partial.p, 64, st);
+        cast_bf16(dqkv, qd, Pi, qd, T.nb.p, qd, st);
+        transpose_pad_bf16(T.nb.p, qd, Pi, qd, T.tA.p, Pp, st);
+        transpose_pad_bf16(T.hc.p, d2, Pi, d2, T.tB.p, Pp, st);
+        gemm_ld(T.tA.p, Pp, T.tB.p, Pp, qd, d2, Pp, epi_resid(grad + gl.qkv_w, d2), st);
+        float *dh = T.wide.p;  // [P][2d] (dqkv consumed)
+        gemm_ld(T.nb.p, qd, T.WqkvT.p, qd, Pi, d2, qd, epi_f32(dh, d2, 1.0f, nullptr), st);
+        // input norms: d norm_emb (the embedding itself is the target's, frozen); df = dx1 +
+        // dRMS(f) . dh[:, d:], d norm_hid
+        {
+            // embedding rows again (fp32), per chunk of <= Mcap rows into the workspace
+            for (size_t jj = 0, o = 0; jj < seqs.size(); ++jj) {
+                for (int p0 = 0; p0 < seqs[jj].len - 1;) {
+                    const int n = std::min(seqs[jj].len - 1 - p0, w.Mcap);
+                    bt.clear();
+                    for (int q = 0; q < n; ++q) bt.rows.push_back(RowDesc{seqs[jj].r, p0 + q, p0 + q, 0, -1, 0, 0, 0});
+                    stage.upload(w.rows.p, bt.rows, st);
+                    k_embed(w.rows.p, n, d.tok, d.tok_cap, d.chain_tok, d.t_max, d.n_max, tgt->emb, s.V, s.d, w.e32.p, st);
+                    rms_bwd(w.e32.p, s.d, drf->norm_emb, dh + o * d2, d2, n, s.d, s.eps, nullptr, 0, nullptr, 0,
+                            T.gterm.p + o * s.d, s.d, st);
+                    RS_CUDA(cudaStreamSynchronize(st));
+                    stage.off = 0;
+                    o += (size_t)n;
+                    p0 += n;
+                }
+            }
+            colsum_f32(T.gterm.p, s.d, Pi, s.d, grad + gl.norm_emb, true, T.partial.p, 64, st);
+        }
+        rms_bwd(T.f.p, s.d, drf->norm_hid, dh + s.d, d2, Pi, s.d, s.eps, T.dx1.p, s.d, T.dx2.p, s.d, T.gterm.p, s.d, st);
+        colsum_f32(T.gterm.p, s.d, Pi, s.d, grad + gl.norm_hid, true, T.partial.p, 64, st);
+        // fc: dW_fc += df^T fin (df in dx2)
+        cast_bf16(T.dx2.p, s.d, Pi, s.d, T.nb.p, s.d, st);
+        transpose_pad_bf16(T.nb.p, s.d, Pi, s.d, T.tA.p, Pp, st);
+        transpose_pad_bf16(T.fin.p, 3 * s.d, Pi, 3 * s.d, T.tB.p, Pp, st);
+        gemm_ld(T.tA.p, Pp, T.tB.p, Pp, s.d, 3 * s.d, Pp, epi_resid(grad + gl.fc, 3 * s.d), st);
+        RS_CUDA(cudaStreamSynchronize(st));
+        stage.off = 0;
+        return loss;
+    }
+
+    // kd_pass: detached training sequences (tokens uploaded into d.tok, one batch slot each);
+    // the target runs teacher-forced over every row first (its KV cache and EAGLE features),
+    // then kd_train.
     double kd_pass(const SdDev &d, const std::vector<KdSeq> &seqs, float *grad) {
         cudaStream_t st = ctx->stream;
-        const int V = s.V, Mcap = w.Mcap;
-        long long need = 0;  // KD rows in total (one per response token)
-        for (const auto &q : seqs) need += std::max(0, (int)q.tokens.size() - q.prompt_len);
-        const int Rcap = (int)std::max<long long>(1, std::min<long long>(Mcap, need));
-        const int ldt = (Rcap + 63) / 64 * 64;
-        const int nt = (V + 255) / 256;
-        DBuf<float> Pb((size_t)Rcap * V), Qb((size_t)Rcap * V);
-        DBuf<double> stP((size_t)Rcap * nt * 2), stQ((size_t)Rcap * nt * 2), lseP(Rcap), lseQ(Rcap), kl((size_t)Rcap * nt),
-            lossr(Rcap), wr(Rcap), br(Rcap);
-        DBuf<bf16> dzT((size_t)V * ldt), hT((size_t)s.d * ldt);
-        std::vector<double> lh(Rcap);
-        double loss = 0.0;
+        prof_set_scope("kd_target");
         size_t r = 0;
         int p = 0;
         while (r < seqs.size()) {
             bt.clear();
-            std::vector<int32_t> kd_src;
-            std::vector<double> kd_w, kd_b;
-            std::vector<std::pair<int, int>> segs;  // (first row, end row) per sequence run
-            while (r < seqs.size() && bt.M() < Mcap) {
+            while (r < seqs.size() && bt.M() < w.Mcap) {
                 const int len = (int)seqs[r].tokens.size();
                 if (p >= len - 1) {
                     ++r;
                     p = 0;
                     continue;
                 }
-                const int take = std::min(len - 1 - p, Mcap - bt.M());
+                const int take = std::min(len - 1 - p, w.Mcap - bt.M());
                 const int r0 = bt.M();
-                for (int k = 0; k < take; ++k, ++p) {
-                    const bool kd = p >= seqs[r].prompt_len - 1;
-                    bt.map_a.push_back(kd ? (int32_t)kd_src.size() : -1);
-                    if (kd) {
-                        kd_src.push_back(bt.M());
-                        kd_w.push_back(seqs[r].weight);
-                        kd_b.push_back(seqs[r].eos_bias);
-                    }
-                    bt.rows.push_back(RowDesc{(int)r, p, p, 0, -1, 0, 0, 0});
-                }
-                segs.emplace_back(r0, bt.M());
+                for (int k = 0; k < take; ++k, ++p) bt.rows.push_back(RowDesc{(int)r, p, p, 0, -1, 0, 0, 0});
+                bt.add_items(r0, bt.M(), per_item_t, -1, 0, 0, 0);
             }
             if (bt.M() == 0) break;
-            const int M = bt.M(), R = (int)kd_src.size();
-            // target: tensor-core attention items
-            for (const auto &sg : segs) bt.add_items(sg.first, sg.second, per_item_t, -1, 0, 0, 0);
             upload(bt, st, tc_attn);
-            prof_set_scope("kd_target");
-            target_forward(d, M, (int)bt.items.size(), Pb.p, true, st);
-            prof_set_scope("kd_drafter");
-            // drafter: the same attention items over the same rows
-            bt.items.clear();
-            for (const auto &sg : segs) bt.add_items(sg.first, sg.second, per_item_t, -1, 0, 0, 0);
-            std::vector<int32_t> dst(R);
-            for (int k = 0; k < R; ++k) dst[k] = k;
-            bt.map_a = kd_src;
-            bt.map_b = dst;
-            upload(bt, st, tc_attn);
-            k_gather_features(w.rows.p, M, s.d, feat.p, max_ctx, nullptr, w.fin.p, nullptr, st);
-            drafter_fc(M, st);
-            drafter_layer(d, M, (int)bt.items.size(), st);
-            if (R == 0) continue;
-            drafter_head(w.map_a.p, w.map_b.p, R, Qb.p, nullptr, st);  // h_norm of the KD rows stays in w.xn
-            stage.upload(wr.p, kd_w, st);
-            stage.upload(br.p, kd_b, st);
-            prof_set_scope("kd_k5");
-            row_stats(Pb.p, nullptr, R, V, tgt->temperature, stP.p, st);
-            row_stats(Qb.p, nullptr, R, V, drf->temperature, stQ.p, st);
-            kd_rows_lse(Pb.p, stP.p, R, V, tgt->temperature, br.p, lseP.p, st);
-            kd_rows_lse(Qb.p, stQ.p, R, V, drf->temperature, br.p, lseQ.p, st);
-            const int Rp = (R + 63) / 64 * 64;
-            kd_rows_elem(Pb.p, Qb.p, lseP.p, lseQ.p, wr.p, br.p, R, V, tgt->temperature, drf->temperature,
-                         s.logit_scale, dzT.p, Rp, kl.p, lossr.p, st);
-            prof_set_scope("kd_grad");
-            transpose_pad_bf16(w.xn.p, s.d, R, s.d, hT.p, Rp, st);
-            GemmArgs g;  // dW[V][d] += dZ^T[V][Rp] . (h^T[d][Rp])^T
-            g.A = dzT.p;
-            g.B = hT.p;
-            g.M = V;
-            g.N = s.d;
-            g.K = Rp;
-            g.lda = Rp;
-            g.ldb = Rp;
-            g.epi.kind = kEpiResidual;
-            g.epi.out = grad;
-            g.epi.ldo = s.d;
-            gemm_bf16(g, st);
-            RS_CUDA(cudaMemcpyAsync(lh.data(), lossr.p, (size_t)R * 8, cudaMemcpyDeviceToHost, st));
+            target_forward(d, bt.M(), (int)bt.items.size(), nullptr, false, st);
             RS_CUDA(cudaStreamSynchronize(st));
-            for (int k = 0; k < R; ++k) loss += lh[k];
             stage.off = 0;
         }
-        return loss;
+        std::vector<KdTrainSeq> ts;
+        for (size_t i = 0; i < seqs.size(); ++i)
+            ts.push_back(KdTrainSeq{(int)i, seqs[i].prompt_len, (int)seqs[i].tokens.size(), seqs[i].weight,
+                                    seqs[i].eos_bias});
+        return kd_train(d, ts, grad, w.Mcap, st);
     }
 
-    // K5 + LM-head gradient from the engine's RESIDENT state instead of a teacher-forced
-    // recompute of prompt + response: the target runs only over the response positions
-    // [plen - 1, len - 2] of each selected request (its prompt keys are already in kv_t from the
-    // prefill; the response keys are rewritten bit-identically by the rows themselves -- every
-    // kernel on the path is row-invariant), storing their EAGLE features next to the prompt's.
-    // The drafter (the given snapshot, not the engine's) then runs teacher-forced over every
-    // position from those features into a private drafter KV cache, so the engine's own drafter
-    // state is untouched. Rows are grouped so a group holds <= Mcap KD rows; the drafter
-    // advances through each request only as far as the group needs. Same loss / gradient as
-    // kd_pass on the same sequences.
+    // KD from the engine's RESIDENT state instead of a teacher-forced recompute of prompt +
+    // response: the target KV cache already holds every position 0..len-2 of each request and
+    // `feat` its EAGLE features (prefill, verify forwards, K4 compaction); the target re-runs
+    // only over the KD rows for their logits (rewriting their keys bit-identically -- every
+    // kernel on the path is row-invariant). The drafter (the given snapshot, not the engine's)
+    // runs teacher-forced into a private drafter KV cache, so the engine's own drafter state is
+    // untouched. Same loss / gradient as kd_pass on the same sequences.
     double kd_cached(const std::vector<KdRef> &refs, const rs_model *m, float *grad,
                      cudaStream_t on = nullptr) override {
         if (!m || m->kind != rs_model::Drafter) throw std::invalid_argument("kd: EAGLE drafter required");
@@ -701,33 +988,13 @@ struct TransformerPair : ModelPair {
         d.t_max = 1;
         d.n_max = 1;
         cudaStream_t st = on ? on : ctx->stream;
-        const int V = s.V;
         const int Mcap = tuning().kd_rows > 0 ? std::min(w.Mcap, tuning().kd_rows) : w.Mcap;
-        long long need = 0;  // KD rows in total: every generated token of every selected request
-        for (const auto &x : refs) need += std::max(0, eng->len[x.req] - eng->prompt_len[x.req]);
-        const int Rcap = (int)std::max<long long>(1, std::min<long long>(Mcap, need));
-        const int ldt = (Rcap + 63) / 64 * 64;
-        const int nt = (V + 255) / 256;
-        // scratch kept on the engine (grow-only): repeated updates allocate nothing
         KdScratch &k = kd_scr;
-        k.Pb.ensure((size_t)Rcap * V);
-        k.Qb.ensure((size_t)Rcap * V);
-        k.stP.ensure((size_t)Rcap * nt * 2);
-        k.stQ.ensure((size_t)Rcap * nt * 2);
-        k.kl.ensure((size_t)Rcap * nt);
-        for (DBuf<double> *b : {&k.lseP, &k.lseQ, &k.lossr, &k.wr, &k.br}) b->ensure(Rcap);
-        k.dzT.ensure((size_t)V * ldt);
-        k.hT.ensure((size_t)s.d * ldt);
-        k.hG.ensure((size_t)Rcap * s.d);
         const size_t kvd = (size_t)B * s.KV * max_ctx * s.hd;
         k.tk.ensure(kvd);
         k.tv.ensure(kvd);
         RS_CUDA(cudaMemsetAsync(k.tk.p, 0, kvd * sizeof(bf16), st));
         RS_CUDA(cudaMemsetAsync(k.tv.p, 0, kvd * sizeof(bf16), st));
-        DBuf<float> &Pb = k.Pb, &Qb = k.Qb;
-        DBuf<double> &stP = k.stP, &stQ = k.stQ, &lseP = k.lseP, &lseQ = k.lseQ, &kl = k.kl, &lossr = k.lossr, &wr = k.wr,
-                     &br = k.br;
-        DBuf<bf16> &dzT = k.dzT, &hT = k.hT, &hG = k.hG, &tk = k.tk, &tv = k.tv;
         struct Swap {  // private drafter cache + the KD snapshot for the duration of the pass
             TransformerPair &t;
             KvCache kv;
@@ -737,117 +1004,12 @@ struct TransformerPair : ModelPair {
                 t.drf = m;
             }
         } swap{*this, kv_d, drf};
-        kv_d = KvCache{tk.p, tv.p, 1, B, s.KV, max_ctx, s.hd};
+        kv_d = KvCache{k.tk.p, k.tv.p, 1, B, s.KV, max_ctx, s.hd};
         drf = kd_drf;
-        std::vector<int> dp(refs.size(), 0);  // drafter positions computed per selected request
-        std::vector<double> lh(Rcap);
-        double loss = 0.0;
-        size_t i = 0;
-        int p = refs.empty() ? 0 : eng->prompt_len[refs[0].req] - 1;
-        while (i < refs.size()) {
-            // ---- one group of <= Mcap KD rows: (request i, positions [first, last]) spans ----
-            struct Span {
-                size_t i;
-                int first, last, kd0;
-            };
-            std::vector<Span> spans;
-            std::vector<double> kd_w, kd_b;
-            bt.clear();
-            while (i < refs.size() && bt.M() < Mcap) {
-                const int r = refs[i].req, last = eng->len[r] - 2;
-                if (p > last) {
-                    if (++i < refs.size()) p = eng->prompt_len[refs[i].req] - 1;
-                    continue;
-                }
-                const int take = std::min(last - p + 1, Mcap - bt.M());
-                const int r0 = bt.M();
-                spans.push_back(Span{i, p, p + take - 1, r0});
-                for (int k = 0; k < take; ++k, ++p) {
-                    bt.rows.push_back(RowDesc{r, p, p, 0, -1, 0, 0, 0});
-                    kd_w.push_back(refs[i].weight);
-                    kd_b.push_back(refs[i].eos_bias);
-                }
-                bt.add_items(r0, bt.M(), per_item_t, -1, 0, 0, 0);
-            }
-            const int R = bt.M();
-            if (R == 0) break;
-            prof_set_scope("kd_target");
-            upload(bt, st, tc_attn);
-            target_forward(d, R, (int)bt.items.size(), Pb.p, false, st);
-            // ---- drafter: teacher-forced from dp[i] through each span's last position ----
-            prof_set_scope("kd_drafter");
-            size_t sp = 0;
-            while (sp < spans.size()) {
-                bt.clear();
-                std::vector<int32_t> src;
-                int dst0 = -1;
-                for (; sp < spans.size(); ++sp) {
-                    const Span &sn = spans[sp];
-                    const int r = refs[sn.i].req;
-                    const int from = dp[sn.i];
-                    if (from > sn.last) continue;
-                    const int room = Mcap - bt.M();
-                    if (room <= 0) break;
-                    const int upto = std::min(sn.last, from + room - 1);
-                    const int r0 = bt.M();
-                    for (int q = from; q <= upto; ++q) {
-                        if (q >= sn.first) {
-                            if (dst0 < 0) dst0 = sn.kd0 + (q - sn.first);
-                            src.push_back(bt.M());
-                        }
-                        bt.rows.push_back(RowDesc{r, q, q, 0, -1, 0, 0, 0});
-                    }
-                    bt.add_items(r0, bt.M(), per_item_t, -1, 0, 0, 0);
-                    dp[sn.i] = upto + 1;
-                    if (upto < sn.last) break;  // chunk full mid-span: resume this span next chunk
-                }
-                const int M = bt.M();
-                if (M == 0) break;
-                const int n = (int)src.size();
-                std::vector<int32_t> dst(n);
-                for (int k = 0; k < n; ++k) dst[k] = dst0 + k;
-                bt.map_a = src;
-                bt.map_b = dst;
-                upload(bt, st, tc_attn);
-                k_gather_features(w.rows.p, M, s.d, feat.p, max_ctx, nullptr, w.fin.p, nullptr, st);
-                drafter_fc(M, st);
-                drafter_layer(d, M, (int)bt.items.size(), st);
-                if (n == 0) continue;
-                drafter_head(w.map_a.p, w.map_b.p, n, Qb.p, nullptr, st);
-                RS_CUDA(cudaMemcpyAsync(hG.p + (size_t)dst0 * s.d, w.xn.p, (size_t)n * s.d * sizeof(bf16),
-                                        cudaMemcpyDeviceToDevice, st));
-            }
-            // ---- K5 + dW_lm over the group's R rows ----
-            prof_set_scope("kd_k5");
-            stage.upload(wr.p, kd_w, st);
-            stage.upload(br.p, kd_b, st);
-            row_stats(Pb.p, nullptr, R, V, tgt->temperature, stP.p, st);
-            row_stats(Qb.p, nullptr, R, V, drf->temperature, stQ.p, st);
-            kd_rows_lse(Pb.p, stP.p, R, V, tgt->temperature, br.p, lseP.p, st);
-            kd_rows_lse(Qb.p, stQ.p, R, V, drf->temperature, br.p, lseQ.p, st);
-            const int Rp = (R + 63) / 64 * 64;
-            kd_rows_elem(Pb.p, Qb.p, lseP.p, lseQ.p, wr.p, br.p, R, V, tgt->temperature, drf->temperature,
-                         s.logit_scale, dzT.p, Rp, kl.p, lossr.p, st);
-            prof_set_scope("kd_grad");
-            transpose_pad_bf16(hG.p, s.d, R, s.d, hT.p, Rp, st);
-            GemmArgs g;  // dW[V][d] += dZ^T[V][Rp] . (h^T[d][Rp])^T
-            g.A = dzT.p;
-            g.B = hT.p;
-            g.M = V;
-            g.N = s.d;
-            g.K = Rp;
-            g.lda = Rp;
-            g.ldb = Rp;
-            g.epi.kind = kEpiResidual;
-            g.epi.out = grad;
-            g.epi.ldo = s.d;
-            gemm_bf16(g, st);
-            RS_CUDA(cudaMemcpyAsync(lh.data(), lossr.p, (size_t)R * 8, cudaMemcpyDeviceToHost, st));
-            RS_CUDA(cudaStreamSynchronize(st));
-            for (int k = 0; k < R; ++k) loss += lh[k];
-            stage.off = 0;
-        }
-        return loss;
+        std::vector<KdTrainSeq> ts;
+        for (const auto &x : refs)
+            ts.push_back(KdTrainSeq{x.req, eng->prompt_len[x.req], eng->len[x.req], x.weight, x.eos_bias});
+        return kd_train(d, ts, grad, Mcap, st);
     }
 
     // Target prefill of prompt positions 0..P-2 (the last prompt token is the first root).
@@ -896,11 +1058,35 @@ std::unique_ptr<ModelPair> make_transformer_pair(rs_ctx *ctx, rs_engine *eng, co
     return p;
 }
 
+DrafterGradLayout drafter_grad_layout(const TfShape &s) {
+    DrafterGradLayout g;
+    size_t o = 0;
+    auto take = [&](size_t n) {
+        const size_t at = o;
+        o += (n + 63) / 64 * 64;  // 256-byte aligned tensors
+        return at;
+    };
+    const size_t q = s.qkv_dim(), HD = (size_t)s.H * s.hd;
+    g.lm = take((size_t)s.V * s.d);
+    g.fc = take((size_t)s.d * 3 * s.d);
+    g.norm_emb = take(s.d);
+    g.norm_hid = take(s.d);
+    g.qkv_w = take(q * 2 * s.d);
+    g.qkv_b = take(q);
+    g.o_w = take((size_t)s.d * HD);
+    g.ln2 = take(s.d);
+    g.gu_w = take((size_t)2 * s.dff * s.d);
+    g.down_w = take((size_t)s.d * s.dff);
+    g.final_norm = take(s.d);
+    g.total = o;
+    return g;
+}
+
 double kd_grad_transformer(rs_ctx *ctx, const TransformerModel *tgt, const DrafterModel *drf,
                            const std::vector<KdSeq> &seqs, float *grad, bool zero_grad) {
     if (!tgt || !drf || drf->target != tgt) throw std::invalid_argument("kd: drafter is bound to a different target");
     cudaStream_t st = ctx->stream;
-    if (zero_grad) RS_CUDA(cudaMemsetAsync(grad, 0, (size_t)tgt->s.V * tgt->s.d * sizeof(float), st));
+    if (zero_grad) RS_CUDA(cudaMemsetAsync(grad, 0, drafter_grad_layout(drf->s).total * sizeof(float), st));
     if (seqs.empty()) return 0.0;
     int tok_cap = 1;
     std::vector<int> plen;
@@ -943,7 +1129,23 @@ DrafterModel *drafter_apply_lm_grad(rs_ctx *ctx, const DrafterModel *drf, const 
     if (m->arena.n != drf->arena.n) throw std::logic_error("drafter arena layout mismatch");
     cudaStream_t st = ctx->stream;
     RS_CUDA(cudaMemcpyAsync(m->arena.p, drf->arena.p, m->arena.n, cudaMemcpyDeviceToDevice, st));
-    if (grad && scale != 0.0) sgd_bf16(drf->lm_w, grad, (float)scale, (size_t)m->s.V * m->s.d, m->lm_w, st);
+    if (grad && scale != 0.0) {  // every drafter tensor: w + scale * grad (drafter_grad_layout)
+        const TfShape &s = m->s;
+        const DrafterGradLayout gl = drafter_grad_layout(s);
+        const float sc = (float)scale;
+        const size_t q = s.qkv_dim(), HD = (size_t)s.H * s.hd;
+        sgd_bf16(drf->lm_w, grad + gl.lm, sc, (size_t)s.V * s.d, m->lm_w, st);
+        sgd_bf16(drf->fc_w, grad + gl.fc, sc, (size_t)s.d * 3 * s.d, m->fc_w, st);
+        sgd_f32(drf->norm_emb, grad + gl.norm_emb, sc, s.d, m->norm_emb, st);
+        sgd_f32(drf->norm_hid, grad + gl.norm_hid, sc, s.d, m->norm_hid, st);
+        sgd_bf16(drf->layer.qkv_w, grad + gl.qkv_w, sc, q * 2 * s.d, m->layer.qkv_w, st);
+        sgd_bf16(drf->layer.qkv_b, grad + gl.qkv_b, sc, q, m->layer.qkv_b, st);
+        sgd_bf16(drf->layer.o_w, grad + gl.o_w, sc, (size_t)s.d * HD, m->layer.o_w, st);
+        sgd_f32(drf->layer.ln2, grad + gl.ln2, sc, s.d, m->layer.ln2, st);
+        sgd_bf16(drf->layer.gu_w, grad + gl.gu_w, sc, (size_t)2 * s.dff * s.d, m->layer.gu_w, st);
+        sgd_bf16(drf->layer.down_w, grad + gl.down_w, sc, (size_t)s.d * s.dff, m->layer.down_w, st);
+        sgd_f32(drf->final_norm, grad + gl.final_norm, sc, s.d, m->final_norm, st);
+    }
     RS_CUDA(cudaStreamSynchronize(st));
     return m.release();
 }

@@ -1,22 +1,147 @@
-"""Multi-GPU plumbing for the rollout path.
+"""Multi-GPU plumbing for the rollout path -- no PyTorch.
 
 Generation shards BY PROMPT: every rank runs its own BatchEngine on its own requests and no
 collective touches the decode path (a request's tokens depend only on its own RNG streams and
 the models -- verified on the compiled reference for fixed configs). The one exchange is the
 KD update of the drafter: the ceil(N/I) selection runs replicated on every rank from the same
 selection stream over GLOBAL buffer indices (learner.cpp:107-121), each rank computes the
-reward-weighted gradient of its locally held selected samples on its GPU (K5), and the
-gradients are summed with torch.distributed (NCCL over NVLink on the GPUs, gloo in the CPU
-tests). The sum equals the reference's gradient up to fp64 summation order
-(learner.cpp:68-80 sums over samples)."""
+reward-weighted gradient of its locally held selected samples on its GPU (K5 + the drafter
+backward), and the gradients are summed by the library's NCCL communicator (`Comm`, rs_comm_*:
+NCCL over NVLink / NVSwitch, in place on the library-owned gradient buffer). The sum equals the
+reference's gradient up to summation order (learner.cpp:68-80 sums over samples).
+
+Ranks find each other through the launcher's environment (RANK / WORLD_SIZE / LOCAL_RANK /
+MASTER_ADDR / MASTER_PORT, as torchrun sets them): rank 0 creates the NCCL unique id and hands
+it to the others over a TCP socket (Comm.from_env). Host-side reductions in tests go through a
+caller-supplied hook (`all_reduce=`), e.g. gloo on CPU."""
 from __future__ import annotations
 
 import ctypes
+import os
+import socket
+import time
 from dataclasses import dataclass
 from typing import Callable, List, Optional, Sequence, Tuple
 
-from . import (KDPolicy, RolloutSample, SelectionRng, TabularARModel, _KDSample, _check, _f64arr, _i32arr,
-               kd_grad_transformer, kd_weight, lib)
+from . import (Device, DeviceBuffer, KDPolicy, RolloutSample, SelectionRng, TabularARModel, _KDSample, _check,
+               _f64arr, _i32arr, default_device, kd_grad_transformer, kd_weight, lib)
+
+RS_COMM_ID_BYTES = 128
+_DT = {"f32": 0, "f64": 1, "i64": 2}
+_OP = {"sum": 0, "max": 1}
+
+
+def dist_env() -> Tuple[int, int, int]:
+    """(rank, world size, local rank) from the launcher's environment (1 rank when unset)."""
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def _rendezvous(rank: int, world: int, payload: Optional[bytes], addr: str, port: int, timeout: float) -> bytes:
+    """Rank 0 serves `payload` to ranks 1..world-1 over TCP; they return it."""
+    if rank == 0:
+        srv = socket.socket(socket.AF_INET, socket.SOCK_STREAM)
+        srv.setsockopt(socket.SOL_SOCKET, socket.SO_REUSEADDR, 1)
+        srv.bind((addr, port))
+        srv.listen(world)
+        srv.settimeout(timeout)
+        try:
+            for _ in range(world - 1):
+                c, _ = srv.accept()
+                with c:
+                    c.sendall(payload)
+        finally:
+            srv.close()
+        return payload
+    deadline = time.time() + timeout
+    while True:
+        try:
+            with socket.create_connection((addr, port), timeout=5) as c:
+                buf = b""
+                while len(buf) < RS_COMM_ID_BYTES:
+                    chunk = c.recv(RS_COMM_ID_BYTES - len(buf))
+                    if not chunk:
+                        raise ConnectionError("rendezvous: short read")
+                    buf += chunk
+                return buf
+        except OSError:
+            if time.time() > deadline:
+                raise TimeoutError(f"rendezvous with rank 0 at {addr}:{port} timed out")
+            time.sleep(0.2)
+
+
+class Comm:
+    """One rank of the library's NCCL communicator (rs_comm_create): the drafter-gradient
+    all-reduce of the prompt-sharded KD update, plus small host reductions (losses, token
+    counts, max-over-ranks device times)."""
+
+    def __init__(self, nranks: int, rank: int, uid: bytes, device: Optional[Device] = None):
+        self.device = device or default_device()
+        self.size, self.rank = nranks, rank
+        idbuf = (ctypes.c_uint8 * RS_COMM_ID_BYTES).from_buffer_copy(uid)
+        h = ctypes.c_void_p()
+        _check(lib().rs_comm_create(self.device.handle, nranks, rank, idbuf, ctypes.byref(h)))
+        self.handle = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * RS_COMM_ID_BYTES)()
+        _check(lib().rs_comm_unique_id(buf))
+        return bytes(buf)
+
+    @staticmethod
+    def nccl_version() -> int:
+        v = ctypes.c_int32()
+        _check(lib().rs_nccl_version(ctypes.byref(v)))
+        return v.value
+
+    @staticmethod
+    def from_env(device: Optional[Device] = None, timeout: float = 300.0) -> "Comm":
+        """All ranks of a torchrun-style launch: rank 0's unique id reaches the others over
+        MASTER_ADDR : (RS_COMM_PORT or MASTER_PORT + 17)."""
+        rank, world, _ = dist_env()
+        addr = os.environ.get("MASTER_ADDR", "127.0.0.1")
+        port = int(os.environ.get("RS_COMM_PORT", int(os.environ.get("MASTER_PORT", 29500)) + 17))
+        uid = Comm.unique_id() if rank == 0 else None
+        if world > 1:
+            uid = _rendezvous(rank, world, uid, addr, port, timeout)
+        return Comm(world, rank, uid, device)
+
+    def allreduce_(self, buf, count: Optional[int] = None, dtype: str = "f32", op: str = "sum"):
+        """In place on a device buffer (DeviceBuffer / pointer), on the device's stream."""
+        ptr = buf.data_ptr() if hasattr(buf, "data_ptr") else int(buf)
+        if count is None:
+            count = buf.nbytes // (8 if dtype in ("f64", "i64") else 4)
+        _check(lib().rs_comm_allreduce(self.handle, self.device.handle, ctypes.c_void_p(ptr), count, _DT[dtype],
+                                       _OP[op]))
+        return buf
+
+    def allreduce_host(self, vals: Sequence[float], op: str = "sum") -> List[float]:
+        arr = (ctypes.c_double * max(1, len(vals)))(*vals)
+        _check(lib().rs_comm_allreduce_host(self.handle, self.device.handle, arr, len(vals), _OP[op]))
+        return list(arr[:len(vals)])
+
+    def barrier(self) -> None:
+        self.allreduce_host([0.0])
+
+    def host_all_reduce(self) -> Callable[[List[float]], List[float]]:
+        """The `all_reduce=` hook of kd_step_distributed (sum of a host vector, in slices)."""
+        def fn(vec):
+            out = []
+            for i in range(0, len(vec), 64):
+                out += self.allreduce_host(vec[i:i + 64])
+            return out
+        return fn
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            lib().rs_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def shard_requests(requests: Sequence, rank: int, world: int, group_size: int = 1) -> List:
@@ -90,7 +215,7 @@ def kd_step_distributed(global_rewards: Sequence[float], global_lengths: Sequenc
     """One prompt-sharded KD step (kd_update, learner.cpp:98-160, minus the weight update):
     replicated selection and weights, local K5 gradient of the selected samples this rank
     holds, then the cross-rank sum. `all_reduce(vec) -> vec` sums a float vector over ranks
-    (torch.distributed in practice; None = single rank)."""
+    (Comm.host_all_reduce() on GPUs, gloo in the CPU tests; None = single rank)."""
     if policy.mode == 2:
         from . import LogicError
         raise LogicError("kd_update: frozen drafter takes no updates")
@@ -108,19 +233,6 @@ def kd_step_distributed(global_rewards: Sequence[float], global_lengths: Sequenc
                                sim_cost_per_token * tokens)
 
 
-def torch_all_reduce(group=None, device: str = "cpu") -> Callable[[List[float]], List[float]]:
-    """Sum over ranks with torch.distributed (NCCL for CUDA tensors, gloo for CPU)."""
-    import torch
-    import torch.distributed as dist
-
-    def fn(vec):
-        t = torch.tensor(vec, dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-        return t.cpu().tolist()
-
-    return fn
-
-
 @dataclass
 class TransformerKDStep:
     drafter: object          # the new EagleDrafter snapshot (version + 1), identical on every rank
@@ -134,18 +246,18 @@ class TransformerKDStep:
 def kd_step_distributed_transformer(drafter, global_rewards: Sequence[float], global_lengths: Sequence[int],
                                     local_samples: Sequence[RolloutSample], local_global_idx: Sequence[int],
                                     policy: KDPolicy, selection_rng: SelectionRng, sim_cost_per_token: float,
-                                    group=None, reduce: bool = True, engine=None,
-                                    local_req_ids: Optional[Sequence[int]] = None) -> TransformerKDStep:
+                                    comm: Optional[Comm] = None, engine=None,
+                                    local_req_ids: Optional[Sequence[int]] = None, grad: Optional[DeviceBuffer] = None
+                                    ) -> TransformerKDStep:
     """Prompt-sharded kd_update for an EAGLE drafter: replicated selection + reward weights over
-    GLOBAL buffer indices (learner.cpp:107-140), this rank's K5 + LM-head gradient on its GPU,
-    ONE all-reduce of the fp32 [V, d] gradient (and the loss) with torch.distributed -- NCCL over
-    NVLink on a B200 box, the only collective of the whole rollout path -- then the same SGD
-    step (-lr) on every rank, so every rank publishes the same snapshot.
+    GLOBAL buffer indices (learner.cpp:107-140), this rank's K5 + whole-drafter gradient on its
+    GPU, ONE in-place all-reduce of the fp32 gradient buffer (every drafter tensor) plus the loss
+    through the library's NCCL communicator -- the only collective of the whole rollout path --
+    then the same SGD step (-lr) on every rank, so every rank publishes the same snapshot.
 
     With `engine` (this rank's BatchEngine that generated the local rollouts; local_req_ids[k] =
     its request index of local_samples[k]) the gradient comes from the engine's resident KV cache
     and features (BatchEngine.kd_grad) instead of a teacher-forced recompute of the prompts."""
-    import torch
     if policy.mode == 2:
         from . import LogicError
         raise LogicError("kd_update: frozen drafter takes no updates")
@@ -157,16 +269,12 @@ def kd_step_distributed_transformer(drafter, global_rewards: Sequence[float], gl
     mine = sorted([(order[g], s, weights[g], q) for s, g, q in zip(local_samples, local_global_idx, rids)
                    if g in weights], key=lambda t: t[0])
     if engine is not None:
-        loss, grad = engine.kd_grad(drafter, [q for *_, q in mine], [w for _, _, w, _ in mine])
+        loss, grad = engine.kd_grad(drafter, [q for *_, q in mine], [w for _, _, w, _ in mine], grad=grad)
     else:
-        loss, grad = kd_grad_transformer(drafter, [s for _, s, _, _ in mine], [w for _, _, w, _ in mine])
-    if reduce:
-        import torch.distributed as dist
-        if dist.is_available() and dist.is_initialized():
-            dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
-            lt = torch.tensor([loss], dtype=torch.float64, device=grad.device)
-            dist.all_reduce(lt, op=dist.ReduceOp.SUM, group=group)
-            loss = float(lt.item())
+        loss, grad = kd_grad_transformer(drafter, [s for _, s, _, _ in mine], [w for _, _, w, _ in mine], grad=grad)
+    if comm is not None and comm.size > 1:
+        comm.allreduce_(grad)
+        loss = comm.allreduce_host([loss])[0]
     new = drafter.apply_grad(grad, -policy.lr)
     tokens = sum(global_lengths[i] for i in sel)
     return TransformerKDStep(new, loss, sel, [weights[i] for i in sel], len(sel), sim_cost_per_token * tokens)

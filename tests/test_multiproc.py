@@ -26,13 +26,21 @@ def _free_port():
     return p
 
 
+def gloo_all_reduce(vec):
+    """Host-reduce hook of kd_step_distributed (the library's NCCL communicator on GPUs)."""
+    import torch
+    t = torch.tensor(vec, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.tolist()
+
+
 def _worker(rank, port, case_idx, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     try:
         import paper_2510_26475_b200 as rb
-        from paper_2510_26475_b200.distributed import kd_step_distributed, shard_requests, torch_all_reduce
+        from paper_2510_26475_b200.distributed import kd_step_distributed, shard_requests
         from oracle_client import Oracle
 
         g = load_golden("kd_update.json")
@@ -52,7 +60,7 @@ def _worker(rank, port, case_idx, q):
         pol = rb.KDPolicy(p["interval"], mode, p["clip_lo"], p["clip_hi"], p["lr"])
         res = kd_step_distributed([s["reward"] for s in buf], [len(s["response"]) for s in buf],
                                   [buf[i] for i in mine], mine, pol, rb.SelectionRng(c["selection_seed"]), 0.02,
-                                  grad_fn, torch_all_reduce())
+                                  grad_fn, gloo_all_reduce)
         new = [z + gr * -p["lr"] for z, gr in zip(g["drafter"]["logits"], res.grad)]
         q.put((rank, mine, new, res.loss, res.samples_used, res.sim_time, res.selected))
     finally:
