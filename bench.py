@@ -62,6 +62,20 @@ def dist_env():
     return rank, world, local
 
 
+def relaunch(n):
+    """`bench.py --gpus N` outside a launcher: re-run this script as N ranks (one process per
+    GPU) under torch.distributed.run, the launcher the driver itself uses, on 127.0.0.1."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] launching {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 # ---- clocks (B200_PROFILING.md recipe) -------------------------------------------------------
 class ClockSampler:
     FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
@@ -300,7 +314,7 @@ def batch256_leg(args, rb, target, drafter, dev, stream, cfg, peaks):
             "north_star_target": ">= 0.60 tensor utilisation in verification"}
 
 
-def tuner_leg(args, rb, target, drafter, reqs, dev, stream, max_len, cfg, world, barrier):
+def tuner_leg(args, rb, target, drafter, reqs, dev, stream, max_len, cfg, world, barrier, comm):
     """cfg3-style leg: the same rollouts with DYNAMIC SD-config tuning -- a ProfileTable measured
     on this GPU (device ms per emitted token per power-of-two bucket and config, profile() of
     server.cpp:182-239 with measured instead of simulated latency), re-solved every cycle from
@@ -333,14 +347,9 @@ def tuner_leg(args, rb, target, drafter, reqs, dev, stream, max_len, cfg, world,
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        n = torch.tensor([tokens], dtype=torch.float64, device="cuda")
-        dist.all_reduce(n)
-        tokens = int(n.item())
+    if comm is not None:
+        ms = comm.allreduce_host([ms], "max")[0]
+        tokens = int(comm.allreduce_host([tokens], "sum")[0])
     return {"value": round(tokens / (ms / 1000.0), 1), "unit": "tokens/s", "ms_per_step": round(ms / args.steps, 3),
             "mean_accept_len": round(acc / drafted, 4) if drafted else 0.0, "configs_used": modes,
             "table_best": {b: table.best_for_bucket(b).key() for b in buckets},
@@ -348,7 +357,7 @@ def tuner_leg(args, rb, target, drafter, reqs, dev, stream, max_len, cfg, world,
             "source": "ProfileTable of measured device ms per emitted token (this GPU)"}
 
 
-def kd_leg(args, rb, eng, drafter, rank, world, barrier):
+def kd_leg(args, rb, eng, drafter, rank, world, barrier, comm):
     """cfg5 leg: one online KD update of the drafter on this step's rollouts (prompt + generated
     tokens of the first --kd requests per GPU), reward-weighted (synthetic rewards), the fp32
     LM-head gradient all-reduced over the ranks (NCCL), the same SGD snapshot on every rank.
@@ -368,24 +377,21 @@ def kd_leg(args, rb, eng, drafter, rank, world, barrier):
         local.append(rb.RolloutSample(list(r.prompt), list(r.generated), [], eos_bias=r.eos_bias, reward=rewards[g]))
         gidx.append(g)
         lengths[g] = len(r.generated)
-    if world > 1:
-        import torch.distributed as dist
-        lt = torch.tensor(lengths, dtype=torch.int64, device="cuda")
-        dist.all_reduce(lt)
-        lengths = lt.tolist()
+    if comm is not None:
+        lengths = [int(x) for x in comm.host_all_reduce()(lengths)]
     pol = rb.KDPolicy(interval=1, mode=0, clip_lo=0.0, clip_hi=4.0, lr=0.5)  # config.hpp:38
     # untimed warm-up of both paths: first-use allocations (the engine's grow-only KD scratch,
     # the recompute path's workspaces) stay out of the timed region, as for an online learner
     # that updates every iteration
     kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02,
-                                    engine=eng, local_req_ids=list(range(len(local))))
-    kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02)
+                                    comm=comm, engine=eng, local_req_ids=list(range(len(local))))
+    kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02, comm=comm)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     step = kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02,
-                                           engine=eng, local_req_ids=list(range(len(local))))
+                                           comm=comm, engine=eng, local_req_ids=list(range(len(local))))
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -393,23 +399,21 @@ def kd_leg(args, rb, eng, drafter, rank, world, barrier):
     barrier()
     torch.cuda.synchronize()
     e0.record()
-    kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02)
+    kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02, comm=comm)
     e1.record()
     torch.cuda.synchronize()
     ms_recompute = e0.elapsed_time(e1)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    if comm is not None:
+        ms = comm.allreduce_host([ms], "max")[0]
     toks = sum(lengths)
     shape = drafter.shape
     return {"rollouts": args.kd * world, "tokens_distilled": toks, "ms": round(ms, 2),
             "source": "engine-resident target KV cache + features (rs_engine_kd_grad)",
             "ms_teacher_forced_recompute": round(ms_recompute, 2),
             "distilled_tokens_per_s": round(toks / (ms / 1000.0), 1), "loss": step.loss,
-            "new_drafter_version": step.drafter.version, "trained": "drafter LM head (fp32 grad [V, d])",
-            "allreduce_bytes": shape.vocab * shape.d_model * 4 if world > 1 else 0,
+            "new_drafter_version": step.drafter.version,
+            "trained": "every EAGLE drafter tensor (LM head, final norm, MLP, O, attention, QKV, input norms, fc)",
+            "allreduce_bytes": drafter.grad_layout()[1] * 4 if world > 1 else 0,
             "context_tokens_per_rollout": args.ctx}
 
 
@@ -418,13 +422,13 @@ def main():
     rank, world, local = dist_env()
     if args.impl == "reference":
         return reference_arm(args, rank, world)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
 
     import torch
     torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2510_26475_b200 as rb
+    from paper_2510_26475_b200.distributed import Comm
 
     s, t, n = map(int, args.sd.split(","))
     cfg = rb.SDConfig.tree(s, t, n)
@@ -437,6 +441,9 @@ def main():
     dev = rb.Device(local)
     stream = torch.cuda.Stream()
     dev.set_stream(stream.cuda_stream)
+    # the library's NCCL communicator (rank 0's id over MASTER_ADDR): barriers, max-over-ranks
+    # times and token sums here, the drafter-gradient all-reduce in the KD leg
+    comm = Comm.from_env(dev) if world > 1 else None
     target = rb.TransformerModel(shape, seed=20251026, device=dev)
     drafter = rb.EagleDrafter(target, seed=4242, version=1)
     import random
@@ -459,8 +466,8 @@ def main():
     print(f"[bench] prefill {prefill_s:.2f} s", file=sys.stderr, flush=True)
 
     def barrier():
-        if world > 1:
-            torch.distributed.barrier()
+        if comm is not None:
+            comm.barrier()
 
     for _ in range(args.warmup):
         eng.step()
@@ -517,10 +524,10 @@ def main():
             eng.step()
         prof = rb.device_profile(enable=False)
 
-    kd = kd_leg(args, rb, eng, drafter, rank, world, barrier) if args.kd > 0 else None
+    kd = kd_leg(args, rb, eng, drafter, rank, world, barrier, comm) if args.kd > 0 else None
     dyn = None
     if not args.tuner and not args.no_tuner_leg:
-        dyn = tuner_leg(args, rb, target, drafter, reqs, dev, stream, max_len, cfg, world, barrier)
+        dyn = tuner_leg(args, rb, target, drafter, reqs, dev, stream, max_len, cfg, world, barrier, comm)
     overlap = None
     if world == 1 and args.kd > 0 and args.model != "tiny":
         overlap = kd_overlap_leg(args, rb, target, drafter, eng, dev, stream, cfg)
@@ -528,14 +535,9 @@ def main():
     if world == 1 and args.model == "3b" and args.batch != 256 and not args.no_b256_leg:
         b256 = batch256_leg(args, rb, target, drafter, dev, stream, cfg, measured_peaks()[0])
 
-    if world > 1:
-        import torch.distributed as dist
-        vals = torch.tensor([ms, e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-        sums = torch.tensor([tokens, accepted, drafted, e2e_tok], dtype=torch.float64, device="cuda")
-        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
-        ms, e2e_s = vals.tolist()
-        tokens, accepted, drafted, e2e_tok = sums.tolist()
+    if comm is not None:
+        ms, e2e_s = comm.allreduce_host([ms, e2e_s], "max")
+        tokens, accepted, drafted, e2e_tok = comm.allreduce_host([tokens, accepted, drafted, e2e_tok], "sum")
     if rank != 0:
         return
 
