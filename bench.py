@@ -314,6 +314,17 @@ def batch256_leg(args, rb, target, drafter, dev, stream, cfg, peaks):
             "north_star_target": ">= 0.60 tensor utilisation in verification"}
 
 
+def tuner_grid(args, rb, cfg):
+    """The reference's profile grid s{1,2,4} x t{1,2} x n{1,2,4} (config.hpp:46-48) plus the bench's
+    configuration, over power-of-two buckets up to the batch (server.cpp:182-239; non-spec is
+    added by profile_measured)."""
+    buckets = [b for b in (1, 2, 4, 8, 16, 32, 64, 128, 256) if b <= args.batch]
+    grid = [rb.SDConfig.tree(s, t, n) for s in (1, 2, 4) for t in (1, 2) for n in (1, 2, 4)]
+    if cfg.key() not in {c.key() for c in grid}:
+        grid.append(cfg)
+    return buckets, grid
+
+
 def tuner_leg(args, rb, target, drafter, reqs, dev, stream, max_len, cfg, world, barrier, comm):
     """cfg3-style leg: the same rollouts with DYNAMIC SD-config tuning -- a ProfileTable measured
     on this GPU (device ms per emitted token per power-of-two bucket and config, profile() of
@@ -321,9 +332,10 @@ def tuner_leg(args, rb, target, drafter, reqs, dev, stream, max_len, cfg, world,
     the live batch (server.cpp:279). Same metric as the headline, device time, max over ranks."""
     import torch
     t0 = time.perf_counter()
-    buckets = [b for b in (1, 2, 4, 8, 16, 32, 64, 128, 256) if b <= args.batch]
-    grid = [rb.SDConfig.chain(3), rb.SDConfig.tree(1, 2, 3), rb.SDConfig.tree(1, 4, 3), cfg]
-    table = rb.profile_measured(target, drafter, buckets, grid, prompt_len=128, warmup=1, cycles=3)
+    buckets, grid = tuner_grid(args, rb, cfg)
+    # measured at the rollout's own context length: attention cost, and with it the argmin,
+    # depends on it
+    table = rb.profile_measured(target, drafter, buckets, grid, prompt_len=args.ctx, warmup=1, cycles=3)
     prof_s = time.perf_counter() - t0
     fresh = [rb.RequestState(r.id, list(r.prompt), r.eos_bias, max_len, rb.DecodeRng.from_seed(11, r.id))
              for r in reqs]
@@ -353,8 +365,10 @@ def tuner_leg(args, rb, target, drafter, reqs, dev, stream, max_len, cfg, world,
     return {"value": round(tokens / (ms / 1000.0), 1), "unit": "tokens/s", "ms_per_step": round(ms / args.steps, 3),
             "mean_accept_len": round(acc / drafted, 4) if drafted else 0.0, "configs_used": modes,
             "table_best": {b: table.best_for_bucket(b).key() for b in buckets},
-            "grid": ["off"] + [c.key() for c in grid], "profile_s": round(prof_s, 2),
-            "source": "ProfileTable of measured device ms per emitted token (this GPU)"}
+            "grid": ["off"] + [c.key() for c in grid], "profile_s": round(prof_s, 2), "profile_context": args.ctx,
+            "table_ms_per_token": {b: {c.key(): round(t, 5) for c, t in table.entries_for(b)} for b in buckets},
+            "source": "ProfileTable of measured device ms per emitted token (this GPU), reference grid "
+                      "s{1,2,4} x t{1,2} x n{1,2,4} + the bench config (config.hpp:46-48), reference tie-break"}
 
 
 def kd_leg(args, rb, eng, drafter, rank, world, barrier, comm):
@@ -403,6 +417,25 @@ def kd_leg(args, rb, eng, drafter, rank, world, barrier, comm):
     e1.record()
     torch.cuda.synchronize()
     ms_recompute = e0.elapsed_time(e1)
+    # K5's HBM roofline (per KD row read the target row and the drafter row, write
+    # dZ: V * (4 + 4 + 2) bytes) and the backward's share, from the per-kernel profiler
+    rb.device_profile(enable=True, reset=True)
+    kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02,
+                                    comm=comm, engine=eng, local_req_ids=list(range(len(local))))
+    kprof = rb.device_profile(enable=False)
+    k5 = kprof.get("kd_k5.kd")
+    peaks = measured_peaks()[0]
+    hbm_peak = peaks.get("hbm_gbs", peaks.get("hbm_GBs", 6650.0))
+    k5_roof = None
+    if k5 and k5["ms"] > 0:
+        gbs = k5["bytes"] / (k5["ms"] / 1000.0) / 1e9
+        k5_roof = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                   "frac": round(gbs / hbm_peak, 4), "bytes_per_launch": k5["bytes"] / max(1, k5["launches"]),
+                   "ms": round(k5["ms"], 3), "kernel": "kd_elem (K5: w KL per row + dZ^T)"}
+    scopes = {}
+    for key, v in kprof.items():
+        sc = key.split(".")[0]
+        scopes[sc] = round(scopes.get(sc, 0.0) + v["ms"], 3)
     if comm is not None:
         ms = comm.allreduce_host([ms], "max")[0]
     toks = sum(lengths)
@@ -414,7 +447,63 @@ def kd_leg(args, rb, eng, drafter, rank, world, barrier, comm):
             "new_drafter_version": step.drafter.version,
             "trained": "every EAGLE drafter tensor (LM head, final norm, MLP, O, attention, QKV, input norms, fc)",
             "allreduce_bytes": drafter.grad_layout()[1] * 4 if world > 1 else 0,
-            "context_tokens_per_rollout": args.ctx}
+            "context_tokens_per_rollout": args.ctx, "k5_roofline": k5_roof, "ms_by_scope": scopes}
+
+
+def parity_leg(args, rb, target, drafter, dev, cfg):
+    """The bench's own configuration checked end to end: on a 4-request subset of
+    the workload (same 3B-shaped target / drafter weights, same context length, same SD config)
+    greedy speculative decoding must emit exactly the tokens of plain greedy decoding of the
+    target (specdec.cpp:197-267 with the greedy rule; row-invariant forward). The sampled-mode
+    acceptance at this geometry is replayed bit-exactly by the CPU oracle in
+    tests/test_parity_qwen_gpu.py (the oracle stays out of the bench's GPU arm)."""
+    import random
+    rng = random.Random(5150)
+    n_tok = 16
+    prompts = [[rng.randrange(target.shape.vocab - 1) for _ in range(args.ctx)] for _ in range(4)]
+
+    def gen(c):
+        reqs = [rb.RequestState(i, list(p), -20.0, n_tok, rb.DecodeRng.from_seed(3, i)) for i, p in enumerate(prompts)]
+        e = rb.BatchEngine(target, lambda: drafter, None, rb.TimingModel(), reqs, c, "greedy",
+                           record_full_logprobs=False, device=dev)
+        while not e.all_done():
+            e.step()
+        return [r.generated for r in e.requests()], [a for r in e.requests() for a in r.accept_lens]
+
+    base, _ = gen(rb.SDConfig.off())
+    sd, al = gen(cfg)
+    return {"check": "greedy SD == greedy decode (token for token)", "requests": 4, "tokens_per_request": n_tok,
+            "context": args.ctx, "sd_config": cfg.key(), "greedy_sd_equals_greedy_decode": sd == base,
+            "accepted_drafted_tokens": sum(al),
+            "sampled_replay": "tests/test_parity_qwen_gpu.py (oracle replay at V=151936, bit-exact)"}
+
+
+def same_workload_leg(rb, dev, lib, kind, tgt_j, drf_j, creqs, forced, cpu_al):
+    """The reference arm's exact workload (its TabularARModel V=8 actor + drafter from make_env,
+    batch, SD config, max_len, eos_bias, seeds) on the GPU engine's parity mode: token-identical
+    responses against the CPU reference, and both mean accept lengths -- the metric's "mean
+    accept length vs CPU ref" on one workload (specdec.hpp:67, server.cpp:319-321)."""
+    import time as _t
+    tgt = rb.TabularARModel.from_json(tgt_j, device=dev)
+    drf = rb.TabularARModel.from_json(drf_j, device=dev)
+    reqs = lambda: [rb.RequestState(r["id"], r["prompt"], r["eos_bias"], r["max_len"],  # noqa: E731
+                                    rb.DecodeRng.from_seed(r["seed"], r["stream"])) for r in creqs]
+    cfg = rb.SDConfig(forced["s"], forced["t"], forced["n"], True)
+    rb.run_generation(reqs(), tgt, lambda: drf, None, rb.TimingModel(), cfg, record_full_logprobs=False, device=dev)
+    t0 = _t.perf_counter()
+    run = rb.run_generation(reqs(), tgt, lambda: drf, None, rb.TimingModel(), cfg, record_full_logprobs=False,
+                            device=dev)
+    wall = _t.perf_counter() - t0
+    toks = sum(len(x.response) for x in run.samples)
+    identical = None
+    if kind == "reference":
+        ref = lib("run_generation", target=tgt_j, drafter=drf_j, requests=creqs, forced=forced, record_logprobs=False)
+        identical = [x.response for x in run.samples] == [x["response"] for x in ref["samples"]] and \
+            run.accept_lens == ref["accept_lens"]
+    return {"workload": "the reference arm's: make_env seed 1 TabularARModel V=8, same batch / SD config / seeds",
+            "gpu_tokens_per_s_e2e": round(toks / wall, 1), "gpu_device_ms": round(run.wall_ms, 2), "tokens": toks,
+            "gpu_mean_accept_len": round(rb.mean_accept_len(run.accept_lens), 4),
+            "cpu_mean_accept_len": round(cpu_al, 4), "token_identical_to_cpu_reference": identical}
 
 
 def main():
@@ -453,9 +542,8 @@ def main():
     table, tuner = None, None
     if args.tuner:
         t_prof = time.perf_counter()
-        buckets = [b for b in (1, 2, 4, 8, 16, 32, 64, 128, 256) if b <= args.batch]
-        grid = [rb.SDConfig.chain(3), rb.SDConfig.tree(1, 2, 3), rb.SDConfig.tree(1, 4, 3), cfg]
-        table = rb.profile_measured(target, drafter, buckets, grid, prompt_len=128, warmup=1, cycles=3)
+        buckets, grid = tuner_grid(args, rb, cfg)
+        table = rb.profile_measured(target, drafter, buckets, grid, prompt_len=args.ctx, warmup=1, cycles=3)
         tuner = {"profile_s": round(time.perf_counter() - t_prof, 2),
                  "best": {b: table.best_for_bucket(b).key() for b in buckets},
                  "grid": ["off"] + [c.key() for c in grid], "source": "measured device ms per emitted token"}
@@ -531,6 +619,7 @@ def main():
     overlap = None
     if world == 1 and args.kd > 0 and args.model != "tiny":
         overlap = kd_overlap_leg(args, rb, target, drafter, eng, dev, stream, cfg)
+    parity = parity_leg(args, rb, target, drafter, dev, cfg) if args.model != "tiny" else None
     b256 = None
     if world == 1 and args.model == "3b" and args.batch != 256 and not args.no_b256_leg:
         b256 = batch256_leg(args, rb, target, drafter, dev, stream, cfg, measured_peaks()[0])
@@ -565,12 +654,26 @@ def main():
     # compaction), per-kernel profiler time; bytes per SURVEY §8(d)
     hbm = {}
     nprof = max(1, min(args.steps, 5))
+    def measured_bytes(name):
+        path = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(path):
+            with open(path) as f:
+                return json.load(f).get("dram_bytes_per_launch")
+        return None
+
+    peak_hbm = measured_peaks()[0].get("hbm_gbs", 6650.0)
     if "accept.accept" in prof and prof["accept.accept"]["ms"] > 0:
         a = prof["accept.accept"]
-        hbm["acceptance"] = {"algorithmic_bytes_per_step": a["bytes"] / nprof, "ms_per_step": a["ms"] / nprof,
-                             "GB_s": round(a["bytes"] / (a["ms"] / 1000.0) / 1e9, 1),
-                             "bytes": "(t*n_eff+1) target + t*n_eff drafter fp32 logit rows of V per sequence, "
-                                      "as if materialised; lazy tile statistics read ~3 rows"}
+        ms_launch = a["ms"] / max(1, a["launches"])
+        dram = measured_bytes("accept_traffic.json")
+        hbm["acceptance"] = {"ms_per_step": a["ms"] / nprof,
+                             "dram_bytes_per_launch": dram,
+                             "GB_s": round(dram / (ms_launch / 1000.0) / 1e9, 1) if dram else None,
+                             "frac_of_hbm_peak": round(dram / (ms_launch / 1000.0) / 1e9 / peak_hbm, 4) if dram else None,
+                             "bytes": "measured DRAM read + write per launch (ncu, profiles/accept_traffic.json) over "
+                                      "the live kernel time: the lazy tile statistics read only the ~3 rows a "
+                                      "sequence's decisions touch, so the kernel is fp64-exp / latency bound",
+                             "algorithmic_bytes_if_materialised": a["bytes"] / nprof}
     if "accept.compact" in prof and prof["accept.compact"]["ms"] > 0 and args.steps > 0:
         c = prof["accept.compact"]
         per_tok = shape.kv_bytes_per_token() + 2 * shape.n_kv_heads * shape.head_dim * 2 + 3 * shape.d_model * 2
@@ -589,6 +692,7 @@ def main():
                "sample": f"{runs} x reference run_generation, TabularARModel V=8 (make_env seed 1), batch "
                          f"{args.batch}, tree({s},{t},{n}), max_len 256, eos_bias -3, {secs:.1f} s wall on "
                          f"{threads} host threads"}
+        cpu["same_workload_on_gpu"] = same_workload_leg(rb, dev, lib, kind, tgt_j, drf_j, creqs, forced, al)
 
     line = {"metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
@@ -606,8 +710,8 @@ def main():
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_tok / e2e_s, 1), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps)},
-            "gpu_launches": launches, "clocks": clk, "breakdown_ms_per_step": breakdown, "kd_update": kd, "kd_async_overlap": overlap, "north_star_batch256": b256,
-            "hbm": hbm or None}
+            "gpu_launches": launches, "clocks": clk, "parity": parity, "breakdown_ms_per_step": breakdown,
+            "kd_update": kd, "kd_async_overlap": overlap, "north_star_batch256": b256, "hbm": hbm or None}
     if dyn:
         line["dynamic_tuning"] = dyn
     if tuner:

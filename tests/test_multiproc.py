@@ -104,3 +104,37 @@ def test_prompt_sharded_kd_step_matches_reference(oracle, case_idx):
     ref = oracle("kd_update", drafter=g["drafter"], buffer=g["buffer"], policy=g["cases"][case_idx]["policy"],
                  selection_seed=g["cases"][case_idx]["selection_seed"], cost_per_token=0.02)
     assert outs[0][6] == ref["selected"]
+
+
+def _rdv_worker(rank, port, q):
+    from paper_2510_26475_b200.distributed import _rendezvous
+    payload = bytes(range(128)) if rank == 0 else None
+    q.put((rank, _rendezvous(rank, WORLD, payload, "127.0.0.1", port, 30.0)))
+
+
+def test_comm_id_rendezvous_two_ranks():
+    """Comm.from_env's id hand-off: rank 0 serves the 128-byte NCCL id, rank 1 receives it."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rdv_worker, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=60) for _ in range(WORLD))
+    for p in procs:
+        p.join(timeout=30)
+    assert got[0] == got[1] == bytes(range(128))
+
+
+def test_bench_relaunches_under_torchrun(monkeypatch):
+    """bench.py --gpus N outside a launcher re-runs itself as N ranks (torch.distributed.run)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    calls = []
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: calls.append(cmd) or 0)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "3"])
+    assert bench.relaunch(4) == 0
+    cmd = calls[0]
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"] and "--nproc-per-node=4" in cmd
+    assert "--master-addr=127.0.0.1" in cmd and cmd[-4:] == ["--gpus", "4", "--steps", "3"]
