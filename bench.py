@@ -394,18 +394,19 @@ def kd_leg(args, rb, eng, drafter, rank, world, barrier, comm):
     if comm is not None:
         lengths = [int(x) for x in comm.host_all_reduce()(lengths)]
     pol = rb.KDPolicy(interval=1, mode=0, clip_lo=0.0, clip_hi=4.0, lr=0.5)  # config.hpp:38
+    grad = drafter.new_grad()  # the learner's gradient buffer (every drafter tensor, fp32), reused per update
     # untimed warm-up of both paths: first-use allocations (the engine's grow-only KD scratch,
     # the recompute path's workspaces) stay out of the timed region, as for an online learner
     # that updates every iteration
     kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02,
-                                    comm=comm, engine=eng, local_req_ids=list(range(len(local))))
-    kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02, comm=comm)
+                                    comm=comm, engine=eng, grad=grad, local_req_ids=list(range(len(local))))
+    kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02, comm=comm, grad=grad)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     step = kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02,
-                                           comm=comm, engine=eng, local_req_ids=list(range(len(local))))
+                                           comm=comm, engine=eng, grad=grad, local_req_ids=list(range(len(local))))
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -413,7 +414,7 @@ def kd_leg(args, rb, eng, drafter, rank, world, barrier, comm):
     barrier()
     torch.cuda.synchronize()
     e0.record()
-    kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02, comm=comm)
+    kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02, comm=comm, grad=grad)
     e1.record()
     torch.cuda.synchronize()
     ms_recompute = e0.elapsed_time(e1)
@@ -421,7 +422,7 @@ def kd_leg(args, rb, eng, drafter, rank, world, barrier, comm):
     # dZ: V * (4 + 4 + 2) bytes) and the backward's share, from the per-kernel profiler
     rb.device_profile(enable=True, reset=True)
     kd_step_distributed_transformer(drafter, rewards, lengths, local, gidx, pol, rb.SelectionRng(123), 0.02,
-                                    comm=comm, engine=eng, local_req_ids=list(range(len(local))))
+                                    comm=comm, engine=eng, grad=grad, local_req_ids=list(range(len(local))))
     kprof = rb.device_profile(enable=False)
     k5 = kprof.get("kd_k5.kd")
     peaks = measured_peaks()[0]

@@ -81,6 +81,7 @@ struct rs_learner {
     std::deque<std::vector<Sample>> jobs;
     bool busy = false, stopping = false, async = false;
     std::string worker_error;   // an update that failed on the worker, raised at the rendezvous
+    rs::DBuf<float> grad_buf;   // drafter gradient of engine-backed updates (grow-only, one updater at a time)
     int worker_status = RS_OK;
     std::thread worker;
 
@@ -112,7 +113,8 @@ struct rs_learner {
             distilled += (size_t)std::max(0, batch[idx[i]].response_len);
         }
         const auto *t = d->target;
-        rs::DBuf<float> grad(rs::drafter_grad_layout(t->s).total);
+        rs::DBuf<float> &grad = grad_buf;  // kept across updates (1.6 GB at 3B: no per-update cudaMalloc)
+        grad.ensure(rs::drafter_grad_layout(t->s).total);
         RS_CUDA(cudaMemsetAsync(grad.p, 0, grad.bytes(), c->stream));
         double loss = 0.0;
         size_t i = 0;

@@ -20,8 +20,9 @@ def test_single_rank_comm_is_identity():
     c = Comm(1, 0, Comm.unique_id())
     assert (c.size, c.rank) == (1, 0)
     buf = rb.DeviceBuffer.floats(1 << 20)
+    host = torch.arange(1 << 20, dtype=torch.float32).numpy()  # kept alive across the copy
     rb._check(rb.lib().rs_memcpy_h2d(buf.device.handle, rb.ctypes.c_void_p(buf.ptr),
-                                      torch.arange(1 << 20, dtype=torch.float32).numpy().ctypes.data, buf.nbytes))
+                                      rb.ctypes.c_void_p(host.ctypes.data), buf.nbytes))
     before = buf.to_numpy().copy()
     c.allreduce_(buf)
     buf.device.sync()

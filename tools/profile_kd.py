@@ -20,7 +20,7 @@ samples = [rb.RolloutSample([rng.randrange(shape.vocab - 1) for _ in range(ctx)]
                             [rng.randrange(shape.vocab - 1) for _ in range(resp)], [], 0.0, rng.random())
            for _ in range(n)]
 w = [1.0] * n
-grad = torch.zeros(shape.vocab, shape.d_model, dtype=torch.float32, device="cuda")
+grad = drf.new_grad()
 for it in range(3):
     if it == 2:
         rb.device_profile(enable=True, reset=True)
@@ -47,6 +47,10 @@ for it in range(3):
     torch.cuda.synchronize()
     t = time.time()
     loss, _ = eng.kd_grad(drf, list(range(n)), w, grad)
+    t2 = time.time()
+    nd = drf.apply_grad(grad, -0.5)
+    torch.cuda.synchronize()
+    print("apply_grad", round((time.time() - t2) * 1e3, 2), "ms", flush=True)
     torch.cuda.synchronize()
     print("engine kd_grad", it, round((time.time() - t) * 1e3, 2), "ms", loss, flush=True)
 prof = rb.device_profile(enable=False)
