@@ -641,7 +641,8 @@ def main():
         peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
-        if os.path.exists(tpath):
+        # the committed ncu capture is of the default workload (cfg2, 3B, batch 64)
+        if os.path.exists(tpath) and args.model == "3b" and args.batch == 64 and not args.tuner:
             with open(tpath) as f:
                 traffic = json.load(f).get("dram_bytes_per_launch")
         roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
@@ -706,7 +707,8 @@ def main():
                        "target_shape": f"qwen2.5-{args.model}", "batch_per_gpu": args.batch, "global_batch": args.batch * world,
                        "sd_config": cfg.key(), "verify": "rejection sampling T=1" if args.verify == "sample"
                        else "greedy", "ctx_len_start": args.ctx, "parallelism": f"prompt-sharded dp{world}",
-                       "l2": "no flush: each step streams 6.2 GB of weights + KV (>> 126 MB L2)",
+                       "l2": f"no flush: each step streams {2 * target.n_params / 1e9:.1f} GB of target weights "
+                             f"+ {2 * drafter.n_params / 1e9:.1f} GB of drafter weights + the KV cache (>> 126 MB L2)",
                        "prefill_s": round(prefill_s, 2)},
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_tok / e2e_s, 1), "unit": "tokens/s",

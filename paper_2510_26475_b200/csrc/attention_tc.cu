@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int jp = pend[i];
                 mbar_wait(&fullV[jp % kStages], (jp / kStages) & 1);
                 mbar_wait(&p_full[i], pv_n[i] & 1);
-                if (tr) trace[2 + 4 * jp + i] = clock64();
+                if (tr) trace[2 + 8 * jp + i] = clock64();
                 tc_fence_after();
                 const uint8_t *v = sKV + (jp % kStages) * kStageBytes + kTileBytes;
                 const uint32_t d_o = tmem + 256 + i * 128, a_p = tmem + i * 128;
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (pend[i] >= 0 && pend[i] <= j - kStages) issue_pv(i);
                 const int s = j % kStages;
                 mbar_wait(&fullK[s], (j / kStages) & 1);
-                if (tr) trace[1 + 4 * j] = clock64();
+                if (tr) trace[1 + 8 * j] = clock64();
                 tc_fence_after();
                 const uint8_t *kt = sKV + s * kStageBytes;
                 for (int i = 0; i < 2; ++i) {
@@ -310,7 +310,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const Pass ps = pl.pass[j];
             if (!(ps.tiles & (1 << tile))) continue;
             mbar_wait(&s_full[tile], n & 1);
-            if (tr && tile == 0 && warp == 4 && lane == 0) trace[4 + 4 * j] = clock64();
+            const bool trs = tr && tile == 0 && warp == 4 && lane == 0;
+            if (trs) trace[4 + 8 * j] = clock64();
             tc_fence_after();
             const int c0 = ps.chunk * kCk + half * 64;
             const bool mine = valid && (ps.grp < 0 || ps.grp == grp);
@@ -321,6 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_ld32_nw(tS + half * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
                 tmem_ld32_nw(tS + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
                 tmem_ld_wait();
+                if (trs) trace[5 + 8 * j] = clock64();
                 float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
                 if (lim >= 63) {
 #pragma unroll
@@ -338,6 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 xch[half * 32 + lane] = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
                 asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");  // both halves loaded S
                 float mx = fmaxf(xch[lane], xch[32 + lane]);
+                if (trs) trace[6 + 8 * j] = clock64();
                 mx = mx == -INFINITY ? mx : mx * scale_log2;  // scale > 0: max commutes with it
                 bool resc = false;
                 float alpha = 1.f;
@@ -367,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     lp[(x + 1) & 7] += p1;
                     pk[x >> 1] = pack_bf16(p0, p1);
                 }
+                if (trs) trace[7 + 8 * j] = clock64();
                 // P (bf16) of this half over S columns [32 half, 32 half + 32), already read by both
                 tmem_st16(tS + half * 32, *reinterpret_cast<uint32_t(*)[16]>(pk));
                 tmem_st16(tS + half * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(pk + 16));
@@ -381,6 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 tmem_st_wait();
+                if (trs) trace[8 + 8 * j] = clock64();
             }
             tc_fence_before();
             __syncwarp();
@@ -447,18 +452,21 @@ void k_attention_tc(const bf16 *q, const RowDesc *rows, const AttnItem *items, c
     const CUtensorMap tv = make_tma_map_bf16(kv.v, total_rows, kHD, kHD, kCk);
     const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(s.hd));
     static long long *trace = nullptr;
-    if (tuning().attn_trace && !trace) RS_CUDA(cudaMalloc(&trace, 8 * (1 + 4 * kMaxPasses)));
+    if (tuning().attn_trace && !trace) RS_CUDA(cudaMalloc(&trace, 8 * (1 + 8 * kMaxPasses)));
     launch_pdl(attn_tc_kernel, dim3(n_items, s.KV), kThreads, kSmem, st, tk, tv, q, rows, items, plan, kv, layer,
                s.H, s.KV, scale_log2, out, tuning().attn_trace ? trace : nullptr);
     if (tuning().attn_trace) {
         RS_CUDA(cudaStreamSynchronize(st));
-        static long long host[1 + 4 * kMaxPasses];
+        static long long host[1 + 8 * kMaxPasses];
         RS_CUDA(cudaMemcpy(host, trace, sizeof(host), cudaMemcpyDeviceToHost));
         if (tuning().attn_trace == layer + 1 && n_items >= 32) {
-            fprintf(stderr, "attn trace layer %d items %d passes %d:\n", layer, n_items, 0);
-            for (int j = 0; j < 24; ++j)
-                fprintf(stderr, "  pass %2d fullK %8lld p0 %8lld p1 %8lld sm0 %8lld\n", j, host[1 + 4 * j] - host[0],
-                        host[2 + 4 * j] - host[0], host[3 + 4 * j] - host[0], host[4 + 4 * j] - host[0]);
+            fprintf(stderr, "attn trace layer %d items %d:\n", layer, n_items);
+            for (int j = 0; j < 24; ++j) {
+                const long long *h = host + 1 + 8 * j;
+                fprintf(stderr, "  pass %2d fullK %8lld p0 %8lld p1 %8lld sm0 %8lld | ld +%lld xch +%lld exp +%lld st +%lld\n",
+                        j, h[0] - host[0], h[1] - host[0], h[2] - host[0], h[3] - host[0], h[4] - h[3], h[5] - h[4],
+                        h[6] - h[5], h[7] - h[6]);
+            }
         }
     }
     RS_LAUNCHED();

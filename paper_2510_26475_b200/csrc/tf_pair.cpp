@@ -503,20 +503,23 @@ struct TransformerPair : ModelPair {
                     const int r = eng->active[a];
                     const int L = eng->len[r];
                     const int from = std::min(dkv_len[r], L - 1);
-                    if (bt.M() + (L - from) > w.Mcap) {
-                        if (bt.M() == 0) throw std::runtime_error("drafter catch-up exceeds workspace");
-                        break;
-                    }
+                    const int room = w.Mcap - bt.M();
+                    if (room <= 0) break;
+                    // a catch-up longer than the workspace (the first spec cycle at an 8K context)
+                    // runs in consecutive chunks: each chunk's rows attend to the drafter keys the
+                    // previous chunks stored, so the result is the same as one pass
+                    const int to = std::min(L, from + room);
                     const int r0 = bt.M();
-                    for (int p = from; p < L; ++p) bt.rows.push_back(RowDesc{r, p, p, 0, -1, 0, 0, 0});
+                    for (int p = from; p < to; ++p) bt.rows.push_back(RowDesc{r, p, p, 0, -1, 0, 0, 0});
                     bt.add_items(r0, bt.M(), per_item_t, -1, 0, 0, 0);
+                    dkv_len[r] = to;
+                    if (to < L) break;  // batch full mid-request: continue it in the next batch
                     head_src.push_back(bt.M() - 1);
                     head_dst.push_back(a * d.slots);
                     for (int i = 0; i < d.t; ++i) {
                         hid_src.push_back(bt.M() - 1);
                         hid_dst.push_back(r * d.t_max + i);
                     }
-                    dkv_len[r] = L;
                 }
                 bt.map_a = head_src;
                 bt.map_b = head_dst;

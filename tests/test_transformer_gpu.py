@@ -216,3 +216,23 @@ def test_step_tokens_match_responses(models):
             got[rid].extend(toks)
     for r in eng.requests():
         assert got[r.id] == r.generated
+
+
+def test_catch_up_longer_than_workspace(models):
+    """A drafter catch-up longer than the forward workspace (2048 rows) -- the first spec cycle
+    at an 8K context (cfg4) -- runs in consecutive chunks; greedy SD still equals greedy decode."""
+    tgt, drf = models
+    big = rb.TransformerShape.tiny(vocab=1024, max_ctx=2400)
+    t2 = rb.TransformerModel(big, seed=11)
+    d2 = rb.EagleDrafter(t2, seed=12)
+    rng = random.Random(9)
+    prompts = [[rng.randrange(1023) for _ in range(2200 + 37 * i)] for i in range(2)]
+
+    def gen(cfg):
+        reqs = [rb.RequestState(i, list(p), -2.0, 8, rb.DecodeRng.from_seed(5, i)) for i, p in enumerate(prompts)]
+        e = rb.BatchEngine(t2, lambda: d2, None, rb.TimingModel(), reqs, cfg, "greedy", record_full_logprobs=False)
+        while not e.all_done():
+            e.step()
+        return [r.generated for r in e.requests()]
+
+    assert gen(rb.SDConfig.tree(1, 2, 2)) == gen(rb.SDConfig.off())
