@@ -938,9 +938,6 @@ int rs_set_tuning(const char *key, int64_t value) {
             rs::tuning().gemm2 = static_cast<int>(value);
         } else if (k == "pdl") {
             rs::tuning().pdl = static_cast<int>(value);
-        } else if (k == "gemm_mc") {
-            if (value != 0 && value != -1 && value != 2) throw std::invalid_argument("gemm_mc must be 0, -1 or 2");
-            rs::tuning().gemm_mc = static_cast<int>(value);
         } else if (k == "kd_rows") {
             if (value < 0) throw std::invalid_argument("kd_rows must be >= 0");
             rs::tuning().kd_rows = static_cast<int>(value);

@@ -39,7 +39,6 @@ Tuning &tuning() {
                     else if (k == "fused_stats") x.fused_stats = v;
                     else if (k == "attn_tc") x.attn_tc = v;
                     else if (k == "attn_trace") x.attn_trace = v;
-                    else if (k == "gemm_mc") x.gemm_mc = v;
                     else if (k == "pdl") x.pdl = v;
                     else if (k == "gemm2") x.gemm2 = v;
                     else if (k == "gemm_trace") x.gemm_trace = v;

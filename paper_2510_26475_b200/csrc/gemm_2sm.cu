@@ -22,7 +22,6 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
-#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <mutex>
@@ -69,16 +68,6 @@ __device__ __forceinline__ void tma_load_2sm(void *dst, const CUtensorMap *map, 
         "l"(map), "r"(bar_cluster), "r"(x), "r"(y)
         : "memory");
 }
-// The same 2-SM load multicast to the CTAs in `mask` (the same-rank CTAs of the cluster's
-// pairs); each destination's complete_tx lands on ITS pair leader's barrier at this offset.
-__device__ __forceinline__ void tma_load_2sm_mc(void *dst, const CUtensorMap *map, uint32_t bar_cluster, int x, int y,
-                                                uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
-        "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(bar_cluster), "r"(x), "r"(y), "h"(mask)
-        : "memory");
-}
 __device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -87,11 +76,11 @@ __device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t adesc, uint64_
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
 // arrive on the barrier at the same offset in both CTAs of the pair once prior MMAs are done
-__device__ __forceinline__ void tc_commit2_mc(uint64_t *bar, uint16_t mask = 3) {
+__device__ __forceinline__ void tc_commit2_mc(uint64_t *bar) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
             smem_u32(bar)),
-        "h"(mask)
+        "h"((uint16_t)3)
         : "memory");
 }
 
@@ -295,14 +284,8 @@ __device__ __forceinline__ void epi2_qkv_rope(const GemmEpi &ep, uint32_t taddr,
 
 // F = features (rows of W), T = tokens (rows of X). Units = (feature pair-tile, token tile, split),
 // token tiles fastest so the pairs that share a weight tile run together (one HBM read).
-// MC = SM pairs per cluster sharing each weight tile: with MC = 2 the cluster's two pairs compute
-// consecutive token tiles of the same 256 features, and every weight k-block is fetched ONCE
-// for both -- each CTA loads 64 of its pair-rank's 128 weight rows and multicasts them to its
-// counterpart in the other pair -- halving the L2 -> SM weight traffic per k-block. A stage
-// may be refilled only when both pairs have consumed it (empty barriers count one commit per
-// pair). Token tiles past the end (an odd count) run on zero-filled rows and store nothing.
-template <int BT, int EPI, int MC>
-__global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2 * MC, 1, 1)
+template <int BT, int EPI>
+__global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmEpi ep, int F,
                  int T, int K, int splits, int *sem, float *ws, long long *g2trace, int g2slot) {
     using C = Cfg2<BT>;
@@ -322,27 +305,19 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2 * MC, 1, 1)
     pdl_trigger();
     if (g2trace && blockIdx.x == 0 && threadIdx.x == 0) g2trace[g2slot * 8 + 0] = clock64();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t crank = cluster_rank();
-    const uint32_t rank = crank & 1;           // rank within the SM pair
-    const uint32_t p2 = crank >> 1;            // pair within the cluster (MC = 2)
+    const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
-    // a "pair" below iterates cluster units: both pairs of a cluster walk the same sequence
-    const int pair = blockIdx.x / (2 * MC), npairs = gridDim.x / (2 * MC);
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     const int num_f = (F + 2 * kBM - 1) / (2 * kBM), num_t = (T + BT - 1) / BT;
-    const int num_tc = (num_t + MC - 1) / MC;  // token-tile groups (one tile per pair)
     const int num_k = (K + kBK - 1) / kBK;
-    const int num_units = num_f * num_tc * splits;
+    const int num_units = num_f * num_t * splits;
     auto unit_coords = [&](int unit, int &f0, int &t0, int &kb0, int &kb1) {
         const int split = unit % splits, tile = unit / splits;
-        f0 = (tile / num_tc) * 2 * kBM + rank * kBM;
-        t0 = ((tile % num_tc) * MC + (int)p2) * BT;
+        f0 = (tile / num_t) * 2 * kBM + rank * kBM;
+        t0 = (tile % num_t) * BT;
         kb0 = split * num_k / splits;
         kb1 = (split + 1) * num_k / splits;
     };
-    constexpr uint16_t kPairMask = 3;
-    const uint16_t pair_mask = (uint16_t)(kPairMask << (2 * p2));
-    const uint16_t all_mask = (uint16_t)((1u << (2 * MC)) - 1);
-    const uint16_t w_mask = (uint16_t)((1u << rank) | (MC == 2 ? (1u << (2 + rank)) : 0u));
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
@@ -351,7 +326,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2 * MC, 1, 1)
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < C::kStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], MC);  // one MMA commit per pair reading this CTA's weight rows
+            mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
@@ -371,17 +346,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2 * MC, 1, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            const uint32_t lead_full = mapa(full, crank & ~1u);  // full[0] of this pair's leader; stage s at + 8 s
-            // weight rows of this CTA's load: all 128 (MC = 1) or its 64-row half of the pair-rank's
-            // 128, multicast to the same rank of the other pair (MC = 2)
-            auto load_w = [&](int stg, int kb, int f0) {
-                if constexpr (MC == 1) {
-                    tma_load_2sm(sA + stg * C::kABytes, &tmW, lead_full + 8 * stg, kb * kBK, f0);
-                } else {
-                    tma_load_2sm_mc(sA + stg * C::kABytes + p2 * (kBM / 2) * 128, &tmW, lead_full + 8 * stg, kb * kBK,
-                                    f0 + (int)p2 * (kBM / 2), w_mask);
-                }
-            };
+            const uint32_t lead_full = mapa(full, 0);  // full[0] of the leader; stage s at + 8 s
             // weights do not depend on the previous kernel: the first ring's worth of W k-blocks
             // goes out before the programmatic-dependency wait, the token rows after it
             int pre = 0;
@@ -391,7 +356,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2 * MC, 1, 1)
                 pre = min(C::kStages, kb1 - kb0);
                 for (int i = 0; i < pre; ++i) {
                     if (leader) mbar_arrive_expect_tx(&full[i], 2 * C::kStageBytes);
-                    load_w(i, kb0 + i, f0);
+                    tma_load_2sm(sA + i * C::kABytes, &tmW, lead_full + 8 * i, (kb0 + i) * kBK, f0);
                 }
             }
             pdl_wait();
@@ -407,7 +372,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2 * MC, 1, 1)
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (issued >= pre) {
                         if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
-                        load_w(stage, kb, f0);
+                        tma_load_2sm(sA + stage * C::kABytes, &tmW, lead_full + 8 * stage, kb * kBK, f0);
                     }
                     tma_load_2sm(sB + stage * C::kBBytes, &tmX, lead_full + 8 * stage, kb * kBK, tb);
                     if (++stage == C::kStages) {
@@ -438,13 +403,13 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2 * MC, 1, 1)
 #pragma unroll
                     for (int k = 0; k < kBK / 16; ++k)
                         tc_mma2(tmem_d, ad + 2 * k, bd + 2 * k, C::kIdesc, (kb != kb0) || k != 0);
-                    tc_commit2_mc(&empty[stage], all_mask);  // both pairs' CTAs: the stage's weight halves
+                    tc_commit2_mc(&empty[stage]);
                     if (++stage == C::kStages) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                tc_commit2_mc(&tfull[acc], pair_mask);
+                tc_commit2_mc(&tfull[acc]);
                 if (g2trace && blockIdx.x == 0 && it == 0) g2trace[g2slot * 8 + 3] = clock64();
             }
         }
@@ -454,7 +419,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2 * MC, 1, 1)
         const int grp = (warp - 4) >> 2;  // chunk parity of this warp's group
         const int ebar = 2 + grp;         // named barrier of the group (QKV epilogue)
         float(*stg_grp)[33] = stg_all + grp * 4 * 32;
-        const uint32_t lead_tempty = mapa(tempty, crank & ~1u);
+        const uint32_t lead_tempty = mapa(tempty, 0);
         int it = 0;
         for (int unit = pair; unit < num_units; unit += npairs, ++it) {
             int f0, t0, kb0, kb1;
@@ -584,22 +549,20 @@ int num_sms2() {
     return n;
 }
 
-template <int BT, int EPI, int MC>
+template <int BT, int EPI>
 void launch2(const GemmArgs &g, cudaStream_t st) {
     using C = Cfg2<BT>;
     static const bool attr = [] {  // thread-safe one-time init (engine + learner threads)
-        RS_CUDA(cudaFuncSetAttribute(gemm2_kernel<BT, EPI, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+        RS_CUDA(cudaFuncSetAttribute(gemm2_kernel<BT, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
         return true;
     }();
     (void)attr;
     const int F = g.N, T = g.M;
-    const CUtensorMap tw = make_tma_map_bf16(g.B, F, g.K, g.ldb, kBM / MC);
+    const CUtensorMap tw = make_tma_map_bf16(g.B, F, g.K, g.ldb, kBM);
     const CUtensorMap tx = make_tma_map_bf16(g.A, T, g.K, g.lda, BT / 2);
     const int tiles = ((F + 2 * kBM - 1) / (2 * kBM)) * ((T + BT - 1) / BT);
-    const int ctiles = ((F + 2 * kBM - 1) / (2 * kBM)) * ((T + BT * MC - 1) / (BT * MC));
     const int num_k = (g.K + kBK - 1) / kBK;
     const int splits = EPI == kEpiResidual ? std::max(1, std::min(gemm2_splits(g), num_k)) : 1;
-    if (MC > 1 && splits > 1) throw std::invalid_argument("gemm2: weight multicast with split-K");
     int *sem = nullptr;
     float *ws = nullptr;
     if (splits > 1) {
@@ -624,28 +587,14 @@ void launch2(const GemmArgs &g, cudaStream_t st) {
         sem = sems;
         ws = wsb;
     }
-    // clusters of 4 need 4 free SMs of one GPC: fewer than sms / 4 fit at once, so the
-    // persistent grid is capped at the co-resident count (no straggler wave)
-    static const int max_clusters = [] {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(2 * MC * 128);
-        cfg.blockDim = dim3(kThr);
-        cfg.dynamicSmemBytes = C::kSmem;
-        int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, gemm2_kernel<BT, EPI, MC>, &cfg) != cudaSuccess || n <= 0) {
-            cudaGetLastError();
-            n = num_sms2() / (2 * MC);
-        }
-        return n;
-    }();
-    const int clusters = std::min({ctiles * splits, num_sms2() / (2 * MC), max_clusters});
+    const int pairs = std::min(tiles * splits, num_sms2() / 2);
     // diagnostics (RS_TUNE gemm_trace=1): per launch of CTA 0: start, after the dependency wait,
     // first full stage, last MMA commit of tile 0, epilogue start / end of tile 0, exit
     static long long *tr = nullptr;
     static int slot = 0;
     if (tuning().gemm_trace && !tr) RS_CUDA(cudaMalloc(&tr, 8 * 8 * 4096));
-    launch_pdl(gemm2_kernel<BT, EPI, MC>, dim3(2 * MC * clusters), kThr, C::kSmem, st, tw, tx, g.epi, F, T, g.K, splits,
-               sem, ws, tuning().gemm_trace ? tr : (long long *)nullptr, slot);
+    launch_pdl(gemm2_kernel<BT, EPI>, dim3(2 * pairs), kThr, C::kSmem, st, tw, tx, g.epi, F, T, g.K, splits, sem, ws,
+               tuning().gemm_trace ? tr : (long long *)nullptr, slot);
     if (tuning().gemm_trace) {
         RS_CUDA(cudaStreamSynchronize(st));
         long long h[8];
@@ -660,60 +609,31 @@ void launch2(const GemmArgs &g, cudaStream_t st) {
 
 }  // namespace
 
-// Co-resident clusters of two SM pairs (one representative instantiation; every MC = 2
-// instantiation has the same block size and ~the same shared-memory footprint).
-int gemm2_mc_clusters(int fallback) {
-    static const int n = [fallback] {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(4 * 128);
-        cfg.blockDim = dim3(kThr);
-        cfg.dynamicSmemBytes = Cfg2<192>::kSmem;
-        RS_CUDA(cudaFuncSetAttribute(gemm2_kernel<192, kEpiResidual, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     Cfg2<192>::kSmem));
-        int v = 0;
-        if (cudaOccupancyMaxActiveClusters(&v, gemm2_kernel<192, kEpiResidual, 2>, &cfg) != cudaSuccess || v <= 0) {
-            cudaGetLastError();
-            v = fallback;
-        }
-        return v;
-    }();
-    return n;
-}
-
 bool gemm2_supported(const GemmArgs &g) {
     return g.K % 8 == 0 && g.lda % 8 == 0 && g.ldb % 8 == 0 && g.epi.stats == nullptr && g.M > 0 && g.N > 0 &&
            g.epi.kind != kEpiSwiGLU;
 }
 
-// Token tile and weight multicast: the (BT, MC) of {256 .. 64} x {1, 2} with the least modelled
-// time for one (features, tokens, splits) problem -- waves of clusters x k-blocks per unit x
-// cycles per k-block, where a k-block costs max(tensor time, per-SM operand traffic at ~58 B/clk;
-// MC = 2 halves the weight bytes) -- plus a fixed charge per extra split. Neither choice changes
-// a token's arithmetic (token-tile invariance; multicast only moves the same bytes), only the
-// schedule. RS_TUNE gemm_mc=-1 / 2 forces MC = 1 / 2.
-int gemm2_mc_clusters(int fallback);
-void gemm2_pick(int F, int T, int K, int splits, int sms, int &bt_out, int &mc_out) {
+// Token tile: the BT of {256 .. 64} with the least modelled time for the unit count of one
+// (features, tokens, splits) problem -- waves of SM pairs x k-blocks per unit x cycles per
+// k-block, where a k-block costs max(tensor time, per-SM operand traffic at ~58 B/clk) -- plus
+// a fixed charge per extra split. The result never changes a token's arithmetic (token-tile
+// invariance), only the schedule.
+int gemm2_pick_bt(int F, int T, int K, int splits, int sms) {
     const int pairs = sms / 2, nf = (F + 255) / 256, nk = (K + 63) / 64;
-    const int force = tuning().gemm_mc;
     double best = 1e30;
-    bt_out = 256;
-    mc_out = 1;
-    for (int mc : {1, 2}) {
-        if (mc == 2 && (splits > 1 || force < 0)) continue;
-        if (mc == 1 && force == 2 && splits == 1) continue;
-        for (int cand : {256, 224, 192, 160, 128, 96, 64}) {
-            if (mc == 2 && cand < 128) continue;  // instantiated for BT >= 128
-            const double units = (double)nf * ((T + cand * mc - 1) / (cand * mc)) * splits;
-            const double waves = std::ceil(units / (mc == 2 ? gemm2_mc_clusters(pairs / 2) : pairs));
-            const double per_kb = std::max(2.12 * cand, (16384.0 / mc + 64.0 * cand) / 58.0);
-            const double cost = waves * std::ceil((double)nk / splits) * per_kb + (splits - 1) * 2000.0;
-            if (cost < best * 0.999) {
-                best = cost;
-                bt_out = cand;
-                mc_out = mc;
-            }
+    int bt = 256;
+    for (int cand : {256, 224, 192, 160, 128, 96, 64}) {
+        const double units = (double)nf * ((T + cand - 1) / cand) * splits;
+        const double waves = std::ceil(units / pairs);
+        const double per_kb = std::max(2.12 * cand, (16384.0 + 64.0 * cand) / 58.0);
+        const double cost = waves * std::ceil((double)nk / splits) * per_kb + (splits - 1) * 2000.0;
+        if (cost < best * 0.999) {
+            best = cost;
+            bt = cand;
         }
     }
+    return bt;
 }
 
 // Split-K for the residual epilogue is a function of (F, K) only -- never of the token count --
@@ -729,33 +649,17 @@ int gemm2_splits(const GemmArgs &g) {
 
 void gemm2_bf16(const GemmArgs &g, cudaStream_t st) {
     const int splits = gemm2_splits(g);
-    int bt = 0, mc = 1;
-    gemm2_pick(g.N, g.M, g.K, splits, num_sms2(), bt, mc);
-    if (g.block_n) {  // explicit token tile: multicast only when forced and instantiated
-        bt = g.block_n;
-        mc = tuning().gemm_mc == 2 && splits == 1 && bt >= 128 ? 2 : 1;
-    }
+    const int bt = g.block_n ? g.block_n : gemm2_pick_bt(g.N, g.M, g.K, splits, num_sms2());
     auto by_bt = [&](auto tag) {
         constexpr int E = decltype(tag)::value;
-        if (mc == 2) {
-            switch (bt) {
-                case 128: launch2<128, E, 2>(g, st); break;
-                case 160: launch2<160, E, 2>(g, st); break;
-                case 192: launch2<192, E, 2>(g, st); break;
-                case 224: launch2<224, E, 2>(g, st); break;
-                case 256: launch2<256, E, 2>(g, st); break;
-                default: throw std::invalid_argument("gemm2: multicast token tile must be 128..256");
-            }
-            return;
-        }
         switch (bt) {
-            case 64: launch2<64, E, 1>(g, st); break;
-            case 96: launch2<96, E, 1>(g, st); break;
-            case 128: launch2<128, E, 1>(g, st); break;
-            case 160: launch2<160, E, 1>(g, st); break;
-            case 192: launch2<192, E, 1>(g, st); break;
-            case 224: launch2<224, E, 1>(g, st); break;
-            case 256: launch2<256, E, 1>(g, st); break;
+            case 64: launch2<64, E>(g, st); break;
+            case 96: launch2<96, E>(g, st); break;
+            case 128: launch2<128, E>(g, st); break;
+            case 160: launch2<160, E>(g, st); break;
+            case 192: launch2<192, E>(g, st); break;
+            case 224: launch2<224, E>(g, st); break;
+            case 256: launch2<256, E>(g, st); break;
             default: throw std::invalid_argument("gemm2: token tile must be 64..256 in steps of 32");
         }
     };

@@ -240,30 +240,3 @@ def test_gemm_split_k_on_sm_pairs(gemm_path):
     assert (o3 - ref).abs().max().item() <= 2e-3 * ref.abs().max().item()
     assert (o1 - ref).abs().max().item() <= 2e-3 * ref.abs().max().item()
 
-
-@pytest.mark.parametrize("epi,M,N,K", [(2, 1344, 2048, 11008), (2, 1344, 2048, 2048), (0, 1344, 2560, 2048),
-                                       (4, 1344, 22016, 2048), (1, 301, 151936 // 16, 2048), (2, 77, 2048, 4096)])
-def test_weight_multicast_is_bitwise_identical(epi, M, N, K):
-    """Sharing each weight k-block between the two SM pairs of a 4-CTA cluster (TMA multicast)
-    only moves the same bytes: outputs are bitwise those of the one-pair schedule at every token
-    tile (odd token-tile counts run a zero-filled tail tile that stores nothing)."""
-    torch.manual_seed(M + N)
-    A = torch.randn(M, K, device="cuda").bfloat16()
-    B = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
-    bias = (torch.randn(N, device="cuda") * 0.1).bfloat16() if epi == 0 else None
-    R = torch.randn(M, N if epi != 4 else N // 2, device="cuda")
-
-    def run(mc, bn):
-        if epi == 0 or epi == 4:
-            out = torch.empty(M, N if epi == 0 else N // 2, device="cuda", dtype=torch.bfloat16)
-        else:
-            out = R.clone()
-        rb.set_tuning("gemm_mc", mc)
-        try:
-            _run(A, B, out, bias, epi, 1.0, bn)
-        finally:
-            rb.set_tuning("gemm_mc", 0)
-        return out
-
-    for bn in (128, 160, 192, 224, 256):
-        assert torch.equal(run(-1, bn), run(2, bn)), bn
