@@ -1,6 +1,6 @@
 """SM-pair GEMM at the verify shapes (Qwen2.5-3B, M = tokens per round) per token tile, next to
 cuBLAS (torch.matmul, warmed up). Each GEMM runs 20x back to back (weights L2-warm except the
-LM head). Usage: python tools/gemm_mc_bench.py [M]"""
+LM head). Usage: python tools/gemm_cublas_bench.py [M]"""
 import ctypes
 import json
 import os
