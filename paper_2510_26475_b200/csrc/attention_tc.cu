@@ -19,10 +19,12 @@
 //               TMEM and O_i += P_i V (TS: P read from TMEM where it overwrote S_i, V as an
 //               MN-major smem operand), ping-ponging the two M-tiles so one tile's softmax
 //               overlaps the other tile's MMAs;
-//   warps 4-7 / 8-11  softmax of M-tile 0 / 1: one thread per row reads S from TMEM
-//               (tcgen05.ld), online softmax in the exp2 domain, writes P as bf16 back into
-//               TMEM (tcgen05.st), rescales O in TMEM when the running max moves, and finally
-//               writes O / l as bf16.
+//   warps 4-7 / 8-11  softmax of M-tile 0 / 1: one thread per row (its TMEM lane) reads the
+//               row's 128 scores of S (tcgen05.ld), online softmax in the exp2 domain, writes P as
+//               bf16 back into TMEM (tcgen05.st), rescales O in TMEM when the running max moves,
+//               and finally writes O / l as bf16. One thread owns the whole row, so the row max
+//               needs no cross-warp exchange (measured: the two-threads-per-row variant spent
+//               ~340 of its ~1.9K cycles per pass in that exchange).
 // TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512) columns.
 #include <cstdio>
 #include <cuda.h>
@@ -49,7 +51,7 @@ constexpr int kQBytes = 2 * kTileBytes;        // two M-tiles
 constexpr int kMaxPasses = kAttnMaxPasses;
 constexpr int kMaxGroups = kAttnMaxGroups;
 constexpr int kMaxTok = 256;
-constexpr int kThreads = 640;  // 4 control warps + 2 x 8 softmax warps
+constexpr int kThreads = 384;  // 4 control warps + 2 x 4 softmax warps
 constexpr uint32_t kIdescS = (1u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
 constexpr uint32_t kIdescPV = kIdescS | (1u << 16);  // B (= V) is MN-major
 
@@ -61,7 +63,6 @@ struct Plan {
     short tok_grp[kMaxTok];
     int tok_pos[kMaxTok];
     Pass pass[kMaxPasses];
-    float xch[2 * 4 * 2 * 32];  // softmax pair exchange [tile][quadrant][half][lane]
 };
 
 constexpr int kBarBytes = 256;
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], 8);
+            mbar_init(&p_full[i], 4);  // the tile's four softmax warps
         }
         mbar_init(o_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -151,19 +152,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
     }
     pdl_wait();  // Q and the K/V cache come from the previous kernel (RoPE / KV store)
-    // ---- Q tiles -> smem (softmax warps: half a row each, zero rows beyond the item) ----------
+    // ---- Q tiles -> smem (softmax warps: one row each, zero rows beyond the item) -------------
     if (warp >= 4) {
         const int T0 = 128 / G;
-        const int tile = (warp - 4) >> 3, half = ((warp - 4) >> 2) & 1, r = (warp & 3) * 32 + lane;
+        const int tile = (warp - 4) >> 2, r = (warp & 3) * 32 + lane;
         const int k = tile * T0 + r / G;
         const bool valid = r < T0 * G && k < it.nrows;
         uint8_t *base = sQ + tile * kTileBytes;
-        const bf16 *src = q + ((size_t)(it.row0 + k) * H + kvh * G + r % G) * kHD + half * 64;
-        int4 v[8];
+        const bf16 *src = q + ((size_t)(it.row0 + k) * H + kvh * G + r % G) * kHD;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) v[c] = valid ? *reinterpret_cast<const int4 *>(src + c * 8) : make_int4(0, 0, 0, 0);
+        for (int h = 0; h < 2; ++h) {
+            int4 v[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) *reinterpret_cast<int4 *>(base + swz_off(r, half * 8 + c)) = v[c];
+            for (int c = 0; c < 8; ++c)
+                v[c] = valid ? *reinterpret_cast<const int4 *>(src + h * 64 + c * 8) : make_int4(0, 0, 0, 0);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) *reinterpret_cast<int4 *>(base + swz_off(r, h * 8 + c)) = v[c];
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     const int T = 128 / G;
@@ -283,14 +288,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_commit(o_done);
         }
     } else if (warp >= 4) {
-        // ---- softmax: two threads per row of M-tile `tile` (column halves) --------------------
-        // Per pass: one TMEM read of the thread's 64 scores, the row max combined with the
-        // partner thread (same TMEM lane, other half) through shared memory, p = 2^(s*scale - m)
-        // written as bf16 over the consumed S columns. The running max m only moves when the
-        // chunk max exceeds it by more than 2^8 (so p <= 256): O in TMEM is then rescaled. Row
-        // sums are kept as 8 interleaved partials per half. Every choice depends only on the
-        // row's own scores, so the arithmetic is identical whatever item the row sits in.
-        const int tile = (warp - 4) >> 3, half = ((warp - 4) >> 2) & 1, qd = warp & 3;
+        // ---- softmax: one thread per row of M-tile `tile` ----------------------------------------
+        // Per pass: one TMEM read of the row's 128 scores, the row max, p = 2^(s*scale - m) written
+        // as bf16 over the consumed S columns (the 64-column halves [64h, 64h + 64) into S columns
+        // [32h, 32h + 32)). The running max m only moves when the chunk max exceeds it by more
+        // than 2^8 (so p <= 256): O in TMEM is then rescaled. Row sums are kept as 8 interleaved
+        // partials per 64-column half. Every choice depends only on the row's own scores, so the
+        // arithmetic is identical whatever item the row sits in.
+        const int tile = (warp - 4) >> 2, qd = warp & 3;
         const int r = qd * 32 + lane;
         const int k = tile * T + r / G;
         const bool valid = r < T * G && k < pl.ntok;
@@ -298,13 +303,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int pos = valid ? pl.tok_pos[k] : -1;
         const int grp = valid ? pl.tok_grp[k] : -2;
         const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-        const uint32_t tS = tmem + lane_off + tile * 128, tO = tmem + lane_off + 256 + tile * 128 + half * 64;
-        float *xch = reinterpret_cast<float *>(pl.xch) + ((tile * 4 + qd) * 2) * 32;  // [half][lane]
-        const int bar_id = 2 + tile * 4 + qd;
+        const uint32_t tS = tmem + lane_off + tile * 128, tO = tmem + lane_off + 256 + tile * 128;
         float m = -INFINITY;
-        float lp[8];
+        float lp[2][8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) lp[i] = 0.f;
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) lp[h][i] = 0.f;
         int n = 0;
         for (int j = 0; j < np; ++j) {
             const Pass ps = pl.pass[j];
@@ -313,33 +318,36 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool trs = tr && tile == 0 && warp == 4 && lane == 0;
             if (trs) trace[4 + 8 * j] = clock64();
             tc_fence_after();
-            const int c0 = ps.chunk * kCk + half * 64;
+            const int c0 = ps.chunk * kCk;
             const bool mine = valid && (ps.grp < 0 || ps.grp == grp);
             const int lim = mine ? pos - c0 : -1;  // own columns x <= lim are visible
-            // both halves of a pair see the same rows, so this branch is pair-uniform
             if (warp_valid) {
-                uint32_t v[64];
-                tmem_ld32_nw(tS + half * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
-                tmem_ld32_nw(tS + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+                uint32_t v[128];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld32_nw(tS + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
                 tmem_ld_wait();
                 if (trs) trace[5 + 8 * j] = clock64();
-                float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-                if (lim >= 63) {
+                float mxh[2];
 #pragma unroll
-                    for (int x = 0; x < 64; x += 4) {
-                        mx0 = fmaxf(mx0, __uint_as_float(v[x]));
-                        mx1 = fmaxf(mx1, __uint_as_float(v[x + 1]));
-                        mx2 = fmaxf(mx2, __uint_as_float(v[x + 2]));
-                        mx3 = fmaxf(mx3, __uint_as_float(v[x + 3]));
+                for (int h = 0; h < 2; ++h) {
+                    const int lh = lim - 64 * h;
+                    float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+                    if (lh >= 63) {
+#pragma unroll
+                        for (int x = 0; x < 64; x += 4) {
+                            mx0 = fmaxf(mx0, __uint_as_float(v[64 * h + x]));
+                            mx1 = fmaxf(mx1, __uint_as_float(v[64 * h + x + 1]));
+                            mx2 = fmaxf(mx2, __uint_as_float(v[64 * h + x + 2]));
+                            mx3 = fmaxf(mx3, __uint_as_float(v[64 * h + x + 3]));
+                        }
+                    } else {
+#pragma unroll
+                        for (int x = 0; x < 64; ++x)
+                            if (x <= lh) mx0 = fmaxf(mx0, __uint_as_float(v[64 * h + x]));
                     }
-                } else {
-#pragma unroll
-                    for (int x = 0; x < 64; ++x)
-                        if (x <= lim) mx0 = fmaxf(mx0, __uint_as_float(v[x]));
+                    mxh[h] = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
                 }
-                xch[half * 32 + lane] = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-                asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");  // both halves loaded S
-                float mx = fmaxf(xch[lane], xch[32 + lane]);
+                float mx = fmaxf(mxh[0], mxh[1]);
                 if (trs) trace[6 + 8 * j] = clock64();
                 mx = mx == -INFINITY ? mx : mx * scale_log2;  // scale > 0: max commutes with it
                 bool resc = false;
@@ -352,31 +360,37 @@ __global__ void __launch_bounds__(kThreads, 1)
                         m = mx;
                         resc = true;
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) lp[i] *= alpha;
+                        for (int h = 0; h < 2; ++h)
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) lp[h][i] *= alpha;
                     }
                 }
                 const float nb = m == -INFINITY ? 0.f : -m;
-                uint32_t pk[32];
-                const bool all = lim >= 63;
 #pragma unroll
-                for (int x = 0; x < 64; x += 2) {
-                    float p0 = ex2(fmaf(__uint_as_float(v[x]), scale_log2, nb));
-                    float p1 = ex2(fmaf(__uint_as_float(v[x + 1]), scale_log2, nb));
-                    if (!all) {
-                        p0 = x <= lim ? p0 : 0.f;
-                        p1 = x + 1 <= lim ? p1 : 0.f;
+                for (int h = 0; h < 2; ++h) {
+                    const int lh = lim - 64 * h;
+                    const bool all = lh >= 63;
+                    uint32_t pk[32];
+#pragma unroll
+                    for (int x = 0; x < 64; x += 2) {
+                        float p0 = ex2(fmaf(__uint_as_float(v[64 * h + x]), scale_log2, nb));
+                        float p1 = ex2(fmaf(__uint_as_float(v[64 * h + x + 1]), scale_log2, nb));
+                        if (!all) {
+                            p0 = x <= lh ? p0 : 0.f;
+                            p1 = x + 1 <= lh ? p1 : 0.f;
+                        }
+                        lp[h][x & 7] += p0;
+                        lp[h][(x + 1) & 7] += p1;
+                        pk[x >> 1] = pack_bf16(p0, p1);
                     }
-                    lp[x & 7] += p0;
-                    lp[(x + 1) & 7] += p1;
-                    pk[x >> 1] = pack_bf16(p0, p1);
+                    // P (bf16) of this half over S columns [32 h, 32 h + 32), already read
+                    tmem_st16(tS + h * 32, *reinterpret_cast<uint32_t(*)[16]>(pk));
+                    tmem_st16(tS + h * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(pk + 16));
                 }
                 if (trs) trace[7 + 8 * j] = clock64();
-                // P (bf16) of this half over S columns [32 half, 32 half + 32), already read by both
-                tmem_st16(tS + half * 32, *reinterpret_cast<uint32_t(*)[16]>(pk));
-                tmem_st16(tS + half * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(pk + 16));
                 if (n > 0 && __any_sync(0xffffffffu, resc)) {
 #pragma unroll 1
-                    for (int cc = 0; cc < 2; ++cc) {
+                    for (int cc = 0; cc < 4; ++cc) {
                         uint32_t o[32];
                         tmem_ld32(tO + cc * 32, o);
 #pragma unroll
@@ -393,19 +407,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++n;
         }
         if (n > 0 && warp_valid) {
-            float lh = ((lp[0] + lp[1]) + (lp[2] + lp[3])) + ((lp[4] + lp[5]) + (lp[6] + lp[7]));
-            // the partner half may still be reading the last pass's maxima from xch: no pass
-            // follows to order it through the S / P barriers, so the pair syncs before reuse
-            asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-            xch[half * 32 + lane] = lh;
-            asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-            const float l = xch[lane] + xch[32 + lane];
+            const float lh0 = ((lp[0][0] + lp[0][1]) + (lp[0][2] + lp[0][3])) + ((lp[0][4] + lp[0][5]) + (lp[0][6] + lp[0][7]));
+            const float lh1 = ((lp[1][0] + lp[1][1]) + (lp[1][2] + lp[1][3])) + ((lp[1][4] + lp[1][5]) + (lp[1][6] + lp[1][7]));
+            const float l = lh0 + lh1;
             mbar_wait(o_done, 0);
             tc_fence_after();
             const float inv = l > 0.f ? 1.f / l : 0.f;
-            bf16 *dst = out + ((size_t)(it.row0 + (valid ? k : 0)) * H + kvh * G + r % G) * kHD + half * 64;
+            bf16 *dst = out + ((size_t)(it.row0 + (valid ? k : 0)) * H + kvh * G + r % G) * kHD;
 #pragma unroll 1
-            for (int cc = 0; cc < 2; ++cc) {
+            for (int cc = 0; cc < 4; ++cc) {
                 uint32_t o[32];
                 tmem_ld32(tO + cc * 32, o);
                 if (valid) {
