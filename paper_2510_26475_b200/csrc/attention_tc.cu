@@ -193,12 +193,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int y = (int)(kvrow0 + ps.chunk * kCk);
                 mbar_wait(&emptyK[s], par);
                 if (t == 0) {
+                    if (tr) trace[9 + 12 * j] = clock64();
                     mbar_arrive_expect_tx(&fullK[s], kTileBytes);
                     tma_load_2d(dst, &tmK, &fullK[s], 0, y);
                     tma_load_2d(dst + kHalfBytes, &tmK, &fullK[s], 64, y);
                 }
                 mbar_wait(&emptyV[s], par);
                 if (t == 0) {
+                    if (tr) trace[10 + 12 * j] = clock64();
                     mbar_arrive_expect_tx(&fullV[s], kTileBytes);
                     tma_load_2d(dst + kTileBytes, &tmV, &fullV[s], 0, y);
                     tma_load_2d(dst + kTileBytes + kHalfBytes, &tmV, &fullV[s], 64, y);
@@ -240,8 +242,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             auto issue_pv = [&](int i) {
                 const int jp = pend[i];
                 mbar_wait(&fullV[jp % kStages], (jp / kStages) & 1);
+                if (tr && i == 0) trace[11 + 12 * jp] = clock64();
                 mbar_wait(&p_full[i], pv_n[i] & 1);
-                if (tr) trace[2 + 8 * jp + i] = clock64();
+                if (tr) trace[2 + 12 * jp + i] = clock64();
                 tc_fence_after();
                 const uint8_t *v = sKV + (jp % kStages) * kStageBytes + kTileBytes;
                 const uint32_t d_o = tmem + 256 + i * 128, a_p = tmem + i * 128;
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (pend[i] >= 0 && pend[i] <= j - kStages) issue_pv(i);
                 const int s = j % kStages;
                 mbar_wait(&fullK[s], (j / kStages) & 1);
-                if (tr) trace[1 + 8 * j] = clock64();
+                if (tr) trace[1 + 12 * j] = clock64();
                 tc_fence_after();
                 const uint8_t *kt = sKV + s * kStageBytes;
                 for (int i = 0; i < 2; ++i) {
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (!(ps.tiles & (1 << tile))) continue;
             mbar_wait(&s_full[tile], n & 1);
             const bool trs = tr && tile == 0 && warp == 4 && lane == 0;
-            if (trs) trace[4 + 8 * j] = clock64();
+            if (trs) trace[4 + 12 * j] = clock64();
             tc_fence_after();
             const int c0 = ps.chunk * kCk;
             const bool mine = valid && (ps.grp < 0 || ps.grp == grp);
@@ -326,7 +329,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) tmem_ld32_nw(tS + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
                 tmem_ld_wait();
-                if (trs) trace[5 + 8 * j] = clock64();
                 float mxh[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -348,7 +350,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mxh[h] = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
                 }
                 float mx = fmaxf(mxh[0], mxh[1]);
-                if (trs) trace[6 + 8 * j] = clock64();
                 mx = mx == -INFINITY ? mx : mx * scale_log2;  // scale > 0: max commutes with it
                 bool resc = false;
                 float alpha = 1.f;
@@ -387,7 +388,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_st16(tS + h * 32, *reinterpret_cast<uint32_t(*)[16]>(pk));
                     tmem_st16(tS + h * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(pk + 16));
                 }
-                if (trs) trace[7 + 8 * j] = clock64();
                 if (n > 0 && __any_sync(0xffffffffu, resc)) {
 #pragma unroll 1
                     for (int cc = 0; cc < 4; ++cc) {
@@ -399,8 +399,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 tmem_st_wait();
-                if (trs) trace[8 + 8 * j] = clock64();
             }
+            if (tr && tile == 0 && lane == 0) trace[5 + (warp - 4) + 12 * j] = clock64();  // this warp's P done
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full[tile]);
@@ -462,20 +462,21 @@ void k_attention_tc(const bf16 *q, const RowDesc *rows, const AttnItem *items, c
     const CUtensorMap tv = make_tma_map_bf16(kv.v, total_rows, kHD, kHD, kCk);
     const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(s.hd));
     static long long *trace = nullptr;
-    if (tuning().attn_trace && !trace) RS_CUDA(cudaMalloc(&trace, 8 * (1 + 8 * kMaxPasses)));
+    if (tuning().attn_trace && !trace) RS_CUDA(cudaMalloc(&trace, 8 * (1 + 12 * kMaxPasses)));
     launch_pdl(attn_tc_kernel, dim3(n_items, s.KV), kThreads, kSmem, st, tk, tv, q, rows, items, plan, kv, layer,
                s.H, s.KV, scale_log2, out, tuning().attn_trace ? trace : nullptr);
     if (tuning().attn_trace) {
         RS_CUDA(cudaStreamSynchronize(st));
-        static long long host[1 + 8 * kMaxPasses];
+        static long long host[1 + 12 * kMaxPasses];
         RS_CUDA(cudaMemcpy(host, trace, sizeof(host), cudaMemcpyDeviceToHost));
         if (tuning().attn_trace == layer + 1 && n_items >= 32) {
             fprintf(stderr, "attn trace layer %d items %d:\n", layer, n_items);
             for (int j = 0; j < 24; ++j) {
-                const long long *h = host + 1 + 8 * j;
-                fprintf(stderr, "  pass %2d fullK %8lld p0 %8lld p1 %8lld sm0 %8lld | ld +%lld xch +%lld exp +%lld st +%lld\n",
-                        j, h[0] - host[0], h[1] - host[0], h[2] - host[0], h[3] - host[0], h[4] - h[3], h[5] - h[4],
-                        h[6] - h[5], h[7] - h[6]);
+                const long long *h = host + 1 + 12 * j;
+                fprintf(stderr, "  pass %2d fullK %6lld p0 %6lld p1 %6lld sm0 %6lld | P done +%lld +%lld +%lld +%lld | "
+                        "issueK %6lld issueV %6lld fullV %6lld\n",
+                        j, h[0] - host[0], h[1] - host[0], h[2] - host[0], h[3] - host[0], h[4] - h[3], h[5] - h[3],
+                        h[6] - h[3], h[7] - h[3], h[8] - host[0], h[9] - host[0], h[10] - host[0]);
             }
         }
     }
