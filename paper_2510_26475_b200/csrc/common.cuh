@@ -48,7 +48,6 @@ const char *dev_err_message(int code);
 // Process-wide tuning knobs set through rs_set_tuning (0 = automatic).
 struct Tuning {
     int accept_cluster = 0;  // CTAs per sequence in the fused acceptance kernel: 0 auto, 1/2/4/8 forced
-    int attn_tc = 0;         // target attention: 0 / 1 tcgen05 kernel, -1 legacy mma.sync kernel
     int fused_stats = 0;     // drafter LM-head stats: 1 fused GEMM epilogue; 0 / -1 separate row-stats kernel
     int attn_trace = 0;      // diagnostics: layer + 1 whose attention pass timeline is printed
     int pdl = 0;             // programmatic dependent launch on the forward path: 0 / 1 on, -1 off

@@ -37,7 +37,6 @@ Tuning &tuning() {
                     const int v = std::atoi(kv.c_str() + eq + 1);
                     if (k == "accept_cluster") x.accept_cluster = v;
                     else if (k == "fused_stats") x.fused_stats = v;
-                    else if (k == "attn_tc") x.attn_tc = v;
                     else if (k == "attn_trace") x.attn_trace = v;
                     else if (k == "pdl") x.pdl = v;
                     else if (k == "gemm2") x.gemm2 = v;

@@ -1,5 +1,5 @@
 // model.h -- Qwen2-shaped target and EAGLE-3-style drafter held in HBM (bf16 weights), and
-// the device kernels of their forwards (model.cu, attention.cu).
+// the device kernels of their forwards (model.cu, attention_tc.cu).
 #pragma once
 #include <cuda_bf16.h>
 
@@ -143,14 +143,7 @@ void k_rmsnorm_bf16(const bf16 *x, int ldx, const float *w, int M, int d, float 
                     cudaStream_t st);
 void k_rope_store(const bf16 *qkv, const RowDesc *rows, int M, const TfShape &s, const float *rope, const KvCache &kv,
                   int layer, bf16 *q, cudaStream_t st);
-// Max tokens per plain attention item for GQA group size G (max warps x 16 rows / G).
-int attn_max_tokens(int G);
-int attn_max_warps();
-// Items: chain -1 = plain causal over the cache; -2 = tree item (groups by RowDesc::chain).
-// flops / bytes: algorithmic work of the launch (profiling only)
-void k_attention(const bf16 *q, const RowDesc *rows, const AttnItem *items, int n_items, const KvCache &kv, int layer,
-                 const TfShape &s, bf16 *out, cudaStream_t st, double flops = 0, double bytes = 0);
-// Target attention on tcgen05/TMEM (attention_tc.cu): same items (chain -1 plain, -2 tree),
+// Target attention on tcgen05/TMEM (attention_tc.cu): items of rows (chain -1 plain causal over the cache, -2 tree),
 // at most attn_tc_max_tokens(G) tokens per item.
 int attn_tc_max_tokens(int G);
 void k_attention_tc(const bf16 *q, const RowDesc *rows, const AttnItem *items, const AttnPlan &plan, int n_items,

@@ -261,28 +261,6 @@ struct Batch {
             items.push_back(AttnItem{rows[a].seq, a, b - a, maxpos, chain, ltree, tbase, nstride});
         }
     }
-    // tree items over rows [r0, r1) of one sequence: groups of consecutive tokens of one chain
-    // (the root joins chain 0), packed into CTAs of at most 16 warps of 16 rows (G rows/token).
-    void add_tree_items(int r0, int r1, int G, int ltree, int tbase, int nstride) {
-        int a = r0, warps = 0, maxpos = 0;
-        int k = r0;
-        while (k < r1) {
-            int ch = rows[k].chain, k1 = k + 1;
-            if (ch < 0 && k1 < r1 && rows[k1].chain == 0) ch = 0;
-            while (k1 < r1 && rows[k1].chain == ch) ++k1;
-            const int gw = ((k1 - k) * G + 15) / 16;
-            if (warps + gw > attn_max_warps() && k > a) {
-                items.push_back(AttnItem{rows[a].seq, a, k - a, maxpos, -2, ltree, tbase, nstride});
-                a = k;
-                warps = 0;
-                maxpos = 0;
-            }
-            warps += gw;
-            for (int j = k; j < k1; ++j) maxpos = std::max(maxpos, rows[j].pos);
-            k = k1;
-        }
-        if (k > a) items.push_back(AttnItem{rows[a].seq, a, k - a, maxpos, -2, ltree, tbase, nstride});
-    }
     // tree items for the tensor-core attention: consecutive runs of at most max_tok tokens (two
     // 128-row M-tiles); the kernel regroups tokens by chain inside an item.
     void add_tree_items_tc(int r0, int r1, int max_tok, int ltree, int tbase, int nstride) {
@@ -315,8 +293,7 @@ struct TransformerPair : ModelPair {
     const DrafterModel *drf = nullptr;
     uint64_t drf_uid = 0;
     TfShape s;
-    int B = 0, slots_max = 1, max_ctx = 0, per_item = 8, per_item_t = 8;
-    bool tc_attn = true;  // target attention on tcgen05 (attention_tc.cu); fixed for the engine's life
+    int B = 0, slots_max = 1, max_ctx = 0, per_item_t = 8;  // per_item_t: tokens per attention item
     KvCache kv_t, kv_d;
     DBuf<bf16> kt, vt, kd, vd, feat;
     DBuf<float> dh;  // drafter hidden per (request, chain) [B][t_max][d]
@@ -352,11 +329,7 @@ struct TransformerPair : ModelPair {
         B = std::max(n_req, 1);
         slots_max = slots;
         max_ctx = s.max_ctx;
-        per_item = attn_max_tokens(s.H / s.KV);
-        tc_attn = tuning().attn_tc >= 0;
-        per_item_t = tc_attn ? attn_tc_max_tokens(s.H / s.KV) : per_item;
-        if (eng && (eng->n_max + 1) * (s.H / s.KV) > 16 * attn_max_warps())
-            throw std::invalid_argument("transformer engine: (draft_len + 1) * GQA group must be <= 192");
+        per_item_t = attn_tc_max_tokens(s.H / s.KV);
         for (int i = 0; i < n_req; ++i)
             if (plen[i] < 1) throw std::invalid_argument("transformer engine: prompts must be non-empty");
         if (tok_cap + slots > max_ctx)
@@ -383,9 +356,9 @@ struct TransformerPair : ModelPair {
         dkv_len.assign(n_req, 0);
     }
 
-    void upload(Batch &b, cudaStream_t st, bool tc_plan = false) {
+    void upload(Batch &b, cudaStream_t st) {
         if (b.M() > w.Mcap) throw std::runtime_error("forward batch exceeds workspace");
-        if (tc_plan) {
+        {  // tensor-core attention plan
             b.plan_tc(s.H / s.KV);
             w.ensure_passes(b.passes.size(), st);
             stage.upload(w.passes.p, b.passes, st);
@@ -415,10 +388,8 @@ struct TransformerPair : ModelPair {
                 gemm(w.xn.p, s.d, lw.qkv_w, M, qd, s.d, epi_bf16(w.qkv.p, qd, lw.qkv_b), st);
                 k_rope_store(w.qkv.p, w.rows.p, M, s, tgt->rope, kv_t, l, w.q.p, st);
             }
-            if (tc_attn)
-                k_attention_tc(w.q.p, w.rows.p, w.items.p, AttnPlan{w.passes.p, w.groups.p, w.tok_grp.p}, ni, kv_t, l, s,
-                               w.ao.p, st, attn_f, attn_b);
-            else k_attention(w.q.p, w.rows.p, w.items.p, ni, kv_t, l, s, w.ao.p, st, attn_f, attn_b);
+            k_attention_tc(w.q.p, w.rows.p, w.items.p, AttnPlan{w.passes.p, w.groups.p, w.tok_grp.p}, ni, kv_t, l, s,
+                           w.ao.p, st, attn_f, attn_b);
             gemm(w.ao.p, HD, lw.o_w, M, s.d, HD, epi_resid(w.x.p, s.d), st);
             k_rmsnorm(w.x.p, s.d, lw.ln2, M, s.d, s.eps, w.xn.p, s.d, st);
             gemm(w.xn.p, s.d, lw.gu_w, M, 2 * s.dff, s.d, epi_swiglu(w.h.p, s.dff), st);
@@ -453,13 +424,8 @@ struct TransformerPair : ModelPair {
             gemm(w.xn.p, d2, drf->layer.qkv_w, M, qd, d2, epi_bf16(w.qkv.p, qd, drf->layer.qkv_b), st);
             k_rope_store(w.qkv.p, w.rows.p, M, drf->s, tgt->rope, kv_d, 0, w.q.p, st);
         }
-        if (tc_attn)
-            k_attention_tc(w.q.p, w.rows.p, w.items.p, AttnPlan{w.passes.p, w.groups.p, w.tok_grp.p}, ni, kv_d, 0,
-                           drf->s, w.ao.p, st, prof_enabled() ? bt.attn_flops(s) : 0,
-                           prof_enabled() ? bt.attn_bytes(s) : 0);
-        else
-            k_attention(w.q.p, w.rows.p, w.items.p, ni, kv_d, 0, drf->s, w.ao.p, st,
-                        prof_enabled() ? bt.attn_flops(s) : 0, prof_enabled() ? bt.attn_bytes(s) : 0);
+        k_attention_tc(w.q.p, w.rows.p, w.items.p, AttnPlan{w.passes.p, w.groups.p, w.tok_grp.p}, ni, kv_d, 0, drf->s,
+                       w.ao.p, st, prof_enabled() ? bt.attn_flops(s) : 0, prof_enabled() ? bt.attn_bytes(s) : 0);
         gemm(w.ao.p, HD, drf->layer.o_w, M, s.d, HD, epi_resid(w.x.p, s.d), st, drafter_splits(HD));
         k_rmsnorm(w.x.p, s.d, drf->layer.ln2, M, s.d, s.eps, w.xn.p, s.d, st);
         gemm(w.xn.p, s.d, drf->layer.gu_w, M, 2 * s.dff, s.d, epi_swiglu(w.h.p, s.dff), st);
@@ -523,7 +489,7 @@ struct TransformerPair : ModelPair {
                 }
                 bt.map_a = head_src;
                 bt.map_b = head_dst;
-                upload(bt, st, tc_attn);
+                upload(bt, st);
                 std::vector<int32_t> hid(hid_src);
                 hid.insert(hid.end(), hid_dst.begin(), hid_dst.end());
                 stage.upload(w.idx.p, hid, st);
@@ -549,10 +515,9 @@ struct TransformerPair : ModelPair {
                 bt.map_a.push_back(r * d.t_max + i);                 // hidden slot in / out
                 bt.map_b.push_back(a * d.slots + 1 + i * d.n + depth);  // Q row
             }
-            if (tc_attn) bt.add_tree_items_tc(r0, bt.M(), per_item_t, L, L, d.n);
-            else bt.add_tree_items(r0, bt.M(), s.H / s.KV, L, L, d.n);
+            bt.add_tree_items_tc(r0, bt.M(), per_item_t, L, L, d.n);
         }
-        upload(bt, st, tc_attn);
+        upload(bt, st);
         const int M = bt.M();
         k_rows_copy_f32(dh.p, s.d, w.map_a.p, w.x.p, s.d, nullptr, M, s.d, st);
         drafter_layer(d, M, (int)bt.items.size(), st);
@@ -583,10 +548,9 @@ struct TransformerPair : ModelPair {
                     bt.map_a.push_back(a * d.slots + 1 + i * d.n + j);
                 }
             // one CTA per (sequence, kv head) for the whole tree; the root rides with chain 0
-            if (tc_attn) bt.add_tree_items_tc(r0, bt.M(), per_item_t, L, L, d.n);
-            else bt.add_tree_items(r0, bt.M(), s.H / s.KV, L, L, d.n);
+            bt.add_tree_items_tc(r0, bt.M(), per_item_t, L, L, d.n);
         }
-        upload(bt, st, tc_attn);
+        upload(bt, st);
         if (!naive) stage.upload(rbase.p, base, st);
         // no stats pass over the verified rows: acceptance computes the 2-3 rows it touches
         target_forward(d, bt.M(), (int)bt.items.size(), P, true, st, d.lazy_pst ? nullptr : const_cast<double *>(d.Pst));
@@ -644,10 +608,7 @@ struct TransformerPair : ModelPair {
             gemm(hc, d2, drf->layer.qkv_w, M, qd, d2, epi_bf16(w.qkv.p, qd, drf->layer.qkv_b), st);
             k_rope_store(w.qkv.p, w.rows.p, M, drf->s, tgt->rope, kv_d, 0, q, st);
         }
-        if (tc_attn)
-            k_attention_tc(q, w.rows.p, w.items.p, AttnPlan{w.passes.p, w.groups.p, w.tok_grp.p}, ni, kv_d, 0, drf->s, ao,
-                           st);
-        else k_attention(q, w.rows.p, w.items.p, ni, kv_d, 0, drf->s, ao, st);
+        k_attention_tc(q, w.rows.p, w.items.p, AttnPlan{w.passes.p, w.groups.p, w.tok_grp.p}, ni, kv_d, 0, drf->s, ao, st);
         RS_CUDA(cudaMemcpyAsync(x1, f, (size_t)M * s.d * sizeof(float), cudaMemcpyDeviceToDevice, st));
         gemm(ao, HD, drf->layer.o_w, M, s.d, HD, epi_resid(x1, s.d), st, drafter_splits(HD));
         k_rmsnorm(x1, s.d, drf->layer.ln2, M, s.d, s.eps, h2, s.d, st);
@@ -746,7 +707,7 @@ struct TransformerPair : ModelPair {
                 }
                 const int M = bt.M();
                 if (M == 0) break;
-                upload(bt, st, tc_attn);
+                upload(bt, st);
                 drafter_forward_train(d, M, (int)bt.items.size(), o, st);
                 o += (size_t)M;
                 RS_CUDA(cudaStreamSynchronize(st));
@@ -800,7 +761,7 @@ struct TransformerPair : ModelPair {
             const int R = bt.M();
             if (R == 0) break;
             prof_set_scope("kd_target");
-            upload(bt, st, tc_attn);
+            upload(bt, st);
             target_forward(d, R, (int)bt.items.size(), k.Pb.p, false, st);
             prof_set_scope("kd_k5");
             for (const Run &u : runs) {  // drafter logits and the final-norm rows of the group
@@ -959,7 +920,7 @@ struct TransformerPair : ModelPair {
                 bt.add_items(r0, bt.M(), per_item_t, -1, 0, 0, 0);
             }
             if (bt.M() == 0) break;
-            upload(bt, st, tc_attn);
+            upload(bt, st);
             target_forward(d, bt.M(), (int)bt.items.size(), nullptr, false, st);
             RS_CUDA(cudaStreamSynchronize(st));
             stage.off = 0;
@@ -1035,7 +996,7 @@ struct TransformerPair : ModelPair {
                 bt.add_items(r0, bt.M(), per_item_t, -1, 0, 0, 0);
             }
             if (bt.M() == 0) break;
-            upload(bt, st, tc_attn);
+            upload(bt, st);
             target_forward(d, bt.M(), (int)bt.items.size(), nullptr, false, st);
             RS_CUDA(cudaStreamSynchronize(st));
             stage.off = 0;
