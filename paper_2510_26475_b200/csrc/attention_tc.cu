@@ -1,31 +1,40 @@
-// attention_tc.cu -- tree-causal GQA attention of the TARGET on 5th-gen tensor cores (sm_100a).
+// attention_tc.cu -- tree-causal GQA attention of the TARGET (and the drafter) on 5th-gen tensor
+// cores (sm_100a).
 //
-// One CTA per work item = up to two 128-row M-tiles of one (sequence, kv head): row =
-// token * G + head (T = 128 / G tokens per tile). Keys are visited in LOGICAL order in chunks
-// of 128 positions; a pass = (chunk, key group). Chunks wholly below the tree start are shared
-// by every token of the item (one K/V tile for both M-tiles); the chunks that reach into the
-// tree are replayed once per group of tokens sharing a key mapping (the tokens of one draft
+// A work item = up to two 128-row M-tiles of one (sequence, kv head): row = token * G + head
+// (T = 128 / G tokens per tile). One CTA per (item, M-tile, kv head). Keys are visited in
+// LOGICAL order in passes of kAttnChunk = 32 positions; a pass = (key block, key group). Blocks
+// wholly below the tree start are shared by every token of the item; the blocks that reach into
+// the tree are replayed once per group of tokens sharing a key mapping (the tokens of one draft
 // chain, the root riding with chain 0), rows of other groups masked -- the tree-causal mask of
-// SURVEY.md §8 A3. Every row therefore sees exactly the key sequence (chunk boundaries, column
+// SURVEY.md §8 A3. Every row therefore sees exactly the key sequence (block boundaries, column
 // order, accumulation order) it would see decoded alone or prefilled, so its output is bitwise
 // independent of the tree it sits in (tests/test_transformer_gpu.py).
 //
-// Warp roles (384 threads):
-//   warps 2-3   producers of a 2-stage shared-memory K/V ring: a chunk is 2 x 2 TMA boxes of
-//               128 keys x 64 dims (128B swizzle) when its keys are physically contiguous, or
-//               cp.async rows (context + the chain's own slots) in the same swizzled layout for
-//               tree passes; warp 2 also owns the TMEM allocation; warp 0 idles;
-//   warp 1      one elected lane issues tcgen05.mma: S_i = Q_i K^T (SS, 128x128x128) into
-//               TMEM and O_i += P_i V (TS: P read from TMEM where it overwrote S_i, V as an
-//               MN-major smem operand), ping-ponging the two M-tiles so one tile's softmax
-//               overlaps the other tile's MMAs;
-//   warps 4-7 / 8-11  softmax of M-tile 0 / 1: one thread per row (its TMEM lane) reads the
-//               row's 128 scores of S (tcgen05.ld), online softmax in the exp2 domain, writes P as
-//               bf16 back into TMEM (tcgen05.st), rescales O in TMEM when the running max moves,
-//               and finally writes O / l as bf16. One thread owns the whole row, so the row max
-//               needs no cross-warp exchange (measured: the two-threads-per-row variant spent
-//               ~340 of its ~1.9K cycles per pass in that exchange).
-// TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512) columns.
+// Why this shape (measured on B200, DESIGN.md §4 "target attention"):
+//   * Q lives in TENSOR MEMORY and S = Q K^T is a TS-form MMA: the tensor core reads only the
+//     K block from shared memory. With Q in shared memory (SS form) every score MMA re-read the
+//     128 x 128 Q tile; the MMAs ran at the ~68 B/clk operand rate, ~90 cycles per 128x64x16
+//     MMA instead of 32, and the issuing thread -- not HBM -- set the pass rate.
+//   * TMEM per CTA = O (128 columns) + Q (64) + two S buffers of 32 keys (2 x 32) = 256, so two
+//     CTAs share an SM (shared memory ~100 KB each): one CTA's softmax overlaps the other's MMAs
+//     and K/V stream, every SM holds work at the benchmarked grids, and each SM keeps up to
+//     2 x 96 KB of K/V in flight.
+//   * S is double-buffered: the score MMAs of pass j + 1 run while the softmax of pass j does.
+//
+// Warp roles (256 threads):
+//   warp 0      plan -> shared memory; then one lane issues O += P(j) V(j) (TS: P read from TMEM
+//               where it overwrote S(j), V an MN-major smem operand, 2 x 128x128x16)
+//   warp 1      one lane issues S(j) = Q K(j)^T (TS, 8 x 128x32x16) into S buffer j & 1
+//   warp 2 / 3  K / V producers: one lane issues the two TMA boxes (32 rows x 64 dims, 128B
+//               swizzle) of a block whose keys are physically contiguous; for tree blocks whose
+//               keys are remapped to a chain's slots the warp copies rows with cp.async in the
+//               same swizzled layout. Warp 2 also owns the TMEM allocation.
+//   warps 4-7   one thread per row (its TMEM lane): Q row -> TMEM; per pass the row's 32 scores
+//               (tcgen05.ld), online softmax in the exp2 domain, P as bf16 over the consumed S
+//               columns (tcgen05.st), O rescale in TMEM when the running max moves (after the
+//               previous P.V completed); finally O / l as bf16.
+// TMEM (256 columns): O [0, 128), Q [128, 192), S(b) at 192 + 32 b.
 #include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -42,23 +51,25 @@ namespace rs {
 namespace {
 
 constexpr int kHD = 128;
-constexpr int kCk = kAttnChunk;                 // keys per chunk
-constexpr int kStages = 2;
-constexpr int kHalfBytes = 128 * 128;          // 128 rows x 64 bf16 (one 128B-swizzled box)
-constexpr int kTileBytes = 2 * kHalfBytes;     // 128 rows x 128 dims
-constexpr int kStageBytes = 2 * kTileBytes;    // K + V
-constexpr int kQBytes = 2 * kTileBytes;        // two M-tiles
+constexpr int kCk = kAttnChunk;              // keys per pass (32)
+constexpr int kNK = 6, kNV = 6;              // K / V ring depths
+constexpr int kBox = kCk * 128;              // kCk rows x 64 bf16 dims: one 128B-swizzled TMA box
+constexpr int kKVBytes = 2 * kBox;           // kCk keys x 128 dims (K or V of one pass)
 constexpr int kMaxPasses = kAttnMaxPasses;
 constexpr int kMaxGroups = kAttnMaxGroups;
-constexpr int kMaxTok = 256;
-constexpr int kThreads = 384;  // 4 control warps + 2 x 4 softmax warps
-constexpr uint32_t kIdescS = (1u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
-constexpr uint32_t kIdescPV = kIdescS | (1u << 16);  // B (= V) is MN-major
+constexpr int kMaxTok = 128;                 // tokens of one M-tile (G >= 1)
+constexpr int kThreads = 256;
+constexpr uint32_t kColO = 0, kColQ = 128, kColS = 192, kTmemCols = 256;
+static_assert(kCk == 32, "TMEM columns and the P packing assume 32-key passes");
+// kind::f16, fp32 accumulate, bf16 A/B, K-major A and B; N at bit 17 (>> 3), M at bit 24 (>> 4)
+constexpr uint32_t kIdescBase = (1u << 4) | (1u << 7) | (1u << 10) | ((128u >> 4) << 24);
+constexpr uint32_t kIdescS = kIdescBase | ((uint32_t)(kCk >> 3) << 17);            // 128 x 32 x 16
+constexpr uint32_t kIdescPV = kIdescBase | ((128u >> 3) << 17) | (1u << 16);       // 128 x 128 x 16, V MN-major
 
 using Pass = AttnPass;
 
 struct Plan {
-    int npasses, ngroups, T, ntok;
+    int npasses, ngroups, ntok;
     int g_chain[kMaxGroups], g_maxpos[kMaxGroups];
     short tok_grp[kMaxTok];
     int tok_pos[kMaxTok];
@@ -66,7 +77,10 @@ struct Plan {
 };
 
 constexpr int kBarBytes = 256;
-constexpr int kSmem = 1024 + kQBytes + kStages * kStageBytes + kBarBytes + (int)sizeof(Plan);
+constexpr int kSmem = 1024 + (kNK + kNV) * kKVBytes + kBarBytes + (int)sizeof(Plan);
+// two CTAs per SM: 228 KB per SM, 1 KB of it reserved per CTA
+static_assert(2 * (kSmem + 1024) <= 233472, "attention: two CTAs per SM must fit in shared memory");
+static_assert((2 * (kNK + kNV) + 2 + 2 + 2 + 1) * 8 + 4 <= kBarBytes, "barrier area");
 
 __device__ __forceinline__ void cp16(uint32_t dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -80,67 +94,82 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t *>(&h);
 }
-// byte offset of (row r, 16-byte chunk c of 16) in a 128-row x 128-dim tile of two swizzled halves
+// byte offset of (row r, 16-byte chunk c of 16) in a tile of two 128B-swizzled 64-dim halves
 __device__ __forceinline__ uint32_t swz_off(int r, int c) {
-    return (uint32_t)((c >> 3) * kHalfBytes + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+    return (uint32_t)((c >> 3) * kBox + r * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, const bf16 *q,
                    const RowDesc *rows, const AttnItem *items, AttnPlan plan, KvCache kv, int layer, int H, int KV,
-                   float scale_log2, bf16 *out, long long *trace) {
-    // trace (diagnostics, CTA (0,0) only): [0] start, per pass j: [1+4j] fullK ok, [2+4j] p0 ok,
-    // [3+4j] p1 ok (MMA thread), [4+4j] softmax tile 0 s_full ok
+                   float scale_log2, bf16 *out, long long *trace, int skip) {
+    const int tile = blockIdx.x & 1;
+    const AttnItem it = items[blockIdx.x >> 1];  // host-uploaded plan: independent of the previous kernel
+    const int G = H / KV;
+    const int T = 128 / G;
+    pdl_trigger();
+    if (tile * T >= it.nrows) return;  // the item has no second M-tile (uniform per CTA)
+    // trace (diagnostics, CTA (0, 0) only): [0] start; per pass j at 1 + 12 j: K issue, V issue,
+    // K landed, V landed, P ready (MMA), -, softmax start / end, -, -, S issue start / end
     const bool tr = trace && blockIdx.x == 0 && blockIdx.y == 0;
     if (tr && threadIdx.x == 0) trace[0] = clock64();
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t *sQ = smem;
-    uint8_t *sKV = smem + kQBytes;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sKV + kStages * kStageBytes);
-    // K and V halves of a stage fill and drain separately: S = Q K^T can start while V is in
-    // flight, and K(j + 2) loads as soon as the S MMAs of pass j are done.
-    uint64_t *fullK = bars, *fullV = bars + kStages, *emptyK = bars + 2 * kStages, *emptyV = bars + 3 * kStages;
-    uint64_t *s_full = bars + 4 * kStages, *p_full = s_full + 2, *o_done = p_full + 2;
+    uint8_t *sK = smem;
+    uint8_t *sV = sK + kNK * kKVBytes;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sV + kNV * kKVBytes);
+    uint64_t *fullK = bars, *emptyK = bars + kNK, *fullV = bars + 2 * kNK, *emptyV = fullV + kNV;
+    uint64_t *s_full = emptyV + kNV;  // [buffer]
+    uint64_t *p_full = s_full + 2;    // [buffer]
+    uint64_t *pv_done = p_full + 2;   // [buffer] P.V(j) completed
+    uint64_t *o_done = pv_done + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_done + 1);
     Plan &pl = *reinterpret_cast<Plan *>(reinterpret_cast<uint8_t *>(bars) + kBarBytes);
 
-    pdl_trigger();
-    const AttnItem it = items[blockIdx.x];  // host-uploaded plan: independent of the previous kernel
     const int kvh = blockIdx.y;
-    const int G = H / KV;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tok0 = tile * T, ntok = min(T, it.nrows - tok0);  // this CTA's tokens
 
-    // ---- plan (host-built, tf_pair.cpp Batch::plan_tc) -> smem, by warp 0 --------------------
+    // ---- plan (host-built, tf_pair.cpp Batch::plan_tc) -> smem, by warp 0: this tile's passes
     if (warp == 0) {
-        for (int j = lane; j < it.npass; j += 32) pl.pass[j] = plan.passes[it.pass0 + j];
+        int n = 0;
+        for (int j0 = 0; j0 < it.npass; j0 += 32) {
+            const int j = j0 + lane;
+            const Pass ps = j < it.npass ? plan.passes[it.pass0 + j] : Pass{};
+            const bool mine = j < it.npass && ((ps.tiles >> tile) & 1);
+            const unsigned m = __ballot_sync(0xffffffffu, mine);
+            if (mine) pl.pass[n + __popc(m & ((1u << lane) - 1))] = ps;
+            n += __popc(m);
+        }
         for (int g = lane; g < it.ngrp; g += 32) {
             const AttnGroup gr = plan.groups[it.grp0 + g];
             pl.g_chain[g] = gr.chain;
             pl.g_maxpos[g] = gr.maxpos;
         }
-        for (int k = lane; k < it.nrows; k += 32) {
-            pl.tok_pos[k] = rows[it.row0 + k].pos;
-            pl.tok_grp[k] = plan.tok_grp[it.row0 + k];
+        for (int k = lane; k < ntok; k += 32) {
+            pl.tok_pos[k] = rows[it.row0 + tok0 + k].pos;
+            pl.tok_grp[k] = plan.tok_grp[it.row0 + tok0 + k];
         }
         if (lane == 0) {
-            pl.npasses = it.npass;
+            pl.npasses = n;
             pl.ngroups = it.ngrp;
-            pl.T = 128 / G;
-            pl.ntok = it.nrows;
+            pl.ntok = ntok;
         }
     }
     if (warp == 1 && lane == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kNK; ++s) {
             mbar_init(&fullK[s], 1);
-            mbar_init(&fullV[s], 1);
             mbar_init(&emptyK[s], 1);
+        }
+        for (int s = 0; s < kNV; ++s) {
+            mbar_init(&fullV[s], 1);
             mbar_init(&emptyV[s], 1);
         }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], 4);  // the tile's four softmax warps
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&s_full[b], 1);
+            mbar_init(&p_full[b], 4);  // the four softmax warps
         }
+        for (int b = 0; b < 2; ++b) mbar_init(&pv_done[b], 1);
         mbar_init(o_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
@@ -148,30 +177,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(512));
+                     "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
     }
-    pdl_wait();  // Q and the K/V cache come from the previous kernel (RoPE / KV store)
-    // ---- Q tiles -> smem (softmax warps: one row each, zero rows beyond the item) -------------
-    if (warp >= 4) {
-        const int T0 = 128 / G;
-        const int tile = (warp - 4) >> 2, r = (warp & 3) * 32 + lane;
-        const int k = tile * T0 + r / G;
-        const bool valid = r < T0 * G && k < it.nrows;
-        uint8_t *base = sQ + tile * kTileBytes;
-        const bf16 *src = q + ((size_t)(it.row0 + k) * H + kvh * G + r % G) * kHD;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            int4 v[8];
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-                v[c] = valid ? *reinterpret_cast<const int4 *>(src + h * 64 + c * 8) : make_int4(0, 0, 0, 0);
-#pragma unroll
-            for (int c = 0; c < 8; ++c) *reinterpret_cast<int4 *>(base + swz_off(r, h * 8 + c)) = v[c];
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    const int T = 128 / G;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -179,177 +187,184 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int np = pl.npasses;
     const size_t kvrow0 = (((size_t)layer * kv.B + it.seq) * kv.KV + kvh) * kv.max_ctx;
 
-    if (warp == 2 || warp == 3) {
-        // ---- producers: one ring, every pass in order (so each thread's parity waits never
-        // alias); contiguous passes by TMA from one thread, tree passes whose keys are
-        // remapped to a chain's slots by cp.async from all 64 threads in the swizzled layout.
-        const int t = threadIdx.x - 64;  // 0..63
-        for (int j = 0; j < np; ++j) {
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---- P.V issuer: O += P(j) V(j) once the softmax wrote P(j); commits free the S
+            // buffer for S(j + 2) (pv_done[j & 1]) and the V stage
+            for (int j = 0; j < np; ++j) {
+                const int s = j % kNV;
+                mbar_wait(&fullV[s], (j / kNV) & 1);
+                const int b = j & 1;
+                mbar_wait(&p_full[b], ((j >> 1) + b) & 1);
+                if (tr) trace[5 + 12 * j] = clock64();
+                tc_fence_after();
+                const uint8_t *vt = sV + s * kKVBytes;
+                if (!(skip & 4)) {
+#pragma unroll
+                    for (int kk = 0; kk < kCk / 16; ++kk)
+                        tc_mma_ts(tmem + kColO, tmem + kColS + b * kCk + kk * 8, sw128_desc_mn(vt + kk * 2048, kBox),
+                                  kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
+                }
+                tc_commit(&pv_done[b]);
+                tc_commit(&emptyV[s]);
+            }
+            tc_commit(o_done);
+        } else if (tr && lane < 3) {
+            // diagnostics: lane 1 / 2 record when each K / V block lands
+            const int depth = lane == 1 ? kNK : kNV;
+            uint64_t *full = lane == 1 ? fullK : fullV;
+            for (int j = 0; j < np; ++j) {
+                mbar_wait(&full[j % depth], (j / depth) & 1);
+                trace[2 + lane + 12 * j] = clock64();
+            }
+        }
+    } else if (warp == 2 || warp == 3) {
+        // ---- producers: warp 2 streams K, warp 3 streams V, each through its own ring in pass
+        // order; contiguous blocks by TMA from one lane, tree blocks whose keys are remapped to a
+        // chain's slots by cp.async from the warp's 32 lanes in the swizzled layout.
+        pdl_wait();  // the K/V cache rows come from the previous kernel (RoPE / KV store)
+        const bool isK = warp == 2;
+        const int depth = isK ? kNK : kNV;
+        uint8_t *ring = isK ? sK : sV;
+        uint64_t *full = isK ? fullK : fullV, *empty = isK ? emptyK : emptyV;
+        const CUtensorMap *tm = isK ? &tmK : &tmV;
+        const bf16 *src = isK ? kv.k : kv.v;
+        for (int j = 0, s = 0, ph = 1; j < np; ++j) {
             const Pass ps = pl.pass[j];
-            const int s = j % kStages;
-            const uint32_t par = ((j / kStages) & 1) ^ 1;
-            uint8_t *dst = sKV + s * kStageBytes;
+            uint8_t *dst = ring + s * kKVBytes;
+            mbar_wait(&empty[s], ph);
             if (!ps.manual) {
-                const int y = (int)(kvrow0 + ps.chunk * kCk);
-                mbar_wait(&emptyK[s], par);
-                if (t == 0) {
-                    if (tr) trace[9 + 12 * j] = clock64();
-                    mbar_arrive_expect_tx(&fullK[s], kTileBytes);
-                    tma_load_2d(dst, &tmK, &fullK[s], 0, y);
-                    tma_load_2d(dst + kHalfBytes, &tmK, &fullK[s], 64, y);
+                if (lane == 0) {
+                    if (tr) trace[1 + 12 * j + (isK ? 0 : 1)] = clock64();
+                    const int y = (int)(kvrow0 + ps.chunk * kCk);
+                    mbar_arrive_expect_tx(&full[s], kKVBytes);
+                    tma_load_2d(dst, tm, &full[s], 0, y);
+                    tma_load_2d(dst + kBox, tm, &full[s], 64, y);
                 }
-                mbar_wait(&emptyV[s], par);
-                if (t == 0) {
-                    if (tr) trace[10 + 12 * j] = clock64();
-                    mbar_arrive_expect_tx(&fullV[s], kTileBytes);
-                    tma_load_2d(dst + kTileBytes, &tmV, &fullV[s], 0, y);
-                    tma_load_2d(dst + kTileBytes + kHalfBytes, &tmV, &fullV[s], 64, y);
+            } else {
+                // keys beyond the group's last position are masked to p = 0 by the softmax; their
+                // rows only need finite values, so they are copied from the contiguous position
+                const int ch = pl.g_chain[ps.grp], lim = pl.g_maxpos[ps.grp];
+                for (int idx = lane; idx < kCk * 16; idx += 32) {
+                    const int rr = idx >> 4, c = idx & 15;
+                    const int p = ps.chunk * kCk + rr;
+                    const int phys = p > lim ? min(p, kv.max_ctx - 1)
+                                             : p < it.ltree ? p : it.tbase + ch * it.nstride + (p - it.ltree);
+                    cp16(smem_u32(dst + swz_off(rr, c)), src + (kvrow0 + phys) * kHD + c * 8);
                 }
-                continue;
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[s]);
             }
-            mbar_wait(&emptyK[s], par);
-            mbar_wait(&emptyV[s], par);
-            const int ch = pl.g_chain[ps.grp], lim = pl.g_maxpos[ps.grp];
-            for (int idx = t; idx < kCk * 16; idx += 64) {
-                const int r = idx >> 4, c = idx & 15;
-                const int p = ps.chunk * kCk + r;
-                const uint32_t o = swz_off(r, c);
-                if (p <= lim) {
-                    const int phys = p < it.ltree ? p : it.tbase + ch * it.nstride + (p - it.ltree);
-                    const size_t go = (kvrow0 + phys) * kHD + c * 8;
-                    cp16(smem_u32(dst + o), kv.k + go);
-                    cp16(smem_u32(dst + kTileBytes + o), kv.v + go);
-                } else {
-                    *reinterpret_cast<int4 *>(dst + o) = make_int4(0, 0, 0, 0);
-                    *reinterpret_cast<int4 *>(dst + kTileBytes + o) = make_int4(0, 0, 0, 0);
-                }
-            }
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("bar.sync 1, 64;" ::: "memory");
-            if (t == 0) {
-                mbar_arrive(&fullK[s]);
-                mbar_arrive(&fullV[s]);
+            if (++s == depth) {
+                s = 0;
+                ph ^= 1;
             }
         }
     } else if (warp == 1) {
-        // ---- MMA issuer ---------------------------------------------------------------------------
+        // ---- score issuer: S(j) = Q K(j)^T into S buffer j & 1 once P.V(j - 2) has read it ---------
+        // (two issuing threads: one thread retires a tcgen05.mma only every ~55 cycles whatever N
+        // is -- tools/mma_issue_bench.cu -- so the 8 score MMAs and the 2 P.V MMAs of a pass would
+        // serialise on one thread; a third issuer for the odd passes measured no further gain)
         if (lane == 0) {
-            int pend[2] = {-1, -1};
-            int pv_n[2] = {0, 0};
-            uint8_t users[kMaxPasses];
-            for (int j = 0; j < np; ++j) users[j] = (uint8_t)__popc(pl.pass[j].tiles);
-            auto issue_pv = [&](int i) {
-                const int jp = pend[i];
-                mbar_wait(&fullV[jp % kStages], (jp / kStages) & 1);
-                if (tr && i == 0) trace[11 + 12 * jp] = clock64();
-                mbar_wait(&p_full[i], pv_n[i] & 1);
-                if (tr) trace[2 + 12 * jp + i] = clock64();
-                tc_fence_after();
-                const uint8_t *v = sKV + (jp % kStages) * kStageBytes + kTileBytes;
-                const uint32_t d_o = tmem + 256 + i * 128, a_p = tmem + i * 128;
-#pragma unroll
-                for (int k = 0; k < kCk / 16; ++k)
-                    tc_mma_ts(d_o, a_p + k * 8, sw128_desc_mn(v + k * 2048, kHalfBytes), kIdescPV,
-                              (pv_n[i] > 0 || k > 0) ? 1u : 0u);
-                ++pv_n[i];
-                pend[i] = -1;
-                if (--users[jp] == 0) tc_commit(&emptyV[jp % kStages]);
-            };
+            // Q is written to TMEM by the softmax warps after their dependency wait; their first
+            // arrival on p_full[1] (its phase 0) says "Q ready", so pass j's P completes phase
+            // (j >> 1) of p_full[0] or phase (j >> 1) + 1 of p_full[1]
+            mbar_wait(&p_full[1], 0);
+            tc_fence_after();
             for (int j = 0; j < np; ++j) {
-                const Pass ps = pl.pass[j];
-                // a pending P.V whose stage the producers need next must go first
-                for (int i = 0; i < 2; ++i)
-                    if (pend[i] >= 0 && pend[i] <= j - kStages) issue_pv(i);
-                const int s = j % kStages;
-                mbar_wait(&fullK[s], (j / kStages) & 1);
-                if (tr) trace[1 + 12 * j] = clock64();
+                const int s = j % kNK;
+                if (j >= 2) mbar_wait(&pv_done[j & 1], ((j >> 1) - 1) & 1);  // P.V(j - 2) read the buffer
+                mbar_wait(&fullK[s], (j / kNK) & 1);
+                if (tr) trace[11 + 12 * j] = clock64();
                 tc_fence_after();
-                const uint8_t *kt = sKV + s * kStageBytes;
-                for (int i = 0; i < 2; ++i) {
-                    if (!(ps.tiles & (1 << i))) continue;
-                    if (pend[i] >= 0) issue_pv(i);
-                    // Phase offset: tile 1's first scores wait for tile 0's first softmax, so the
-                    // two softmax groups run half a period apart -- each overlaps the other
-                    // tile's MMAs instead of both contending for the MUFU at once.
-                    if (i == 1 && j == 0 && (ps.tiles & 1) && pv_n[1] == 0) mbar_wait(&p_full[0], 0);
-                    const uint8_t *qt = sQ + i * kTileBytes;
-                    const uint32_t d_s = tmem + i * 128;
+                const uint8_t *kt = sK + s * kKVBytes;
+                const uint32_t d_s = tmem + kColS + (j & 1) * kCk;
+                if (!(skip & 2)) {
 #pragma unroll
-                    for (int h = 0; h < 2; ++h)
-#pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            tc_mma(d_s, sw128_desc(qt + h * kHalfBytes) + 2 * k, sw128_desc(kt + h * kHalfBytes) + 2 * k,
-                                   kIdescS, (h | k) ? 1u : 0u);
-                    tc_commit(&s_full[i]);
-                    pend[i] = j;
+                    for (int kk = 0; kk < 8; ++kk)
+                        tc_mma_ts(d_s, tmem + kColQ + kk * 8, sw128_desc(kt + (kk >> 2) * kBox) + 2 * (kk & 3), kIdescS,
+                                  kk > 0 ? 1u : 0u);
                 }
+                tc_commit(&s_full[j & 1]);
                 tc_commit(&emptyK[s]);
+                if (tr) trace[12 + 12 * j] = clock64();
             }
-            for (int i = 0; i < 2; ++i)
-                if (pend[i] >= 0) issue_pv(i);
-            tc_commit(o_done);
         }
-    } else if (warp >= 4) {
-        // ---- softmax: one thread per row of M-tile `tile` ----------------------------------------
-        // Per pass: one TMEM read of the row's 128 scores, the row max, p = 2^(s*scale - m) written
-        // as bf16 over the consumed S columns (the 64-column halves [64h, 64h + 64) into S columns
-        // [32h, 32h + 32)). The running max m only moves when the chunk max exceeds it by more
-        // than 2^8 (so p <= 256): O in TMEM is then rescaled. Row sums are kept as 8 interleaved
-        // partials per 64-column half. Every choice depends only on the row's own scores, so the
-        // arithmetic is identical whatever item the row sits in.
-        const int tile = (warp - 4) >> 2, qd = warp & 3;
-        const int r = qd * 32 + lane;
-        const int k = tile * T + r / G;
-        const bool valid = r < T * G && k < pl.ntok;
+    } else {
+        // ---- softmax warps: one thread per row (row r = token k, head kvh * G + r % G) -------------
+        const int r = (warp & 3) * 32 + lane;
+        const int k = r / G;
+        const bool valid = r < T * G && k < ntok;
         const bool warp_valid = __any_sync(0xffffffffu, valid);
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        pdl_wait();  // Q comes from the previous kernel (QKV + RoPE)
+        {
+            // Q row -> TMEM columns [128, 192) as bf16 pairs (zero rows beyond the tile's tokens)
+            const bf16 *src = q + ((size_t)(it.row0 + tok0 + (valid ? k : 0)) * H + kvh * G + r % G) * kHD;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint32_t w[32];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const int4 v = valid ? *reinterpret_cast<const int4 *>(src + h * 64 + c * 8) : make_int4(0, 0, 0, 0);
+                    w[4 * c] = (uint32_t)v.x;
+                    w[4 * c + 1] = (uint32_t)v.y;
+                    w[4 * c + 2] = (uint32_t)v.z;
+                    w[4 * c + 3] = (uint32_t)v.w;
+                }
+                tmem_st32(tmem + lane_off + kColQ + h * 32, w);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[1]);  // "Q ready"
+        }
+        // Per pass: one TMEM read of the row's 32 scores, the row max, p = 2^(s*scale - m) written
+        // as bf16 over the consumed S columns [0, 16) of the buffer. The running max m only moves
+        // when the block max exceeds it by more than 2^8 (so p <= 256): O in TMEM is then rescaled
+        // once the previous P.V has completed. Row sums are kept as 8 interleaved partials. Every
+        // choice depends only on the row's own scores, so the arithmetic is identical whatever
+        // item the row sits in.
         const int pos = valid ? pl.tok_pos[k] : -1;
         const int grp = valid ? pl.tok_grp[k] : -2;
-        const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-        const uint32_t tS = tmem + lane_off + tile * 128, tO = tmem + lane_off + 256 + tile * 128;
+        const uint32_t tO = tmem + lane_off + kColO;
+        const bool trs = tr && warp == 4 && lane == 0;
         float m = -INFINITY;
-        float lp[2][8];
+        float lp[8];
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int i = 0; i < 8; ++i) lp[h][i] = 0.f;
-        int n = 0;
+        for (int i = 0; i < 8; ++i) lp[i] = 0.f;
         for (int j = 0; j < np; ++j) {
             const Pass ps = pl.pass[j];
-            if (!(ps.tiles & (1 << tile))) continue;
-            mbar_wait(&s_full[tile], n & 1);
-            const bool trs = tr && tile == 0 && warp == 4 && lane == 0;
-            if (trs) trace[4 + 12 * j] = clock64();
+            const int b = j & 1;
+            const uint32_t tS = tmem + lane_off + kColS + b * kCk;
+            mbar_wait(&s_full[b], (j >> 1) & 1);
+            if (trs) trace[7 + 12 * j] = clock64();
             tc_fence_after();
             const int c0 = ps.chunk * kCk;
             const bool mine = valid && (ps.grp < 0 || ps.grp == grp);
             const int lim = mine ? pos - c0 : -1;  // own columns x <= lim are visible
-            if (warp_valid) {
-                uint32_t v[128];
+            if (warp_valid && !(skip & 1)) {
+                uint32_t v[32];
+                tmem_ld32(tS, v);
+                float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+                if (lim >= kCk - 1) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c) tmem_ld32_nw(tS + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
-                tmem_ld_wait();
-                float mxh[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int lh = lim - 64 * h;
-                    float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-                    if (lh >= 63) {
-#pragma unroll
-                        for (int x = 0; x < 64; x += 4) {
-                            mx0 = fmaxf(mx0, __uint_as_float(v[64 * h + x]));
-                            mx1 = fmaxf(mx1, __uint_as_float(v[64 * h + x + 1]));
-                            mx2 = fmaxf(mx2, __uint_as_float(v[64 * h + x + 2]));
-                            mx3 = fmaxf(mx3, __uint_as_float(v[64 * h + x + 3]));
-                        }
-                    } else {
-#pragma unroll
-                        for (int x = 0; x < 64; ++x)
-                            if (x <= lh) mx0 = fmaxf(mx0, __uint_as_float(v[64 * h + x]));
+                    for (int x = 0; x < 32; x += 4) {
+                        mx0 = fmaxf(mx0, __uint_as_float(v[x]));
+                        mx1 = fmaxf(mx1, __uint_as_float(v[x + 1]));
+                        mx2 = fmaxf(mx2, __uint_as_float(v[x + 2]));
+                        mx3 = fmaxf(mx3, __uint_as_float(v[x + 3]));
                     }
-                    mxh[h] = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+                } else {
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) {
+                        if (x > lim) v[x] = __float_as_uint(-INFINITY);  // masked: exp2 -> +0
+                        mx0 = fmaxf(mx0, __uint_as_float(v[x]));
+                    }
                 }
-                float mx = fmaxf(mxh[0], mxh[1]);
+                float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
                 mx = mx == -INFINITY ? mx : mx * scale_log2;  // scale > 0: max commutes with it
                 bool resc = false;
                 float alpha = 1.f;
@@ -361,34 +376,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                         m = mx;
                         resc = true;
 #pragma unroll
-                        for (int h = 0; h < 2; ++h)
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) lp[h][i] *= alpha;
+                        for (int i = 0; i < 8; ++i) lp[i] *= alpha;
                     }
                 }
                 const float nb = m == -INFINITY ? 0.f : -m;
+                uint32_t pk[16];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int lh = lim - 64 * h;
-                    const bool all = lh >= 63;
-                    uint32_t pk[32];
-#pragma unroll
-                    for (int x = 0; x < 64; x += 2) {
-                        float p0 = ex2(fmaf(__uint_as_float(v[64 * h + x]), scale_log2, nb));
-                        float p1 = ex2(fmaf(__uint_as_float(v[64 * h + x + 1]), scale_log2, nb));
-                        if (!all) {
-                            p0 = x <= lh ? p0 : 0.f;
-                            p1 = x + 1 <= lh ? p1 : 0.f;
-                        }
-                        lp[h][x & 7] += p0;
-                        lp[h][(x + 1) & 7] += p1;
-                        pk[x >> 1] = pack_bf16(p0, p1);
-                    }
-                    // P (bf16) of this half over S columns [32 h, 32 h + 32), already read
-                    tmem_st16(tS + h * 32, *reinterpret_cast<uint32_t(*)[16]>(pk));
-                    tmem_st16(tS + h * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(pk + 16));
+                for (int x = 0; x < 32; x += 2) {
+                    // masked columns hold -inf: fma(-inf, scale, nb) = -inf and ex2(-inf) = +0
+                    const float p0 = ex2(fmaf(__uint_as_float(v[x]), scale_log2, nb));
+                    const float p1 = ex2(fmaf(__uint_as_float(v[x + 1]), scale_log2, nb));
+                    lp[x & 7] += p0;
+                    lp[(x + 1) & 7] += p1;
+                    pk[x >> 1] = pack_bf16(p0, p1);
                 }
-                if (n > 0 && __any_sync(0xffffffffu, resc)) {
+                tmem_st16(tS, pk);  // P (bf16) over S columns [0, 16) of this buffer, already read
+                if (j > 0 && __any_sync(0xffffffffu, resc)) {
+                    // O may still be accumulating the previous pass: wait for that P.V (the only
+                    // one that can be in flight -- the next one needs this pass's P)
+                    mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+                    tc_fence_after();
 #pragma unroll 1
                     for (int cc = 0; cc < 4; ++cc) {
                         uint32_t o[32];
@@ -400,20 +407,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 tmem_st_wait();
             }
-            if (tr && tile == 0 && lane == 0) trace[5 + (warp - 4) + 12 * j] = clock64();  // this warp's P done
+            if (trs) trace[8 + 12 * j] = clock64();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[tile]);
-            ++n;
+            if (lane == 0) mbar_arrive(&p_full[b]);
         }
-        if (n > 0 && warp_valid) {
-            const float lh0 = ((lp[0][0] + lp[0][1]) + (lp[0][2] + lp[0][3])) + ((lp[0][4] + lp[0][5]) + (lp[0][6] + lp[0][7]));
-            const float lh1 = ((lp[1][0] + lp[1][1]) + (lp[1][2] + lp[1][3])) + ((lp[1][4] + lp[1][5]) + (lp[1][6] + lp[1][7]));
-            const float l = lh0 + lh1;
+        if (np > 0 && warp_valid) {
+            const float l = ((lp[0] + lp[1]) + (lp[2] + lp[3])) + ((lp[4] + lp[5]) + (lp[6] + lp[7]));
             mbar_wait(o_done, 0);
             tc_fence_after();
             const float inv = l > 0.f ? 1.f / l : 0.f;
-            bf16 *dst = out + ((size_t)(it.row0 + (valid ? k : 0)) * H + kvh * G + r % G) * kHD;
+            bf16 *dst = out + ((size_t)(it.row0 + tok0 + (valid ? k : 0)) * H + kvh * G + r % G) * kHD;
 #pragma unroll 1
             for (int cc = 0; cc < 4; ++cc) {
                 uint32_t o[32];
@@ -436,13 +440,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
     }
 }
 
 }  // namespace
 
 int attn_tc_max_tokens(int G) { return 2 * (128 / G); }
+
+long long *trace_buf() {
+    static long long *p = nullptr;
+    if (!p) {
+        RS_CUDA(cudaMalloc(&p, 8 * (1 + 12 * kMaxPasses)));
+        RS_CUDA(cudaMemset(p, 0, 8 * (1 + 12 * kMaxPasses)));
+    }
+    return p;
+}
 
 void k_attention_tc(const bf16 *q, const RowDesc *rows, const AttnItem *items, const AttnPlan &plan, int n_items,
                     const KvCache &kv, int layer, const TfShape &s, bf16 *out, cudaStream_t st, double flops,
@@ -452,7 +465,6 @@ void k_attention_tc(const bf16 *q, const RowDesc *rows, const AttnItem *items, c
     if (s.hd != kHD) throw std::invalid_argument("attention: head_dim must be 128");
     if (s.H / s.KV > 128) throw std::invalid_argument("attention: GQA group too large");
     static const bool attr = [] {  // thread-safe one-time init (engine + learner threads)
-        static_assert(sizeof(Plan) + kBarBytes + 1024 + kQBytes + kStages * kStageBytes <= 232448, "smem");
         RS_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
         return true;
     }();
@@ -461,22 +473,20 @@ void k_attention_tc(const bf16 *q, const RowDesc *rows, const AttnItem *items, c
     const CUtensorMap tk = make_tma_map_bf16(kv.k, total_rows, kHD, kHD, kCk);
     const CUtensorMap tv = make_tma_map_bf16(kv.v, total_rows, kHD, kHD, kCk);
     const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(s.hd));
-    static long long *trace = nullptr;
-    if (tuning().attn_trace && !trace) RS_CUDA(cudaMalloc(&trace, 8 * (1 + 12 * kMaxPasses)));
-    launch_pdl(attn_tc_kernel, dim3(n_items, s.KV), kThreads, kSmem, st, tk, tv, q, rows, items, plan, kv, layer,
-               s.H, s.KV, scale_log2, out, tuning().attn_trace ? trace : nullptr);
+    launch_pdl(attn_tc_kernel, dim3(2 * n_items, s.KV), kThreads, kSmem, st, tk, tv, q, rows, items, plan, kv, layer,
+               s.H, s.KV, scale_log2, out, tuning().attn_trace ? trace_buf() : (long long *)nullptr,
+               tuning().attn_skip);
     if (tuning().attn_trace) {
         RS_CUDA(cudaStreamSynchronize(st));
         static long long host[1 + 12 * kMaxPasses];
-        RS_CUDA(cudaMemcpy(host, trace, sizeof(host), cudaMemcpyDeviceToHost));
+        RS_CUDA(cudaMemcpy(host, trace_buf(), sizeof(host), cudaMemcpyDeviceToHost));
         if (tuning().attn_trace == layer + 1 && n_items >= 32) {
-            fprintf(stderr, "attn trace layer %d items %d:\n", layer, n_items);
-            for (int j = 0; j < 24; ++j) {
+            fprintf(stderr, "attn trace layer %d items %d (cycles from CTA start):\n", layer, n_items);
+            for (int j = 0; j < 64; ++j) {
                 const long long *h = host + 1 + 12 * j;
-                fprintf(stderr, "  pass %2d fullK %6lld p0 %6lld p1 %6lld sm0 %6lld | P done +%lld +%lld +%lld +%lld | "
-                        "issueK %6lld issueV %6lld fullV %6lld\n",
-                        j, h[0] - host[0], h[1] - host[0], h[2] - host[0], h[3] - host[0], h[4] - h[3], h[5] - h[3],
-                        h[6] - h[3], h[7] - h[3], h[8] - host[0], h[9] - host[0], h[10] - host[0]);
+                auto t = [&](int i) { return h[i] ? h[i] - host[0] : -1; };
+                fprintf(stderr, "  pass %2d issueK %6lld issueV %6lld | landK %6lld landV %6lld P %6lld | sm %6lld..%6lld | "
+                        "S %6lld..%6lld\n", j, t(0), t(1), t(2), t(3), t(4), t(6), t(7), t(10), t(11));
             }
         }
     }

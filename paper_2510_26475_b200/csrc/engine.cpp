@@ -38,6 +38,7 @@ Tuning &tuning() {
                     if (k == "accept_cluster") x.accept_cluster = v;
                     else if (k == "fused_stats") x.fused_stats = v;
                     else if (k == "attn_trace") x.attn_trace = v;
+                    else if (k == "attn_skip") x.attn_skip = v;
                     else if (k == "pdl") x.pdl = v;
                     else if (k == "gemm2") x.gemm2 = v;
                     else if (k == "gemm_trace") x.gemm_trace = v;

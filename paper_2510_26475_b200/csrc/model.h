@@ -123,8 +123,8 @@ struct AttnPlan {
     const AttnGroup *groups = nullptr;
     const int16_t *tok_grp = nullptr;  // per forward row: group index within its item
 };
-constexpr int kAttnChunk = 128;     // keys per chunk of the tensor-core attention
-constexpr int kAttnMaxPasses = 192;
+constexpr int kAttnChunk = 32;      // keys per pass of the tensor-core attention
+constexpr int kAttnMaxPasses = 400;
 constexpr int kAttnMaxGroups = 64;
 
 struct KvCache {
