@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         uint64_t *full = isK ? fullK : fullV, *empty = isK ? emptyK : emptyV;
         const CUtensorMap *tm = isK ? &tmK : &tmV;
         const bf16 *src = isK ? kv.k : kv.v;
+        const uint64_t pol = l2_evict_first_policy();  // the K/V stream is read once
         for (int j = 0, s = 0, ph = 1; j < np; ++j) {
             const Pass ps = pl.pass[j];
             uint8_t *dst = ring + s * kKVBytes;
@@ -238,8 +239,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                     if (tr) trace[1 + 12 * j + (isK ? 0 : 1)] = clock64();
                     const int y = (int)(kvrow0 + ps.chunk * kCk);
                     mbar_arrive_expect_tx(&full[s], kKVBytes);
-                    tma_load_2d(dst, tm, &full[s], 0, y);
-                    tma_load_2d(dst + kBox, tm, &full[s], 64, y);
+                    tma_load_2d_hint(dst, tm, &full[s], 0, y, pol);
+                    tma_load_2d_hint(dst + kBox, tm, &full[s], 64, y, pol);
                 }
             } else {
                 // keys beyond the group's last position are masked to p = 0 by the softmax; their

@@ -219,29 +219,31 @@ __device__ __forceinline__ void epi2_chunk(const GemmEpi &ep, uint32_t taddr, in
 // QKV + bias + RoPE + K/V cache store for one 32-token chunk. The CTA's 128 features are one
 // head (hd = 128): the four epilogue warps stage bf16(acc + bias) of all 128 dims x 32 tokens,
 // then every thread rotates 8-dim vectors (i, i + 64 pairs, rotate-half, Qwen2) and stores 16 B
-// into q [t][head] or the K / V cache slot of the token (RowDesc::seq / phys / pos).
+// into q [t][head] or the K / V cache slot of the token (RowDesc::seq / phys / pos). The bias
+// value of the thread's dim is loaded once per tile and the cos / sin of the chunk were loaded
+// during the previous chunk (rope_cs_load), so no global round trip sits on the chunk's path.
+__device__ __forceinline__ void rope_cs_load(const QkvStore &s, const int4 *tok, int tbase, int t0, int T, int tid,
+                                             float4 (&cs)[4][4]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int vi = tid + 128 * k, j = vi >> 4, g = vi & 15;
+        const int pos = t0 + j < T ? tok[t0 + j - tbase].x : 0;
+        const float4 *src = reinterpret_cast<const float4 *>(s.rope + ((size_t)pos * 64 + ((8 * g) & 63)) * 2);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cs[k][e] = __ldg(src + e);
+    }
+}
+
 __device__ __forceinline__ void epi2_qkv_rope(const GemmEpi &ep, uint32_t taddr, int head, int q_warp, int t0, int T,
-                                              float (*stg)[132], const int4 *tok, int tbase, int bar) {
+                                              float (*stg)[132], const int4 *tok, int tbase, int bar,
+                                              const float4 (&cs)[4][4], float b) {
     const int lane = threadIdx.x & 31;
     const int dim = q_warp * 32 + lane;
     const QkvStore &s = ep.qkv;
     const int tid = q_warp * 32 + lane;
     const bool is_q = head < s.H, is_k = !is_q && head < s.H + s.KV;
-    // cos / sin of this thread's four 8-dim vectors first: their latency overlaps the TMEM read
-    float4 cs[4][4];
-    if (is_q || is_k) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int vi = tid + 128 * k, j = vi >> 4, g = vi & 15;
-            const int pos = t0 + j < T ? tok[t0 + j - tbase].x : 0;
-            const float4 *src = reinterpret_cast<const float4 *>(s.rope + ((size_t)pos * 64 + ((8 * g) & 63)) * 2);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) cs[k][e] = __ldg(src + e);
-        }
-    }
     uint32_t v[32];
     tmem_ld32(taddr, v);
-    const float b = __bfloat162float(static_cast<const __nv_bfloat16 *>(ep.bias)[head * 128 + dim]);
 #pragma unroll
     for (int j = 0; j < 32; ++j) stg[j][dim] = __bfloat162float(__float2bfloat16(__uint_as_float(v[j]) + b));
     asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
@@ -506,10 +508,18 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                 tc_fence_after();
             }
             if constexpr (EPI == kEpiQKVRope) {
+                const int head = f0 / 128, tid = q * 32 + lane;
+                const bool rope = head < ep.qkv.H + ep.qkv.KV;  // q and k heads rotate, v heads do not
+                const float b = __bfloat162float(static_cast<const __nv_bfloat16 *>(ep.bias)[f0 + tid]);
+                float4 cs[4][4];
+                if (rope && grp < BT / 32) rope_cs_load(ep.qkv, tok_tab, t0, t0 + grp * 32, T, tid, cs);
 #pragma unroll 1
-                for (int c = grp; c < BT / 32; c += 2)
-                    epi2_qkv_rope(ep, tb + c * 32, f0 / 128, q, t0 + c * 32, T,
-                                  reinterpret_cast<float(*)[132]>(stg_grp), tok_tab, t0, ebar);
+                for (int c = grp; c < BT / 32; c += 2) {
+                    epi2_qkv_rope(ep, tb + c * 32, head, q, t0 + c * 32, T, reinterpret_cast<float(*)[132]>(stg_grp),
+                                  tok_tab, t0, ebar, cs, b);
+                    // the next chunk's cos / sin, in flight during its TMEM read and staging
+                    if (rope && c + 2 < BT / 32) rope_cs_load(ep.qkv, tok_tab, t0, t0 + (c + 2) * 32, T, tid, cs);
+                }
             } else if constexpr (EPI == kEpiResidual) {
                 // software-pipelined: chunk c + 1's residual rows are in flight while chunk c is done
                 float4 cur[2][8];
