@@ -31,6 +31,9 @@ extern "C" {
 #define RS_VERIFY_SAMPLE 0 /* lossless rejection sampling, specdec.cpp:197-267 */
 #define RS_VERIFY_GREEDY 1 /* greedy verification (not in the reference) */
 
+#define RS_DTYPE_BF16 0 /* host tensor elements: bf16 bit patterns (uint16) */
+#define RS_DTYPE_F32 1  /* host tensor elements: fp32 */
+
 typedef struct rs_ctx rs_ctx;       /* one GPU + stream + scratch */
 typedef struct rs_model rs_model;   /* immutable device-resident model (tabular or transformer) */
 typedef struct rs_table rs_table;   /* ProfileTable, server.hpp:21-49 */
@@ -288,6 +291,28 @@ int rs_row_stats(rs_ctx *ctx, const float *rows_dev, int32_t nrows, int32_t V, d
    ("emb", "final_norm", "rope", per layer "qkv_w", "qkv_b", "o_w", "gu_w", "down_w", "ln1",
    "ln2"; drafter "fc_w", "norm_emb", "norm_hid", "lm_w"), for export / test references. */
 int rs_model_tensor(const rs_model *m, const char *name, int32_t layer, void **dev_ptr, int64_t *bytes);
+/* Checkpoint load / store -- the transformer counterpart of TabularARModel::to_json /
+   from_json (model.cpp:176-191), so real Qwen2.5 / EAGLE-3 weights can be served. Tensors use
+   the Hugging Face names and layouts, row-major [rows][cols] on the host:
+     target:  "embed_tokens.weight" [V][d] (tied LM head), "norm.weight" [d], per layer
+              "input_layernorm.weight", "post_attention_layernorm.weight" [d],
+              "q_proj.weight" [H*hd][d], "k_proj.weight" / "v_proj.weight" [KV*hd][d],
+              "q_proj.bias" / "k_proj.bias" / "v_proj.bias", "o_proj.weight" [d][H*hd],
+              "gate_proj.weight" / "up_proj.weight" [d_ff][d], "down_proj.weight" [d][d_ff];
+     drafter: "fc.weight" [d][3d], "input_layernorm.weight" (norm of the token embedding),
+              "hidden_norm.weight" (norm of the fused feature), "norm.weight",
+              "lm_head.weight" [V][d], and the decoder-layer names above with QKV input 2d
+              (layer argument ignored).
+   The library scatters them into its arena (fused QKV rows, pairwise-interleaved gate/up rows).
+   dtype RS_DTYPE_BF16 / RS_DTYPE_F32 is the HOST element type; it is converted (fp32 -> bf16
+   round-to-nearest-even for bf16 weights, exact otherwise). n must equal rows * cols. Loading
+   gives the model a new snapshot identity (engines re-prefill a drafter's cache); do not load
+   into a model while an engine is stepping on it. */
+int rs_model_tensor_shape(const rs_model *m, const char *name, int32_t layer, int64_t *rows, int64_t *cols);
+int rs_model_load_tensor(rs_ctx *ctx, rs_model *m, const char *name, int32_t layer, const void *host, int32_t dtype,
+                         int64_t n);
+int rs_model_store_tensor(rs_ctx *ctx, const rs_model *m, const char *name, int32_t layer, void *host, int32_t dtype,
+                          int64_t n);
 /* Device-to-device copy on the context stream (synchronous). */
 int rs_memcpy_d2d(rs_ctx *ctx, void *dst_dev, const void *src_dev, int64_t bytes);
 /* Parameter count of a model (tabular: table size). */

@@ -42,6 +42,7 @@ class CudaError(RuntimeError):
 
 RS_OK, RS_EINVAL, RS_ESTATE, RS_ELOGIC, RS_ECUDA, RS_ENOMEM = range(6)
 RS_VERIFY_SAMPLE, RS_VERIFY_GREEDY = 0, 1
+RS_DTYPE_BF16, RS_DTYPE_F32 = 0, 1
 
 
 # ---- C structs ------------------------------------------------------------------------------
@@ -114,6 +115,7 @@ class _LearnerMetric(ctypes.Structure):
 
 # Every symbol include/respec_b200.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = [
+    "rs_model_tensor_shape", "rs_model_load_tensor", "rs_model_store_tensor",
     "rs_last_error", "rs_version", "rs_launch_count", "rs_launch_count_reset",
     "rs_ctx_create", "rs_ctx_destroy", "rs_ctx_sync", "rs_ctx_set_stream",
     "rs_tabular_create", "rs_tabular_logits", "rs_transformer_create", "rs_drafter_create",
@@ -260,6 +262,9 @@ def lib():
             "rs_memset_async": ([vp, vp, i32, i64], ctypes.c_int),
             "rs_memcpy_h2d": ([vp, vp, vp, i64], ctypes.c_int),
             "rs_memcpy_d2h": ([vp, vp, vp, i64], ctypes.c_int),
+            "rs_model_tensor_shape": ([vp, ctypes.c_char_p, i32, P(i64), P(i64)], ctypes.c_int),
+            "rs_model_load_tensor": ([vp, vp, ctypes.c_char_p, i32, vp, i32, i64], ctypes.c_int),
+            "rs_model_store_tensor": ([vp, vp, ctypes.c_char_p, i32, vp, i32, i64], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -633,6 +638,74 @@ class _NeuralModel(Model):
         _check(lib().rs_model_params(self.handle, ctypes.byref(v)))
         return v.value
 
+    # ---- checkpoints (Hugging Face names; the transformer counterpart of to_json / from_json,
+    # model.cpp:176-191). Host arrays are numpy float32 (converted to bf16 with round-to-nearest-
+    # even for bf16 weights), numpy uint16 (bf16 bit patterns) or torch tensors.
+    # subclasses name their tensors: checkpoint_names() and _split(full) -> (name, layer)
+    def tensor_shape(self, name: str, layer: int = -1):
+        r, c = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().rs_model_tensor_shape(self.handle, name.encode(), layer, ctypes.byref(r), ctypes.byref(c)))
+        return (r.value, c.value) if r.value > 1 else (c.value,)
+
+    def load_tensor(self, name: str, layer: int, array) -> None:
+        import numpy as np
+        if hasattr(array, "detach"):  # torch tensor
+            import torch
+            t = array.detach().contiguous().cpu()
+            array = t.view(torch.int16).numpy().view(np.uint16) if t.dtype == torch.bfloat16 else t.float().numpy()
+        a = np.ascontiguousarray(array)
+        if a.dtype == np.uint16:
+            dt = RS_DTYPE_BF16
+        else:
+            a = np.ascontiguousarray(a, dtype=np.float32)
+            dt = RS_DTYPE_F32
+        _check(lib().rs_model_load_tensor(self.device.handle, self.handle, name.encode(), layer,
+                                          a.ctypes.data_as(ctypes.c_void_p), dt, a.size))
+
+    def store_tensor(self, name: str, layer: int = -1, bf16_bits: bool = False):
+        """The tensor as numpy float32 (exact for bf16 weights) or, bf16_bits, uint16 bit patterns."""
+        import numpy as np
+        shape = self.tensor_shape(name, layer)
+        a = np.empty(shape, dtype=np.uint16 if bf16_bits else np.float32)
+        _check(lib().rs_model_store_tensor(self.device.handle, self.handle, name.encode(), layer,
+                                           a.ctypes.data_as(ctypes.c_void_p),
+                                           RS_DTYPE_BF16 if bf16_bits else RS_DTYPE_F32, a.size))
+        return a
+
+    def state_dict(self, bf16_bits: bool = False) -> dict:
+        return {full: self.store_tensor(*self._split(full), bf16_bits=bf16_bits) for full in self.checkpoint_names()}
+
+    def load_state_dict(self, sd: dict, strict: bool = True) -> None:
+        names = set(self.checkpoint_names())
+        if strict:
+            missing, extra = names - set(sd), set(sd) - names - set(self._optional)
+            if missing or extra:
+                raise InvalidArgument(f"load_state_dict: missing {sorted(missing)[:4]}, unexpected {sorted(extra)[:4]}")
+        for full, arr in sd.items():
+            if full in names:
+                self.load_tensor(*self._split(full), arr)
+
+    def save(self, path: str) -> None:
+        """numpy .npz of the checkpoint: bf16 weights as uint16 bit patterns, norm gains fp32."""
+        import numpy as np
+        out = {}
+        for full in self.checkpoint_names():
+            name, layer = self._split(full)
+            out[full] = self.store_tensor(name, layer, bf16_bits=not name.endswith("norm.weight"))
+        np.savez(path, **out)
+
+    def load(self, path: str) -> None:
+        import numpy as np
+        with np.load(path) as z:
+            self.load_state_dict({k: z[k] for k in z.files})
+
+    _optional = ()
+
+    _LAYER_TENSORS = ("self_attn.q_proj.weight", "self_attn.k_proj.weight", "self_attn.v_proj.weight",
+                      "self_attn.q_proj.bias", "self_attn.k_proj.bias", "self_attn.v_proj.bias",
+                      "self_attn.o_proj.weight", "mlp.gate_proj.weight", "mlp.up_proj.weight",
+                      "mlp.down_proj.weight", "post_attention_layernorm.weight")
+
 
 class TransformerModel(_NeuralModel):
     """Qwen2-shaped target with synthetic N(0, init_std) bf16 weights generated on the device."""
@@ -646,6 +719,29 @@ class TransformerModel(_NeuralModel):
                                            ctypes.byref(h)))
         self.handle = h
 
+    # Qwen2 checkpoint names (model.safetensors of Qwen2.5-*); the LM head is tied to the embedding
+    _optional = ("lm_head.weight",)
+
+    def checkpoint_names(self) -> List[str]:
+        names = ["model.embed_tokens.weight", "model.norm.weight"]
+        for i in range(self.shape.n_layers):
+            names.append(f"model.layers.{i}.input_layernorm.weight")
+            names += [f"model.layers.{i}.{t}" for t in self._LAYER_TENSORS]
+        return names
+
+    def _split(self, full: str):
+        parts = full.split(".")
+        if parts[0] == "model" and parts[1] == "layers":
+            return ".".join(parts[-2:]), int(parts[2])
+        return ".".join(parts[-2:]), -1
+
+    @staticmethod
+    def from_pretrained(shape: TransformerShape, state_dict: dict, device: Optional[Device] = None):
+        """A target with the given checkpoint tensors (HF Qwen2 names)."""
+        m = TransformerModel(shape, seed=0, device=device)
+        m.load_state_dict(state_dict)
+        return m
+
 
 class EagleDrafter(_NeuralModel):
     """EAGLE-3-style drafter bound to `target` (consumes its low/mid/high hidden states)."""
@@ -658,6 +754,14 @@ class EagleDrafter(_NeuralModel):
         _check(lib().rs_drafter_create(self.device.handle, target.handle, seed & (2 ** 64 - 1), version,
                                        ctypes.byref(h)))
         self.handle = h
+
+    # EAGLE-3 checkpoint names (one decoder layer "midlayer" over [norm(emb), hidden_norm(f)])
+    def checkpoint_names(self) -> List[str]:
+        return (["fc.weight", "midlayer.input_layernorm.weight", "midlayer.hidden_norm.weight", "norm.weight",
+                 "lm_head.weight"] + [f"midlayer.{t}" for t in self._LAYER_TENSORS])
+
+    def _split(self, full: str):
+        return ".".join(full.split(".")[-2:]), 0
 
     @staticmethod
     def _wrap(handle, target: TransformerModel) -> "EagleDrafter":

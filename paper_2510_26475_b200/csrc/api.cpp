@@ -924,6 +924,164 @@ int rs_model_tensor(const rs_model *m, const char *name, int32_t layer, void **p
     });
 }
 
+namespace {
+// A checkpoint tensor (Hugging Face Qwen2 / EAGLE-3 naming) as a strided view of the arena:
+// `rows` rows of `cols` elements, row r at dev + r * row_stride (elements of the device dtype).
+// q/k/v_proj are row slices of the fused QKV matrix; gate/up_proj are the even / odd rows of
+// the pairwise-interleaved gate/up matrix.
+struct CkptView {
+    char *dev = nullptr;
+    bool f32 = false;  // device dtype: fp32 (norm gains) or bf16
+    int64_t rows = 0, cols = 0, row_stride = 0;
+};
+
+CkptView ckpt_view(const rs_model *m, const std::string &nm, int layer) {
+    CkptView v;
+    auto bf = [&](void *p, int64_t rows, int64_t cols, int64_t stride) {
+        v.dev = static_cast<char *>(p);
+        v.rows = rows;
+        v.cols = cols;
+        v.row_stride = stride;
+    };
+    auto gain = [&](float *p, int64_t n) {
+        bf(p, 1, n, n);
+        v.f32 = true;
+    };
+    auto layer_view = [&](const LayerW &w, const TfShape &s, int d_in) -> bool {
+        const int64_t hq = (int64_t)s.H * s.hd, hk = (int64_t)s.KV * s.hd;
+        if (nm == "q_proj.weight") bf(w.qkv_w, hq, d_in, d_in);
+        else if (nm == "k_proj.weight") bf(w.qkv_w + hq * d_in, hk, d_in, d_in);
+        else if (nm == "v_proj.weight") bf(w.qkv_w + (hq + hk) * d_in, hk, d_in, d_in);
+        else if (nm == "q_proj.bias") bf(w.qkv_b, 1, hq, hq);
+        else if (nm == "k_proj.bias") bf(w.qkv_b + hq, 1, hk, hk);
+        else if (nm == "v_proj.bias") bf(w.qkv_b + hq + hk, 1, hk, hk);
+        else if (nm == "o_proj.weight") bf(w.o_w, s.d, hq, hq);
+        else if (nm == "gate_proj.weight") bf(w.gu_w, s.dff, s.d, 2 * (int64_t)s.d);
+        else if (nm == "up_proj.weight") bf(w.gu_w + s.d, s.dff, s.d, 2 * (int64_t)s.d);
+        else if (nm == "down_proj.weight") bf(w.down_w, s.d, s.dff, s.dff);
+        else if (nm == "post_attention_layernorm.weight") gain(w.ln2, s.d);
+        else return false;
+        return true;
+    };
+    if (m->kind == rs_model::Transformer) {
+        const auto *t = static_cast<const TransformerModel *>(m);
+        const TfShape &s = t->s;
+        if (nm == "embed_tokens.weight") bf(t->emb, s.V, s.d, s.d);
+        else if (nm == "norm.weight") gain(t->final_norm, s.d);
+        else {
+            if (layer < 0 || layer >= s.L) throw std::invalid_argument("rs_model_load_tensor: layer out of range");
+            const LayerW &w = t->layers[layer];
+            if (nm == "input_layernorm.weight") gain(w.ln1, s.d);
+            else if (!layer_view(w, s, s.d)) throw std::invalid_argument("rs_model_load_tensor: unknown tensor " + nm);
+        }
+    } else if (m->kind == rs_model::Drafter) {
+        const auto *dm = static_cast<const DrafterModel *>(m);
+        const TfShape &s = dm->s;
+        if (nm == "fc.weight") bf(dm->fc_w, s.d, 3 * (int64_t)s.d, 3 * (int64_t)s.d);
+        else if (nm == "input_layernorm.weight") gain(dm->norm_emb, s.d);  // EAGLE-3: norm of emb(x)
+        else if (nm == "hidden_norm.weight") gain(dm->norm_hid, s.d);      // EAGLE-3: norm of f
+        else if (nm == "norm.weight") gain(dm->final_norm, s.d);
+        else if (nm == "lm_head.weight") bf(dm->lm_w, s.V, s.d, s.d);
+        else if (!layer_view(dm->layer, s, 2 * s.d)) throw std::invalid_argument("rs_model_load_tensor: unknown tensor " + nm);
+    } else {
+        throw std::invalid_argument("rs_model_load_tensor: tabular models have no named tensors");
+    }
+    return v;
+}
+
+uint16_t f32_to_bf16_rne(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40);  // quiet NaN
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+float bf16_to_f32(uint16_t h) {
+    const uint32_t u = (uint32_t)h << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+// host rows (dtype 0 = bf16 bits, 1 = fp32; row-major, `cols` per row) <-> the strided view
+void ckpt_copy(rs_ctx *ctx, const CkptView &v, void *host, int dtype, int64_t n, bool load) {
+    if (dtype != RS_DTYPE_BF16 && dtype != RS_DTYPE_F32) throw std::invalid_argument("rs_model_load_tensor: dtype must be bf16 or f32");
+    if (n != v.rows * v.cols)
+        throw std::invalid_argument("rs_model_load_tensor: element count " + std::to_string(n) + " != " +
+                                    std::to_string(v.rows) + " x " + std::to_string(v.cols));
+    const size_t des = v.f32 ? 4 : 2;
+    const bool same = (dtype == RS_DTYPE_F32) == v.f32;
+    std::vector<char> conv;
+    char *h = static_cast<char *>(host);
+    if (!same) conv.resize((size_t)n * des);
+    if (load && !same) {
+        for (int64_t i = 0; i < n; ++i) {
+            if (v.f32) {
+                const float f = bf16_to_f32(static_cast<const uint16_t *>(host)[i]);
+                std::memcpy(conv.data() + 4 * i, &f, 4);
+            } else {
+                const uint16_t b = f32_to_bf16_rne(static_cast<const float *>(host)[i]);
+                std::memcpy(conv.data() + 2 * i, &b, 2);
+            }
+        }
+    }
+    char *src = same ? h : conv.data();
+    const size_t row_bytes = (size_t)v.cols * des, pitch = (size_t)v.row_stride * des;
+    if (load)
+        RS_CUDA(cudaMemcpy2DAsync(v.dev, pitch, src, row_bytes, row_bytes, (size_t)v.rows, cudaMemcpyHostToDevice, ctx->stream));
+    else
+        RS_CUDA(cudaMemcpy2DAsync(src, row_bytes, v.dev, pitch, row_bytes, (size_t)v.rows, cudaMemcpyDeviceToHost, ctx->stream));
+    RS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (!load && !same) {
+        for (int64_t i = 0; i < n; ++i) {
+            if (v.f32) {
+                float f;
+                std::memcpy(&f, conv.data() + 4 * i, 4);
+                static_cast<uint16_t *>(host)[i] = f32_to_bf16_rne(f);
+            } else {
+                uint16_t b;
+                std::memcpy(&b, conv.data() + 2 * i, 2);
+                static_cast<float *>(host)[i] = bf16_to_f32(b);
+            }
+        }
+    }
+}
+}  // namespace
+
+int rs_model_tensor_shape(const rs_model *m, const char *name, int32_t layer, int64_t *rows, int64_t *cols) {
+    return guard([&] {
+        need(m, "rs_model_tensor_shape");
+        need(name, "rs_model_tensor_shape: name");
+        const CkptView v = ckpt_view(m, name, layer);
+        if (rows) *rows = v.rows;
+        if (cols) *cols = v.cols;
+    });
+}
+
+int rs_model_load_tensor(rs_ctx *ctx, rs_model *m, const char *name, int32_t layer, const void *host, int32_t dtype,
+                         int64_t n) {
+    return guard([&] {
+        need(ctx, "rs_model_load_tensor");
+        need(m, "rs_model_load_tensor");
+        need(name, "rs_model_load_tensor: name");
+        need(host, "rs_model_load_tensor: host buffer");
+        ckpt_copy(ctx, ckpt_view(m, name, layer), const_cast<void *>(host), dtype, n, true);
+        // engines key their drafter-cache invalidation on the snapshot id: new weights = new snapshot
+        m->uid = rs_model::next_uid();
+    });
+}
+
+int rs_model_store_tensor(rs_ctx *ctx, const rs_model *m, const char *name, int32_t layer, void *host, int32_t dtype,
+                          int64_t n) {
+    return guard([&] {
+        need(ctx, "rs_model_store_tensor");
+        need(m, "rs_model_store_tensor");
+        need(name, "rs_model_store_tensor: name");
+        need(host, "rs_model_store_tensor: host buffer");
+        ckpt_copy(ctx, ckpt_view(m, name, layer), host, dtype, n, false);
+    });
+}
+
 void rs_prof_enable(int32_t on) { prof_enable(on != 0); }
 int rs_set_tuning(const char *key, int64_t value) {
     return guard([&] {
@@ -938,6 +1096,8 @@ int rs_set_tuning(const char *key, int64_t value) {
             rs::tuning().gemm2 = static_cast<int>(value);
         } else if (k == "pdl") {
             rs::tuning().pdl = static_cast<int>(value);
+        } else if (k == "attn_poly") {
+            rs::tuning().attn_poly = static_cast<int>(value);
         } else if (k == "kd_rows") {
             if (value < 0) throw std::invalid_argument("kd_rows must be >= 0");
             rs::tuning().kd_rows = static_cast<int>(value);

@@ -79,7 +79,8 @@ struct rs_model {
     std::atomic<int> refs{1};
     // Process-unique id: a snapshot allocated at a freed snapshot's address is still a new
     // snapshot (engines key their drafter-cache invalidation on it, not on the pointer).
-    const uint64_t uid = next_uid();
+    // Loading checkpoint tensors into a model (rs_model_load_tensor) gives it a fresh id.
+    uint64_t uid = next_uid();
     explicit rs_model(Kind k) : kind(k) {}
     static uint64_t next_uid() {
         static std::atomic<uint64_t> n{1};
