@@ -1096,8 +1096,6 @@ int rs_set_tuning(const char *key, int64_t value) {
             rs::tuning().gemm2 = static_cast<int>(value);
         } else if (k == "pdl") {
             rs::tuning().pdl = static_cast<int>(value);
-        } else if (k == "attn_poly") {
-            rs::tuning().attn_poly = static_cast<int>(value);
         } else if (k == "kd_rows") {
             if (value < 0) throw std::invalid_argument("kd_rows must be >= 0");
             rs::tuning().kd_rows = static_cast<int>(value);

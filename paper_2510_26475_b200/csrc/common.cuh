@@ -50,7 +50,6 @@ struct Tuning {
     int accept_cluster = 0;  // CTAs per sequence in the fused acceptance kernel: 0 auto, 1/2/4/8 forced
     int fused_stats = 0;     // drafter LM-head stats: 1 fused GEMM epilogue; 0 / -1 separate row-stats kernel
     int attn_trace = 0;      // diagnostics: layer + 1 whose attention pass timeline is printed
-    int attn_poly = 0;       // attention softmax: a quarter of the exponentials by polynomial on the FMA pipe
     int attn_skip = 0;       // diagnostics (wrong results): bit 0 softmax math, bit 1 score MMAs, bit 2 P.V MMAs, bit 3 exps, bit 4 S loads
     int pdl = 0;             // programmatic dependent launch on the forward path: 0 / 1 on, -1 off
     int gemm2 = 0;           // weight GEMMs on SM pairs (gemm_2sm.cu): 0 / 1 on, -1 single-SM kernel

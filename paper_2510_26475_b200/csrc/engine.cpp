@@ -39,7 +39,6 @@ Tuning &tuning() {
                     else if (k == "fused_stats") x.fused_stats = v;
                     else if (k == "attn_trace") x.attn_trace = v;
                     else if (k == "attn_skip") x.attn_skip = v;
-                    else if (k == "attn_poly") x.attn_poly = v;
                     else if (k == "pdl") x.pdl = v;
                     else if (k == "gemm2") x.gemm2 = v;
                     else if (k == "gemm_trace") x.gemm_trace = v;
