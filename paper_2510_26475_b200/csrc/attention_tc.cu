@@ -35,7 +35,9 @@
 //               columns (tcgen05.st), O rescale in TMEM when the running max moves (after the
 //               previous P.V completed); finally O / l as bf16.
 // TMEM (256 columns): O [0, 128), Q [128, 192), S(b) at 192 + 32 b.
+#include <algorithm>
 #include <cstdio>
+#include <vector>
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -82,6 +84,11 @@ constexpr int kSmem = 1024 + (kNK + kNV) * kKVBytes + kBarBytes + (int)sizeof(Pl
 static_assert(2 * (kSmem + 1024) <= 233472, "attention: two CTAs per SM must fit in shared memory");
 static_assert((2 * (kNK + kNV) + 2 + 2 + 2 + 1) * 8 + 4 <= kBarBytes, "barrier area");
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void cp16(uint32_t dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -126,6 +133,14 @@ __global__ void __launch_bounds__(kThreads, 2)
     // K landed, V landed, P ready (MMA), -, softmax start / end, -, -, S issue start / end
     const bool tr = trace && blockIdx.x == 0 && blockIdx.y == 0;
     if (tr && threadIdx.x == 0) trace[0] = clock64();
+    // per-CTA timeline (diagnostics): [start ns, prologue done ns, end ns, smid] after the pass trace
+    long long *ctat = trace ? trace + 1 + 12 * kMaxPasses + 4 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+    if (ctat && threadIdx.x == 0) {
+        ctat[0] = (long long)globaltimer_ns();
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        ctat[3] = smid;
+    }
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sK = smem;
@@ -198,6 +213,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const int np = pl.npasses;
+    if (ctat && threadIdx.x == 0) ctat[1] = (long long)globaltimer_ns();
     const size_t kvrow0 = (((size_t)layer * kv.B + it.seq) * kv.KV + kvh) * kv.max_ctx;
 
     if (warp == 0) {
@@ -453,6 +469,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     tc_fence_before();
     __syncthreads();
+    if (ctat && threadIdx.x == 0) ctat[2] = (long long)globaltimer_ns();
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
@@ -466,8 +483,8 @@ int attn_tc_max_tokens(int G) { return 2 * (128 / G); }
 long long *trace_buf() {
     static long long *p = nullptr;
     if (!p) {
-        RS_CUDA(cudaMalloc(&p, 8 * (1 + 12 * kMaxPasses)));
-        RS_CUDA(cudaMemset(p, 0, 8 * (1 + 12 * kMaxPasses)));
+        RS_CUDA(cudaMalloc(&p, 8 * (1 + 12 * kMaxPasses + 4 * 16384)));
+        RS_CUDA(cudaMemset(p, 0, 8 * (1 + 12 * kMaxPasses + 4 * 16384)));
     }
     return p;
 }
@@ -493,16 +510,45 @@ void k_attention_tc(const bf16 *q, const RowDesc *rows, const AttnItem *items, c
                tuning().attn_skip);
     if (tuning().attn_trace) {
         RS_CUDA(cudaStreamSynchronize(st));
-        static long long host[1 + 12 * kMaxPasses];
-        RS_CUDA(cudaMemcpy(host, trace_buf(), sizeof(host), cudaMemcpyDeviceToHost));
+        const int nct = 2 * n_items * s.KV;
+        static std::vector<long long> host;
+        host.assign(1 + 12 * kMaxPasses + 4 * (size_t)nct, 0);
+        RS_CUDA(cudaMemcpy(host.data(), trace_buf(), host.size() * 8, cudaMemcpyDeviceToHost));
+        RS_CUDA(cudaMemset(trace_buf(), 0, host.size() * 8));
         if (tuning().attn_trace == layer + 1 && n_items >= 32) {
             fprintf(stderr, "attn trace layer %d items %d (cycles from CTA start):\n", layer, n_items);
             for (int j = 0; j < 64; ++j) {
-                const long long *h = host + 1 + 12 * j;
+                const long long *h = host.data() + 1 + 12 * j;
                 auto t = [&](int i) { return h[i] ? h[i] - host[0] : -1; };
                 fprintf(stderr, "  pass %2d issueK %6lld issueV %6lld | landK %6lld landV %6lld P %6lld | sm %6lld..%6lld | "
                         "S %6lld..%6lld\n", j, t(0), t(1), t(2), t(3), t(4), t(6), t(7), t(10), t(11));
             }
+            // per-CTA timeline (ns from the first CTA start): start, prologue, duration; CTAs that
+            // exited early (no second M-tile) have no record
+            const long long *c = host.data() + 1 + 12 * kMaxPasses;
+            long long t0 = -1, tend = 0;
+            std::vector<long long> st0, pro, dur;
+            std::vector<int> per_sm(1024, 0);
+            for (int i = 0; i < nct; ++i)
+                if (c[4 * i]) t0 = t0 < 0 ? c[4 * i] : std::min(t0, c[4 * i]);
+            for (int i = 0; i < nct; ++i) {
+                if (!c[4 * i]) continue;
+                st0.push_back(c[4 * i] - t0);
+                pro.push_back(c[4 * i + 1] - c[4 * i]);
+                dur.push_back(c[4 * i + 2] - c[4 * i]);
+                tend = std::max(tend, c[4 * i + 2] - t0);
+                per_sm[c[4 * i + 3] & 1023]++;
+            }
+            auto pct = [](std::vector<long long> v, double q) {
+                std::sort(v.begin(), v.end());
+                return v.empty() ? 0LL : v[(size_t)(q * (v.size() - 1))];
+            };
+            int sm2 = 0, sm1 = 0;
+            for (int x : per_sm) sm2 += x >= 2, sm1 += x == 1;
+            fprintf(stderr, "  CTAs %zu (of %d), SMs with 1 / >=2: %d / %d; span %lld ns; start p50/p90/max %lld/%lld/%lld; "
+                    "prologue p50/max %lld/%lld; duration min/p50/p90/max %lld/%lld/%lld/%lld ns\n",
+                    dur.size(), nct, sm1, sm2, tend, pct(st0, .5), pct(st0, .9), pct(st0, 1), pct(pro, .5), pct(pro, 1),
+                    pct(dur, 0), pct(dur, .5), pct(dur, .9), pct(dur, 1));
         }
     }
     RS_LAUNCHED();
