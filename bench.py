@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--no-profile", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--no-port", action="store_true", help="skip the CPU-port timing of the same workload")
+    p.add_argument("--port-seconds", type=float, default=15.0)
     p.add_argument("--kd", type=int, default=4, help="rollouts per GPU in the online KD update leg (0 = off)")
     p.add_argument("--no-tuner-leg", action="store_true", help="skip the dynamic-tuning (cfg3-style) leg")
     p.add_argument("--no-b256-leg", action="store_true", help="skip the batch-256 north-star leg")
@@ -174,6 +176,41 @@ def cpu_time(lib, kind, target, drafter, reqs, forced, threads, budget_s):
             aln += len(out["accept_lens"])
         runs += 1
     return tok / secs, (als / aln if aln else 0.0), runs, secs
+
+
+def port_leg(args, s, t, n, budget_s):
+    """The SAME workload on the host cores: the CPU port of the transformer models (oracle/tf_cpu.cpp,
+    identical architecture and synthetic weights) driven by the restated reference engine
+    (oracle/restate.cpp, row by row like the reference's own engine). Context K/V of `ctx` positions
+    is synthetic (a CPU prefill of it would take minutes); every timed row is a real forward over
+    it. Bounded sample: SD cycles of one request until ~budget_s."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_client import Oracle
+    orc = Oracle()
+    sh = {"3b": (151936, 2048, 36, 16, 2, 11008), "7b": (152064, 3584, 28, 28, 4, 18944),
+          "14b": (152064, 5120, 48, 40, 8, 13824), "tiny": (1024, 256, 2, 4, 2, 512)}[args.model]
+    t0 = time.perf_counter()
+    pid = orc("tf_cpu_create", shape=dict(zip(("V", "d", "L", "H", "KV", "dff"), sh)), seed=20251026,
+              drafter_seed=4242)["id"]
+    init_s = time.perf_counter() - t0
+    threads = os.cpu_count()
+    tok = secs = 0.0
+    cycles = 0
+    try:
+        while secs < budget_s or cycles == 0:
+            out = orc("tf_cpu_bench", id=pid, ctx=args.ctx, batch=1, steps=1, cfg={"s": s, "t": t, "n": n, "enabled": True},
+                      seed=7 + cycles, threads=threads)
+            tok += out["tokens"]
+            secs += out["seconds"]
+            cycles += 1
+    finally:
+        orc("tf_cpu_free", id=pid)
+    return {"value": round(tok / secs, 3), "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"{cycles} SD cycles tree({s},{t},{n}) of one request of the {args.model} target + EAGLE drafter "
+                      f"(CPU port oracle/tf_cpu.cpp, same architecture and synthetic weights, fp32 on bf16 weights) "
+                      f"through the restated reference engine, context {args.ctx} (synthetic K/V), {secs:.1f} s on "
+                      f"{threads} host threads; weight generation {init_s:.1f} s not timed",
+            "tokens": int(tok), "seconds": round(secs, 2)}
 
 
 def reference_arm(args, rank, world):
@@ -695,6 +732,10 @@ def main():
                          f"{args.batch}, tree({s},{t},{n}), max_len 256, eos_bias -3, {secs:.1f} s wall on "
                          f"{threads} host threads"}
         cpu["same_workload_on_gpu"] = same_workload_leg(rb, dev, lib, kind, tgt_j, drf_j, creqs, forced, al)
+        if not args.no_port:
+            # the GPU arm's own workload on the host cores (CPU port of the same models)
+            cpu["same_workload_port"] = port_leg(args, s, t, n, args.port_seconds)
+            cpu["same_workload_port"]["gpu_over_port_e2e"] = round((e2e_tok / e2e_s) / cpu["same_workload_port"]["value"], 1)
 
     line = {"metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,

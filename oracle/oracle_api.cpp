@@ -10,6 +10,9 @@
 #include <mutex>
 
 #include "restate.hpp"
+#include "tf_cpu.hpp"
+#include <chrono>
+#include <omp.h>
 
 using nlohmann::json;
 using namespace orc;
@@ -32,8 +35,27 @@ std::mutex g_reg_mu;
 std::map<int, std::shared_ptr<LookupModel>> g_reg;
 int g_reg_next = 1;
 
+// CPU transformer ports (tf_cpu.hpp), created by op "tf_cpu_create" and referenced as
+// {"kind": "tf_cpu_target" | "tf_cpu_drafter", "id": k}.
+struct TfPair {
+    std::shared_ptr<TfWeights> w;
+    std::shared_ptr<CpuTransformer> target;
+    std::shared_ptr<CpuEagleDrafter> drafter;
+};
+std::map<int, TfPair> g_tf;
+int g_tf_next = 1;
+
+TfPair & tf_of(const json & j) {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    auto it = g_tf.find(j.at("id").get<int>());
+    if (it == g_tf.end()) throw std::invalid_argument("tf_cpu: unknown id");
+    return it->second;
+}
+
 std::shared_ptr<Model> model_of(const json & j) {
     const std::string kind = j.value("kind", "tabular");
+    if (kind == "tf_cpu_target") return tf_of(j).target;
+    if (kind == "tf_cpu_drafter") return tf_of(j).drafter;
     if (kind == "lookup_ref") {
         std::lock_guard<std::mutex> lk(g_reg_mu);
         auto it = g_reg.find(j.at("id").get<int>());
@@ -229,8 +251,113 @@ json op_profile_table(const json & req) {
     return {{"best", best}, {"solve", solved}, {"csv", t.to_csv()}};
 }
 
+// {"shape": {V, d, L, H, KV, dff, [rope_theta, eps, std, logit_scale]}, "seed", "drafter_seed",
+// "temperature", "drafter_version"} -> {"id"}: target + drafter weights generated like model.cu
+json op_tf_cpu_create(const json & req) {
+    const json & sh = req.at("shape");
+    TfShape s;
+    s.V = sh.at("V");
+    s.d = sh.at("d");
+    s.L = sh.at("L");
+    s.H = sh.at("H");
+    s.KV = sh.at("KV");
+    s.dff = sh.at("dff");
+    s.hd = sh.value("hd", 128);
+    s.rope_theta = sh.value("rope_theta", 1e6f);
+    s.eps = sh.value("eps", 1e-6f);
+    s.std = sh.value("std", 0.02f);
+    s.logit_scale = sh.value("logit_scale", 1.0f);
+    if (s.hd != 128 || s.H % s.KV) throw std::invalid_argument("tf_cpu: head_dim 128 and H % KV == 0 required");
+    TfPair p;
+    p.w = std::make_shared<TfWeights>();
+    p.w->init_target(s, req.at("seed").get<uint64_t>(), 0);
+    if (req.contains("drafter_seed")) p.w->init_drafter(req.at("drafter_seed").get<uint64_t>());
+    p.target = std::make_shared<CpuTransformer>(p.w, req.value("temperature", 1.0));
+    if (req.contains("drafter_seed")) p.drafter = std::make_shared<CpuEagleDrafter>(p.w, p.target, req.value("drafter_version", 0));
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    g_tf[g_tf_next] = std::move(p);
+    return {{"id", g_tf_next++}};
+}
+
+// {"id", "role": "target" | "drafter", "ctx", "depth"} -> {"logits"} (raw row, fp32 values)
+json op_tf_cpu_logits(const json & req) {
+    TfPair & p = tf_of(req);
+    const std::vector<int> ctx = req.at("ctx").get<std::vector<int>>();
+    if (req.value("role", "target") == "drafter") {
+        if (!p.drafter) throw std::invalid_argument("tf_cpu: no drafter");
+        return {{"logits", p.drafter->logits_at(ctx, req.value("depth", 0))}};
+    }
+    return {{"logits", p.target->logits(ctx)}};
+}
+
+// {"id", "name", "layer", "drafter": bool} -> {"bits"} bf16 bit patterns, or {"f32"} for gains
+json op_tf_cpu_tensor(const json & req) {
+    TfPair & p = tf_of(req);
+    const TfWeights & w = *p.w;
+    const std::string nm = req.at("name");
+    const bool dr = req.value("drafter", false);
+    const TfLayer & L = dr ? w.dl : w.layers.at(req.value("layer", 0));
+    if (nm == "emb") return {{"bits", w.emb}};
+    if (nm == "lm_w") return {{"bits", w.lm_w}};
+    if (nm == "fc_w") return {{"bits", w.fc_w}};
+    if (nm == "qkv_w") return {{"bits", L.qkv_w}};
+    if (nm == "qkv_b") return {{"bits", L.qkv_b}};
+    if (nm == "o_w") return {{"bits", L.o_w}};
+    if (nm == "gu_w") return {{"bits", L.gu_w}};
+    if (nm == "down_w") return {{"bits", L.down_w}};
+    throw std::invalid_argument("tf_cpu: unknown tensor " + nm);
+}
+
+// Timing sample of the SAME workload as the GPU bench, on the host cores: the target's and the
+// drafter's caches hold `ctx` synthetic context positions, then `steps` engine steps (each one SD
+// cycle of the restated engine over the CPU transformer port) run for `batch` requests.
+json op_tf_cpu_bench(const json & req) {
+    TfPair & p = tf_of(req);
+    const int ctx = req.at("ctx"), batch = req.value("batch", 1), steps = req.value("steps", 1);
+    if (req.contains("threads")) omp_set_num_threads(req.at("threads").get<int>());
+    std::vector<RequestState> reqs;
+    for (int b = 0; b < batch; ++b) {
+        RequestState r;
+        r.id = b;
+        uint64_t st = 0x5eed + b;
+        for (int i = 0; i < ctx; ++i) r.prompt.push_back(static_cast<int>(splitmix64(st) % (p.w->s.V - 1)));
+        r.eos_bias = req.value("eos_bias", -20.0);
+        r.max_len = req.value("max_len", 256);
+        r.rng = DecodeRng::from_seed(req.value("seed", uint64_t{1}), b);
+        // every context position but the last is synthetic: the first step computes the last
+        // prompt row and then runs real SD cycles over the cache
+        p.target->synthetic_prefix(r.prompt, ctx - 1, 1000 + b);
+        if (p.drafter) p.drafter->synthetic_prefix(r.prompt, ctx - 1, 2000 + b);
+        reqs.push_back(std::move(r));
+    }
+    std::function<std::shared_ptr<const Model>()> snap;
+    if (p.drafter) {
+        auto d = p.drafter;
+        snap = [d]() { return d; };
+    }
+    BatchEngine eng(*p.target, snap, nullptr, std::move(reqs), cfg_of(req.at("cfg")), mode_of(req), false);
+    eng.step();  // prompt rows (not timed): the engine's prefill of the last context position
+    size_t before = 0;
+    for (const auto & r : eng.requests()) before += r.generated.size();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < steps && !eng.all_done(); ++i) eng.step();
+    const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    size_t after = 0;
+    for (const auto & r : eng.requests()) after += r.generated.size();
+    return {{"seconds", sec}, {"tokens", after - before}, {"threads", omp_get_max_threads()}, {"steps", steps}};
+}
+
 json dispatch(const json & req) {
     const std::string op = req.at("op");
+    if (op == "tf_cpu_create") return op_tf_cpu_create(req);
+    if (op == "tf_cpu_logits") return op_tf_cpu_logits(req);
+    if (op == "tf_cpu_tensor") return op_tf_cpu_tensor(req);
+    if (op == "tf_cpu_bench") return op_tf_cpu_bench(req);
+    if (op == "tf_cpu_free") {
+        std::lock_guard<std::mutex> lk(g_reg_mu);
+        g_tf.erase(req.at("id").get<int>());
+        return json::object();
+    }
     if (op == "run_generation") return op_run_generation(req);
     if (op == "spec_step_tree") return op_spec_step_tree(req);
     if (op == "kd_update") return op_kd_update(req);
