@@ -72,7 +72,11 @@ int rs_ctx_create(int device, rs_ctx **out) {
         auto c = std::make_unique<rs_ctx>();
         c->device = device;
         RS_CUDA(cudaSetDevice(device));
-        RS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        // the rollout path is latency-critical: its stream gets the GREATEST priority (background
+        // work -- an asynchronous learner's update -- runs at the least, learner.cpp)
+        int least = 0, greatest = 0;
+        RS_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        RS_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, greatest));
         c->own_stream = true;
         RS_CUDA(cudaEventCreate(&c->ev0));
         RS_CUDA(cudaEventCreate(&c->ev1));

@@ -287,6 +287,14 @@ int rs_learner_create(rs_ctx *ctx, const rs_model *drafter, rs_kd_policy policy,
         l->async = async != 0;
         if (l->async) {
             rs_abi::rethrow(rs_ctx_create(ctx->device, &l->own));
+            // the update is background work: its stream gets the LEAST priority, so the block
+            // scheduler hands freed SMs to the rollout's kernels first and the KD kernels fill the
+            // gaps (with equal priorities the two streams' kernels interleave and every rollout
+            // step waits behind KD CTAs)
+            int least = 0, greatest = 0;
+            RS_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            RS_CUDA(cudaStreamDestroy(l->own->stream));
+            RS_CUDA(cudaStreamCreateWithPriority(&l->own->stream, cudaStreamNonBlocking, least));
             rs_learner *raw = l.get();
             l->worker = std::thread([raw] { raw->worker_loop(); });
         }
