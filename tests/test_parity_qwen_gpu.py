@@ -204,3 +204,33 @@ def test_mean_accept_len_definition(models):
         assert all(0 <= a <= 5 for a in r.accept_lens)
     al = [a for r in eng.requests() for a in r.accept_lens]
     assert rb.mean_accept_len(al) == pytest.approx(sum(al) / len(al))
+
+
+def test_north_star_batch256_greedy_sd_equals_greedy_decode():
+    """BASELINE north star: the 3B-geometry SD step at BATCH 256 (the bench's north-star leg) still
+    decodes exactly like greedy decoding, request for request -- attention items, GEMM token
+    tiles and acceptance clusters are all at their batch-256 sizes."""
+    shape = shape_of("3b", max_len=6)
+    tgt = rb.TransformerModel(shape, seed=20251026)
+    drf = rb.EagleDrafter(tgt, seed=4242, version=1)
+    reqs = lambda: make_requests(shape, 256, 6, seed=31)  # noqa: E731
+    want = [r.generated for r in run(tgt, drf, reqs(), rb.SDConfig.off(), "greedy").requests()]
+    got = [r.generated for r in run(tgt, drf, reqs(), rb.SDConfig.tree(1, 4, 5), "greedy").requests()]
+    assert all(len(w) == 6 for w in want) and got == want
+    del tgt, drf
+    torch.cuda.empty_cache()
+
+
+def test_bench_config_batch64_replay_bit_exact(oracle):
+    """The bench's own configuration -- 3B geometry, batch 64, tree(1,4,5), rejection sampling at
+    T = 1 -- replayed by the CPU oracle on the engine's captured rows: tokens, accept lengths,
+    ledger and log-probabilities bit-exact for every one of the 64 requests."""
+    shape = shape_of("3b", max_len=4)
+    tgt = rb.TransformerModel(shape, seed=20251026)
+    drf = rb.EagleDrafter(tgt, seed=4242, version=1)
+    cfg = rb.SDConfig.tree(1, 4, 5)
+    eng = run(tgt, drf, make_requests(shape, 64, 4, seed=37), cfg, "sample", capture=True)
+    reqs, tl, dl = _replay(oracle, eng, shape.vocab, "sample", cfg)
+    assert len(reqs) == 64 and tl.added > 64 * 5
+    del eng, tgt, drf
+    torch.cuda.empty_cache()
