@@ -439,6 +439,19 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                     }
                 asm volatile("bar.sync 4, 256;" ::: "memory");
             }
+            // the epilogue's first global inputs do not depend on the MMAs: in flight before the
+            // accumulator is ready (the first residual rows; the QKV bias and first cos / sin)
+            float4 cur[2][8];
+            float4 cs[4][4];
+            float qb = 0.f;
+            if constexpr (EPI == kEpiResidual) {
+                if (splits == 1 && grp < BT / 32) resid_prefetch(ep, f0 + q * 32, t0 + grp * 32, F, T, cur[0]);
+            } else if constexpr (EPI == kEpiQKVRope) {
+                const int tid = q * 32 + lane;
+                qb = __bfloat162float(static_cast<const __nv_bfloat16 *>(ep.bias)[f0 + tid]);
+                if (f0 / 128 < ep.qkv.H + ep.qkv.KV && grp < BT / 32)
+                    rope_cs_load(ep.qkv, tok_tab, t0, t0 + grp * 32, T, tid, cs);
+            }
             mbar_wait(&tfull[acc], (it >> 1) & 1);
             if (g2trace && blockIdx.x == 0 && threadIdx.x == 128 && it == 0) g2trace[g2slot * 8 + 4] = clock64();
             tc_fence_after();
@@ -510,9 +523,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
             if constexpr (EPI == kEpiQKVRope) {
                 const int head = f0 / 128, tid = q * 32 + lane;
                 const bool rope = head < ep.qkv.H + ep.qkv.KV;  // q and k heads rotate, v heads do not
-                const float b = __bfloat162float(static_cast<const __nv_bfloat16 *>(ep.bias)[f0 + tid]);
-                float4 cs[4][4];
-                if (rope && grp < BT / 32) rope_cs_load(ep.qkv, tok_tab, t0, t0 + grp * 32, T, tid, cs);
+                const float b = qb;
 #pragma unroll 1
                 for (int c = grp; c < BT / 32; c += 2) {
                     epi2_qkv_rope(ep, tb + c * 32, head, q, t0 + c * 32, T, reinterpret_cast<float(*)[132]>(stg_grp),
@@ -522,8 +533,9 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                 }
             } else if constexpr (EPI == kEpiResidual) {
                 // software-pipelined: chunk c + 1's residual rows are in flight while chunk c is done
-                float4 cur[2][8];
-                if (grp < BT / 32) resid_prefetch(ep, f0 + q * 32, t0 + grp * 32, F, T, cur[0]);
+                // (the first chunk's were issued before the accumulator wait; after a split-K
+                // reduction they are read now, the other splits having updated nothing)
+                if (splits > 1 && grp < BT / 32) resid_prefetch(ep, f0 + q * 32, t0 + grp * 32, F, T, cur[0]);
 #pragma unroll
                 for (int i = 0, c = grp; c < BT / 32; ++i, c += 2) {
                     if (c + 2 < BT / 32) resid_prefetch(ep, f0 + q * 32, t0 + (c + 2) * 32, F, T, cur[(i + 1) & 1]);
