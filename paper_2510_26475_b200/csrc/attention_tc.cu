@@ -2,7 +2,8 @@
 // cores (sm_100a).
 //
 // A work item = up to two 128-row M-tiles of one (sequence, kv head): row = token * G + head
-// (T = 128 / G tokens per tile). One CTA per (item, M-tile, kv head). Keys are visited in
+// (at most 128 / G tokens per tile; an item of more splits its tokens evenly between the two
+// tiles, so the two CTAs carry the same softmax load -- attn_tile_tokens). One CTA per (item, M-tile, kv head). Keys are visited in
 // LOGICAL order in passes of kAttnChunk = 32 positions; a pass = (key block, key group). Blocks
 // wholly below the tree start are shared by every token of the item; the blocks that reach into
 // the tree are replayed once per group of tokens sharing a key mapping (the tokens of one draft
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int tile = blockIdx.x & 1;
     const AttnItem it = items[blockIdx.x >> 1];  // host-uploaded plan: independent of the previous kernel
     const int G = H / KV;
-    const int T = 128 / G;
+    const int T = attn_tile_tokens(it.nrows, 128 / G);  // tokens of the first M-tile (tf_pair.cpp plan_tc)
     pdl_trigger();
     if (tile * T >= it.nrows) return;  // the item has no second M-tile (uniform per CTA)
     // trace (diagnostics, CTA (0, 0) only): [0] start; per pass j at 1 + 12 j: K issue, V issue,

@@ -123,6 +123,10 @@ struct AttnPlan {
     const AttnGroup *groups = nullptr;
     const int16_t *tok_grp = nullptr;  // per forward row: group index within its item
 };
+// Tokens of an attention item's first M-tile (tmax = 128 / G): items that need two tiles split
+// their tokens evenly (tree items of 1 + t * n tokens would otherwise leave the second tile mostly
+// empty while the first carries 128 rows). Host plan and kernel use this one definition.
+__host__ __device__ inline int attn_tile_tokens(int ntok, int tmax) { return ntok > tmax ? (ntok + 1) / 2 : tmax; }
 constexpr int kAttnChunk = 32;      // keys per pass of the tensor-core attention
 constexpr int kAttnMaxPasses = 400;
 constexpr int kAttnMaxGroups = 64;

@@ -208,7 +208,7 @@ struct Batch {
         passes.clear();
         groups.clear();
         tok_grp.assign(rows.size(), 0);
-        const int T = 128 / G;
+        const int Tmax = 128 / G;
         for (auto &it : items) {
             it.pass0 = (int)passes.size();
             it.grp0 = (int)groups.size();
@@ -239,7 +239,7 @@ struct Batch {
                     uint8_t tiles = 0;
                     for (int k = 0; k < ntok; ++k)
                         if ((g < 0 || tok_grp[it.row0 + k] == g) && rows[it.row0 + k].pos >= c0)
-                            tiles |= (uint8_t)(1u << (k / T));
+                            tiles |= (uint8_t)(1u << (k / attn_tile_tokens(ntok, Tmax)));
                     if (!tiles) continue;
                     const int ch = g < 0 ? -1 : groups[it.grp0 + g].chain;
                     const bool contiguous = ch < 0 || (ch == 0 && it.tbase == it.ltree);
@@ -248,7 +248,7 @@ struct Batch {
             }
             it.npass = (int)passes.size() - it.pass0;
             it.ngrp = ng;
-            if (it.npass > kAttnMaxPasses || ng > kAttnMaxGroups || ntok > 2 * T)
+            if (it.npass > kAttnMaxPasses || ng > kAttnMaxGroups || ntok > 2 * Tmax)
                 throw std::runtime_error("attention plan exceeds the kernel's limits");
         }
     }
