@@ -379,7 +379,7 @@ def tuner_leg(args, rb, target, drafter, reqs, dev, stream, max_len, cfg, world,
     buckets, grid = tuner_grid(args, rb, cfg)
     # measured at the rollout's own context length: attention cost, and with it the argmin,
     # depends on it
-    table = rb.profile_measured(target, drafter, buckets, grid, prompt_len=args.ctx, warmup=1, cycles=3)
+    table = rb.profile_measured(target, drafter, buckets, grid, prompt_len=args.ctx, warmup=1, cycles=8)
     prof_s = time.perf_counter() - t0
     fresh = [rb.RequestState(r.id, list(r.prompt), r.eos_bias, max_len, rb.DecodeRng.from_seed(11, r.id))
              for r in reqs]
@@ -588,7 +588,7 @@ def main():
     if args.tuner:
         t_prof = time.perf_counter()
         buckets, grid = tuner_grid(args, rb, cfg)
-        table = rb.profile_measured(target, drafter, buckets, grid, prompt_len=args.ctx, warmup=1, cycles=3)
+        table = rb.profile_measured(target, drafter, buckets, grid, prompt_len=args.ctx, warmup=1, cycles=8)
         tuner = {"profile_s": round(time.perf_counter() - t_prof, 2),
                  "best": {b: table.best_for_bucket(b).key() for b in buckets},
                  "grid": ["off"] + [c.key() for c in grid], "source": "measured device ms per emitted token"}
