@@ -37,6 +37,7 @@ Tuning &tuning() {
                     const int v = std::atoi(kv.c_str() + eq + 1);
                     if (k == "accept_cluster") x.accept_cluster = v;
                     else if (k == "fused_stats") x.fused_stats = v;
+                    else if (k == "accept_minb") x.accept_minb = v;
                     else if (k == "attn_trace") x.attn_trace = v;
                     else if (k == "attn_skip") x.attn_skip = v;
                     else if (k == "pdl") x.pdl = v;

@@ -643,8 +643,10 @@ __global__ void redraft_check_kernel(SdDev d) {
     atomicExch(d.flag, 1);
 }
 
-template <class T>
-__global__ void __launch_bounds__(512, 1) accept_kernel(SdDev d, int round, int naive) {
+// MB = minimum resident CTAs per SM the register budget is sized for: 1 (up to 512 threads) or,
+// for the 256-thread clusters of large vocabularies, 3 / 4 (a wave holds more sequences' clusters)
+template <class T, int MB>
+__global__ void __launch_bounds__(MB == 1 ? 512 : 256, MB) accept_kernel(SdDev d, int round, int naive) {
     pdl_trigger();
     pdl_wait();
     // an EOS-shortened chain shifted the draft-stream offsets of later chains: this optimistic
@@ -1017,6 +1019,9 @@ void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t s
     // algorithmic bytes: every target row of the round plus every drafter row
     const double es = rt == RowType::F64 ? 8.0 : 4.0;
     ProfScope prof("accept", 0, (double)d.nact * (naive ? 1 : 2 * d.slots - 1) * d.V * es, st);
+    // Register budget: 256-thread CTAs compiled for 4 resident per SM (64 registers, some spills)
+    // -- measured at cfg2 (batch 64, V = 152K): 0.569 ms vs 0.657 at 2 per SM (128 registers) and
+    // 0.625 at 3: a wave holds every sequence's cluster. Results are bitwise the same.
     // Large vocabularies: a cluster of up to 8 CTAs per sequence -- the residual passes are fp64 /
     // load-latency bound, so more CTAs in flight win even past one resident wave. Measured (cfg2,
     // V = 152K): batch 32 / 64 -> 8 CTAs (0.39 / 0.62 ms vs 0.57 / 0.68 at 4); batch 256 -> 4
@@ -1052,8 +1057,16 @@ void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t s
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     const int nv = naive ? 1 : 0;
-    if (rt == RowType::F64) RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<double>, d, round, nv));
-    else RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<float>, d, round, nv));
+    const int mb = threads == 256 ? tuning().accept_minb : 1;
+    if (rt == RowType::F64) {
+        if (mb == 4) RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<double, 4>, d, round, nv));
+        else if (mb == 3) RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<double, 3>, d, round, nv));
+        else RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<double, 1>, d, round, nv));
+    } else {
+        if (mb == 4) RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<float, 4>, d, round, nv));
+        else if (mb == 3) RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<float, 3>, d, round, nv));
+        else RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<float, 1>, d, round, nv));
+    }
     RS_LAUNCHED();
 }
 
