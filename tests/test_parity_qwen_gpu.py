@@ -234,3 +234,33 @@ def test_bench_config_batch64_replay_bit_exact(oracle):
     assert len(reqs) == 64 and tl.added > 64 * 5
     del eng, tgt, drf
     torch.cuda.empty_cache()
+
+
+def test_cfg4_long_context_14b_8k(oracle):
+    """BASELINE cfg4's long-context regime: Qwen2.5-14B head geometry (G = 5, V = 152064, 4 layers)
+    at 8K contexts -- ~260 key passes per attention item, the drafter's first catch-up longer than
+    its 2048-row workspace (chunked) -- with greedy SD == greedy decode and the oracle's bit-exact
+    replay of rejection sampling at T = 1 on the engine's own rows."""
+    g = GEOM["14b"]
+    ctx = 8192
+    shape = rb.TransformerShape(g["vocab"], g["d_model"], LAYERS, g["n_heads"], g["n_kv_heads"], 128, g["d_ff"],
+                                max_ctx=ctx + 8 + 6 + 64)
+    tgt = rb.TransformerModel(shape, seed=20251026)
+    drf = rb.EagleDrafter(tgt, seed=4242, version=1)
+    rng = random.Random(41)
+
+    def reqs(max_len, seed):
+        return [rb.RequestState(i, [rng.randrange(shape.vocab - 1) for _ in range(ctx + i)], -20.0, max_len,
+                                rb.DecodeRng.from_seed(seed, i)) for i in range(2)]
+
+    base = reqs(6, 43)
+    clone = lambda: [rb.RequestState(r.id, list(r.prompt), r.eos_bias, r.max_len, rb.DecodeRng.from_seed(43, r.id))  # noqa: E731
+                     for r in base]
+    want = [r.generated for r in run(tgt, drf, clone(), rb.SDConfig.off(), "greedy").requests()]
+    got = [r.generated for r in run(tgt, drf, clone(), rb.SDConfig.tree(1, 4, 5), "greedy").requests()]
+    assert all(len(w) == 6 for w in want) and got == want
+    cfg = rb.SDConfig.tree(1, 4, 5)
+    eng = run(tgt, drf, clone(), cfg, "sample", capture=True)
+    _replay(oracle, eng, shape.vocab, "sample", cfg)
+    del eng, tgt, drf
+    torch.cuda.empty_cache()
