@@ -264,3 +264,74 @@ def test_cfg4_long_context_14b_8k(oracle):
     _replay(oracle, eng, shape.vocab, "sample", cfg)
     del eng, tgt, drf
     torch.cuda.empty_cache()
+
+
+def test_cfg3_dynamic_tuning_7b_replay_bit_exact(oracle):
+    """BASELINE cfg3's dynamic SD-config tuning at the 7B head geometry (G = 7, V = 152064): a
+    ProfileTable whose best configuration changes as requests finish (server.cpp:21-54,
+    :266-349), so the engine switches trees between cycles. Greedy decoding is reproduced token
+    for token, and the oracle's run_generation -- given the same table -- replays rejection
+    sampling on the engine's own rows bit-exactly, switch events and ledger included."""
+    shape = shape_of("7b", max_len=14)
+    tgt = rb.TransformerModel(shape, seed=20251026)
+    drf = rb.EagleDrafter(tgt, seed=4242, version=1)
+    buckets = [1, 2, 4, 8]
+    best = {1: rb.SDConfig.chain(3), 2: rb.SDConfig.tree(1, 2, 3), 4: rb.SDConfig.tree(1, 4, 5),
+            8: rb.SDConfig.tree(1, 2, 2)}
+    grid = [rb.SDConfig.chain(3), rb.SDConfig.tree(1, 2, 3), rb.SDConfig.tree(1, 4, 5), rb.SDConfig.tree(1, 2, 2)]
+
+    def table():
+        t = rb.ProfileTable(buckets)
+        for b in buckets:
+            t.set_entry(b, rb.SDConfig.off(), 10.0)
+            for c in grid:
+                t.set_entry(b, c, 1.0 if c == best[b] else 5.0)
+        t.finalize()
+        return t
+
+    rng = random.Random(53)
+    prompts = [[rng.randrange(shape.vocab - 1) for _ in range(CTX + i)] for i in range(8)]
+    lens = [3, 5, 7, 9, 11, 12, 13, 14]  # requests finish one by one: the active batch crosses the buckets
+
+    def reqs():
+        return [rb.RequestState(i, list(prompts[i]), -20.0, lens[i], rb.DecodeRng.from_seed(61, i)) for i in range(8)]
+
+    def run_t(mode, capture=False):
+        eng = rb.BatchEngine(tgt, lambda: drf, table(), rb.TimingModel(), reqs(), rb.SDConfig.off(), mode,
+                             record_full_logprobs=False)
+        if capture:
+            eng.set_capture(True)
+        while not eng.all_done():
+            eng.step()
+        return eng
+
+    want = [r.generated for r in run(tgt, drf, reqs(), rb.SDConfig.off(), "greedy").requests()]
+    g = run_t("greedy")
+    assert [r.generated for r in g.requests()] == want
+    eng = run_t("sample", capture=True)
+    sw = eng.switches()
+    assert len({s.to.key() for s in sw}) >= 2, [(s.cycle, s.active_batch, s.to.key()) for s in sw]
+    done = eng.requests()
+    full = [r.prompt + r.generated for r in done]
+    meta = eng.captured_meta()
+    tl = oracle.lookup(shape.vocab, 1.0, depth_aware=False)
+    dl = oracle.lookup(shape.vocab, 1.0, depth_aware=True)
+    for first in range(0, len(meta), 64):
+        rows = eng.captured_logits_f32(first, min(64, len(meta) - first))
+        for j, row in enumerate(rows):
+            role, req, cl, ext = meta[first + j]
+            (tl if role == 1 else dl).add(full[req][:cl] + ext, len(ext) if role == 0 else 0, row)
+    entries = [{"bucket": b, "s": c.rounds, "t": c.branching, "n": c.draft_len, "enabled": c.enabled,
+                "time_per_token": 10.0 if not c.enabled else (1.0 if c == best[b] else 5.0)}
+               for b in buckets for c in [rb.SDConfig.off()] + grid]
+    exp = oracle("run_generation", target=tl.json(), drafter=dl.json(), table={"buckets": buckets, "entries": entries},
+                 requests=[{"id": r.id, "prompt": r.prompt, "eos_bias": r.eos_bias, "max_len": r.max_len, "seed": 61,
+                            "stream": r.id} for r in done], verify_mode="sample", record_logprobs=False)
+    assert [r.generated for r in done] == [s["response"] for s in exp["samples"]]
+    assert [r.accept_lens for r in done] == [s["accept_lens"] for s in exp["samples"]]
+    assert [list(e) for e in eng.ledger()] == exp["ledger"]
+    assert [(s.cycle, s.active_batch, s.to.key()) for s in sw] == \
+        [(e["cycle"], e["active_batch"], rb.SDConfig(e["to"]["s"], e["to"]["t"], e["to"]["n"], e["to"]["enabled"]).key())
+         for e in exp["switches"]]
+    del eng, g, tgt, drf
+    torch.cuda.empty_cache()
