@@ -105,7 +105,10 @@ struct Cfg2 {
     static_assert(kStages >= 2, "gemm2: ring needs at least two stages");
 };
 
-__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+// SiLU with the approximate division (MUFU.RCP + FMUL): the IEEE quotient's special-case check
+// and slow path sat in every SwiGLU epilogue chunk; the output is rounded to bf16 anyway.
+// g -> -inf: __expf(-g) = inf, __fdividef(g, inf) = -0.
+__device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 // Epilogue of one 32-token chunk of this warp's 32 feature rows f0w .. f0w + 31 (lane = row).
 // The accumulator (thread = feature row, registers = tokens) is transposed through a

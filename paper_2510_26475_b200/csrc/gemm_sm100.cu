@@ -41,7 +41,7 @@ struct Cfg {
                                        (static_cast<uint32_t>(BM >> 4) << 24);
 };
 
-__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+__device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.0f + __expf(-g)); }  // as gemm_2sm.cu
 
 // Epilogue for one thread = one output row, 32 consecutive accumulator columns.
 template <int EPI, int BN>
