@@ -157,6 +157,9 @@ int64_t rs_launch_count(void);
 void rs_launch_count_reset(void);
 
 /* ---- context ------------------------------------------------------------------------- */
+/* A context owns a non-blocking stream at the device's GREATEST priority (the rollout path is
+   latency-critical); an asynchronous learner's worker context runs at the LEAST priority, so its
+   update fills gaps instead of delaying rollout kernels. rs_ctx_set_stream replaces the stream. */
 int rs_ctx_create(int device, rs_ctx **out);
 int rs_ctx_destroy(rs_ctx *ctx);
 int rs_ctx_sync(rs_ctx *ctx);
