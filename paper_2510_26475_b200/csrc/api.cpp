@@ -306,7 +306,7 @@ int rs_engine_create(rs_ctx *ctx, const rs_model *target, const rs_model *drafte
         e->d_st_logq.alloc((size_t)N * steps_cap);
         e->d_st_drafted.alloc((size_t)N * steps_cap);
         if (e->record_full) e->d_st_full.alloc((size_t)N * steps_cap * e->V);
-        e->d_cyc.alloc((size_t)N * 11);
+        e->d_cyc.alloc((size_t)N * 17);  // + [N][6] two-stage acceptance state
         e->d_round_cost.alloc((size_t)N * kMaxRounds * 3);
         e->d_chain.alloc((size_t)N * e->t_max * (e->n_max + 3));
         RS_CUDA(cudaMemset(e->d_chain.p, 0, e->d_chain.bytes()));
@@ -1100,6 +1100,8 @@ int rs_set_tuning(const char *key, int64_t value) {
             rs::tuning().gemm2 = static_cast<int>(value);
         } else if (k == "pdl") {
             rs::tuning().pdl = static_cast<int>(value);
+        } else if (k == "lazy_lm") {
+            rs::tuning().lazy_lm = static_cast<int>(value);
         } else if (k == "kd_rows") {
             if (value < 0) throw std::invalid_argument("kd_rows must be >= 0");
             rs::tuning().kd_rows = static_cast<int>(value);

@@ -38,6 +38,7 @@ Tuning &tuning() {
                     if (k == "accept_cluster") x.accept_cluster = v;
                     else if (k == "fused_stats") x.fused_stats = v;
                     else if (k == "accept_minb") x.accept_minb = v;
+                    else if (k == "lazy_lm") x.lazy_lm = v;
                     else if (k == "attn_trace") x.attn_trace = v;
                     else if (k == "attn_skip") x.attn_skip = v;
                     else if (k == "pdl") x.pdl = v;
@@ -204,6 +205,7 @@ SdDev rs_engine::dev(const rs_sdconfig &cfg, int nact) {
     d.n_rounds = c + 8 * n;
     d.rsel = c + 9 * n;
     d.racc = c + 10 * n;
+    d.stg = c + 11 * n;
     d.round_cost = d_round_cost.p;
     const size_t ch = (size_t)n * t_max;
     d.chain_tok = d_chain.p;
@@ -237,7 +239,9 @@ SdDev rs_engine::dev(const rs_sdconfig &cfg, int nact) {
     return d;
 }
 
-void rs_engine::capture_rows(const SdDev &d, bool verify, int depth) {
+// which (verify rows): 0 every row, 1 the roots only, 2 the selected chains only (lazy verify LM
+// head: the chains' rows exist after the branch point picked them, the others are never computed)
+void rs_engine::capture_rows(const SdDev &d, bool verify, int depth, int which) {
     // Debug path: copies the rows this launch produced plus their contexts to the host.
     RS_CUDA(cudaStreamSynchronize(ctx->stream));
     const int nact = d.nact;
@@ -246,6 +250,8 @@ void rs_engine::capture_rows(const SdDev &d, bool verify, int depth) {
     RS_CUDA(cudaMemcpy(neff.data(), d.n_eff, n * 4, cudaMemcpyDeviceToHost));
     RS_CUDA(cudaMemcpy(clen.data(), d.chain_len, clen.size() * 4, cudaMemcpyDeviceToHost));
     RS_CUDA(cudaMemcpy(ctok.data(), d.chain_tok, ctok.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> stg((size_t)n * 6, -1);
+    if (which == 2) RS_CUDA(cudaMemcpy(stg.data(), d.stg, stg.size() * 4, cudaMemcpyDeviceToHost));
     const size_t es = pair->row_type() == RowType::F64 ? 8 : 4;
     std::vector<char> row(V * es);
     auto grab = [&](const void *base, int a, int slot, int role, int r, const int *ext, int e) {
@@ -269,9 +275,10 @@ void rs_engine::capture_rows(const SdDev &d, bool verify, int depth) {
         const int ne = naive ? 0 : neff[r];
         if (!naive && ne < 0) continue;
         if (verify) {
-            grab(d.P, a, 0, 1, r, nullptr, 0);
-            if (naive) continue;
+            if (which != 2) grab(d.P, a, 0, 1, r, nullptr, 0);
+            if (naive || which == 1) continue;
             for (int i = 0; i < d.t; ++i) {
+                if (which == 2 && stg[(size_t)r * 6] != i) continue;
                 const int *ch = &ctok[((size_t)r * t_max + i) * n_max];
                 for (int j = 0; j < clen[(size_t)r * t_max + i]; ++j) grab(d.P, a, 1 + i * d.n + j, 1, r, ch, j + 1);
             }
@@ -287,6 +294,29 @@ void rs_engine::capture_rows(const SdDev &d, bool verify, int depth) {
             }
         }
     }
+}
+
+// One round's target verification + acceptance. Transformer pairs with a lazy verify LM head
+// (TransformerPair::lazy_lm_head) compute the root rows' logits, run the branch point (acceptance
+// stage 1), then the selected chains' logits and the chain verification (stage 2): the other
+// chains' rows -- most of the tree -- never go through the LM head.
+void rs_engine::verify_accept(const SdDev &d, int round, RowType rt, cudaStream_t st) {
+    prof_set_scope("verify");
+    pair->verify_rows(d, false, st);
+    if (!pair->lazy_lm_head(d)) {
+        if (capture) capture_rows(d, true, 0, 0);
+        prof_set_scope("accept");
+        sd_accept(d, round, false, rt, st);
+        return;
+    }
+    if (capture) capture_rows(d, true, 0, 1);
+    prof_set_scope("accept");
+    sd_accept(d, round, false, rt, st, 1);
+    prof_set_scope("verify");
+    pair->verify_rows_selected(d, st);
+    if (capture) capture_rows(d, true, 0, 2);
+    prof_set_scope("accept");
+    sd_accept(d, round, false, rt, st, 2);
 }
 
 // BatchEngine::step (server.cpp:266-349)
@@ -352,10 +382,7 @@ void rs_engine::step(rs_step_info *info) {
             sd_draft_sample(d, depth, rt, st);
         }
         sd_redraft_check(d, st);
-        prof_set_scope("verify");
-        pair->verify_rows(d, false, st);
-        prof_set_scope("accept");
-        sd_accept(d, 0, false, rt, st);
+        verify_accept(d, 0, rt, st);
         pair->after_accept(d, false, st);
         sd_cycle_end(d, false, st);
         RS_CUDA(cudaEventRecord(ctx->ev1, st));
@@ -379,7 +406,7 @@ void rs_engine::step(rs_step_info *info) {
                     prof_set_scope("draft");
                     pair->draft_rows(d, depth, st);
                     sd_draft_sample(d, depth, rt, st);
-                    if (capture) capture_rows(d, false, depth);
+                    if (capture) capture_rows(d, false, depth, 0);
                 }
                 if (verify_mode == RS_VERIFY_GREEDY || mode.branching == 1) break;
                 sd_redraft_check(d, st);
@@ -390,11 +417,7 @@ void rs_engine::step(rs_step_info *info) {
                 RS_CUDA(cudaMemsetAsync(d_flag.p, 0, sizeof(int32_t), st));
                 ++redraft_passes;
             }
-            prof_set_scope("verify");
-            pair->verify_rows(d, false, st);
-            if (capture) capture_rows(d, true, 0);
-            prof_set_scope("accept");
-            sd_accept(d, round, false, rt, st);
+            verify_accept(d, round, rt, st);
             pair->after_accept(d, false, st);
             if (round + 1 < mode.rounds) {
                 // any request continuing into the next round? (lockstep, server.cpp:154-178)
@@ -412,7 +435,7 @@ void rs_engine::step(rs_step_info *info) {
     } else {
         prof_set_scope("naive");
         pair->verify_rows(d, true, st);
-        if (capture) capture_rows(d, true, 0);
+        if (capture) capture_rows(d, true, 0, 0);
         sd_accept(d, 0, true, rt, st);
         pair->after_accept(d, true, st);
     }

@@ -132,6 +132,10 @@ struct ModelPair {
     virtual void draft_rows(const SdDev &d, int depth, cudaStream_t st) = 0;
     virtual void verify_rows(const SdDev &d, bool naive, cudaStream_t st) = 0;
     virtual void after_accept(const SdDev &, bool /*naive*/, cudaStream_t) {}
+    // Lazy verify LM head (transformer pairs): verify_rows then produced only the root rows'
+    // logits; verify_rows_selected computes the chains the acceptance's branch point selected.
+    virtual bool lazy_lm_head(const SdDev &) const { return false; }
+    virtual void verify_rows_selected(const SdDev &, cudaStream_t) {}
     virtual void on_spec_enable(const SdDev &, cudaStream_t) {}
     virtual void set_drafter(const rs_model *) {}
     virtual void begin_step() {}
@@ -228,5 +232,6 @@ struct rs_engine {
     ~rs_engine();
     rs::SdDev dev(const rs_sdconfig &cfg, int nact);
     void step(rs_step_info *info);
-    void capture_rows(const rs::SdDev &d, bool verify, int depth);
+    void capture_rows(const rs::SdDev &d, bool verify, int depth, int which);
+    void verify_accept(const rs::SdDev &d, int round, rs::RowType rt, cudaStream_t st);
 };

@@ -432,4 +432,34 @@ void init_drafter(DrafterModel &m, uint64_t seed, cudaStream_t st) {
     k_init_normal(m.lm_w, (size_t)s.V * s.d, seed, 1020, s.std, st);
 }
 
+namespace {
+// Lazy verify LM head: the final-normed rows of each active sequence's SELECTED chain (acceptance
+// stage 1 parked its index in stg[r * 6], -1 when the cycle already ended) gathered into n rows per
+// sequence, and the P row each maps to (-1: no row; the LM head epilogue drops it).
+__global__ void gather_selected_kernel(const bf16 *xn, const int32_t *active, const int32_t *stg,
+                                       const int32_t *chain_len, int t_max, int n, int slots, int d, bf16 *out,
+                                       int32_t *map) {
+    pdl_trigger();
+    pdl_wait();
+    const int m = blockIdx.x, a = m / n, j = m % n;
+    const int r = active[a];
+    const int sel = stg[(size_t)r * 6];
+    const int L = sel >= 0 ? chain_len[(size_t)r * t_max + sel] : 0;
+    const bool live = j < L;
+    const int src = a * slots + 1 + sel * n + j;
+    if (threadIdx.x == 0) map[m] = live ? src : -1;
+    if (!live) return;
+    const int4 *s4 = reinterpret_cast<const int4 *>(xn + (size_t)src * d);
+    int4 *o4 = reinterpret_cast<int4 *>(out + (size_t)m * d);
+    for (int i = threadIdx.x; i < d / 8; i += blockDim.x) o4[i] = s4[i];
+}
+}  // namespace
+
+void k_gather_selected(const bf16 *xn, const int32_t *active, const int32_t *stg, const int32_t *chain_len, int t_max,
+                       int nact, int n, int slots, int d, bf16 *out, int32_t *map, cudaStream_t st) {
+    if (nact <= 0) return;
+    launch_pdl(gather_selected_kernel, nact * n, 128, 0, st, xn, active, stg, chain_len, t_max, n, slots, d, out, map);
+    RS_LAUNCHED();
+}
+
 }  // namespace rs

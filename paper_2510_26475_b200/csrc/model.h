@@ -159,6 +159,9 @@ void k_gather_features(const RowDesc *rows, int M, int d, const bf16 *feat, int 
                        int *use_hidden, cudaStream_t st);
 void k_rows_copy_f32(const float *src, int ld_src, const int *src_rows, float *dst, int ld_dst, const int *dst_rows,
                      int n, int d, cudaStream_t st);
+// Lazy verify LM head: rows of the selected chains (stg[r * 6]) -> out [nact * n][d], P-row map (-1 none)
+void k_gather_selected(const bf16 *xn, const int32_t *active, const int32_t *stg, const int32_t *chain_len, int t_max,
+                       int nact, int n, int slots, int d, bf16 *out, int32_t *map, cudaStream_t st);
 void k_init_normal(bf16 *p, size_t n, uint64_t seed, uint64_t tensor_id, float std, cudaStream_t st);
 void k_fill_f32(float *p, size_t n, float v, cudaStream_t st);
 void k_rope_table(float *rope, int max_ctx, int hd, float theta, cudaStream_t st);

@@ -39,6 +39,7 @@ struct SdDev {
     int32_t *n_eff, *d_used, *a_used, *cont, *ended, *accept_len, *drafted, *emitted, *n_rounds;
     int32_t *round_cost;     // [B][kMaxRounds][3]
     int32_t *rsel, *racc;    // this round's selected chain (-1 none) and accepted drafted count (K4)
+    int32_t *stg;            // [B][6] two-stage acceptance: sel (-1: cycle done), acur, alen, alen0, emitted, len
     // draft tree [B][t_max][n_max]
     int32_t *chain_tok, *chain_len, *chain_stop, *chain_off;
     int32_t t_max, n_max;
@@ -71,7 +72,8 @@ void sd_cycle_begin(const SdDev &d, cudaStream_t st);
 void sd_round_setup(const SdDev &d, int round, cudaStream_t st);
 void sd_draft_sample(const SdDev &d, int depth, RowType rt, cudaStream_t st);
 void sd_redraft_check(const SdDev &d, cudaStream_t st);
-void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t st);
+// stage 0: whole acceptance; 1 / 2: before / after the LM head of the selected chains (lazy verify LM head)
+void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t st, int stage = 0);
 void sd_cycle_end(const SdDev &d, bool naive, cudaStream_t st);
 
 // Exact fp64 softmax tile partials of fp32 logit rows (rowstats.cu); row_ids null = rows 0..n-1.

@@ -646,7 +646,7 @@ __global__ void redraft_check_kernel(SdDev d) {
 // MB = minimum resident CTAs per SM the register budget is sized for: 1 (up to 512 threads) or,
 // for the 256-thread clusters of large vocabularies, 3 / 4 (a wave holds more sequences' clusters)
 template <class T, int MB>
-__global__ void __launch_bounds__(MB == 1 ? 512 : 256, MB) accept_kernel(SdDev d, int round, int naive) {
+__global__ void __launch_bounds__(MB == 1 ? 512 : 256, MB) accept_kernel(SdDev d, int round, int naive, int stage) {
     pdl_trigger();
     pdl_wait();
     // an EOS-shortened chain shifted the draft-stream offsets of later chains: this optimistic
@@ -669,6 +669,10 @@ __global__ void __launch_bounds__(MB == 1 ? 512 : 256, MB) accept_kernel(SdDev d
     bool ended = false;
     int emitted = 0;
 
+    // stage 0: the whole acceptance; 1 / 2: split around the LM head of the selected chains (lazy
+    // verify LM head): stage 1 runs the branch point on the root rows and, when a chain is
+    // selected, parks (sel, acur, alen, alen0, emitted, len) in d.stg; stage 2 verifies that chain
+    if (naive && stage == 2) return;
     if (naive) {
         // Non-spec step (server.cpp:328-347): one target sample on the DRAFT stream.
         const RowRef<T> p = prow_ready<T>(d, q, 0, cl);
@@ -689,9 +693,11 @@ __global__ void __launch_bounds__(MB == 1 ? 512 : 256, MB) accept_kernel(SdDev d
 
     const int ne = d.n_eff[r];
     if (ne < 0) return;
+    if (stage == 2 && d.stg[(size_t)r * 6] < 0) return;  // the cycle ended in stage 1
+    if (stage == 1 && cl.lead()) d.stg[(size_t)r * 6] = -1;
     int acur = d.a_used[r];
     int alen = d.accept_len[r];
-    const int alen0 = alen;
+    int alen0 = alen;
     int sel_out = -1;
     int cont = 0;
     const int t = d.t, n = d.n;
@@ -718,6 +724,16 @@ __global__ void __launch_bounds__(MB == 1 ? 512 : 256, MB) accept_kernel(SdDev d
     }
 
     {
+      int sel = -1;
+      if (stage == 2) {
+        const int32_t *sv = d.stg + (size_t)r * 6;
+        sel = sv[0];
+        acur = sv[1];
+        alen = sv[2];
+        alen0 = sv[3];
+        emitted = sv[4];
+        q.len = sv[5];
+      } else {
         // RoundCost{longest, t, tree_tokens + 1} (specdec.cpp:195)
         int longest = 0, tree = 0;
         for (int i = 0; i < t; ++i) {
@@ -743,7 +759,6 @@ __global__ void __launch_bounds__(MB == 1 ? 512 : 256, MB) accept_kernel(SdDev d
         const RowRef<T> q1 = qrow<T>(d, q, 0);
         const Stats s1 = row_stats(p1, red);
         const Stats t1 = row_stats(q1, red);
-        int sel = -1;
         if (greedy) {
             const int a1 = row_argmax(p1, s1, red, redl, nullptr, 0, cl, &slot_v, &slot_k);
             for (int i = 0; i < t && sel < 0; ++i)
@@ -813,13 +828,27 @@ __global__ void __launch_bounds__(MB == 1 ? 512 : 256, MB) accept_kernel(SdDev d
                 goto done;
             }
         }
+        emit(d, q, ctok[(size_t)sel * d.n_max], p1, s1, true, log(prob(q1, t1, ctok[(size_t)sel * d.n_max])), ended, cl);
+        ++emitted;
+        ++alen;
+        sel_out = sel;
+        if (ended) goto done;
+        if (stage == 1) {
+            if (cl.lead()) {
+                int32_t *sv = d.stg + (size_t)r * 6;
+                sv[0] = sel;
+                sv[1] = acur;
+                sv[2] = alen;
+                sv[3] = alen0;
+                sv[4] = emitted;
+                sv[5] = q.len;
+            }
+            return;
+        }
+      }
         sel_out = sel;
         const int *chain = ctok + (size_t)sel * d.n_max;
         const int L = clen[sel];
-        emit(d, q, chain[0], p1, s1, true, log(prob(q1, t1, chain[0])), ended, cl);
-        ++emitted;
-        ++alen;
-        if (ended) goto done;
         // Chain-style verification of the selected chain (specdec.cpp:226-245).
         for (int pos = 1; pos < L; ++pos) {
             {  // this position's pair and the next target row (next position or bonus)
@@ -1013,7 +1042,7 @@ void sd_redraft_check(const SdDev &d, cudaStream_t st) {
     RS_LAUNCHED();
 }
 
-void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t st) {
+void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t st, int stage) {
     if (d.nact <= 0) return;
     const int th = sd_threads(d.V, false);
     // algorithmic bytes: every target row of the round plus every drafter row
@@ -1059,13 +1088,13 @@ void sd_accept(const SdDev &d, int round, bool naive, RowType rt, cudaStream_t s
     const int nv = naive ? 1 : 0;
     const int mb = threads == 256 ? tuning().accept_minb : 1;
     if (rt == RowType::F64) {
-        if (mb == 4) RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<double, 4>, d, round, nv));
-        else if (mb == 3) RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<double, 3>, d, round, nv));
-        else RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<double, 1>, d, round, nv));
+        if (mb == 4) RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<double, 4>, d, round, nv, stage));
+        else if (mb == 3) RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<double, 3>, d, round, nv, stage));
+        else RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<double, 1>, d, round, nv, stage));
     } else {
-        if (mb == 4) RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<float, 4>, d, round, nv));
-        else if (mb == 3) RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<float, 3>, d, round, nv));
-        else RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<float, 1>, d, round, nv));
+        if (mb == 4) RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<float, 4>, d, round, nv, stage));
+        else if (mb == 3) RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<float, 3>, d, round, nv, stage));
+        else RS_CUDA(cudaLaunchKernelEx(&cfg, accept_kernel<float, 1>, d, round, nv, stage));
     }
     RS_LAUNCHED();
 }

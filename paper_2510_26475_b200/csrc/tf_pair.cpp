@@ -552,8 +552,26 @@ struct TransformerPair : ModelPair {
         }
         upload(bt, st);
         if (!naive) stage.upload(rbase.p, base, st);
+        if (!naive && lazy_lm_head(d)) {
+            // lazy verify LM head: the final norm of every row, the logits of the ROOT rows only
+            // (row a * slots of the batch; P slot 0 of sequence a); the selected chains' rows follow
+            // in verify_rows_selected once the acceptance's branch point picked them
+            target_forward(d, bt.M(), (int)bt.items.size(), nullptr, false, st);
+            k_rmsnorm(w.x.p, s.d, tgt->final_norm, bt.M(), s.d, s.eps, w.xn.p, s.d, st);
+            gemm(w.xn.p, d.slots * s.d, tgt->emb, nact, s.V, s.d, epi_f32(P, d.slots * s.V, s.logit_scale, nullptr), st);
+            return;
+        }
         // no stats pass over the verified rows: acceptance computes the 2-3 rows it touches
         target_forward(d, bt.M(), (int)bt.items.size(), P, true, st, d.lazy_pst ? nullptr : const_cast<double *>(d.Pst));
+    }
+
+    bool lazy_lm_head(const SdDev &d) const override { return tuning().lazy_lm >= 0 && d.lazy_pst && d.n > 0; }
+
+    void verify_rows_selected(const SdDev &d, cudaStream_t st) override {
+        float *P = static_cast<float *>(const_cast<void *>(d.P));
+        const int m = d.nact * d.n;
+        k_gather_selected(w.xn.p, d.active, d.stg, d.chain_len, d.t_max, d.nact, d.n, d.slots, s.d, w.h.p, w.idx.p, st);
+        gemm(w.h.p, s.d, tgt->emb, m, s.V, s.d, epi_f32(P, s.V, s.logit_scale, w.idx.p), st);
     }
 
     void after_accept(const SdDev &d, bool naive, cudaStream_t st) override {
