@@ -13,7 +13,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --n
   --csv --log-file $O/launches.csv python tools/profile_step.py 3 > $O/launches.log 2>&1; echo "ncu launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "verify/" -k regex:gemm -s 0 -c 4 \
   -o $O/gemm_full python tools/profile_step.py 2 > $O/gemm_full.log 2>&1; echo "ncu full rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "verify/" -k regex:gemm -s 144 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "verify/" -k regex:gemm -s 144 -c 2 \
   -o $O/lmhead_full python tools/profile_step.py 2 > $O/lmhead_full.log 2>&1; echo "ncu lmhead rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "accept/" -k regex:"accept|compact" -s 0 -c 4 \
   -o $O/accept_full python tools/profile_step.py 2 > $O/accept_full.log 2>&1; echo "ncu accept rc=$?"
