@@ -1102,6 +1102,8 @@ int rs_set_tuning(const char *key, int64_t value) {
             rs::tuning().pdl = static_cast<int>(value);
         } else if (k == "lazy_lm") {
             rs::tuning().lazy_lm = static_cast<int>(value);
+        } else if (k == "epi3") {
+            rs::tuning().epi3 = static_cast<int>(value);
         } else if (k == "kd_rows") {
             if (value < 0) throw std::invalid_argument("kd_rows must be >= 0");
             rs::tuning().kd_rows = static_cast<int>(value);

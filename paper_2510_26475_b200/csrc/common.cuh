@@ -49,6 +49,7 @@ const char *dev_err_message(int code);
 struct Tuning {
     int accept_cluster = 0;  // CTAs per sequence in the fused acceptance kernel: 0 auto, 1/2/4/8 forced
     int lazy_lm = 0;         // lazy verify LM head (root rows, then the selected chains): 0 on, -1 off
+    int epi3 = 0;            // single-wave SM-pair GEMMs: third epilogue group on the producer / MMA warps: 0 on, -1 off
     int accept_minb = 4;     // acceptance kernel register budget for 256-thread CTAs: resident CTAs per SM (1, 3 or 4)
     int fused_stats = 0;     // drafter LM-head stats: 1 fused GEMM epilogue; 0 / -1 separate row-stats kernel
     int attn_trace = 0;      // diagnostics: layer + 1 whose attention pass timeline is printed

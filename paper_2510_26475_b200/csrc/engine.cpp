@@ -39,6 +39,7 @@ Tuning &tuning() {
                     else if (k == "fused_stats") x.fused_stats = v;
                     else if (k == "accept_minb") x.accept_minb = v;
                     else if (k == "lazy_lm") x.lazy_lm = v;
+                    else if (k == "epi3") x.epi3 = v;
                     else if (k == "attn_trace") x.attn_trace = v;
                     else if (k == "attn_skip") x.attn_skip = v;
                     else if (k == "pdl") x.pdl = v;

@@ -292,7 +292,7 @@ __device__ __forceinline__ void epi2_qkv_rope(const GemmEpi &ep, uint32_t taddr,
 template <int BT, int EPI>
 __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmEpi ep, int F,
-                 int T, int K, int splits, int *sem, float *ws, long long *g2trace, int g2slot) {
+                 int T, int K, int splits, int ngrp, int *sem, float *ws, long long *g2trace, int g2slot) {
     using C = Cfg2<BT>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -418,12 +418,17 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                 if (g2trace && blockIdx.x == 0 && it == 0) g2trace[g2slot * 8 + 3] = clock64();
             }
         }
-    } else if (warp >= 4) {
+    }
+    // Single-wave launches (ngrp == 3: one unit per pair, no split-K) give the accumulator to a third
+    // epilogue group: warps 0-3, idle once the last k-block is issued. Their staging buffer is the
+    // first ring stages, free once the accumulator is complete (every TMA load was consumed).
+    __syncwarp();
+    if (warp >= 4 || (ngrp == 3 && pair < num_units)) {
         pdl_wait();
-        const int q = warp & 3;          // TMEM lane quadrant
-        const int grp = (warp - 4) >> 2;  // chunk parity of this warp's group
-        const int ebar = 2 + grp;         // named barrier of the group (QKV epilogue)
-        float(*stg_grp)[33] = stg_all + grp * 4 * 32;
+        const int q = warp & 3;                          // TMEM lane quadrant
+        const int grp = warp >= 4 ? (warp - 4) >> 2 : 2;  // chunks grp, grp + ngrp, ...
+        const int ebar = grp < 2 ? 2 + grp : 5;          // named barrier of the group (QKV epilogue)
+        float(*stg_grp)[33] = grp < 2 ? stg_all + grp * 4 * 32 : reinterpret_cast<float(*)[33]>(sA);
         const uint32_t lead_tempty = mapa(tempty, 0);
         int it = 0;
         for (int unit = pair; unit < num_units; unit += npairs, ++it) {
@@ -434,13 +439,18 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
             if constexpr (EPI == kEpiQKVRope) {
                 // (pos, seq, phys) of the tile's tokens, staged while the MMAs still run
                 const RowDesc *rws = static_cast<const RowDesc *>(ep.qkv.rows);
-                asm volatile("bar.sync 4, 256;" ::: "memory");  // previous tile done with the table
-                for (int i = threadIdx.x - 128; i < BT; i += 256)
-                    if (t0 + i < T) {
-                        const RowDesc r = rws[t0 + i];
-                        tok_tab[i] = make_int4(r.pos, r.seq, r.phys, 0);
-                    }
-                asm volatile("bar.sync 4, 256;" ::: "memory");
+                if (grp < 2) {
+                    asm volatile("bar.sync 4, 256;" ::: "memory");  // previous tile done with the table
+                    for (int i = threadIdx.x - 128; i < BT; i += 256)
+                        if (t0 + i < T) {
+                            const RowDesc r = rws[t0 + i];
+                            tok_tab[i] = make_int4(r.pos, r.seq, r.phys, 0);
+                        }
+                    asm volatile("bar.sync 4, 256;" ::: "memory");
+                    if (ngrp == 3) asm volatile("bar.arrive 6, 384;" ::: "memory");
+                } else {
+                    asm volatile("bar.sync 6, 384;" ::: "memory");  // the table is staged
+                }
             }
             // the epilogue's first global inputs do not depend on the MMAs: in flight before the
             // accumulator is ready (the first residual rows; the QKV bias and first cos / sin)
@@ -528,29 +538,32 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                 const bool rope = head < ep.qkv.H + ep.qkv.KV;  // q and k heads rotate, v heads do not
                 const float b = qb;
 #pragma unroll 1
-                for (int c = grp; c < BT / 32; c += 2) {
+                for (int c = grp; c < BT / 32; c += ngrp) {
                     epi2_qkv_rope(ep, tb + c * 32, head, q, t0 + c * 32, T, reinterpret_cast<float(*)[132]>(stg_grp),
                                   tok_tab, t0, ebar, cs, b);
                     // the next chunk's cos / sin, in flight during its TMEM read and staging
-                    if (rope && c + 2 < BT / 32) rope_cs_load(ep.qkv, tok_tab, t0, t0 + (c + 2) * 32, T, tid, cs);
+                    if (rope && c + ngrp < BT / 32) rope_cs_load(ep.qkv, tok_tab, t0, t0 + (c + ngrp) * 32, T, tid, cs);
                 }
             } else if constexpr (EPI == kEpiResidual) {
                 // software-pipelined: chunk c + 1's residual rows are in flight while chunk c is done
                 // (the first chunk's were issued before the accumulator wait; after a split-K
                 // reduction they are read now, the other splits having updated nothing)
                 if (splits > 1 && grp < BT / 32) resid_prefetch(ep, f0 + q * 32, t0 + grp * 32, F, T, cur[0]);
+                // (the loop counter stays compile-time so the register double buffer does too)
 #pragma unroll
-                for (int i = 0, c = grp; c < BT / 32; ++i, c += 2) {
-                    if (c + 2 < BT / 32) resid_prefetch(ep, f0 + q * 32, t0 + (c + 2) * 32, F, T, cur[(i + 1) & 1]);
+                for (int i = 0; i < (BT / 32 + 1) / 2; ++i) {
+                    const int c = grp + i * ngrp;
+                    if (c >= BT / 32) break;
+                    if (c + ngrp < BT / 32) resid_prefetch(ep, f0 + q * 32, t0 + (c + ngrp) * 32, F, T, cur[(i + 1) & 1]);
                     epi2_chunk<EPI>(ep, tb + c * 32, f0 + q * 32, t0 + c * 32, F, T, stg_grp + q * 32, cur[i & 1]);
                 }
             } else {
 #pragma unroll 1
-                for (int c = grp; c < BT / 32; c += 2)
+                for (int c = grp; c < BT / 32; c += ngrp)
                     epi2_chunk<EPI>(ep, tb + c * 32, f0 + q * 32, t0 + c * 32, F, T, stg_grp + q * 32);
             }
             tc_fence_before();
-            mbar_arrive_remote(lead_tempty + 8 * acc);
+            if (grp < 2) mbar_arrive_remote(lead_tempty + 8 * acc);  // the third group only runs single-unit
             if (g2trace && blockIdx.x == 0 && threadIdx.x == 128 && it == 0) g2trace[g2slot * 8 + 5] = clock64();
         }
     }
@@ -613,12 +626,13 @@ void launch2(const GemmArgs &g, cudaStream_t st) {
         ws = wsb;
     }
     const int pairs = std::min(tiles * splits, num_sms2() / 2);
+    const int ngrp = tuning().epi3 >= 0 && splits == 1 && tiles <= pairs ? 3 : 2;
     // diagnostics (RS_TUNE gemm_trace=1): per launch of CTA 0: start, after the dependency wait,
     // first full stage, last MMA commit of tile 0, epilogue start / end of tile 0, exit
     static long long *tr = nullptr;
     static int slot = 0;
     if (tuning().gemm_trace && !tr) RS_CUDA(cudaMalloc(&tr, 8 * 8 * 4096));
-    launch_pdl(gemm2_kernel<BT, EPI>, dim3(2 * pairs), kThr, C::kSmem, st, tw, tx, g.epi, F, T, g.K, splits, sem, ws,
+    launch_pdl(gemm2_kernel<BT, EPI>, dim3(2 * pairs), kThr, C::kSmem, st, tw, tx, g.epi, F, T, g.K, splits, ngrp, sem, ws,
                tuning().gemm_trace ? tr : (long long *)nullptr, slot);
     if (tuning().gemm_trace) {
         RS_CUDA(cudaStreamSynchronize(st));
