@@ -58,8 +58,15 @@ __device__ __forceinline__ uint32_t mapa(const void *p, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
     return r;
 }
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+// "accumulator drained": the epilogue's TMEM reads have completed (tcgen05.wait::ld) when it
+// arrives, and the MMA warp only needs that, not the epilogue's global stores -- a release arrive
+// would make every epilogue thread wait for its stores to reach the GPU (MEMBAR.ALL.GPU)
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// the exit barrier only protects the CTAs' shared memory / barriers / TMEM, not global data
+__device__ __forceinline__ void cluster_sync_exit() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tma_load_2sm(void *dst, const CUtensorMap *map, uint32_t bar_cluster, int x, int y) {
     asm volatile(
@@ -494,7 +501,7 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                 asm volatile("bar.sync 1, 256;" ::: "memory");
                 if (!s_last) {
                     tc_fence_before();
-                    mbar_arrive_remote(lead_tempty + 8 * acc);
+                    if (unit + 2 * npairs < num_units) mbar_arrive_remote_relaxed(lead_tempty + 8 * acc);
                     continue;
                 }
                 __threadfence();
@@ -563,13 +570,15 @@ __global__ void __launch_bounds__(kThr, 1) __cluster_dims__(2, 1, 1)
                     epi2_chunk<EPI>(ep, tb + c * 32, f0 + q * 32, t0 + c * 32, F, T, stg_grp + q * 32);
             }
             tc_fence_before();
-            if (grp < 2) mbar_arrive_remote(lead_tempty + 8 * acc);  // the third group only runs single-unit
+            // the MMA warp waits for this accumulator again only if the pair has a unit two ahead
+            // (the third group only runs single-unit launches)
+            if (grp < 2 && unit + 2 * npairs < num_units) mbar_arrive_remote_relaxed(lead_tempty + 8 * acc);
             if (g2trace && blockIdx.x == 0 && threadIdx.x == 128 && it == 0) g2trace[g2slot * 8 + 5] = clock64();
         }
     }
     tc_fence_before();
     __syncthreads();
-    cluster_sync_all();  // no CTA leaves while its peer may still signal its barriers
+    cluster_sync_exit();  // no CTA leaves while its peer may still signal its barriers
     if (g2trace && blockIdx.x == 0 && threadIdx.x == 128) g2trace[g2slot * 8 + 6] = clock64();
     if (warp == 2) {
         tc_fence_after();
