@@ -143,7 +143,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         ctat[3] = smid;
     }
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // aligned by pointer arithmetic on the shared array (not through an integer), so the compiler
+    // keeps the shared address space and emits STS / LDS instead of generic ST / LD
+    uint8_t *smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
     uint8_t *sK = smem;
     uint8_t *sV = sK + kNK * kKVBytes;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sV + kNV * kKVBytes);

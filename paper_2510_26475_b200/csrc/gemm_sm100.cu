@@ -220,7 +220,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int N, int K, int splits, int *sem) {
     using C = Cfg<BN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // aligned by pointer arithmetic on the shared array (not through an integer), so the compiler
+    // keeps the shared address space and emits STS / LDS instead of generic ST / LD
+    uint8_t *smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
     uint8_t *sA = smem;
     uint8_t *sB = smem + C::kStages * C::kABytes;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::kStages * C::kStageBytes);
