@@ -328,7 +328,10 @@ void rs_prof_enable(int32_t on);
    partials in the GEMM epilogue (1) or a separate row-stats kernel (0); results are bitwise
    independent of both; "gemm2" -- weight GEMMs on SM pairs (0 auto/on, -1 single-SM kernel);
    "pdl" -- programmatic dependent launch on the forward path (0 on, -1 off); "kd_rows" -- cap on
-   the KD rows per group of rs_engine_kd_grad (tests of the grouping; 0 = workspace size). */
+   the KD rows per group of rs_engine_kd_grad (tests of the grouping; 0 = workspace size);
+   "lazy_lm" -- verify LM head on the root rows, then only the selected chains (0 on, -1 one pass);
+   "epi3" -- single-wave SM-pair GEMMs give a third of the epilogue to the control warps (0 on,
+   -1 off). Results are bitwise independent of every key. */
 int rs_set_tuning(const char *key, int64_t value);
 void rs_prof_reset(void);
 int rs_prof_json(char *buf, int64_t cap, int64_t *len);
