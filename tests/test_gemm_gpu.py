@@ -240,3 +240,43 @@ def test_gemm_split_k_on_sm_pairs(gemm_path):
     assert (o3 - ref).abs().max().item() <= 2e-3 * ref.abs().max().item()
     assert (o1 - ref).abs().max().item() <= 2e-3 * ref.abs().max().item()
 
+
+
+@pytest.fixture
+def epi3_default():
+    yield
+    rb.set_tuning("epi3", 0)
+
+
+@pytest.mark.parametrize("T,F,K,epi", [(1344, 2048, 2048, 2), (1344, 2048, 11008, 2), (1344, 2560, 2048, 0),
+                                       (300, 2048, 2048, 4), (256, 2048, 4096, 1)])
+def test_gemm_third_epilogue_group_bitwise(gemm_path, epi3_default, T, F, K, epi):
+    """Single-wave launches hand a third of the accumulator chunks to the control warps
+    (tuning key "epi3"); the outputs are bitwise those of the two-group epilogue."""
+    rb.set_tuning("gemm2", 0)
+    torch.manual_seed(T + F + K)
+    A = (torch.randn(T, K, device="cuda") * 0.5).bfloat16()
+    B = (torch.randn(F, K, device="cuda") * 0.03).bfloat16()
+    bias = (torch.randn(F, device="cuda") * 0.1).bfloat16()
+    base = torch.randn(T, F, device="cuda")
+    outs = []
+    for v in (0, -1):
+        rb.set_tuning("epi3", v)
+        if epi == 0:
+            out = torch.empty(T, F, device="cuda", dtype=torch.bfloat16)
+            _run(A, B, out, bias, 0)
+        elif epi == 1:
+            out = torch.empty(T, F, device="cuda", dtype=torch.float32)
+            _run(A, B, out, None, 1, 0.5)
+        elif epi == 2:
+            out = base.clone()
+            _run(A, B, out, None, 2)
+        else:
+            out = torch.empty(T, F // 2, device="cuda", dtype=torch.bfloat16)
+            _run(A, B, out, None, 4)
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
+    ref = A.float() @ B.float().t()
+    want = {0: ref + bias.float(), 1: ref * 0.5, 2: base + ref}.get(epi)
+    if want is not None:
+        assert (outs[0].float() - want).abs().max().item() <= 1e-2 * want.abs().max().item() + 1e-3
