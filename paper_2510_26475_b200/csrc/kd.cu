@@ -139,6 +139,47 @@ __global__ void __launch_bounds__(1024, 1) kd_rows_kernel(const float *trow, con
 }
 
 // ---- K5 at full-chip parallelism (transformer KD) ------------------------------------------
+// Softmax tile partials of the target (P) and drafter (Q) rows in one pass: per row and 256-column
+// tile (EOS column V-1 excluded, kd_lse_kernel folds it in with the row's bias) m = max(z / tau)
+// and s = sum exp(z / tau - m). Same layout as row_stats (rowstats.cu), but the exponentials run in
+// fp32: KD's p~ and q only feed a bf16 dZ and a fp64-accumulated loss, so the fp64 exp that the
+// acceptance path needs for bitwise parity would only make this pass fp64-pipe bound.
+__global__ void __launch_bounds__(256) kd_tile_stats_kernel(const float *P, const float *Q, int R, int V, float inv_p,
+                                                            float inv_q, double *stP, double *stQ) {
+    const int nt = (V + 255) / 256;
+    const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (gw >= (long long)R * nt) return;
+    const int r = static_cast<int>(gw / nt), t = static_cast<int>(gw % nt);
+    const int lo = t * 256, hi = min(lo + 256, V - 1);
+    const float *zp = P + (size_t)r * V, *zq = Q + (size_t)r * V;
+    float vp[8], vq[8], mp = -INFINITY, mq = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int x = lo + lane + 32 * j;
+        vp[j] = x < hi ? zp[x] * inv_p : -INFINITY;
+        vq[j] = x < hi ? zq[x] * inv_q : -INFINITY;
+        mp = fmaxf(mp, vp[j]);
+        mq = fmaxf(mq, vq[j]);
+    }
+    mp = warp_maxf(mp);
+    mq = warp_maxf(mq);
+    float sp = 0.f, sq = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        if (vp[j] != -INFINITY) sp += expf(vp[j] - mp);
+        if (vq[j] != -INFINITY) sq += expf(vq[j] - mq);
+    }
+    const double Sp = warp_sum((double)sp), Sq = warp_sum((double)sq);
+    if (lane == 0) {
+        double *op = stP + ((size_t)r * nt + t) * 2, *oq = stQ + ((size_t)r * nt + t) * 2;
+        op[0] = mp == -INFINITY ? -INFINITY : (double)mp;
+        op[1] = mp == -INFINITY ? 0.0 : Sp;
+        oq[0] = mq == -INFINITY ? -INFINITY : (double)mq;
+        oq[1] = mq == -INFINITY ? 0.0 : Sq;
+    }
+}
+
 // Row log-normaliser log sum_x exp(z'/tau) of fp32 logit rows from their 256-column tile
 // partials (rowstats.cu; EOS column excluded) plus the EOS column with the row's bias.
 __global__ void kd_lse_kernel(const float *rows, const double *st, int nrows, int V, double tau, const double *bias,
@@ -163,6 +204,9 @@ __global__ void kd_lse_kernel(const float *rows, const double *st, int nrows, in
 // learner.cpp:44-50) and dZ = w (q - p~) / tau_q (learner.cpp:75) times the LM-head output
 // scale -- written TRANSPOSED ([V][ldt] bf16) so it is the K-major A operand of the
 // dW = dZ^T . h GEMM. One warp per row, lane l on columns l + 32 j; KL partials per (row, tile).
+// UnitTau (tau_p == tau_q == 1, the KD default): the three fp64 divisions per element are
+// skipped -- x / 1.0 == x exactly, so the outputs are bitwise those of the general path.
+template <bool UnitTau>
 __global__ void __launch_bounds__(256) kd_elem_kernel(const float *P, const float *Q, const double *lseP,
                                                       const double *lseQ, const double *w, const double *bias, int R,
                                                       int V, double tau_p, double tau_q, float zscale, bf16 *dzT,
@@ -177,20 +221,31 @@ __global__ void __launch_bounds__(256) kd_elem_kernel(const float *P, const floa
         if (r < R) {
             const float *zp = P + (size_t)r * V, *zq = Q + (size_t)r * V;
             const double b = bias[r], lp0 = lseP[r], lq0 = lseQ[r], wr = w[r];
-#pragma unroll 4
+            float fp[8], fq[8];  // all 16 loads of the row issued before any math
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int x = t * 256 + lane + 32 * j;
+                fp[j] = x < V ? __ldcs(zp + x) : 0.f;
+                fq[j] = x < V ? __ldcs(zq + x) : 0.f;
+            }
+#pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int c = lane + 32 * j, x = t * 256 + c;
                 float dz = 0.f;
                 if (x < V) {
-                    double vp = zp[x], vq = zq[x];
+                    double vp = fp[j], vq = fq[j];
                     if (x == V - 1) {
                         vp += b;
                         vq += b;
                     }
-                    const double lp = vp / tau_p - lp0, lq = vq / tau_q - lq0;
-                    const double p = exp(lp), q = exp(lq);
-                    if (p > 0.0) kl += p * (lp - lq);
-                    dz = (float)(wr * (q - p) / tau_q) * zscale;
+                    const double lp = (UnitTau ? vp : vp / tau_p) - lp0, lq = (UnitTau ? vq : vq / tau_q) - lq0;
+                    // fp32 exponentials: dZ is rounded to bf16 for the GEMM (rel. 4e-3) and a KL
+                    // term's relative error stays ~1e-7, so fp64 exp bought nothing here but
+                    // made the kernel fp64-pipe bound (0.5 ms vs ~0.12 ms of HBM per 487 rows)
+                    const float p = expf((float)lp), q = expf((float)lq);
+                    if (p > 0.f) kl += (double)p * (lp - lq);
+                    const float g = (float)wr * (q - p);
+                    dz = (UnitTau ? g : g / (float)tau_q) * zscale;
                 }
                 tile[rr][c] = __float2bfloat16(dz);
             }
@@ -249,6 +304,15 @@ __global__ void sgd_bf16_kernel(const bf16 *w, const float *g, float scale, size
 
 }  // namespace
 
+void kd_tile_stats(const float *P, const float *Q, int R, int V, double tau_p, double tau_q, double *stP, double *stQ,
+                   cudaStream_t st) {
+    if (R <= 0) return;
+    const long long warps = (long long)R * ((V + 255) / 256);
+    kd_tile_stats_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(P, Q, R, V, (float)(1.0 / tau_p),
+                                                                      (float)(1.0 / tau_q), stP, stQ);
+    RS_LAUNCHED();
+}
+
 void kd_rows_lse(const float *rows, const double *stats, int nrows, int V, double tau, const double *bias, double *lse,
                  cudaStream_t st) {
     if (nrows <= 0) return;
@@ -262,8 +326,9 @@ void kd_rows_elem(const float *P, const float *Q, const double *lseP, const doub
     if (R <= 0) return;
     const int nt = (V + 255) / 256;
     ProfScope prof("kd", 0, (double)R * V * (4.0 + 4.0 + 2.0), st);
-    kd_elem_kernel<<<dim3(nt, (R + 63) / 64), 256, 0, st>>>(P, Q, lseP, lseQ, w, bias, R, V, tau_p, tau_q, zscale,
-                                                              dzT, ldt, kl_part);
+    auto kern = tau_p == 1.0 && tau_q == 1.0 ? kd_elem_kernel<true> : kd_elem_kernel<false>;
+    kern<<<dim3(nt, (R + 63) / 64), 256, 0, st>>>(P, Q, lseP, lseQ, w, bias, R, V, tau_p, tau_q, zscale, dzT, ldt,
+                                                  kl_part);
     RS_LAUNCHED();
     kd_rowloss_kernel<<<(R + 7) / 8, 256, 0, st>>>(kl_part, R, nt, w, loss);
     RS_LAUNCHED();

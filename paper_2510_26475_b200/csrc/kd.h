@@ -30,6 +30,9 @@ void kd_rows_loss_grad(const float *target_rows, const float *drafter_rows, cons
                        const double *eos_bias, int rows, int V, double tau_p, double tau_q, double *loss_out,
                        float *dz_out, cudaStream_t st);
 
+// Softmax tile partials (row_stats layout) of KD's target and drafter rows, fp32 exponentials.
+void kd_tile_stats(const float *P, const float *Q, int R, int V, double tau_p, double tau_q, double *stP, double *stQ,
+                   cudaStream_t st);
 // K5 at full-chip parallelism (transformer drafters): per-row log-normalisers from the rows'
 // 256-column tile partials, then one pass over 64 x 256 tiles producing the weighted KL per row
 // (loss[r] = w_r KL_r) and dZ^T = (w (q - p~) / tau_q * zscale)^T as bf16 [V][ldt].
@@ -45,7 +48,8 @@ void sgd_bf16(const __nv_bfloat16 *w, const float *g, float scale, size_t n, __n
 // rms_bwd: dx = base + dRMSNorm/dx . dy (base / dx / gterm optional), gterm = dy * x * r (the
 // per-row gain gradient terms); colsum_f32: out[c] (+)= sum over rows in a fixed order
 // (partial needs max_chunks * C floats); swiglu_bwd: pairwise-interleaved gate/up gradient;
-// rope_bwd: inverse rotation in place; softmax_bwd: causal rows, P and dS (times scale) in
+// rope_bwd: inverse rotation in place; softmax_bwd: causal rows (row i of a head stack sees keys
+// 0 .. i % T), P and dS (times scale) in
 // bf16; cast_bf16: fp32 -> bf16 sub-matrix; sgd_f32: out = w + scale * g.
 void rms_bwd(const float *x, int ldx, const float *g, const float *dy, int lddy, int M, int d, float eps,
              const float *base, int ldb, float *dx, int lddx, float *gterm, int ldg, cudaStream_t st);
@@ -54,8 +58,12 @@ void colsum_f32(const float *in, int ld, int M, int C, float *out, bool accumula
 void swiglu_bwd(const __nv_bfloat16 *gu, int ldgu, const float *dh, int lddh, int M, int F, __nv_bfloat16 *dgu,
                 int lddgu, cudaStream_t st);
 void rope_bwd(float *x, int ldx, int M, int heads, int hd, const int *pos, const float *rope, cudaStream_t st);
-void softmax_bwd(const float *S, const float *dP, int lds, int T, float scale, __nv_bfloat16 *P, __nv_bfloat16 *dS,
-                 int ldo, cudaStream_t st);
+void softmax_bwd(const float *S, const float *dP, int lds, int rows, int T, float scale, __nv_bfloat16 *P,
+                 __nv_bfloat16 *dS, int ldo, cudaStream_t st);
+// stack_heads: the heads of a GQA group as [heads * T][hd] rows (bf16); unstack_heads: the fp32
+// inverse into a [T][ldo] row-major block at the group's first head.
+void stack_heads(const __nv_bfloat16 *in, int ldi, int T, int heads, int hd, __nv_bfloat16 *out, cudaStream_t st);
+void unstack_heads(const float *in, int T, int heads, int hd, float *out, int ldo, cudaStream_t st);
 void cast_bf16(const float *in, int ldi, int M, int C, __nv_bfloat16 *out, int ldo, cudaStream_t st);
 void sgd_f32(const float *w, const float *g, float scale, size_t n, float *out, cudaStream_t st);
 

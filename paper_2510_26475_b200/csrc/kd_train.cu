@@ -109,12 +109,13 @@ __global__ void rope_bwd_kernel(float *x, int ldx, int heads, int hd, const int 
 // Causal softmax backward of one query row i (keys 0..i of the same sequence):
 //   P = softmax(S * scale), D = sum_j P dP, dS = P (dP - D) * scale (w.r.t. the raw scores)
 // P and dS are written in bf16 over [0, ldo) with zeros past the row's keys.
+// Row i of a stack of query heads, each T causal rows: row i attends keys 0 .. i % T.
 __global__ void __launch_bounds__(256) softmax_bwd_kernel(const float *S, const float *dP, int lds, int T, float scale,
                                                           bf16 *P, bf16 *dS, int ldo) {
     __shared__ float red[8];
     const int i = blockIdx.x;
     const float *s = S + (size_t)i * lds, *dp = dP + (size_t)i * lds;
-    const int n = i + 1;
+    const int n = i % T + 1;
     float mx = -INFINITY;
     for (int j = threadIdx.x; j < n; j += blockDim.x) mx = fmaxf(mx, s[j] * scale);
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -142,7 +143,33 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const float *S, const 
         po[j] = __float2bfloat16(p);
         dso[j] = __float2bfloat16(d);
     }
-    (void)T;
+}
+
+// out[(k T + t) hd + c] = in[t ldi + k hd + c]: the heads of one GQA group stacked row-wise
+// (16-byte vectors; hd % 8 == 0).
+__global__ void stack_heads_kernel(const bf16 *in, int ldi, int T, int heads, int hd, bf16 *out) {
+    const int v = hd / 8;
+    const size_t n = (size_t)heads * T * v;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % v) * 8;
+        const size_t r = i / v;
+        const int k = (int)(r / T), t = (int)(r % T);
+        *reinterpret_cast<int4 *>(out + r * hd + c) =
+            *reinterpret_cast<const int4 *>(in + (size_t)t * ldi + (size_t)k * hd + c);
+    }
+}
+
+// out[t ldo + k hd + c] = in[(k T + t) hd + c] (fp32, the inverse of stack_heads)
+__global__ void unstack_heads_kernel(const float *in, int T, int heads, int hd, float *out, int ldo) {
+    const int v = hd / 4;
+    const size_t n = (size_t)heads * T * v;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % v) * 4;
+        const size_t r = i / v;
+        const int k = (int)(r / T), t = (int)(r % T);
+        *reinterpret_cast<float4 *>(out + (size_t)t * ldo + (size_t)k * hd + c) =
+            *reinterpret_cast<const float4 *>(in + r * hd + c);
+    }
 }
 
 __global__ void cast_bf16_kernel(const float *in, int ldi, int M, int C, bf16 *out, int ldo) {
@@ -195,10 +222,22 @@ void rope_bwd(float *x, int ldx, int M, int heads, int hd, const int *pos, const
     RS_LAUNCHED();
 }
 
-void softmax_bwd(const float *S, const float *dP, int lds, int T, float scale, bf16 *P, bf16 *dS, int ldo,
+void softmax_bwd(const float *S, const float *dP, int lds, int rows, int T, float scale, bf16 *P, bf16 *dS, int ldo,
                  cudaStream_t st) {
-    if (T <= 0) return;
-    softmax_bwd_kernel<<<T, 256, 0, st>>>(S, dP, lds, T, scale, P, dS, ldo);
+    if (rows <= 0 || T <= 0) return;
+    softmax_bwd_kernel<<<rows, 256, 0, st>>>(S, dP, lds, T, scale, P, dS, ldo);
+    RS_LAUNCHED();
+}
+
+void stack_heads(const bf16 *in, int ldi, int T, int heads, int hd, bf16 *out, cudaStream_t st) {
+    if (T <= 0 || heads <= 0) return;
+    stack_heads_kernel<<<grid_for((size_t)heads * T * (hd / 8)), 256, 0, st>>>(in, ldi, T, heads, hd, out);
+    RS_LAUNCHED();
+}
+
+void unstack_heads(const float *in, int T, int heads, int hd, float *out, int ldo, cudaStream_t st) {
+    if (T <= 0 || heads <= 0) return;
+    unstack_heads_kernel<<<grid_for((size_t)heads * T * (hd / 4)), 256, 0, st>>>(in, T, heads, hd, out, ldo);
     RS_LAUNCHED();
 }
 

@@ -598,8 +598,9 @@ struct TransformerPair : ModelPair {
         DBuf<bf16> gu, dgu, nb, tA, tB;          // [P][2dff] x2, [P][max(d, HD, qd)], transposes
         DBuf<float> partial;                     // column-sum partials
         DBuf<bf16> WdT, WguT, WoT, WqkvT, lmT;   // transposed drafter weights
-        DBuf<float> S, dP;                       // attention backward, per (sequence, head)
-        DBuf<bf16> P, dS, PT, dST, KT, QT, dOT;
+        DBuf<float> S, dP;                       // attention backward, per (sequence, GQA group)
+        DBuf<bf16> P, dS, PT, dST, KT, QT, dOT, Qs, dOs;  // Qs / dOs: a GQA group's heads stacked
+        DBuf<float> dQs;
         DBuf<int32_t> pos, rowmap;
         DBuf<bf16> dz;                           // [Rp][V] dZ row-major
     } trs;
@@ -685,10 +686,13 @@ struct TransformerPair : ModelPair {
         T.WoT.ensure((size_t)HD * s.d);
         T.WqkvT.ensure((size_t)d2 * qd);
         T.lmT.ensure((size_t)s.d * V);
-        T.S.ensure((size_t)Tmax * Tp);
-        T.dP.ensure((size_t)Tmax * Tp);
-        for (DBuf<bf16> *b : {&T.P, &T.dS, &T.PT, &T.dST}) b->ensure((size_t)Tmax * Tp);
-        for (DBuf<bf16> *b : {&T.KT, &T.QT, &T.dOT}) b->ensure((size_t)hd * Tp);
+        const size_t GTp = (size_t)round64(G * Tmax);  // stacked rows of one GQA group
+        T.S.ensure(GTp * Tp);
+        T.dP.ensure(GTp * Tp);
+        for (DBuf<bf16> *b : {&T.P, &T.dS, &T.PT, &T.dST}) b->ensure(GTp * Tp);
+        T.KT.ensure((size_t)hd * Tp);
+        for (DBuf<bf16> *b : {&T.QT, &T.dOT, &T.Qs, &T.dOs}) b->ensure((size_t)hd * GTp);
+        T.dQs.ensure((size_t)hd * GTp);
         T.pos.ensure(P);
         T.rowmap.ensure(Rcap);
         T.dz.ensure((size_t)Rp * V);
@@ -782,17 +786,16 @@ struct TransformerPair : ModelPair {
             upload(bt, st);
             target_forward(d, R, (int)bt.items.size(), k.Pb.p, false, st);
             prof_set_scope("kd_k5");
-            for (const Run &u : runs) {  // drafter logits and the final-norm rows of the group
-                gemm(T.hf.p + u.grow * s.d, s.d, drf->lm_w, u.n, V, s.d,
-                     epi_f32(k.Qb.p + (size_t)u.k0 * V, V, s.logit_scale, nullptr), st);
+            for (const Run &u : runs)  // the group's final-norm rows, contiguous
                 RS_CUDA(cudaMemcpyAsync(k.hG.p + (size_t)u.k0 * s.d, T.hf.p + u.grow * s.d, (size_t)u.n * s.d * sizeof(bf16),
                                         cudaMemcpyDeviceToDevice, st));
-            }
+            // drafter logits of the whole group in one LM-head pass (the 622 MB weight streams once
+            // per group, not once per rollout; rows are bitwise the per-run GEMM's: token-tile invariance)
+            gemm(k.hG.p, s.d, drf->lm_w, R, V, s.d, epi_f32(k.Qb.p, V, s.logit_scale, nullptr), st);
             stage.upload(k.wr.p, kd_w, st);
             stage.upload(k.br.p, kd_b, st);
             stage.upload(T.rowmap.p, gmap, st);
-            row_stats(k.Pb.p, nullptr, R, V, tgt->temperature, k.stP.p, st);
-            row_stats(k.Qb.p, nullptr, R, V, drf->temperature, k.stQ.p, st);
+            kd_tile_stats(k.Pb.p, k.Qb.p, R, V, tgt->temperature, drf->temperature, k.stP.p, k.stQ.p, st);
             kd_rows_lse(k.Pb.p, k.stP.p, R, V, tgt->temperature, k.br.p, k.lseP.p, st);
             kd_rows_lse(k.Qb.p, k.stQ.p, R, V, drf->temperature, k.br.p, k.lseQ.p, st);
             const int Rq = round64(R);
@@ -844,32 +847,34 @@ struct TransformerPair : ModelPair {
         gemm_ld(T.tA.p, Pp, T.tB.p, Pp, s.d, HD, Pp, epi_resid(grad + gl.o_w, HD), st);
         bf16 *da = T.gu.p;  // gate/up no longer needed: [P][HD] bf16
         gemm_ld(T.nb.p, s.d, T.WoT.p, s.d, Pi, HD, s.d, epi_bf16(da, HD), st);
-        // attention backward per (sequence, query head): S = Q K^T, dP = dO V^T, softmax
-        // backward, dV += P^T dO, dK += dS^T Q, dQ = dS K (K / V post-RoPE from the private
-        // drafter cache; GQA heads of one kv head accumulate in head order)
+        // attention backward per (sequence, GQA group): the group's G query heads stacked as
+        // G*Tn rows, so each step is one GEMM per group instead of one per head: S = Q K^T,
+        // dP = dO V^T, softmax backward, dV += P^T dO and dK += dS^T Q (the head sum inside the
+        // GEMM's K loop), dQ = dS K (K / V post-RoPE from the private drafter cache)
         RS_CUDA(cudaMemsetAsync(dqkv, 0, P * qd * sizeof(float), st));
         const float scale = 1.0f / sqrtf((float)hd);
         for (size_t jj = 0; jj < seqs.size(); ++jj) {
             const int Tn = seqs[jj].len - 1;
             if (Tn <= 0) continue;
-            const int Tq = round64(Tn);
+            const int Tq = round64(Tn), GT = G * Tn, GTq = round64(GT);
             const size_t g0 = row0[jj];
-            for (int h = 0; h < s.H; ++h) {
-                const int g = h / G;
+            float *rowq = dqkv + g0 * qd;
+            for (int g = 0; g < s.KV; ++g) {
                 const bf16 *Kg = kv_d.k + kv_d.off(0, seqs[jj].r, g, 0), *Vg = kv_d.v + kv_d.off(0, seqs[jj].r, g, 0);
-                const bf16 *Qh = T.q.p + g0 * HD + (size_t)h * hd, *dOh = da + g0 * HD + (size_t)h * hd;
-                if (h % G == 0) transpose_pad_bf16(Kg, hd, Tn, hd, T.KT.p, Tq, st);
-                gemm_ld(Qh, HD, Kg, hd, Tn, Tn, hd, epi_f32(T.S.p, Tq, 1.0f, nullptr), st);
-                gemm_ld(dOh, HD, Vg, hd, Tn, Tn, hd, epi_f32(T.dP.p, Tq, 1.0f, nullptr), st);
-                softmax_bwd(T.S.p, T.dP.p, Tq, Tn, scale, T.P.p, T.dS.p, Tq, st);
-                transpose_pad_bf16(T.P.p, Tq, Tn, Tn, T.PT.p, Tq, st);
-                transpose_pad_bf16(T.dS.p, Tq, Tn, Tn, T.dST.p, Tq, st);
-                transpose_pad_bf16(dOh, HD, Tn, hd, T.dOT.p, Tq, st);
-                transpose_pad_bf16(Qh, HD, Tn, hd, T.QT.p, Tq, st);
-                float *rowq = dqkv + g0 * qd;
-                gemm_ld(T.PT.p, Tq, T.dOT.p, Tq, Tn, hd, Tq, epi_resid(rowq + HD + s.KV * hd + g * hd, qd), st);
-                gemm_ld(T.dST.p, Tq, T.QT.p, Tq, Tn, hd, Tq, epi_resid(rowq + HD + g * hd, qd), st);
-                gemm_ld(T.dS.p, Tq, T.KT.p, Tq, Tn, hd, Tq, epi_f32(rowq + h * hd, qd, 1.0f, nullptr), st);
+                stack_heads(T.q.p + g0 * HD + (size_t)g * G * hd, HD, Tn, G, hd, T.Qs.p, st);
+                stack_heads(da + g0 * HD + (size_t)g * G * hd, HD, Tn, G, hd, T.dOs.p, st);
+                transpose_pad_bf16(Kg, hd, Tn, hd, T.KT.p, Tq, st);
+                gemm_ld(T.Qs.p, hd, Kg, hd, GT, Tn, hd, epi_f32(T.S.p, Tq, 1.0f, nullptr), st);
+                gemm_ld(T.dOs.p, hd, Vg, hd, GT, Tn, hd, epi_f32(T.dP.p, Tq, 1.0f, nullptr), st);
+                softmax_bwd(T.S.p, T.dP.p, Tq, GT, Tn, scale, T.P.p, T.dS.p, Tq, st);
+                transpose_pad_bf16(T.P.p, Tq, GT, Tn, T.PT.p, GTq, st);
+                transpose_pad_bf16(T.dS.p, Tq, GT, Tn, T.dST.p, GTq, st);
+                transpose_pad_bf16(T.dOs.p, hd, GT, hd, T.dOT.p, GTq, st);
+                transpose_pad_bf16(T.Qs.p, hd, GT, hd, T.QT.p, GTq, st);
+                gemm_ld(T.PT.p, GTq, T.dOT.p, GTq, Tn, hd, GTq, epi_resid(rowq + HD + s.KV * hd + g * hd, qd), st);
+                gemm_ld(T.dST.p, GTq, T.QT.p, GTq, Tn, hd, GTq, epi_resid(rowq + HD + g * hd, qd), st);
+                gemm_ld(T.dS.p, Tq, T.KT.p, Tq, GT, hd, Tq, epi_f32(T.dQs.p, hd, 1.0f, nullptr), st);
+                unstack_heads(T.dQs.p, Tn, G, hd, rowq + (size_t)g * G * hd, qd, st);
             }
         }
         // RoPE backward on dq, dk; QKV bias; dh = dqkv . W_qkv; dW_qkv += dqkv^T h

@@ -42,7 +42,7 @@ def samples(n=5, seed=1):
     return out
 
 
-def torch_kd(tgt, drf, ss, ws):
+def torch_kd(tgt, drf, ss, ws, tau=1.0):
     tref = TargetRef(tgt)
     dref = DrafterRef(drf, tref)
     V, d = SHAPE.vocab, SHAPE.d_model
@@ -62,10 +62,10 @@ def torch_kd(tgt, drf, ss, ws):
         a, b = zt[rows].double().clone(), zq[rows].double().clone()
         a[:, -1] += s.eos_bias
         b[:, -1] += s.eos_bias
-        lp, lq = torch.log_softmax(a, -1), torch.log_softmax(b, -1)
+        lp, lq = torch.log_softmax(a / tau, -1), torch.log_softmax(b / tau, -1)
         p, q = lp.exp(), lq.exp()
         loss += w * float((p * (lp - lq)).sum())
-        dz = w * (q - p) * SHAPE.logit_scale
+        dz = w * (q - p) / tau * SHAPE.logit_scale
         dW += dz.t() @ hn[rows].double()
     return loss, dW
 
@@ -85,6 +85,24 @@ def test_kd_loss_and_lm_grad_match_torch(models):
     assert loss2 == loss and torch.equal(gb.to_torch(), g2.to_torch())
     _, g3 = rb.kd_grad_transformer(drf, ss, ws, grad=g2.clone(), zero_grad=False)
     assert torch.allclose(g3.to_torch(), 2 * gb.to_torch(), rtol=1e-6, atol=1e-7)
+
+
+def test_kd_non_unit_temperature_matches_torch():
+    """tau != 1 takes K5's general path (the unit-temperature kernel skips the divisions)."""
+    shape = rb.TransformerShape.tiny(vocab=1024, max_ctx=256, temperature=0.7)
+    tgt = rb.TransformerModel(shape, seed=31)
+    drf = rb.EagleDrafter(tgt, seed=32, version=5)
+    ss = samples(4, seed=5)
+    ws = [1.0, 0.5, 2.0, 1.5]
+    loss, gb = rb.kd_grad_transformer(drf, ss, ws)
+    rl, rg = torch_kd(tgt, drf, ss, ws, tau=0.7)
+    assert loss == pytest.approx(rl, rel=2e-2)
+    g = gb.to_torch(*drf.grad_layout("lm_w")).view(shape.vocab, shape.d_model)
+    err = (g.double() - rg).abs().max().item()
+    assert err <= 3e-2 * rg.abs().max().item(), (err, rg.abs().max().item())
+    # and differs from the unit-temperature gradient of the same weights
+    _, g1 = rb.kd_grad_transformer(rb.EagleDrafter(rb.TransformerModel(SHAPE, seed=31), seed=32, version=5), ss, ws)
+    assert not torch.equal(g1.to_torch(), gb.to_torch())
 
 
 def test_kd_weights_are_linear(models):
