@@ -207,7 +207,7 @@ __global__ void kd_lse_kernel(const float *rows, const double *st, int nrows, in
 // UnitTau (tau_p == tau_q == 1, the KD default): the three fp64 divisions per element are
 // skipped -- x / 1.0 == x exactly, so the outputs are bitwise those of the general path.
 template <bool UnitTau>
-__global__ void __launch_bounds__(256) kd_elem_kernel(const float *P, const float *Q, const double *lseP,
+__global__ void __launch_bounds__(256, 4) kd_elem_kernel(const float *P, const float *Q, const double *lseP,
                                                       const double *lseQ, const double *w, const double *bias, int R,
                                                       int V, double tau_p, double tau_q, float zscale, bf16 *dzT,
                                                       int ldt, double *kl_part) {

@@ -236,7 +236,7 @@ def torch_kd_full(tgt, drf, ss, ws):
     loss = sum_i w_i sum_t KL(p~_t || q_t) over the response positions; returns the loss and the
     gradient of every drafter tensor in the library's layout (gate / up interleaved pairwise)."""
     tref = TargetRef(tgt)
-    s = SHAPE
+    s = drf.shape
     d, H, KV, hd = s.d_model, s.n_heads, s.n_kv_heads, s.head_dim
     q = (H + 2 * KV) * hd
     W = {n: drf.to_torch(n).float().clone().requires_grad_(True) for n in rb.EagleDrafter.GRAD_TENSORS}
@@ -313,4 +313,27 @@ def test_whole_drafter_grad_matches_autograd(models):
         x, y = gt[o:o + n].double(), ref[name].double()
         errs[name] = ((x - y).norm() / y.norm().clamp_min(1e-30)).item()
     print("whole-drafter grad rel. errors:", {k: round(v, 4) for k, v in errs.items()})
+    assert all(v < 5e-2 for v in errs.values()), errs
+
+
+def test_whole_drafter_grad_gqa8_matches_autograd():
+    """The attention backward stacks a GQA group's query heads; G = 8 as at Qwen2.5-3B (one KV head
+    of eight query heads, hd = 128) against torch autograd."""
+    shape = rb.TransformerShape(1024, 1024, 2, 8, 1, 128, 512, 256)
+    tgt = rb.TransformerModel(shape, seed=41)
+    drf = rb.EagleDrafter(tgt, seed=42, version=1)
+    rng = random.Random(9)
+    ss = [rb.RolloutSample([rng.randrange(shape.vocab - 1) for _ in range(20 + 7 * i)],
+                           [rng.randrange(shape.vocab) for _ in range(9 + 5 * i)], [], eos_bias=0.25 * i,
+                           reward=rng.random()) for i in range(3)]
+    ws = [0.7, 1.3, 1.0]
+    loss, g = rb.kd_grad_transformer(drf, ss, ws)
+    rl, ref = torch_kd_full(tgt, drf, ss, ws)
+    assert loss == pytest.approx(rl, rel=2e-2)
+    gt = g.to_torch()
+    errs = {}
+    for name in rb.EagleDrafter.GRAD_TENSORS:
+        o, n = drf.grad_layout(name)
+        x, y = gt[o:o + n].double(), ref[name].double()
+        errs[name] = ((x - y).norm() / y.norm().clamp_min(1e-30)).item()
     assert all(v < 5e-2 for v in errs.values()), errs

@@ -29,7 +29,7 @@ timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_d
   --nvtx-include "accept/" -k regex:"accept|compact" --csv --log-file $O/accept_traffic.csv python tools/profile_step.py 1 > $O/accept_traffic.log 2>&1
 python tools/gemm_traffic.py $O/accept_traffic.csv accept > $O/accept_traffic.json; head -3 $O/accept_traffic.json
 python tools/gemm_traffic.py $O/accept_traffic.csv compact > $O/compact_traffic.json
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"kd_elem|kd_lse|row_stats" -s 0 -c 4 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"kd_elem|kd_lse|kd_tile_stats|row_stats" -s 0 -c 4 \
   -o $O/kd_full python tools/profile_kd.py 1 1664 65 > $O/kd_full.log 2>&1; echo "ncu kd rc=$?"
 python tools/ncu_summary.py $O > $O/ncu_summary.md 2> $O/ncu_summary.err; echo "summary rc=$?"
 # keep the copy-back under gpurun's 64 MiB: summaries stay, the large reports go
