@@ -766,7 +766,7 @@ def main():
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_tok / e2e_s, 1), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps)},
-            "gpu_launches": launches, "clocks": clk, "parity": parity, "breakdown_ms_per_step": breakdown,
+            "gpu_launches": launches, "clocks": clk, "parity": parity, "breakdown_ms_per_step": breakdown, "breakdown_note": "per-kernel profiler pass over separate untimed steps: events around each kernel group defeat the programmatic-dependent-launch overlap, so the groups sum to ~10-15 % above ms_per_step; read them as shares",
             "kd_update": kd, "kd_async_overlap": overlap, "north_star_batch256": b256, "hbm": hbm or None}
     if dyn:
         line["dynamic_tuning"] = dyn
