@@ -55,6 +55,7 @@ struct DrafterModel : rs_model {
     bf16 *lm_w = nullptr;      // [V, d]
     size_t n_params = 0;
     DrafterModel() : rs_model(Drafter) {}
+    ~DrafterModel() override;  // the arena goes back to the snapshot pool (model.cu)
 };
 
 void init_transformer(TransformerModel &m, uint64_t seed, cudaStream_t st);
